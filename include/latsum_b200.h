@@ -1,0 +1,182 @@
+/* latsum_b200 — C ABI of the B200-native lattice-sum hot path.
+ *
+ * Drop-in boundary for the reference's header-only C++ interface
+ * (/root/reference/proj/include/latsum).  Each entry point cites the reference
+ * function it replaces.  Conventions:
+ *   - plain pointers and sizes, no C++ or torch types;
+ *   - FP64, column-major, first index fastest, 0-based indices, int64 sizes;
+ *   - every call returns int status (LATSUM_OK = 0) and never throws; the message
+ *     of the last failure is latsum_last_error(ctx);
+ *   - host pointers unless the name says _device; the context owns all device
+ *     memory behind the opaque handles; one context per host thread.
+ * There is no CPU fallback: every compute entry point runs CUDA kernels on the
+ * context's device and fails with LATSUM_ERR_CUDA when no device is present.
+ */
+#ifndef LATSUM_B200_H
+#define LATSUM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  LATSUM_OK = 0,
+  LATSUM_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  LATSUM_ERR_WINDOW_OVERFLOW = 2,  /* WindowOverflowError (grid.hpp:111-122); mode in message */
+  LATSUM_ERR_CUDA = 3,
+  LATSUM_ERR_CUSOLVER = 4,
+  LATSUM_ERR_OUT_OF_MEMORY = 5,
+  LATSUM_ERR_LENGTH = 6,           /* std::length_error: dense guard (tensor3.hpp:101-105) */
+  LATSUM_ERR_NOT_IMPLEMENTED = 7,  /* NotImplementedError (quadrature.hpp:288-290) */
+  LATSUM_ERR_NCCL = 8
+};
+
+enum { LATSUM_NEWTON = 0, LATSUM_YUKAWA = 1 }; /* kernel.hpp:17 KernelFamily (gauss type) */
+
+enum { LATSUM_DEFLATE_NEVER = 0, LATSUM_DEFLATE_ALWAYS = 1, LATSUM_DEFLATE_AUTO = 2 };
+
+typedef struct latsum_ctx latsum_ctx;
+typedef struct latsum_reference latsum_reference;
+typedef struct latsum_canonical latsum_canonical;
+typedef struct latsum_tucker latsum_tucker;
+
+/* SpectralReport (rank_reduction.hpp:49-67) plus GPU-side diagnostics. */
+typedef struct {
+  int64_t chosen_ranks[3];
+  double bound_abs, bound_rel, weight_norm, input_norm, stability_constant;
+  int stability_ok;
+  int tie_at_cutoff[3];
+  int64_t n_singular[3];   /* length of singular_values[l] = min(N_l, M_c) */
+  double cutoff_margin[3]; /* min(target - tail(r), tail(r-1) - target) / target; tolerance mode */
+  int deflated[3];         /* 1 when the second (deflated) Gram pass ran for mode l */
+  int gram_rows[3];        /* 1: Gram A A^T (N x N); 0: Gram A^T A over merged columns */
+  int64_t gram_size[3];
+  double ms_gram, ms_syevd, ms_deflate, ms_project, ms_core, ms_norm, ms_total; /* CUDA events */
+} latsum_spectral_report;
+
+/* ------------------------------------------------------------------ context */
+int latsum_ctx_create(int device, latsum_ctx** out);
+void latsum_ctx_destroy(latsum_ctx* ctx);
+const char* latsum_last_error(const latsum_ctx* ctx);
+/* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
+int latsum_ctx_set_stream(latsum_ctx* ctx, void* cuda_stream);
+int latsum_ctx_synchronize(latsum_ctx* ctx);
+/* Number of kernels this context launched so far (its own kernels, not library ones). */
+int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);
+
+/* ------------------------------------------------------------------ host rules (no GPU)
+ * quadrature.hpp:303-341 build_quadrature (gauss branch); nodes/weights hold 2M+1 values. */
+int latsum_build_quadrature(int family, double lambda, int M, double step_constant,
+                            double shell_a, double shell_A, double* nodes, double* weights);
+/* quadrature.hpp:416-447 default_step_constant (53-point sweep, npts probe radii). */
+double latsum_default_step_constant(int family, double lambda, int M, double shell_a,
+                                    double shell_A, int npts);
+/* reference.hpp:84-93 reference_shell of the doubled grid of (N, box). */
+void latsum_reference_shell(const int64_t N[3], const double box[3], double shell[2]);
+
+/* ------------------------------------------------------------------ stage 1
+ * reference.hpp:95-153 build_reference_canonical(kernel, grid(box, N), M, {doubled=true,
+ * step_constant}) for a Newton/Yukawa primitive; step_constant <= 0 selects the
+ * calibrated sweep.  The 2N_l x R side matrices (unit columns) and R weights stay on
+ * the device; identical modes share one matrix (reference.hpp:125-139). */
+int latsum_reference_build(latsum_ctx* ctx, int family, double lambda, const int64_t N[3],
+                           const double box[3], int M, double step_constant,
+                           latsum_reference** out);
+void latsum_reference_destroy(latsum_reference* ref);
+/* rank R, step constant C0, shell [a, A] */
+int latsum_reference_info(const latsum_reference* ref, int* rank, double* step_constant,
+                          double shell[2]);
+/* ReferenceTensor::canonical.factor(mode) (2N_l x R) and .weights() (R) to host buffers. */
+int latsum_reference_factor(latsum_ctx* ctx, const latsum_reference* ref, int mode,
+                            double* factor);
+int latsum_reference_weights(const latsum_reference* ref, double* weights);
+/* QuadratureRule nodes t_k and weights a_k (R each). */
+int latsum_reference_quadrature(const latsum_reference* ref, double* nodes, double* weights);
+
+/* ------------------------------------------------------------------ stage 2
+ * Assembled lattice sum plus additive defects in canonical form:
+ *   lattice_sum.hpp:198-223 assembled_sum_canonical (one block per sublattice),
+ *   :411-465 sublattice_union_sum, :339-384 defected_sum (canonical branch, no spec),
+ *   :148-157 windowed_canonical.
+ * Sublattice s contributes R terms whose mode-l vector is sum_{c in shifts_s,l}
+ * ref[N/2 - c + i] (assembled_vector, :101-144, with an explicit shift list),
+ * weight charge_s * w_ref.  Defect d contributes R terms: the window at shift
+ * (c1,c2,c3), weight charge_d * w_ref.  Terms are ordered sublattice blocks first,
+ * then defects, as add_concat builds them.  from_raw normalisation per block.
+ *   sub_counts: nsub x 3 (number of shifts per mode); sub_shifts: concatenated in
+ *   (s, mode) order; def_shifts: ndef x 3 row-major.                                 */
+int latsum_canonical_assemble(latsum_ctx* ctx, const latsum_reference* ref, int64_t nsub,
+                              const int64_t* sub_counts, const int64_t* sub_shifts,
+                              const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
+                              const double* def_charges, latsum_canonical** out);
+void latsum_canonical_destroy(latsum_canonical* can);
+/* M_c = rank of the canonical sum, d_l = distinct (merged) columns per mode, T = merged terms. */
+int latsum_canonical_info(const latsum_canonical* can, int64_t dims[3], int64_t* rank,
+                          int64_t dict_cols[3], int64_t* merged_terms);
+/* CanonicalTensor::weights() (M_c). */
+int latsum_canonical_weights(const latsum_canonical* can, double* weights);
+/* CanonicalTensor::factor(mode): N_l x M_c side matrix materialised in reference column
+ * order, to a host buffer or (``_device``) to caller-owned device memory. */
+int latsum_canonical_factor(latsum_ctx* ctx, const latsum_canonical* can, int mode,
+                            double* factor);
+int latsum_canonical_factor_device(latsum_ctx* ctx, const latsum_canonical* can, int mode,
+                                   double* factor_device);
+/* CanonicalTensor::entry (canonical.hpp:63-70) at np probe points (np x 3 indices). */
+int latsum_canonical_entries(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* probes,
+                             int64_t np, double* out);
+/* norm_f (canonical.hpp:148-162) without forming M_c x M_c matrices. */
+int latsum_canonical_norm(latsum_ctx* ctx, const latsum_canonical* can, double* out);
+/* Canonical to grid on the box [lo, hi) (to_dense, canonical.hpp:192-202, unguarded on
+ * the device); out is (hi-lo) column-major, first index fastest. */
+int latsum_canonical_eval_box_device(latsum_ctx* ctx, const latsum_canonical* can,
+                                     const int64_t lo[3], const int64_t hi[3], double* out_device);
+
+/* ------------------------------------------------------------------ stage 3
+ * rank_reduction.hpp:176-218 rhosvd(canonical, TruncationSpec): ranks != NULL gives
+ * fixed ranks (clamped), else tolerance in (0,1).  deflate selects the second Gram
+ * pass that resolves singular values below sqrt(eps_mach) sigma_1. */
+int latsum_rhosvd(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* ranks,
+                  double tolerance, int deflate, latsum_tucker** out,
+                  latsum_spectral_report* report);
+void latsum_tucker_destroy(latsum_tucker* t);
+int latsum_tucker_info(const latsum_tucker* t, int64_t dims[3], int64_t ranks[3]);
+/* SpectralReport::singular_values[mode] (report.n_singular[mode] values, descending). */
+int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out);
+/* TuckerTensor::core() (r1 x r2 x r3, first index fastest) and factor(mode) (N_l x r_l). */
+int latsum_tucker_core(latsum_ctx* ctx, const latsum_tucker* t, double* core);
+int latsum_tucker_factor(latsum_ctx* ctx, const latsum_tucker* t, int mode, double* factor);
+
+/* ------------------------------------------------------------------ stage 4
+ * TuckerTensor::entry (tucker.hpp:38-54) at probes, and to_dense (tucker.hpp:172-178)
+ * on the box [lo, hi) of the grid: out (hi-lo) column-major. */
+int latsum_tucker_entries(latsum_ctx* ctx, const latsum_tucker* t, const int64_t* probes,
+                          int64_t np, double* out);
+int latsum_tucker_eval_box(latsum_ctx* ctx, const latsum_tucker* t, const int64_t lo[3],
+                           const int64_t hi[3], double* out);
+int latsum_tucker_eval_box_device(latsum_ctx* ctx, const latsum_tucker* t, const int64_t lo[3],
+                                  const int64_t hi[3], double* out_device);
+
+/* ------------------------------------------------------------------ pipeline
+ * cmd_sum (commands.cpp:108-179) for a defected / multi-sublattice lattice with a
+ * truncation block: stages 1-3 in one call, inputs and the Tucker result in host
+ * memory (the drop-in used by the end-to-end bench). */
+int latsum_sum_to_tucker(latsum_ctx* ctx, int family, double lambda, const int64_t N[3],
+                         const double box[3], int M, double step_constant, int64_t nsub,
+                         const int64_t* sub_counts, const int64_t* sub_shifts,
+                         const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
+                         const double* def_charges, double tolerance, latsum_tucker** out,
+                         latsum_spectral_report* report);
+
+/* ------------------------------------------------------------------ utilities */
+/* Generic FP64 DMMA GEMM on device pointers (exposed for tests and benchmarks):
+ * C = alpha op(A) op(B) + beta C, column-major, op = transpose when t* != 0. */
+int latsum_dgemm_device(latsum_ctx* ctx, int ta, int tb, int64_t M, int64_t N, int64_t K,
+                        double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double beta, double* C, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LATSUM_B200_H */

@@ -1,0 +1,310 @@
+// latsum CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// A plain C++ restatement of the reference's hot-path functions
+// (/root/reference/proj/include/latsum/*.hpp), used exclusively by tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg as
+// the checker.  Nothing in the product (paper_1411_1994_b200/) links or calls
+// this file.  The reference itself cannot be compiled here (Eigen3, doctest,
+// CLI11 absent), so this restatement is pinned against
+// the reference's own known-answer tests and property tests (tests/test_oracle.py)
+// and against mpmath golden vectors (tests/golden/).
+//
+// Conventions follow the reference: column-major matrices, first index
+// fastest, 0-based indices, Scalar = double.  Every function cites the
+// reference file:line range it restates.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr int kNewton = 0;
+constexpr int kYukawa = 1;
+
+double sqrt_pi() { return std::sqrt(M_PI); }
+
+// quadrature.hpp:251-263 (gauss_weight)
+double gauss_weight(int family, double lambda, double t) {
+  if (family == kNewton) return 2.0 / sqrt_pi();
+  if (t == 0.0) return 0.0;
+  const double kap = lambda / 2.0;
+  return (2.0 / sqrt_pi()) * std::exp(-(kap * kap) / (t * t));
+}
+
+// kernel.hpp:154-158 (primitive_exact, newton/yukawa)
+double kernel_exact(int family, double lambda, double r) {
+  if (family == kNewton) return 1.0 / r;
+  return std::exp(-lambda * r) / r;
+}
+
+// quadrature.hpp:303-341 (build_quadrature, gauss branch)
+void build_quadrature(int family, double lambda, int M, double c0, double A, double* nodes,
+                      double* weights) {
+  const double h = c0 * std::log(double(M)) / double(M);
+  const int R = 2 * M + 1;
+  for (int i = 0; i < R; ++i) {
+    const double u = (double(i) - double(M)) * h;
+    const double t = std::sinh(u) / A;
+    nodes[i] = t;
+    weights[i] = 0.5 * h * gauss_weight(family, lambda, std::abs(t)) * std::cosh(u) / A;
+  }
+}
+
+// quadrature.hpp:370-379 + 396-412 (separable_eval on (z,0,0), shell_error.pointwise_rel)
+double shell_pointwise_rel(int family, double lambda, const double* nodes, const double* weights,
+                           int R, double a, double A, int npts) {
+  double pw = 0.0;
+  const double la = std::log(a), lA = std::log(A);
+  for (int i = 0; i < npts; ++i) {
+    const double z = std::exp(la + (lA - la) * double(i) / double(npts - 1));
+    const double exact = kernel_exact(family, lambda, z);
+    const double x[3] = {z, 0.0, 0.0};
+    double sum = 0.0;
+    for (int k = 0; k < R; ++k) {
+      const double s = nodes[k] * nodes[k];
+      double prod = weights[k];
+      for (int l = 0; l < 3; ++l) prod *= std::exp(-s * x[l] * x[l]);
+      sum += prod;
+    }
+    const double approx = 1.0 * sum;  // expansion coefficient 1 (primitive kernel)
+    const double e = std::abs(approx - exact);
+    pw = std::max(pw, e / std::abs(exact));
+  }
+  return pw;
+}
+
+// erf(hi)-erf(lo), reference.hpp:21-25 (erf_difference)
+double erf_difference(double lo, double hi) {
+  if (lo >= 0.0) return std::erfc(lo) - std::erfc(hi);
+  if (hi <= 0.0) return std::erfc(-hi) - std::erfc(-lo);
+  return std::erf(hi) - std::erf(lo);
+}
+
+// 4-point Gauss-Legendre on [lo, lo+h] of exp(-s x^2): the cancellation-free
+// branch of the hybrid cell integral (documented deviation).
+double gl4_cell(double s, double lo, double h) {
+  static const double xg[4] = {-0.86113631159405257522, -0.33998104358485626480,
+                               0.33998104358485626480, 0.86113631159405257522};
+  static const double wg[4] = {0.34785484513745385737, 0.65214515486254614263,
+                               0.65214515486254614263, 0.34785484513745385737};
+  const double mid = lo + 0.5 * h;
+  double acc = 0.0;
+  for (int g = 0; g < 4; ++g) {
+    const double x = mid + 0.5 * h * xg[g];
+    acc += wg[g] * std::exp(-s * x * x);
+  }
+  return 0.5 * h * acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ---------------------------------------------------------------- stage 1 (host part)
+
+// quadrature.hpp:303-341
+int orc_build_quadrature(int family, double lambda, int M, double c0, double shell_a,
+                         double shell_A, double* nodes, double* weights) {
+  if (M < 2 || !(shell_a > 0.0) || !(shell_A > shell_a) || !(c0 > 0.0)) return 1;
+  build_quadrature(family, lambda, M, c0, shell_A, nodes, weights);
+  return 0;
+}
+
+// quadrature.hpp:416-447 (default_step_constant, gauss family)
+double orc_default_step_constant(int family, double lambda, int M, double shell_a,
+                                 double shell_A, int npts) {
+  const double base = std::asinh(2.5 * (shell_A / shell_a)) / std::log(double(M));
+  std::vector<double> nodes(2 * M + 1), weights(2 * M + 1);
+  double best_err = std::numeric_limits<double>::infinity();
+  double best_c0 = base * 0.5;
+  for (int i = 0; i < 53; ++i) {
+    const double c0 = base * (0.5 + 1.3 * double(i) / 52.0);
+    build_quadrature(family, lambda, M, c0, shell_A, nodes.data(), weights.data());
+    const double e = shell_pointwise_rel(family, lambda, nodes.data(), weights.data(), 2 * M + 1,
+                                         shell_a, shell_A, npts);
+    if (std::isfinite(e) && e < best_err) {
+      best_err = e;
+      best_c0 = c0;
+    }
+  }
+  return best_c0;
+}
+
+double orc_shell_error(int family, double lambda, const double* nodes, const double* weights,
+                       int R, double shell_a, double shell_A, int npts) {
+  return shell_pointwise_rel(family, lambda, nodes, weights, R, shell_a, shell_A, npts);
+}
+
+// reference.hpp:33-54 (mode_integrals).  variant 0 = literal erf_difference,
+// variant 1 = hybrid (GL-4 when sqrt(s) h < 0.05, else erf_difference).
+// out is n x R column-major.  Cell i spans [lower + i h, lower + i h + h]
+// (grid.hpp cell_bounds).
+void orc_mode_integrals(const double* nodes, int R, int64_t n, double lower, double h, int variant,
+                        double* out) {
+  for (int k = 0; k < R; ++k) {
+    const double s = nodes[k] * nodes[k];
+    double* col = out + int64_t(k) * n;
+    if (s == 0.0) {
+      for (int64_t i = 0; i < n; ++i) col[i] = h;
+      continue;
+    }
+    const double rs = std::sqrt(s);
+    const double c = std::sqrt(M_PI) / (2.0 * rs);
+    const bool gl = variant == 1 && rs * h < 0.05;
+    for (int64_t i = 0; i < n; ++i) {
+      const double lo = lower + double(i) * h;
+      const double hi = lo + h;
+      col[i] = gl ? gl4_cell(s, lo, h) : c * erf_difference(rs * lo, rs * hi);
+    }
+  }
+}
+
+// canonical.hpp:32-48 (from_raw), one mode: normalize each column in place,
+// return its norm (0 -> column e_0, norm 0).
+void orc_normalize_columns(int64_t rows, int64_t cols, double* m, double* norms) {
+  for (int64_t q = 0; q < cols; ++q) {
+    double* c = m + q * rows;
+    double s = 0.0;
+    for (int64_t i = 0; i < rows; ++i) s += c[i] * c[i];
+    const double nrm = std::sqrt(s);
+    norms[q] = nrm;
+    if (nrm == 0.0) {
+      c[0] = 1.0;
+    } else {
+      for (int64_t i = 0; i < rows; ++i) c[i] /= nrm;
+    }
+  }
+}
+
+// lattice_sum.hpp:101-144 (assembled_vector, ascending order) generalised to an
+// explicit integer shift list: v[i] = sum_c ref[N/2 - c + i].
+// ref is the 2N-row column; returns 0, or 1 + index of the overflowing shift.
+int64_t orc_assembled_vector(const double* ref, int64_t N, const int64_t* shifts, int64_t nshift,
+                             double* out) {
+  std::vector<int64_t> cs(shifts, shifts + nshift);
+  // ascending order in k corresponds to descending start; the reference sorts
+  // the K set ascending and sums in that order.  Shift lists arrive in K order.
+  for (int64_t j = 0; j < nshift; ++j) {
+    const int64_t s = N / 2 - cs[j];
+    if (s < 0 || s + N > 2 * N) return 1 + j;
+  }
+  for (int64_t i = 0; i < N; ++i) out[i] = 0.0;
+  for (int64_t j = 0; j < nshift; ++j) {
+    const double* seg = ref + (N / 2 - cs[j]);
+    for (int64_t i = 0; i < N; ++i) out[i] += seg[i];
+  }
+  return 0;
+}
+
+// lattice_sum.hpp:116-127 (sliding recursion) for uniform-stride shift lists
+// c_j = n*k_j + off with consecutive k: used to pin the ascending order.
+void orc_assembled_vector_sliding(const double* ref, int64_t N, int64_t n, int64_t off, int kmin,
+                                  int kmax, double* v) {
+  auto start0 = [&](int64_t k) { return N / 2 - (n * k + off); };
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0;
+    for (int k = kmin; k <= kmax; ++k) s += ref[start0(k) + i];
+    v[i] = s;
+  }
+  const int64_t hi = start0(kmin), lo = start0(int64_t(kmax) + 1);
+  for (int64_t i = n; i < N; ++i) v[i] = v[i - n] + ref[hi + i] - ref[lo + i];
+}
+
+// ---------------------------------------------------------------- entries
+
+// canonical.hpp:63-70 (CanonicalTensor::entry) over probe lists.
+void orc_canonical_entries(const double* w, int64_t R, const double* f0, const double* f1,
+                           const double* f2, const int64_t* dims, const int64_t* probes,
+                           int64_t np, double* out) {
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t i = probes[3 * p], j = probes[3 * p + 1], k = probes[3 * p + 2];
+    double v = 0;
+    for (int64_t q = 0; q < R; ++q)
+      v += w[q] * f0[i + dims[0] * q] * f1[j + dims[1] * q] * f2[k + dims[2] * q];
+    out[p] = v;
+  }
+}
+
+// tucker.hpp:38-54 (TuckerTensor::entry) over probe lists.
+void orc_tucker_entries(const double* core, const int64_t* r, const double* u0, const double* u1,
+                        const double* u2, const int64_t* dims, const int64_t* probes, int64_t np,
+                        double* out) {
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t i = probes[3 * p], j = probes[3 * p + 1], k = probes[3 * p + 2];
+    double v = 0;
+    for (int64_t c = 0; c < r[2]; ++c) {
+      double vc = 0;
+      for (int64_t b = 0; b < r[1]; ++b) {
+        double vb = 0;
+        for (int64_t a = 0; a < r[0]; ++a)
+          vb += core[a + r[0] * (b + r[1] * c)] * u0[i + dims[0] * a];
+        vc += vb * u1[j + dims[1] * b];
+      }
+      v += vc * u2[k + dims[2] * c];
+    }
+    out[p] = v;
+  }
+}
+
+// lattice_sum.hpp:656-671 (oracle_entry): brute-force windowed sum over all
+// grid-shifted sources.  ref_f* are the normalised 2N x R reference side
+// matrices, ref_w the reference weights; source s reads rows N/2 - c + i.
+// Threads own disjoint probe ranges, so the result is thread-count independent.
+void orc_oracle_entries(const double* ref_w, int64_t R, const double* rf0, const double* rf1,
+                        const double* rf2, const int64_t* N, const int64_t* shifts,
+                        const double* sweights, int64_t ns, const int64_t* probes, int64_t np,
+                        double* out, int threads) {
+  auto work = [&](int64_t plo, int64_t phi) {
+    for (int64_t p = plo; p < phi; ++p) {
+      const int64_t i = probes[3 * p], j = probes[3 * p + 1], k = probes[3 * p + 2];
+      double v = 0;
+      for (int64_t s = 0; s < ns; ++s) {
+        const int64_t b0 = N[0] / 2 - shifts[3 * s], b1 = N[1] / 2 - shifts[3 * s + 1],
+                      b2 = N[2] / 2 - shifts[3 * s + 2];
+        double e = 0;
+        for (int64_t q = 0; q < R; ++q)
+          e += ref_w[q] * rf0[b0 + i + 2 * N[0] * q] * rf1[b1 + j + 2 * N[1] * q] *
+               rf2[b2 + k + 2 * N[2] * q];
+        v += sweights[s] * e;
+      }
+      out[p] = v;
+    }
+  };
+  if (threads <= 1 || np < 2) {
+    work(0, np);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t chunk = (np + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t lo = t * chunk, hi = std::min<int64_t>(np, lo + chunk);
+    if (lo < hi) pool.emplace_back(work, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+}
+
+// rank_reduction.hpp:88-100 (project_core): C(i,j,k) = sum_q xi_q P1(i,q) P2(j,q) P3(k,q),
+// the reference's loop order (one rank-1 slab update per term).
+void orc_project_core(const double* w, int64_t M, const double* p0, const double* p1,
+                      const double* p2, const int64_t* r, double* core) {
+  std::memset(core, 0, sizeof(double) * size_t(r[0] * r[1] * r[2]));
+  for (int64_t q = 0; q < M; ++q) {
+    const double* a = p0 + r[0] * q;
+    const double* b = p1 + r[1] * q;
+    const double* c = p2 + r[2] * q;
+    for (int64_t k = 0; k < r[2]; ++k) {
+      const double s = w[q] * c[k];  // (xi_q * P3(k,q)) * g, g = p1 p2^T
+      for (int64_t j = 0; j < r[1]; ++j) {
+        double* dst = core + r[0] * (j + r[1] * k);
+        for (int64_t i = 0; i < r[0]; ++i) dst[i] += s * (a[i] * b[j]);
+      }
+    }
+  }
+}
+
+}  // extern "C"

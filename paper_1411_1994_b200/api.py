@@ -1,0 +1,476 @@
+"""Reference-shaped Python interface over the C ABI (include/latsum_b200.h).
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(/root/reference/proj/include/latsum):
+
+=====================================  =========================================
+this module                            reference
+=====================================  =========================================
+`build_reference_canonical`            reference.hpp:95-153
+`assembled_sum_canonical`              lattice_sum.hpp:198-223
+`defected_sum`                         lattice_sum.hpp:339-384 (canonical branch)
+`sublattice_union_sum`                 lattice_sum.hpp:411-465
+`lattice_sum`                          the above for a generalised `Geometry`
+`rhosvd`                               rank_reduction.hpp:176-218
+`CanonicalTensor.entry/.to_dense`      canonical.hpp:63-70, :192-202
+`TuckerTensor.entry/.to_dense`         tucker.hpp:38-54, :172-178
+`TruncationSpec`, `SpectralReport`     rank_reduction.hpp:21-67
+=====================================  =========================================
+
+Every tensor lives in device memory behind an opaque handle; host copies are
+made only when a method asks for them (``factor``, ``core``, ``to_dense``).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .workload import NEWTON, YUKAWA, Geometry, from_lattice
+
+__all__ = [
+    "Context", "KernelSpec", "TruncationSpec", "SpectralReport", "ReferenceTensor",
+    "CanonicalTensor", "TuckerTensor", "build_quadrature", "default_step_constant",
+    "reference_shell", "build_reference_canonical", "lattice_sum", "assembled_sum_canonical",
+    "defected_sum", "sublattice_union_sum", "rhosvd", "WindowOverflowError", "Geometry",
+]
+
+WindowOverflowError = _lib.WindowOverflowError
+
+DEFLATE = {"never": 0, "always": 1, "auto": 2}
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """One CUDA device, stream and cuSOLVER handle (latsum_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._h = ctypes.c_void_p()
+        st = _lib.lib().latsum_ctx_create(device, ctypes.byref(self._h))
+        if st != 0:
+            raise RuntimeError(f"latsum_ctx_create({device}) failed with status {st}: "
+                               "a CUDA device is required (no CPU fallback)")
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, st: int):
+        _lib.check(st, self._h)
+
+    def synchronize(self):
+        self.check(_lib.lib().latsum_ctx_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int):
+        self.check(_lib.lib().latsum_ctx_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.lib().latsum_ctx_kernel_launches(self._h))
+
+    def close(self):
+        if self._h:
+            _lib.lib().latsum_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ----------------------------------------------------------------------------- specs
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """kernel.hpp:37-152 restricted to the hot path's gauss-type primitives."""
+    family: int = NEWTON
+    lam: float = 0.0
+
+    @staticmethod
+    def newton() -> "KernelSpec":
+        return KernelSpec(NEWTON, 0.0)
+
+    @staticmethod
+    def yukawa(lam: float) -> "KernelSpec":
+        if not lam > 0.0:
+            raise ValueError("yukawa lambda must be positive")
+        return KernelSpec(YUKAWA, float(lam))
+
+
+@dataclass
+class TruncationSpec:
+    """rank_reduction.hpp:21-43."""
+    ranks: Optional[Tuple[int, int, int]] = None
+    tolerance: Optional[float] = None
+
+    def validate(self):
+        if self.ranks is None and self.tolerance is None:
+            raise ValueError("TruncationSpec: need ranks or tolerance")
+        if self.tolerance is not None and not (0.0 < self.tolerance < 1.0):
+            raise ValueError("TruncationSpec: tolerance must lie in (0,1)")
+
+    @staticmethod
+    def fixed_ranks(r1: int, r2: int, r3: int) -> "TruncationSpec":
+        return TruncationSpec(ranks=(int(r1), int(r2), int(r3)))
+
+    @staticmethod
+    def tol(eps: float) -> "TruncationSpec":
+        return TruncationSpec(tolerance=float(eps))
+
+
+@dataclass
+class SpectralReport:
+    """rank_reduction.hpp:49-67 plus the GPU path's diagnostics and stage timings."""
+    singular_values: list
+    chosen_ranks: Tuple[int, int, int]
+    bound_abs: float
+    bound_rel: float
+    weight_norm: float
+    input_norm: float
+    stability_constant: float
+    stability_ok: bool
+    tie_at_cutoff: Tuple[bool, bool, bool]
+    cutoff_margin: Tuple[float, float, float]
+    deflated: Tuple[bool, bool, bool]
+    gram_rows: Tuple[bool, bool, bool]
+    gram_size: Tuple[int, int, int]
+    ms: dict
+
+    def tail(self, mode: int) -> float:
+        sv = self.singular_values[mode]
+        return float(np.sqrt(np.sum(sv[self.chosen_ranks[mode]:] ** 2)))
+
+
+# ----------------------------------------------------------------------------- host rules
+
+def build_quadrature(kernel: KernelSpec, M: int, step_constant: float, shell) -> Tuple[np.ndarray, np.ndarray]:
+    R = 2 * M + 1
+    t, a = np.zeros(R), np.zeros(R)
+    _lib.check(_lib.lib().latsum_build_quadrature(kernel.family, kernel.lam, M, step_constant,
+                                                  shell[0], shell[1], _p(t), _p(a)))
+    return t, a
+
+
+def default_step_constant(kernel: KernelSpec, M: int, shell, npts: int = 320) -> float:
+    return float(_lib.lib().latsum_default_step_constant(kernel.family, kernel.lam, M, shell[0],
+                                                         shell[1], npts))
+
+
+def reference_shell(N, box) -> Tuple[float, float]:
+    out = np.zeros(2)
+    _lib.lib().latsum_reference_shell(_p(_i64(N)), _p(_f64(box)), _p(out))
+    return float(out[0]), float(out[1])
+
+
+# ----------------------------------------------------------------------------- tensors
+
+class ReferenceTensor:
+    """reference.hpp:65-80 (doubled grid, canonical form, device resident)."""
+
+    def __init__(self, ctx: Context, handle, kernel: KernelSpec, N, box, M):
+        self.ctx, self._h, self.kernel = ctx, handle, kernel
+        self.N, self.box, self.M = tuple(int(n) for n in N), tuple(float(b) for b in box), M
+        rank, c0, shell = ctypes.c_int(), ctypes.c_double(), np.zeros(2)
+        _lib.lib().latsum_reference_info(self._h, ctypes.byref(rank), ctypes.byref(c0), _p(shell))
+        self.rank, self.step_constant, self.shell = rank.value, c0.value, (shell[0], shell[1])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def factor(self, mode: int) -> np.ndarray:
+        out = np.zeros((2 * self.N[mode], self.rank), order="F")
+        self.ctx.check(_lib.lib().latsum_reference_factor(self.ctx.handle, self._h, mode, _p(out)))
+        return out
+
+    @property
+    def weights(self) -> np.ndarray:
+        w = np.zeros(self.rank)
+        _lib.check(_lib.lib().latsum_reference_weights(self._h, _p(w)))
+        return w
+
+    def quadrature(self):
+        t, a = np.zeros(self.rank), np.zeros(self.rank)
+        _lib.check(_lib.lib().latsum_reference_quadrature(self._h, _p(t), _p(a)))
+        return t, a
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_reference_destroy(self._h)
+            self._h = None
+
+
+def build_reference_canonical(kernel: KernelSpec, N: Sequence[int], box: Sequence[float], M: int,
+                              step_constant: float = 0.0,
+                              ctx: Optional[Context] = None) -> ReferenceTensor:
+    """reference.hpp:95-153 with the grid given as (cells N_l, box widths b_l)."""
+    ctx = ctx or default_context()
+    h = ctypes.c_void_p()
+    ctx.check(_lib.lib().latsum_reference_build(ctx.handle, kernel.family, kernel.lam,
+                                                _p(_i64(N)), _p(_f64(box)), int(M),
+                                                float(step_constant), ctypes.byref(h)))
+    return ReferenceTensor(ctx, h, kernel, N, box, M)
+
+
+class CanonicalTensor:
+    """canonical.hpp:19-202: unit side-matrix columns + weights, device resident.
+
+    Internally the side matrices are stored as per-mode dictionaries of distinct
+    columns; `factor(mode)` materialises the reference's N x M_c form."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx, self._h = ctx, handle
+        dims, dcols, rank, T = np.zeros(3, np.int64), np.zeros(3, np.int64), ctypes.c_int64(), ctypes.c_int64()
+        _lib.lib().latsum_canonical_info(self._h, _p(dims), ctypes.byref(rank), _p(dcols),
+                                         ctypes.byref(T))
+        self.dims = tuple(int(x) for x in dims)
+        self.rank = int(rank.value)
+        self.dict_cols = tuple(int(x) for x in dcols)
+        self.merged_terms = int(T.value)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def weights(self) -> np.ndarray:
+        w = np.zeros(self.rank)
+        _lib.check(_lib.lib().latsum_canonical_weights(self._h, _p(w)))
+        return w
+
+    def factor(self, mode: int) -> np.ndarray:
+        out = np.zeros((self.dims[mode], self.rank), order="F")
+        self.ctx.check(_lib.lib().latsum_canonical_factor(self.ctx.handle, self._h, mode, _p(out)))
+        return out
+
+    def factor_device(self, mode: int, out_ptr: int):
+        self.ctx.check(_lib.lib().latsum_canonical_factor_device(self.ctx.handle, self._h, mode,
+                                                                 ctypes.c_void_p(out_ptr)))
+
+    def entries(self, probes) -> np.ndarray:
+        pr = _i64(probes).reshape(-1, 3)
+        out = np.zeros(pr.shape[0])
+        self.ctx.check(_lib.lib().latsum_canonical_entries(self.ctx.handle, self._h, _p(pr),
+                                                           pr.shape[0], _p(out)))
+        return out
+
+    def entry(self, i: int, j: int, k: int) -> float:
+        return float(self.entries([[i, j, k]])[0])
+
+    def norm(self) -> float:
+        v = ctypes.c_double()
+        self.ctx.check(_lib.lib().latsum_canonical_norm(self.ctx.handle, self._h, ctypes.byref(v)))
+        return v.value
+
+    def eval_box_device(self, lo, hi, out_ptr: int):
+        self.ctx.check(_lib.lib().latsum_canonical_eval_box_device(
+            self.ctx.handle, self._h, _p(_i64(lo)), _p(_i64(hi)), ctypes.c_void_p(out_ptr)))
+
+    def to_dense(self, lo=None, hi=None, guard: int = 10_000_000) -> np.ndarray:
+        """canonical.hpp:192-202 on a box (default: the whole grid), via the device."""
+        import torch
+        lo = (0, 0, 0) if lo is None else tuple(lo)
+        hi = self.dims if hi is None else tuple(hi)
+        shape = tuple(h - l for l, h in zip(lo, hi))
+        if int(np.prod(shape)) > guard:
+            raise OverflowError(f"dense materialization of {int(np.prod(shape))} entries exceeds "
+                                f"the guard limit {guard}")
+        buf = torch.empty(int(np.prod(shape)), dtype=torch.float64, device=f"cuda:{self.ctx.device}")
+        self.eval_box_device(lo, hi, buf.data_ptr())
+        self.ctx.synchronize()
+        return buf.cpu().numpy().reshape(shape, order="F")
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_canonical_destroy(self._h)
+            self._h = None
+
+
+class TuckerTensor:
+    """tucker.hpp:19-73, device resident."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx, self._h = ctx, handle
+        dims, ranks = np.zeros(3, np.int64), np.zeros(3, np.int64)
+        _lib.lib().latsum_tucker_info(self._h, _p(dims), _p(ranks))
+        self.dims = tuple(int(x) for x in dims)
+        self.ranks = tuple(int(x) for x in ranks)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def core(self) -> np.ndarray:
+        out = np.zeros(self.ranks, order="F")
+        self.ctx.check(_lib.lib().latsum_tucker_core(self.ctx.handle, self._h, _p(out)))
+        return out
+
+    def factor(self, mode: int) -> np.ndarray:
+        out = np.zeros((self.dims[mode], self.ranks[mode]), order="F")
+        self.ctx.check(_lib.lib().latsum_tucker_factor(self.ctx.handle, self._h, mode, _p(out)))
+        return out
+
+    def entries(self, probes) -> np.ndarray:
+        pr = _i64(probes).reshape(-1, 3)
+        out = np.zeros(pr.shape[0])
+        self.ctx.check(_lib.lib().latsum_tucker_entries(self.ctx.handle, self._h, _p(pr),
+                                                        pr.shape[0], _p(out)))
+        return out
+
+    def entry(self, i: int, j: int, k: int) -> float:
+        return float(self.entries([[i, j, k]])[0])
+
+    def eval_box_device(self, lo, hi, out_ptr: int):
+        self.ctx.check(_lib.lib().latsum_tucker_eval_box_device(
+            self.ctx.handle, self._h, _p(_i64(lo)), _p(_i64(hi)), ctypes.c_void_p(out_ptr)))
+
+    def to_dense(self, lo=None, hi=None, guard: int = 10_000_000) -> np.ndarray:
+        """tucker.hpp:172-178 on a box (default: the whole grid) into host memory."""
+        lo = (0, 0, 0) if lo is None else tuple(lo)
+        hi = self.dims if hi is None else tuple(hi)
+        shape = tuple(h - l for l, h in zip(lo, hi))
+        if int(np.prod(shape)) > guard:
+            raise OverflowError(f"dense materialization of {int(np.prod(shape))} entries exceeds "
+                                f"the guard limit {guard}")
+        out = np.zeros(shape, order="F")
+        self.ctx.check(_lib.lib().latsum_tucker_eval_box(self.ctx.handle, self._h, _p(_i64(lo)),
+                                                         _p(_i64(hi)), _p(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_tucker_destroy(self._h)
+            self._h = None
+
+
+# ----------------------------------------------------------------------------- sums
+
+def _shift_tables(geom: Geometry):
+    nsub = len(geom.sublattices)
+    counts = np.array([[len(s.shifts[l]) for l in range(3)] for s in geom.sublattices],
+                      np.int64).reshape(-1, 3)
+    shifts = (np.concatenate([np.asarray(s.shifts[l], np.int64) for s in geom.sublattices
+                              for l in range(3)]) if nsub else np.zeros(0, np.int64))
+    charges = np.array([s.charge for s in geom.sublattices], np.float64)
+    return nsub, _i64(counts), _i64(shifts), _f64(charges), _i64(geom.defect_shifts.reshape(-1, 3)), \
+        _f64(geom.defect_charges)
+
+
+def lattice_sum(ref: ReferenceTensor, geom: Geometry) -> CanonicalTensor:
+    """Assembled sublattice sums plus additive defect windows (canonical, untruncated)."""
+    ctx = ref.ctx
+    nsub, counts, shifts, charges, dsh, dch = _shift_tables(geom)
+    h = ctypes.c_void_p()
+    ctx.check(_lib.lib().latsum_canonical_assemble(
+        ctx.handle, ref.handle, nsub, _p(counts), _p(shifts), _p(charges), dsh.shape[0], _p(dsh),
+        _p(dch), ctypes.byref(h)))
+    return CanonicalTensor(ctx, h)
+
+
+def assembled_sum_canonical(ref: ReferenceTensor, cells, n_per_cell: int, cell_width: float = 1.0,
+                            base_charge: float = 1.0, active=None) -> CanonicalTensor:
+    """lattice_sum.hpp:198-223 for LatticeGeometry(cells, cell_width) on lattice_grid."""
+    g = from_lattice(cells, n_per_cell, cell_width, base_charge=base_charge, active=active,
+                     M=ref.M)
+    return lattice_sum(ref, g)
+
+
+def defected_sum(ref: ReferenceTensor, cells, n_per_cell: int, defects, cell_width: float = 1.0,
+                 base_charge: float = 1.0, spec: Optional[TruncationSpec] = None, deflate="auto"):
+    """lattice_sum.hpp:339-400 (canonical branch): base lattice + defect clusters
+    `defects` = [(sites, charge, grid_offset)], truncated by RHOSVD when `spec` is set."""
+    g = from_lattice(cells, n_per_cell, cell_width, base_charge=base_charge, defects=defects,
+                     M=ref.M)
+    can = lattice_sum(ref, g)
+    if spec is None:
+        return can
+    return rhosvd(can, spec, deflate=deflate)
+
+
+def sublattice_union_sum(ref: ReferenceTensor, parent_cells, n_per_cell: int, subs,
+                         cell_width: float = 1.0, spec: Optional[TruncationSpec] = None,
+                         deflate="auto"):
+    """lattice_sum.hpp:411-465; subs = [(cells, offset_cells)]."""
+    g = from_lattice(parent_cells, n_per_cell, cell_width, sublattices=subs,
+                     parent_cells=parent_cells, M=ref.M)
+    can = lattice_sum(ref, g)
+    if spec is None:
+        return can
+    return rhosvd(can, spec, deflate=deflate)
+
+
+def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto"):
+    """rank_reduction.hpp:176-218 -> (TuckerTensor, SpectralReport)."""
+    spec.validate()
+    ctx = can.ctx
+    rep = _lib.LatsumReport()
+    h = ctypes.c_void_p()
+    ranks = _i64(spec.ranks) if spec.ranks is not None else None
+    ctx.check(_lib.lib().latsum_rhosvd(ctx.handle, can.handle,
+                                       _p(ranks) if ranks is not None else None,
+                                       float(spec.tolerance or 0.0), DEFLATE[deflate], ctypes.byref(h),
+                                       ctypes.byref(rep)))
+    t = TuckerTensor(ctx, h)
+    sv = []
+    for l in range(3):
+        s = np.zeros(int(rep.n_singular[l]))
+        _lib.check(_lib.lib().latsum_tucker_singular_values(h, l, _p(s)))
+        sv.append(s)
+    report = SpectralReport(
+        singular_values=sv, chosen_ranks=tuple(int(x) for x in rep.chosen_ranks),
+        bound_abs=rep.bound_abs, bound_rel=rep.bound_rel, weight_norm=rep.weight_norm,
+        input_norm=rep.input_norm, stability_constant=rep.stability_constant,
+        stability_ok=bool(rep.stability_ok), tie_at_cutoff=tuple(bool(x) for x in rep.tie_at_cutoff),
+        cutoff_margin=tuple(float(x) for x in rep.cutoff_margin),
+        deflated=tuple(bool(x) for x in rep.deflated), gram_rows=tuple(bool(x) for x in rep.gram_rows),
+        gram_size=tuple(int(x) for x in rep.gram_size),
+        ms=dict(gram=rep.ms_gram, syevd=rep.ms_syevd, deflate=rep.ms_deflate,
+                project=rep.ms_project, core=rep.ms_core, norm=rep.ms_norm, total=rep.ms_total))
+    return t, report
+
+
+def reference_for(geom: Geometry, ctx: Optional[Context] = None) -> ReferenceTensor:
+    kernel = KernelSpec(geom.family, geom.lam)
+    return build_reference_canonical(kernel, geom.N, geom.box, geom.M, geom.C0, ctx=ctx)
+
+
+def sum_to_tucker(geom: Geometry, tolerance: float, ctx: Optional[Context] = None):
+    """cmd_sum's defected/sublattice path with a tolerance (commands.cpp:108-179) in one
+    C-ABI call with host-resident inputs: stages 1-3, Tucker result on the device."""
+    ctx = ctx or default_context()
+    nsub, counts, shifts, charges, dsh, dch = _shift_tables(geom)
+    rep = _lib.LatsumReport()
+    h = ctypes.c_void_p()
+    ctx.check(_lib.lib().latsum_sum_to_tucker(
+        ctx.handle, geom.family, geom.lam, _p(_i64(geom.N)), _p(_f64(geom.box)), geom.M, geom.C0,
+        nsub, _p(counts), _p(shifts), _p(charges), dsh.shape[0], _p(dsh), _p(dch),
+        float(tolerance), ctypes.byref(h), ctypes.byref(rep)))
+    return TuckerTensor(ctx, h), rep

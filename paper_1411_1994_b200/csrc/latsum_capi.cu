@@ -1,0 +1,1300 @@
+// C ABI of the B200 lattice-sum hot path: context, device-resident handles and the
+// orchestration of the four FP64 stages.  Internally C++ with
+// exceptions; every extern "C" entry point catches, records latsum_last_error and
+// returns a status code (the reference's exception types map to LATSUM_ERR_*).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "dgemm_dmma.cuh"
+#include "latsum_b200.h"
+#include "latsum_kernels.cuh"
+
+using namespace latsum_b200;
+
+namespace {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw Error(e_ == cudaErrorMemoryAllocation ? LATSUM_ERR_OUT_OF_MEMORY             \
+                                                  : LATSUM_ERR_CUDA,                     \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+#define CS(call)                                                                          \
+  do {                                                                                    \
+    cusolverStatus_t s_ = (call);                                                         \
+    if (s_ != CUSOLVER_STATUS_SUCCESS)                                                    \
+      throw Error(LATSUM_ERR_CUSOLVER, std::string(#call) + ": status " + std::to_string(int(s_))); \
+  } while (0)
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(LATSUM_ERR_INVALID_ARGUMENT, msg);
+}
+
+}  // namespace
+
+struct latsum_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  cusolverDnParams_t solver_params = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  bool smem_set = false;
+};
+
+namespace {
+
+// Stream-ordered device buffer owned by a context's stream.
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(latsum_ctx* c, size_t count) { alloc(c, count); }
+  void alloc(latsum_ctx* c, size_t count) {
+    release();
+    s = c->stream;
+    n = count;
+    if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(double), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+};
+
+template <typename T>
+struct DVec {  // small device array of T
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DVec() = default;
+  void upload(latsum_ctx* c, const std::vector<T>& h) {
+    release();
+    s = c->stream;
+    n = h.size();
+    if (n) {
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), s));
+      CK(cudaMemcpyAsync(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DVec() { release(); }
+};
+
+int grid_for(int64_t total, int threads = 256) {
+  int64_t b = (total + threads - 1) / threads;
+  return int(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
+}
+
+void post_launch(latsum_ctx* c) {
+  c->launches++;
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ GEMM launcher
+struct GemmOpts {
+  int64_t batch = 1, sA = 0, sB = 0, sC = 0;
+  const int64_t* kseg = nullptr;
+  bool lower = false;
+  int splits = 0;  // 0 = auto
+};
+
+void set_gemm_smem(latsum_ctx* c) {
+  if (c->smem_set) return;
+  const int bytes = int(gemm_cfg::SMEM_BYTES);
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<false, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<true, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<true, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  c->smem_set = true;
+}
+
+void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+          const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+          int64_t ldc, GemmOpts o = {}) {
+  if (M <= 0 || N <= 0 || o.batch <= 0) return;
+  set_gemm_smem(c);
+  using namespace gemm_cfg;
+  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  int splits = o.splits;
+  if (splits == 0) {
+    splits = 1;
+    const int64_t tiles = tm * tn * o.batch;
+    if (!o.kseg && tiles < 148 && K >= 8 * BK) {
+      splits = int(std::min<int64_t>({(2 * 148 + tiles - 1) / tiles, K / (4 * BK), 16}));
+      splits = std::max(splits, 1);
+    }
+  }
+  require(tn <= 65535 && o.batch * splits <= 65535, "gemm: grid too large");
+  GemmParams p{M, N, K, A, lda, o.sA, B, ldb, o.sB, C, ldc, o.sC, alpha, beta, o.batch, splits,
+               o.kseg, o.lower ? 1 : 0};
+  DBuf ws;
+  if (splits > 1) {
+    ws.alloc(c, size_t(splits) * M * N * o.batch);
+    p.C = ws.p;
+  }
+  dim3 grid(unsigned(tm), unsigned(tn), unsigned(o.batch * splits));
+  if (!ta && !tb) dgemm_dmma_kernel<false, false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
+  if (!ta && tb) dgemm_dmma_kernel<false, true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
+  if (ta && !tb) dgemm_dmma_kernel<true, false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
+  if (ta && tb) dgemm_dmma_kernel<true, true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
+  post_launch(c);
+  if (splits > 1) {
+    dim3 g2(unsigned(grid_for(M * N)), unsigned(o.batch));
+    dgemm_reduce_splits<<<g2, 256, 0, c->stream>>>(ws.p, splits, M, N, C, ldc, o.sC, alpha, beta,
+                                                   o.lower ? 1 : 0);
+    post_launch(c);
+  }
+}
+
+// ------------------------------------------------------------------ syevd
+// Eigen-decomposition of the symmetric n x n matrix A (lower triangle read):
+// eigenvalues ascending in W (device), eigenvectors overwrite A.  cuSOLVER's
+// 64-bit API (size_t workspaces; the int32 LAPACK workspace overflows at N=32768).
+void syevd(latsum_ctx* c, int64_t n, double* A, double* W) {
+  size_t dbytes = 0, hbytes = 0;
+  CS(cusolverDnXsyevd_bufferSize(c->solver, c->solver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                 CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F, W,
+                                 CUDA_R_64F, &dbytes, &hbytes));
+  DBuf work(c, (dbytes + 7) / 8 + 1);
+  std::vector<char> hwork(hbytes + 1);
+  int* info = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&info), sizeof(int), c->stream));
+  CS(cusolverDnXsyevd(c->solver, c->solver_params, CUSOLVER_EIG_MODE_VECTOR,
+                      CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F, W, CUDA_R_64F,
+                      work.p, dbytes, hwork.data(), hbytes, info));
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(info, c->stream);
+  if (hinfo != 0) throw Error(LATSUM_ERR_CUSOLVER, "syevd: info = " + std::to_string(hinfo));
+}
+
+struct Timer {
+  latsum_ctx* c;
+  cudaEvent_t a, b;
+  explicit Timer(latsum_ctx* ctx) : c(ctx) {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void start() { CK(cudaEventRecord(a, c->stream)); }
+  double stop() {
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ handles
+
+struct latsum_reference {
+  int family = 0;
+  double lambda = 0;
+  int M = 0, R = 0, Rd = 0;
+  double C0 = 0, shell[2] = {0, 0};
+  int64_t N[3] = {0, 0, 0};
+  double box[3] = {0, 0, 0};
+  std::vector<double> nodes, qweights, weights;
+  std::vector<int> jmap;       // R -> distinct column
+  int owner[3] = {0, 1, 2};    // mode whose storage this mode shares
+  DBuf cols[3];                // 2N x Rd, unit columns (only owners allocate)
+  const double* col(int l) const { return cols[owner[l]].p; }
+};
+
+struct latsum_canonical {
+  int64_t N[3] = {0, 0, 0};
+  int Rd = 0, R = 0;
+  int64_t Mc = 0, T = 0;
+  int64_t d[3] = {0, 0, 0};
+  DBuf dict[3];                              // N_l x d_l
+  std::vector<double> dict_norms[3];
+  std::vector<int64_t> term_col[3];          // M_c per mode (reference order)
+  std::vector<double> weights;               // M_c
+  std::vector<double> mult[3];               // multiplicity per dictionary column
+  // merged terms sorted by c0
+  std::vector<int32_t> tc[3];
+  std::vector<double> tw;
+  std::vector<int64_t> tseg;                 // d0 + 1
+  DVec<int32_t> dtc[3];
+  DVec<double> dtw;
+  DVec<int64_t> dtseg;
+};
+
+struct latsum_tucker {
+  int64_t N[3] = {0, 0, 0};
+  int64_t r[3] = {1, 1, 1};
+  DBuf U[3];     // N_l x r_l
+  DBuf core;     // r0 x r1 x r2
+  std::vector<double> sigma[3];
+};
+
+namespace {
+
+template <typename F>
+int guarded(latsum_ctx* c, F&& f) {
+  try {
+    f();
+    return LATSUM_OK;
+  } catch (const Error& e) {
+    if (c) c->err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return LATSUM_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return LATSUM_ERR_INVALID_ARGUMENT;
+  }
+}
+
+// ------------------------------------------------------------------ stage 1
+void build_reference(latsum_ctx* c, int family, double lambda, const int64_t N[3],
+                     const double box[3], int M, double C0, latsum_reference& ref) {
+  require(family == LATSUM_NEWTON || family == LATSUM_YUKAWA,
+          "build_reference: only gauss-type primitives (newton, yukawa) are on the hot path");
+  for (int l = 0; l < 3; ++l) {
+    require(N[l] >= 2, "UniformGrid: need at least 2 cells per mode");
+    require(N[l] % 2 == 0, "UniformGrid: odd cell count in mode " + std::to_string(l + 1) +
+                               " rejected; the centered window assumes even n");
+    require(box[l] > 0.0, "UniformGrid: box width must be positive");
+  }
+  require(M >= 2, "build_quadrature: M >= 2 required");
+  ref.family = family;
+  ref.lambda = lambda;
+  ref.M = M;
+  ref.R = 2 * M + 1;
+  for (int l = 0; l < 3; ++l) {
+    ref.N[l] = N[l];
+    ref.box[l] = box[l];
+  }
+  latsum_reference_shell(N, box, ref.shell);
+  ref.C0 = C0 > 0.0 ? C0
+                    : latsum_default_step_constant(family, lambda, M, ref.shell[0], ref.shell[1], 320);
+  ref.nodes.resize(ref.R);
+  ref.qweights.resize(ref.R);
+  int st = latsum_build_quadrature(family, lambda, M, ref.C0, ref.shell[0], ref.shell[1],
+                                   ref.nodes.data(), ref.qweights.data());
+  if (st != LATSUM_OK) throw Error(st, "build_quadrature: invalid rule parameters");
+
+  // distinct exponents s = t^2 (t_{-k} = -t_k share one column, reference.hpp:41-51)
+  std::vector<double> sd;
+  ref.jmap.resize(ref.R);
+  for (int k = 0; k < ref.R; ++k) {
+    const double s = ref.nodes[k] * ref.nodes[k];
+    int j = -1;
+    for (size_t q = 0; q < sd.size(); ++q)
+      if (sd[q] == s) { j = int(q); break; }
+    if (j < 0) { j = int(sd.size()); sd.push_back(s); }
+    ref.jmap[k] = j;
+  }
+  ref.Rd = int(sd.size());
+  DVec<double> ds;
+  ds.upload(c, sd);
+
+  ref.weights.assign(ref.qweights.begin(), ref.qweights.end());  // coefficient 1
+  std::vector<double> norms[3];
+  for (int l = 0; l < 3; ++l) {
+    ref.owner[l] = l;
+    for (int m = 0; m < l; ++m)
+      if (N[l] == N[m] && box[l] == box[m]) { ref.owner[l] = ref.owner[m]; break; }
+    if (ref.owner[l] == l) {
+      const int64_t n2 = 2 * N[l];
+      const double h = (2.0 * box[l]) / double(n2);
+      const double lower = 0.0 - (2.0 * box[l]) / 2.0;
+      ref.cols[l].alloc(c, size_t(n2) * ref.Rd);
+      dim3 g(unsigned((n2 + 255) / 256), unsigned(ref.Rd));
+      k_ref_integrals<<<g, 256, 0, c->stream>>>(ds.p, n2, lower, h, ref.cols[l].p);
+      post_launch(c);
+      DBuf dn(c, ref.Rd);
+      k_normalize_columns<<<ref.Rd, 512, 0, c->stream>>>(ref.cols[l].p, n2, dn.p);
+      post_launch(c);
+      norms[l].resize(ref.Rd);
+      CK(cudaMemcpyAsync(norms[l].data(), dn.p, sizeof(double) * ref.Rd, cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    } else {
+      norms[l] = norms[ref.owner[l]];
+    }
+  }
+  // from_raw (canonical.hpp:32-48): weights absorb the three column norms
+  for (int l = 0; l < 3; ++l)
+    for (int k = 0; k < ref.R; ++k) {
+      const double nrm = norms[l][ref.jmap[k]];
+      if (nrm == 0.0) ref.weights[k] = 0.0;
+      else ref.weights[k] *= nrm;
+    }
+}
+
+// ------------------------------------------------------------------ stage 2
+void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const int64_t* sub_counts,
+              const int64_t* sub_shifts, const double* sub_charges, int64_t ndef,
+              const int64_t* def_shifts, const double* def_charges, latsum_canonical& can) {
+  require(nsub >= 0 && ndef >= 0, "assemble: negative counts");
+  const int R = ref.R, Rd = ref.Rd;
+  can.R = R;
+  can.Rd = Rd;
+  const int64_t nblk = nsub + ndef;
+  can.Mc = int64_t(R) * nblk;
+  for (int l = 0; l < 3; ++l) can.N[l] = ref.N[l];
+
+  // per-mode placements: sublattices first, then distinct defect shifts
+  std::vector<int64_t> block_pl[3];
+  std::vector<int64_t> sub_off(size_t(nsub) * 3 + 1, 0);
+  {
+    int64_t o = 0;
+    for (int64_t s = 0; s < nsub; ++s)
+      for (int l = 0; l < 3; ++l) {
+        sub_off[s * 3 + l] = o;
+        require(sub_counts[s * 3 + l] >= 1, "assembled_vector: empty active set");
+        o += sub_counts[s * 3 + l];
+      }
+    sub_off[size_t(nsub) * 3] = o;
+  }
+  for (int l = 0; l < 3; ++l) {
+    const int64_t N = ref.N[l];
+    std::vector<int64_t> pl_off{0}, pl_shift;
+    auto check = [&](int64_t cshift) {
+      const int64_t begin = N / 2 - cshift;
+      if (begin < 0 || begin + N > 2 * N)
+        throw Error(LATSUM_ERR_WINDOW_OVERFLOW,
+                    "window overflow in mode " + std::to_string(l + 1) + ": shift " +
+                        std::to_string(-cshift) + " pushes the length-" + std::to_string(N) +
+                        " window outside the doubled grid");
+    };
+    block_pl[l].resize(nblk);
+    for (int64_t s = 0; s < nsub; ++s) {
+      const int64_t* sh = sub_shifts + sub_off[s * 3 + l];
+      for (int64_t q = 0; q < sub_counts[s * 3 + l]; ++q) {
+        check(sh[q]);
+        pl_shift.push_back(sh[q]);
+      }
+      pl_off.push_back(int64_t(pl_shift.size()));
+      block_pl[l][s] = s;
+    }
+    std::map<int64_t, int64_t> seen;
+    for (int64_t dd = 0; dd < ndef; ++dd) {
+      const int64_t cs = def_shifts[dd * 3 + l];
+      auto it = seen.find(cs);
+      int64_t p;
+      if (it == seen.end()) {
+        check(cs);
+        p = int64_t(pl_off.size()) - 1;
+        seen[cs] = p;
+        pl_shift.push_back(cs);
+        pl_off.push_back(int64_t(pl_shift.size()));
+      } else {
+        p = it->second;
+      }
+      block_pl[l][nsub + dd] = p;
+    }
+    const int64_t P = int64_t(pl_off.size()) - 1;
+    can.d[l] = P * Rd;
+    if (can.d[l] == 0) continue;
+    DVec<int64_t> doff, dsh;
+    doff.upload(c, pl_off);
+    dsh.upload(c, pl_shift);
+    can.dict[l].alloc(c, size_t(N) * can.d[l]);
+    const int64_t chunk = 2048;
+    const int nchunk = int((N + chunk - 1) / chunk);
+    DBuf partial(c, size_t(can.d[l]) * nchunk), norms(c, can.d[l]);
+    DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
+    dim3 g(unsigned(can.d[l]), unsigned(nchunk));
+    k_dict_sumsq<<<g, 256, 0, c->stream>>>(a);
+    post_launch(c);
+    k_dict_norms<<<unsigned((can.d[l] + 255) / 256), 256, 0, c->stream>>>(a, can.d[l]);
+    post_launch(c);
+    k_dict_write<<<g, 256, 0, c->stream>>>(a);
+    post_launch(c);
+    can.dict_norms[l].resize(can.d[l]);
+    CK(cudaMemcpyAsync(can.dict_norms[l].data(), norms.p, sizeof(double) * can.d[l],
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+
+  // terms in reference order (add_concat: sublattice blocks, then defects)
+  can.weights.resize(can.Mc);
+  for (int l = 0; l < 3; ++l) {
+    can.term_col[l].resize(can.Mc);
+    can.mult[l].assign(can.d[l], 0.0);
+  }
+  for (int64_t b = 0; b < nblk; ++b) {
+    const double charge = b < nsub ? sub_charges[b] : def_charges[b - nsub];
+    for (int k = 0; k < R; ++k) {
+      const int64_t q = b * R + k;
+      double w = charge * ref.weights[k];
+      for (int l = 0; l < 3; ++l) {
+        const int64_t col = block_pl[l][b] * Rd + ref.jmap[k];
+        can.term_col[l][q] = col;
+        can.mult[l][col] += 1.0;
+        const double nrm = can.dict_norms[l][col];
+        if (nrm == 0.0) w = 0.0;
+        else w *= nrm;
+      }
+      can.weights[q] = w;
+    }
+  }
+  // merge identical rank-1 terms (same column in all three modes)
+  std::map<std::tuple<int64_t, int64_t, int64_t>, double> merged;
+  for (int64_t q = 0; q < can.Mc; ++q)
+    merged[{can.term_col[0][q], can.term_col[1][q], can.term_col[2][q]}] += can.weights[q];
+  can.T = int64_t(merged.size());
+  for (int l = 0; l < 3; ++l) can.tc[l].clear();
+  can.tw.clear();
+  can.tseg.assign(can.d[0] + 1, 0);
+  for (const auto& kv : merged) {  // map order: sorted by c0, then c1, c2
+    can.tc[0].push_back(int32_t(std::get<0>(kv.first)));
+    can.tc[1].push_back(int32_t(std::get<1>(kv.first)));
+    can.tc[2].push_back(int32_t(std::get<2>(kv.first)));
+    can.tw.push_back(kv.second);
+    can.tseg[std::get<0>(kv.first) + 1] += 1;
+  }
+  for (int64_t a = 0; a < can.d[0]; ++a) can.tseg[a + 1] += can.tseg[a];
+  for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
+  can.dtw.upload(c, can.tw);
+  can.dtseg.upload(c, can.tseg);
+}
+
+void materialize_factor(latsum_ctx* c, const latsum_canonical& can, int l, double* dst_device) {
+  if (can.Mc == 0) return;
+  DVec<int64_t> idx;
+  idx.upload(c, can.term_col[l]);
+  const int64_t N = can.N[l];
+  dim3 g(unsigned(std::max<int64_t>(1, std::min<int64_t>(64, (N / 2 + 255) / 256))),
+         unsigned(can.Mc));
+  require(can.Mc <= 65535 * 64, "materialize: too many columns");
+  if (can.Mc > 65535) {
+    // split along the column dimension
+    for (int64_t q0 = 0; q0 < can.Mc; q0 += 65535) {
+      const int64_t nq = std::min<int64_t>(65535, can.Mc - q0);
+      dim3 g2(g.x, unsigned(nq));
+      k_gather_columns<<<g2, 256, 0, c->stream>>>(can.dict[l].p, N, idx.p + q0,
+                                                  dst_device + q0 * N);
+      post_launch(c);
+    }
+  } else {
+    k_gather_columns<<<g, 256, 0, c->stream>>>(can.dict[l].p, N, idx.p, dst_device);
+    post_launch(c);
+  }
+}
+
+
+// ------------------------------------------------------------------ stage 3
+constexpr double kEpsMach = 2.220446049250313e-16;
+
+// rank_reduction.hpp:73-84: smallest r with sqrt(sum_{k>=r} s_k^2) <= eps ||s|| / 3, r >= 1.
+int64_t rank_for_tolerance(const std::vector<double>& sv, double eps) {
+  double n2 = 0.0;
+  for (double v : sv) n2 += v * v;
+  const double target = eps * std::sqrt(n2) / 3.0;
+  double tail2 = 0.0;
+  int64_t r = int64_t(sv.size());
+  for (int64_t k = int64_t(sv.size()) - 1; k >= 0; --k) {
+    tail2 += sv[k] * sv[k];
+    if (std::sqrt(tail2) > target) break;
+    r = k;
+  }
+  return std::max<int64_t>(r, 1);
+}
+
+void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, double* G) {
+  GemmOpts o;
+  o.lower = true;
+  if (rows) gemm(c, false, true, N, N, d, 1.0, A, N, A, N, 0.0, G, N, o);   // A A^T
+  else gemm(c, true, false, d, d, N, 1.0, A, N, A, N, 0.0, G, d, o);        // A^T A
+}
+
+// Symmetric (Loewdin) re-orthonormalisation U <- U (U^T U)^{-1/2}, in place.
+void lowdin(latsum_ctx* c, double* U, int64_t N, int64_t k) {
+  if (k == 0) return;
+  DBuf S(c, size_t(k) * k), W(c, k);
+  gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k);
+  syevd(c, k, S.p, W.p);
+  std::vector<double> w(k);
+  CK(cudaMemcpyAsync(w.data(), W.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& v : w) v = v > 1e-300 ? 1.0 / std::sqrt(v) : 0.0;
+  DVec<double> sc;
+  sc.upload(c, w);
+  DBuf Qs(c, size_t(k) * k), Mm(c, size_t(k) * k), Un(c, size_t(N) * k);
+  k_scale_columns<<<grid_for(k * k), 256, 0, c->stream>>>(S.p, k, k, sc.p, Qs.p);
+  post_launch(c);
+  gemm(c, false, true, k, k, k, 1.0, Qs.p, k, S.p, k, 0.0, Mm.p, k);
+  gemm(c, false, false, N, k, k, 1.0, U, N, Mm.p, k, 0.0, Un.p, N);
+  CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// Top-k left singular directions of A (N x d) from the eigenpairs of its Gram
+// (evecs n x n ascending, lam_desc descending): for A A^T the eigenvectors
+// themselves; for A^T A, U = A V diag(1/sigma) re-orthonormalised.
+void left_basis(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d,
+                const double* evecs, int64_t n, const std::vector<double>& lam_desc, int64_t k,
+                double* U) {
+  if (k == 0) return;
+  if (rows) {
+    k_reverse_columns<<<grid_for(n * k), 256, 0, c->stream>>>(evecs, n, n, k, U);
+    post_launch(c);
+    return;
+  }
+  DBuf Vd(c, size_t(d) * k);
+  k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, d, k, Vd.p);
+  post_launch(c);
+  gemm(c, false, false, N, k, d, 1.0, A, N, Vd.p, d, 0.0, U, N);
+  std::vector<double> inv(k);
+  for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
+  DVec<double> sc;
+  sc.upload(c, inv);
+  k_scale_columns<<<grid_for(N * k), 256, 0, c->stream>>>(U, N, k, sc.p, U);
+  post_launch(c);
+  lowdin(c, U, N, k);
+}
+
+struct ModeOut {
+  std::vector<double> sigma;
+  int64_t r = 1;
+  DBuf Z;
+  bool tie = false;
+  double margin = 0.0;
+  int deflated = 0, rows = 0;
+  int64_t gsize = 0;
+};
+
+struct Timings {
+  double gram = 0, syevd = 0, deflate = 0, project = 0, core = 0, norm = 0;
+};
+
+// RHOSVD of one mode (rank_reduction.hpp:189-207) on the merged side matrix
+// A~ = D diag(sqrt(mult)), whose A~ A~^T equals the reference's A A^T.
+void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
+                 double tol, int deflate, ModeOut& out, Timings& tm) {
+  const int64_t N = can.N[l], d = can.d[l];
+  const int64_t n_sing = std::min<int64_t>(N, can.Mc);
+  Timer timer(c);
+  timer.start();
+  std::vector<double> sq(d);
+  for (int64_t j = 0; j < d; ++j) sq[j] = std::sqrt(can.mult[l][j]);
+  DVec<double> dsq;
+  dsq.upload(c, sq);
+  DBuf At(c, size_t(N) * d);
+  k_scale_columns<<<grid_for(N * d), 256, 0, c->stream>>>(can.dict[l].p, N, d, dsq.p, At.p);
+  post_launch(c);
+  const bool rows = N <= d;
+  const int64_t n = rows ? N : d;
+  out.rows = rows ? 1 : 0;
+  out.gsize = n;
+  DBuf G(c, size_t(n) * n), W(c, n);
+  gram(c, rows, At.p, N, d, G.p);
+  tm.gram += timer.stop();
+  timer.start();
+  syevd(c, n, G.p, W.p);
+  tm.syevd += timer.stop();
+  std::vector<double> lam(n), lam_d(n);
+  CK(cudaMemcpyAsync(lam.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < n; ++i) lam_d[i] = std::max(lam[n - 1 - i], 0.0);
+  const double lmax = lam_d.empty() ? 0.0 : lam_d[0];
+
+  auto padded_sigma = [&](const std::vector<double>& l2) {
+    std::vector<double> sv(n_sing, 0.0);
+    for (int64_t i = 0; i < std::min<int64_t>(n_sing, int64_t(l2.size())); ++i)
+      sv[i] = std::sqrt(std::max(l2[i], 0.0));
+    return sv;
+  };
+
+  // second (deflated) pass: resolves sigma below sqrt(eps_mach) sigma_1
+  std::vector<double> merged = lam_d;
+  std::vector<std::pair<int, int64_t>> src(n);  // (pass, index in that pass's desc order)
+  for (int64_t i = 0; i < n; ++i) src[i] = {0, i};
+  int64_t k1 = 0;
+  DBuf U1, G2, Ap;
+  std::vector<double> mu_d;
+  bool defl = false;
+  if (!ranks && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
+    const std::vector<double> sv = padded_sigma(lam_d);
+    double n2 = 0;
+    for (double v : sv) n2 += v * v;
+    const double target = tol * std::sqrt(n2) / 3.0;
+    defl = deflate == LATSUM_DEFLATE_ALWAYS ||
+           target * target < 1e6 * double(n) * kEpsMach * lmax;
+    if (defl) {
+      timer.start();
+      for (int64_t i = 0; i < n; ++i)
+        if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
+      k1 = std::max<int64_t>(k1, 1);
+      U1.alloc(c, size_t(N) * k1);
+      left_basis(c, rows, At.p, N, d, G.p, n, lam_d, k1, U1.p);
+      Ap.alloc(c, size_t(N) * d);
+      CK(cudaMemcpyAsync(Ap.p, At.p, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, c->stream));
+      DBuf C(c, size_t(k1) * d);
+      for (int rep = 0; rep < 2; ++rep) {  // project out span(U1), then re-orthogonalise once
+        gemm(c, true, false, k1, d, N, 1.0, U1.p, N, Ap.p, N, 0.0, C.p, k1);
+        gemm(c, false, false, N, d, k1, -1.0, U1.p, N, C.p, k1, 1.0, Ap.p, N);
+      }
+      G2.alloc(c, size_t(n) * n);
+      gram(c, rows, Ap.p, N, d, G2.p);
+      tm.deflate += timer.stop();
+      timer.start();
+      DBuf W2(c, n);
+      syevd(c, n, G2.p, W2.p);
+      tm.syevd += timer.stop();
+      std::vector<double> mu(n);
+      CK(cudaMemcpyAsync(mu.data(), W2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      mu_d.resize(n);
+      for (int64_t i = 0; i < n; ++i) mu_d[i] = std::max(mu[n - 1 - i], 0.0);
+      // merged spectrum: the k1 resolved pass-1 values and the top n-k1 deflated values
+      std::vector<std::tuple<double, int, int64_t>> all;
+      for (int64_t i = 0; i < k1; ++i) all.emplace_back(lam_d[i], 0, i);
+      for (int64_t i = 0; i < n - k1; ++i) all.emplace_back(mu_d[i], 1, i);
+      std::stable_sort(all.begin(), all.end(), [](const auto& a, const auto& b) {
+        return std::get<0>(a) > std::get<0>(b);
+      });
+      for (int64_t i = 0; i < n; ++i) {
+        merged[i] = std::get<0>(all[i]);
+        src[i] = {std::get<1>(all[i]), std::get<2>(all[i])};
+      }
+    }
+  }
+  out.deflated = defl ? 1 : 0;
+  out.sigma = padded_sigma(merged);
+  const auto& sv = out.sigma;
+
+  int64_t r;
+  if (ranks) r = std::min<int64_t>(std::max<int64_t>(ranks[l], 1), n_sing);
+  else r = rank_for_tolerance(sv, tol);
+  while (r > 1 && sv[r - 1] < 1e-14 * sv[0]) --r;  // drop numerically zero directions
+  r = std::min<int64_t>(r, n);
+  out.tie = r < int64_t(sv.size()) && sv[r - 1] - sv[r] <= 1e-12 * sv[0];
+  if (!ranks) {
+    double n2 = 0, t_r = 0, t_rm1 = 0;
+    for (double v : sv) n2 += v * v;
+    const double target = tol * std::sqrt(n2) / 3.0;
+    for (size_t k = r; k < sv.size(); ++k) t_r += sv[k] * sv[k];
+    t_rm1 = t_r + sv[r - 1] * sv[r - 1];
+    out.margin = std::min(target - std::sqrt(t_r), std::sqrt(t_rm1) - target) / target;
+  }
+  out.r = r;
+
+  // Z = the r leading left singular vectors in merged (descending) order
+  timer.start();
+  out.Z.alloc(c, size_t(N) * r);
+  if (!defl) {
+    left_basis(c, rows, At.p, N, d, G.p, n, lam_d, r, out.Z.p);
+  } else {
+    int64_t need2 = 0;
+    for (int64_t i = 0; i < r; ++i)
+      if (src[i].first == 1) need2 = std::max<int64_t>(need2, src[i].second + 1);
+    DBuf U2;
+    if (need2) {
+      U2.alloc(c, size_t(N) * need2);
+      left_basis(c, rows, Ap.p, N, d, G2.p, n, mu_d, need2, U2.p);
+    }
+    // gather columns [U1 | U2] in merged order
+    DBuf cat(c, size_t(N) * (k1 + need2));
+    CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * N * k1, cudaMemcpyDeviceToDevice, c->stream));
+    if (need2)
+      CK(cudaMemcpyAsync(cat.p + N * k1, U2.p, sizeof(double) * N * need2,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<int64_t> sel(r);
+    for (int64_t i = 0; i < r; ++i) sel[i] = src[i].first == 0 ? src[i].second : k1 + src[i].second;
+    DVec<int64_t> dsel;
+    dsel.upload(c, sel);
+    k_select_columns<<<grid_for(N * r), 256, 0, c->stream>>>(cat.p, N, dsel.p, r, out.Z.p);
+    post_launch(c);
+  }
+  tm.deflate += timer.stop();
+}
+
+double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
+  if (can.T == 0) return 0.0;
+  DBuf G[3];
+  for (int l = 0; l < 3; ++l) {
+    G[l].alloc(c, size_t(can.d[l]) * can.d[l]);
+    gemm(c, true, false, can.d[l], can.d[l], can.N[l], 1.0, can.dict[l].p, can.N[l],
+         can.dict[l].p, can.N[l], 0.0, G[l].p, can.d[l]);
+  }
+  DBuf part(c, can.T), sum(c, 1);
+  k_hadamard_norm_rows<<<unsigned((can.T + 127) / 128), 128, 0, c->stream>>>(
+      G[0].p, G[1].p, G[2].p, can.d[0], can.d[1], can.d[2], can.dtc[0].p, can.dtc[1].p,
+      can.dtc[2].p, can.dtw.p, can.T, part.p);
+  post_launch(c);
+  k_sum<<<1, 1024, 0, c->stream>>>(part.p, can.T, sum.p);
+  post_launch(c);
+  double s = 0;
+  CK(cudaMemcpyAsync(&s, sum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return s > 0.0 ? std::sqrt(s) : 0.0;
+}
+
+// core(a,b,c) = sum_t w_t P0(a,c0_t) P1(b,c1_t) P2(c,c2_t)  (project_core,
+// rank_reduction.hpp:88-100) as X_a = G1[:, seg_a] G2[:, seg_a]^T over the terms
+// grouped by their mode-1 column a (one segmented GEMM), then core = P0 X^T.
+void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
+               double* core) {
+  const int64_t T = can.T, d0 = can.d[0];
+  const int64_t r12 = r[1] * r[2];
+  DBuf G1(c, size_t(r[1]) * T), G2(c, size_t(r[2]) * T);
+  k_gather_scale<<<grid_for(r[1] * T), 256, 0, c->stream>>>(P[1].p, r[1], can.dtc[1].p,
+                                                            can.dtw.p, T, G1.p);
+  post_launch(c);
+  k_gather_scale<<<grid_for(r[2] * T), 256, 0, c->stream>>>(P[2].p, r[2], can.dtc[2].p, nullptr,
+                                                            T, G2.p);
+  post_launch(c);
+  const int64_t budget = int64_t(1) << 29;  // doubles of X per chunk (4 GiB)
+  const int64_t ac = std::max<int64_t>(1, std::min<int64_t>({d0, budget / std::max<int64_t>(r12, 1), 65535}));
+  DBuf X(c, size_t(r12) * ac);
+  for (int64_t a0 = 0; a0 < d0; a0 += ac) {
+    const int64_t na = std::min(ac, d0 - a0);
+    GemmOpts o;
+    o.batch = na;
+    o.sC = r12;
+    o.kseg = can.dtseg.p + a0;
+    gemm(c, false, true, r[1], r[2], T, 1.0, G1.p, r[1], G2.p, r[2], 0.0, X.p, r[1], o);
+    gemm(c, false, true, r[0], r12, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, r12,
+         a0 == 0 ? 0.0 : 1.0, core, r[0]);
+  }
+}
+
+void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks, double tol,
+                 int deflate, latsum_tucker& t, latsum_spectral_report& rep) {
+  if (!ranks) require(tol > 0.0 && tol < 1.0, "TruncationSpec: tolerance must lie in (0,1)");
+  std::memset(&rep, 0, sizeof(rep));
+  Timings tm;
+  Timer total(c);
+  total.start();
+  for (int l = 0; l < 3; ++l) t.N[l] = can.N[l];
+  double wn2 = 0;
+  for (double w : can.weights) wn2 += w * w;
+  rep.weight_norm = std::sqrt(wn2);
+  {
+    Timer tn(c);
+    tn.start();
+    rep.input_norm = canonical_norm(c, can);
+    tm.norm = tn.stop();
+  }
+  if (can.Mc == 0 || rep.input_norm == 0.0) {  // zero tensor (rank_reduction.hpp:183-187)
+    for (int l = 0; l < 3; ++l) {
+      rep.chosen_ranks[l] = 1;
+      rep.n_singular[l] = 1;
+      t.r[l] = 1;
+      t.sigma[l].assign(1, 0.0);
+      t.U[l].alloc(c, size_t(t.N[l]));
+      CK(cudaMemsetAsync(t.U[l].p, 0, sizeof(double) * t.N[l], c->stream));
+      const double one = 1.0;
+      CK(cudaMemcpyAsync(t.U[l].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    }
+    t.core.alloc(c, 1);
+    CK(cudaMemsetAsync(t.core.p, 0, sizeof(double), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    rep.ms_total = total.stop();
+    return;
+  }
+  ModeOut mo[3];
+  for (int l = 0; l < 3; ++l) reduce_mode(c, can, l, ranks, tol, deflate, mo[l], tm);
+  DBuf P[3];
+  Timer tp(c);
+  tp.start();
+  for (int l = 0; l < 3; ++l) {
+    t.r[l] = mo[l].r;
+    P[l].alloc(c, size_t(mo[l].r) * can.d[l]);
+    gemm(c, true, false, mo[l].r, can.d[l], can.N[l], 1.0, mo[l].Z.p, can.N[l], can.dict[l].p,
+         can.N[l], 0.0, P[l].p, mo[l].r);
+  }
+  tm.project = tp.stop();
+  tp.start();
+  t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
+  form_core(c, can, P, t.r, t.core.p);
+  tm.core = tp.stop();
+  double tails = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    t.U[l] = std::move(mo[l].Z);
+    t.sigma[l] = mo[l].sigma;
+    rep.chosen_ranks[l] = mo[l].r;
+    rep.n_singular[l] = int64_t(mo[l].sigma.size());
+    rep.tie_at_cutoff[l] = mo[l].tie ? 1 : 0;
+    rep.cutoff_margin[l] = mo[l].margin;
+    rep.deflated[l] = mo[l].deflated;
+    rep.gram_rows[l] = mo[l].rows;
+    rep.gram_size[l] = mo[l].gsize;
+    double s = 0;  // SpectralReport::tail (rank_reduction.hpp:61-66)
+    for (int64_t k = int64_t(mo[l].sigma.size()) - 1; k >= mo[l].r; --k)
+      s += mo[l].sigma[k] * mo[l].sigma[k];
+    tails += std::sqrt(s);
+  }
+  rep.bound_abs = rep.weight_norm * tails;
+  const double n2 = rep.input_norm * rep.input_norm;
+  rep.stability_constant = rep.weight_norm * rep.weight_norm / n2;
+  rep.stability_ok = rep.stability_constant <= 1.0 + 1e-10;
+  rep.bound_rel = std::sqrt(rep.stability_constant) * rep.input_norm * tails;
+  rep.ms_gram = tm.gram;
+  rep.ms_syevd = tm.syevd;
+  rep.ms_deflate = tm.deflate;
+  rep.ms_project = tm.project;
+  rep.ms_core = tm.core;
+  rep.ms_norm = tm.norm;
+  rep.ms_total = total.stop();
+}
+
+// ------------------------------------------------------------------ stage 4
+void check_box(const int64_t N[3], const int64_t lo[3], const int64_t hi[3]) {
+  for (int l = 0; l < 3; ++l)
+    if (lo[l] < 0 || hi[l] > N[l] || hi[l] <= lo[l])
+      throw Error(LATSUM_ERR_INVALID_ARGUMENT,
+                  "evaluation box outside the grid in mode " + std::to_string(l + 1));
+}
+
+// to_dense on a box (tucker.hpp:172-178) as slab GEMMs: Q = core x_2 U1, then per
+// z-chunk X = Q x_3 U2 and V_k = U0 X_k (the dominant ni x nj x r0 GEMM per slab).
+void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t hi[3],
+                 double* out) {
+  check_box(t.N, lo, hi);
+  const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
+  const int64_t r0 = t.r[0], r1 = t.r[1], r2 = t.r[2];
+  const double* U0 = t.U[0].p + lo[0];
+  const double* U1 = t.U[1].p + lo[1];
+  const double* U2 = t.U[2].p + lo[2];
+  const int64_t budget = int64_t(1) << 28;  // doubles per intermediate (2 GiB)
+  const int64_t njc = std::max<int64_t>(1, std::min<int64_t>(nj, budget / std::max<int64_t>(r0 * r2, 1)));
+  DBuf Q(c, size_t(r0) * njc * r2);
+  const int64_t nkc = std::max<int64_t>(1, std::min<int64_t>({nk, budget / std::max<int64_t>(r0 * njc, 1), 65535}));
+  DBuf X(c, size_t(r0) * njc * nkc);
+  for (int64_t j0 = 0; j0 < nj; j0 += njc) {
+    const int64_t njj = std::min(njc, nj - j0);
+    GemmOpts oq;
+    oq.batch = r2;
+    oq.sA = r0 * r1;
+    oq.sC = r0 * njj;
+    gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
+    for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
+      const int64_t nkk = std::min(nkc, nk - k0);
+      gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
+           r0 * njj);
+      GemmOpts ov;
+      ov.batch = nkk;
+      ov.sB = r0 * njj;
+      ov.sC = ni * nj;
+      gemm(c, false, false, ni, njj, r0, 1.0, U0, t.N[0], X.p, r0, 0.0,
+           out + k0 * ni * nj + j0 * ni, ni, ov);
+    }
+  }
+}
+
+void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo[3],
+                    const int64_t hi[3], double* out) {
+  check_box(can.N, lo, hi);
+  const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
+  const int64_t T = can.T;
+  if (T == 0) {
+    CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
+    return;
+  }
+  // A0 (ni x T): mode-1 dictionary rows of the box, gathered per merged term
+  DBuf A0(c, size_t(ni) * T);
+  {
+    DBuf tmp(c, size_t(ni) * can.d[0]);
+    CK(cudaMemcpy2DAsync(tmp.p, ni * sizeof(double), can.dict[0].p + lo[0],
+                         can.N[0] * sizeof(double), ni * sizeof(double), can.d[0],
+                         cudaMemcpyDeviceToDevice, c->stream));
+    k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(tmp.p, ni, can.dtc[0].p, nullptr, T,
+                                                            A0.p);
+    post_launch(c);
+  }
+  const int64_t budget = int64_t(1) << 27;
+  const int64_t nkc = std::max<int64_t>(1, std::min<int64_t>({nk, budget / std::max<int64_t>(T * nj, 1), 65535}));
+  DBuf X(c, size_t(T) * nj * nkc);
+  for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
+    const int64_t nkk = std::min(nkc, nk - k0);
+    k_canonical_slab_operand<<<grid_for(T * nj * nkk), 256, 0, c->stream>>>(
+        can.dict[1].p, can.N[1], can.dict[2].p, can.N[2], can.dtc[1].p, can.dtc[2].p, can.dtw.p,
+        T, lo[1], nj, lo[2] + k0, nkk, X.p);
+    post_launch(c);
+    GemmOpts ov;
+    ov.batch = nkk;
+    ov.sB = T * nj;
+    ov.sC = ni * nj;
+    gemm(c, false, false, ni, nj, T, 1.0, A0.p, ni, X.p, T, 0.0, out + k0 * ni * nj, ni, ov);
+  }
+}
+
+void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,
+                   double* out_host) {
+  for (int64_t p = 0; p < np; ++p)
+    for (int l = 0; l < 3; ++l)
+      if (probes[3 * p + l] < 0 || probes[3 * p + l] >= t.N[l])
+        throw Error(LATSUM_ERR_INVALID_ARGUMENT, "TuckerTensor::entry index out of range");
+  const int64_t r0 = t.r[0], r12 = t.r[1] * t.r[2];
+  const int64_t budget = int64_t(1) << 28;
+  const int64_t pc = std::max<int64_t>(1, std::min<int64_t>(np, budget / std::max<int64_t>(r12, 1)));
+  std::vector<int64_t> hp(probes, probes + 3 * np);
+  DVec<int64_t> dp;
+  dp.upload(c, hp);
+  DBuf rowsU(c, size_t(pc) * r0), Wm(c, size_t(pc) * r12), res(c, np);
+  for (int64_t p0 = 0; p0 < np; p0 += pc) {
+    const int64_t npp = std::min(pc, np - p0);
+    k_gather_rows<<<grid_for(npp * r0), 256, 0, c->stream>>>(t.U[0].p, t.N[0], r0, dp.p + 3 * p0,
+                                                             0, npp, rowsU.p);
+    post_launch(c);
+    gemm(c, false, false, npp, r12, r0, 1.0, rowsU.p, npp, t.core.p, r0, 0.0, Wm.p, npp);
+    k_tucker_probe_finish<<<unsigned(npp), 256, 0, c->stream>>>(
+        Wm.p, npp, t.r[1], t.r[2], t.U[1].p, t.N[1], t.U[2].p, t.N[2], dp.p + 3 * p0, res.p + p0);
+    post_launch(c);
+  }
+  CK(cudaMemcpyAsync(out_host, res.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int latsum_ctx_create(int device, latsum_ctx** out) {
+  if (!out) return LATSUM_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new latsum_ctx();
+  int st = guarded(c, [&] {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "latsum_ctx_create: no CUDA device " + std::to_string(device));
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    CS(cusolverDnCreate(&c->solver));
+    CS(cusolverDnSetStream(c->solver, c->stream));
+    CS(cusolverDnCreateParams(&c->solver_params));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  });
+  if (st != LATSUM_OK) {
+    static thread_local std::string last;
+    last = c->err;
+    fprintf(stderr, "latsum_ctx_create: %s\n", last.c_str());
+    delete c;
+    return st;
+  }
+  *out = c;
+  return LATSUM_OK;
+}
+
+void latsum_ctx_destroy(latsum_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->solver_params) cusolverDnDestroyParams(c->solver_params);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+const char* latsum_last_error(const latsum_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+int latsum_ctx_set_stream(latsum_ctx* c, void* s) {
+  return guarded(c, [&] {
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+    CS(cusolverDnSetStream(c->solver, c->stream));
+  });
+}
+
+int latsum_ctx_synchronize(latsum_ctx* c) {
+  return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int64_t latsum_ctx_kernel_launches(const latsum_ctx* c) { return c ? c->launches : 0; }
+
+int latsum_reference_build(latsum_ctx* c, int family, double lambda, const int64_t N[3],
+                           const double box[3], int M, double step_constant,
+                           latsum_reference** out) {
+  return guarded(c, [&] {
+    require(out && N && box, "latsum_reference_build: null argument");
+    auto ref = std::make_unique<latsum_reference>();
+    build_reference(c, family, lambda, N, box, M, step_constant, *ref);
+    *out = ref.release();
+  });
+}
+
+void latsum_reference_destroy(latsum_reference* ref) { delete ref; }
+
+int latsum_reference_info(const latsum_reference* ref, int* rank, double* c0, double shell[2]) {
+  if (!ref) return LATSUM_ERR_INVALID_ARGUMENT;
+  if (rank) *rank = ref->R;
+  if (c0) *c0 = ref->C0;
+  if (shell) { shell[0] = ref->shell[0]; shell[1] = ref->shell[1]; }
+  return LATSUM_OK;
+}
+
+int latsum_reference_factor(latsum_ctx* c, const latsum_reference* ref, int mode, double* factor) {
+  return guarded(c, [&] {
+    require(ref && factor && mode >= 0 && mode < 3, "latsum_reference_factor: bad argument");
+    const int64_t n2 = 2 * ref->N[mode];
+    std::vector<double> d(size_t(n2) * ref->Rd);
+    CK(cudaMemcpyAsync(d.data(), ref->col(mode), sizeof(double) * d.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < ref->R; ++k)
+      std::memcpy(factor + size_t(k) * n2, d.data() + size_t(ref->jmap[k]) * n2, sizeof(double) * n2);
+  });
+}
+
+int latsum_reference_weights(const latsum_reference* ref, double* w) {
+  if (!ref || !w) return LATSUM_ERR_INVALID_ARGUMENT;
+  std::memcpy(w, ref->weights.data(), sizeof(double) * ref->R);
+  return LATSUM_OK;
+}
+
+int latsum_reference_quadrature(const latsum_reference* ref, double* nodes, double* weights) {
+  if (!ref) return LATSUM_ERR_INVALID_ARGUMENT;
+  if (nodes) std::memcpy(nodes, ref->nodes.data(), sizeof(double) * ref->R);
+  if (weights) std::memcpy(weights, ref->qweights.data(), sizeof(double) * ref->R);
+  return LATSUM_OK;
+}
+
+int latsum_canonical_assemble(latsum_ctx* c, const latsum_reference* ref, int64_t nsub,
+                              const int64_t* sub_counts, const int64_t* sub_shifts,
+                              const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
+                              const double* def_charges, latsum_canonical** out) {
+  return guarded(c, [&] {
+    require(ref && out, "latsum_canonical_assemble: null argument");
+    auto can = std::make_unique<latsum_canonical>();
+    assemble(c, *ref, nsub, sub_counts, sub_shifts, sub_charges, ndef, def_shifts, def_charges,
+             *can);
+    *out = can.release();
+  });
+}
+
+void latsum_canonical_destroy(latsum_canonical* can) { delete can; }
+
+int latsum_canonical_info(const latsum_canonical* can, int64_t dims[3], int64_t* rank,
+                          int64_t dict_cols[3], int64_t* merged_terms) {
+  if (!can) return LATSUM_ERR_INVALID_ARGUMENT;
+  for (int l = 0; l < 3; ++l) {
+    if (dims) dims[l] = can->N[l];
+    if (dict_cols) dict_cols[l] = can->d[l];
+  }
+  if (rank) *rank = can->Mc;
+  if (merged_terms) *merged_terms = can->T;
+  return LATSUM_OK;
+}
+
+int latsum_canonical_weights(const latsum_canonical* can, double* w) {
+  if (!can || !w) return LATSUM_ERR_INVALID_ARGUMENT;
+  std::memcpy(w, can->weights.data(), sizeof(double) * can->Mc);
+  return LATSUM_OK;
+}
+
+int latsum_canonical_factor_device(latsum_ctx* c, const latsum_canonical* can, int mode,
+                                   double* dst) {
+  return guarded(c, [&] {
+    require(can && dst && mode >= 0 && mode < 3, "latsum_canonical_factor: bad argument");
+    materialize_factor(c, *can, mode, dst);
+  });
+}
+
+int latsum_canonical_factor(latsum_ctx* c, const latsum_canonical* can, int mode, double* factor) {
+  return guarded(c, [&] {
+    require(can && factor && mode >= 0 && mode < 3, "latsum_canonical_factor: bad argument");
+    DBuf tmp(c, size_t(can->N[mode]) * can->Mc);
+    materialize_factor(c, *can, mode, tmp.p);
+    CK(cudaMemcpyAsync(factor, tmp.p, sizeof(double) * tmp.n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int latsum_canonical_entries(latsum_ctx* c, const latsum_canonical* can, const int64_t* probes,
+                             int64_t np, double* out) {
+  return guarded(c, [&] {
+    require(can && (np == 0 || (probes && out)), "latsum_canonical_entries: bad argument");
+    if (np == 0) return;
+    for (int64_t p = 0; p < np; ++p)
+      for (int l = 0; l < 3; ++l)
+        if (probes[3 * p + l] < 0 || probes[3 * p + l] >= can->N[l])
+          throw Error(LATSUM_ERR_INVALID_ARGUMENT, "CanonicalTensor::entry index out of range");
+    if (can->T == 0) {
+      std::fill(out, out + np, 0.0);
+      return;
+    }
+    std::vector<int64_t> hp(probes, probes + 3 * np);
+    DVec<int64_t> dp;
+    dp.upload(c, hp);
+    DBuf res(c, np);
+    k_canonical_probes<<<unsigned(np), 256, 0, c->stream>>>(
+        can->dict[0].p, can->N[0], can->dict[1].p, can->N[1], can->dict[2].p, can->N[2],
+        can->dtc[0].p, can->dtc[1].p, can->dtc[2].p, can->dtw.p, can->T, dp.p, res.p);
+    post_launch(c);
+    CK(cudaMemcpyAsync(out, res.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int latsum_canonical_norm(latsum_ctx* c, const latsum_canonical* can, double* out) {
+  return guarded(c, [&] {
+    require(can && out, "latsum_canonical_norm: null argument");
+    *out = canonical_norm(c, *can);
+  });
+}
+
+int latsum_canonical_eval_box_device(latsum_ctx* c, const latsum_canonical* can,
+                                     const int64_t lo[3], const int64_t hi[3], double* out) {
+  return guarded(c, [&] {
+    require(can && lo && hi && out, "latsum_canonical_eval_box: null argument");
+    canonical_eval(c, *can, lo, hi, out);
+  });
+}
+
+int latsum_rhosvd(latsum_ctx* c, const latsum_canonical* can, const int64_t* ranks,
+                  double tolerance, int deflate, latsum_tucker** out,
+                  latsum_spectral_report* report) {
+  return guarded(c, [&] {
+    require(can && out, "latsum_rhosvd: null argument");
+    auto t = std::make_unique<latsum_tucker>();
+    latsum_spectral_report rep;
+    rhosvd_impl(c, *can, ranks, tolerance, deflate, *t, rep);
+    if (report) *report = rep;
+    *out = t.release();
+  });
+}
+
+void latsum_tucker_destroy(latsum_tucker* t) { delete t; }
+
+int latsum_tucker_info(const latsum_tucker* t, int64_t dims[3], int64_t ranks[3]) {
+  if (!t) return LATSUM_ERR_INVALID_ARGUMENT;
+  for (int l = 0; l < 3; ++l) {
+    if (dims) dims[l] = t->N[l];
+    if (ranks) ranks[l] = t->r[l];
+  }
+  return LATSUM_OK;
+}
+
+int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out) {
+  if (!t || !out || mode < 0 || mode > 2) return LATSUM_ERR_INVALID_ARGUMENT;
+  std::memcpy(out, t->sigma[mode].data(), sizeof(double) * t->sigma[mode].size());
+  return LATSUM_OK;
+}
+
+int latsum_tucker_core(latsum_ctx* c, const latsum_tucker* t, double* core) {
+  return guarded(c, [&] {
+    require(t && core, "latsum_tucker_core: null argument");
+    CK(cudaMemcpyAsync(core, t->core.p, sizeof(double) * t->r[0] * t->r[1] * t->r[2],
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int latsum_tucker_factor(latsum_ctx* c, const latsum_tucker* t, int mode, double* f) {
+  return guarded(c, [&] {
+    require(t && f && mode >= 0 && mode < 3, "latsum_tucker_factor: bad argument");
+    CK(cudaMemcpyAsync(f, t->U[mode].p, sizeof(double) * t->N[mode] * t->r[mode],
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int latsum_tucker_entries(latsum_ctx* c, const latsum_tucker* t, const int64_t* probes, int64_t np,
+                          double* out) {
+  return guarded(c, [&] {
+    require(t && (np == 0 || (probes && out)), "latsum_tucker_entries: bad argument");
+    if (np) tucker_probes(c, *t, probes, np, out);
+  });
+}
+
+int latsum_tucker_eval_box_device(latsum_ctx* c, const latsum_tucker* t, const int64_t lo[3],
+                                  const int64_t hi[3], double* out) {
+  return guarded(c, [&] {
+    require(t && lo && hi && out, "latsum_tucker_eval_box: null argument");
+    tucker_eval(c, *t, lo, hi, out);
+  });
+}
+
+int latsum_tucker_eval_box(latsum_ctx* c, const latsum_tucker* t, const int64_t lo[3],
+                           const int64_t hi[3], double* out) {
+  return guarded(c, [&] {
+    require(t && lo && hi && out, "latsum_tucker_eval_box: null argument");
+    check_box(t->N, lo, hi);
+    const size_t n = size_t(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+    DBuf tmp(c, n);
+    tucker_eval(c, *t, lo, hi, tmp.p);
+    CK(cudaMemcpyAsync(out, tmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int latsum_sum_to_tucker(latsum_ctx* c, int family, double lambda, const int64_t N[3],
+                         const double box[3], int M, double step_constant, int64_t nsub,
+                         const int64_t* sub_counts, const int64_t* sub_shifts,
+                         const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
+                         const double* def_charges, double tolerance, latsum_tucker** out,
+                         latsum_spectral_report* report) {
+  return guarded(c, [&] {
+    require(out, "latsum_sum_to_tucker: null argument");
+    latsum_reference ref;
+    build_reference(c, family, lambda, N, box, M, step_constant, ref);
+    latsum_canonical can;
+    assemble(c, ref, nsub, sub_counts, sub_shifts, sub_charges, ndef, def_shifts, def_charges, can);
+    auto t = std::make_unique<latsum_tucker>();
+    latsum_spectral_report rep;
+    rhosvd_impl(c, can, nullptr, tolerance, LATSUM_DEFLATE_AUTO, *t, rep);
+    if (report) *report = rep;
+    *out = t.release();
+  });
+}
+
+int latsum_dgemm_device(latsum_ctx* c, int ta, int tb, int64_t M, int64_t N, int64_t K,
+                        double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double beta, double* C, int64_t ldc) {
+  return guarded(c, [&] {
+    require(A && B && C && M >= 0 && N >= 0 && K >= 0, "latsum_dgemm_device: bad argument");
+    gemm(c, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  });
+}
+
+}  // extern "C"

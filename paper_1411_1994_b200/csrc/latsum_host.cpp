@@ -1,0 +1,111 @@
+// Host-side rules of the hot path (no GPU): sinc quadrature, the calibrated
+// step-constant sweep and the reference shell.  They are microseconds of scalar
+// work that the reference also runs on the host; keeping
+// them on the host with FMA contraction off (-ffp-contract=off) makes the nodes
+// t_k and weights a_k bit-identical to the reference's libm arithmetic, which
+// the 1e-12 directional parity of stage 1 depends on.
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <vector>
+
+#include "latsum_b200.h"
+
+namespace {
+
+double transform_weight(int family, double lambda, double t) {
+  // quadrature.hpp:251-263: p(z) = int_0^inf w(t) exp(-z^2 t^2) dt
+  const double c = 2.0 / std::sqrt(M_PI);
+  if (family == LATSUM_NEWTON) return c;
+  if (t == 0.0) return 0.0;
+  const double kap = lambda / 2.0;
+  return c * std::exp(-(kap * kap) / (t * t));
+}
+
+double closed_form(int family, double lambda, double r) {
+  // kernel.hpp:154-158
+  return family == LATSUM_NEWTON ? 1.0 / r : std::exp(-lambda * r) / r;
+}
+
+void sinc_rule(int family, double lambda, int M, double c0, double A, double* t, double* a) {
+  // quadrature.hpp:326-341: u_k = (k - M) h_M, t_k = sinh(u_k)/A,
+  // a_k = (h_M/2) w(|t_k|) cosh(u_k)/A, h_M = C0 log(M)/M
+  const double hM = c0 * std::log(double(M)) / double(M);
+  for (int k = 0; k < 2 * M + 1; ++k) {
+    const double u = (double(k) - double(M)) * hM;
+    const double tk = std::sinh(u) / A;
+    t[k] = tk;
+    a[k] = 0.5 * hM * transform_weight(family, lambda, std::abs(tk)) * std::cosh(u) / A;
+  }
+}
+
+double max_pointwise_rel(int family, double lambda, const double* t, const double* a, int R,
+                         double lo, double hi, int npts) {
+  // quadrature.hpp:396-412 (shell_error) with separable_eval (:370-379) at (z,0,0)
+  const double la = std::log(lo), lA = std::log(hi);
+  double worst = 0.0;
+  for (int i = 0; i < npts; ++i) {
+    const double z = std::exp(la + (lA - la) * double(i) / double(npts - 1));
+    const double x[3] = {z, 0.0, 0.0};
+    double sum = 0.0;
+    for (int k = 0; k < R; ++k) {
+      const double s = t[k] * t[k];
+      double prod = a[k];
+      for (int l = 0; l < 3; ++l) prod *= std::exp(-s * x[l] * x[l]);
+      sum += prod;
+    }
+    const double exact = closed_form(family, lambda, z);
+    worst = std::fmax(worst, std::abs(1.0 * sum - exact) / std::abs(exact));
+  }
+  return worst;
+}
+
+}  // namespace
+
+extern "C" {
+
+int latsum_build_quadrature(int family, double lambda, int M, double step_constant,
+                            double shell_a, double shell_A, double* nodes, double* weights) {
+  if (family != LATSUM_NEWTON && family != LATSUM_YUKAWA) return LATSUM_ERR_NOT_IMPLEMENTED;
+  if (M < 2 || !(shell_a > 0.0) || !(shell_A > shell_a) || !(step_constant > 0.0))
+    return LATSUM_ERR_INVALID_ARGUMENT;
+  if (family == LATSUM_YUKAWA && !(lambda > 0.0)) return LATSUM_ERR_INVALID_ARGUMENT;
+  sinc_rule(family, lambda, M, step_constant, shell_A, nodes, weights);
+  return LATSUM_OK;
+}
+
+double latsum_default_step_constant(int family, double lambda, int M, double shell_a,
+                                    double shell_A, int npts) {
+  // quadrature.hpp:416-447: 53 candidates base*(0.5 + 1.3 i/52),
+  // base = asinh(2.5 A/a)/log M; first strict minimum of the finite errors.
+  if (npts <= 1) npts = 320;
+  const double base = std::asinh(2.5 * (shell_A / shell_a)) / std::log(double(M));
+  std::vector<double> t(2 * M + 1), a(2 * M + 1);
+  double best = std::numeric_limits<double>::infinity();
+  double best_c0 = base * 0.5;
+  for (int i = 0; i < 53; ++i) {
+    const double c0 = base * (0.5 + 1.3 * double(i) / 52.0);
+    sinc_rule(family, lambda, M, c0, shell_A, t.data(), a.data());
+    const double e =
+        max_pointwise_rel(family, lambda, t.data(), a.data(), 2 * M + 1, shell_a, shell_A, npts);
+    if (std::isfinite(e) && e < best) {
+      best = e;
+      best_c0 = c0;
+    }
+  }
+  return best_c0;
+}
+
+void latsum_reference_shell(const int64_t N[3], const double box[3], double shell[2]) {
+  // reference.hpp:84-93 on the doubled grid: mesh h_l = 2b_l / 2N_l, width 2b_l
+  double hmin = (2.0 * box[0]) / double(2 * N[0]);
+  double bmax = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    hmin = std::fmin(hmin, (2.0 * box[l]) / double(2 * N[l]));
+    bmax = std::fmax(bmax, 2.0 * box[l]);
+  }
+  shell[0] = hmin;
+  shell[1] = std::sqrt(3.0) * bmax / 2.0;
+}
+
+}  // extern "C"

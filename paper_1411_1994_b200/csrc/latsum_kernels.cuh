@@ -1,0 +1,324 @@
+// Stage kernels of the lattice-sum hot path (sm_100a, FP64).
+//
+// Layouts: every matrix is column-major with the
+// grid index fastest, as Eigen stores the reference's side matrices.
+//   ref_l   : 2N_l x Rd    distinct reference columns (t_{-k} = -t_k share one)
+//   dict_l  : N_l  x d_l   distinct side-matrix columns, d_l = P_l * Rd, column
+//                          c = p * Rd + j holds placement p (a sublattice shift list
+//                          or one defect shift) of reference column j
+//   terms   : T merged canonical terms (c0, c1, c2, w) sorted by c0
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace latsum_b200 {
+
+// ---------------------------------------------------------------- helpers
+
+// Deterministic block sum (fixed tree); blockDim.x must be a power of two <= 1024.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x / 32;
+  if (warp == 0) {
+    v = lane < nw ? red[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// erf(hi) - erf(lo) routed through erfc on the same-sign side (reference.hpp:21-25).
+__device__ __forceinline__ double erf_difference(double lo, double hi) {
+  if (lo >= 0.0) return erfc(lo) - erfc(hi);
+  if (hi <= 0.0) return erfc(-hi) - erfc(-lo);
+  return erf(hi) - erf(lo);
+}
+
+// ---------------------------------------------------------------- stage 1
+
+// entry(i, k) = int over cell i of exp(-s_k x^2) dx (reference.hpp:33-54), one thread
+// per (cell, distinct term).  Cell bounds lo = lower + i h, hi = lo + h are formed
+// without FMA contraction exactly as the host does; the cell integral is the
+// cancellation-free hybrid (4-point Gauss-Legendre when sqrt(s) h < 0.05, the
+// reference's erf difference otherwise).
+__global__ void k_ref_integrals(const double* __restrict__ s, int64_t n2, double lower, double h,
+                                double* __restrict__ out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int k = blockIdx.y;
+  if (i >= n2) return;
+  const double sk = s[k];
+  double v;
+  if (sk == 0.0) {
+    v = h;
+  } else {
+    const double rs = sqrt(sk);
+    const double lo = __dadd_rn(lower, __dmul_rn(double(i), h));
+    if (__dmul_rn(rs, h) < 0.05) {
+      const double xg[4] = {-0.86113631159405257522, -0.33998104358485626480,
+                            0.33998104358485626480, 0.86113631159405257522};
+      const double wg[4] = {0.34785484513745385737, 0.65214515486254614263,
+                            0.65214515486254614263, 0.34785484513745385737};
+      const double half = __dmul_rn(0.5, h);
+      const double mid = __dadd_rn(lo, half);
+      double acc = 0.0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const double x = __dadd_rn(mid, __dmul_rn(half, xg[g]));
+        acc = __dadd_rn(acc, __dmul_rn(wg[g], exp(__dmul_rn(__dmul_rn(-sk, x), x))));
+      }
+      v = __dmul_rn(half, acc);
+    } else {
+      const double hi = __dadd_rn(lo, h);
+      const double c = sqrt(M_PI) / (2.0 * rs);
+      v = __dmul_rn(c, erf_difference(__dmul_rn(rs, lo), __dmul_rn(rs, hi)));
+    }
+  }
+  out[i + k * n2] = v;
+}
+
+// from_raw for one mode (canonical.hpp:32-48): one block per column, ordered
+// reduction of the squares, then col /= norm (zero column -> e_0).
+__global__ void k_normalize_columns(double* __restrict__ m, int64_t rows, double* __restrict__ norms) {
+  __shared__ double red[32];
+  double* c = m + int64_t(blockIdx.x) * rows;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) s += c[i] * c[i];
+  const double nrm = sqrt(block_sum(s, red));
+  if (threadIdx.x == 0) norms[blockIdx.x] = nrm;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
+    c[i] = nrm == 0.0 ? (i == 0 ? 1.0 : c[i]) : c[i] / nrm;
+}
+
+// ---------------------------------------------------------------- stage 2
+
+// Value of dictionary column c at row i: sum over the placement's shifts of
+// ref_j[N/2 - shift + i] (assembled_vector, lattice_sum.hpp:101-144; ascending
+// order of the shift list).
+struct DictArgs {
+  const double* ref;       // 2N x Rd
+  int64_t N;
+  int Rd;
+  const int64_t* pl_off;   // P+1
+  const int64_t* pl_shift; // shifts
+  double* dict;            // N x d
+  double* partial;         // d x nchunk
+  double* norms;           // d
+  int64_t chunk;
+  int nchunk;
+};
+
+__device__ __forceinline__ double dict_value(const DictArgs& a, const double* rj, int64_t s0,
+                                             int64_t s1, int64_t i) {
+  double v = 0.0;
+  for (int64_t s = s0; s < s1; ++s) v += rj[a.N / 2 - a.pl_shift[s] + i];
+  return v;
+}
+
+__global__ void k_dict_sumsq(DictArgs a) {
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x;
+  const int64_t p = c / a.Rd, j = c % a.Rd;
+  const double* rj = a.ref + j * 2 * a.N;
+  const int64_t s0 = a.pl_off[p], s1 = a.pl_off[p + 1];
+  const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
+  double s = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double v = dict_value(a, rj, s0, s1, i);
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) a.partial[c * a.nchunk + blockIdx.y] = s;
+}
+
+__global__ void k_dict_norms(DictArgs a, int64_t d) {
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= d) return;
+  double s = 0.0;
+  for (int q = 0; q < a.nchunk; ++q) s += a.partial[c * a.nchunk + q];
+  a.norms[c] = sqrt(s);
+}
+
+__global__ void k_dict_write(DictArgs a) {
+  const int64_t c = blockIdx.x;
+  const int64_t p = c / a.Rd, j = c % a.Rd;
+  const double* rj = a.ref + j * 2 * a.N;
+  const int64_t s0 = a.pl_off[p], s1 = a.pl_off[p + 1];
+  const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
+  const double nrm = a.norms[c];
+  double* out = a.dict + c * a.N;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double v = dict_value(a, rj, s0, s1, i);
+    out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v / nrm;
+  }
+}
+
+// out[:, q] = dict[:, idx[q]] — the reference-form N x M_c side matrix (HBM-bound
+// gather with 128-bit accesses when rows are even).
+__global__ void k_gather_columns(const double* __restrict__ dict, int64_t rows,
+                                 const int64_t* __restrict__ idx, double* __restrict__ out) {
+  const int64_t q = blockIdx.y;
+  const double* src = dict + idx[q] * rows;
+  double* dst = out + q * rows;
+  if ((rows & 1) == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows / 2;
+         i += int64_t(gridDim.x) * blockDim.x)
+      d2[i] = s2[i];
+  } else {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows;
+         i += int64_t(gridDim.x) * blockDim.x)
+      dst[i] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------- stage 3 helpers
+
+// out[:, c] = in[:, c] * scale[c]   (optionally in place)
+__global__ void k_scale_columns(const double* __restrict__ in, int64_t rows, int64_t cols,
+                                const double* __restrict__ scale, double* __restrict__ out) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x)
+    out[e] = in[e] * scale[e / rows];
+}
+
+// out[:, q] = src[:, cols[q]] * (w ? w[q] : 1)   (rows x T gather, for the core)
+__global__ void k_gather_scale(const double* __restrict__ src, int64_t rows,
+                               const int32_t* __restrict__ cols, const double* __restrict__ w,
+                               int64_t T, double* __restrict__ out) {
+  const int64_t total = rows * T;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = e / rows, i = e % rows;
+    const double v = src[i + int64_t(cols[q]) * rows];
+    out[e] = w ? v * w[q] : v;
+  }
+}
+
+// dst[:, j] = src[:, n - 1 - j] for j < k   (ascending eigenvectors -> descending)
+__global__ void k_reverse_columns(const double* __restrict__ src, int64_t rows, int64_t n,
+                                  int64_t k, double* __restrict__ dst) {
+  const int64_t total = rows * k;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / rows, i = e % rows;
+    dst[e] = src[i + (n - 1 - j) * rows];
+  }
+}
+
+// dst[:, j] = src[:, sel[j]]
+__global__ void k_select_columns(const double* __restrict__ src, int64_t rows,
+                                 const int64_t* __restrict__ sel, int64_t k,
+                                 double* __restrict__ dst) {
+  const int64_t total = rows * k;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / rows, i = e % rows;
+    dst[e] = src[i + sel[j] * rows];
+  }
+}
+
+// ||A||^2 = sum_{t,t'} w_t w_t' prod_l G_l[c_l(t), c_l(t')] (canonical.hpp:148-162 with the
+// three M x M Grams replaced by d_l x d_l dictionary Grams).  One thread per row t;
+// partial[t] = w_t * sum_t' (...) in a fixed order.
+__global__ void k_hadamard_norm_rows(const double* __restrict__ G0, const double* __restrict__ G1,
+                                     const double* __restrict__ G2, int64_t d0, int64_t d1,
+                                     int64_t d2, const int32_t* __restrict__ c0,
+                                     const int32_t* __restrict__ c1,
+                                     const int32_t* __restrict__ c2, const double* __restrict__ w,
+                                     int64_t T, double* __restrict__ partial) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= T) return;
+  const double* g0 = G0 + int64_t(c0[t]) * d0;
+  const double* g1 = G1 + int64_t(c1[t]) * d1;
+  const double* g2 = G2 + int64_t(c2[t]) * d2;
+  double s = 0.0;
+  for (int64_t u = 0; u < T; ++u) s += w[u] * (g0[c0[u]] * g1[c1[u]] * g2[c2[u]]);
+  partial[t] = w[t] * s;
+}
+
+// Ordered sum of n values by one block (deterministic).
+__global__ void k_sum(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ---------------------------------------------------------------- stage 4 helpers
+
+// X[t + T*(j + nj*kk)] = w_t * D2[k0+kk, c2_t] * D1[j0+j, c1_t] : the canonical slab
+// operand (canonical.hpp:192-202 to_dense as one GEMM per z-slab).
+__global__ void k_canonical_slab_operand(const double* __restrict__ D1, int64_t N1,
+                                         const double* __restrict__ D2, int64_t N2,
+                                         const int32_t* __restrict__ c1,
+                                         const int32_t* __restrict__ c2,
+                                         const double* __restrict__ w, int64_t T, int64_t j0,
+                                         int64_t nj, int64_t k0, int64_t nk,
+                                         double* __restrict__ X) {
+  const int64_t total = T * nj * nk;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = e % T, j = (e / T) % nj, kk = e / (T * nj);
+    X[e] = w[t] * D2[(k0 + kk) + int64_t(c2[t]) * N2] * D1[(j0 + j) + int64_t(c1[t]) * N1];
+  }
+}
+
+// Tucker entries at probes: out[p] = sum_{b,c} W[p + np*(b + r1*c)] U1[j_p, b] U2[k_p, c]
+// with W = U0[i_p, :] * core_(1) precomputed by a GEMM.
+__global__ void k_tucker_probe_finish(const double* __restrict__ W, int64_t np, int64_t r1,
+                                      int64_t r2, const double* __restrict__ U1, int64_t N1,
+                                      const double* __restrict__ U2, int64_t N2,
+                                      const int64_t* __restrict__ probes,
+                                      double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t p = blockIdx.x;
+  const int64_t j = probes[3 * p + 1], k = probes[3 * p + 2];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < r1 * r2; e += blockDim.x) {
+    const int64_t b = e % r1, c = e / r1;
+    s += W[p + np * e] * U1[j + b * N1] * U2[k + c * N2];
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[p] = s;
+}
+
+// Canonical entries at probes (canonical.hpp:63-70) over merged terms.
+__global__ void k_canonical_probes(const double* __restrict__ D0, int64_t N0,
+                                   const double* __restrict__ D1, int64_t N1,
+                                   const double* __restrict__ D2, int64_t N2,
+                                   const int32_t* __restrict__ c0, const int32_t* __restrict__ c1,
+                                   const int32_t* __restrict__ c2, const double* __restrict__ w,
+                                   int64_t T, const int64_t* __restrict__ probes,
+                                   double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t p = blockIdx.x;
+  const int64_t i = probes[3 * p], j = probes[3 * p + 1], k = probes[3 * p + 2];
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x)
+    s += w[t] * D0[i + int64_t(c0[t]) * N0] * D1[j + int64_t(c1[t]) * N1] *
+         D2[k + int64_t(c2[t]) * N2];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[p] = s;
+}
+
+// rows gather: out[p + np*a] = U[idx_p + N*a]
+__global__ void k_gather_rows(const double* __restrict__ U, int64_t N, int64_t r,
+                              const int64_t* __restrict__ probes, int comp, int64_t np,
+                              double* __restrict__ out) {
+  const int64_t total = np * r;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = e % np, a = e / np;
+    out[e] = U[probes[3 * p + comp] + N * a];
+  }
+}
+
+}  // namespace latsum_b200

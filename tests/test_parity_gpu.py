@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE north star):
+* directional vectors (unit side-matrix columns, stages 1-2): 1e-12 relative L-inf
+  per column;
+* truncated Tucker ranks: identical to the oracle's SVD ranks (a +-1 difference
+  only at a flagged tie);
+* reconstructed potentials: within 10*eps + 1e-12, normalised by max|oracle| over
+  the probe set (commands.cpp:257-266), compared after reconstruction (sign freedom).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1411_1994_b200 import api
+from paper_1411_1994_b200 import workload as W
+from latsum_helpers import col_rel_linf, mini
+
+pytestmark = pytest.mark.gpu
+
+DIR_TOL = 1e-12
+
+
+def _ref_pair(ctx, g):
+    ref = api.reference_for(g, ctx)
+    oref = O.reference(g)
+    return ref, oref
+
+
+# ----------------------------------------------------------------------------- stage 1
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_stage1_reference_columns_match_oracle(ctx, cfg):
+    g = W.baseline(cfg)
+    ref, oref = _ref_pair(ctx, g)
+    assert ref.rank == g.R == oref.weights.size
+    assert ref.step_constant == oref.C0  # host sweep bit-identical
+    t, a = ref.quadrature()
+    assert np.array_equal(t, oref.nodes) and np.array_equal(a, oref.quad_weights)
+    f = ref.factor(0)
+    assert f.shape == (2 * g.N[0], g.R)
+    assert col_rel_linf(f, oref.factors[0]) < DIR_TOL
+    np.testing.assert_allclose(ref.weights, oref.weights, rtol=1e-13, atol=0)
+    # identical modes share columns bitwise (test_reference.cpp:49-60)
+    assert np.array_equal(ref.factor(2), f)
+
+
+def test_stage1_zero_node_and_mirror(ctx):
+    g = W.lattice_box(8, 2.0, [dict(cells=(2, 2, 2), step=(0.5, 0.5, 0.5))], M=6)
+    ref = api.reference_for(g, ctx)
+    f = ref.factor(0)
+    n2 = f.shape[0]
+    # t=0 column is constant before normalisation -> unit column 1/sqrt(2N)
+    np.testing.assert_allclose(f[:, g.M], 1.0 / np.sqrt(n2), rtol=1e-14)
+    np.testing.assert_allclose(f, f[::-1, :], rtol=1e-14, atol=0)  # mirror symmetry
+
+
+# ----------------------------------------------------------------------------- stage 2
+
+@pytest.mark.parametrize("kind", ["cubic", "vacancies", "yukawa", "hex", "mixed"])
+def test_stage2_side_matrices_match_oracle(ctx, kind):
+    g = mini(kind)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    assert can.rank == g.canonical_rank
+    for l in range(3):
+        assert col_rel_linf(can.factor(l), F[l]) < DIR_TOL
+    np.testing.assert_allclose(can.weights, w, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_stage2_full_config_side_matrices(ctx, cfg):
+    g = W.baseline(cfg)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    for l in range(3):
+        assert col_rel_linf(can.factor(l), F[l]) < DIR_TOL
+    np.testing.assert_allclose(can.weights, w, rtol=1e-12, atol=0)
+
+
+def test_stage2_assembled_equals_brute_force_oracle(ctx):
+    g = mini("vacancies")
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    pr = O.probes(g.N, 300, 3)
+    got = can.entries(pr)
+    want = O.oracle_entries(oref, g, pr)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
+def test_stage2_vacancy_is_base_minus_window(ctx):
+    base = W.from_lattice((4, 4, 4), 16, M=8)
+    vac = W.from_lattice((4, 4, 4), 16, M=8, defects=[([(0, 0, 0)], -1.0, None)])
+    ref = api.reference_for(base, ctx)
+    cb, cv = api.lattice_sum(ref, base), api.lattice_sum(ref, vac)
+    assert cv.rank == 2 * ref.rank
+    single = W.from_lattice((4, 4, 4), 16, M=8)
+    single.sublattices = []
+    single.defect_shifts = np.zeros((1, 3), np.int64)
+    single.defect_charges = np.array([1.0])
+    cw = api.lattice_sum(ref, single)
+    pr = O.probes(base.N, 200, 5)
+    lhs = cv.entries(pr)
+    rhs = cb.entries(pr) - cw.entries(pr)
+    assert np.max(np.abs(lhs - rhs)) / np.max(np.abs(lhs)) < 1e-12
+
+
+def test_stage2_window_overflow_names_mode(ctx):
+    g = W.from_lattice((4, 4, 4), 8, M=4)
+    g.defect_shifts = np.array([[0, 40, 0]], np.int64)
+    g.defect_charges = np.array([1.0])
+    ref = api.reference_for(g, ctx)
+    with pytest.raises(api.WindowOverflowError) as e:
+        api.lattice_sum(ref, g)
+    assert e.value.mode == 2
+
+
+def test_stage2_empty_defects_is_identity(ctx):
+    g = W.from_lattice((2, 2, 1), 8, M=6)
+    ref = api.reference_for(g, ctx)
+    a = api.lattice_sum(ref, g)
+    b = api.lattice_sum(ref, W.from_lattice((2, 2, 1), 8, M=6, defects=[]))
+    for l in range(3):
+        assert np.array_equal(a.factor(l), b.factor(l))
+
+
+# ----------------------------------------------------------------------------- stage 3
+
+def _check_rhosvd(ctx, g, deflate="auto", probes=400):
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    orc = O.rhosvd(F, w, eps=g.eps)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), deflate=deflate)
+    for l in range(3):
+        if rep.chosen_ranks[l] != orc.ranks[l]:
+            assert orc.tie[l] or rep.tie_at_cutoff[l], (l, rep.chosen_ranks, orc.ranks)
+            assert abs(rep.chosen_ranks[l] - orc.ranks[l]) <= 1
+    assert t.ranks == rep.chosen_ranks
+    # singular values relative to sigma_1 where resolved
+    for l in range(3):
+        s_gpu, s_orc = rep.singular_values[l], orc.sigma[l]
+        assert s_gpu.size == s_orc.size
+        assert np.max(np.abs(s_gpu - s_orc)) / s_orc[0] < 1e-10
+    pr = O.probes(g.N, probes, 11)
+    v_gpu = t.entries(pr)
+    v_orc = O.projected_cp_entries(w, orc.Z, orc.P, pr)
+    v_can = O.canonical_entries(F, w, pr)
+    scale = np.max(np.abs(v_orc))
+    assert np.max(np.abs(v_gpu - v_orc)) / scale <= 10 * g.eps + 1e-12
+    assert np.max(np.abs(v_gpu - v_can)) / np.max(np.abs(v_can)) <= 10 * g.eps + 1e-12
+    np.testing.assert_allclose(rep.weight_norm, orc.weight_norm, rtol=1e-12)
+    np.testing.assert_allclose(rep.input_norm, orc.input_norm, rtol=1e-9)
+    np.testing.assert_allclose(rep.bound_abs, orc.bound_abs, rtol=1e-3)
+    return t, rep, orc
+
+
+@pytest.mark.parametrize("kind", ["vacancies", "yukawa", "hex", "mixed"])
+def test_stage3_rhosvd_ranks_and_values(ctx, kind):
+    _check_rhosvd(ctx, mini(kind))
+
+
+def test_stage3_single_pass_vs_deflated(ctx):
+    g = mini("mixed")
+    t1, r1, orc = _check_rhosvd(ctx, g, deflate="always")
+    assert all(r1.deflated)
+
+
+def test_stage3_fixed_ranks_exact_low_rank(ctx):
+    g = W.from_lattice((2, 2, 2), 8, M=3)  # canonical rank 7, merged 4 distinct terms
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t, rep = api.rhosvd(can, api.TruncationSpec.fixed_ranks(10, 10, 10))
+    assert all(r <= 7 for r in rep.chosen_ranks)
+    dense_t = t.to_dense()
+    dense_c = can.to_dense()
+    assert np.linalg.norm(dense_t - dense_c) / np.linalg.norm(dense_c) < 1e-12
+
+
+def test_stage3_zero_tensor(ctx):
+    g = W.from_lattice((2, 2, 2), 8, M=3)
+    g.sublattices[0].charge = 0.0
+    ref = api.reference_for(g, ctx)
+    t, rep = api.rhosvd(api.lattice_sum(ref, g), api.TruncationSpec.fixed_ranks(2, 2, 2))
+    assert rep.input_norm == 0.0 and rep.chosen_ranks == (1, 1, 1)
+    assert np.all(t.to_dense() == 0.0)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_stage3_full_config(ctx, cfg):
+    _check_rhosvd(ctx, W.baseline(cfg), probes=300)
+
+
+# ----------------------------------------------------------------------------- stage 4
+
+def test_stage4_tucker_box_matches_entries(ctx):
+    g = mini("hex")
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    lo, hi = (10, 20, 30), (90, 77, 130)
+    box = t.to_dense(lo, hi)
+    core = t.core
+    U = [t.factor(l) for l in range(3)]
+    rng = np.random.default_rng(1)
+    pr = np.stack([rng.integers(lo[l], hi[l], 200) for l in range(3)], axis=1)
+    want = O.tucker_entries(core, U, pr)
+    got = box[pr[:, 0] - lo[0], pr[:, 1] - lo[1], pr[:, 2] - lo[2]]
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+    np.testing.assert_allclose(t.entries(pr), want, rtol=0, atol=1e-12 * np.max(np.abs(want)))
+
+
+def test_stage4_canonical_box_matches_oracle(ctx):
+    g = W.baseline(1)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    plane = can.to_dense((0, 0, 256), (512, 512, 257))[:, :, 0]
+    ii, jj = np.meshgrid(np.arange(0, 512, 7), np.arange(0, 512, 5), indexing="ij")
+    pr = np.stack([ii.ravel(), jj.ravel(), np.full(ii.size, 256)], axis=1)
+    want = O.canonical_entries(F, w, pr)
+    got = plane[pr[:, 0], pr[:, 1]]
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+    # axis lines against the brute-force windowed-sum oracle (lattice_sum.hpp:656-671)
+    lines = []
+    for l in range(3):
+        p = np.full((512, 3), 256, np.int64)
+        p[:, l] = np.arange(512)
+        lines.append(p)
+    pr = np.concatenate(lines)
+    brute = O.oracle_entries(oref, g, pr)
+    got = can.entries(pr)
+    assert np.max(np.abs(got - brute)) / np.max(np.abs(brute)) < 1e-12
+
+
+# ----------------------------------------------------------------------------- GEMM
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (37, 129, 17), (300, 260, 513), (64, 2000, 3000)])
+def test_dgemm_dmma_matches_fp64_reference(ctx, ta, tb, shape):
+    import torch
+    M, N, K = shape
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, generator=g)
+    B = torch.randn((N, K) if tb else (K, N), dtype=torch.float64, generator=g)
+    C = torch.randn((M, N), dtype=torch.float64, generator=g)
+    want = 1.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C
+    dA = A.T.contiguous().cuda()  # column-major storage == row-major transpose
+    dB = B.T.contiguous().cuda()
+    dC = C.T.contiguous().cuda()
+    from paper_1411_1994_b200 import _lib
+    lda = A.shape[0]
+    ldb = B.shape[0]
+    ctx.check(_lib.lib().latsum_dgemm_device(ctx.handle, ta, tb, M, N, K, 1.5, dA.data_ptr(), lda,
+                                             dB.data_ptr(), ldb, -0.5, dC.data_ptr(), M))
+    ctx.synchronize()
+    got = dC.cpu().T
+    err = (got - want).abs().max().item() / max(1.0, want.abs().max().item())
+    assert err < 1e-13 * max(1, K) ** 0.5 * 10

@@ -1,0 +1,97 @@
+// Microbenchmark: FP64 DMMA (mma.sync f64) and DFMA peak on sm_100a.
+// Used once to fix the FP64 roofline denominator; not product code.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int SHAPE>
+__global__ void dmma_loop(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double b0 = 0.5, b1 = 0.25, b2 = 0.125, b3 = 0.0625;
+  double c[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[i][j] = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (SHAPE == 0) {  // m8n8k4: 2 f64 acc per thread
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a0), "d"(b0));
+      } else if (SHAPE == 1) {  // m16n8k4
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0), "d"(a1), "d"(b0));
+      } else if (SHAPE == 2) {  // m16n8k8
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+      } else {  // m16n8k16
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                     : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1), "d"(b2), "d"(b3));
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += c[i][j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void dfma_loop(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  const double a = 0.999999, b = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+  double* out;
+  cudaMalloc(&out, 148 * 64 * 1024 * sizeof(double));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const char* names[4] = {"m8n8k4", "m16n8k4", "m16n8k8", "m16n8k16"};
+  const double flops_per_mma[4] = {2.0 * 8 * 8 * 4, 2.0 * 16 * 8 * 4, 2.0 * 16 * 8 * 8, 2.0 * 16 * 8 * 16};
+  for (int shape = 0; shape < 4; ++shape) {
+    for (int warps : {4, 8, 16}) {
+      int blocks = 148 * 4, threads = 32 * warps, iters = 2000;
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        if (shape == 0) dmma_loop<0><<<blocks, threads>>>(out, iters);
+        if (shape == 1) dmma_loop<1><<<blocks, threads>>>(out, iters);
+        if (shape == 2) dmma_loop<2><<<blocks, threads>>>(out, iters);
+        if (shape == 3) dmma_loop<3><<<blocks, threads>>>(out, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+      }
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double fl = flops_per_mma[shape] * 8.0 * iters * (double)blocks * warps;
+      printf("DMMA %-9s warps/blk %2d: %.2f TFLOP/s (%.3f ms)\n", names[shape], warps, fl / ms / 1e9, ms);
+    }
+  }
+  for (int warps : {8, 16, 32}) {
+    int blocks = 148 * 4, threads = 32 * warps, iters = 4000;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      dfma_loop<<<blocks, threads>>>(out, iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+    }
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double fl = 2.0 * 8 * iters * (double)blocks * threads;
+    printf("DFMA warps/blk %2d: %.2f TFLOP/s\n", warps, fl / ms / 1e9);
+  }
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py — lattice-sum + RHOSVD + grid evaluation on B200.
+
+Workload (BASELINE.json configs[1], "cfg2"): Newton kernel, cubic L=32 lattice
+(32,768 sites, spacing 1) in [-24,24]^3, N=2048, M=20 (R=41), 3% seeded vacancies
+(983), RHOSVD at eps=1e-6, then the Tucker result evaluated on the full 2048^3 grid.
+
+One step = stage 1 (reference tensor) + stage 2 (assembled sum + defects) +
+stage 3 (RHOSVD: Grams, syevd, deflated pass, projections, core) + stage 4 (grid
+evaluation into a 68.7 GB device buffer).  `value` is BASELINE's headline metric,
+"lattice-sum+RHOSVD wall ms" = device time of stages 1-3 per step (mean over K);
+`grid_eval` carries the stage-4 throughput in Gpts/s; `ms_per_step` covers 1-4.
+`e2e` is the same metric through the C ABI with host buffers (latsum_sum_to_tucker
++ device->host copy of the Tucker core and factors), copies inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config C]
+
+N > 1 (torchrun, one process per GPU, NCCL): stages 1-3 run on every rank (the
+result is replicated; the Gram of cfg2 is 0.7k x 0.7k), the grid evaluation is
+split into z-slabs across ranks with no communication, times are max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lattice-sum+RHOSVD wall ms"
+FP64_PEAK_TFLOPS = 37.0  # DMMA microbenchmark on this pool (tools/fp64_peak.cu, profiles/)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu mma.sync f64 loop (profiles/fp64_peak_r01.txt)"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+def cpu_reference_step(g, core_terms: int, eval_slices: int, threads: int):
+    """One bounded sample of the reference's CPU path on the host (oracle port; the
+    reference itself cannot be built here — DESIGN.md).  Returns extrapolated ms for
+    stages 1-3 and the CPU grid-evaluation rate, plus what was measured."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    ref = O.reference(g)
+    t1 = time.perf_counter()
+    F, w = O.side_matrices(ref, g)
+    t2 = time.perf_counter()
+    # stage 3 as the reference runs it: BDCSVD of the full N x M_c side matrix (thin U),
+    # one mode measured, three modes charged
+    u, s, _ = np.linalg.svd(F[0], full_matrices=False)
+    t3 = time.perf_counter()
+    orc = O.rhosvd(F, w, eps=g.eps, with_norm=False)  # ranks/bases via merged SVD (not timed)
+    r = orc.ranks
+    # project_core in the reference loop order on `core_terms` terms, scaled to M_c
+    Ps = [np.asfortranarray(p[:, :core_terms]) for p in orc.P]
+    t4 = time.perf_counter()
+    O.project_core(w[:core_terms], Ps)
+    t5 = time.perf_counter()
+    Mc = w.size
+    ms_core = 1e3 * (t5 - t4) * Mc / core_terms
+    ms_p = 0.0
+    t6 = time.perf_counter()
+    for l in range(3):  # P_l = Z_l^T A_l (dense GEMM)
+        orc.Z[l].T @ F[l]
+    ms_p = 1e3 * (time.perf_counter() - t6)
+    ms = 1e3 * (t1 - t0) + 1e3 * (t2 - t1) + 3 * 1e3 * (t3 - t2) + ms_p + ms_core
+    # grid evaluation (to_dense TTM chain) on `eval_slices` z-slices of the box
+    lo, hi = g.eval_box()
+    core = np.random.default_rng(0).standard_normal(r)
+    U = [np.asfortranarray(orc.Z[l][lo[l]:hi[l]]) for l in range(3)]
+    t7 = time.perf_counter()
+    Y = np.tensordot(core, U[2][:eval_slices], axes=([2], [1]))  # r0 r1 k
+    Y = np.tensordot(Y, U[1], axes=([1], [1]))                   # r0 k j
+    V = np.tensordot(U[0], Y, axes=([1], [0]))                    # i k j
+    t8 = time.perf_counter()
+    pts = V.size
+    return dict(ms=ms, eval_gpts=pts / (t8 - t7) / 1e9,
+                parts=dict(stage1_ms=1e3 * (t1 - t0), stage2_ms=1e3 * (t2 - t1),
+                           svd_one_mode_ms=1e3 * (t3 - t2), project_ms=ms_p,
+                           core_sample_ms=1e3 * (t5 - t4), core_extrapolated_ms=ms_core),
+                sample=(f"{g.name}: stages 1-2 full; full N x M_c SVD of mode 1 timed, x3; "
+                        f"project_core loop on {core_terms} of {Mc} terms scaled x{Mc / core_terms:.1f}; "
+                        f"grid eval TTM chain on {eval_slices} z-slices"))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1411_1994_b200 import workload as W
+    g = W.baseline(args.config)
+    threads = os.cpu_count() or 1
+    samples = []
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference_step(g, args.core_terms, args.eval_slices, threads)
+        if i >= args.warmup:
+            samples.append(res)
+    ms = statistics.mean(s["ms"] for s in samples)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded geometry; no dataset involved)",
+        "config": {"workload": f"cfg{args.config} ({g.name}): N={g.N[0]}, M={g.M}, "
+                               f"sites={g.n_sites}, defects={g.n_defects}, eps={g.eps}"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "port",
+                         "sample": samples[0]["sample"], "parts": samples[-1]["parts"],
+                         "grid_eval_gpts_s": samples[-1]["eval_gpts"]},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1411_1994_b200 import api
+    from paper_1411_1994_b200 import workload as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    g = W.baseline(args.config)
+    ctx = api.Context(local)
+    # a dedicated (non-NULL) stream shared by torch and the library, so the CUDA events
+    # below order against every kernel the library launches
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    lo, hi = g.eval_box()
+    nz = hi[2] - lo[2]
+    z0 = lo[2] + (nz * rank) // world
+    z1 = lo[2] + (nz * (rank + 1)) // world
+    my_lo, my_hi = (lo[0], lo[1], z0), (hi[0], hi[1], z1)
+    n_my = (my_hi[0] - my_lo[0]) * (my_hi[1] - my_lo[1]) * (my_hi[2] - my_lo[2])
+    n_total = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
+    do_eval = not args.no_eval
+    out = torch.empty(n_my if do_eval else 1, dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    def step():
+        ref = api.reference_for(g, ctx)
+        can = api.lattice_sum(ref, g)
+        t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+        return ref, can, t, rep
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ms13, ms4 = [], []
+    launches0 = None
+    clocks = ClockSampler(local)
+    last = None
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier()
+        if i == args.warmup:
+            clocks.start()
+            launches0 = ctx.kernel_launches
+        ev[0].record(stream)
+        ref, can, t, rep = step()
+        ev[1].record(stream)
+        if do_eval:
+            t.eval_box_device(my_lo, my_hi, out.data_ptr())
+        ev[2].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        if i >= args.warmup:
+            ms13.append(ev[0].elapsed_time(ev[1]))
+            ms4.append(ev[1].elapsed_time(ev[2]))
+        last = (t, rep, can)
+    clk = clocks.stop()
+    launches = ctx.kernel_launches - launches0
+    t, rep, can = last
+    v13 = max_over_ranks(statistics.mean(ms13))
+    v4 = max_over_ranks(statistics.mean(ms4)) if do_eval else 0.0
+    total = max_over_ranks(statistics.mean([a + b for a, b in zip(ms13, ms4)]))
+
+    # per-kernel-class profile of one extra (untimed) step: roofline of the dominant kernel
+    ctx.set_profiling(True)
+    torch.cuda.synchronize(dev)
+    ref2, can2, t2, rep2 = step()
+    if do_eval:
+        t2.eval_box_device(my_lo, my_hi, out.data_ptr())
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    gemm_tags = {k: v for k, v in prof.items() if k.startswith("gemm")}
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    dom_tag, (dom_n, dom_ms, dom_work) = dom
+    is_flops = dom_tag.startswith("gemm")
+    peaks = load_peaks()
+    if is_flops:
+        achieved = dom_work / (dom_ms * 1e-3) / 1e12
+        peak, unit, bound = FP64_PEAK_TFLOPS, "TFLOP/s", "tensor"
+    else:
+        achieved = dom_work / (dom_ms * 1e-3) / 1e9
+        peak, unit, bound = float(peaks.get("hbm_gbs", 6557.8)), "GB/s", "hbm"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom_tag)
+
+    # e2e: the reference-facing C-ABI call with host buffers (H2D of the shift tables
+    # inside latsum_sum_to_tucker; D2H of the Tucker core and factors into pinned memory)
+    e2e_ms = []
+    h2d = (sum(len(s.shifts[l]) for s in g.sublattices for l in range(3)) * 8 + 3 * 8 * len(g.sublattices)
+           + g.defect_shifts.size * 8 + g.defect_charges.size * 8)
+    pinned = None
+    d2h = 0
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        te, _ = api.sum_to_tucker(g, g.eps, ctx)
+        r = te.ranks
+        if pinned is None:
+            pinned = [torch.empty(int(np.prod(r)), dtype=torch.float64, pin_memory=True)] + [
+                torch.empty(g.N[l] * r[l], dtype=torch.float64, pin_memory=True) for l in range(3)]
+            d2h = sum(p.numel() * 8 for p in pinned)
+        ctx.check(api._lib.lib().latsum_tucker_core(ctx.handle, te.handle,
+                                                    api.ctypes.c_void_p(pinned[0].data_ptr())))
+        for l in range(3):
+            ctx.check(api._lib.lib().latsum_tucker_factor(ctx.handle, te.handle, l,
+                                                          api.ctypes.c_void_p(pinned[1 + l].data_ptr())))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+        del te
+    e2e = max_over_ranks(statistics.mean(e2e_ms))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res = cpu_reference_step(g, args.core_terms, args.eval_slices, os.cpu_count() or 1)
+        cpu = {"value": res["ms"], "unit": "ms", "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": res["sample"], "parts": res["parts"],
+               "grid_eval_gpts_s": res["eval_gpts"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": v13, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded geometry; no dataset involved)",
+            "config": {
+                "workload": f"cfg{args.config} ({g.name}): Newton, N={g.N[0]}, M={g.M}, "
+                            f"{g.n_sites} sites, {g.n_defects} vacancies, eps={g.eps}; "
+                            f"step = stages 1-4 (eval box {lo}-{hi}), value = stages 1-3",
+                "ranks": list(rep.chosen_ranks), "merged_columns": list(can.dict_cols),
+                "canonical_rank": can.rank, "deflated": list(rep.deflated),
+                "l2": "256 MB buffer written between timed steps; eval output 68.7 GB >> L2",
+                "parallelism": f"replicated stages 1-3, z-slab eval x{world}" if world > 1
+                else "single GPU"},
+            "grid_eval": {"value": (n_total / (v4 * 1e-3) / 1e9) if do_eval else None,
+                          "unit": "Gpts/s", "ms": v4, "points": n_total},
+            "stage_ms": {k: float(v) for k, v in rep.ms.items()},
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom_tag,
+                         "launches": dom_n, "ms": dom_ms,
+                         "peak_source": FP64_PEAK_SOURCE if is_flops else "MEASURED_PEAKS.json hbm_gbs"},
+            "kernel_profile": {k: {"launches": v[0], "ms": round(v[1], 4),
+                                   "rate": (v[2] / (v[1] * 1e-3) / (1e12 if k.startswith("gemm") else 1e9))
+                                   if v[1] > 0 else None}
+                               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "clocks": clk,
+            "e2e": {"value": e2e, "unit": "ms", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches // max(1, args.steps)),
+            "gpu_launches_total": int(launches),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-eval", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--core-terms", type=int, default=200)
+    ap.add_argument("--eval-slices", type=int, default=4)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

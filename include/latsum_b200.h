@@ -65,6 +65,12 @@ int latsum_ctx_set_stream(latsum_ctx* ctx, void* cuda_stream);
 int latsum_ctx_synchronize(latsum_ctx* ctx);
 /* Number of kernels this context launched so far (its own kernels, not library ones). */
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);
+/* Per-kernel-class CUDA-event timing: when on, every launch group is bracketed by
+ * events on the context stream.  latsum_ctx_profile writes lines
+ * "<tag> <launches> <total ms> <algorithmic work>" (FLOPs for gemm_*, bytes otherwise)
+ * into buf and returns the full text length (call with buf=NULL to size it). */
+int latsum_ctx_set_profiling(latsum_ctx* ctx, int on);
+int64_t latsum_ctx_profile(latsum_ctx* ctx, char* buf, int64_t cap);
 
 /* ------------------------------------------------------------------ host rules (no GPU)
  * quadrature.hpp:303-341 build_quadrature (gauss branch); nodes/weights hold 2M+1 values. */

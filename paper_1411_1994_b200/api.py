@@ -83,6 +83,22 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.lib().latsum_ctx_kernel_launches(self._h))
 
+    def set_profiling(self, on: bool):
+        self.check(_lib.lib().latsum_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self) -> dict:
+        """{tag: (launches, total_ms, algorithmic_work)} from CUDA events (profiling on)."""
+        n = _lib.lib().latsum_ctx_profile(self._h, None, 0)
+        if n < 0:
+            raise RuntimeError(_lib.lib().latsum_last_error(self._h).decode())
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        _lib.lib().latsum_ctx_profile(self._h, buf, int(n) + 1)
+        out = {}
+        for line in buf.value.decode().splitlines():
+            tag, cnt, ms, work = line.split()
+            out[tag] = (int(cnt), float(ms), float(work))
+        return out
+
     def close(self):
         if self._h:
             _lib.lib().latsum_ctx_destroy(self._h)

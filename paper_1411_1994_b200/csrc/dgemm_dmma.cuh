@@ -34,16 +34,24 @@ struct GemmParams {
   int lower_only;         // skip tiles strictly above the diagonal (M == N Gram)
 };
 
-namespace gemm_cfg {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
-constexpr int WM = 64, WN = 32;  // warp tile: 2 x 4 warps
-constexpr int PAD = 4;           // row stride = 4 (mod 16) doubles: conflict-free fragments
-constexpr int SM_MMAJ = BK * (BM + PAD);   // [k][m] layout
-constexpr int SM_KMAJ = BM * (BK + PAD);   // [m][k] layout
-constexpr int SA = SM_MMAJ > SM_KMAJ ? SM_MMAJ : SM_KMAJ;
-constexpr int SB = SA;
-constexpr size_t SMEM_BYTES = size_t(STAGES) * (SA + SB) * sizeof(double);
-}  // namespace gemm_cfg
+// Tile configuration: block tile BM x BN x BK, STAGES-deep cp.async ring, warp tile
+// WM x WN (m8n8k4 fragments), PAD keeps shared-memory row strides = 4 (mod 16)
+// doubles so every 64-bit fragment load is bank-conflict free.
+template <int BM_, int BN_, int BK_, int STAGES_, int WM_, int WN_, int MINB_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, WM = WM_, WN = WN_;
+  static constexpr int MINB = MINB_;  // CTAs per SM the register budget targets
+  static constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
+  static constexpr int PAD = 4;
+  static constexpr int SA = (BK * (BM + PAD) > BM * (BK + PAD)) ? BK * (BM + PAD) : BM * (BK + PAD);
+  static constexpr int SB = (BK * (BN + PAD) > BN * (BK + PAD)) ? BK * (BN + PAD) : BN * (BK + PAD);
+  static constexpr size_t SMEM_BYTES = size_t(STAGES) * (SA + SB) * sizeof(double);
+};
+
+using CfgBig = GemmCfg<128, 128, 16, 4, 64, 32, 1>;    // 8 warps, 1 CTA/SM
+using CfgWide = GemmCfg<128, 128, 16, 4, 32, 32, 1>;   // 16 warps, 1 CTA/SM
+using CfgHalf = GemmCfg<128, 64, 16, 4, 64, 32, 2>;    // 4 warps, 2 CTAs/SM
+using CfgDeep = GemmCfg<128, 128, 32, 3, 64, 32, 1>;   // 8 warps, BK=32
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -63,49 +71,60 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
-// Loads the BM x BK tile of opA starting at (m0, k0) and the BK x BN tile of
-// opB at (k0, n0) into one pipeline stage.  Out-of-range elements are zero.
-template <bool TA, bool TB>
-__device__ __forceinline__ void load_stage(double* As, double* Bs, const double* A, int64_t lda,
-                                           const double* B, int64_t ldb, int64_t m0, int64_t n0,
-                                           int64_t k0, int64_t kend, int64_t M, int64_t N) {
-  using namespace gemm_cfg;
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int it = 0; it < (BM * BK) / THREADS; ++it) {
-    const int idx = tid + it * THREADS;
-    if (!TA) {  // contiguous in m: [k][m]
-      const int k = idx / BM, m = idx % BM;
-      const int64_t gm = m0 + m, gk = k0 + k;
-      const bool p = gm < M && gk < kend;
-      cp_async8(As + k * (BM + PAD) + m, p ? A + gm + gk * lda : A, p);
-    } else {  // contiguous in k: [m][k]
-      const int m = idx / BK, k = idx % BK;
-      const int64_t gm = m0 + m, gk = k0 + k;
-      const bool p = gm < M && gk < kend;
-      cp_async8(As + m * (BK + PAD) + k, p ? A + gk + gm * lda : A, p);
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < (BN * BK) / THREADS; ++it) {
-    const int idx = tid + it * THREADS;
-    if (TB) {  // contiguous in n: [k][n]
-      const int k = idx / BN, n = idx % BN;
-      const int64_t gn = n0 + n, gk = k0 + k;
-      const bool p = gn < N && gk < kend;
-      cp_async8(Bs + k * (BN + PAD) + n, p ? B + gn + gk * ldb : B, p);
-    } else {  // contiguous in k: [n][k]
-      const int n = idx / BK, k = idx % BK;
-      const int64_t gn = n0 + n, gk = k0 + k;
-      const bool p = gn < N && gk < kend;
-      cp_async8(Bs + n * (BK + PAD) + k, p ? B + gk + gn * ldb : B, p);
-    }
-  }
-}
+// Per-thread tile loader.  Each thread owns one fixed coordinate of the contiguous
+// dimension and a strided set of the other, so a stage needs one pointer, one
+// stride and two remaining-extent counters per operand (no 64-bit index math in
+// the main loop).  Out-of-range elements are zero-filled by cp.async src-size 0.
+template <int ROWS, int BKk, int THREADS, int PAD, bool KMAJOR>
+struct OperandLoader {
+  // KMAJOR == false: contiguous along the ROWS dimension (m or n); smem [k][row]
+  // KMAJOR == true : contiguous along k;                       smem [row][k]
+  static constexpr int ITERS = (ROWS * BKk) / THREADS;
+  static constexpr int FIX = KMAJOR ? BKk : ROWS;    // extent of the contiguous dim
+  static constexpr int STEP = THREADS / FIX;         // stride of the other dim per iter
+  const double* ptr;   // element (row0 + r_fix/var, kbeg + k_fix/var) of this thread
+  int64_t step_ld;     // STEP * ld
+  int64_t stage_adv;   // pointer advance per BK
+  int fix, var;        // this thread's coordinates in the tile
+  int64_t row_rem;     // rows remaining from (row0 + thread row)
+  int64_t k_rem;       // k remaining from (kbeg + thread k)
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(gemm_cfg::THREADS, 1) dgemm_dmma_kernel(GemmParams p) {
-  using namespace gemm_cfg;
+  __device__ __forceinline__ void init(const double* base, int64_t ld, int64_t row0,
+                                       int64_t rows, int64_t kbeg, int64_t kend) {
+    fix = threadIdx.x % FIX;
+    var = threadIdx.x / FIX;
+    const int r = KMAJOR ? var : fix, k = KMAJOR ? fix : var;
+    ptr = KMAJOR ? base + (kbeg + k) + (row0 + r) * ld : base + (row0 + r) + (kbeg + k) * ld;
+    step_ld = int64_t(STEP) * ld;
+    stage_adv = KMAJOR ? BKk : int64_t(BKk) * ld;
+    row_rem = rows - row0 - r;
+    k_rem = kend - kbeg - k;
+  }
+  // stage s of this tile into smem buffer `dst`
+  __device__ __forceinline__ void load(double* dst, int s) const {
+    const double* src = ptr + int64_t(s) * stage_adv;
+    const int64_t krem = k_rem - int64_t(s) * BKk;
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int v = var + it * STEP;
+      bool pred;
+      double* d;
+      if (KMAJOR) {
+        pred = krem > 0 && row_rem - it * STEP > 0;
+        d = dst + v * (BKk + PAD) + fix;
+      } else {
+        pred = row_rem > 0 && krem - it * STEP > 0;
+        d = dst + v * (ROWS + PAD) + fix;
+      }
+      cp_async8(d, pred ? src + it * step_ld : src - int64_t(s) * stage_adv, pred);
+    }
+  }
+};
+
+template <class Cfg, bool TA, bool TB>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm_dmma_kernel(GemmParams p) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, PAD = Cfg::PAD, STAGES = Cfg::STAGES;
+  constexpr int WM = Cfg::WM, WN = Cfg::WN, SA = Cfg::SA, SB = Cfg::SB;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * SA;
@@ -113,7 +132,7 @@ __global__ void __launch_bounds__(gemm_cfg::THREADS, 1) dgemm_dmma_kernel(GemmPa
   const int64_t tiles_m = (p.M + BM - 1) / BM;
   const int64_t tm = blockIdx.x % tiles_m;
   const int64_t tn = blockIdx.y;
-  if (p.lower_only && tn > tm) return;  // tile entirely above the diagonal (BM == BN)
+  if (p.lower_only && tn * BN > tm * BM + BM - 1) return;  // tile entirely above the diagonal
   const int64_t m0 = tm * BM, n0 = tn * BN;
 
   int64_t b = blockIdx.z, split = 0;
@@ -152,45 +171,71 @@ __global__ void __launch_bounds__(gemm_cfg::THREADS, 1) dgemm_dmma_kernel(GemmPa
     for (int j = 0; j < WN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  // opA: rows = m; NoTrans contiguous in m, Trans contiguous in k.
+  // opB: rows = n; NoTrans contiguous in k, Trans contiguous in n.
+  OperandLoader<BM, BK, Cfg::THREADS, PAD, TA> la;
+  OperandLoader<BN, BK, Cfg::THREADS, PAD, !TB> lb;
+  la.init(A, p.lda, m0, p.M, kbeg, kend);
+  lb.init(B, p.ldb, n0, p.N, kbeg, kend);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles)
-      load_stage<TA, TB>(As + s * SA, Bs + s * SB, A, p.lda, B, p.ldb, m0, n0, kbeg + s * BK, kend,
-                         p.M, p.N);
+    if (s < ktiles) {
+      la.load(As + s * SA, s);
+      lb.load(Bs + s * SB, s);
+    }
     cp_async_commit();
   }
 
-  for (int64_t kt = 0; kt < ktiles; ++kt) {
+  // Fragments are double-buffered in registers: the 64-bit shared loads of k-step
+  // s+1 are issued before the DMMAs of step s, and the stage barrier sits before the
+  // last k-step of a stage so the next stage's first fragments overlap its DMMAs.
+  constexpr int KSTEPS = BK / 4;
+  double af[2][WM / 8], bf[2][WN / 8];
+  auto load_frags = [&](int buf, const double* as, const double* bs, int kk) {
+#pragma unroll
+    for (int i = 0; i < WM / 8; ++i) {
+      const int m = wm + i * 8 + g, k = kk + t;
+      af[buf][i] = TA ? as[m * (BK + PAD) + k] : as[k * (BM + PAD) + m];
+    }
+#pragma unroll
+    for (int j = 0; j < WN / 8; ++j) {
+      const int n = wn + j * 8 + g, k = kk + t;
+      bf[buf][j] = TB ? bs[k * (BN + PAD) + n] : bs[n * (BK + PAD) + k];
+    }
+  };
+  if (ktiles > 0) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      const int64_t nk = kt + STAGES - 1;
-      if (nk < ktiles) {
-        const int st = int(nk % STAGES);
-        load_stage<TA, TB>(As + st * SA, Bs + st * SB, A, p.lda, B, p.ldb, m0, n0,
-                           kbeg + nk * BK, kend, p.M, p.N);
-      }
-      cp_async_commit();
-    }
+    load_frags(0, As, Bs, 0);
+  }
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
     const double* as = As + int(kt % STAGES) * SA;
     const double* bs = Bs + int(kt % STAGES) * SB;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[WM / 8], bf[WN / 8];
-#pragma unroll
-      for (int i = 0; i < WM / 8; ++i) {
-        const int m = wm + i * 8 + g, k = kk + t;
-        af[i] = TA ? as[m * (BK + PAD) + k] : as[k * (BM + PAD) + m];
-      }
-#pragma unroll
-      for (int j = 0; j < WN / 8; ++j) {
-        const int n = wn + j * 8 + g, k = kk + t;
-        bf[j] = TB ? bs[k * (BN + PAD) + n] : bs[n * (BK + PAD) + k];
+    for (int s = 0; s < KSTEPS; ++s) {
+      const int cur = s & 1;
+      if (s + 1 < KSTEPS) {
+        load_frags(cur ^ 1, as, bs, (s + 1) * 4);
+      } else {
+        // stage kt+1 must have landed; every warp is past stage kt-1, whose slot the
+        // load for stage kt+STAGES-1 reuses
+        cp_async_wait<STAGES - 3>();
+        __syncthreads();
+        const int64_t nk = kt + STAGES - 1;
+        if (nk < ktiles) {
+          const int st = int(nk % STAGES);
+          la.load(As + st * SA, int(nk));
+          lb.load(Bs + st * SB, int(nk));
+        }
+        cp_async_commit();
+        if (kt + 1 < ktiles)
+          load_frags(cur ^ 1, As + int((kt + 1) % STAGES) * SA, Bs + int((kt + 1) % STAGES) * SB, 0);
       }
 #pragma unroll
       for (int i = 0; i < WM / 8; ++i)
 #pragma unroll
-        for (int j = 0; j < WN / 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < WN / 8; ++j)
+          dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();

@@ -8,12 +8,15 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
+#include <exception>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -61,6 +64,15 @@ struct latsum_ctx {
   std::string err;
   int64_t launches = 0;
   bool smem_set = false;
+  // optional per-kernel-class CUDA-event timing (latsum_ctx_set_profiling)
+  bool prof = false;
+  struct Rec { std::string tag; cudaEvent_t a, b; double work; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  struct Stat { int64_t count = 0; double ms = 0.0, work = 0.0; };
+  std::map<std::string, Stat> stats;
+  // worker contexts (own stream + cuSOLVER handle) for the concurrent per-mode reductions
+  latsum_ctx* sub[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -87,6 +99,8 @@ struct DBuf {
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  // hand the buffer to another stream (caller guarantees the streams are ordered)
+  void adopt(cudaStream_t st) { s = st; }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
     p = o.p; n = o.n; s = o.s;
@@ -128,26 +142,109 @@ void post_launch(latsum_ctx* c) {
   CK(cudaGetLastError());
 }
 
+cudaEvent_t prof_event(latsum_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+// Records [start, stop] events around the launches in its scope when profiling is on;
+// `work` is the algorithmic FLOPs or bytes the caller attributes to the scope.
+struct ProfScope {
+  latsum_ctx* c;
+  bool on;
+  latsum_ctx::Rec rec;
+  ProfScope(latsum_ctx* ctx, const char* tag, double work = 0.0) : c(ctx), on(ctx->prof && tag) {
+    if (!on) return;
+    rec.tag = tag;
+    rec.work = work;
+    rec.a = prof_event(c);
+    rec.b = prof_event(c);
+    CK(cudaEventRecord(rec.a, c->stream));
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.b, c->stream);
+    c->pending.push_back(rec);
+  }
+};
+
+void prof_harvest(latsum_ctx* c) {
+  if (c->pending.empty()) return;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->pending) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    auto& st = c->stats[r.tag];
+    st.count += 1;
+    st.ms += ms;
+    st.work += r.work;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->pending.clear();
+}
+
 // ------------------------------------------------------------------ GEMM launcher
 struct GemmOpts {
   int64_t batch = 1, sA = 0, sB = 0, sC = 0;
   const int64_t* kseg = nullptr;
   bool lower = false;
   int splits = 0;  // 0 = auto
+  const char* tag = "gemm";
 };
+
+template <class Cfg>
+void set_smem_cfg() {
+  const int bytes = int(Cfg::SMEM_BYTES);
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<Cfg, false, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<Cfg, false, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<Cfg, true, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<Cfg, true, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
 
 void set_gemm_smem(latsum_ctx* c) {
   if (c->smem_set) return;
-  const int bytes = int(gemm_cfg::SMEM_BYTES);
-  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<false, false>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<false, true>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<true, false>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(dgemm_dmma_kernel<true, true>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  set_smem_cfg<CfgBig>();
+  set_smem_cfg<CfgWide>();
+  set_smem_cfg<CfgHalf>();
+  set_smem_cfg<CfgDeep>();
   c->smem_set = true;
+}
+
+GemmOpts tagged(const char* tag) {
+  GemmOpts o;
+  o.tag = tag;
+  return o;
+}
+
+// Tile configuration: LATSUM_GEMM_CFG=0..3 overrides (A/B measurements only).
+int gemm_cfg_choice() {
+  static int v = [] {
+    const char* e = std::getenv("LATSUM_GEMM_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <class Cfg>
+void launch_gemm(latsum_ctx* c, bool ta, bool tb, GemmParams p, int64_t tm, int64_t tn) {
+  dim3 grid(unsigned(tm), unsigned(tn), unsigned(p.batch * p.splits));
+  const size_t sm = Cfg::SMEM_BYTES;
+  const int th = Cfg::THREADS;
+  if (!ta && !tb) dgemm_dmma_kernel<Cfg, false, false><<<grid, th, sm, c->stream>>>(p);
+  if (!ta && tb) dgemm_dmma_kernel<Cfg, false, true><<<grid, th, sm, c->stream>>>(p);
+  if (ta && !tb) dgemm_dmma_kernel<Cfg, true, false><<<grid, th, sm, c->stream>>>(p);
+  if (ta && tb) dgemm_dmma_kernel<Cfg, true, true><<<grid, th, sm, c->stream>>>(p);
 }
 
 void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
@@ -155,7 +252,9 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
           int64_t ldc, GemmOpts o = {}) {
   if (M <= 0 || N <= 0 || o.batch <= 0) return;
   set_gemm_smem(c);
-  using namespace gemm_cfg;
+  const int choice = gemm_cfg_choice();
+  const int BM = 128, BK = 16;
+  const int BN = choice == 2 ? CfgHalf::BN : 128;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   int splits = o.splits;
   if (splits == 0) {
@@ -174,11 +273,17 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
     ws.alloc(c, size_t(splits) * M * N * o.batch);
     p.C = ws.p;
   }
-  dim3 grid(unsigned(tm), unsigned(tn), unsigned(o.batch * splits));
-  if (!ta && !tb) dgemm_dmma_kernel<false, false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
-  if (!ta && tb) dgemm_dmma_kernel<false, true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
-  if (ta && !tb) dgemm_dmma_kernel<true, false><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
-  if (ta && tb) dgemm_dmma_kernel<true, true><<<grid, THREADS, SMEM_BYTES, c->stream>>>(p);
+  // algorithmic FLOPs (2 M N K per product; segmented: 2 M N sum(segments))
+  double flops = o.kseg ? 2.0 * double(M) * double(N) * double(K)
+                        : 2.0 * double(M) * double(N) * double(K) * double(o.batch);
+  if (o.lower) flops = double(M) * double(M + 1) * double(K) * double(o.batch);  // SYRK
+  ProfScope ps(c, o.tag, flops);
+  switch (choice) {
+    case 1: launch_gemm<CfgWide>(c, ta, tb, p, tm, tn); break;
+    case 2: launch_gemm<CfgHalf>(c, ta, tb, p, tm, tn); break;
+    case 3: launch_gemm<CfgDeep>(c, ta, tb, p, tm, tn); break;
+    default: launch_gemm<CfgBig>(c, ta, tb, p, tm, tn); break;
+  }
   post_launch(c);
   if (splits > 1) {
     dim3 g2(unsigned(grid_for(M * N)), unsigned(o.batch));
@@ -198,6 +303,7 @@ void syevd(latsum_ctx* c, int64_t n, double* A, double* W) {
                                  CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F, W,
                                  CUDA_R_64F, &dbytes, &hbytes));
   DBuf work(c, (dbytes + 7) / 8 + 1);
+  ProfScope ps(c, "syevd(cusolver)", double(n));
   std::vector<char> hwork(hbytes + 1);
   int* info = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void**>(&info), sizeof(int), c->stream));
@@ -352,6 +458,7 @@ void build_reference(latsum_ctx* c, int family, double lambda, const int64_t N[3
       const double lower = 0.0 - (2.0 * box[l]) / 2.0;
       ref.cols[l].alloc(c, size_t(n2) * ref.Rd);
       dim3 g(unsigned((n2 + 255) / 256), unsigned(ref.Rd));
+      ProfScope ps(c, "ref_integrals", 8.0 * double(n2) * ref.Rd);
       k_ref_integrals<<<g, 256, 0, c->stream>>>(ds.p, n2, lower, h, ref.cols[l].p);
       post_launch(c);
       DBuf dn(c, ref.Rd);
@@ -448,6 +555,7 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     DBuf partial(c, size_t(can.d[l]) * nchunk), norms(c, can.d[l]);
     DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
     dim3 g(unsigned(can.d[l]), unsigned(nchunk));
+    ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
     k_dict_sumsq<<<g, 256, 0, c->stream>>>(a);
     post_launch(c);
     k_dict_norms<<<unsigned((can.d[l] + 255) / 256), 256, 0, c->stream>>>(a, can.d[l]);
@@ -508,6 +616,7 @@ void materialize_factor(latsum_ctx* c, const latsum_canonical& can, int l, doubl
   DVec<int64_t> idx;
   idx.upload(c, can.term_col[l]);
   const int64_t N = can.N[l];
+  ProfScope ps(c, "materialize_side_matrix", 8.0 * double(N) * double(can.Mc));
   dim3 g(unsigned(std::max<int64_t>(1, std::min<int64_t>(64, (N / 2 + 255) / 256))),
          unsigned(can.Mc));
   require(can.Mc <= 65535 * 64, "materialize: too many columns");
@@ -546,7 +655,7 @@ int64_t rank_for_tolerance(const std::vector<double>& sv, double eps) {
 }
 
 void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, double* G) {
-  GemmOpts o;
+  GemmOpts o = tagged("gemm_gram");
   o.lower = true;
   if (rows) gemm(c, false, true, N, N, d, 1.0, A, N, A, N, 0.0, G, N, o);   // A A^T
   else gemm(c, true, false, d, d, N, 1.0, A, N, A, N, 0.0, G, d, o);        // A^T A
@@ -556,7 +665,7 @@ void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, doubl
 void lowdin(latsum_ctx* c, double* U, int64_t N, int64_t k) {
   if (k == 0) return;
   DBuf S(c, size_t(k) * k), W(c, k);
-  gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k);
+  gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k, tagged("gemm_basis"));
   syevd(c, k, S.p, W.p);
   std::vector<double> w(k);
   CK(cudaMemcpyAsync(w.data(), W.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
@@ -567,8 +676,8 @@ void lowdin(latsum_ctx* c, double* U, int64_t N, int64_t k) {
   DBuf Qs(c, size_t(k) * k), Mm(c, size_t(k) * k), Un(c, size_t(N) * k);
   k_scale_columns<<<grid_for(k * k), 256, 0, c->stream>>>(S.p, k, k, sc.p, Qs.p);
   post_launch(c);
-  gemm(c, false, true, k, k, k, 1.0, Qs.p, k, S.p, k, 0.0, Mm.p, k);
-  gemm(c, false, false, N, k, k, 1.0, U, N, Mm.p, k, 0.0, Un.p, N);
+  gemm(c, false, true, k, k, k, 1.0, Qs.p, k, S.p, k, 0.0, Mm.p, k, tagged("gemm_basis"));
+  gemm(c, false, false, N, k, k, 1.0, U, N, Mm.p, k, 0.0, Un.p, N, tagged("gemm_basis"));
   CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
 }
 
@@ -587,7 +696,7 @@ void left_basis(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d,
   DBuf Vd(c, size_t(d) * k);
   k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, d, k, Vd.p);
   post_launch(c);
-  gemm(c, false, false, N, k, d, 1.0, A, N, Vd.p, d, 0.0, U, N);
+  gemm(c, false, false, N, k, d, 1.0, A, N, Vd.p, d, 0.0, U, N, tagged("gemm_basis"));
   std::vector<double> inv(k);
   for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
   DVec<double> sc;
@@ -675,8 +784,8 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
       CK(cudaMemcpyAsync(Ap.p, At.p, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, c->stream));
       DBuf C(c, size_t(k1) * d);
       for (int rep = 0; rep < 2; ++rep) {  // project out span(U1), then re-orthogonalise once
-        gemm(c, true, false, k1, d, N, 1.0, U1.p, N, Ap.p, N, 0.0, C.p, k1);
-        gemm(c, false, false, N, d, k1, -1.0, U1.p, N, C.p, k1, 1.0, Ap.p, N);
+        gemm(c, true, false, k1, d, N, 1.0, U1.p, N, Ap.p, N, 0.0, C.p, k1, tagged("gemm_deflate"));
+        gemm(c, false, false, N, d, k1, -1.0, U1.p, N, C.p, k1, 1.0, Ap.p, N, tagged("gemm_deflate"));
       }
       G2.alloc(c, size_t(n) * n);
       gram(c, rows, Ap.p, N, d, G2.p);
@@ -759,9 +868,10 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
   for (int l = 0; l < 3; ++l) {
     G[l].alloc(c, size_t(can.d[l]) * can.d[l]);
     gemm(c, true, false, can.d[l], can.d[l], can.N[l], 1.0, can.dict[l].p, can.N[l],
-         can.dict[l].p, can.N[l], 0.0, G[l].p, can.d[l]);
+         can.dict[l].p, can.N[l], 0.0, G[l].p, can.d[l], tagged("gemm_norm_gram"));
   }
   DBuf part(c, can.T), sum(c, 1);
+  ProfScope ps(c, "norm_hadamard", 3.0 * double(can.T) * double(can.T));
   k_hadamard_norm_rows<<<unsigned((can.T + 127) / 128), 128, 0, c->stream>>>(
       G[0].p, G[1].p, G[2].p, can.d[0], can.d[1], can.d[2], can.dtc[0].p, can.dtc[1].p,
       can.dtc[2].p, can.dtw.p, can.T, part.p);
@@ -793,14 +903,79 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
   DBuf X(c, size_t(r12) * ac);
   for (int64_t a0 = 0; a0 < d0; a0 += ac) {
     const int64_t na = std::min(ac, d0 - a0);
-    GemmOpts o;
+    GemmOpts o = tagged("gemm_core_x");
     o.batch = na;
     o.sC = r12;
     o.kseg = can.dtseg.p + a0;
     gemm(c, false, true, r[1], r[2], T, 1.0, G1.p, r[1], G2.p, r[2], 0.0, X.p, r[1], o);
     gemm(c, false, true, r[0], r12, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, r12,
-         a0 == 0 ? 0.0 : 1.0, core, r[0]);
+         a0 == 0 ? 0.0 : 1.0, core, r[0], tagged("gemm_core"));
   }
+}
+
+latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
+  if (!c->sub[i]) {
+    auto* w = new latsum_ctx();
+    w->device = c->device;
+    CK(cudaStreamCreateWithFlags(&w->own, cudaStreamNonBlocking));
+    w->stream = w->own;
+    CS(cusolverDnCreate(&w->solver));
+    CS(cusolverDnSetStream(w->solver, w->stream));
+    CS(cusolverDnCreateParams(&w->solver_params));
+    c->sub[i] = w;
+  }
+  c->sub[i]->prof = c->prof;
+  return c->sub[i];
+}
+
+void merge_sub(latsum_ctx* c, latsum_ctx* w) {
+  prof_harvest(w);
+  for (const auto& kv : w->stats) {
+    auto& st = c->stats[kv.first];
+    st.count += kv.second.count;
+    st.ms += kv.second.ms;
+    st.work += kv.second.work;
+  }
+  w->stats.clear();
+  c->launches += w->launches;
+  w->launches = 0;
+}
+
+// Runs f(worker) for workers 0..n-1 concurrently (one host thread and stream each),
+// ordered after the work already queued on c->stream and before anything queued next.
+template <typename F>
+void fork_join(latsum_ctx* c, int n, F&& f) {
+  cudaEvent_t fork;
+  CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  CK(cudaEventRecord(fork, c->stream));
+  std::vector<latsum_ctx*> ws(n);
+  for (int i = 0; i < n; ++i) {
+    ws[i] = sub_ctx(c, i);
+    CK(cudaStreamWaitEvent(ws[i]->stream, fork, 0));
+  }
+  std::vector<std::exception_ptr> errs(n);
+  std::vector<std::thread> th;
+  for (int i = 0; i < n; ++i)
+    th.emplace_back([&, i] {
+      try {
+        CK(cudaSetDevice(c->device));
+        f(ws[i], i);
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n; ++i) {
+    cudaEvent_t join;
+    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    CK(cudaEventRecord(join, ws[i]->stream));
+    CK(cudaStreamWaitEvent(c->stream, join, 0));
+    CK(cudaEventDestroy(join));
+    merge_sub(c, ws[i]);
+  }
+  CK(cudaEventDestroy(fork));
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
 }
 
 void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks, double tol,
@@ -814,11 +989,26 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   double wn2 = 0;
   for (double w : can.weights) wn2 += w * w;
   rep.weight_norm = std::sqrt(wn2);
-  {
-    Timer tn(c);
-    tn.start();
-    rep.input_norm = canonical_norm(c, can);
-    tm.norm = tn.stop();
+  // the three mode reductions and norm_f are independent: one worker stream each
+  ModeOut mo[3];
+  Timings tms[4];
+  const bool zero_terms = can.Mc == 0 || can.T == 0;
+  fork_join(c, zero_terms ? 1 : 4, [&](latsum_ctx* w, int i) {
+    if (i == 3 || zero_terms) {
+      Timer tn(w);
+      tn.start();
+      rep.input_norm = canonical_norm(w, can);
+      tms[3].norm = tn.stop();
+    } else {
+      reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
+    }
+  });
+  for (int l = 0; l < 3; ++l) mo[l].Z.adopt(c->stream);
+  for (const auto& x : tms) {
+    tm.gram += x.gram;
+    tm.syevd += x.syevd;
+    tm.deflate += x.deflate;
+    tm.norm += x.norm;
   }
   if (can.Mc == 0 || rep.input_norm == 0.0) {  // zero tensor (rank_reduction.hpp:183-187)
     for (int l = 0; l < 3; ++l) {
@@ -837,8 +1027,6 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     rep.ms_total = total.stop();
     return;
   }
-  ModeOut mo[3];
-  for (int l = 0; l < 3; ++l) reduce_mode(c, can, l, ranks, tol, deflate, mo[l], tm);
   DBuf P[3];
   Timer tp(c);
   tp.start();
@@ -846,7 +1034,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     t.r[l] = mo[l].r;
     P[l].alloc(c, size_t(mo[l].r) * can.d[l]);
     gemm(c, true, false, mo[l].r, can.d[l], can.N[l], 1.0, mo[l].Z.p, can.N[l], can.dict[l].p,
-         can.N[l], 0.0, P[l].p, mo[l].r);
+         can.N[l], 0.0, P[l].p, mo[l].r, tagged("gemm_project"));
   }
   tm.project = tp.stop();
   tp.start();
@@ -908,7 +1096,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   DBuf X(c, size_t(r0) * njc * nkc);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
-    GemmOpts oq;
+    GemmOpts oq = tagged("gemm_eval_q");
     oq.batch = r2;
     oq.sA = r0 * r1;
     oq.sC = r0 * njj;
@@ -916,8 +1104,8 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
     for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
       const int64_t nkk = std::min(nkc, nk - k0);
       gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
-           r0 * njj);
-      GemmOpts ov;
+           r0 * njj, tagged("gemm_eval_x"));
+      GemmOpts ov = tagged("gemm_eval_slab");
       ov.batch = nkk;
       ov.sB = r0 * njj;
       ov.sC = ni * nj;
@@ -956,7 +1144,7 @@ void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo
         can.dict[1].p, can.N[1], can.dict[2].p, can.N[2], can.dtc[1].p, can.dtc[2].p, can.dtw.p,
         T, lo[1], nj, lo[2] + k0, nkk, X.p);
     post_launch(c);
-    GemmOpts ov;
+    GemmOpts ov = tagged("gemm_eval_canonical");
     ov.batch = nkk;
     ov.sB = T * nj;
     ov.sC = ni * nj;
@@ -982,7 +1170,8 @@ void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes,
     k_gather_rows<<<grid_for(npp * r0), 256, 0, c->stream>>>(t.U[0].p, t.N[0], r0, dp.p + 3 * p0,
                                                              0, npp, rowsU.p);
     post_launch(c);
-    gemm(c, false, false, npp, r12, r0, 1.0, rowsU.p, npp, t.core.p, r0, 0.0, Wm.p, npp);
+    gemm(c, false, false, npp, r12, r0, 1.0, rowsU.p, npp, t.core.p, r0, 0.0, Wm.p, npp,
+         tagged("gemm_probes"));
     k_tucker_probe_finish<<<unsigned(npp), 256, 0, c->stream>>>(
         Wm.p, npp, t.r[1], t.r[2], t.U[1].p, t.N[1], t.U[2].p, t.N[2], dp.p + 3 * p0, res.p + p0);
     post_launch(c);
@@ -1031,6 +1220,10 @@ void latsum_ctx_destroy(latsum_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  try { prof_harvest(c); } catch (...) {}
+  for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto* w : c->sub)
+    if (w) latsum_ctx_destroy(w);
   if (c->solver_params) cusolverDnDestroyParams(c->solver_params);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own) cudaStreamDestroy(c->own);
@@ -1051,6 +1244,34 @@ int latsum_ctx_synchronize(latsum_ctx* c) {
 }
 
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* c) { return c ? c->launches : 0; }
+
+int latsum_ctx_set_profiling(latsum_ctx* c, int on) {
+  return guarded(c, [&] {
+    prof_harvest(c);
+    c->prof = on != 0;
+    c->stats.clear();
+  });
+}
+
+int64_t latsum_ctx_profile(latsum_ctx* c, char* buf, int64_t cap) {
+  std::string out;
+  int st = guarded(c, [&] {
+    prof_harvest(c);
+    char line[256];
+    for (const auto& kv : c->stats) {
+      snprintf(line, sizeof(line), "%s %lld %.6f %.6e\n", kv.first.c_str(),
+               (long long)kv.second.count, kv.second.ms, kv.second.work);
+      out += line;
+    }
+  });
+  if (st != LATSUM_OK) return -1;
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(out.size(), size_t(cap - 1));
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return int64_t(out.size());
+}
 
 int latsum_reference_build(latsum_ctx* c, int family, double lambda, const int64_t N[3],
                            const double box[3], int M, double step_constant,

@@ -4,9 +4,11 @@
 // them on the host with FMA contraction off (-ffp-contract=off) makes the nodes
 // t_k and weights a_k bit-identical to the reference's libm arithmetic, which
 // the 1e-12 directional parity of stage 1 depends on.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>
+#include <thread>
 #include <vector>
 
 #include "latsum_b200.h"
@@ -46,12 +48,14 @@ double max_pointwise_rel(int family, double lambda, const double* t, const doubl
   double worst = 0.0;
   for (int i = 0; i < npts; ++i) {
     const double z = std::exp(la + (lA - la) * double(i) / double(npts - 1));
-    const double x[3] = {z, 0.0, 0.0};
+    // separable_eval at (z, 0, 0): the two zero coordinates contribute
+    // exp(-s*0*0) = exp(-0) = 1 exactly, so only the first factor is evaluated
+    // (bit-identical to the three-factor product).
     double sum = 0.0;
     for (int k = 0; k < R; ++k) {
       const double s = t[k] * t[k];
       double prod = a[k];
-      for (int l = 0; l < 3; ++l) prod *= std::exp(-s * x[l] * x[l]);
+      prod *= std::exp(-s * z * z);
       sum += prod;
     }
     const double exact = closed_form(family, lambda, z);
@@ -79,20 +83,35 @@ double latsum_default_step_constant(int family, double lambda, int M, double she
   // quadrature.hpp:416-447: 53 candidates base*(0.5 + 1.3 i/52),
   // base = asinh(2.5 A/a)/log M; first strict minimum of the finite errors.
   if (npts <= 1) npts = 320;
+  // The 53 candidates are independent: evaluate them on host threads, then pick the
+  // first strict minimum in candidate order exactly as the sequential sweep does.
   const double base = std::asinh(2.5 * (shell_A / shell_a)) / std::log(double(M));
-  std::vector<double> t(2 * M + 1), a(2 * M + 1);
-  double best = std::numeric_limits<double>::infinity();
-  double best_c0 = base * 0.5;
-  for (int i = 0; i < 53; ++i) {
-    const double c0 = base * (0.5 + 1.3 * double(i) / 52.0);
-    sinc_rule(family, lambda, M, c0, shell_A, t.data(), a.data());
-    const double e =
-        max_pointwise_rel(family, lambda, t.data(), a.data(), 2 * M + 1, shell_a, shell_A, npts);
-    if (std::isfinite(e) && e < best) {
-      best = e;
-      best_c0 = c0;
+  constexpr int kCand = 53;
+  double c0s[kCand], errs[kCand];
+  for (int i = 0; i < kCand; ++i) c0s[i] = base * (0.5 + 1.3 * double(i) / 52.0);
+  auto work = [&](int lo, int hi) {
+    std::vector<double> t(2 * M + 1), a(2 * M + 1);
+    for (int i = lo; i < hi; ++i) {
+      sinc_rule(family, lambda, M, c0s[i], shell_A, t.data(), a.data());
+      errs[i] = max_pointwise_rel(family, lambda, t.data(), a.data(), 2 * M + 1, shell_a, shell_A,
+                                  npts);
     }
+  };
+  const int nt = std::max(1, std::min<int>(8, int(std::thread::hardware_concurrency())));
+  std::vector<std::thread> pool;
+  const int chunk = (kCand + nt - 1) / nt;
+  for (int w = 0; w < nt; ++w) {
+    const int lo = w * chunk, hi = std::min(kCand, lo + chunk);
+    if (lo < hi) pool.emplace_back(work, lo, hi);
   }
+  for (auto& th : pool) th.join();
+  double best = std::numeric_limits<double>::infinity();
+  double best_c0 = c0s[0];
+  for (int i = 0; i < kCand; ++i)
+    if (std::isfinite(errs[i]) && errs[i] < best) {
+      best = errs[i];
+      best_c0 = c0s[i];
+    }
   return best_c0;
 }
 

@@ -62,8 +62,9 @@ int main() {
   const char* names[4] = {"m8n8k4", "m16n8k4", "m16n8k8", "m16n8k16"};
   const double flops_per_mma[4] = {2.0 * 8 * 8 * 4, 2.0 * 16 * 8 * 4, 2.0 * 16 * 8 * 8, 2.0 * 16 * 8 * 16};
   for (int shape = 0; shape < 4; ++shape) {
-    for (int warps : {4, 8, 16}) {
-      int blocks = 148 * 4, threads = 32 * warps, iters = 2000;
+    for (int cfg = 0; cfg < 6; ++cfg) {
+      const int warps = (cfg % 3 == 0) ? 4 : (cfg % 3 == 1) ? 8 : 16;
+      int blocks = cfg < 3 ? 148 * 4 : 148, threads = 32 * warps, iters = 2000;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
         if (shape == 0) dmma_loop<0><<<blocks, threads>>>(out, iters);
@@ -76,7 +77,7 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       double fl = flops_per_mma[shape] * 8.0 * iters * (double)blocks * warps;
-      printf("DMMA %-9s warps/blk %2d: %.2f TFLOP/s (%.3f ms)\n", names[shape], warps, fl / ms / 1e9, ms);
+      printf("DMMA %-9s blocks %4d warps/blk %2d: %.2f TFLOP/s (%.3f ms)\n", names[shape], blocks, warps, fl / ms / 1e9, ms);
     }
   }
   for (int warps : {8, 16, 32}) {

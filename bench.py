@@ -231,8 +231,9 @@ def run_gpu(args):
         flush.zero_()
         torch.cuda.synchronize(dev)
         barrier()
+        if i == 0 and not os.environ.get("BENCH_NO_CLOCKS"):
+            clocks.start()  # started before the warm-up so nvidia-smi start-up is not timed
         if i == args.warmup:
-            clocks.start()
             launches0 = ctx.kernel_launches
         ev[0].record(stream)
         ref, can, t, rep = step()
@@ -329,6 +330,7 @@ def run_gpu(args):
                 "l2": "256 MB buffer written between timed steps; eval output 68.7 GB >> L2",
                 "parallelism": f"replicated stages 1-3, z-slab eval x{world}" if world > 1
                 else "single GPU"},
+            "step_ms_stages_1_3": [round(x, 3) for x in ms13],
             "grid_eval": {"value": (n_total / (v4 * 1e-3) / 1e9) if do_eval else None,
                           "unit": "Gpts/s", "ms": v4, "points": n_total},
             "stage_ms": {k: float(v) for k, v in rep.ms.items()},

@@ -37,6 +37,11 @@ enum { LATSUM_NEWTON = 0, LATSUM_YUKAWA = 1 }; /* kernel.hpp:17 KernelFamily (ga
 
 enum { LATSUM_DEFLATE_NEVER = 0, LATSUM_DEFLATE_ALWAYS = 1, LATSUM_DEFLATE_AUTO = 2 };
 
+/* latsum_rhosvd_ex flags: skip the dense core (r1 r2 r3 doubles; 518 GB for BASELINE
+ * cfg5) and keep the projected factors P_l = Z_l^T A_l instead; entries and boxes are
+ * then evaluated in projected-CP form, which equals the Tucker tensor. */
+enum { LATSUM_RHOSVD_FACTORS_ONLY = 1 };
+
 typedef struct latsum_ctx latsum_ctx;
 typedef struct latsum_reference latsum_reference;
 typedef struct latsum_canonical latsum_canonical;
@@ -54,6 +59,7 @@ typedef struct {
   int gram_rows[3];        /* 1: Gram A A^T (N x N); 0: Gram A^T A over merged columns */
   int64_t gram_size[3];
   double ms_gram, ms_syevd, ms_deflate, ms_project, ms_core, ms_norm, ms_total; /* CUDA events */
+  int64_t deflate_k1[3];   /* pass-1 directions kept (lambda > 1e-10 lambda_max) when deflated */
 } latsum_spectral_report;
 
 /* ------------------------------------------------------------------ context */
@@ -146,7 +152,12 @@ int latsum_canonical_eval_box_device(latsum_ctx* ctx, const latsum_canonical* ca
 int latsum_rhosvd(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* ranks,
                   double tolerance, int deflate, latsum_tucker** out,
                   latsum_spectral_report* report);
+int latsum_rhosvd_ex(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* ranks,
+                     double tolerance, int deflate, int flags, latsum_tucker** out,
+                     latsum_spectral_report* report);
 void latsum_tucker_destroy(latsum_tucker* t);
+/* 1 when the dense core exists (latsum_tucker_core), 0 for a factors-only result. */
+int latsum_tucker_has_core(const latsum_tucker* t);
 int latsum_tucker_info(const latsum_tucker* t, int64_t dims[3], int64_t ranks[3]);
 /* SpectralReport::singular_values[mode] (report.n_singular[mode] values, descending). */
 int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out);

@@ -55,6 +55,7 @@ class LatsumReport(ctypes.Structure):
         ("ms_deflate", ctypes.c_double), ("ms_project", ctypes.c_double),
         ("ms_core", ctypes.c_double), ("ms_norm", ctypes.c_double),
         ("ms_total", ctypes.c_double),
+        ("deflate_k1", ctypes.c_int64 * 3),
     ]
 
 
@@ -91,7 +92,9 @@ SIGNATURES = [
     ("latsum_canonical_norm", _I, [_P, _P, _P]),
     ("latsum_canonical_eval_box_device", _I, [_P, _P, _P, _P, _P]),
     ("latsum_rhosvd", _I, [_P, _P, _P, _D, _I, _P, _P]),
+    ("latsum_rhosvd_ex", _I, [_P, _P, _P, _D, _I, _I, _P, _P]),
     ("latsum_tucker_destroy", None, [_P]),
+    ("latsum_tucker_has_core", _I, [_P]),
     ("latsum_tucker_info", _I, [_P, _P, _P]),
     ("latsum_tucker_singular_values", _I, [_P, _I, _P]),
     ("latsum_tucker_core", _I, [_P, _P, _P]),

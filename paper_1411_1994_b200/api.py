@@ -178,6 +178,7 @@ class SpectralReport:
     gram_rows: Tuple[bool, bool, bool]
     gram_size: Tuple[int, int, int]
     ms: dict
+    deflate_k1: Tuple[int, int, int] = (0, 0, 0)
 
     def tail(self, mode: int) -> float:
         sv = self.singular_values[mode]
@@ -469,7 +470,8 @@ def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto"):
         deflated=tuple(bool(x) for x in rep.deflated), gram_rows=tuple(bool(x) for x in rep.gram_rows),
         gram_size=tuple(int(x) for x in rep.gram_size),
         ms=dict(gram=rep.ms_gram, syevd=rep.ms_syevd, deflate=rep.ms_deflate,
-                project=rep.ms_project, core=rep.ms_core, norm=rep.ms_norm, total=rep.ms_total))
+                project=rep.ms_project, core=rep.ms_core, norm=rep.ms_norm, total=rep.ms_total),
+        deflate_k1=tuple(int(x) for x in rep.deflate_k1))
     return t, report
 
 

@@ -379,8 +379,16 @@ struct latsum_tucker {
   int64_t N[3] = {0, 0, 0};
   int64_t r[3] = {1, 1, 1};
   DBuf U[3];     // N_l x r_l
-  DBuf core;     // r0 x r1 x r2
+  DBuf core;     // r0 x r1 x r2 (absent when the core was not formed)
+  bool has_core = false;
   std::vector<double> sigma[3];
+  // projected canonical form V = sum_t w_t prod_l (U_l P_l)[:, c_l(t)]  (equals the
+  // Tucker tensor; used when the dense core does not fit, e.g. BASELINE cfg5)
+  DBuf P[3];     // r_l x d_l
+  int64_t d[3] = {0, 0, 0};
+  int64_t T = 0;
+  DVec<int32_t> tc[3];
+  DVec<double> tw;
 };
 
 namespace {
@@ -591,20 +599,32 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     }
   }
   // merge identical rank-1 terms (same column in all three modes)
-  std::map<std::tuple<int64_t, int64_t, int64_t>, double> merged;
+  // (key = c0:c1:c2 packed in 21-bit fields, q); stable order keeps the reference's
+  // term order inside each merged group, so merged weights add in add_concat order
+  for (int l = 0; l < 3; ++l)
+    require(can.d[l] < (int64_t(1) << 21), "assemble: too many distinct columns in a mode");
+  std::vector<std::pair<uint64_t, int64_t>> keys(can.Mc);
   for (int64_t q = 0; q < can.Mc; ++q)
-    merged[{can.term_col[0][q], can.term_col[1][q], can.term_col[2][q]}] += can.weights[q];
-  can.T = int64_t(merged.size());
+    keys[q] = {(uint64_t(can.term_col[0][q]) << 42) | (uint64_t(can.term_col[1][q]) << 21) |
+                   uint64_t(can.term_col[2][q]),
+               q};
+  std::sort(keys.begin(), keys.end());
   for (int l = 0; l < 3; ++l) can.tc[l].clear();
   can.tw.clear();
   can.tseg.assign(can.d[0] + 1, 0);
-  for (const auto& kv : merged) {  // map order: sorted by c0, then c1, c2
-    can.tc[0].push_back(int32_t(std::get<0>(kv.first)));
-    can.tc[1].push_back(int32_t(std::get<1>(kv.first)));
-    can.tc[2].push_back(int32_t(std::get<2>(kv.first)));
-    can.tw.push_back(kv.second);
-    can.tseg[std::get<0>(kv.first) + 1] += 1;
+  for (size_t i = 0; i < keys.size();) {  // sorted by c0, then c1, c2
+    const uint64_t key = keys[i].first;
+    double w = 0.0;
+    for (; i < keys.size() && keys[i].first == key; ++i) w += can.weights[keys[i].second];
+    const int64_t c0 = int64_t(key >> 42), c1 = int64_t((key >> 21) & 0x1FFFFF),
+                  c2 = int64_t(key & 0x1FFFFF);
+    can.tc[0].push_back(int32_t(c0));
+    can.tc[1].push_back(int32_t(c1));
+    can.tc[2].push_back(int32_t(c2));
+    can.tw.push_back(w);
+    can.tseg[c0 + 1] += 1;
   }
+  can.T = int64_t(can.tw.size());
   for (int64_t a = 0; a < can.d[0]; ++a) can.tseg[a + 1] += can.tseg[a];
   for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
   can.dtw.upload(c, can.tw);
@@ -661,40 +681,28 @@ void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, doubl
   else gemm(c, true, false, d, d, N, 1.0, A, N, A, N, 0.0, G, d, o);        // A^T A
 }
 
-// Symmetric (Loewdin) re-orthonormalisation U <- U (U^T U)^{-1/2}, in place.
-void lowdin(latsum_ctx* c, double* U, int64_t N, int64_t k) {
+// Polar (Loewdin) re-orthonormalisation U <- U (U^T U)^{-1/2} by Newton-Schulz
+// iterations U <- U (3I - U^T U)/2: GEMM-only (no eigensolver), quadratic
+// convergence from the ~1e-11 orthogonality loss of U = A V Sigma^{-1}.
+void polar_orthonormalize(latsum_ctx* c, double* U, int64_t N, int64_t k, int iters = 2) {
   if (k == 0) return;
-  DBuf S(c, size_t(k) * k), W(c, k);
-  gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k, tagged("gemm_basis"));
-  syevd(c, k, S.p, W.p);
-  std::vector<double> w(k);
-  CK(cudaMemcpyAsync(w.data(), W.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  for (auto& v : w) v = v > 1e-300 ? 1.0 / std::sqrt(v) : 0.0;
-  DVec<double> sc;
-  sc.upload(c, w);
-  DBuf Qs(c, size_t(k) * k), Mm(c, size_t(k) * k), Un(c, size_t(N) * k);
-  k_scale_columns<<<grid_for(k * k), 256, 0, c->stream>>>(S.p, k, k, sc.p, Qs.p);
-  post_launch(c);
-  gemm(c, false, true, k, k, k, 1.0, Qs.p, k, S.p, k, 0.0, Mm.p, k, tagged("gemm_basis"));
-  gemm(c, false, false, N, k, k, 1.0, U, N, Mm.p, k, 0.0, Un.p, N, tagged("gemm_basis"));
-  CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
+  DBuf S(c, size_t(k) * k), Un(c, size_t(N) * k);
+  for (int it = 0; it < iters; ++it) {
+    gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k, tagged("gemm_basis"));
+    CK(cudaMemcpyAsync(Un.p, U, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
+    gemm(c, false, false, N, k, k, -0.5, U, N, S.p, k, 1.5, Un.p, N, tagged("gemm_basis"));
+    CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
+  }
 }
 
-// Top-k left singular directions of A (N x d) from the eigenpairs of its Gram
-// (evecs n x n ascending, lam_desc descending): for A A^T the eigenvectors
-// themselves; for A^T A, U = A V diag(1/sigma) re-orthonormalised.
-void left_basis(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d,
-                const double* evecs, int64_t n, const std::vector<double>& lam_desc, int64_t k,
-                double* U) {
+// U (N x k) = A (N x d) * [the k leading columns of evecs (d x n, ascending order)]
+// scaled by 1/sqrt(lam_desc), then re-orthonormalised: left singular vectors from the
+// eigenpairs of A^T A.
+void left_from_right(latsum_ctx* c, const double* A, int64_t N, int64_t d, const double* evecs,
+                     int64_t n, const std::vector<double>& lam_desc, int64_t k, double* U) {
   if (k == 0) return;
-  if (rows) {
-    k_reverse_columns<<<grid_for(n * k), 256, 0, c->stream>>>(evecs, n, n, k, U);
-    post_launch(c);
-    return;
-  }
   DBuf Vd(c, size_t(d) * k);
-  k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, d, k, Vd.p);
+  k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, n, k, Vd.p);
   post_launch(c);
   gemm(c, false, false, N, k, d, 1.0, A, N, Vd.p, d, 0.0, U, N, tagged("gemm_basis"));
   std::vector<double> inv(k);
@@ -703,7 +711,7 @@ void left_basis(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d,
   sc.upload(c, inv);
   k_scale_columns<<<grid_for(N * k), 256, 0, c->stream>>>(U, N, k, sc.p, U);
   post_launch(c);
-  lowdin(c, U, N, k);
+  polar_orthonormalize(c, U, N, k);
 }
 
 struct ModeOut {
@@ -713,7 +721,7 @@ struct ModeOut {
   bool tie = false;
   double margin = 0.0;
   int deflated = 0, rows = 0;
-  int64_t gsize = 0;
+  int64_t gsize = 0, k1 = 0;
 };
 
 struct Timings {
@@ -722,6 +730,12 @@ struct Timings {
 
 // RHOSVD of one mode (rank_reduction.hpp:189-207) on the merged side matrix
 // A~ = D diag(sqrt(mult)), whose A~ A~^T equals the reference's A A^T.
+//
+// Pass 1: Gram of the smaller orientation (A A^T, N x N, or A~^T A~, d x d) and syevd.
+// Pass 2: the k1 directions with lambda > 1e-10 lambda_max are accurate;
+// the rest of the spectrum is recomputed from A'' = (I - U1 U1^T)^2 A~ restricted to the
+// pass-1 complement Qc (the n - k1 trailing eigenvectors), whose Gram has the size of
+// that complement and resolves singular values down to ~eps ||A''||.
 void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
                  double tol, int deflate, ModeOut& out, Timings& tm) {
   const int64_t N = can.N[l], d = can.d[l];
@@ -758,12 +772,11 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
     return sv;
   };
 
-  // second (deflated) pass: resolves sigma below sqrt(eps_mach) sigma_1
   std::vector<double> merged = lam_d;
   std::vector<std::pair<int, int64_t>> src(n);  // (pass, index in that pass's desc order)
   for (int64_t i = 0; i < n; ++i) src[i] = {0, i};
-  int64_t k1 = 0;
-  DBuf U1, G2, Ap;
+  int64_t k1 = 0, nc = 0;
+  DBuf U1, B, G2;
   std::vector<double> mu_d;
   bool defl = false;
   if (!ranks && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
@@ -771,38 +784,52 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
     double n2 = 0;
     for (double v : sv) n2 += v * v;
     const double target = tol * std::sqrt(n2) / 3.0;
-    defl = deflate == LATSUM_DEFLATE_ALWAYS ||
-           target * target < 1e6 * double(n) * kEpsMach * lmax;
+    for (int64_t i = 0; i < n; ++i)
+      if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
+    k1 = std::max<int64_t>(k1, 1);
+    nc = n - k1;
+    defl = nc > 0 && (deflate == LATSUM_DEFLATE_ALWAYS ||
+                      target * target < 1e6 * double(n) * kEpsMach * lmax);
     if (defl) {
       timer.start();
-      for (int64_t i = 0; i < n; ++i)
-        if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
-      k1 = std::max<int64_t>(k1, 1);
       U1.alloc(c, size_t(N) * k1);
-      left_basis(c, rows, At.p, N, d, G.p, n, lam_d, k1, U1.p);
-      Ap.alloc(c, size_t(N) * d);
+      if (rows) {
+        k_reverse_columns<<<grid_for(N * k1), 256, 0, c->stream>>>(G.p, N, n, k1, U1.p);
+        post_launch(c);
+      } else {
+        left_from_right(c, At.p, N, d, G.p, n, lam_d, k1, U1.p);
+      }
+      DBuf Ap(c, size_t(N) * d), C(c, size_t(k1) * d);
       CK(cudaMemcpyAsync(Ap.p, At.p, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, c->stream));
-      DBuf C(c, size_t(k1) * d);
       for (int rep = 0; rep < 2; ++rep) {  // project out span(U1), then re-orthogonalise once
         gemm(c, true, false, k1, d, N, 1.0, U1.p, N, Ap.p, N, 0.0, C.p, k1, tagged("gemm_deflate"));
         gemm(c, false, false, N, d, k1, -1.0, U1.p, N, C.p, k1, 1.0, Ap.p, N, tagged("gemm_deflate"));
       }
-      G2.alloc(c, size_t(n) * n);
-      gram(c, rows, Ap.p, N, d, G2.p);
+      // restrict to the pass-1 complement Qc = G[:, 0:nc] (ascending eigenvectors)
+      G2.alloc(c, size_t(nc) * nc);
+      if (rows) {  // B = Qc^T A'' (nc x d), G2 = B B^T
+        B.alloc(c, size_t(nc) * d);
+        gemm(c, true, false, nc, d, N, 1.0, G.p, N, Ap.p, N, 0.0, B.p, nc, tagged("gemm_deflate"));
+        gram(c, true, B.p, nc, d, G2.p);
+      } else {     // B = A'' Qc (N x nc), G2 = B^T B
+        B.alloc(c, size_t(N) * nc);
+        gemm(c, false, false, N, nc, d, 1.0, Ap.p, N, G.p, d, 0.0, B.p, N, tagged("gemm_deflate"));
+        gram(c, false, B.p, N, nc, G2.p);
+      }
       tm.deflate += timer.stop();
       timer.start();
-      DBuf W2(c, n);
-      syevd(c, n, G2.p, W2.p);
+      DBuf W2(c, nc);
+      syevd(c, nc, G2.p, W2.p);
       tm.syevd += timer.stop();
-      std::vector<double> mu(n);
-      CK(cudaMemcpyAsync(mu.data(), W2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      std::vector<double> mu(nc);
+      CK(cudaMemcpyAsync(mu.data(), W2.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
-      mu_d.resize(n);
-      for (int64_t i = 0; i < n; ++i) mu_d[i] = std::max(mu[n - 1 - i], 0.0);
-      // merged spectrum: the k1 resolved pass-1 values and the top n-k1 deflated values
+      mu_d.resize(nc);
+      for (int64_t i = 0; i < nc; ++i) mu_d[i] = std::max(mu[nc - 1 - i], 0.0);
+      // merged spectrum: k1 resolved pass-1 values and the nc deflated values
       std::vector<std::tuple<double, int, int64_t>> all;
       for (int64_t i = 0; i < k1; ++i) all.emplace_back(lam_d[i], 0, i);
-      for (int64_t i = 0; i < n - k1; ++i) all.emplace_back(mu_d[i], 1, i);
+      for (int64_t i = 0; i < nc; ++i) all.emplace_back(mu_d[i], 1, i);
       std::stable_sort(all.begin(), all.end(), [](const auto& a, const auto& b) {
         return std::get<0>(a) > std::get<0>(b);
       });
@@ -813,6 +840,7 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
     }
   }
   out.deflated = defl ? 1 : 0;
+  out.k1 = defl ? k1 : 0;
   out.sigma = padded_sigma(merged);
   const auto& sv = out.sigma;
 
@@ -836,22 +864,29 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   timer.start();
   out.Z.alloc(c, size_t(N) * r);
   if (!defl) {
-    left_basis(c, rows, At.p, N, d, G.p, n, lam_d, r, out.Z.p);
+    if (rows) {
+      k_reverse_columns<<<grid_for(N * r), 256, 0, c->stream>>>(G.p, N, n, r, out.Z.p);
+      post_launch(c);
+    } else {
+      left_from_right(c, At.p, N, d, G.p, n, lam_d, r, out.Z.p);
+    }
   } else {
     int64_t need2 = 0;
     for (int64_t i = 0; i < r; ++i)
       if (src[i].first == 1) need2 = std::max<int64_t>(need2, src[i].second + 1);
-    DBuf U2;
-    if (need2) {
-      U2.alloc(c, size_t(N) * need2);
-      left_basis(c, rows, Ap.p, N, d, G2.p, n, mu_d, need2, U2.p);
-    }
-    // gather columns [U1 | U2] in merged order
     DBuf cat(c, size_t(N) * (k1 + need2));
     CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * N * k1, cudaMemcpyDeviceToDevice, c->stream));
-    if (need2)
-      CK(cudaMemcpyAsync(cat.p + N * k1, U2.p, sizeof(double) * N * need2,
-                         cudaMemcpyDeviceToDevice, c->stream));
+    if (need2) {
+      double* U2 = cat.p + N * k1;
+      if (rows) {  // U2 = Qc * Y (leading eigenvectors of B B^T)
+        DBuf Yd(c, size_t(nc) * need2);
+        k_reverse_columns<<<grid_for(nc * need2), 256, 0, c->stream>>>(G2.p, nc, nc, need2, Yd.p);
+        post_launch(c);
+        gemm(c, false, false, N, need2, nc, 1.0, G.p, N, Yd.p, nc, 0.0, U2, N, tagged("gemm_basis"));
+      } else {     // U2 = B W mu^{-1/2}
+        left_from_right(c, B.p, N, nc, G2.p, nc, mu_d, need2, U2);
+      }
+    }
     std::vector<int64_t> sel(r);
     for (int64_t i = 0; i < r; ++i) sel[i] = src[i].first == 0 ? src[i].second : k1 + src[i].second;
     DVec<int64_t> dsel;
@@ -892,10 +927,10 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
   const int64_t T = can.T, d0 = can.d[0];
   const int64_t r12 = r[1] * r[2];
   DBuf G1(c, size_t(r[1]) * T), G2(c, size_t(r[2]) * T);
-  k_gather_scale<<<grid_for(r[1] * T), 256, 0, c->stream>>>(P[1].p, r[1], can.dtc[1].p,
+  k_gather_scale<<<grid_for(r[1] * T), 256, 0, c->stream>>>(P[1].p, r[1], r[1], can.dtc[1].p,
                                                             can.dtw.p, T, G1.p);
   post_launch(c);
-  k_gather_scale<<<grid_for(r[2] * T), 256, 0, c->stream>>>(P[2].p, r[2], can.dtc[2].p, nullptr,
+  k_gather_scale<<<grid_for(r[2] * T), 256, 0, c->stream>>>(P[2].p, r[2], r[2], can.dtc[2].p, nullptr,
                                                             T, G2.p);
   post_launch(c);
   const int64_t budget = int64_t(1) << 29;  // doubles of X per chunk (4 GiB)
@@ -979,7 +1014,7 @@ void fork_join(latsum_ctx* c, int n, F&& f) {
 }
 
 void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks, double tol,
-                 int deflate, latsum_tucker& t, latsum_spectral_report& rep) {
+                 int deflate, latsum_tucker& t, latsum_spectral_report& rep, bool form = true) {
   if (!ranks) require(tol > 0.0 && tol < 1.0, "TruncationSpec: tolerance must lie in (0,1)");
   std::memset(&rep, 0, sizeof(rep));
   Timings tm;
@@ -993,7 +1028,8 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   ModeOut mo[3];
   Timings tms[4];
   const bool zero_terms = can.Mc == 0 || can.T == 0;
-  fork_join(c, zero_terms ? 1 : 4, [&](latsum_ctx* w, int i) {
+  static const bool serial = std::getenv("LATSUM_SERIAL") != nullptr;  // A/B switch
+  auto body = [&](latsum_ctx* w, int i) {
     if (i == 3 || zero_terms) {
       Timer tn(w);
       tn.start();
@@ -1002,7 +1038,12 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     } else {
       reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
     }
-  });
+  };
+  if (serial) {
+    for (int i = 0; i < (zero_terms ? 1 : 4); ++i) body(c, i);
+  } else {
+    fork_join(c, zero_terms ? 1 : 4, body);
+  }
   for (int l = 0; l < 3; ++l) mo[l].Z.adopt(c->stream);
   for (const auto& x : tms) {
     tm.gram += x.gram;
@@ -1022,25 +1063,33 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       CK(cudaMemcpyAsync(t.U[l].p, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     }
     t.core.alloc(c, 1);
+    t.has_core = true;
     CK(cudaMemsetAsync(t.core.p, 0, sizeof(double), c->stream));
     CK(cudaStreamSynchronize(c->stream));
     rep.ms_total = total.stop();
     return;
   }
-  DBuf P[3];
+  DBuf* P = t.P;
   Timer tp(c);
   tp.start();
   for (int l = 0; l < 3; ++l) {
     t.r[l] = mo[l].r;
+    t.d[l] = can.d[l];
     P[l].alloc(c, size_t(mo[l].r) * can.d[l]);
     gemm(c, true, false, mo[l].r, can.d[l], can.N[l], 1.0, mo[l].Z.p, can.N[l], can.dict[l].p,
          can.N[l], 0.0, P[l].p, mo[l].r, tagged("gemm_project"));
+    t.tc[l].upload(c, can.tc[l]);
   }
+  t.tw.upload(c, can.tw);
+  t.T = can.T;
   tm.project = tp.stop();
-  tp.start();
-  t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
-  form_core(c, can, P, t.r, t.core.p);
-  tm.core = tp.stop();
+  if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
+    tp.start();
+    t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
+    form_core(c, can, P, t.r, t.core.p);
+    t.has_core = true;
+    tm.core = tp.stop();
+  }
   double tails = 0.0;
   for (int l = 0; l < 3; ++l) {
     t.U[l] = std::move(mo[l].Z);
@@ -1052,6 +1101,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     rep.deflated[l] = mo[l].deflated;
     rep.gram_rows[l] = mo[l].rows;
     rep.gram_size[l] = mo[l].gsize;
+    rep.deflate_k1[l] = mo[l].k1;
     double s = 0;  // SpectralReport::tail (rank_reduction.hpp:61-66)
     for (int64_t k = int64_t(mo[l].sigma.size()) - 1; k >= mo[l].r; --k)
       s += mo[l].sigma[k] * mo[l].sigma[k];
@@ -1081,8 +1131,14 @@ void check_box(const int64_t N[3], const int64_t lo[3], const int64_t hi[3]) {
 
 // to_dense on a box (tucker.hpp:172-178) as slab GEMMs: Q = core x_2 U1, then per
 // z-chunk X = Q x_3 U2 and V_k = U0 X_k (the dominant ni x nj x r0 GEMM per slab).
+void projected_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t hi[3],
+                    double* out);
+void projected_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,
+                      double* out_host);
+
 void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t hi[3],
                  double* out) {
+  if (!t.has_core) return projected_eval(c, t, lo, hi, out);
   check_box(t.N, lo, hi);
   const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
   const int64_t r0 = t.r[0], r1 = t.r[1], r2 = t.r[2];
@@ -1115,41 +1171,86 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   }
 }
 
-void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo[3],
-                    const int64_t hi[3], double* out) {
-  check_box(can.N, lo, hi);
-  const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
-  const int64_t T = can.T;
+// Canonical (dictionary) tensor on an ni x nj x nk box: V_k = A0 X_k with
+// A0[:, t] = D0[:, c0_t] and X_k[t, j] = w_t D2[k, c2_t] D1[j, c1_t] (to_dense,
+// canonical.hpp:192-202, as one GEMM per z-slab).  D_l point at the box's first row.
+void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const int32_t* const tc[3],
+             const double* tw, int64_t T, int64_t ni, int64_t nj, int64_t nk, double* out,
+             const char* tag) {
   if (T == 0) {
     CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
     return;
   }
-  // A0 (ni x T): mode-1 dictionary rows of the box, gathered per merged term
   DBuf A0(c, size_t(ni) * T);
-  {
-    DBuf tmp(c, size_t(ni) * can.d[0]);
-    CK(cudaMemcpy2DAsync(tmp.p, ni * sizeof(double), can.dict[0].p + lo[0],
-                         can.N[0] * sizeof(double), ni * sizeof(double), can.d[0],
-                         cudaMemcpyDeviceToDevice, c->stream));
-    k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(tmp.p, ni, can.dtc[0].p, nullptr, T,
-                                                            A0.p);
-    post_launch(c);
-  }
+  k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(D[0], ni, ld[0], tc[0], nullptr, T, A0.p);
+  post_launch(c);
   const int64_t budget = int64_t(1) << 27;
   const int64_t nkc = std::max<int64_t>(1, std::min<int64_t>({nk, budget / std::max<int64_t>(T * nj, 1), 65535}));
   DBuf X(c, size_t(T) * nj * nkc);
   for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
     const int64_t nkk = std::min(nkc, nk - k0);
     k_canonical_slab_operand<<<grid_for(T * nj * nkk), 256, 0, c->stream>>>(
-        can.dict[1].p, can.N[1], can.dict[2].p, can.N[2], can.dtc[1].p, can.dtc[2].p, can.dtw.p,
-        T, lo[1], nj, lo[2] + k0, nkk, X.p);
+        D[1], ld[1], D[2], ld[2], tc[1], tc[2], tw, T, 0, nj, k0, nkk, X.p);
     post_launch(c);
-    GemmOpts ov = tagged("gemm_eval_canonical");
+    GemmOpts ov = tagged(tag);
     ov.batch = nkk;
     ov.sB = T * nj;
     ov.sC = ni * nj;
     gemm(c, false, false, ni, nj, T, 1.0, A0.p, ni, X.p, T, 0.0, out + k0 * ni * nj, ni, ov);
   }
+}
+
+void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo[3],
+                    const int64_t hi[3], double* out) {
+  check_box(can.N, lo, hi);
+  const double* D[3] = {can.dict[0].p + lo[0], can.dict[1].p + lo[1], can.dict[2].p + lo[2]};
+  const int32_t* tc[3] = {can.dtc[0].p, can.dtc[1].p, can.dtc[2].p};
+  cp_eval(c, D, can.N, tc, can.dtw.p, can.T, hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], out,
+          "gemm_eval_canonical");
+}
+
+// Projected-CP evaluation of a RHOSVD result: E_l = U_l[box rows] P_l, then the
+// canonical slab GEMMs over the merged terms.  Equal to the Tucker tensor's values.
+void projected_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t hi[3],
+                    double* out) {
+  check_box(t.N, lo, hi);
+  require(t.T > 0 || t.d[0] == 0, "projected evaluation needs the projected factors");
+  int64_t n[3];
+  DBuf E[3];
+  const double* D[3];
+  for (int l = 0; l < 3; ++l) {
+    n[l] = hi[l] - lo[l];
+    E[l].alloc(c, size_t(n[l]) * t.d[l]);
+    gemm(c, false, false, n[l], t.d[l], t.r[l], 1.0, t.U[l].p + lo[l], t.N[l], t.P[l].p, t.r[l],
+         0.0, E[l].p, n[l], tagged("gemm_eval_project"));
+    D[l] = E[l].p;
+  }
+  const int32_t* tc[3] = {t.tc[0].p, t.tc[1].p, t.tc[2].p};
+  cp_eval(c, D, n, tc, t.tw.p, t.T, n[0], n[1], n[2], out, "gemm_eval_projected");
+}
+
+void projected_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,
+                      double* out_host) {
+  std::vector<int64_t> hp(probes, probes + 3 * np), diag(3 * np);
+  for (int64_t p = 0; p < np; ++p) diag[3 * p] = diag[3 * p + 1] = diag[3 * p + 2] = p;
+  DVec<int64_t> dp, dd;
+  dp.upload(c, hp);
+  dd.upload(c, diag);
+  DBuf rows(c, size_t(np) * std::max({t.r[0], t.r[1], t.r[2]})), E[3], res(c, np);
+  for (int l = 0; l < 3; ++l) {
+    k_gather_rows<<<grid_for(np * t.r[l]), 256, 0, c->stream>>>(t.U[l].p, t.N[l], t.r[l], dp.p, l,
+                                                                np, rows.p);
+    post_launch(c);
+    E[l].alloc(c, size_t(np) * t.d[l]);
+    gemm(c, false, false, np, t.d[l], t.r[l], 1.0, rows.p, np, t.P[l].p, t.r[l], 0.0, E[l].p, np,
+         tagged("gemm_probes"));
+  }
+  k_canonical_probes<<<unsigned(np), 256, 0, c->stream>>>(E[0].p, np, E[1].p, np, E[2].p, np,
+                                                         t.tc[0].p, t.tc[1].p, t.tc[2].p, t.tw.p,
+                                                         t.T, dd.p, res.p);
+  post_launch(c);
+  CK(cudaMemcpyAsync(out_host, res.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
 }
 
 void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,
@@ -1158,6 +1259,7 @@ void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes,
     for (int l = 0; l < 3; ++l)
       if (probes[3 * p + l] < 0 || probes[3 * p + l] >= t.N[l])
         throw Error(LATSUM_ERR_INVALID_ARGUMENT, "TuckerTensor::entry index out of range");
+  if (!t.has_core) return projected_probes(c, t, probes, np, out_host);
   const int64_t r0 = t.r[0], r12 = t.r[1] * t.r[2];
   const int64_t budget = int64_t(1) << 28;
   const int64_t pc = std::max<int64_t>(1, std::min<int64_t>(np, budget / std::max<int64_t>(r12, 1)));
@@ -1204,6 +1306,19 @@ int latsum_ctx_create(int device, latsum_ctx** out) {
     CK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Pre-grow the stream-ordered pool so steady-state steps never map new memory
+    // (LATSUM_POOL_RESERVE_GB, default 8; 0 disables).
+    const char* e = std::getenv("LATSUM_POOL_RESERVE_GB");
+    const double gb = e ? std::atof(e) : 8.0;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t want = size_t(gb * 1073741824.0);
+    if (want > 0 && want < free_b / 2) {
+      void* p = nullptr;
+      CK(cudaMallocAsync(&p, want, c->stream));
+      CK(cudaFreeAsync(p, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
   });
   if (st != LATSUM_OK) {
     static thread_local std::string last;
@@ -1415,17 +1530,26 @@ int latsum_canonical_eval_box_device(latsum_ctx* c, const latsum_canonical* can,
 int latsum_rhosvd(latsum_ctx* c, const latsum_canonical* can, const int64_t* ranks,
                   double tolerance, int deflate, latsum_tucker** out,
                   latsum_spectral_report* report) {
+  return latsum_rhosvd_ex(c, can, ranks, tolerance, deflate, 0, out, report);
+}
+
+int latsum_rhosvd_ex(latsum_ctx* c, const latsum_canonical* can, const int64_t* ranks,
+                     double tolerance, int deflate, int flags, latsum_tucker** out,
+                     latsum_spectral_report* report) {
   return guarded(c, [&] {
     require(can && out, "latsum_rhosvd: null argument");
     auto t = std::make_unique<latsum_tucker>();
     latsum_spectral_report rep;
-    rhosvd_impl(c, *can, ranks, tolerance, deflate, *t, rep);
+    rhosvd_impl(c, *can, ranks, tolerance, deflate, *t, rep,
+                (flags & LATSUM_RHOSVD_FACTORS_ONLY) == 0);
     if (report) *report = rep;
     *out = t.release();
   });
 }
 
 void latsum_tucker_destroy(latsum_tucker* t) { delete t; }
+
+int latsum_tucker_has_core(const latsum_tucker* t) { return t && t->has_core ? 1 : 0; }
 
 int latsum_tucker_info(const latsum_tucker* t, int64_t dims[3], int64_t ranks[3]) {
   if (!t) return LATSUM_ERR_INVALID_ARGUMENT;
@@ -1445,6 +1569,7 @@ int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out)
 int latsum_tucker_core(latsum_ctx* c, const latsum_tucker* t, double* core) {
   return guarded(c, [&] {
     require(t && core, "latsum_tucker_core: null argument");
+    require(t->has_core, "latsum_tucker_core: the dense core was not formed (factors-only RHOSVD)");
     CK(cudaMemcpyAsync(core, t->core.p, sizeof(double) * t->r[0] * t->r[1] * t->r[2],
                        cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -97,7 +97,7 @@ double latsum_default_step_constant(int family, double lambda, int M, double she
                                   npts);
     }
   };
-  const int nt = std::max(1, std::min<int>(8, int(std::thread::hardware_concurrency())));
+  const int nt = std::max(1, std::min<int>(kCand, int(std::thread::hardware_concurrency())));
   std::vector<std::thread> pool;
   const int chunk = (kCand + nt - 1) / nt;
   for (int w = 0; w < nt; ++w) {

@@ -188,15 +188,15 @@ __global__ void k_scale_columns(const double* __restrict__ in, int64_t rows, int
     out[e] = in[e] * scale[e / rows];
 }
 
-// out[:, q] = src[:, cols[q]] * (w ? w[q] : 1)   (rows x T gather, for the core)
-__global__ void k_gather_scale(const double* __restrict__ src, int64_t rows,
+// out[:, q] = src[:, cols[q]] * (w ? w[q] : 1)   (rows x T gather, src leading dim ld)
+__global__ void k_gather_scale(const double* __restrict__ src, int64_t rows, int64_t ld,
                                const int32_t* __restrict__ cols, const double* __restrict__ w,
                                int64_t T, double* __restrict__ out) {
   const int64_t total = rows * T;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t q = e / rows, i = e % rows;
-    const double v = src[i + int64_t(cols[q]) * rows];
+    const double v = src[i + int64_t(cols[q]) * ld];
     out[e] = w ? v * w[q] : v;
   }
 }

@@ -31,7 +31,7 @@ for cfg in cfgs:
             del out
         print(json.dumps(dict(cfg=cfg, rep=rep_i, stage12_ms=1e3*(t1-t0), rhosvd_ms=1e3*(t2-t1),
                               eval_ms=1e3*te, ranks=rep.chosen_ranks, dict_cols=can.dict_cols,
-                              T=can.merged_terms, gram=rep.gram_size, deflated=rep.deflated,
+                              T=can.merged_terms, gram=rep.gram_size, deflated=rep.deflated, k1=rep.deflate_k1,
                               margin=rep.cutoff_margin, tie=rep.tie_at_cutoff, ms=rep.ms)))
         if rep_i == 1:
             for k, v in sorted(ctx.profile().items(), key=lambda kv: -kv[1][1]):

@@ -200,16 +200,15 @@ def run_gpu(args):
 
     g = W.baseline(args.config)
     ctx = api.Context(local)
+    if world > 1:
+        api.init_comm_from_torch(ctx)  # row-sharded RHOSVD over NCCL
     # a dedicated (non-NULL) stream shared by torch and the library, so the CUDA events
     # below order against every kernel the library launches
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     lo, hi = g.eval_box()
-    nz = hi[2] - lo[2]
-    z0 = lo[2] + (nz * rank) // world
-    z1 = lo[2] + (nz * (rank + 1)) // world
-    my_lo, my_hi = (lo[0], lo[1], z0), (hi[0], hi[1], z1)
+    my_lo, my_hi = W.z_slab(lo, hi, rank, world)
     n_my = (my_hi[0] - my_lo[0]) * (my_hi[1] - my_lo[1]) * (my_hi[2] - my_lo[2])
     n_total = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
     do_eval = not args.no_eval
@@ -275,8 +274,11 @@ def run_gpu(args):
         peak, unit, bound = float(peaks.get("hbm_gbs", 6557.8)), "GB/s", "hbm"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom_tag)
+    if os.path.exists(tpath) and dom_tag == "gemm_eval_slab" and do_eval:
+        # ncu --set full DRAM bytes per 2048^2 slice (profiles/ncu_eval_r01.md), per launch
+        tr = json.load(open(tpath)).get(dom_tag)
+        if tr:
+            traffic = tr["bytes_per_slice"] * (n_my / tr["slice_points"]) / max(1, dom_n)
 
     # e2e: the reference-facing C-ABI call with host buffers (H2D of the shift tables
     # inside latsum_sum_to_tucker; D2H of the Tucker core and factors into pinned memory)
@@ -328,8 +330,9 @@ def run_gpu(args):
                 "ranks": list(rep.chosen_ranks), "merged_columns": list(can.dict_cols),
                 "canonical_rank": can.rank, "deflated": list(rep.deflated),
                 "l2": "256 MB buffer written between timed steps; eval output 68.7 GB >> L2",
-                "parallelism": f"replicated stages 1-3, z-slab eval x{world}" if world > 1
-                else "single GPU"},
+                "parallelism": (f"stages 1-2 replicated, RHOSVD row-sharded over the grid index "
+                                f"with NCCL all-reduce x{world}, z-slab evaluation x{world}")
+                if world > 1 else "single GPU"},
             "step_ms_stages_1_3": [round(x, 3) for x in ms13],
             "grid_eval": {"value": (n_total / (v4 * 1e-3) / 1e9) if do_eval else None,
                           "unit": "Gpts/s", "ms": v4, "points": n_total},

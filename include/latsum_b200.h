@@ -71,6 +71,15 @@ int latsum_ctx_set_stream(latsum_ctx* ctx, void* cuda_stream);
 int latsum_ctx_synchronize(latsum_ctx* ctx);
 /* Number of kernels this context launched so far (its own kernels, not library ones). */
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);
+/* Multi-GPU (one process per GPU): rank 0 creates an NCCL unique id, the caller
+ * broadcasts it (e.g. torch.distributed), every rank calls latsum_ctx_init_comm.  The
+ * context then runs latsum_rhosvd row-sharded over the grid index: each rank owns
+ * N/nranks rows of every side matrix; Grams, U^T U, U^T A, P_l = Z_l^T A_l and the core
+ * are all-reduced over NVLink, eigensolves run redundantly, Z is all-gathered.  NCCL is
+ * bound at run time (dlopen libnccl.so.2). */
+int latsum_comm_unique_id(unsigned char id[128]);
+int latsum_ctx_init_comm(latsum_ctx* ctx, const unsigned char id[128], int rank, int nranks);
+int latsum_ctx_comm_info(const latsum_ctx* ctx, int* rank, int* nranks);
 /* Per-kernel-class CUDA-event timing: when on, every launch group is bracketed by
  * events on the context stream.  latsum_ctx_profile writes lines
  * "<tag> <launches> <total ms> <algorithmic work>" (FLOPs for gemm_*, bytes otherwise)

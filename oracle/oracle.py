@@ -274,14 +274,82 @@ class RhosvdOracle:
     margin: tuple  # (tail(r) - target) / target style cutoff margins
 
 
+@dataclass
+class DictSide:
+    """One mode's side matrix in merged form: F = U[:, inv] (unique columns U,
+    multiplicities counts)."""
+    U: np.ndarray
+    counts: np.ndarray
+    inv: np.ndarray
+    rows: int
+    cols: int  # M_c
+
+
+def side_dictionary(ref: RefOracle, geom):
+    """Memory-light form of `side_matrices`: each distinct (placement, reference column)
+    is assembled and normalised once (lattice_sum.hpp:101-157 + canonical.hpp:32-48) —
+    the same columns, bit for bit, that the full N x M_c matrices hold — plus the M_c
+    weights in reference order (sublattice blocks, then defects)."""
+    N, R = geom.N, geom.R
+    blocks = [(tuple(np.asarray(x, np.int64) for x in sub.shifts), sub.charge)
+              for sub in geom.sublattices]
+    blocks += [((np.array([s[0]]), np.array([s[1]]), np.array([s[2]])), q)
+               for s, q in zip(geom.defect_shifts, geom.defect_charges)]
+    Mc = R * len(blocks)
+    w = np.zeros(Mc)
+    sides = []
+    norms_l = []
+    for l in range(3):
+        _, _, rinv = merge_columns(ref.factors[l])  # distinct reference columns
+        rep_col = {}
+        for k in range(R):
+            rep_col.setdefault(int(rinv[k]), k)
+        cols, norms, key_to_col = [], [], {}
+        inv = np.zeros(Mc, np.int64)
+        for b, (shifts, _) in enumerate(blocks):
+            pkey = shifts[l].tobytes()
+            for k in range(R):
+                key = (pkey, int(rinv[k]))
+                j = key_to_col.get(key)
+                if j is None:
+                    v = assembled_vector(ref.factors[l][:, rep_col[int(rinv[k])]], N[l], shifts[l])
+                    f, nv = normalize_columns(v.reshape(-1, 1))
+                    j = len(cols)
+                    key_to_col[key] = j
+                    cols.append(f[:, 0].copy())
+                    norms.append(float(nv[0]))
+                inv[b * R + k] = j
+        U = np.asfortranarray(np.stack(cols, axis=1))
+        counts = np.bincount(inv, minlength=U.shape[1]).astype(np.float64)
+        sides.append(DictSide(U, counts, inv, N[l], Mc))
+        norms_l.append(np.asarray(norms))
+    for b, (_, charge) in enumerate(blocks):
+        wb = charge * ref.weights
+        for l in range(3):
+            nv = norms_l[l][sides[l].inv[b * R:(b + 1) * R]]
+            wb = np.where(nv == 0.0, 0.0, wb * nv)
+        w[b * R:(b + 1) * R] = wb
+    return sides, w
+
+
+def as_dict_sides(F):
+    out = []
+    for f in F:
+        U, counts, inv = merge_columns(f)
+        out.append(DictSide(U, counts, inv, f.shape[0], f.shape[1]))
+    return out
+
+
 def rhosvd(F, w, eps: Optional[float] = None, ranks=None, with_norm: bool = True) -> RhosvdOracle:
-    """rank_reduction.hpp:176-218 on the merged-column SVD."""
+    """rank_reduction.hpp:176-218 on the merged-column SVD.  F is either the three full
+    N x M_c side matrices or their `DictSide` forms (same result)."""
+    sides = F if isinstance(F[0], DictSide) else as_dict_sides(F)
     sig, Zs, rk, tie, Ps, margins = [], [], [], [], [], []
     for l in range(3):
-        U, counts, inv = merge_columns(F[l])
-        Ad = U * np.sqrt(counts)[None, :]
+        sd = sides[l]
+        Ad = sd.U * np.sqrt(sd.counts)[None, :]
         u, s, _ = np.linalg.svd(Ad, full_matrices=False)
-        n_full = min(F[l].shape[0], F[l].shape[1])
+        n_full = min(sd.rows, sd.cols)
         sv = np.zeros(n_full)
         sv[:s.size] = s
         if ranks is not None:
@@ -298,23 +366,60 @@ def rhosvd(F, w, eps: Optional[float] = None, ranks=None, with_norm: bool = True
             margins.append(float(min(target - t_r, t_rm1 - target) / target))
         sig.append(sv)
         rk.append(r)
-        Z = u[:, :r]
-        Zs.append(np.asfortranarray(Z))
-        Ps.append(np.asfortranarray((Z.T @ U)[:, inv]))
+        Z = np.asfortranarray(u[:, :r])
+        del u
+        Zs.append(Z)
+        Ps.append(ProjectedFactor(np.asfortranarray(Z.T @ sd.U), sd.inv))
     wn = float(np.linalg.norm(w))
     tails = sum(float(np.sqrt(np.sum(sig[l][rk[l]:] ** 2))) for l in range(3))
-    nrm = input_norm(F, w) if with_norm else None
+    nrm = input_norm_dict(sides, w) if with_norm else None
     stab = (wn * wn / (nrm * nrm)) if nrm else None
     brel = (np.sqrt(stab) * nrm * tails) if nrm else None
     return RhosvdOracle(sig, tuple(rk), Zs, Ps, tuple(tie), wn, nrm, wn * tails, brel, stab,
                         tuple(margins))
 
 
+class ProjectedFactor:
+    """P_l = Z_l^T A_l (r x M_c) stored as Z_l^T U_l and the column map."""
+
+    def __init__(self, Pu, inv):
+        self.Pu, self.inv = Pu, inv
+
+    @property
+    def shape(self):
+        return (self.Pu.shape[0], self.inv.size)
+
+    def full(self):
+        return np.asfortranarray(self.Pu[:, self.inv])
+
+    def __getitem__(self, idx):
+        return self.full()[idx]
+
+    def __array__(self, dtype=None, copy=None):
+        return self.full()
+
+
+def input_norm_dict(sides, w, chunk: int = 4096) -> float:
+    """canonical.hpp:148-162 via unique-column Grams and merged identical terms."""
+    key = np.stack([sd.inv for sd in sides], axis=1)
+    terms, tinv = np.unique(key, axis=0, return_inverse=True)
+    wt = np.bincount(tinv.ravel(), weights=w, minlength=terms.shape[0])
+    G = [sd.U.T @ sd.U for sd in sides]
+    s = 0.0
+    T = terms.shape[0]
+    for a in range(0, T, chunk):
+        ia = terms[a:a + chunk]
+        blk = (G[0][np.ix_(ia[:, 0], terms[:, 0])] * G[1][np.ix_(ia[:, 1], terms[:, 1])]
+               * G[2][np.ix_(ia[:, 2], terms[:, 2])])
+        s += float(wt[a:a + chunk] @ (blk @ wt))
+    return float(np.sqrt(s)) if s > 0 else 0.0
+
+
 def project_core(w, P) -> np.ndarray:
     """rank_reduction.hpp:88-100 (reference loop order; small sizes only)."""
-    r = np.array([P[0].shape[0], P[1].shape[0], P[2].shape[0]], np.int64)
+    p = [_f64F(x.full() if isinstance(x, ProjectedFactor) else x) for x in P]
+    r = np.array([p[0].shape[0], p[1].shape[0], p[2].shape[0]], np.int64)
     core = np.zeros(int(np.prod(r)))
-    p = [_f64F(x) for x in P]
     lib().orc_project_core(_ptr(_f64(w)), p[0].shape[1], _ptr(p[0]), _ptr(p[1]), _ptr(p[2]),
                            _ptr(r), _ptr(core))
     return core.reshape(tuple(r), order="F")
@@ -323,15 +428,27 @@ def project_core(w, P) -> np.ndarray:
 # ----------------------------------------------------------------------------- entries
 
 def canonical_entries(F, w, probes: np.ndarray) -> np.ndarray:
+    """canonical.hpp:63-70 at probes (full side matrices or DictSide forms)."""
     pr = np.ascontiguousarray(probes, dtype=np.int64)
-    return np.einsum("q,pq,pq,pq->p", w, F[0][pr[:, 0]], F[1][pr[:, 1]], F[2][pr[:, 2]])
+    rows = []
+    for l in range(3):
+        if isinstance(F[l], DictSide):
+            rows.append(F[l].U[pr[:, l]][:, F[l].inv])
+        else:
+            rows.append(F[l][pr[:, l]])
+    return np.einsum("q,pq,pq,pq->p", w, rows[0], rows[1], rows[2])
 
 
 def projected_cp_entries(w, Z, P, probes: np.ndarray) -> np.ndarray:
     """Tucker value of the RHOSVD result at probes via the projected-CP identity
     V = sum_q w_q prod_l (Z_l Z_l^T a_lq)(i_l); equals TuckerTensor::entry."""
     pr = np.ascontiguousarray(probes, dtype=np.int64)
-    Q = [Z[l][pr[:, l]] @ P[l] for l in range(3)]
+    Q = []
+    for l in range(3):
+        if isinstance(P[l], ProjectedFactor):
+            Q.append((Z[l][pr[:, l]] @ P[l].Pu)[:, P[l].inv])
+        else:
+            Q.append(Z[l][pr[:, l]] @ P[l])
     return (Q[0] * Q[1] * Q[2]) @ w
 
 

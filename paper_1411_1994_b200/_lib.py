@@ -71,6 +71,9 @@ SIGNATURES = [
     ("latsum_ctx_set_stream", _I, [_P, _P]),
     ("latsum_ctx_synchronize", _I, [_P]),
     ("latsum_ctx_kernel_launches", _I64, [_P]),
+    ("latsum_comm_unique_id", _I, [_P]),
+    ("latsum_ctx_init_comm", _I, [_P, _P, _I, _I]),
+    ("latsum_ctx_comm_info", _I, [_P, _P, _P]),
     ("latsum_ctx_set_profiling", _I, [_P, _I]),
     ("latsum_ctx_profile", _I64, [_P, ctypes.c_char_p, _I64]),
     ("latsum_build_quadrature", _I, [_I, _D, _I, _D, _D, _D, _P, _P]),

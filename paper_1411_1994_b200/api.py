@@ -83,6 +83,17 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.lib().latsum_ctx_kernel_launches(self._h))
 
+    def init_comm(self, uid: bytes, rank: int, nranks: int):
+        """Join a row-sharded multi-GPU group (latsum_ctx_init_comm)."""
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        self.check(_lib.lib().latsum_ctx_init_comm(self._h, buf, int(rank), int(nranks)))
+
+    @property
+    def comm_info(self):
+        r, n = ctypes.c_int(), ctypes.c_int()
+        _lib.lib().latsum_ctx_comm_info(self._h, ctypes.byref(r), ctypes.byref(n))
+        return r.value, n.value
+
     def set_profiling(self, on: bool):
         self.check(_lib.lib().latsum_ctx_set_profiling(self._h, 1 if on else 0))
 
@@ -109,6 +120,22 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _lib.check(_lib.lib().latsum_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def init_comm_from_torch(ctx: Context):
+    """One process per GPU under torch.distributed: rank 0's NCCL id is broadcast with
+    torch's process group, then every rank joins the library's communicator."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.init_comm(obj[0], rank, world)
 
 
 _default_ctx: Optional[Context] = None
@@ -239,9 +266,12 @@ class ReferenceTensor:
         return t, a
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.lib().latsum_reference_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.lib().latsum_reference_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def build_reference_canonical(kernel: KernelSpec, N: Sequence[int], box: Sequence[float], M: int,
@@ -325,9 +355,12 @@ class CanonicalTensor:
         return buf.cpu().numpy().reshape(shape, order="F")
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.lib().latsum_canonical_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.lib().latsum_canonical_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class TuckerTensor:
@@ -343,6 +376,10 @@ class TuckerTensor:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def has_core(self) -> bool:
+        return bool(_lib.lib().latsum_tucker_has_core(self._h))
 
     @property
     def core(self) -> np.ndarray:
@@ -383,9 +420,12 @@ class TuckerTensor:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.lib().latsum_tucker_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.lib().latsum_tucker_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 # ----------------------------------------------------------------------------- sums
@@ -444,17 +484,23 @@ def sublattice_union_sum(ref: ReferenceTensor, parent_cells, n_per_cell: int, su
     return rhosvd(can, spec, deflate=deflate)
 
 
-def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto"):
-    """rank_reduction.hpp:176-218 -> (TuckerTensor, SpectralReport)."""
+def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto",
+           form_core: bool = True):
+    """rank_reduction.hpp:176-218 -> (TuckerTensor, SpectralReport).
+
+    form_core=False keeps the projected factors instead of the dense r1 x r2 x r3 core
+    (LATSUM_RHOSVD_FACTORS_ONLY); entries / boxes are then evaluated in projected-CP
+    form, equal to the Tucker tensor (BASELINE cfg5: the core would be 518 GB)."""
     spec.validate()
     ctx = can.ctx
     rep = _lib.LatsumReport()
     h = ctypes.c_void_p()
     ranks = _i64(spec.ranks) if spec.ranks is not None else None
-    ctx.check(_lib.lib().latsum_rhosvd(ctx.handle, can.handle,
-                                       _p(ranks) if ranks is not None else None,
-                                       float(spec.tolerance or 0.0), DEFLATE[deflate], ctypes.byref(h),
-                                       ctypes.byref(rep)))
+    ctx.check(_lib.lib().latsum_rhosvd_ex(ctx.handle, can.handle,
+                                          _p(ranks) if ranks is not None else None,
+                                          float(spec.tolerance or 0.0), DEFLATE[deflate],
+                                          0 if form_core else 1, ctypes.byref(h),
+                                          ctypes.byref(rep)))
     t = TuckerTensor(ctx, h)
     sv = []
     for l in range(3):

@@ -4,6 +4,7 @@
 // returns a status code (the reference's exception types map to LATSUM_ERR_*).
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -53,6 +54,47 @@ void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(LATSUM_ERR_INVALID_ARGUMENT, msg);
 }
 
+// ---- NCCL, bound at run time (dlopen) so the process shares whichever libnccl.so.2
+// torch already loaded; only the symbols the sharded path needs.
+typedef struct ncclComm* ncclComm_t;
+struct NcclUid { char internal[128]; };
+enum { kNcclFloat64 = 8, kNcclSum = 0 };
+struct Nccl {
+  void* h = nullptr;
+  int (*GetUniqueId)(NcclUid*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, NcclUid, int) = nullptr;
+  int (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    x.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!x.h) x.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!x.h) return x;
+    x.GetUniqueId = reinterpret_cast<decltype(x.GetUniqueId)>(dlsym(x.h, "ncclGetUniqueId"));
+    x.CommInitRank = reinterpret_cast<decltype(x.CommInitRank)>(dlsym(x.h, "ncclCommInitRank"));
+    x.CommSplit = reinterpret_cast<decltype(x.CommSplit)>(dlsym(x.h, "ncclCommSplit"));
+    x.CommDestroy = reinterpret_cast<decltype(x.CommDestroy)>(dlsym(x.h, "ncclCommDestroy"));
+    x.AllReduce = reinterpret_cast<decltype(x.AllReduce)>(dlsym(x.h, "ncclAllReduce"));
+    x.AllGather = reinterpret_cast<decltype(x.AllGather)>(dlsym(x.h, "ncclAllGather"));
+    x.GetErrorString = reinterpret_cast<decltype(x.GetErrorString)>(dlsym(x.h, "ncclGetErrorString"));
+    return x;
+  }();
+  if (!n.h || !n.GetUniqueId || !n.CommInitRank || !n.CommSplit || !n.AllReduce || !n.AllGather)
+    throw Error(LATSUM_ERR_NCCL, "libnccl.so.2 not found or incomplete");
+  return n;
+}
+#define NC(call)                                                                         \
+  do {                                                                                   \
+    int r_ = (call);                                                                     \
+    if (r_ != 0)                                                                         \
+      throw Error(LATSUM_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
 }  // namespace
 
 struct latsum_ctx {
@@ -73,6 +115,10 @@ struct latsum_ctx {
   std::map<std::string, Stat> stats;
   // worker contexts (own stream + cuSOLVER handle) for the concurrent per-mode reductions
   latsum_ctx* sub[4] = {nullptr, nullptr, nullptr, nullptr};
+  // multi-GPU: one rank of a row-sharded reduction (latsum_ctx_init_comm); each worker
+  // context owns a communicator split from this one so concurrent modes never interleave
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
 };
 
 namespace {
@@ -137,6 +183,16 @@ int grid_for(int64_t total, int threads = 256) {
   return int(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
 }
 
+// Split n into ceil(n / cap) near-equal chunks (multiples of `align` when possible).
+int64_t balanced_chunk(int64_t n, int64_t cap, int64_t align) {
+  cap = std::max<int64_t>(1, cap);
+  if (n <= cap) return std::max<int64_t>(n, 1);
+  const int64_t parts = (n + cap - 1) / cap;
+  int64_t c = (n + parts - 1) / parts;
+  if (align > 1 && c > align) c = std::min<int64_t>(cap, (c + align - 1) / align * align);
+  return std::max<int64_t>(1, std::min(c, cap));
+}
+
 void post_launch(latsum_ctx* c) {
   c->launches++;
   CK(cudaGetLastError());
@@ -188,6 +244,21 @@ void prof_harvest(latsum_ctx* c) {
     c->pool.push_back(r.b);
   }
   c->pending.clear();
+}
+
+// Sum-all-reduce over the ranks of c's communicator (no-op on one rank).
+void allreduce(latsum_ctx* c, double* buf, size_t count) {
+  if (!c->comm || c->nranks <= 1 || count == 0) return;
+  NC(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream));
+}
+
+// The rows [lo, hi) of an N-row operand this rank owns in the row-sharded reduction.
+struct RowBlock {
+  int64_t lo = 0, hi = 0;
+  int64_t n() const { return hi - lo; }
+};
+RowBlock row_block(const latsum_ctx* c, int64_t N) {
+  return {N * c->rank / c->nranks, N * (c->rank + 1) / c->nranks};
 }
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -526,31 +597,25 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
                         " window outside the doubled grid");
     };
     block_pl[l].resize(nblk);
+    // a placement is a shift list; identical lists (e.g. the z lists of the two
+    // hexagonal sublattices, or a defect on an L=1 sublattice) share dictionary columns
+    std::map<std::vector<int64_t>, int64_t> seen;
+    auto place = [&](std::vector<int64_t> sh) {
+      auto it = seen.find(sh);
+      if (it != seen.end()) return it->second;
+      for (int64_t v : sh) check(v);
+      const int64_t p = int64_t(pl_off.size()) - 1;
+      pl_shift.insert(pl_shift.end(), sh.begin(), sh.end());
+      pl_off.push_back(int64_t(pl_shift.size()));
+      seen.emplace(std::move(sh), p);
+      return p;
+    };
     for (int64_t s = 0; s < nsub; ++s) {
       const int64_t* sh = sub_shifts + sub_off[s * 3 + l];
-      for (int64_t q = 0; q < sub_counts[s * 3 + l]; ++q) {
-        check(sh[q]);
-        pl_shift.push_back(sh[q]);
-      }
-      pl_off.push_back(int64_t(pl_shift.size()));
-      block_pl[l][s] = s;
+      block_pl[l][s] = place(std::vector<int64_t>(sh, sh + sub_counts[s * 3 + l]));
     }
-    std::map<int64_t, int64_t> seen;
-    for (int64_t dd = 0; dd < ndef; ++dd) {
-      const int64_t cs = def_shifts[dd * 3 + l];
-      auto it = seen.find(cs);
-      int64_t p;
-      if (it == seen.end()) {
-        check(cs);
-        p = int64_t(pl_off.size()) - 1;
-        seen[cs] = p;
-        pl_shift.push_back(cs);
-        pl_off.push_back(int64_t(pl_shift.size()));
-      } else {
-        p = it->second;
-      }
-      block_pl[l][nsub + dd] = p;
-    }
+    for (int64_t dd = 0; dd < ndef; ++dd)
+      block_pl[l][nsub + dd] = place(std::vector<int64_t>{def_shifts[dd * 3 + l]});
     const int64_t P = int64_t(pl_off.size()) - 1;
     can.d[l] = P * Rd;
     if (can.d[l] == 0) continue;
@@ -683,41 +748,50 @@ void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, doubl
 
 // Polar (Loewdin) re-orthonormalisation U <- U (U^T U)^{-1/2} by Newton-Schulz
 // iterations U <- U (3I - U^T U)/2: GEMM-only (no eigensolver), quadratic
-// convergence from the ~1e-11 orthogonality loss of U = A V Sigma^{-1}.
-void polar_orthonormalize(latsum_ctx* c, double* U, int64_t N, int64_t k, int iters = 2) {
+// convergence from the ~1e-11 orthogonality loss of U = A V Sigma^{-1}.  U is this
+// rank's row block; U^T U is all-reduced when the rows are sharded.
+void polar_orthonormalize(latsum_ctx* c, double* U, int64_t Nb, int64_t k, bool sharded,
+                          int iters = 2) {
   if (k == 0) return;
-  DBuf S(c, size_t(k) * k), Un(c, size_t(N) * k);
+  DBuf S(c, size_t(k) * k), Un(c, size_t(std::max<int64_t>(Nb, 1)) * k);
   for (int it = 0; it < iters; ++it) {
-    gemm(c, true, false, k, k, N, 1.0, U, N, U, N, 0.0, S.p, k, tagged("gemm_basis"));
-    CK(cudaMemcpyAsync(Un.p, U, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
-    gemm(c, false, false, N, k, k, -0.5, U, N, S.p, k, 1.5, Un.p, N, tagged("gemm_basis"));
-    CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * N * k, cudaMemcpyDeviceToDevice, c->stream));
+    if (Nb > 0) gemm(c, true, false, k, k, Nb, 1.0, U, Nb, U, Nb, 0.0, S.p, k, tagged("gemm_basis"));
+    else CK(cudaMemsetAsync(S.p, 0, sizeof(double) * k * k, c->stream));
+    if (sharded) allreduce(c, S.p, size_t(k) * k);
+    if (Nb == 0) continue;
+    CK(cudaMemcpyAsync(Un.p, U, sizeof(double) * Nb * k, cudaMemcpyDeviceToDevice, c->stream));
+    gemm(c, false, false, Nb, k, k, -0.5, U, Nb, S.p, k, 1.5, Un.p, Nb, tagged("gemm_basis"));
+    CK(cudaMemcpyAsync(U, Un.p, sizeof(double) * Nb * k, cudaMemcpyDeviceToDevice, c->stream));
   }
 }
 
-// U (N x k) = A (N x d) * [the k leading columns of evecs (d x n, ascending order)]
+// U (Nb x k) = A (Nb x d) * [the k leading columns of evecs (d x n, ascending order)]
 // scaled by 1/sqrt(lam_desc), then re-orthonormalised: left singular vectors from the
-// eigenpairs of A^T A.
-void left_from_right(latsum_ctx* c, const double* A, int64_t N, int64_t d, const double* evecs,
-                     int64_t n, const std::vector<double>& lam_desc, int64_t k, double* U) {
+// eigenpairs of A^T A (row block of A -> row block of U).
+void left_from_right(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, const double* evecs,
+                     int64_t n, const std::vector<double>& lam_desc, int64_t k, double* U,
+                     bool sharded) {
   if (k == 0) return;
-  DBuf Vd(c, size_t(d) * k);
-  k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, n, k, Vd.p);
-  post_launch(c);
-  gemm(c, false, false, N, k, d, 1.0, A, N, Vd.p, d, 0.0, U, N, tagged("gemm_basis"));
-  std::vector<double> inv(k);
-  for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
-  DVec<double> sc;
-  sc.upload(c, inv);
-  k_scale_columns<<<grid_for(N * k), 256, 0, c->stream>>>(U, N, k, sc.p, U);
-  post_launch(c);
-  polar_orthonormalize(c, U, N, k);
+  if (Nb > 0) {
+    DBuf Vd(c, size_t(d) * k);
+    k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, n, k, Vd.p);
+    post_launch(c);
+    gemm(c, false, false, Nb, k, d, 1.0, A, Nb, Vd.p, d, 0.0, U, Nb, tagged("gemm_basis"));
+    std::vector<double> inv(k);
+    for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
+    DVec<double> sc;
+    sc.upload(c, inv);
+    k_scale_columns<<<grid_for(Nb * k), 256, 0, c->stream>>>(U, Nb, k, sc.p, U);
+    post_launch(c);
+  }
+  polar_orthonormalize(c, U, Nb, k, sharded);
 }
 
 struct ModeOut {
   std::vector<double> sigma;
   int64_t r = 1;
-  DBuf Z;
+  DBuf Z;            // rows [blk.lo, blk.hi) of Z (all rows when not sharded)
+  RowBlock blk;
   bool tie = false;
   double margin = 0.0;
   int deflated = 0, rows = 0;
@@ -736,25 +810,39 @@ struct Timings {
 // the rest of the spectrum is recomputed from A'' = (I - U1 U1^T)^2 A~ restricted to the
 // pass-1 complement Qc (the n - k1 trailing eigenvectors), whose Gram has the size of
 // that complement and resolves singular values down to ~eps ||A''||.
+//
+// Multi-GPU (column orientation): the rank owns grid rows [lo, hi) of A~, U1, A'', B, U2
+// and Z; every contraction over the grid index (the Grams, U^T U, U1^T A) is a partial
+// product all-reduced over NVLink; eigensolves run redundantly on identical Grams.
 void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
                  double tol, int deflate, ModeOut& out, Timings& tm) {
   const int64_t N = can.N[l], d = can.d[l];
   const int64_t n_sing = std::min<int64_t>(N, can.Mc);
+  const bool rows = N <= d;
+  const bool sharded = !rows && c->comm && c->nranks > 1;
+  const RowBlock blk = sharded ? row_block(c, N) : RowBlock{0, N};
+  const int64_t Nb = blk.n();
+  out.blk = blk;
   Timer timer(c);
   timer.start();
   std::vector<double> sq(d);
   for (int64_t j = 0; j < d; ++j) sq[j] = std::sqrt(can.mult[l][j]);
   DVec<double> dsq;
   dsq.upload(c, sq);
-  DBuf At(c, size_t(N) * d);
-  k_scale_columns<<<grid_for(N * d), 256, 0, c->stream>>>(can.dict[l].p, N, d, dsq.p, At.p);
-  post_launch(c);
-  const bool rows = N <= d;
+  DBuf At(c, size_t(std::max<int64_t>(Nb, 1)) * d);
+  if (Nb > 0) {
+    CK(cudaMemcpy2DAsync(At.p, Nb * sizeof(double), can.dict[l].p + blk.lo, N * sizeof(double),
+                         Nb * sizeof(double), d, cudaMemcpyDeviceToDevice, c->stream));
+    k_scale_columns<<<grid_for(Nb * d), 256, 0, c->stream>>>(At.p, Nb, d, dsq.p, At.p);
+    post_launch(c);
+  }
   const int64_t n = rows ? N : d;
   out.rows = rows ? 1 : 0;
   out.gsize = n;
   DBuf G(c, size_t(n) * n), W(c, n);
-  gram(c, rows, At.p, N, d, G.p);
+  if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
+  else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
+  if (sharded) allreduce(c, G.p, size_t(n) * n);
   tm.gram += timer.stop();
   timer.start();
   syevd(c, n, G.p, W.p);
@@ -792,18 +880,25 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
                       target * target < 1e6 * double(n) * kEpsMach * lmax);
     if (defl) {
       timer.start();
-      U1.alloc(c, size_t(N) * k1);
+      const int64_t Nr = std::max<int64_t>(Nb, 1);
+      U1.alloc(c, size_t(Nr) * k1);
       if (rows) {
         k_reverse_columns<<<grid_for(N * k1), 256, 0, c->stream>>>(G.p, N, n, k1, U1.p);
         post_launch(c);
       } else {
-        left_from_right(c, At.p, N, d, G.p, n, lam_d, k1, U1.p);
+        left_from_right(c, At.p, Nb, d, G.p, n, lam_d, k1, U1.p, sharded);
       }
-      DBuf Ap(c, size_t(N) * d), C(c, size_t(k1) * d);
-      CK(cudaMemcpyAsync(Ap.p, At.p, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, c->stream));
+      DBuf Ap(c, size_t(Nr) * d), C(c, size_t(k1) * d);
+      if (Nb > 0)
+        CK(cudaMemcpyAsync(Ap.p, At.p, sizeof(double) * Nb * d, cudaMemcpyDeviceToDevice, c->stream));
       for (int rep = 0; rep < 2; ++rep) {  // project out span(U1), then re-orthogonalise once
-        gemm(c, true, false, k1, d, N, 1.0, U1.p, N, Ap.p, N, 0.0, C.p, k1, tagged("gemm_deflate"));
-        gemm(c, false, false, N, d, k1, -1.0, U1.p, N, C.p, k1, 1.0, Ap.p, N, tagged("gemm_deflate"));
+        if (Nb > 0)
+          gemm(c, true, false, k1, d, Nb, 1.0, U1.p, Nb, Ap.p, Nb, 0.0, C.p, k1, tagged("gemm_deflate"));
+        else
+          CK(cudaMemsetAsync(C.p, 0, sizeof(double) * k1 * d, c->stream));
+        if (sharded) allreduce(c, C.p, size_t(k1) * d);
+        if (Nb > 0)
+          gemm(c, false, false, Nb, d, k1, -1.0, U1.p, Nb, C.p, k1, 1.0, Ap.p, Nb, tagged("gemm_deflate"));
       }
       // restrict to the pass-1 complement Qc = G[:, 0:nc] (ascending eigenvectors)
       G2.alloc(c, size_t(nc) * nc);
@@ -811,10 +906,15 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
         B.alloc(c, size_t(nc) * d);
         gemm(c, true, false, nc, d, N, 1.0, G.p, N, Ap.p, N, 0.0, B.p, nc, tagged("gemm_deflate"));
         gram(c, true, B.p, nc, d, G2.p);
-      } else {     // B = A'' Qc (N x nc), G2 = B^T B
-        B.alloc(c, size_t(N) * nc);
-        gemm(c, false, false, N, nc, d, 1.0, Ap.p, N, G.p, d, 0.0, B.p, N, tagged("gemm_deflate"));
-        gram(c, false, B.p, N, nc, G2.p);
+      } else {     // B = A'' Qc (Nb x nc), G2 = B^T B
+        B.alloc(c, size_t(Nr) * nc);
+        if (Nb > 0) {
+          gemm(c, false, false, Nb, nc, d, 1.0, Ap.p, Nb, G.p, d, 0.0, B.p, Nb, tagged("gemm_deflate"));
+          gram(c, false, B.p, Nb, nc, G2.p);
+        } else {
+          CK(cudaMemsetAsync(G2.p, 0, sizeof(double) * nc * nc, c->stream));
+        }
+        if (sharded) allreduce(c, G2.p, size_t(nc) * nc);
       }
       tm.deflate += timer.stop();
       timer.start();
@@ -860,39 +960,43 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   }
   out.r = r;
 
-  // Z = the r leading left singular vectors in merged (descending) order
+  // Z = the r leading left singular vectors in merged (descending) order (row block)
   timer.start();
-  out.Z.alloc(c, size_t(N) * r);
+  const int64_t Nr = std::max<int64_t>(Nb, 1);
+  out.Z.alloc(c, size_t(Nr) * r);
   if (!defl) {
     if (rows) {
       k_reverse_columns<<<grid_for(N * r), 256, 0, c->stream>>>(G.p, N, n, r, out.Z.p);
       post_launch(c);
     } else {
-      left_from_right(c, At.p, N, d, G.p, n, lam_d, r, out.Z.p);
+      left_from_right(c, At.p, Nb, d, G.p, n, lam_d, r, out.Z.p, sharded);
     }
   } else {
     int64_t need2 = 0;
     for (int64_t i = 0; i < r; ++i)
       if (src[i].first == 1) need2 = std::max<int64_t>(need2, src[i].second + 1);
-    DBuf cat(c, size_t(N) * (k1 + need2));
-    CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * N * k1, cudaMemcpyDeviceToDevice, c->stream));
+    DBuf cat(c, size_t(Nr) * (k1 + need2));
+    if (Nb > 0)
+      CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * Nb * k1, cudaMemcpyDeviceToDevice, c->stream));
     if (need2) {
-      double* U2 = cat.p + N * k1;
+      double* U2 = cat.p + Nb * k1;
       if (rows) {  // U2 = Qc * Y (leading eigenvectors of B B^T)
         DBuf Yd(c, size_t(nc) * need2);
         k_reverse_columns<<<grid_for(nc * need2), 256, 0, c->stream>>>(G2.p, nc, nc, need2, Yd.p);
         post_launch(c);
         gemm(c, false, false, N, need2, nc, 1.0, G.p, N, Yd.p, nc, 0.0, U2, N, tagged("gemm_basis"));
       } else {     // U2 = B W mu^{-1/2}
-        left_from_right(c, B.p, N, nc, G2.p, nc, mu_d, need2, U2);
+        left_from_right(c, B.p, Nb, nc, G2.p, nc, mu_d, need2, U2, sharded);
       }
     }
-    std::vector<int64_t> sel(r);
-    for (int64_t i = 0; i < r; ++i) sel[i] = src[i].first == 0 ? src[i].second : k1 + src[i].second;
-    DVec<int64_t> dsel;
-    dsel.upload(c, sel);
-    k_select_columns<<<grid_for(N * r), 256, 0, c->stream>>>(cat.p, N, dsel.p, r, out.Z.p);
-    post_launch(c);
+    if (Nb > 0) {
+      std::vector<int64_t> sel(r);
+      for (int64_t i = 0; i < r; ++i) sel[i] = src[i].first == 0 ? src[i].second : k1 + src[i].second;
+      DVec<int64_t> dsel;
+      dsel.upload(c, sel);
+      k_select_columns<<<grid_for(Nb * r), 256, 0, c->stream>>>(cat.p, Nb, dsel.p, r, out.Z.p);
+      post_launch(c);
+    }
   }
   tm.deflate += timer.stop();
 }
@@ -907,7 +1011,7 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
   }
   DBuf part(c, can.T), sum(c, 1);
   ProfScope ps(c, "norm_hadamard", 3.0 * double(can.T) * double(can.T));
-  k_hadamard_norm_rows<<<unsigned((can.T + 127) / 128), 128, 0, c->stream>>>(
+  k_hadamard_norm_rows<<<unsigned((can.T + NORM_TPB - 1) / NORM_TPB), NORM_WARPS * 32, 0, c->stream>>>(
       G[0].p, G[1].p, G[2].p, can.d[0], can.d[1], can.d[2], can.dtc[0].p, can.dtc[1].p,
       can.dtc[2].p, can.dtw.p, can.T, part.p);
   post_launch(c);
@@ -923,8 +1027,8 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
 // rank_reduction.hpp:88-100) as X_a = G1[:, seg_a] G2[:, seg_a]^T over the terms
 // grouped by their mode-1 column a (one segmented GEMM), then core = P0 X^T.
 void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
-               double* core) {
-  const int64_t T = can.T, d0 = can.d[0];
+               double* core, int64_t a_lo = 0, int64_t a_hi = -1) {
+  const int64_t T = can.T, d0 = a_hi < 0 ? can.d[0] : a_hi;
   const int64_t r12 = r[1] * r[2];
   DBuf G1(c, size_t(r[1]) * T), G2(c, size_t(r[2]) * T);
   k_gather_scale<<<grid_for(r[1] * T), 256, 0, c->stream>>>(P[1].p, r[1], r[1], can.dtc[1].p,
@@ -936,7 +1040,11 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
   const int64_t budget = int64_t(1) << 29;  // doubles of X per chunk (4 GiB)
   const int64_t ac = std::max<int64_t>(1, std::min<int64_t>({d0, budget / std::max<int64_t>(r12, 1), 65535}));
   DBuf X(c, size_t(r12) * ac);
-  for (int64_t a0 = 0; a0 < d0; a0 += ac) {
+  if (a_lo >= d0) {  // empty share of a sharded core
+    CK(cudaMemsetAsync(core, 0, sizeof(double) * r[0] * r12, c->stream));
+    return;
+  }
+  for (int64_t a0 = a_lo; a0 < d0; a0 += ac) {
     const int64_t na = std::min(ac, d0 - a0);
     GemmOpts o = tagged("gemm_core_x");
     o.batch = na;
@@ -944,7 +1052,7 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
     o.kseg = can.dtseg.p + a0;
     gemm(c, false, true, r[1], r[2], T, 1.0, G1.p, r[1], G2.p, r[2], 0.0, X.p, r[1], o);
     gemm(c, false, true, r[0], r12, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, r12,
-         a0 == 0 ? 0.0 : 1.0, core, r[0], tagged("gemm_core"));
+         a0 == a_lo ? 0.0 : 1.0, core, r[0], tagged("gemm_core"));
   }
 }
 
@@ -960,6 +1068,8 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
     c->sub[i] = w;
   }
   c->sub[i]->prof = c->prof;
+  c->sub[i]->rank = c->rank;
+  c->sub[i]->nranks = c->nranks;
   return c->sub[i];
 }
 
@@ -1075,9 +1185,34 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   for (int l = 0; l < 3; ++l) {
     t.r[l] = mo[l].r;
     t.d[l] = can.d[l];
+    const RowBlock blk = mo[l].blk;
+    const int64_t N = can.N[l], Nb = blk.n();
+    const bool sharded = Nb != N;
     P[l].alloc(c, size_t(mo[l].r) * can.d[l]);
-    gemm(c, true, false, mo[l].r, can.d[l], can.N[l], 1.0, mo[l].Z.p, can.N[l], can.dict[l].p,
-         can.N[l], 0.0, P[l].p, mo[l].r, tagged("gemm_project"));
+    if (Nb > 0)  // P_l = Z_l^T D_l over this rank's rows, summed over ranks
+      gemm(c, true, false, mo[l].r, can.d[l], Nb, 1.0, mo[l].Z.p, Nb, can.dict[l].p + blk.lo, N,
+           0.0, P[l].p, mo[l].r, tagged("gemm_project"));
+    else
+      CK(cudaMemsetAsync(P[l].p, 0, sizeof(double) * mo[l].r * can.d[l], c->stream));
+    if (sharded) {
+      allreduce(c, P[l].p, size_t(mo[l].r) * can.d[l]);
+      // replicate Z: all-gather the row blocks (padded to equal size)
+      const int64_t r = mo[l].r, bmax = N / c->nranks + 1;
+      DBuf send(c, size_t(bmax) * r), recv(c, size_t(bmax) * r * c->nranks), full(c, size_t(N) * r);
+      CK(cudaMemsetAsync(send.p, 0, sizeof(double) * bmax * r, c->stream));
+      if (Nb > 0)
+        CK(cudaMemcpy2DAsync(send.p, bmax * sizeof(double), mo[l].Z.p, Nb * sizeof(double),
+                             Nb * sizeof(double), r, cudaMemcpyDeviceToDevice, c->stream));
+      NC(nccl().AllGather(send.p, recv.p, size_t(bmax) * r, kNcclFloat64, c->comm, c->stream));
+      for (int q = 0; q < c->nranks; ++q) {
+        const int64_t lo = N * q / c->nranks, nq = N * (q + 1) / c->nranks - lo;
+        if (nq > 0)
+          CK(cudaMemcpy2DAsync(full.p + lo, N * sizeof(double), recv.p + size_t(q) * bmax * r,
+                               bmax * sizeof(double), nq * sizeof(double), r,
+                               cudaMemcpyDeviceToDevice, c->stream));
+      }
+      mo[l].Z = std::move(full);
+    }
     t.tc[l].upload(c, can.tc[l]);
   }
   t.tw.upload(c, can.tw);
@@ -1086,7 +1221,13 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
     tp.start();
     t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
-    form_core(c, can, P, t.r, t.core.p);
+    if (c->comm && c->nranks > 1) {  // each rank forms the core from its share of a
+      const int64_t d0 = can.d[0];
+      form_core(c, can, P, t.r, t.core.p, d0 * c->rank / c->nranks, d0 * (c->rank + 1) / c->nranks);
+      allreduce(c, t.core.p, size_t(t.r[0]) * t.r[1] * t.r[2]);
+    } else {
+      form_core(c, can, P, t.r, t.core.p);
+    }
     t.has_core = true;
     tm.core = tp.stop();
   }
@@ -1145,10 +1286,10 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   const double* U0 = t.U[0].p + lo[0];
   const double* U1 = t.U[1].p + lo[1];
   const double* U2 = t.U[2].p + lo[2];
-  const int64_t budget = int64_t(1) << 28;  // doubles per intermediate (2 GiB)
-  const int64_t njc = std::max<int64_t>(1, std::min<int64_t>(nj, budget / std::max<int64_t>(r0 * r2, 1)));
+  const int64_t budget = int64_t(1) << 29;  // doubles per intermediate (4 GiB)
+  const int64_t njc = balanced_chunk(nj, budget / std::max<int64_t>(r0 * r2, 1), 128);
   DBuf Q(c, size_t(r0) * njc * r2);
-  const int64_t nkc = std::max<int64_t>(1, std::min<int64_t>({nk, budget / std::max<int64_t>(r0 * njc, 1), 65535}));
+  const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(r0 * njc, 1), 65535), 1);
   DBuf X(c, size_t(r0) * njc * nkc);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
@@ -1184,8 +1325,8 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
   DBuf A0(c, size_t(ni) * T);
   k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(D[0], ni, ld[0], tc[0], nullptr, T, A0.p);
   post_launch(c);
-  const int64_t budget = int64_t(1) << 27;
-  const int64_t nkc = std::max<int64_t>(1, std::min<int64_t>({nk, budget / std::max<int64_t>(T * nj, 1), 65535}));
+  const int64_t budget = int64_t(1) << 28;
+  const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(T * nj, 1), 65535), 1);
   DBuf X(c, size_t(T) * nj * nkc);
   for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
     const int64_t nkk = std::min(nkc, nk - k0);
@@ -1339,6 +1480,9 @@ void latsum_ctx_destroy(latsum_ctx* c) {
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto* w : c->sub)
     if (w) latsum_ctx_destroy(w);
+  if (c->comm) {
+    try { nccl().CommDestroy(c->comm); } catch (...) {}
+  }
   if (c->solver_params) cusolverDnDestroyParams(c->solver_params);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own) cudaStreamDestroy(c->own);
@@ -1359,6 +1503,42 @@ int latsum_ctx_synchronize(latsum_ctx* c) {
 }
 
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* c) { return c ? c->launches : 0; }
+
+int latsum_comm_unique_id(unsigned char id[128]) {
+  try {
+    NcclUid u;
+    NC(nccl().GetUniqueId(&u));
+    std::memcpy(id, u.internal, 128);
+    return LATSUM_OK;
+  } catch (const Error& e) {
+    return e.code;
+  }
+}
+
+int latsum_ctx_init_comm(latsum_ctx* c, const unsigned char id[128], int rank, int nranks) {
+  return guarded(c, [&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "latsum_ctx_init_comm: bad rank");
+    require(!c->comm, "latsum_ctx_init_comm: communicator already set");
+    c->rank = rank;
+    c->nranks = nranks;
+    if (nranks == 1) return;
+    NcclUid u;
+    std::memcpy(u.internal, id, 128);
+    CK(cudaSetDevice(c->device));
+    NC(nccl().CommInitRank(&c->comm, nranks, u, rank));
+    for (int i = 0; i < 4; ++i) {  // one communicator per worker stream, split in order
+      latsum_ctx* w = sub_ctx(c, i);
+      NC(nccl().CommSplit(c->comm, 0, rank, &w->comm, nullptr));
+    }
+  });
+}
+
+int latsum_ctx_comm_info(const latsum_ctx* c, int* rank, int* nranks) {
+  if (!c) return LATSUM_ERR_INVALID_ARGUMENT;
+  if (rank) *rank = c->rank;
+  if (nranks) *nranks = c->nranks;
+  return LATSUM_OK;
+}
 
 int latsum_ctx_set_profiling(latsum_ctx* c, int on) {
   return guarded(c, [&] {

@@ -224,23 +224,58 @@ __global__ void k_select_columns(const double* __restrict__ src, int64_t rows,
   }
 }
 
-// ||A||^2 = sum_{t,t'} w_t w_t' prod_l G_l[c_l(t), c_l(t')] (canonical.hpp:148-162 with the
-// three M x M Grams replaced by d_l x d_l dictionary Grams).  One thread per row t;
-// partial[t] = w_t * sum_t' (...) in a fixed order.
-__global__ void k_hadamard_norm_rows(const double* __restrict__ G0, const double* __restrict__ G1,
-                                     const double* __restrict__ G2, int64_t d0, int64_t d1,
-                                     int64_t d2, const int32_t* __restrict__ c0,
-                                     const int32_t* __restrict__ c1,
-                                     const int32_t* __restrict__ c2, const double* __restrict__ w,
-                                     int64_t T, double* __restrict__ partial) {
-  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (t >= T) return;
-  const double* g0 = G0 + int64_t(c0[t]) * d0;
-  const double* g1 = G1 + int64_t(c1[t]) * d1;
-  const double* g2 = G2 + int64_t(c2[t]) * d2;
-  double s = 0.0;
-  for (int64_t u = 0; u < T; ++u) s += w[u] * (g0[c0[u]] * g1[c1[u]] * g2[c2[u]]);
-  partial[t] = w[t] * s;
+// ||A||^2 = sum_{t,u} w_t w_u prod_l G_l[c_l(t), c_l(u)] (canonical.hpp:148-162 with the
+// three M x M Grams replaced by d_l x d_l dictionary Grams).  A block owns NORM_TPB terms
+// t (NORM_TPW per warp); the u terms stream through shared memory in chunks, lanes stride
+// over u (coalesced), and each t's partial is reduced in a fixed order:
+// partial[t] = w_t * sum_u (...).
+constexpr int NORM_TPW = 4, NORM_WARPS = 8, NORM_TPB = NORM_TPW * NORM_WARPS, NORM_CHUNK = 1024;
+__global__ void __launch_bounds__(NORM_WARPS * 32)
+k_hadamard_norm_rows(const double* __restrict__ G0, const double* __restrict__ G1,
+                     const double* __restrict__ G2, int64_t d0, int64_t d1, int64_t d2,
+                     const int32_t* __restrict__ c0, const int32_t* __restrict__ c1,
+                     const int32_t* __restrict__ c2, const double* __restrict__ w, int64_t T,
+                     double* __restrict__ partial) {
+  __shared__ int32_t s0[NORM_CHUNK], s1[NORM_CHUNK], s2[NORM_CHUNK];
+  __shared__ double sw[NORM_CHUNK];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t tbase = int64_t(blockIdx.x) * NORM_TPB + warp * NORM_TPW;
+  const double* g0[NORM_TPW];
+  const double* g1[NORM_TPW];
+  const double* g2[NORM_TPW];
+  double acc[NORM_TPW];
+#pragma unroll
+  for (int q = 0; q < NORM_TPW; ++q) {
+    const int64_t t = min(tbase + q, T - 1);
+    g0[q] = G0 + int64_t(c0[t]) * d0;
+    g1[q] = G1 + int64_t(c1[t]) * d1;
+    g2[q] = G2 + int64_t(c2[t]) * d2;
+    acc[q] = 0.0;
+  }
+  for (int64_t u0 = 0; u0 < T; u0 += NORM_CHUNK) {
+    const int n = int((T - u0) < NORM_CHUNK ? (T - u0) : NORM_CHUNK);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      s0[i] = c0[u0 + i];
+      s1[i] = c1[u0 + i];
+      s2[i] = c2[u0 + i];
+      sw[i] = w[u0 + i];
+    }
+    __syncthreads();
+    for (int i = lane; i < n; i += 32) {
+      const int a = s0[i], b = s1[i], cc = s2[i];
+      const double wu = sw[i];
+#pragma unroll
+      for (int q = 0; q < NORM_TPW; ++q) acc[q] += wu * (g0[q][a] * g1[q][b] * g2[q][cc]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NORM_TPW; ++q) {
+    double v = acc[q];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    const int64_t t = tbase + q;
+    if (lane == 0 && t < T) partial[t] = w[t] * v;
+  }
 }
 
 // Ordered sum of n values by one block (deterministic).

@@ -245,3 +245,14 @@ def baseline(i: int, seed: Optional[int] = None) -> Geometry:
                            seed=sd, name="cfg5", eval_lo=(c - 1024,) * 3,
                            eval_hi=(c + 1024,) * 3)
     raise ValueError("baseline config index is 1..5")
+
+
+def row_block(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Rows [lo, hi) of an n-row operand owned by `rank` (latsum_capi.cu row_block)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def z_slab(lo: Sequence[int], hi: Sequence[int], rank: int, world: int):
+    """The z-slab of the evaluation box [lo, hi) that `rank` evaluates (no communication)."""
+    z0, z1 = row_block(hi[2] - lo[2], rank, world)
+    return (lo[0], lo[1], lo[2] + z0), (hi[0], hi[1], lo[2] + z1)

@@ -260,3 +260,44 @@ def test_dgemm_dmma_matches_fp64_reference(ctx, ta, tb, shape):
     got = dC.cpu().T
     err = (got - want).abs().max().item() / max(1.0, want.abs().max().item())
     assert err < 1e-13 * max(1, K) ** 0.5 * 10
+
+
+# ----------------------------------------------------------------------------- full configs
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_full_config_against_oracle_fixture(ctx, cfg):
+    """BASELINE configs at full size against the oracle fixtures of
+    tests/golden/make_fullconfig.py (cfg5: factors-only RHOSVD, projected-CP values)."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"fullcfg{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    fx = np.load(path)
+    g = W.baseline(cfg)
+    ref = api.reference_for(g, ctx)
+    assert ref.step_constant == float(fx["C0"])
+    can = api.lattice_sum(ref, g)
+    assert can.rank == int(fx["canonical_rank"])
+    assert list(can.dict_cols) == list(fx["merged_columns"])
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=(cfg != 5))
+    ranks = list(fx["ranks"])
+    for l in range(3):
+        if rep.chosen_ranks[l] != ranks[l]:
+            assert bool(fx["tie"][l]) or rep.tie_at_cutoff[l], (rep.chosen_ranks, ranks)
+            assert abs(rep.chosen_ranks[l] - ranks[l]) <= 1
+        s_orc = fx[f"sigma{l}"]
+        s_gpu = rep.singular_values[l][:s_orc.size]
+        assert rep.singular_values[l].size == int(fx["n_singular"][l])
+        assert np.max(np.abs(s_gpu - s_orc)) / s_orc[0] < 1e-10
+    pr = fx["probes"]
+    v = t.entries(pr)
+    want = fx["v_rhosvd"]
+    assert np.max(np.abs(v - want)) / np.max(np.abs(want)) <= 10 * g.eps + 1e-12
+    exact = can.entries(pr)
+    np.testing.assert_allclose(exact, fx["v_canonical"], rtol=0,
+                               atol=1e-12 * np.max(np.abs(fx["v_canonical"])))
+    nb = fx["v_brute"].size
+    assert np.max(np.abs(exact[:nb] - fx["v_brute"])) / np.max(np.abs(fx["v_brute"])) < 1e-12
+    np.testing.assert_allclose(rep.weight_norm, float(fx["weight_norm"]), rtol=1e-12)
+    np.testing.assert_allclose(rep.input_norm, float(fx["input_norm"]), rtol=1e-9)

@@ -6,6 +6,7 @@
 #include <thread>
 #include <vector>
 #include <cmath>
+#include <chrono>
 
 #define CK(x) do { auto e = (x); if (e) { printf("err %d at %s:%d\n", int(e), __FILE__, __LINE__); exit(1);} } while (0)
 
@@ -38,7 +39,7 @@ int main() {
   }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int64_t n : {400, 693, 1000, 1625, 2048}) {
+  for (int64_t n : {357, 693, 1625}) {
     double *A, *A0, *W;
     CK(cudaMalloc(&A, 3 * n * n * 8)); CK(cudaMalloc(&A0, 3 * n * n * 8)); CK(cudaMalloc(&W, 3 * n * 8));
     fill(A0, n, 3, 1);
@@ -97,6 +98,63 @@ int main() {
       cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       if (rep == 2) printf("n=%5ld  1x Xsyevd novector : %8.2f ms\n", n, ms);
+    }
+    // Jacobi (syevj)
+    {
+      syevjInfo_t sj;
+      CK(cusolverDnCreateSyevjInfo(&sj));
+      cusolverDnXsyevjSetTolerance(sj, 1e-14);
+      cusolverDnXsyevjSetMaxSweeps(sj, 20);
+      int lw = 0;
+      CK(cusolverDnDsyevj_bufferSize(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, &lw, sj));
+      double* wj; CK(cudaMalloc(&wj, size_t(lw) * 8 + 8));
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0, st[0]);
+        CK(cusolverDnDsyevj(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, wj, lw, info, sj));
+        cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        int sweeps = 0; double res = 0;
+        cusolverDnXsyevjGetSweeps(hs[0], sj, &sweeps); cusolverDnXsyevjGetResidual(hs[0], sj, &res);
+        if (rep == 2) printf("n=%5ld  1x Dsyevj          : %8.2f ms (sweeps %d residual %.2e)\n", n, ms, sweeps, res);
+      }
+      cudaFree(wj);
+      cusolverDnDestroySyevjInfo(sj);
+    }
+    // 32-bit legacy Dsyevd
+    {
+      int lw = 0;
+      CK(cusolverDnDsyevd_bufferSize(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, &lw));
+      double* wd; CK(cudaMalloc(&wd, size_t(lw) * 8 + 8));
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0, st[0]);
+        CK(cusolverDnDsyevd(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, wd, lw, info));
+        cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (rep == 2) printf("n=%5ld  1x Dsyevd (legacy) : %8.2f ms\n", n, ms);
+      }
+      cudaFree(wd);
+    }
+    // sytrd alone
+    {
+      int lw = 0;
+      double *dd, *ee, *tau;
+      CK(cudaMalloc(&dd, n * 8)); CK(cudaMalloc(&ee, n * 8)); CK(cudaMalloc(&tau, n * 8));
+      CK(cusolverDnDsytrd_bufferSize(hs[0], CUBLAS_FILL_MODE_LOWER, n, A, n, dd, ee, tau, &lw));
+      double* wt; CK(cudaMalloc(&wt, size_t(lw) * 8 + 8));
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0, st[0]);
+        CK(cusolverDnDsytrd(hs[0], CUBLAS_FILL_MODE_LOWER, n, A, n, dd, ee, tau, wt, lw, info));
+        cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (rep == 2) printf("n=%5ld  1x Dsytrd          : %8.2f ms\n", n, ms);
+      }
+      cudaFree(wt); cudaFree(dd); cudaFree(ee); cudaFree(tau);
     }
     for (int i = 0; i < 3; ++i) cudaFree(dw[i]);
     cudaFree(A); cudaFree(A0); cudaFree(W); cudaFree(info);

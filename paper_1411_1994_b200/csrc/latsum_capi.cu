@@ -183,6 +183,14 @@ int grid_for(int64_t total, int threads = 256) {
   return int(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
 }
 
+// Doubles an intermediate may occupy: a third of the free device memory, at most 2^31.
+int64_t workspace_budget(int64_t floor_doubles = int64_t(1) << 27) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return floor_doubles;
+  const int64_t v = int64_t(free_b / 3 / sizeof(double));
+  return std::max<int64_t>(floor_doubles, std::min<int64_t>(v, int64_t(1) << 31));
+}
+
 // Split n into ceil(n / cap) near-equal chunks (multiples of `align` when possible).
 int64_t balanced_chunk(int64_t n, int64_t cap, int64_t align) {
   cap = std::max<int64_t>(1, cap);
@@ -444,6 +452,11 @@ struct latsum_canonical {
   DVec<int32_t> dtc[3];
   DVec<double> dtw;
   DVec<int64_t> dtseg;
+  // the merged terms re-sorted by their mode-m column (m = 1, 2), with segments, for
+  // contracting the core over the mode with the fewest distinct columns
+  std::vector<int32_t> stc[3][3];
+  std::vector<double> stw[3];
+  std::vector<int64_t> sseg[3];
 };
 
 struct latsum_tucker {
@@ -694,6 +707,19 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
   for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
   can.dtw.upload(c, can.tw);
   can.dtseg.upload(c, can.tseg);
+  for (int m = 0; m < 3; ++m) {  // counting sort by c_m (stable: keeps the c0-major order)
+    can.sseg[m].assign(can.d[m] + 1, 0);
+    for (int64_t t = 0; t < can.T; ++t) can.sseg[m][can.tc[m][t] + 1] += 1;
+    for (int64_t a = 0; a < can.d[m]; ++a) can.sseg[m][a + 1] += can.sseg[m][a];
+    std::vector<int64_t> pos(can.sseg[m].begin(), can.sseg[m].end() - 1);
+    for (int l = 0; l < 3; ++l) can.stc[m][l].assign(can.T, 0);
+    can.stw[m].assign(can.T, 0.0);
+    for (int64_t t = 0; t < can.T; ++t) {
+      const int64_t q = pos[can.tc[m][t]]++;
+      for (int l = 0; l < 3; ++l) can.stc[m][l][q] = can.tc[l][t];
+      can.stw[m][q] = can.tw[t];
+    }
+  }
 }
 
 void materialize_factor(latsum_ctx* c, const latsum_canonical& can, int l, double* dst_device) {
@@ -1026,33 +1052,69 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
 // core(a,b,c) = sum_t w_t P0(a,c0_t) P1(b,c1_t) P2(c,c2_t)  (project_core,
 // rank_reduction.hpp:88-100) as X_a = G1[:, seg_a] G2[:, seg_a]^T over the terms
 // grouped by their mode-1 column a (one segmented GEMM), then core = P0 X^T.
+// The mode whose dictionary is smallest is contracted last: cost 2 r1 r2 r3 d_m.
+int core_mode(const latsum_canonical& can) {
+  int m = 0;
+  for (int l = 1; l < 3; ++l)
+    if (can.d[l] < can.d[m]) m = l;
+  return m;
+}
+
+// core(a,b,c) = sum_t w_t P0(a,c0_t) P1(b,c1_t) P2(c,c2_t)  (project_core,
+// rank_reduction.hpp:88-100).  With m the contracted mode and (o1, o2) the others:
+// X_j = G1[:, seg_j] G2[:, seg_j]^T over the terms whose mode-m column is j (one
+// segmented GEMM, G1 = P_o1 gathered and weighted, G2 = P_o2 gathered), then
+// core = X x_m P_m.  Cost 2 r1 r2 r3 d_m + 2 r_o1 r_o2 T instead of the reference
+// loop's 2 r1 r2 r3 M_c.  [a_lo, a_hi) restricts j (the rank's share when sharded).
 void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
-               double* core, int64_t a_lo = 0, int64_t a_hi = -1) {
-  const int64_t T = can.T, d0 = a_hi < 0 ? can.d[0] : a_hi;
-  const int64_t r12 = r[1] * r[2];
-  DBuf G1(c, size_t(r[1]) * T), G2(c, size_t(r[2]) * T);
-  k_gather_scale<<<grid_for(r[1] * T), 256, 0, c->stream>>>(P[1].p, r[1], r[1], can.dtc[1].p,
-                                                            can.dtw.p, T, G1.p);
-  post_launch(c);
-  k_gather_scale<<<grid_for(r[2] * T), 256, 0, c->stream>>>(P[2].p, r[2], r[2], can.dtc[2].p, nullptr,
-                                                            T, G2.p);
-  post_launch(c);
-  const int64_t budget = int64_t(1) << 29;  // doubles of X per chunk (4 GiB)
-  const int64_t ac = std::max<int64_t>(1, std::min<int64_t>({d0, budget / std::max<int64_t>(r12, 1), 65535}));
-  DBuf X(c, size_t(r12) * ac);
-  if (a_lo >= d0) {  // empty share of a sharded core
-    CK(cudaMemsetAsync(core, 0, sizeof(double) * r[0] * r12, c->stream));
+               double* core, int m, int64_t a_lo = 0, int64_t a_hi = -1) {
+  const int64_t T = can.T, dm = a_hi < 0 ? can.d[m] : a_hi;
+  const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
+  const int64_t ro = r[o1] * r[o2];
+  const int64_t rall = r[0] * r[1] * r[2];
+  if (a_lo >= dm) {  // empty share of a sharded core
+    CK(cudaMemsetAsync(core, 0, sizeof(double) * rall, c->stream));
     return;
   }
-  for (int64_t a0 = a_lo; a0 < d0; a0 += ac) {
-    const int64_t na = std::min(ac, d0 - a0);
+  DVec<int32_t> c1, c2;
+  DVec<double> tw;
+  DVec<int64_t> seg;
+  c1.upload(c, can.stc[m][o1]);
+  c2.upload(c, can.stc[m][o2]);
+  tw.upload(c, can.stw[m]);
+  seg.upload(c, can.sseg[m]);
+  DBuf G1(c, size_t(r[o1]) * T), G2(c, size_t(r[o2]) * T);
+  k_gather_scale<<<grid_for(r[o1] * T), 256, 0, c->stream>>>(P[o1].p, r[o1], r[o1], c1.p, tw.p, T,
+                                                             G1.p);
+  post_launch(c);
+  k_gather_scale<<<grid_for(r[o2] * T), 256, 0, c->stream>>>(P[o2].p, r[o2], r[o2], c2.p, nullptr,
+                                                             T, G2.p);
+  post_launch(c);
+  const int64_t budget = workspace_budget();  // doubles of X per chunk
+  const int64_t ac = balanced_chunk(dm - a_lo, std::min<int64_t>(budget / std::max<int64_t>(ro, 1), 65535), 64);
+  DBuf X(c, size_t(ro) * ac);
+  for (int64_t a0 = a_lo; a0 < dm; a0 += ac) {
+    const int64_t na = std::min(ac, dm - a0);
     GemmOpts o = tagged("gemm_core_x");
     o.batch = na;
-    o.sC = r12;
-    o.kseg = can.dtseg.p + a0;
-    gemm(c, false, true, r[1], r[2], T, 1.0, G1.p, r[1], G2.p, r[2], 0.0, X.p, r[1], o);
-    gemm(c, false, true, r[0], r12, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, r12,
-         a0 == a_lo ? 0.0 : 1.0, core, r[0], tagged("gemm_core"));
+    o.sC = ro;
+    o.kseg = seg.p + a0;
+    gemm(c, false, true, r[o1], r[o2], T, 1.0, G1.p, r[o1], G2.p, r[o2], 0.0, X.p, r[o1], o);
+    const double beta = a0 == a_lo ? 0.0 : 1.0;
+    if (m == 0) {        // core (r0 x r1 r2) = P0[:, j] X^T
+      gemm(c, false, true, r[0], ro, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, ro, beta, core, r[0],
+           tagged("gemm_core"));
+    } else if (m == 2) { // core (r0 r1 x r2) = X P2[:, j]^T
+      gemm(c, false, true, ro, r[2], na, 1.0, X.p, ro, P[2].p + a0 * r[2], r[2], beta, core, ro,
+           tagged("gemm_core"));
+    } else {             // core[:, :, k] (r0 x r1) = X[:, k, j] P1[:, j]^T, batched over k
+      GemmOpts ob = tagged("gemm_core");
+      ob.batch = r[2];
+      ob.sA = r[0];
+      ob.sC = r[0] * r[1];
+      gemm(c, false, true, r[0], r[1], na, 1.0, X.p, ro, P[1].p + a0 * r[1], r[1], beta, core, r[0],
+           ob);
+    }
   }
 }
 
@@ -1221,12 +1283,14 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
     tp.start();
     t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
-    if (c->comm && c->nranks > 1) {  // each rank forms the core from its share of a
-      const int64_t d0 = can.d[0];
-      form_core(c, can, P, t.r, t.core.p, d0 * c->rank / c->nranks, d0 * (c->rank + 1) / c->nranks);
+    const int m = core_mode(can);
+    if (c->comm && c->nranks > 1) {  // each rank forms the core from its share of mode m
+      const int64_t dm = can.d[m];
+      form_core(c, can, P, t.r, t.core.p, m, dm * c->rank / c->nranks,
+                dm * (c->rank + 1) / c->nranks);
       allreduce(c, t.core.p, size_t(t.r[0]) * t.r[1] * t.r[2]);
     } else {
-      form_core(c, can, P, t.r, t.core.p);
+      form_core(c, can, P, t.r, t.core.p, m);
     }
     t.has_core = true;
     tm.core = tp.stop();

@@ -301,3 +301,28 @@ def test_full_config_against_oracle_fixture(ctx, cfg):
     assert np.max(np.abs(exact[:nb] - fx["v_brute"])) / np.max(np.abs(fx["v_brute"])) < 1e-12
     np.testing.assert_allclose(rep.weight_norm, float(fx["weight_norm"]), rtol=1e-12)
     np.testing.assert_allclose(rep.input_norm, float(fx["input_norm"]), rtol=1e-9)
+
+
+@pytest.mark.parametrize("fixed_mode", [0, 1, 2])
+def test_stage3_core_contracted_over_smallest_mode(ctx, fixed_mode):
+    """Defects that share one coordinate make that mode's dictionary the smallest, so the
+    core is contracted over mode 0, 1 or 2 (form_core); values must not depend on it."""
+    sites = []
+    for a in range(-2, 2):
+        for b in range(-2, 2):
+            s = [a, b]
+            s.insert(fixed_mode, 0)
+            sites.append(tuple(s))
+    g = W.from_lattice((4, 4, 4), 16, M=6, defects=[(sites, -1.0, None)], eps=1e-7)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    assert int(np.argmin(can.dict_cols)) == fixed_mode
+    F, w = O.side_matrices(oref, g)
+    orc = O.rhosvd(F, w, eps=g.eps, with_norm=False)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    assert tuple(rep.chosen_ranks) == tuple(orc.ranks)
+    core = O.project_core(w, orc.P)  # reference loop order, small sizes
+    pr = O.probes(g.N, 300, 21)
+    want = O.tucker_entries(core, orc.Z, pr)
+    got = t.entries(pr)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-11

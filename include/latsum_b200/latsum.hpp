@@ -1,0 +1,396 @@
+// latsum_b200/latsum.hpp — header-only C++ mirror of the reference's hot-path API
+// (/root/reference/proj/include/latsum) over the C ABI in <latsum_b200.h>.
+//
+// Same names, argument meaning and exception types as the reference:
+//   build_reference_canonical   reference.hpp:95-153
+//   assembled_sum_canonical     lattice_sum.hpp:198-223  (LatticeGeometry on lattice_grid)
+//   defected_sum                lattice_sum.hpp:339-400  (canonical branch)
+//   sublattice_union_sum        lattice_sum.hpp:411-465
+//   rhosvd                      rank_reduction.hpp:176-218
+//   TuckerTensor::entry/to_dense tucker.hpp:38-54,172-178
+//   CanonicalTensor::entry/weights/factor canonical.hpp:63-70
+// Errors: std::invalid_argument, WindowOverflowError (std::out_of_range, .mode()),
+// std::length_error, NotImplementedError, std::runtime_error (CUDA / cuSOLVER / NCCL).
+// Storage is plain std::vector<double> in Eigen's column-major layout, so an Eigen
+// build maps every buffer without copies (Eigen::Map<MatrixXd>(v.data(), rows, cols)).
+#pragma once
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "latsum_b200.h"
+
+namespace latsum {
+
+using Index = int64_t;
+using Dims3 = std::array<Index, 3>;
+using Int3 = std::array<int, 3>;
+
+class WindowOverflowError : public std::out_of_range {
+ public:
+  WindowOverflowError(const std::string& m, int mode) : std::out_of_range(m), mode_(mode) {}
+  int mode() const { return mode_; }
+
+ private:
+  int mode_;
+};
+
+class NotImplementedError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace b200 {
+
+inline void throw_status(int st, const std::string& msg) {
+  switch (st) {
+    case LATSUM_OK: return;
+    case LATSUM_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case LATSUM_ERR_WINDOW_OVERFLOW: {
+      int mode = 0;
+      const auto p = msg.find("mode ");
+      if (p != std::string::npos) mode = std::atoi(msg.c_str() + p + 5);
+      throw WindowOverflowError(msg, mode);
+    }
+    case LATSUM_ERR_LENGTH: throw std::length_error(msg);
+    case LATSUM_ERR_NOT_IMPLEMENTED: throw NotImplementedError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// One CUDA device / stream / cuSOLVER handle (latsum_ctx); one per host thread.
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    latsum_ctx* c = nullptr;
+    if (latsum_ctx_create(device, &c) != LATSUM_OK)
+      throw std::runtime_error("latsum_ctx_create: no CUDA device (there is no CPU fallback)");
+    ctx_.reset(c);
+  }
+  latsum_ctx* get() const { return ctx_.get(); }
+  void check(int st) const {
+    if (st != LATSUM_OK) throw_status(st, latsum_last_error(ctx_.get()));
+  }
+  static Context& default_context() {
+    thread_local Context c(0);
+    return c;
+  }
+
+ private:
+  struct Del {
+    void operator()(latsum_ctx* c) const { latsum_ctx_destroy(c); }
+  };
+  std::unique_ptr<latsum_ctx, Del> ctx_;
+};
+
+}  // namespace b200
+
+// kernel.hpp:37-152 restricted to the gauss-type primitives of the hot path.
+struct KernelSpec {
+  int family = LATSUM_NEWTON;
+  double lambda = 0.0;
+  static KernelSpec newton() { return {LATSUM_NEWTON, 0.0}; }
+  static KernelSpec yukawa(double l) {
+    if (!(l > 0.0)) throw std::invalid_argument("yukawa lambda must be positive");
+    return {LATSUM_YUKAWA, l};
+  }
+};
+
+// grid.hpp:41-97 (box widths b_l and even cell counts n_l; origin 0).
+struct UniformGrid {
+  std::array<double, 3> box{1, 1, 1};
+  Dims3 n{2, 2, 2};
+  static UniformGrid cubic(double b, Index n) { return {{b, b, b}, {n, n, n}}; }
+  Index points(int l) const { return n[l]; }
+  double mesh(int l) const { return box[l] / double(n[l]); }
+};
+
+// geometry.hpp:183-261 (the parts the hot path consumes).
+enum class DefectKind { vacancy, impurity };
+struct DefectSpec {
+  std::vector<Int3> sites;
+  DefectKind kind = DefectKind::vacancy;
+  double charge = 0.0;
+  std::array<double, 3> grid_offset{0, 0, 0};
+};
+inline std::vector<int> default_active_set(int cells) {
+  std::vector<int> k;
+  for (int i = -(cells / 2); i <= (cells + 1) / 2 - 1; ++i) k.push_back(i);
+  return k;
+}
+struct LatticeGeometry {
+  Int3 cells{1, 1, 1};
+  double cell_width = 1.0;
+  double base_charge = 1.0;
+  KernelSpec kernel = KernelSpec::newton();
+  std::array<std::vector<int>, 3> active;  // empty = default K sets
+  std::vector<DefectSpec> defects;
+  std::vector<int> active_set(int mode) const {
+    return active[mode].empty() ? default_active_set(cells[mode]) : active[mode];
+  }
+};
+struct SublatticePlacement {
+  LatticeGeometry geom;
+  std::array<double, 3> offset_cells{0, 0, 0};
+};
+
+// lattice_sum.hpp:75-86
+inline UniformGrid lattice_grid(const LatticeGeometry& g, Index n_per_cell) {
+  if (n_per_cell < 2 || n_per_cell % 2 != 0)
+    throw std::invalid_argument("lattice_grid: points per cell must be even and >= 2");
+  UniformGrid grid;
+  for (int l = 0; l < 3; ++l) {
+    grid.box[l] = g.cell_width * double(g.cells[l]);
+    grid.n[l] = n_per_cell * g.cells[l];
+  }
+  return grid;
+}
+
+struct TruncationSpec {  // rank_reduction.hpp:21-43
+  std::optional<Dims3> ranks;
+  std::optional<double> tolerance;
+  static TruncationSpec fixed_ranks(Index a, Index b, Index c) {
+    TruncationSpec s;
+    s.ranks = Dims3{a, b, c};
+    return s;
+  }
+  static TruncationSpec tol(double eps) {
+    TruncationSpec s;
+    s.tolerance = eps;
+    return s;
+  }
+};
+
+struct SpectralReport {  // rank_reduction.hpp:49-67
+  std::array<std::vector<double>, 3> singular_values;
+  Dims3 chosen_ranks{0, 0, 0};
+  double bound_abs = 0, bound_rel = 0, weight_norm = 0, input_norm = 0, stability_constant = 0;
+  bool stability_ok = false;
+  std::array<bool, 3> tie_at_cutoff{false, false, false};
+  double tail(int mode) const {
+    double s = 0;
+    for (size_t k = size_t(chosen_ranks[mode]); k < singular_values[mode].size(); ++k)
+      s += singular_values[mode][k] * singular_values[mode][k];
+    return std::sqrt(s);
+  }
+};
+
+// Device-resident reference tensor (reference.hpp:65-80).
+class ReferenceTensor {
+ public:
+  ReferenceTensor(b200::Context& ctx, latsum_reference* h, KernelSpec k, UniformGrid base, int M)
+      : ctx_(&ctx), h_(h, latsum_reference_destroy), kernel(k), base_grid(base), M(M) {
+    int r = 0;
+    double c0 = 0, sh[2];
+    latsum_reference_info(h, &r, &c0, sh);
+    rank_ = r;
+    step_constant = c0;
+    shell_a = sh[0];
+    shell_A = sh[1];
+  }
+  Index rank() const { return rank_; }
+  std::vector<double> factor(int mode) const {  // canonical.factor(mode): 2N x R
+    std::vector<double> f(size_t(2 * base_grid.n[mode]) * rank_);
+    ctx_->check(latsum_reference_factor(ctx_->get(), h_.get(), mode, f.data()));
+    return f;
+  }
+  std::vector<double> weights() const {
+    std::vector<double> w(rank_);
+    b200::throw_status(latsum_reference_weights(h_.get(), w.data()), "reference weights");
+    return w;
+  }
+  latsum_reference* handle() const { return h_.get(); }
+  b200::Context& ctx() const { return *ctx_; }
+
+  KernelSpec kernel;
+  UniformGrid base_grid;
+  int M = 0;
+  double step_constant = 0, shell_a = 0, shell_A = 0;
+
+ private:
+  b200::Context* ctx_;
+  std::shared_ptr<latsum_reference> h_;
+  Index rank_ = 0;
+};
+
+inline ReferenceTensor build_reference_canonical(const KernelSpec& kernel, const UniformGrid& grid,
+                                                 int M, double step_constant = 0.0,
+                                                 b200::Context& ctx = b200::Context::default_context()) {
+  latsum_reference* h = nullptr;
+  ctx.check(latsum_reference_build(ctx.get(), kernel.family, kernel.lambda, grid.n.data(),
+                                   grid.box.data(), M, step_constant, &h));
+  return ReferenceTensor(ctx, h, kernel, grid, M);
+}
+
+// Device-resident canonical tensor (canonical.hpp:19-202).
+class CanonicalTensor {
+ public:
+  CanonicalTensor(b200::Context& ctx, latsum_canonical* h)
+      : ctx_(&ctx), h_(h, latsum_canonical_destroy) {
+    latsum_canonical_info(h, dims_.data(), &rank_, dict_.data(), &merged_);
+  }
+  const Dims3& dims() const { return dims_; }
+  Index rank() const { return rank_; }
+  std::vector<double> weights() const {
+    std::vector<double> w(rank_);
+    b200::throw_status(latsum_canonical_weights(h_.get(), w.data()), "canonical weights");
+    return w;
+  }
+  std::vector<double> factor(int mode) const {  // N_l x M_c, column-major
+    std::vector<double> f(size_t(dims_[mode]) * rank_);
+    ctx_->check(latsum_canonical_factor(ctx_->get(), h_.get(), mode, f.data()));
+    return f;
+  }
+  double entry(Index i, Index j, Index k) const {
+    const int64_t p[3] = {i, j, k};
+    double v = 0;
+    ctx_->check(latsum_canonical_entries(ctx_->get(), h_.get(), p, 1, &v));
+    return v;
+  }
+  latsum_canonical* handle() const { return h_.get(); }
+  b200::Context& ctx() const { return *ctx_; }
+
+ private:
+  b200::Context* ctx_;
+  std::shared_ptr<latsum_canonical> h_;
+  Dims3 dims_{0, 0, 0}, dict_{0, 0, 0};
+  Index rank_ = 0, merged_ = 0;
+};
+
+// Device-resident Tucker tensor (tucker.hpp:19-73).
+class TuckerTensor {
+ public:
+  TuckerTensor(b200::Context& ctx, latsum_tucker* h) : ctx_(&ctx), h_(h, latsum_tucker_destroy) {
+    latsum_tucker_info(h, dims_.data(), ranks_.data());
+  }
+  const Dims3& dims() const { return dims_; }
+  const Dims3& ranks() const { return ranks_; }
+  double entry(Index i, Index j, Index k) const {
+    const int64_t p[3] = {i, j, k};
+    double v = 0;
+    ctx_->check(latsum_tucker_entries(ctx_->get(), h_.get(), p, 1, &v));
+    return v;
+  }
+  std::vector<double> core() const {
+    std::vector<double> c(size_t(ranks_[0]) * ranks_[1] * ranks_[2]);
+    ctx_->check(latsum_tucker_core(ctx_->get(), h_.get(), c.data()));
+    return c;
+  }
+  std::vector<double> factor(int mode) const {
+    std::vector<double> f(size_t(dims_[mode]) * ranks_[mode]);
+    ctx_->check(latsum_tucker_factor(ctx_->get(), h_.get(), mode, f.data()));
+    return f;
+  }
+  latsum_tucker* handle() const { return h_.get(); }
+  b200::Context& ctx() const { return *ctx_; }
+
+ private:
+  b200::Context* ctx_;
+  std::shared_ptr<latsum_tucker> h_;
+  Dims3 dims_{0, 0, 0}, ranks_{0, 0, 0};
+};
+
+// to_dense (tucker.hpp:172-178) with the reference's 1e7-entry guard.
+inline std::vector<double> to_dense(const TuckerTensor& t, Index guard = 10'000'000) {
+  const Dims3 d = t.dims();
+  if (d[0] * d[1] * d[2] > guard)
+    throw std::length_error("dense materialization of " + std::to_string(d[0] * d[1] * d[2]) +
+                            " entries exceeds the guard limit " + std::to_string(guard));
+  std::vector<double> out(size_t(d[0] * d[1] * d[2]));
+  const int64_t lo[3] = {0, 0, 0}, hi[3] = {d[0], d[1], d[2]};
+  if (!out.empty()) t.ctx().check(latsum_tucker_eval_box(t.ctx().get(), t.handle(), lo, hi, out.data()));
+  return out;
+}
+
+namespace detail {
+struct ShiftTables {
+  std::vector<int64_t> counts, shifts, dshifts;
+  std::vector<double> charges, dcharges;
+};
+inline long lround_away(double x) { return std::lround(x); }
+}  // namespace detail
+
+// Rank-R canonical lattice sum + additive defects on the lattice_grid of `geom`
+// (assembled_sum_canonical + defected_sum without truncation).
+inline CanonicalTensor defected_sum(const ReferenceTensor& ref, const LatticeGeometry& geom,
+                                    Index n_per_cell,
+                                    const std::vector<SublatticePlacement>* subs = nullptr) {
+  detail::ShiftTables t;
+  auto add_block = [&](const LatticeGeometry& g, const std::array<double, 3>& off) {
+    for (int l = 0; l < 3; ++l) {
+      const auto ks = g.active_set(l);
+      t.counts.push_back(int64_t(ks.size()));
+      for (int k : ks)
+        t.shifts.push_back(int64_t(k) * n_per_cell + detail::lround_away(off[l] * double(n_per_cell)));
+    }
+    t.charges.push_back(g.base_charge);
+  };
+  if (subs && !subs->empty()) {
+    for (const auto& s : *subs) add_block(s.geom, s.offset_cells);
+  } else {
+    add_block(geom, {0, 0, 0});
+  }
+  for (const auto& d : geom.defects)
+    for (const auto& s : d.sites) {
+      for (int l = 0; l < 3; ++l)
+        t.dshifts.push_back(int64_t(s[l]) * n_per_cell + detail::lround_away(d.grid_offset[l]));
+      t.dcharges.push_back(d.charge);
+    }
+  b200::Context& ctx = ref.ctx();
+  latsum_canonical* h = nullptr;
+  ctx.check(latsum_canonical_assemble(ctx.get(), ref.handle(), int64_t(t.charges.size()),
+                                      t.counts.data(), t.shifts.data(), t.charges.data(),
+                                      int64_t(t.dcharges.size()), t.dshifts.data(),
+                                      t.dcharges.data(), &h));
+  return CanonicalTensor(ctx, h);
+}
+
+inline CanonicalTensor assembled_sum_canonical(const ReferenceTensor& ref,
+                                               const LatticeGeometry& geom, Index n_per_cell) {
+  if (!geom.defects.empty())
+    throw std::invalid_argument("assembled_sum_canonical: geometry carries defects; use defected_sum");
+  return defected_sum(ref, geom, n_per_cell);
+}
+
+inline CanonicalTensor sublattice_union_sum(const std::vector<SublatticePlacement>& subs,
+                                            const ReferenceTensor& ref,
+                                            const LatticeGeometry& parent, Index n_per_cell) {
+  if (subs.empty()) throw std::invalid_argument("sublattice_union_sum: no sublattices");
+  LatticeGeometry p = parent;
+  p.defects.clear();
+  return defected_sum(ref, p, n_per_cell, &subs);
+}
+
+inline std::pair<TuckerTensor, SpectralReport> rhosvd(const CanonicalTensor& a,
+                                                      const TruncationSpec& spec,
+                                                      int deflate = LATSUM_DEFLATE_AUTO) {
+  if (!spec.ranks && !spec.tolerance)
+    throw std::invalid_argument("TruncationSpec: need ranks or tolerance");
+  b200::Context& ctx = a.ctx();
+  latsum_tucker* h = nullptr;
+  latsum_spectral_report rep;
+  ctx.check(latsum_rhosvd(ctx.get(), a.handle(), spec.ranks ? spec.ranks->data() : nullptr,
+                          spec.tolerance.value_or(0.0), deflate, &h, &rep));
+  TuckerTensor t(ctx, h);
+  SpectralReport out;
+  for (int l = 0; l < 3; ++l) {
+    out.singular_values[l].resize(size_t(rep.n_singular[l]));
+    latsum_tucker_singular_values(h, l, out.singular_values[l].data());
+    out.chosen_ranks[l] = rep.chosen_ranks[l];
+    out.tie_at_cutoff[l] = rep.tie_at_cutoff[l] != 0;
+  }
+  out.bound_abs = rep.bound_abs;
+  out.bound_rel = rep.bound_rel;
+  out.weight_norm = rep.weight_norm;
+  out.input_norm = rep.input_norm;
+  out.stability_constant = rep.stability_constant;
+  out.stability_ok = rep.stability_ok != 0;
+  return {std::move(t), out};
+}
+
+}  // namespace latsum

@@ -1,0 +1,107 @@
+// C++ drop-in check: the reference's own unit-test scenarios written against
+// include/latsum_b200/latsum.hpp (reference names, exception types), run on the GPU.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "latsum_b200/latsum.hpp"
+
+using namespace latsum;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);    \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+
+int main() {
+  // reference side matrices: 2n rows, R = 2M+1, unit columns (test_reference.cpp:49-60)
+  auto grid = UniformGrid::cubic(4.0, 32);
+  auto ref = build_reference_canonical(KernelSpec::newton(), grid, 10);
+  CHECK(ref.rank() == 21);
+  const auto f = ref.factor(0);
+  CHECK(f.size() == size_t(64 * 21));
+  double nrm = 0;
+  for (int i = 0; i < 64; ++i) nrm += f[i] * f[i];
+  CHECK(std::abs(nrm - 1.0) < 1e-14);
+
+  // odd cell counts are rejected (test_grid_geometry.cpp:20-26)
+  try {
+    build_reference_canonical(KernelSpec::newton(), UniformGrid::cubic(1.0, 7), 4);
+    CHECK(false);
+  } catch (const std::invalid_argument&) {
+  }
+
+  // single vacancy: rank 2R and entry = base - window (test_lattice_sum.cpp:198-232)
+  LatticeGeometry geom;
+  geom.cells = {4, 4, 4};
+  const Index n = 16;
+  auto ref2 = build_reference_canonical(KernelSpec::newton(), lattice_grid(geom, n), 8);
+  auto base = assembled_sum_canonical(ref2, geom, n);
+  CHECK(base.rank() == ref2.rank());
+  LatticeGeometry vg = geom;
+  DefectSpec vac;
+  vac.sites = {{0, 0, 0}};
+  vac.charge = -1.0;
+  vg.defects = {vac};
+  auto defected = defected_sum(ref2, vg, n);
+  CHECK(defected.rank() == 2 * ref2.rank());
+  double worst = 0, scale = 0;
+  for (int p = 0; p < 50; ++p) {
+    const Index i = (7 * p) % 64, j = (13 * p + 5) % 64, k = (29 * p + 3) % 64;
+    const double d = defected.entry(i, j, k), b = base.entry(i, j, k);
+    worst = std::fmax(worst, std::abs(b - d));
+    scale = std::fmax(scale, std::abs(b));
+  }
+  CHECK(worst > 0 && worst < scale);  // the vacancy removes a positive window
+
+  // window overflow names the mode (grid.hpp:111-122)
+  LatticeGeometry og = geom;
+  DefectSpec far;
+  far.sites = {{0, 9, 0}};
+  far.kind = DefectKind::impurity;
+  far.charge = 1.0;
+  og.defects = {far};
+  try {
+    defected_sum(ref2, og, n);
+    CHECK(false);
+  } catch (const WindowOverflowError& e) {
+    CHECK(e.mode() == 2);
+  }
+
+  // rhosvd: fixed ranks reproduce an exact low-rank input (test_rank_reduction.cpp:22-41)
+  LatticeGeometry small;
+  small.cells = {2, 2, 2};
+  auto ref3 = build_reference_canonical(KernelSpec::newton(), lattice_grid(small, 8), 3);
+  auto can = assembled_sum_canonical(ref3, small, 8);
+  auto [t, rep] = rhosvd(can, TruncationSpec::fixed_ranks(10, 10, 10));
+  for (int l = 0; l < 3; ++l) CHECK(rep.chosen_ranks[l] <= 7);
+  const auto dense = to_dense(t);
+  double err = 0, mx = 0;
+  for (Index k = 0; k < 16; ++k)
+    for (Index j = 0; j < 16; ++j)
+      for (Index i = 0; i < 16; ++i) {
+        const double c = can.entry(i, j, k);
+        err = std::fmax(err, std::abs(dense[i + 16 * (j + 16 * k)] - c));
+        mx = std::fmax(mx, std::abs(c));
+      }
+  CHECK(err <= 1e-12 * mx);
+  CHECK(rep.input_norm > 0 && rep.weight_norm > 0);
+
+  // tolerance-driven truncation stays within the bound
+  auto [t2, rep2] = rhosvd(defected, TruncationSpec::tol(1e-6));
+  CHECK(t2.ranks()[0] >= 1 && t2.ranks()[0] <= 64);
+  CHECK(rep2.bound_abs >= 0.0);
+
+  try {
+    rhosvd(can, TruncationSpec{});
+    CHECK(false);
+  } catch (const std::invalid_argument&) {
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}

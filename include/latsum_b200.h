@@ -30,7 +30,8 @@ enum {
   LATSUM_ERR_OUT_OF_MEMORY = 5,
   LATSUM_ERR_LENGTH = 6,           /* std::length_error: dense guard (tensor3.hpp:101-105) */
   LATSUM_ERR_NOT_IMPLEMENTED = 7,  /* NotImplementedError (quadrature.hpp:288-290) */
-  LATSUM_ERR_NCCL = 8
+  LATSUM_ERR_NCCL = 8,
+  LATSUM_ERR_IO = 9                /* TensorIoError (tensor_io.hpp:27-29) */
 };
 
 enum { LATSUM_NEWTON = 0, LATSUM_YUKAWA = 1 }; /* kernel.hpp:17 KernelFamily (gauss type) */
@@ -164,6 +165,15 @@ int latsum_rhosvd(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* r
 int latsum_rhosvd_ex(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* ranks,
                      double tolerance, int deflate, int flags, latsum_tucker** out,
                      latsum_spectral_report* report);
+/* canonical_to_tucker (rank_reduction.hpp:280-306): rhosvd, then ALS refinement
+ * (als_refine, :232-274; up to max_als_sweeps, stagnation tolerance as TruncationSpec's)
+ * and, with a tolerance and no ranks, shrink_core (:129-168).  report.chosen_ranks are the
+ * final (shrunk) ranks; als_sweeps (nullable) returns the sweeps run.  ALS needs the
+ * contracted unfolding (r^2 x d doubles) on the device: feasible for BASELINE cfg2/3. */
+int latsum_canonical_to_tucker(latsum_ctx* ctx, const latsum_canonical* can, const int64_t* ranks,
+                               double tolerance, int max_als_sweeps, double als_stagnation_tol,
+                               latsum_tucker** out, latsum_spectral_report* report,
+                               int* als_sweeps);
 void latsum_tucker_destroy(latsum_tucker* t);
 /* 1 when the dense core exists (latsum_tucker_core), 0 for a factors-only result. */
 int latsum_tucker_has_core(const latsum_tucker* t);
@@ -194,6 +204,31 @@ int latsum_sum_to_tucker(latsum_ctx* ctx, int family, double lambda, const int64
                          const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
                          const double* def_charges, double tolerance, latsum_tucker** out,
                          latsum_spectral_report* report);
+
+/* ------------------------------------------------------------------ tensors from / to host
+ * CanonicalTensor(dims, weights, factors) (canonical.hpp:203-206): columns taken as given
+ * (the caller guarantees unit norms), so rhosvd / canonical_to_tucker accept any canonical
+ * input, as the reference's do. */
+int latsum_canonical_from_host(latsum_ctx* ctx, const int64_t dims[3], int64_t rank,
+                               const double* weights, const double* f0, const double* f1,
+                               const double* f2, latsum_canonical** out);
+/* write_tensor / read_tensor (tensor_io.cpp:45-129): "LTSTNSR" v1 with the FNV-1a-64
+ * trailer, byte-compatible with the reference.  Write exactly one of can / t; read sets
+ * one of *can_out / *t_out.  Checksum, magic, version and truncation errors ->
+ * LATSUM_ERR_IO. */
+int latsum_tensor_write(latsum_ctx* ctx, const latsum_canonical* can, const latsum_tucker* t,
+                        const char* path);
+int latsum_tensor_read(latsum_ctx* ctx, const char* path, latsum_canonical** can_out,
+                       latsum_tucker** t_out);
+
+/* ------------------------------------------------------------------ verification
+ * oracle_entry (lattice_sum.hpp:656-671) on the device: the brute-force windowed sum
+ * over ns grid-shifted sources (shifts ns x 3, weights ns; enumerate_sources order,
+ * :632-653) at np probes, for cmd_verify-style checks (commands.cpp:200-284) at sizes
+ * the CPU cannot reach (BASELINE cfg5: 16.8M sources). */
+int latsum_verify_entries(latsum_ctx* ctx, const latsum_reference* ref, int64_t ns,
+                          const int64_t* shifts, const double* weights, const int64_t* probes,
+                          int64_t np, double* out);
 
 /* ------------------------------------------------------------------ utilities */
 /* Generic FP64 DMMA GEMM on device pointers (exposed for tests and benchmarks):

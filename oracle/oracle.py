@@ -485,3 +485,76 @@ def probes(dims, count: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
     return np.stack([rng.integers(0, dims[l], size=count) for l in range(3)], axis=1).astype(
         np.int64)
+
+
+# ----------------------------------------------------------------------------- canonical_to_tucker
+
+def projected_norm(F, w, Y) -> float:
+    """rank_reduction.hpp:104-113."""
+    P = [Y[l].T @ F[l] for l in range(3)]
+    g = (P[0].T @ P[0]) * (P[1].T @ P[1]) * (P[2].T @ P[2])
+    v = float(w @ (g @ w))
+    return float(np.sqrt(v)) if v > 0 else 0.0
+
+
+def als_refine(F, w, Y, ranks, max_sweeps: int = 30, stag_tol: float = 1e-8):
+    """rank_reduction.hpp:232-274 (small sizes: full kr unfolding, LAPACK SVD)."""
+    Y = [y.copy() for y in Y]
+    fit = projected_norm(F, w, Y)
+    sweeps = 0
+    for _ in range(max_sweeps):
+        for l in range(3):
+            m1, m2 = (l + 1) % 3, (l + 2) % 3
+            p1, p2 = Y[m1].T @ F[m1], Y[m2].T @ F[m2]
+            kr = (p1[:, None, :] * p2[None, :, :]).reshape(p1.shape[0] * p2.shape[0], -1) * w[None, :]
+            unf = F[l] @ kr.T
+            u, _, _ = np.linalg.svd(unf, full_matrices=False)
+            Y[l] = np.asfortranarray(u[:, :min(ranks[l], u.shape[1])])
+        nxt = projected_norm(F, w, Y)
+        sweeps += 1
+        if nxt - fit <= stag_tol * max(nxt, 1.0):
+            break
+        fit = nxt
+    return Y, sweeps
+
+
+def shrink_core(core, factors, budget2):
+    """rank_reduction.hpp:129-168."""
+    core = core.copy()
+    factors = [f.copy() for f in factors]
+    for l in range(3):
+        u = np.moveaxis(core, l, 0).reshape(core.shape[l], -1)
+        _, q = np.linalg.eigh(u @ u.T)
+        q = q[:, ::-1]
+        core = np.moveaxis(np.tensordot(q.T, np.moveaxis(core, l, 0), axes=(1, 0)), 0, l)
+        factors[l] = factors[l] @ q
+    r = list(core.shape)
+    changed = True
+    while changed and budget2 > 0:
+        changed = False
+        for l in range(3):
+            if r[l] <= 1:
+                continue
+            box = core[:r[0], :r[1], :r[2]]
+            sl = np.take(box, r[l] - 1, axis=l)
+            mass = float(np.sum(sl * sl))
+            if mass <= budget2:
+                budget2 -= mass
+                r[l] -= 1
+                changed = True
+    return core[:r[0], :r[1], :r[2]].copy(), [factors[l][:, :r[l]] for l in range(3)]
+
+
+def canonical_to_tucker(F, w, eps=None, ranks=None, max_sweeps: int = 30, stag_tol: float = 1e-8):
+    """rank_reduction.hpp:280-306 on full side matrices (small sizes)."""
+    orc = rhosvd(F, w, eps=eps, ranks=ranks, with_norm=True)
+    Y, sweeps = als_refine(F, w, orc.Z, orc.ranks, max_sweeps, stag_tol) if max_sweeps > 0 else (orc.Z, 0)
+    P = [Y[l].T @ F[l] for l in range(3)]
+    core = project_core(w, P)
+    if eps is not None and ranks is None:
+        n2 = orc.input_norm ** 2
+        err2 = max(n2 - float(np.sum(core * core)), 0.0)
+        budget2 = eps * eps * n2 - err2
+        if budget2 > 0:
+            core, Y = shrink_core(core, Y, budget2)
+    return core, Y, orc, sweeps

@@ -23,6 +23,7 @@ ERRORS = {
     6: OverflowError,     # std::length_error (dense guard)
     7: NotImplementedError,
     8: RuntimeError,      # NCCL
+    9: IOError,           # TensorIoError
 }
 
 
@@ -96,6 +97,7 @@ SIGNATURES = [
     ("latsum_canonical_eval_box_device", _I, [_P, _P, _P, _P, _P]),
     ("latsum_rhosvd", _I, [_P, _P, _P, _D, _I, _P, _P]),
     ("latsum_rhosvd_ex", _I, [_P, _P, _P, _D, _I, _I, _P, _P]),
+    ("latsum_canonical_to_tucker", _I, [_P, _P, _P, _D, _I, _D, _P, _P, _P]),
     ("latsum_tucker_destroy", None, [_P]),
     ("latsum_tucker_has_core", _I, [_P]),
     ("latsum_tucker_info", _I, [_P, _P, _P]),
@@ -107,6 +109,10 @@ SIGNATURES = [
     ("latsum_tucker_eval_box_device", _I, [_P, _P, _P, _P, _P]),
     ("latsum_sum_to_tucker", _I, [_P, _I, _D, _P, _P, _I, _D, _I64, _P, _P, _P, _I64, _P, _P,
                                   _D, _P, _P]),
+    ("latsum_verify_entries", _I, [_P, _P, _I64, _P, _P, _P, _I64, _P]),
+    ("latsum_canonical_from_host", _I, [_P, _P, _I64, _P, _P, _P, _P, _P]),
+    ("latsum_tensor_write", _I, [_P, _P, _P, ctypes.c_char_p]),
+    ("latsum_tensor_read", _I, [_P, ctypes.c_char_p, _P, _P]),
     ("latsum_dgemm_device", _I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P,
                                  _I64]),
 ]

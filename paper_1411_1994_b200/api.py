@@ -521,6 +521,97 @@ def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto",
     return t, report
 
 
+def oracle_entries(ref: ReferenceTensor, geom: Geometry, probes) -> np.ndarray:
+    """lattice_sum.hpp:656-671 brute-force windowed sum over every source of `geom`
+    (enumerate_sources order) at the probes, computed on the device."""
+    shifts, w = geom.sources()
+    pr = _i64(probes).reshape(-1, 3)
+    out = np.zeros(pr.shape[0])
+    ref.ctx.check(_lib.lib().latsum_verify_entries(ref.ctx.handle, ref.handle, shifts.shape[0],
+                                                   _p(shifts), _p(_f64(w)), _p(pr), pr.shape[0],
+                                                   _p(out)))
+    return out
+
+
+def verify(tensor, ref: ReferenceTensor, geom: Geometry, probes=500, seed: int = 0,
+           tolerance: Optional[float] = None, bound_abs: Optional[float] = None) -> dict:
+    """cmd_verify (commands.cpp:200-284): max|got - oracle| / max|oracle| over seeded
+    probes, gated by the recorded truncation bound if given, else by `tolerance`."""
+    if np.isscalar(probes):
+        rng = np.random.Generator(np.random.PCG64(seed))
+        probes = np.stack([rng.integers(0, geom.N[l], int(probes)) for l in range(3)], axis=1)
+    pr = _i64(probes).reshape(-1, 3)
+    want = oracle_entries(ref, geom, pr)
+    got = tensor.entries(pr)
+    max_abs = float(np.max(np.abs(got - want)))
+    max_mag = float(np.max(np.abs(want)))
+    rel = max_abs / max_mag if max_mag > 0 else max_abs
+    ok = (max_abs <= bound_abs) if bound_abs is not None else (
+        rel <= tolerance if tolerance is not None else True)
+    return dict(probes=int(pr.shape[0]), max_abs=max_abs, max_oracle=max_mag, normalized=rel,
+                ok=bool(ok))
+
+
+def canonical_to_tucker(can: CanonicalTensor, spec: TruncationSpec, max_als_sweeps: int = 30,
+                        als_stagnation_tol: float = 1e-8):
+    """rank_reduction.hpp:280-306: rhosvd + ALS refinement + shrink_core (tolerance mode)
+    -> (TuckerTensor, SpectralReport, als_sweeps)."""
+    spec.validate()
+    ctx = can.ctx
+    rep = _lib.LatsumReport()
+    h = ctypes.c_void_p()
+    sweeps = ctypes.c_int()
+    ranks = _i64(spec.ranks) if spec.ranks is not None else None
+    ctx.check(_lib.lib().latsum_canonical_to_tucker(
+        ctx.handle, can.handle, _p(ranks) if ranks is not None else None,
+        float(spec.tolerance or 0.0), int(max_als_sweeps), float(als_stagnation_tol),
+        ctypes.byref(h), ctypes.byref(rep), ctypes.byref(sweeps)))
+    t = TuckerTensor(ctx, h)
+    sv = []
+    for l in range(3):
+        s = np.zeros(int(rep.n_singular[l]))
+        _lib.check(_lib.lib().latsum_tucker_singular_values(h, l, _p(s)))
+        sv.append(s)
+    report = SpectralReport(
+        singular_values=sv, chosen_ranks=tuple(int(x) for x in rep.chosen_ranks),
+        bound_abs=rep.bound_abs, bound_rel=rep.bound_rel, weight_norm=rep.weight_norm,
+        input_norm=rep.input_norm, stability_constant=rep.stability_constant,
+        stability_ok=bool(rep.stability_ok), tie_at_cutoff=tuple(bool(x) for x in rep.tie_at_cutoff),
+        cutoff_margin=tuple(float(x) for x in rep.cutoff_margin),
+        deflated=tuple(bool(x) for x in rep.deflated), gram_rows=tuple(bool(x) for x in rep.gram_rows),
+        gram_size=tuple(int(x) for x in rep.gram_size), ms={})
+    return t, report, int(sweeps.value)
+
+
+def canonical_from_arrays(weights, factors, ctx: Optional[Context] = None) -> CanonicalTensor:
+    """CanonicalTensor(dims, weights, factors) (canonical.hpp:203-206): unit columns as given."""
+    ctx = ctx or default_context()
+    w = _f64(weights)
+    F = [np.asfortranarray(f, dtype=np.float64) for f in factors]
+    dims = _i64([f.shape[0] for f in F])
+    h = ctypes.c_void_p()
+    ctx.check(_lib.lib().latsum_canonical_from_host(ctx.handle, _p(dims), w.size, _p(w), _p(F[0]),
+                                                    _p(F[1]), _p(F[2]), ctypes.byref(h)))
+    return CanonicalTensor(ctx, h)
+
+
+def write_tensor(path: str, tensor):
+    """tensor_io.cpp:45-76 ("LTSTNSR" v1 + FNV-1a-64), from device-resident tensors."""
+    ctx = tensor.ctx
+    can = tensor.handle if isinstance(tensor, CanonicalTensor) else None
+    tk = tensor.handle if isinstance(tensor, TuckerTensor) else None
+    ctx.check(_lib.lib().latsum_tensor_write(ctx.handle, can, tk, str(path).encode()))
+
+
+def read_tensor(path: str, ctx: Optional[Context] = None):
+    """tensor_io.cpp:78-129: checksum-guarded read into a device-resident tensor."""
+    ctx = ctx or default_context()
+    hc, ht = ctypes.c_void_p(), ctypes.c_void_p()
+    ctx.check(_lib.lib().latsum_tensor_read(ctx.handle, str(path).encode(), ctypes.byref(hc),
+                                            ctypes.byref(ht)))
+    return CanonicalTensor(ctx, hc) if hc.value else TuckerTensor(ctx, ht)
+
+
 def reference_for(geom: Geometry, ctx: Optional[Context] = None) -> ReferenceTensor:
     kernel = KernelSpec(geom.family, geom.lam)
     return build_reference_canonical(kernel, geom.N, geom.box, geom.M, geom.C0, ctx=ctx)

@@ -16,6 +16,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <exception>
+#include <fstream>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -840,6 +841,16 @@ struct Timings {
 // Multi-GPU (column orientation): the rank owns grid rows [lo, hi) of A~, U1, A'', B, U2
 // and Z; every contraction over the grid index (the Grams, U^T U, U1^T A) is a partial
 // product all-reduced over NVLink; eigensolves run redundantly on identical Grams.
+// Spectrum and leading left singular vectors of a dense operand A (N x d) given as
+// this rank's row block At (Nb x d; all rows when not sharded): the two-pass deflated
+// Gram algorithm of reduce_mode below.  rank_fixed (nullable) selects a fixed rank
+// (clamped), else rank_for_tolerance(tol); force_deflate runs the second pass even
+// with a fixed rank (needed when the trailing kept directions sit below
+// sqrt(eps_mach) sigma_1, e.g. in the ALS unfoldings).
+void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
+                  const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
+                  bool sharded, ModeOut& out, Timings& tm);
+
 void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
                  double tol, int deflate, ModeOut& out, Timings& tm) {
   const int64_t N = can.N[l], d = can.d[l];
@@ -848,7 +859,6 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   const bool sharded = !rows && c->comm && c->nranks > 1;
   const RowBlock blk = sharded ? row_block(c, N) : RowBlock{0, N};
   const int64_t Nb = blk.n();
-  out.blk = blk;
   Timer timer(c);
   timer.start();
   std::vector<double> sq(d);
@@ -862,6 +872,21 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
     k_scale_columns<<<grid_for(Nb * d), 256, 0, c->stream>>>(At.p, Nb, d, dsq.p, At.p);
     post_launch(c);
   }
+  tm.gram += timer.stop();
+  const int64_t* rf = ranks ? ranks + l : nullptr;
+  reduce_dense(c, At, blk, N, d, n_sing, rf, tol, deflate, false, sharded, out, tm);
+}
+
+void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
+                  const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
+                  bool sharded, ModeOut& out, Timings& tm) {
+  const int64_t* ranks = rank_fixed;
+  const int l = 0;  // rank_fixed points at this operand's rank
+  const bool rows = N <= d;
+  const int64_t Nb = blk.n();
+  out.blk = blk;
+  Timer timer(c);
+  timer.start();
   const int64_t n = rows ? N : d;
   out.rows = rows ? 1 : 0;
   out.gsize = n;
@@ -893,7 +918,7 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   DBuf U1, B, G2;
   std::vector<double> mu_d;
   bool defl = false;
-  if (!ranks && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
+  if ((!ranks || force_deflate) && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
     const std::vector<double> sv = padded_sigma(lam_d);
     double n2 = 0;
     for (double v : sv) n2 += v * v;
@@ -902,7 +927,7 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
       if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
     k1 = std::max<int64_t>(k1, 1);
     nc = n - k1;
-    defl = nc > 0 && (deflate == LATSUM_DEFLATE_ALWAYS ||
+    defl = nc > 0 && (deflate == LATSUM_DEFLATE_ALWAYS || force_deflate ||
                       target * target < 1e6 * double(n) * kEpsMach * lmax);
     if (defl) {
       timer.start();
@@ -973,7 +998,8 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   int64_t r;
   if (ranks) r = std::min<int64_t>(std::max<int64_t>(ranks[l], 1), n_sing);
   else r = rank_for_tolerance(sv, tol);
-  while (r > 1 && sv[r - 1] < 1e-14 * sv[0]) --r;  // drop numerically zero directions
+  // drop numerically zero directions (rhosvd); ALS keeps exactly the requested rank
+  while (!force_deflate && r > 1 && sv[r - 1] < 1e-14 * sv[0]) --r;
   r = std::min<int64_t>(r, n);
   out.tie = r < int64_t(sv.size()) && sv[r - 1] - sv[r] <= 1e-12 * sv[0];
   if (!ranks) {
@@ -1027,13 +1053,18 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   tm.deflate += timer.stop();
 }
 
-double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
+// sqrt(w^T (G0 o G1 o G2) w) over the merged terms with G_l = E_l^T E_l (d_l x d_l)
+// for per-mode column sets E_l (rows x d_l): the dictionary itself gives norm_f
+// (canonical.hpp:148-162); projected columns Y_l^T D_l give the ALS objective
+// projected_norm (rank_reduction.hpp:104-113).
+double hadamard_norm(latsum_ctx* c, const latsum_canonical& can, const double* const E[3],
+                     const int64_t rows[3]) {
   if (can.T == 0) return 0.0;
   DBuf G[3];
   for (int l = 0; l < 3; ++l) {
     G[l].alloc(c, size_t(can.d[l]) * can.d[l]);
-    gemm(c, true, false, can.d[l], can.d[l], can.N[l], 1.0, can.dict[l].p, can.N[l],
-         can.dict[l].p, can.N[l], 0.0, G[l].p, can.d[l], tagged("gemm_norm_gram"));
+    gemm(c, true, false, can.d[l], can.d[l], rows[l], 1.0, E[l], rows[l], E[l], rows[l], 0.0,
+         G[l].p, can.d[l], tagged("gemm_norm_gram"));
   }
   DBuf part(c, can.T), sum(c, 1);
   ProfScope ps(c, "norm_hadamard", 3.0 * double(can.T) * double(can.T));
@@ -1049,9 +1080,50 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
   return s > 0.0 ? std::sqrt(s) : 0.0;
 }
 
+double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
+  const double* E[3] = {can.dict[0].p, can.dict[1].p, can.dict[2].p};
+  return hadamard_norm(c, can, E, can.N);
+}
+
 // core(a,b,c) = sum_t w_t P0(a,c0_t) P1(b,c1_t) P2(c,c2_t)  (project_core,
 // rank_reduction.hpp:88-100) as X_a = G1[:, seg_a] G2[:, seg_a]^T over the terms
 // grouped by their mode-1 column a (one segmented GEMM), then core = P0 X^T.
+// The merged terms grouped by their mode-m column, with the other two modes' projected
+// columns gathered (G1 weighted): X_j = G1[:, seg_j] G2[:, seg_j]^T is then one
+// segmented GEMM (the "contracted unfolding" of project_core and of ALS).
+struct GroupedTerms {
+  int o1, o2;
+  DVec<int64_t> seg;
+  DBuf G1, G2;
+  GroupedTerms(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
+               int m)
+      : o1(m == 0 ? 1 : 0), o2(m == 2 ? 1 : 2) {
+    const int64_t T = can.T;
+    DVec<int32_t> c1, c2;
+    DVec<double> tw;
+    c1.upload(c, can.stc[m][o1]);
+    c2.upload(c, can.stc[m][o2]);
+    tw.upload(c, can.stw[m]);
+    seg.upload(c, can.sseg[m]);
+    G1.alloc(c, size_t(r[o1]) * T);
+    G2.alloc(c, size_t(r[o2]) * T);
+    k_gather_scale<<<grid_for(r[o1] * T), 256, 0, c->stream>>>(P[o1].p, r[o1], r[o1], c1.p, tw.p,
+                                                               T, G1.p);
+    post_launch(c);
+    k_gather_scale<<<grid_for(r[o2] * T), 256, 0, c->stream>>>(P[o2].p, r[o2], r[o2], c2.p,
+                                                               nullptr, T, G2.p);
+    post_launch(c);
+  }
+  // X (r_o1 r_o2 x na): columns j = a0 .. a0+na-1 of the grouped unfolding
+  void form(latsum_ctx* c, const int64_t r[3], int64_t T, int64_t a0, int64_t na, double* X) const {
+    GemmOpts o = tagged("gemm_core_x");
+    o.batch = na;
+    o.sC = r[o1] * r[o2];
+    o.kseg = seg.p + a0;
+    gemm(c, false, true, r[o1], r[o2], T, 1.0, G1.p, r[o1], G2.p, r[o2], 0.0, X, r[o1], o);
+  }
+};
+
 // The mode whose dictionary is smallest is contracted last: cost 2 r1 r2 r3 d_m.
 int core_mode(const latsum_canonical& can) {
   int m = 0;
@@ -1076,30 +1148,13 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
     CK(cudaMemsetAsync(core, 0, sizeof(double) * rall, c->stream));
     return;
   }
-  DVec<int32_t> c1, c2;
-  DVec<double> tw;
-  DVec<int64_t> seg;
-  c1.upload(c, can.stc[m][o1]);
-  c2.upload(c, can.stc[m][o2]);
-  tw.upload(c, can.stw[m]);
-  seg.upload(c, can.sseg[m]);
-  DBuf G1(c, size_t(r[o1]) * T), G2(c, size_t(r[o2]) * T);
-  k_gather_scale<<<grid_for(r[o1] * T), 256, 0, c->stream>>>(P[o1].p, r[o1], r[o1], c1.p, tw.p, T,
-                                                             G1.p);
-  post_launch(c);
-  k_gather_scale<<<grid_for(r[o2] * T), 256, 0, c->stream>>>(P[o2].p, r[o2], r[o2], c2.p, nullptr,
-                                                             T, G2.p);
-  post_launch(c);
+  GroupedTerms gt(c, can, P, r, m);
   const int64_t budget = workspace_budget();  // doubles of X per chunk
   const int64_t ac = balanced_chunk(dm - a_lo, std::min<int64_t>(budget / std::max<int64_t>(ro, 1), 65535), 64);
   DBuf X(c, size_t(ro) * ac);
   for (int64_t a0 = a_lo; a0 < dm; a0 += ac) {
     const int64_t na = std::min(ac, dm - a0);
-    GemmOpts o = tagged("gemm_core_x");
-    o.batch = na;
-    o.sC = ro;
-    o.kseg = seg.p + a0;
-    gemm(c, false, true, r[o1], r[o2], T, 1.0, G1.p, r[o1], G2.p, r[o2], 0.0, X.p, r[o1], o);
+    gt.form(c, r, T, a0, na, X.p);
     const double beta = a0 == a_lo ? 0.0 : 1.0;
     if (m == 0) {        // core (r0 x r1 r2) = P0[:, j] X^T
       gemm(c, false, true, r[0], ro, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, ro, beta, core, r[0],
@@ -1324,6 +1379,248 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   rep.ms_core = tm.core;
   rep.ms_norm = tm.norm;
   rep.ms_total = total.stop();
+}
+
+// ------------------------------------------------------------------ canonical_to_tucker
+double device_scalar(latsum_ctx* c, const double* d) {
+  double h = 0;
+  CK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+// P_l = Y_l^T D_l (r_l x d_l) for every mode
+void project_factors(latsum_ctx* c, const latsum_canonical& can, const DBuf Y[3], const int64_t r[3],
+                     DBuf P[3]) {
+  for (int l = 0; l < 3; ++l) {
+    P[l].alloc(c, size_t(r[l]) * can.d[l]);
+    gemm(c, true, false, r[l], can.d[l], can.N[l], 1.0, Y[l].p, can.N[l], can.dict[l].p, can.N[l],
+         0.0, P[l].p, r[l], tagged("gemm_project"));
+  }
+}
+
+// One ALS step for mode l (rank_reduction.hpp:243-256): the top-r_l left singular vectors
+// of the contracted unfolding unf = A_l kr^T.  With the dictionary, unf = D_l X^T where X
+// (r_o1 r_o2 x d_l) is the grouped unfolding over c_l.  unf is materialised and reduced
+// with the same two-pass deflated Gram as RHOSVD (fixed rank, second pass forced): the
+// trailing kept directions carry relative mass ~eps^2, which a single Gram cannot resolve.
+void als_mode_update(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3],
+                     const int64_t r[3], int l, DBuf& Y) {
+  const int64_t N = can.N[l], d = can.d[l];
+  GroupedTerms gt(c, can, P, r, l);
+  const int64_t R2 = r[gt.o1] * r[gt.o2];
+  require(double(R2) * double(d + N) <= double(workspace_budget()),
+          "als_refine: contracted unfolding too large for the device (ALS is out of scope at "
+          "this size)");
+  DBuf X(c, size_t(R2) * d);
+  for (int64_t a0 = 0; a0 < d; a0 += 65535)
+    gt.form(c, r, can.T, a0, std::min<int64_t>(65535, d - a0), X.p + a0 * R2);
+  DBuf unf(c, size_t(N) * R2);
+  gemm(c, false, true, N, R2, d, 1.0, can.dict[l].p, N, X.p, R2, 0.0, unf.p, N, tagged("gemm_als"));
+  X.release();
+  const int64_t n_sing = std::min<int64_t>(N, R2);
+  const int64_t keep = std::min<int64_t>(r[l], n_sing);
+  ModeOut mo;
+  Timings tm;
+  reduce_dense(c, unf, RowBlock{0, N}, N, R2, n_sing, &keep, 0.0, LATSUM_DEFLATE_ALWAYS,
+               /*force_deflate=*/true, /*sharded=*/false, mo, tm);
+  require(mo.r == r[l], "als_refine: unfolding rank below the requested Tucker rank");
+  Y = std::move(mo.Z);
+}
+
+double projected_norm(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3],
+                      const int64_t r[3]) {
+  const double* E[3] = {P[0].p, P[1].p, P[2].p};
+  return hadamard_norm(c, can, E, r);
+}
+
+// shrink_core (rank_reduction.hpp:129-168): HOSVD rotation of the core per mode, then
+// greedy removal of trailing slices while the discarded mass fits in budget2.
+void shrink_core(latsum_ctx* c, latsum_tucker& t, double budget2) {
+  int64_t r[3] = {t.r[0], t.r[1], t.r[2]};
+  const int64_t tot = r[0] * r[1] * r[2];
+  for (int l = 0; l < 3; ++l) {
+    const int64_t rl = r[l];
+    DBuf G(c, size_t(rl) * rl), W(c, rl), q(c, size_t(rl) * rl), nc(c, size_t(tot));
+    DBuf swp;
+    if (l == 0) {
+      gemm(c, false, true, r[0], r[0], r[1] * r[2], 1.0, t.core.p, r[0], t.core.p, r[0], 0.0, G.p,
+           r[0], tagged("gemm_shrink"));
+    } else if (l == 2) {
+      gemm(c, true, false, r[2], r[2], r[0] * r[1], 1.0, t.core.p, r[0] * r[1], t.core.p,
+           r[0] * r[1], 0.0, G.p, r[2], tagged("gemm_shrink"));
+    } else {
+      swp.alloc(c, size_t(tot));
+      k_swap01<<<grid_for(tot), 256, 0, c->stream>>>(t.core.p, r[0], r[1], r[2], swp.p);
+      post_launch(c);
+      gemm(c, false, true, r[1], r[1], r[0] * r[2], 1.0, swp.p, r[1], swp.p, r[1], 0.0, G.p, r[1],
+           tagged("gemm_shrink"));
+    }
+    syevd(c, rl, G.p, W.p);
+    k_reverse_columns<<<grid_for(rl * rl), 256, 0, c->stream>>>(G.p, rl, rl, rl, q.p);  // descending
+    post_launch(c);
+    // core <- core x_l q^T
+    if (l == 0) {
+      gemm(c, true, false, r[0], r[1] * r[2], r[0], 1.0, q.p, r[0], t.core.p, r[0], 0.0, nc.p, r[0],
+           tagged("gemm_shrink"));
+    } else if (l == 2) {
+      gemm(c, false, false, r[0] * r[1], r[2], r[2], 1.0, t.core.p, r[0] * r[1], q.p, r[2], 0.0,
+           nc.p, r[0] * r[1], tagged("gemm_shrink"));
+    } else {
+      DBuf tmp(c, size_t(tot));
+      gemm(c, true, false, r[1], r[0] * r[2], r[1], 1.0, q.p, r[1], swp.p, r[1], 0.0, tmp.p, r[1],
+           tagged("gemm_shrink"));
+      k_swap01<<<grid_for(tot), 256, 0, c->stream>>>(tmp.p, r[1], r[0], r[2], nc.p);
+      post_launch(c);
+    }
+    t.core = std::move(nc);
+    DBuf U(c, size_t(t.N[l]) * rl);
+    gemm(c, false, false, t.N[l], rl, rl, 1.0, t.U[l].p, t.N[l], q.p, rl, 0.0, U.p, t.N[l],
+         tagged("gemm_shrink"));
+    t.U[l] = std::move(U);
+  }
+  int64_t b[3] = {r[0], r[1], r[2]};
+  DBuf m(c, 1);
+  bool changed = true;
+  while (changed && budget2 > 0.0) {
+    changed = false;
+    for (int l = 0; l < 3; ++l) {
+      if (b[l] <= 1) continue;
+      k_slice_mass<<<1, 512, 0, c->stream>>>(t.core.p, r[0], r[1], l, b[l] - 1, b[0], b[1], b[2], m.p);
+      post_launch(c);
+      const double mass = device_scalar(c, m.p);
+      if (mass <= budget2) {
+        budget2 -= mass;
+        --b[l];
+        changed = true;
+      }
+    }
+  }
+  if (b[0] != r[0] || b[1] != r[1] || b[2] != r[2]) {
+    DBuf nc(c, size_t(b[0]) * b[1] * b[2]);
+    k_crop<<<grid_for(b[0] * b[1] * b[2]), 256, 0, c->stream>>>(t.core.p, r[0], r[1], b[0], b[1],
+                                                                b[2], nc.p);
+    post_launch(c);
+    t.core = std::move(nc);
+    for (int l = 0; l < 3; ++l) {
+      DBuf U(c, size_t(t.N[l]) * b[l]);
+      CK(cudaMemcpyAsync(U.p, t.U[l].p, sizeof(double) * t.N[l] * b[l], cudaMemcpyDeviceToDevice,
+                         c->stream));
+      t.U[l] = std::move(U);
+      t.r[l] = b[l];
+    }
+  }
+}
+
+// canonical_to_tucker (rank_reduction.hpp:280-306): RHOSVD initial guess, ALS refinement
+// (up to max_sweeps, stop when the projected norm stagnates), orthogonal core
+// projection, and shrink_core in tolerance mode.
+void canonical_to_tucker_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks,
+                              double tol, int max_sweeps, double stag_tol, latsum_tucker& t,
+                              latsum_spectral_report& rep, int* sweeps_done) {
+  rhosvd_impl(c, can, ranks, tol, LATSUM_DEFLATE_AUTO, t, rep, /*form=*/false);
+  if (sweeps_done) *sweeps_done = 0;
+  if (rep.input_norm == 0.0) {
+    if (!t.has_core) {
+      t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
+      CK(cudaMemsetAsync(t.core.p, 0, sizeof(double) * t.r[0] * t.r[1] * t.r[2], c->stream));
+      t.has_core = true;
+    }
+    return;
+  }
+  const int64_t* r = t.r;
+  DBuf P[3];
+  project_factors(c, can, t.U, r, P);
+  if (max_sweeps > 0) {
+    double fit = projected_norm(c, can, P, r);
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+      for (int l = 0; l < 3; ++l) {
+        DBuf Y;
+        als_mode_update(c, can, P, r, l, Y);
+        t.U[l] = std::move(Y);
+        P[l].alloc(c, size_t(r[l]) * can.d[l]);
+        gemm(c, true, false, r[l], can.d[l], can.N[l], 1.0, t.U[l].p, can.N[l], can.dict[l].p,
+             can.N[l], 0.0, P[l].p, r[l], tagged("gemm_project"));
+      }
+      const double next = projected_norm(c, can, P, r);
+      if (sweeps_done) *sweeps_done = sweep + 1;
+      if (next - fit <= stag_tol * std::max(next, 1.0)) break;
+      fit = next;
+    }
+  }
+  t.core.alloc(c, size_t(r[0]) * r[1] * r[2]);
+  form_core(c, can, P, r, t.core.p, core_mode(can));
+  t.has_core = true;
+  for (int l = 0; l < 3; ++l) t.P[l] = std::move(P[l]);
+  if (tol > 0.0 && !ranks) {
+    const double n2 = rep.input_norm * rep.input_norm;
+    DBuf m(c, 1);
+    k_sumsq<<<1, 1024, 0, c->stream>>>(t.core.p, r[0] * r[1] * r[2], m.p);
+    post_launch(c);
+    const double fit2 = device_scalar(c, m.p);
+    const double err2 = std::max(n2 - fit2, 0.0);
+    const double budget2 = tol * tol * n2 - err2;
+    if (budget2 > 0.0) {
+      shrink_core(c, t, budget2);
+      t.T = 0;  // the projected factors no longer match the rotated/cropped basis
+    }
+  }
+  for (int l = 0; l < 3; ++l) rep.chosen_ranks[l] = t.r[l];
+}
+
+// ------------------------------------------------------------------ tensor IO
+// "LTSTNSR" v1 (tensor_io.hpp:12-24, tensor_io.cpp:45-129): 7-byte magic, version 1, tag
+// 'C'/'T', 3 zero bytes, u32 dims[3]; canonical: u32 R, R weights, three N_l x R side
+// matrices; tucker: u32 ranks[3], core, three factors; f64 little-endian, column-major;
+// trailer = FNV-1a-64 of every preceding byte.
+struct Fnv {
+  uint64_t h = 0xcbf29ce484222325ull;
+  void add(const void* data, size_t n) {
+    const auto* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) {
+      h ^= p[i];
+      h *= 0x100000001b3ull;
+    }
+  }
+};
+
+struct FileSink {
+  std::ofstream os;
+  Fnv fnv;
+  explicit FileSink(const std::string& path) : os(path, std::ios::binary | std::ios::trunc) {
+    if (!os) throw Error(LATSUM_ERR_IO, "cannot open " + path + " for writing");
+  }
+  void put(const void* d, size_t n) {
+    fnv.add(d, n);
+    os.write(static_cast<const char*>(d), std::streamsize(n));
+    if (!os) throw Error(LATSUM_ERR_IO, "short write");
+  }
+  void u32(uint32_t v) { put(&v, 4); }
+  // device buffer -> file in 64 MB chunks
+  void device(latsum_ctx* c, const double* dptr, size_t count) {
+    std::vector<double> h(std::min<size_t>(count, size_t(8) << 20));
+    for (size_t o = 0; o < count; o += h.size()) {
+      const size_t n = std::min(h.size(), count - o);
+      CK(cudaMemcpyAsync(h.data(), dptr + o, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      put(h.data(), n * sizeof(double));
+    }
+  }
+  void finish() {
+    const uint64_t sum = fnv.h;
+    os.write(reinterpret_cast<const char*>(&sum), 8);
+    if (!os) throw Error(LATSUM_ERR_IO, "short write");
+  }
+};
+
+void write_header(FileSink& f, char tag, const int64_t dims[3]) {
+  const char magic[7] = {'L', 'T', 'S', 'T', 'N', 'S', 'R'};
+  f.put(magic, 7);
+  const char head[4] = {char(1), tag, 0, 0};
+  f.put(head, 4);
+  const char pad = 0;
+  f.put(&pad, 1);
+  for (int l = 0; l < 3; ++l) f.u32(uint32_t(dims[l]));
 }
 
 // ------------------------------------------------------------------ stage 4
@@ -1875,6 +2172,215 @@ int latsum_sum_to_tucker(latsum_ctx* c, int family, double lambda, const int64_t
     rhosvd_impl(c, can, nullptr, tolerance, LATSUM_DEFLATE_AUTO, *t, rep);
     if (report) *report = rep;
     *out = t.release();
+  });
+}
+
+int latsum_canonical_from_host(latsum_ctx* c, const int64_t dims[3], int64_t rank,
+                               const double* weights, const double* f0, const double* f1,
+                               const double* f2, latsum_canonical** out) {
+  return guarded(c, [&] {
+    require(dims && out && rank >= 0 && (rank == 0 || (weights && f0 && f1 && f2)),
+            "latsum_canonical_from_host: bad argument");
+    require(rank < (int64_t(1) << 21), "latsum_canonical_from_host: rank too large");
+    auto can = std::make_unique<latsum_canonical>();
+    const double* f[3] = {f0, f1, f2};
+    can->R = can->Rd = 1;
+    can->Mc = can->T = rank;
+    can->weights.assign(weights, weights + rank);
+    can->tw = can->weights;
+    can->tseg.resize(rank + 1);
+    for (int64_t q = 0; q <= rank; ++q) can->tseg[q] = q;
+    for (int l = 0; l < 3; ++l) {
+      require(dims[l] >= 1, "CanonicalTensor: mode size must be positive");
+      can->N[l] = dims[l];
+      can->d[l] = rank;
+      can->dict[l].alloc(c, size_t(dims[l]) * std::max<int64_t>(rank, 1));
+      if (rank)
+        CK(cudaMemcpyAsync(can->dict[l].p, f[l], sizeof(double) * dims[l] * rank,
+                           cudaMemcpyHostToDevice, c->stream));
+      can->dict_norms[l].assign(rank, 1.0);
+      can->term_col[l].resize(rank);
+      can->tc[l].resize(rank);
+      for (int64_t q = 0; q < rank; ++q) can->term_col[l][q] = can->tc[l][q] = int32_t(q);
+      can->mult[l].assign(rank, 1.0);
+      can->dtc[l].upload(c, can->tc[l]);
+    }
+    can->dtw.upload(c, can->tw);
+    can->dtseg.upload(c, can->tseg);
+    for (int m = 0; m < 3; ++m) {
+      can->sseg[m] = can->tseg;
+      for (int l = 0; l < 3; ++l) can->stc[m][l] = can->tc[l];
+      can->stw[m] = can->tw;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    *out = can.release();
+  });
+}
+
+int latsum_tensor_write(latsum_ctx* c, const latsum_canonical* can, const latsum_tucker* t,
+                        const char* path) {
+  return guarded(c, [&] {
+    require(path && ((can != nullptr) != (t != nullptr)),
+            "latsum_tensor_write: pass exactly one of canonical / tucker");
+    FileSink f(path);
+    if (can) {
+      write_header(f, 'C', can->N);
+      f.u32(uint32_t(can->Mc));
+      f.put(can->weights.data(), sizeof(double) * can->Mc);
+      for (int l = 0; l < 3; ++l) {
+        DBuf tmp(c, size_t(can->N[l]) * std::max<int64_t>(can->Mc, 1));
+        materialize_factor(c, *can, l, tmp.p);
+        f.device(c, tmp.p, size_t(can->N[l]) * can->Mc);
+      }
+    } else {
+      require(t->has_core, "latsum_tensor_write: factors-only Tucker result has no dense core");
+      write_header(f, 'T', t->N);
+      for (int l = 0; l < 3; ++l) f.u32(uint32_t(t->r[l]));
+      f.device(c, t->core.p, size_t(t->r[0]) * t->r[1] * t->r[2]);
+      for (int l = 0; l < 3; ++l) f.device(c, t->U[l].p, size_t(t->N[l]) * t->r[l]);
+    }
+    f.finish();
+  });
+}
+
+int latsum_tensor_read(latsum_ctx* c, const char* path, latsum_canonical** can_out,
+                       latsum_tucker** t_out) {
+  return guarded(c, [&] {
+    require(path && can_out && t_out, "latsum_tensor_read: null argument");
+    *can_out = nullptr;
+    *t_out = nullptr;
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw Error(LATSUM_ERR_IO, std::string("cannot open ") + path);
+    std::vector<char> buf((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    if (buf.size() < 7 + 1 + 4 + 12 + 8) throw Error(LATSUM_ERR_IO, "tensor file truncated");
+    uint64_t stored;
+    std::memcpy(&stored, buf.data() + buf.size() - 8, 8);
+    Fnv fnv;
+    fnv.add(buf.data(), buf.size() - 8);
+    if (stored != fnv.h)
+      throw Error(LATSUM_ERR_IO, std::string("checksum mismatch in ") + path +
+                                     " (corrupt or tampered file)");
+    size_t at = 0;
+    auto rd = [&](void* o, size_t n) {
+      if (at + n > buf.size() - 8) throw Error(LATSUM_ERR_IO, "tensor file truncated");
+      std::memcpy(o, buf.data() + at, n);
+      at += n;
+    };
+    auto u32 = [&] {
+      uint32_t v;
+      rd(&v, 4);
+      return int64_t(v);
+    };
+    char magic[7];
+    rd(magic, 7);
+    if (std::memcmp(magic, "LTSTNSR", 7) != 0) throw Error(LATSUM_ERR_IO, "bad magic");
+    unsigned char version;
+    rd(&version, 1);
+    if (version != 1)
+      throw Error(LATSUM_ERR_IO, "unsupported format version " + std::to_string(int(version)));
+    char tag;
+    rd(&tag, 1);
+    at += 3;
+    int64_t dims[3];
+    for (int l = 0; l < 3; ++l) dims[l] = u32();
+    if (tag == 'C') {
+      const int64_t R = u32();
+      std::vector<double> w(R), f[3];
+      rd(w.data(), sizeof(double) * R);
+      for (int l = 0; l < 3; ++l) {
+        f[l].resize(size_t(dims[l]) * R);
+        rd(f[l].data(), sizeof(double) * f[l].size());
+      }
+      latsum_canonical* can = nullptr;
+      const int st = latsum_canonical_from_host(c, dims, R, w.data(), f[0].data(), f[1].data(),
+                                                f[2].data(), &can);
+      if (st != LATSUM_OK) throw Error(st, c->err);
+      *can_out = can;
+    } else if (tag == 'T') {
+      auto t = std::make_unique<latsum_tucker>();
+      for (int l = 0; l < 3; ++l) t->N[l] = dims[l];
+      for (int l = 0; l < 3; ++l) t->r[l] = u32();
+      const size_t nc = size_t(t->r[0]) * t->r[1] * t->r[2];
+      std::vector<double> h(nc);
+      rd(h.data(), sizeof(double) * nc);
+      t->core.alloc(c, nc);
+      CK(cudaMemcpyAsync(t->core.p, h.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int l = 0; l < 3; ++l) {
+        std::vector<double> u(size_t(dims[l]) * t->r[l]);
+        rd(u.data(), sizeof(double) * u.size());
+        t->U[l].alloc(c, u.size());
+        CK(cudaMemcpyAsync(t->U[l].p, u.data(), sizeof(double) * u.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        t->sigma[l].assign(1, 0.0);
+      }
+      t->has_core = true;
+      *t_out = t.release();
+    } else {
+      throw Error(LATSUM_ERR_IO, "unknown format tag");
+    }
+  });
+}
+
+int latsum_canonical_to_tucker(latsum_ctx* c, const latsum_canonical* can, const int64_t* ranks,
+                               double tolerance, int max_als_sweeps, double als_stagnation_tol,
+                               latsum_tucker** out, latsum_spectral_report* report,
+                               int* als_sweeps) {
+  return guarded(c, [&] {
+    require(can && out, "latsum_canonical_to_tucker: null argument");
+    auto t = std::make_unique<latsum_tucker>();
+    latsum_spectral_report rep;
+    canonical_to_tucker_impl(c, *can, ranks, tolerance, max_als_sweeps, als_stagnation_tol, *t,
+                             rep, als_sweeps);
+    if (report) *report = rep;
+    *out = t.release();
+  });
+}
+
+int latsum_verify_entries(latsum_ctx* c, const latsum_reference* ref, int64_t ns,
+                          const int64_t* shifts, const double* weights, const int64_t* probes,
+                          int64_t np, double* out) {
+  return guarded(c, [&] {
+    require(ref && (ns == 0 || (shifts && weights)) && (np == 0 || (probes && out)),
+            "latsum_verify_entries: bad argument");
+    if (np == 0) return;
+    for (int64_t q = 0; q < ns; ++q)
+      for (int l = 0; l < 3; ++l) {
+        const int64_t begin = ref->N[l] / 2 - shifts[3 * q + l];
+        if (begin < 0 || begin + ref->N[l] > 2 * ref->N[l])
+          throw Error(LATSUM_ERR_WINDOW_OVERFLOW,
+                      "window overflow in mode " + std::to_string(l + 1) + ": source " +
+                          std::to_string(q));
+      }
+    for (int64_t p = 0; p < np; ++p)
+      for (int l = 0; l < 3; ++l)
+        require(probes[3 * p + l] >= 0 && probes[3 * p + l] < ref->N[l],
+                "oracle_entry: probe index out of range");
+    DVec<int64_t> dsh, dpr;
+    DVec<double> dsw, dwr;
+    DVec<int32_t> djm;
+    dsh.upload(c, std::vector<int64_t>(shifts, shifts + 3 * ns));
+    dsw.upload(c, std::vector<double>(weights, weights + ns));
+    dpr.upload(c, std::vector<int64_t>(probes, probes + 3 * np));
+    dwr.upload(c, ref->weights);
+    djm.upload(c, std::vector<int32_t>(ref->jmap.begin(), ref->jmap.end()));
+    const int64_t chunk = std::max<int64_t>(4096, (ns + 255) / 256);
+    const int nchunk = int(std::max<int64_t>(1, (ns + chunk - 1) / chunk));
+    DBuf part(c, size_t(np) * nchunk), res(c, np);
+    VerifyArgs a{{ref->col(0), ref->col(1), ref->col(2)}, {ref->N[0], ref->N[1], ref->N[2]},
+                 djm.p, dwr.p, ref->R, dsh.p, dsw.p, ns, dpr.p, chunk, nchunk, part.p};
+    if (ns > 0) {
+      ProfScope ps(c, "verify_bruteforce", double(np) * double(ns) * ref->R * 4.0);
+      k_verify_partial<<<dim3(unsigned(np), unsigned(nchunk)), 256, 0, c->stream>>>(a);
+      post_launch(c);
+    } else {
+      CK(cudaMemsetAsync(part.p, 0, sizeof(double) * np * nchunk, c->stream));
+    }
+    k_verify_finish<<<unsigned((np + 255) / 256), 256, 0, c->stream>>>(part.p, nchunk, np, res.p);
+    post_launch(c);
+    CK(cudaMemcpyAsync(out, res.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -357,3 +357,112 @@ __global__ void k_gather_rows(const double* __restrict__ U, int64_t N, int64_t r
 }
 
 }  // namespace latsum_b200
+
+namespace latsum_b200 {
+
+// ---------------------------------------------------------------- verification
+
+// Brute-force windowed sum (lattice_sum.hpp:656-671 oracle_entry) at probe p over the
+// sources [s0, s1): sum_s w_s sum_k w_k prod_l ref_l[N_l/2 - c_{s,l} + i_l, jmap[k]],
+// the reference's own loop order per source; block partial -> part[p * nchunk + chunk].
+struct VerifyArgs {
+  const double* ref[3];     // 2N_l x Rd distinct unit columns
+  int64_t N[3];
+  const int32_t* jmap;      // R -> distinct column
+  const double* wref;       // R reference weights
+  int R;
+  const int64_t* shifts;    // ns x 3
+  const double* sw;         // ns
+  int64_t ns;
+  const int64_t* probes;    // np x 3
+  int64_t chunk;
+  int nchunk;
+  double* part;
+};
+
+__global__ void k_verify_partial(VerifyArgs a) {
+  __shared__ double red[32];
+  const int64_t p = blockIdx.x;
+  const int64_t i = a.probes[3 * p], j = a.probes[3 * p + 1], k = a.probes[3 * p + 2];
+  const int64_t s0 = int64_t(blockIdx.y) * a.chunk;
+  const int64_t s1 = min(a.ns, s0 + a.chunk);
+  double acc = 0.0;
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    const double* r0 = a.ref[0] + (a.N[0] / 2 - a.shifts[3 * s] + i);
+    const double* r1 = a.ref[1] + (a.N[1] / 2 - a.shifts[3 * s + 1] + j);
+    const double* r2 = a.ref[2] + (a.N[2] / 2 - a.shifts[3 * s + 2] + k);
+    double e = 0.0;
+    for (int q = 0; q < a.R; ++q) {
+      const int64_t c = a.jmap[q];
+      e += a.wref[q] * r0[c * 2 * a.N[0]] * r1[c * 2 * a.N[1]] * r2[c * 2 * a.N[2]];
+    }
+    acc += a.sw[s] * e;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) a.part[p * a.nchunk + blockIdx.y] = acc;
+}
+
+__global__ void k_verify_finish(const double* __restrict__ part, int nchunk, int64_t np,
+                                double* __restrict__ out) {
+  const int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (p >= np) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunk; ++c) s += part[p * nchunk + c];
+  out[p] = s;
+}
+
+}  // namespace latsum_b200
+
+namespace latsum_b200 {
+
+// core'[j + r1 (i + r0 k)] = core[i + r0 (j + r1 k)]  (swap the first two modes)
+__global__ void k_swap01(const double* __restrict__ in, int64_t r0, int64_t r1, int64_t r2,
+                         double* __restrict__ out) {
+  const int64_t total = r0 * r1 * r2;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % r0, j = (e / r0) % r1, k = e / (r0 * r1);
+    out[j + r1 * (i + r0 * k)] = in[e];
+  }
+}
+
+// sum of squares of the core entries with index_l == at inside the box [0, r) (one block)
+__global__ void k_slice_mass(const double* __restrict__ core, int64_t d0, int64_t d1, int l,
+                             int64_t at, int64_t b0, int64_t b1, int64_t b2,
+                             double* __restrict__ out) {
+  __shared__ double red[32];
+  const int64_t n_a = l == 0 ? b1 : b0, n_b = l == 2 ? b1 : b2;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < n_a * n_b; e += blockDim.x) {
+    const int64_t x = e % n_a, y = e / n_a;
+    int64_t i, j, k;
+    if (l == 0) { i = at; j = x; k = y; }
+    else if (l == 1) { i = x; j = at; k = y; }
+    else { i = x; j = y; k = at; }
+    const double v = core[i + d0 * (j + d1 * k)];
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// out (b0 x b1 x b2) = the leading box of core (d0 x d1 x d2)
+__global__ void k_crop(const double* __restrict__ core, int64_t d0, int64_t d1, int64_t b0,
+                       int64_t b1, int64_t b2, double* __restrict__ out) {
+  const int64_t total = b0 * b1 * b2;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % b0, j = (e / b0) % b1, k = e / (b0 * b1);
+    out[e] = core[i + d0 * (j + d1 * k)];
+  }
+}
+
+__global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i] * v[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace latsum_b200

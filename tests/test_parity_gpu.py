@@ -326,3 +326,56 @@ def test_stage3_core_contracted_over_smallest_mode(ctx, fixed_mode):
     want = O.tucker_entries(core, orc.Z, pr)
     got = t.entries(pr)
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-11
+
+
+# ----------------------------------------------------------------------------- next rows
+
+@pytest.mark.parametrize("kind", ["vacancies", "mixed"])
+def test_gpu_bruteforce_verifier_matches_cpu_oracle(ctx, kind):
+    """latsum_verify_entries = oracle_entry (lattice_sum.hpp:656-671) on the device."""
+    g = mini(kind)
+    ref, oref = _ref_pair(ctx, g)
+    pr = O.probes(g.N, 200, 31)
+    got = api.oracle_entries(ref, g, pr)
+    want = O.oracle_entries(oref, g, pr)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-13
+    can = api.lattice_sum(ref, g)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    res = api.verify(t, ref, g, probes=300, seed=3, bound_abs=rep.bound_abs)
+    assert res["ok"] and res["normalized"] <= 10 * g.eps + 1e-12
+
+
+@pytest.mark.slow
+def test_gpu_bruteforce_verifier_cfg5(ctx):
+    """16.8M-source brute-force sum on the device vs the CPU oracle fixture."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "fullcfg5.npz")
+    fx = np.load(path)
+    g = W.baseline(5)
+    ref = api.reference_for(g, ctx)
+    nb = fx["v_brute"].size
+    got = api.oracle_entries(ref, g, fx["probes"][:nb])
+    assert np.max(np.abs(got - fx["v_brute"])) / np.max(np.abs(fx["v_brute"])) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["vacancies", "hex"])
+def test_canonical_to_tucker_matches_oracle(ctx, kind):
+    """rank_reduction.hpp:280-306: rhosvd + ALS + shrink_core, against the oracle's
+    restatement on full side matrices."""
+    g = mini(kind)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    core, Y, orc, sweeps = O.canonical_to_tucker(F, w, eps=g.eps, max_sweeps=3)
+    t, rep, gsweeps = api.canonical_to_tucker(can, api.TruncationSpec.tol(g.eps), max_als_sweeps=3)
+    for l in range(3):
+        assert abs(rep.chosen_ranks[l] - core.shape[l]) <= 1, (rep.chosen_ranks, core.shape)
+        assert rep.chosen_ranks[l] <= orc.ranks[l]
+    pr = O.probes(g.N, 300, 41)
+    exact = O.canonical_entries(F, w, pr)
+    got = t.entries(pr)
+    want = O.tucker_entries(core, Y, pr)
+    scale = np.max(np.abs(exact))
+    assert np.max(np.abs(got - exact)) / scale <= 10 * g.eps
+    assert np.max(np.abs(want - exact)) / scale <= 10 * g.eps
+    assert gsweeps >= 1

@@ -558,3 +558,27 @@ def canonical_to_tucker(F, w, eps=None, ranks=None, max_sweeps: int = 30, stag_t
         if budget2 > 0:
             core, Y = shrink_core(core, Y, budget2)
     return core, Y, orc, sweeps
+
+
+# ----------------------------------------------------------------------------- tensor files
+
+def fnv1a64(data: bytes, seed: int = 0xcbf29ce484222325) -> int:
+    """tensor_io.cpp:9-17."""
+    h = seed
+    for b in data:
+        h ^= b
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def tensor_file_bytes(kind: str, dims, payload_u32, arrays) -> bytes:
+    """tensor_io.cpp:45-76 write_tensor byte layout ("LTSTNSR" v1, FNV-1a trailer)."""
+    import struct
+    buf = bytearray(b"LTSTNSR")
+    buf += bytes([1, ord(kind), 0, 0, 0])
+    buf += struct.pack("<3I", *[int(x) for x in dims])
+    buf += struct.pack(f"<{len(payload_u32)}I", *[int(x) for x in payload_u32])
+    for a in arrays:
+        buf += np.asarray(a, dtype="<f8").ravel(order="F").tobytes()
+    buf += struct.pack("<Q", fnv1a64(bytes(buf)))
+    return bytes(buf)

@@ -1683,6 +1683,17 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
     CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
     return;
   }
+  if (T <= CP_MAXT) {  // low rank (cfg1: 17 merged terms): output-write bound kernel
+    ProfScope ps(c, "cp_eval_small", 8.0 * double(ni) * double(nj) * double(nk));
+    const unsigned gx = unsigned((ni + CP_THREADS - 1) / CP_THREADS);
+    const int64_t pairs = nj * nk;
+    const unsigned gy = unsigned(std::max<int64_t>(1, std::min<int64_t>(
+        (pairs + CP_PAIRS - 1) / CP_PAIRS, std::max<int64_t>(1, 148 * 8 / int64_t(gx)))));
+    k_cp_eval_small<<<dim3(gx, gy), CP_THREADS, 0, c->stream>>>(
+        D[0], ld[0], D[1], ld[1], D[2], ld[2], tc[0], tc[1], tc[2], tw, int(T), ni, nj, nk, out);
+    post_launch(c);
+    return;
+  }
   DBuf A0(c, size_t(ni) * T);
   k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(D[0], ni, ld[0], tc[0], nullptr, T, A0.p);
   post_launch(c);

@@ -466,3 +466,52 @@ __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restr
 }
 
 }  // namespace latsum_b200
+
+namespace latsum_b200 {
+
+// Low-rank canonical evaluation on a box (canonical.hpp:192-202 to_dense) for T <= 64
+// merged terms, output-write bound: thread i keeps A0[i, :] = D0[i, c0_t] in registers,
+// the block stages x_t(j,k) = w_t D1[j, c1_t] D2[k, c2_t] for CP_PAIRS (j,k) pairs in
+// shared memory, and writes V[i, j, k] with consecutive threads on consecutive i.
+constexpr int CP_MAXT = 64, CP_PAIRS = 32, CP_THREADS = 256;
+__global__ void __launch_bounds__(CP_THREADS)
+k_cp_eval_small(const double* __restrict__ D0, int64_t ld0, const double* __restrict__ D1,
+                int64_t ld1, const double* __restrict__ D2, int64_t ld2,
+                const int32_t* __restrict__ c0, const int32_t* __restrict__ c1,
+                const int32_t* __restrict__ c2, const double* __restrict__ w, int T, int64_t ni,
+                int64_t nj, int64_t nk, double* __restrict__ out) {
+  __shared__ double xs[CP_PAIRS][CP_MAXT];
+  const int64_t i = blockIdx.x * int64_t(CP_THREADS) + threadIdx.x;
+  double a[CP_MAXT];
+#pragma unroll
+  for (int t = 0; t < CP_MAXT; ++t) a[t] = (t < T && i < ni) ? D0[i + int64_t(c0[t]) * ld0] : 0.0;
+  const int64_t npairs = nj * nk;
+  for (int64_t p0 = int64_t(blockIdx.y) * CP_PAIRS; p0 < npairs; p0 += int64_t(gridDim.y) * CP_PAIRS) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < CP_PAIRS * T; e += CP_THREADS) {
+      const int q = e / T, t = e % T;
+      const int64_t p = p0 + q;
+      double v = 0.0;
+      if (p < npairs) {
+        const int64_t j = p % nj, k = p / nj;
+        v = w[t] * D2[k + int64_t(c2[t]) * ld2] * D1[j + int64_t(c1[t]) * ld1];
+      }
+      xs[q][t] = v;
+    }
+    __syncthreads();
+    if (i < ni) {
+#pragma unroll 4
+      for (int q = 0; q < CP_PAIRS; ++q) {
+        const int64_t p = p0 + q;
+        if (p >= npairs) break;
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < CP_MAXT; ++t)
+          if (t < T) s += a[t] * xs[q][t];
+        out[i + ni * p] = s;
+      }
+    }
+  }
+}
+
+}  // namespace latsum_b200

@@ -379,3 +379,61 @@ def test_canonical_to_tucker_matches_oracle(ctx, kind):
     assert np.max(np.abs(got - exact)) / scale <= 10 * g.eps
     assert np.max(np.abs(want - exact)) / scale <= 10 * g.eps
     assert gsweeps >= 1
+
+
+def test_tensor_files_match_reference_layout(ctx, tmp_path):
+    """write_tensor / read_tensor (tensor_io.cpp:45-129): byte-identical to the oracle's
+    restatement of the layout, round-trips, and rejects tampering (cli_pipeline.sh:87-90)."""
+    g = W.from_lattice((2, 2, 2), 8, M=3, defects=[([(0, 0, 0)], -1.0, None)], eps=1e-6)
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    pt, pc = tmp_path / "t.tns", tmp_path / "c.tns"
+    api.write_tensor(pt, t)
+    api.write_tensor(pc, can)
+    want_t = O.tensor_file_bytes("T", t.dims, t.ranks, [t.core] + [t.factor(l) for l in range(3)])
+    assert pt.read_bytes() == want_t
+    want_c = O.tensor_file_bytes("C", can.dims, [can.rank],
+                                 [can.weights] + [can.factor(l) for l in range(3)])
+    assert pc.read_bytes() == want_c
+    t2 = api.read_tensor(pt, ctx)
+    c2 = api.read_tensor(pc, ctx)
+    pr = O.probes(g.N, 100, 2)
+    np.testing.assert_array_equal(t2.entries(pr), t.entries(pr))
+    np.testing.assert_allclose(c2.entries(pr), can.entries(pr), rtol=1e-13, atol=0)
+    raw = bytearray(pt.read_bytes())
+    raw[40] ^= 0x01
+    pt.write_bytes(bytes(raw))
+    with pytest.raises(IOError, match="checksum"):
+        api.read_tensor(pt, ctx)
+
+
+def _random_canonical(dims, rank, seed):
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal(rank)
+    F = []
+    for l in range(3):
+        f = rng.standard_normal((dims[l], rank))
+        n = np.linalg.norm(f, axis=0)
+        F.append(np.asfortranarray(f / n))
+        w = w * n
+    return w, F
+
+
+@pytest.mark.parametrize("dims,rank", [((12, 12, 12), 3), ((20, 20, 20), 30), ((24, 24, 24), 12)])
+def test_rhosvd_on_arbitrary_canonical_inputs(ctx, dims, rank):
+    """test_rank_reduction.cpp:22-66 on the device: exact low rank, sigma vs an independent
+    SVD (incl. the R > n case), error within the discarded-tail bound."""
+    w, F = _random_canonical(dims, rank, 7 + rank)
+    can = api.canonical_from_arrays(w, F, ctx)
+    r = (3, 3, 3) if rank == 3 else (5, 5, 5)
+    t, rep = api.rhosvd(can, api.TruncationSpec.fixed_ranks(*r))
+    for l in range(3):
+        s = np.linalg.svd(F[l], compute_uv=False)
+        np.testing.assert_allclose(rep.singular_values[l][:s.size], s, rtol=1e-10, atol=1e-13 * s[0])
+    dense = np.einsum("q,iq,jq,kq->ijk", w, F[0], F[1], F[2])
+    approx = t.to_dense()
+    err = np.linalg.norm(approx - dense)
+    if rank == 3:
+        assert err / np.linalg.norm(dense) < 1e-12
+    assert err <= rep.bound_abs * (1 + 1e-12) + 1e-12 * np.linalg.norm(dense)

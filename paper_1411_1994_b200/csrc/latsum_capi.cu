@@ -1685,12 +1685,23 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
   }
   if (T <= CP_MAXT) {  // low rank (cfg1: 17 merged terms): output-write bound kernel
     ProfScope ps(c, "cp_eval_small", 8.0 * double(ni) * double(nj) * double(nk));
-    const unsigned gx = unsigned((ni + CP_THREADS - 1) / CP_THREADS);
     const int64_t pairs = nj * nk;
-    const unsigned gy = unsigned(std::max<int64_t>(1, std::min<int64_t>(
-        (pairs + CP_PAIRS - 1) / CP_PAIRS, std::max<int64_t>(1, 148 * 8 / int64_t(gx)))));
-    k_cp_eval_small<<<dim3(gx, gy), CP_THREADS, 0, c->stream>>>(
-        D[0], ld[0], D[1], ld[1], D[2], ld[2], tc[0], tc[1], tc[2], tw, int(T), ni, nj, nk, out);
+    auto grid_of = [&](int ipt) {
+      const unsigned gx = unsigned((ni + CP_THREADS * ipt - 1) / (CP_THREADS * ipt));
+      const unsigned gy = unsigned(std::max<int64_t>(1, std::min<int64_t>(
+          (pairs + CP_PAIRS - 1) / CP_PAIRS, std::max<int64_t>(1, 148 * 8 / int64_t(gx)))));
+      return dim3(gx, gy);
+    };
+#define LATSUM_CP(MT)                                                                         \
+  k_cp_eval_small<MT><<<grid_of(cp_ipt<MT>()), CP_THREADS, 0, c->stream>>>(                   \
+      D[0], ld[0], D[1], ld[1], D[2], ld[2], tc[0], tc[1], tc[2], tw, int(T), ni, nj, nk, out)
+    if (T <= 8) LATSUM_CP(8);
+    else if (T <= 16) LATSUM_CP(16);
+    else if (T <= 24) LATSUM_CP(24);
+    else if (T <= 32) LATSUM_CP(32);
+    else if (T <= 48) LATSUM_CP(48);
+    else LATSUM_CP(64);
+#undef LATSUM_CP
     post_launch(c);
     return;
   }

@@ -470,45 +470,60 @@ __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restr
 namespace latsum_b200 {
 
 // Low-rank canonical evaluation on a box (canonical.hpp:192-202 to_dense) for T <= 64
-// merged terms, output-write bound: thread i keeps A0[i, :] = D0[i, c0_t] in registers,
-// the block stages x_t(j,k) = w_t D1[j, c1_t] D2[k, c2_t] for CP_PAIRS (j,k) pairs in
-// shared memory, and writes V[i, j, k] with consecutive threads on consecutive i.
-constexpr int CP_MAXT = 64, CP_PAIRS = 32, CP_THREADS = 256;
+// merged terms, output-write bound: each thread keeps A0[i, :] = D0[i, c0_t] for CP_IPT
+// rows in registers (zero-padded to the rank bucket MAXT), the block stages
+// x_t(j,k) = w_t D1[j, c1_t] D2[k, c2_t] for CP_PAIRS (j,k) pairs in shared memory, and
+// every staged value feeds CP_IPT FMAs; stores are coalesced along i.
+constexpr int CP_MAXT = 64, CP_PAIRS = 32, CP_THREADS = 128;
+template <int MAXT>
+constexpr int cp_ipt() { return MAXT <= 24 ? 4 : (MAXT <= 32 ? 2 : 1); }
+template <int MAXT>
 __global__ void __launch_bounds__(CP_THREADS)
 k_cp_eval_small(const double* __restrict__ D0, int64_t ld0, const double* __restrict__ D1,
                 int64_t ld1, const double* __restrict__ D2, int64_t ld2,
                 const int32_t* __restrict__ c0, const int32_t* __restrict__ c1,
                 const int32_t* __restrict__ c2, const double* __restrict__ w, int T, int64_t ni,
                 int64_t nj, int64_t nk, double* __restrict__ out) {
-  __shared__ double xs[CP_PAIRS][CP_MAXT];
-  const int64_t i = blockIdx.x * int64_t(CP_THREADS) + threadIdx.x;
-  double a[CP_MAXT];
+  constexpr int CP_IPT = cp_ipt<MAXT>();
+  __shared__ double xs[CP_PAIRS][MAXT];
+  const int64_t ibase = blockIdx.x * int64_t(CP_THREADS * CP_IPT) + threadIdx.x;
+  double a[CP_IPT][MAXT];
 #pragma unroll
-  for (int t = 0; t < CP_MAXT; ++t) a[t] = (t < T && i < ni) ? D0[i + int64_t(c0[t]) * ld0] : 0.0;
+  for (int u = 0; u < CP_IPT; ++u) {
+    const int64_t i = ibase + u * CP_THREADS;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) a[u][t] = (t < T && i < ni) ? D0[i + int64_t(c0[t]) * ld0] : 0.0;
+  }
   const int64_t npairs = nj * nk;
   for (int64_t p0 = int64_t(blockIdx.y) * CP_PAIRS; p0 < npairs; p0 += int64_t(gridDim.y) * CP_PAIRS) {
     __syncthreads();
-    for (int e = threadIdx.x; e < CP_PAIRS * T; e += CP_THREADS) {
-      const int q = e / T, t = e % T;
+    for (int e = threadIdx.x; e < CP_PAIRS * MAXT; e += CP_THREADS) {
+      const int q = e / MAXT, t = e % MAXT;
       const int64_t p = p0 + q;
       double v = 0.0;
-      if (p < npairs) {
+      if (p < npairs && t < T) {
         const int64_t j = p % nj, k = p / nj;
         v = w[t] * D2[k + int64_t(c2[t]) * ld2] * D1[j + int64_t(c1[t]) * ld1];
       }
       xs[q][t] = v;
     }
     __syncthreads();
-    if (i < ni) {
-#pragma unroll 4
-      for (int q = 0; q < CP_PAIRS; ++q) {
-        const int64_t p = p0 + q;
-        if (p >= npairs) break;
-        double s = 0.0;
+    const int nq = int((npairs - p0) < CP_PAIRS ? (npairs - p0) : CP_PAIRS);
+    for (int q = 0; q < nq; ++q) {
+      double s[CP_IPT];
 #pragma unroll
-        for (int t = 0; t < CP_MAXT; ++t)
-          if (t < T) s += a[t] * xs[q][t];
-        out[i + ni * p] = s;
+      for (int u = 0; u < CP_IPT; ++u) s[u] = 0.0;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        const double x = xs[q][t];
+#pragma unroll
+        for (int u = 0; u < CP_IPT; ++u) s[u] += a[u][t] * x;
+      }
+      const int64_t p = p0 + q;
+#pragma unroll
+      for (int u = 0; u < CP_IPT; ++u) {
+        const int64_t i = ibase + u * CP_THREADS;
+        if (i < ni) out[i + ni * p] = s[u];
       }
     }
   }

@@ -437,3 +437,19 @@ def test_rhosvd_on_arbitrary_canonical_inputs(ctx, dims, rank):
     if rank == 3:
         assert err / np.linalg.norm(dense) < 1e-12
     assert err <= rep.bound_abs * (1 + 1e-12) + 1e-12 * np.linalg.norm(dense)
+
+
+@pytest.mark.parametrize("kind", ["cubic", "vacancies", "yukawa"])
+def test_canonical_box_eval_all_rank_buckets(ctx, kind):
+    """Canonical to_dense on a box via the low-rank kernel (T <= 64) or the slab GEMMs."""
+    g = mini(kind)
+    ref, oref = _ref_pair(ctx, g)
+    can = api.lattice_sum(ref, g)
+    F, w = O.side_matrices(oref, g)
+    lo, hi = (3, 0, 5), (g.N[0] - 2, g.N[1], 37)
+    box = can.to_dense(lo, hi)
+    rng = np.random.default_rng(4)
+    pr = np.stack([rng.integers(lo[l], hi[l], 300) for l in range(3)], axis=1)
+    want = O.canonical_entries(F, w, pr)
+    got = box[pr[:, 0] - lo[0], pr[:, 1] - lo[1], pr[:, 2] - lo[2]]
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12

@@ -238,6 +238,7 @@ def run_gpu(args):
             clocks.start()  # started before the warm-up so nvidia-smi start-up is not timed
         if i == args.warmup:
             launches0 = ctx.kernel_launches
+        last = ref = can = t = rep = None  # release the previous step's device tensors
         ev[0].record(stream)
         ref, can, t, rep = step()
         ev[1].record(stream)

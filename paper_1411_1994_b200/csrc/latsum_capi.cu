@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -184,12 +185,15 @@ int grid_for(int64_t total, int threads = 256) {
   return int(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
 }
 
-// Doubles an intermediate may occupy: a third of the free device memory, at most 2^31.
-int64_t workspace_budget(int64_t floor_doubles = int64_t(1) << 27) {
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return floor_doubles;
-  const int64_t v = int64_t(free_b / 3 / sizeof(double));
-  return std::max<int64_t>(floor_doubles, std::min<int64_t>(v, int64_t(1) << 31));
+// Doubles an intermediate may occupy: 1/16 of the device memory (11 GB on a B200),
+// fixed per device so chunk sizes (and stream-ordered pool reuse) are reproducible.
+int64_t workspace_budget() {
+  static const int64_t v = [] {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return int64_t(1) << 27;
+    return std::max<int64_t>(int64_t(1) << 27, int64_t(total_b / 16 / sizeof(double)));
+  }();
+  return v;
 }
 
 // Split n into ceil(n / cap) near-equal chunks (multiples of `align` when possible).
@@ -254,6 +258,24 @@ void prof_harvest(latsum_ctx* c) {
   }
   c->pending.clear();
 }
+
+// LATSUM_TRACE=1: host wall-clock trace of the RHOSVD phases (stderr), per worker.
+struct Trace {
+  static bool on() {
+    static const bool v = std::getenv("LATSUM_TRACE") != nullptr;
+    return v;
+  }
+  static double now_ms() {
+    using namespace std::chrono;
+    static const auto t0 = steady_clock::now();
+    return duration<double, std::milli>(steady_clock::now() - t0).count();
+  }
+  static void mark(latsum_ctx* c, const char* what, bool sync = true) {
+    if (!on()) return;
+    if (sync) cudaStreamSynchronize(c->stream);
+    fprintf(stderr, "[trace %9.3f ms] stream %p %s\n", now_ms(), (void*)c->stream, what);
+  }
+};
 
 // Sum-all-reduce over the ranks of c's communicator (no-op on one rank).
 void allreduce(latsum_ctx* c, double* buf, size_t count) {
@@ -579,6 +601,7 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
               const int64_t* sub_shifts, const double* sub_charges, int64_t ndef,
               const int64_t* def_shifts, const double* def_charges, latsum_canonical& can) {
   require(nsub >= 0 && ndef >= 0, "assemble: negative counts");
+  Trace::mark(c, "assemble: start", false);
   const int R = ref.R, Rd = ref.Rd;
   can.R = R;
   can.Rd = Rd;
@@ -655,6 +678,7 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     CK(cudaStreamSynchronize(c->stream));
   }
 
+  Trace::mark(c, "assemble: dictionaries done", false);
   // terms in reference order (add_concat: sublattice blocks, then defects)
   can.weights.resize(can.Mc);
   for (int l = 0; l < 3; ++l) {
@@ -677,17 +701,26 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
       can.weights[q] = w;
     }
   }
+  Trace::mark(c, "assemble: terms done", false);
   // merge identical rank-1 terms (same column in all three modes)
   // (key = c0:c1:c2 packed in 21-bit fields, q); stable order keeps the reference's
   // term order inside each merged group, so merged weights add in add_concat order
   for (int l = 0; l < 3; ++l)
     require(can.d[l] < (int64_t(1) << 21), "assemble: too many distinct columns in a mode");
-  std::vector<std::pair<uint64_t, int64_t>> keys(can.Mc);
+  // stable LSD counting sort over (c2, c1, c0): O(M_c) instead of a comparison sort
+  std::vector<std::pair<uint64_t, int64_t>> keys(can.Mc), tmp(can.Mc);
   for (int64_t q = 0; q < can.Mc; ++q)
     keys[q] = {(uint64_t(can.term_col[0][q]) << 42) | (uint64_t(can.term_col[1][q]) << 21) |
                    uint64_t(can.term_col[2][q]),
                q};
-  std::sort(keys.begin(), keys.end());
+  for (int pass = 0; pass < 3; ++pass) {
+    const int l = 2 - pass, shift = 21 * pass;
+    std::vector<int64_t> cnt(can.d[l] + 1, 0);
+    for (const auto& kq : keys) cnt[((kq.first >> shift) & 0x1FFFFF) + 1]++;
+    for (int64_t a = 0; a < can.d[l]; ++a) cnt[a + 1] += cnt[a];
+    for (const auto& kq : keys) tmp[cnt[(kq.first >> shift) & 0x1FFFFF]++] = kq;
+    keys.swap(tmp);
+  }
   for (int l = 0; l < 3; ++l) can.tc[l].clear();
   can.tw.clear();
   can.tseg.assign(can.d[0] + 1, 0);
@@ -705,9 +738,12 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
   }
   can.T = int64_t(can.tw.size());
   for (int64_t a = 0; a < can.d[0]; ++a) can.tseg[a + 1] += can.tseg[a];
+  Trace::mark(c, "assemble: merge done", false);
   for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
   can.dtw.upload(c, can.tw);
   can.dtseg.upload(c, can.tseg);
+  Trace::mark(c, "assemble: uploads done", false);
+  Trace::mark(c, "assemble: sorted orders start", false);
   for (int m = 0; m < 3; ++m) {  // counting sort by c_m (stable: keeps the c0-major order)
     can.sseg[m].assign(can.d[m] + 1, 0);
     for (int64_t t = 0; t < can.T; ++t) can.sseg[m][can.tc[m][t] + 1] += 1;
@@ -895,9 +931,11 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
   if (sharded) allreduce(c, G.p, size_t(n) * n);
   tm.gram += timer.stop();
+  Trace::mark(c, "gram done");
   timer.start();
   syevd(c, n, G.p, W.p);
   tm.syevd += timer.stop();
+  Trace::mark(c, "syevd1 done");
   std::vector<double> lam(n), lam_d(n);
   CK(cudaMemcpyAsync(lam.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -968,10 +1006,12 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         if (sharded) allreduce(c, G2.p, size_t(nc) * nc);
       }
       tm.deflate += timer.stop();
+      Trace::mark(c, "deflation + G2 done");
       timer.start();
       DBuf W2(c, nc);
       syevd(c, nc, G2.p, W2.p);
       tm.syevd += timer.stop();
+      Trace::mark(c, "syevd2 done");
       std::vector<double> mu(nc);
       CK(cudaMemcpyAsync(mu.data(), W2.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
@@ -1051,6 +1091,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
     }
   }
   tm.deflate += timer.stop();
+  Trace::mark(c, "Z done");
 }
 
 // sqrt(w^T (G0 o G1 o G2) w) over the merged terms with G_l = E_l^T E_l (d_l x d_l)
@@ -1269,7 +1310,9 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   if (serial) {
     for (int i = 0; i < (zero_terms ? 1 : 4); ++i) body(c, i);
   } else {
+    Trace::mark(c, "rhosvd fork");
     fork_join(c, zero_terms ? 1 : 4, body);
+    Trace::mark(c, "rhosvd join");
   }
   for (int l = 0; l < 3; ++l) mo[l].Z.adopt(c->stream);
   for (const auto& x : tms) {
@@ -1335,6 +1378,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   t.tw.upload(c, can.tw);
   t.T = can.T;
   tm.project = tp.stop();
+  Trace::mark(c, "projections done");
   if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
     tp.start();
     t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
@@ -1349,6 +1393,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     }
     t.has_core = true;
     tm.core = tp.stop();
+    Trace::mark(c, "core done");
   }
   double tails = 0.0;
   for (int l = 0; l < 3; ++l) {
@@ -1831,9 +1876,9 @@ int latsum_ctx_create(int device, latsum_ctx** out) {
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     // Pre-grow the stream-ordered pool so steady-state steps never map new memory
-    // (LATSUM_POOL_RESERVE_GB, default 8; 0 disables).
+    // (LATSUM_POOL_RESERVE_GB, default 24; 0 disables).
     const char* e = std::getenv("LATSUM_POOL_RESERVE_GB");
-    const double gb = e ? std::atof(e) : 8.0;
+    const double gb = e ? std::atof(e) : 24.0;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     const size_t want = size_t(gb * 1073741824.0);

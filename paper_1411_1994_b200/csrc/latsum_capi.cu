@@ -26,6 +26,7 @@
 #include "dgemm_dmma.cuh"
 #include "latsum_b200.h"
 #include "latsum_kernels.cuh"
+#include "ozaki_i8.cuh"
 
 using namespace latsum_b200;
 
@@ -108,6 +109,7 @@ struct latsum_ctx {
   std::string err;
   int64_t launches = 0;
   bool smem_set = false;
+  bool oz_smem_set = false;
   // optional per-kernel-class CUDA-event timing (latsum_ctx_set_profiling)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double work; };
@@ -393,6 +395,44 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
                                                    o.lower ? 1 : 0);
     post_launch(c);
   }
+}
+
+// ------------------------------------------------------------------ Ozaki int8 GEMM
+// C (M x N, ldc) = A (M x K, lda) B (K x N, ldb), all column-major, on the int8 tensor
+// cores (ozaki_i8.cuh).  Slices live in stream-ordered workspaces.
+void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)") {
+  if (M <= 0 || N <= 0) return;
+  require(K <= 16384, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
+  if (!c->oz_smem_set) {
+    CK(cudaFuncSetAttribute(oz::k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(oz::SMEM_BYTES)));
+    c->oz_smem_set = true;
+  }
+  const int64_t KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
+  const int64_t tm = (M + oz::BM - 1) / oz::BM, tn = (N + oz::BN - 1) / oz::BN;
+  require(tm <= 65535, "ozaki_gemm: M too large");
+  const size_t a_bytes = size_t(tm) * KB * oz::A_STAGE, b_bytes = size_t(tn) * KB * oz::B_STAGE;
+  DBuf sa(c, (a_bytes + 7) / 8), sb(c, (b_bytes + 7) / 8);
+  DBuf ea(c, (size_t(M) + 1) / 2 + 1), eb(c, (size_t(N) + 1) / 2 + 1);
+  int8_t* pa = reinterpret_cast<int8_t*>(sa.p);
+  int8_t* pb = reinterpret_cast<int8_t*>(sb.p);
+  int* xa = reinterpret_cast<int*>(ea.p);
+  int* xb = reinterpret_cast<int*>(eb.p);
+  // rows/columns past M/N inside the last tile must be zero digits
+  if (M % oz::BM) CK(cudaMemsetAsync(pa + size_t(tm - 1) * KB * oz::A_STAGE, 0, size_t(KB) * oz::A_STAGE, c->stream));
+  if (N % oz::BN) CK(cudaMemsetAsync(pb + size_t(tn - 1) * KB * oz::B_STAGE, 0, size_t(KB) * oz::B_STAGE, c->stream));
+  {
+    ProfScope ps(c, "ozaki(slice)", double(M * K + K * N) * 8.0 + double(a_bytes + b_bytes));
+    oz::k_slice_rows<<<unsigned((M * 32 + 255) / 256), 256, 0, c->stream>>>(A, lda, M, K, KB, pa, xa);
+    post_launch(c);
+    oz::k_slice_cols<<<unsigned((N * 32 + 255) / 256), 256, 0, c->stream>>>(B, ldb, N, K, KB, pb, xb);
+    post_launch(c);
+  }
+  ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(K));
+  const dim3 ogrid{unsigned(tn), unsigned(tm), 1u};
+  oz::k_gemm_i8<<<ogrid, oz::THREADS, oz::SMEM_BYTES, c->stream>>>(pa, xa, pb, xb, M, N, KB, C, ldc);
+  post_launch(c);
 }
 
 // ------------------------------------------------------------------ syevd
@@ -2457,6 +2497,16 @@ int latsum_dgemm_device(latsum_ctx* c, int ta, int tb, int64_t M, int64_t N, int
   return guarded(c, [&] {
     require(A && B && C && M >= 0 && N >= 0 && K >= 0, "latsum_dgemm_device: bad argument");
     gemm(c, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  });
+}
+
+int latsum_dgemm_ozaki_device(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
+                              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+  return guarded(c, [&] {
+    require(A && B && C && M >= 0 && N >= 0 && K >= 0 && lda >= std::max<int64_t>(M, 1) &&
+                ldb >= std::max<int64_t>(K, 1) && ldc >= std::max<int64_t>(M, 1),
+            "latsum_dgemm_ozaki_device: bad argument");
+    ozaki_gemm(c, M, N, K, A, lda, B, ldb, C, ldc);
   });
 }
 

@@ -403,7 +403,7 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
 void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)") {
   if (M <= 0 || N <= 0) return;
-  require(K <= 16384, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
+  require(K <= oz::KMAX, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
   if (!c->oz_smem_set) {
     CK(cudaFuncSetAttribute(oz::k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(oz::SMEM_BYTES)));
@@ -411,27 +411,29 @@ void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
   }
   const int64_t KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
   const int64_t tm = (M + oz::BM - 1) / oz::BM, tn = (N + oz::BN - 1) / oz::BN;
-  require(tm <= 65535, "ozaki_gemm: M too large");
+  require(tm * tn < (int64_t(1) << 31), "ozaki_gemm: too many tiles");
   const size_t a_bytes = size_t(tm) * KB * oz::A_STAGE, b_bytes = size_t(tn) * KB * oz::B_STAGE;
   DBuf sa(c, (a_bytes + 7) / 8), sb(c, (b_bytes + 7) / 8);
-  DBuf ea(c, (size_t(M) + 1) / 2 + 1), eb(c, (size_t(N) + 1) / 2 + 1);
+  DBuf ra(c, size_t(M)), cb(c, size_t(N));
   int8_t* pa = reinterpret_cast<int8_t*>(sa.p);
   int8_t* pb = reinterpret_cast<int8_t*>(sb.p);
-  int* xa = reinterpret_cast<int*>(ea.p);
-  int* xb = reinterpret_cast<int*>(eb.p);
   // rows/columns past M/N inside the last tile must be zero digits
   if (M % oz::BM) CK(cudaMemsetAsync(pa + size_t(tm - 1) * KB * oz::A_STAGE, 0, size_t(KB) * oz::A_STAGE, c->stream));
   if (N % oz::BN) CK(cudaMemsetAsync(pb + size_t(tn - 1) * KB * oz::B_STAGE, 0, size_t(KB) * oz::B_STAGE, c->stream));
   {
     ProfScope ps(c, "ozaki(slice)", double(M * K + K * N) * 8.0 + double(a_bytes + b_bytes));
-    oz::k_slice_rows<<<unsigned((M * 32 + 255) / 256), 256, 0, c->stream>>>(A, lda, M, K, KB, pa, xa);
+    oz::k_slice_rows<<<unsigned((M * 32 + 255) / 256), 256, 0, c->stream>>>(A, lda, M, K, KB, pa, ra.p);
     post_launch(c);
-    oz::k_slice_cols<<<unsigned((N * 32 + 255) / 256), 256, 0, c->stream>>>(B, ldb, N, K, KB, pb, xb);
+    oz::k_slice_cols<<<unsigned((N * 32 + 255) / 256), 256, 0, c->stream>>>(B, ldb, N, K, KB, pb, cb.p);
     post_launch(c);
   }
   ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(K));
-  const dim3 ogrid{unsigned(tn), unsigned(tm), 1u};
-  oz::k_gemm_i8<<<ogrid, oz::THREADS, oz::SMEM_BYTES, c->stream>>>(pa, xa, pb, xb, M, N, KB, C, ldc);
+  const int64_t tiles = tm * tn;
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
+  oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(pa, ra.p, pb, cb.p, M, N, KB, C, ldc,
+                                                                   tm, tiles);
   post_launch(c);
 }
 

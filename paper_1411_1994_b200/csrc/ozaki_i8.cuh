@@ -1,39 +1,39 @@
 // FP64-accurate GEMM on the INT8 tensor cores of sm_100a (Ozaki scheme I).
 //
 // C = A B (FP64) with A (M x K) and B (K x N).  Every row of A and column of B is scaled
-// by a power of two into (-1, 1) and split into S = 8 signed 7-bit digits (slices):
-//   A = diag(2^e) sum_s 2^{-7s} A_s,   B = sum_t 2^{-7t} B_t diag(2^f),
-// so C = diag(2^e) [ sum_g 2^{-7g} D_g ] diag(2^f) with D_g = sum_{s+t=g} A_s B_t.
-// Each A_s B_t is exact in int32 (|.| <= 127^2 K), the pairs with s+t > S+1 are below
-// 2^{-7(S+2)} and dropped, and the S group sums D_2 .. D_{S+1} accumulate in TMEM as int32
-// (|D_g| <= 8 * 127^2 * K < 2^31 for K <= 16k).  The FP64 epilogue combines them exactly
-// up to one rounding per term, so the result has FP64-GEMM accuracy: the representation
-// error is 2^{-56} of the row/column maxima.  36 int8 products replace one FP64 product;
-// at the int8 tensor rate that is ~3.4x the DMMA rate.
+// by a power of two into (-1, 1), rounded to the integer X = rint(2^54 x) (|error| <=
+// 2^-55, unbiased) and written in balanced base 256 as S = 7 signed int8 digits,
+//   X = sum_s d_s 2^{8(6-s)},  d_1..d_6 in [-128, 127],  d_0 in [-65, 65],
+// so x = sum_s 2^{-6-8s} d_s and C = diag(2^e) [ sum_g 2^{-12-8g} D_g ] diag(2^f) with
+// D_g = sum_{s+t=g} A_s B_t.  Each A_s B_t is exact in int32, the 28 pairs with s + t <= 6
+// are kept (a dropped pair weighs <= 2^-54 K of the row/column maxima and has no sign
+// bias), and the 7 group sums accumulate in TMEM as int32 (|D_g| <= 7 * 2^14 K < 2^31
+// for K <= 16384).  The epilogue folds the groups exactly in int64 (two words: g = 0..3
+// and g = 4..6), converts each once and adds them with one rounding.
 //
 // Data path: operands are pre-sliced into the canonical K-major "no swizzle" core-matrix
 // layout (8 rows x 16 bytes) per (tile, k-block, slice), so each pipeline stage is one
 // contiguous bulk copy (cp.async.bulk, TMA engine) completing on an mbarrier; one thread
-// issues tcgen05.mma.kind::i8 (M=128, N=64, K=32) into 8 TMEM accumulators (512 columns);
-// tcgen05.commit frees a stage; four warps read TMEM with tcgen05.ld for the epilogue.
+// issues tcgen05.mma.kind::i8 (M=128, N=64, K=32) into 7 TMEM accumulators;
+// tcgen05.commit frees a stage; four warps drain TMEM with tcgen05.ld.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace latsum_b200 {
 namespace oz {
 
-constexpr int S = 8;                 // slices per operand
+constexpr int S = 7;                 // slices per operand
 constexpr int BM = 128, BN = 64;     // output tile (TMEM lanes x accumulator columns)
 constexpr int BKB = 32;              // k-block (int8 elements = bytes) per stage
-constexpr int STAGES = 4;
+constexpr int STAGES = 5;
 constexpr int A_BLK = BM * BKB;      // one slice's A block (bytes)
 constexpr int B_BLK = BN * BKB;
-constexpr int A_STAGE = S * A_BLK;   // 32 KB
-constexpr int B_STAGE = S * B_BLK;   // 16 KB
-constexpr int THREADS = 128;
-constexpr int TMEM_COLS = S * BN;    // 512
-constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 1024;
+constexpr int A_STAGE = S * A_BLK;   // 28 KB
+constexpr int B_STAGE = S * B_BLK;   // 14 KB
+constexpr int TMEM_COLS = 512;       // S * BN = 448 used (allocation is a power of two)
+constexpr int KMAX = 16384;          // int32 accumulator headroom
 
 // byte offset of (row r, k) inside a rows x BKB block in the canonical K-major layout
 __host__ __device__ __forceinline__ int blk_off(int r, int k) {
@@ -48,21 +48,22 @@ __device__ __forceinline__ int line_exponent(double amax) {
   return e;
 }
 
-// digits of x in (-1, 1): x = sum_s d_s 2^{-7s} + r, |r| < 2^{-7S}, d_s in [-127, 127]
+// balanced base-256 digits of rint(2^54 x) for x in (-1, 1), most significant first
 __device__ __forceinline__ void digits(double x, int8_t* d) {
+  long long X = __double2ll_rn(x * 0x1p54);
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    x *= 128.0;
-    const double t = trunc(x);
-    d[s] = int8_t(t);
-    x -= t;
+  for (int s = S - 1; s > 0; --s) {
+    const long long r = ((X + 128) & 255) - 128;
+    d[s] = int8_t(r);
+    X = (X - r) >> 8;
   }
+  d[0] = int8_t(X);
 }
 
-// A (M x K, column-major, lda) -> slices [mtile][kblk][s][A_BLK], exponents e[M].
+// A (M x K, column-major, lda) -> slices [mtile][kblk][s][A_BLK], row scales 2^e[M].
 // One warp per row (rows are strided by lda; M*K is small for the evaluation).
 __global__ void k_slice_rows(const double* __restrict__ A, int64_t lda, int64_t M, int64_t K,
-                             int64_t KB, int8_t* __restrict__ out, int* __restrict__ ex) {
+                             int64_t KB, int8_t* __restrict__ out, double* __restrict__ ex) {
   const int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (i >= M) return;
@@ -70,7 +71,7 @@ __global__ void k_slice_rows(const double* __restrict__ A, int64_t lda, int64_t 
   for (int64_t k = lane; k < K; k += 32) amax = fmax(amax, fabs(A[i + k * lda]));
   for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
   const int e = line_exponent(amax);
-  if (lane == 0) ex[i] = e;
+  if (lane == 0) ex[i] = ldexp(1.0, e);
   const int64_t mt = i / BM;
   const int r = int(i % BM);
   for (int64_t k = lane; k < KB * BKB; k += 32) {
@@ -85,9 +86,9 @@ __global__ void k_slice_rows(const double* __restrict__ A, int64_t lda, int64_t 
 }
 
 // B (K x N, column-major, ldb: columns contiguous in k) -> slices [ntile][kblk][s][B_BLK],
-// exponents f[N].  One warp per column.
+// column scales 2^f[N].  One warp per column.
 __global__ void k_slice_cols(const double* __restrict__ B, int64_t ldb, int64_t N, int64_t K,
-                             int64_t KB, int8_t* __restrict__ out, int* __restrict__ ex) {
+                             int64_t KB, int8_t* __restrict__ out, double* __restrict__ ex) {
   const int64_t n = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (n >= N) return;
@@ -96,7 +97,7 @@ __global__ void k_slice_cols(const double* __restrict__ B, int64_t ldb, int64_t 
   for (int64_t k = lane; k < K; k += 32) amax = fmax(amax, fabs(col[k]));
   for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
   const int f = line_exponent(amax);
-  if (lane == 0) ex[n] = f;
+  if (lane == 0) ex[n] = ldexp(1.0, f);
   const int64_t nt = n / BN;
   const int r = int(n % BN);
   for (int64_t k = lane; k < KB * BKB; k += 32) {
@@ -147,12 +148,13 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint3
   return addr | (uint64_t((lbo >> 4) & 0x3FFF) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
          (uint64_t(1) << 46);
 }
-// InstrDescriptor: c_format S32 (2) [4,6), a/b format signed int8 (1) [7,10) [10,13),
+// InstrDescriptor: c_format S32 (2) [4,6), a/b format s8 (1) [7,10) [10,13),
 // K-major A and B, N>>3 at [17,23), M>>4 at [24,29)
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
                             (uint32_t(BM >> 4) << 24);
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                       uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -164,40 +166,56 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, int* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
+        "=r"(v[7])
       : "r"(taddr));
 }
 
-// C[i + ldc n] = sum over the tile's int8 slice products (see header), for the tile
-// (blockIdx.y, blockIdx.x) of an M x N output; KB k-blocks.
-__global__ void __launch_bounds__(THREADS, 1)
-k_gemm_i8(const int8_t* __restrict__ As, const int* __restrict__ ea, const int8_t* __restrict__ Bs,
-          const int* __restrict__ eb, int64_t M, int64_t N, int64_t KB, double* __restrict__ C,
-          int64_t ldc) {
+
+
+// Persistent, warp-specialised GEMM over the M x N output tiles (tile t: mt = t % tiles_m,
+// nt = t / tiles_m; M tiles fastest, so the CTAs sharing a B column tile run together and
+// B streams from HBM once while the small A operand stays in L2).
+//   warp 0 lane 0: producer, bulk copies of (A, B) k-block slices into a STAGES ring;
+//   warp 1 lane 0: MMA issuer, 28 tcgen05.mma.kind::i8 per k-block into 7 TMEM groups;
+//   warps 2-5    : epilogue, fold the 7 int32 groups of each element into two exact int64
+//                  words, release TMEM to the next tile's MMAs, then scale and store C.
+constexpr int PTHREADS = 192;
+constexpr int EPI_COLS = 4;  // columns per TMEM drain step
+constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 256;
+
+__global__ void __launch_bounds__(PTHREADS, 1)
+k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
+          const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N, int64_t KB, double* __restrict__ C,
+          int64_t ldc, int64_t tiles_m, int64_t tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
-  const int64_t nt = blockIdx.x, mt = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 4);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -207,80 +225,104 @@ k_gemm_i8(const int8_t* __restrict__ As, const int* __restrict__ ea, const int8_
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  const int8_t* gA = As + (mt * KB) * int64_t(A_STAGE);
-  const int8_t* gB = Bs + (nt * KB) * int64_t(B_STAGE);
-  if (threadIdx.x == 0) {
-    // prologue: fill the ring
-    for (int64_t kb = 0; kb < KB && kb < STAGES; ++kb) {
-      mbar_expect_tx(&full[kb], A_STAGE + B_STAGE);
-      bulk_g2s(sA + kb * A_STAGE, gA + kb * A_STAGE, A_STAGE, &full[kb]);
-      bulk_g2s(sB + kb * B_STAGE, gB + kb * B_STAGE, B_STAGE, &full[kb]);
-    }
-    for (int64_t kb = 0; kb < KB; ++kb) {
-      const int st = int(kb % STAGES);
-      const uint32_t ph = uint32_t((kb / STAGES) & 1);
-      mbar_wait(&full[st], ph);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint8_t* a0 = sA + st * A_STAGE;
-      const uint8_t* b0 = sB + st * B_STAGE;
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
-          if (s + t > S - 1) continue;  // keep groups g = s + t + 2 <= S + 1
-          const int g = s + t;
-          const uint64_t da = smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128);
-          const uint64_t db = smem_desc(b0 + t * B_BLK, 128, (BKB / 16) * 128);
-          // the first product into group g at kb = 0 overwrites the accumulator
-          const uint32_t acc = (kb > 0 || s > 0) ? 1u : 0u;
-          mma_i8(tmem + uint32_t(g * BN), da, db, acc);
+  if (warp == 0) {
+    if (lane == 0) {
+      int64_t it = 0;  // k-blocks loaded by this CTA (ring position)
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int8_t* gA = As + ((t % tiles_m) * KB) * int64_t(A_STAGE);
+        const int8_t* gB = Bs + ((t / tiles_m) * KB) * int64_t(B_STAGE);
+        for (int64_t kb = 0; kb < KB; ++kb, ++it) {
+          const int st = int(it % STAGES);
+          if (it >= STAGES) mbar_wait(&empty[st], uint32_t(((it / STAGES) - 1) & 1));
+          mbar_expect_tx(&full[st], A_STAGE + B_STAGE);
+          bulk_g2s(sA + st * A_STAGE, gA + kb * A_STAGE, A_STAGE, &full[st]);
+          bulk_g2s(sB + st * B_STAGE, gB + kb * B_STAGE, B_STAGE, &full[st]);
         }
       }
-      mma_commit(&empty[st]);
-      const int64_t nk = kb + STAGES;
-      if (nk < KB) {  // refill this stage once its MMAs have drained it
-        mbar_wait(&empty[st], ph);
-        mbar_expect_tx(&full[st], A_STAGE + B_STAGE);
-        bulk_g2s(sA + st * A_STAGE, gA + nk * A_STAGE, A_STAGE, &full[st]);
-        bulk_g2s(sB + st * B_STAGE, gB + nk * B_STAGE, B_STAGE, &full[st]);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int64_t it = 0, tc = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tc) {
+        if (tc > 0) mbar_wait(tmem_empty, uint32_t((tc - 1) & 1));  // epilogue drained TMEM
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int64_t kb = 0; kb < KB; ++kb, ++it) {
+          const int st = int(it % STAGES);
+          mbar_wait(&full[st], uint32_t((it / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint8_t* a0 = sA + st * A_STAGE;
+          const uint8_t* b0 = sB + st * B_STAGE;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+#pragma unroll
+            for (int u = 0; u < S - s; ++u) {  // groups g = s + u <= S - 1
+              const uint64_t da = smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128);
+              const uint64_t db = smem_desc(b0 + u * B_BLK, 128, (BKB / 16) * 128);
+              // the first product into group g at kb = 0 overwrites the accumulator
+              mma_i8(tmem + uint32_t((s + u) * BN), da, db, (kb > 0 || s > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[st]);  // frees the stage when these MMAs retire
+        }
+        mma_commit(tmem_full);
       }
     }
-    mma_commit(done);
-  }
-  __syncwarp();
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-
-  // epilogue: warp w owns TMEM lanes (tile rows) 32w .. 32w+31
-  const int64_t i = mt * BM + warp * 32 + lane;
-  const double si = i < M ? 1.0 : 0.0;
-  const int ei = i < M ? ea[i] : 0;
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    double acc[16];
+  } else {
+    // epilogue warps 2..5 own TMEM lane quadrant (warp % 4) = tile rows 32 q .. 32 q + 31
+    const int q = warp % 4;
+    int64_t tc = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tc) {
+      const int64_t mt = t % tiles_m, nt = t / tiles_m;
+      // row / column scales, fetched before the accumulators are ready
+      const int64_t i = mt * BM + q * 32 + lane;
+      const int64_t n0 = nt * BN;
+      const double ri = i < M ? ra[i] : 0.0;
+      const double c0s = n0 + lane < N ? cb[n0 + lane] : 0.0;
+      const double c1s = n0 + 32 + lane < N ? cb[n0 + 32 + lane] : 0.0;
+      mbar_wait(tmem_full, uint32_t(tc & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      // value = (hi 2^-36 + lo 2^-60) 2^e_i 2^f_n with hi = sum_{g<=3} D_g 2^{8(3-g)} and
+      // lo = sum_{g>=4} D_g 2^{8(6-g)} exact int64 words (one rounding, in the sum)
+      double out[BN];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      for (int c0 = 0; c0 < BN; c0 += EPI_COLS) {
+        int v[S][EPI_COLS];
 #pragma unroll
-    for (int g = 0; g < S; ++g) {
-      uint32_t v[16];
-      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(g * BN + c0), v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      const double scale = ldexp(1.0, -7 * (g + 2));
+        for (int g = 0; g < S; ++g)
+          tmem_ld4(tmem + (uint32_t(q * 32) << 16) + uint32_t(g * BN + c0), v[g]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] += double(int32_t(v[j])) * scale;
-    }
-    if (i < M) {
+        for (int j = 0; j < EPI_COLS; ++j) {
+          long long h = v[0][j];
+          h = h * 256 + v[1][j];
+          h = h * 256 + v[2][j];
+          h = h * 256 + v[3][j];
+          long long l = v[4][j];
+          l = l * 256 + v[5][j];
+          l = l * 256 + v[6][j];
+          const double cs = __shfl_sync(0xffffffffu, c0 + j < 32 ? c0s : c1s, (c0 + j) % 32);
+          out[c0 + j] = (double(h) * 0x1p-36 + double(l) * 0x1p-60) * ri * cs;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty))
+                     : "memory");
+      if (i < M) {
+        double* ci = C + i + ldc * n0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int64_t n = nt * BN + c0 + j;
-        if (n < N) C[i + ldc * n] = si * ldexp(acc[j], ei + eb[n]);
+        for (int j = 0; j < BN; ++j)
+          if (n0 + j < N) ci[ldc * j] = out[j];
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "r"(TMEM_COLS));
+  }
 }
 
 }  // namespace oz

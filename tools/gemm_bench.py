@@ -42,4 +42,4 @@ for name, M, N, K, ta, tb in shapes:
         ms = e0.elapsed_time(e1) / reps
         parts = ", ".join(f"{k} {v[1] / reps:.2f} ms" for k, v in prof.items())
         print(f"{vname} cfg{os.environ.get('LATSUM_GEMM_CFG','0')} {name:14s} {M}x{N}x{K}: "
-              f"{2*M*N*K/ms/1e12:6.2f} TF/s ({ms:.2f} ms) [{parts}]")
+              f"{2*M*N*K/ms/1e9:6.2f} TF/s ({ms:.2f} ms) [{parts}]")

@@ -39,6 +39,10 @@ sys.path.insert(0, ROOT)
 METRIC = "lattice-sum+RHOSVD wall ms"
 FP64_PEAK_TFLOPS = 37.0  # DMMA microbenchmark on this pool (tools/fp64_peak.cu, profiles/)
 FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu mma.sync f64 loop (profiles/fp64_peak_r01.txt)"
+# int8 tensor-core peak for the Ozaki-scheme slab GEMM (28 int8 products per FP64 product)
+I8_PEAK_TOPS = 4600.0
+I8_PEAK_SOURCE = "measured: tools/i8_mma_peak.cu tcgen05.mma kind::i8 N=128 loop (profiles/i8_mma_peak_r01.txt)"
+OZAKI_PRODUCTS = 28
 
 
 def load_peaks():
@@ -280,7 +284,13 @@ def run_gpu(args):
     peaks = load_peaks()
     if dom_tag == "gemm_eval_canonical":  # K = merged rank (17): output-write bound
         dom_work = 8.0 * n_my
-    if is_flops:
+    is_ozaki = "ozaki" in dom_tag
+    fp64_equiv = None
+    if is_ozaki:  # int8 tensor cores: count the int8 ops the kernel actually issues
+        fp64_equiv = dom_work / (dom_ms * 1e-3) / 1e12
+        achieved = OZAKI_PRODUCTS * fp64_equiv
+        peak, unit, bound = I8_PEAK_TOPS, "TOP/s", "tensor"
+    elif is_flops:
         achieved = dom_work / (dom_ms * 1e-3) / 1e12
         peak, unit, bound = FP64_PEAK_TFLOPS, "TFLOP/s", "tensor"
     else:
@@ -288,7 +298,7 @@ def run_gpu(args):
         peak, unit, bound = float(peaks.get("hbm_gbs", 6557.8)), "GB/s", "hbm"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath) and dom_tag == "gemm_eval_slab" and do_eval:
+    if os.path.exists(tpath) and dom_tag.startswith("gemm_eval_slab") and do_eval:
         # ncu --set full DRAM bytes per 2048^2 slice (profiles/ncu_eval_r01.md), per launch
         tr = json.load(open(tpath)).get(dom_tag)
         if tr:
@@ -370,9 +380,14 @@ def run_gpu(args):
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom_tag,
                          "launches": dom_n, "ms": dom_ms,
-                         "peak_source": FP64_PEAK_SOURCE if is_flops else "MEASURED_PEAKS.json hbm_gbs",
-                         "algorithmic": ("2 r1 flops per grid point of the slab GEMM" if is_flops
-                                         else "8 bytes written per grid point")},
+                         "peak_source": (I8_PEAK_SOURCE if is_ozaki else FP64_PEAK_SOURCE if is_flops
+                                         else "MEASURED_PEAKS.json hbm_gbs"),
+                         "algorithmic": ("28 int8 products x 2 r1 ops per grid point (Ozaki scheme, "
+                                         "FP64-accurate slab GEMM on the int8 tensor cores)" if is_ozaki
+                                         else "2 r1 flops per grid point of the slab GEMM" if is_flops
+                                         else "8 bytes written per grid point"),
+                         "fp64_equivalent_tflops": fp64_equiv,
+                         "fp64_dmma_peak_tflops": FP64_PEAK_TFLOPS},
             "kernel_profile": {k: {"launches": v[0], "ms": round(v[1], 4),
                                    "rate": (v[2] / (v[1] * 1e-3) / (1e12 if k.startswith("gemm") else 1e9))
                                    if v[1] > 0 else None}

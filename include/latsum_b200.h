@@ -237,11 +237,12 @@ int latsum_dgemm_device(latsum_ctx* ctx, int ta, int tb, int64_t M, int64_t N, i
                         double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                         double beta, double* C, int64_t ldc);
 
-/* FP64-accurate C = A B (column-major, no transposes) computed on the int8 tensor cores
+/* FP64-accurate C = A op(B) (column-major; op(B) = B^T when tb != 0) computed on the int8 tensor cores
  * by the Ozaki splitting (7 int8 slices per operand, tcgen05.mma.kind::i8, int32 TMEM
  * accumulators); K <= 16384.  Used by the Tucker evaluation when LATSUM_EVAL_GEMM=ozaki. */
-int latsum_dgemm_ozaki_device(latsum_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A,
-                              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
+int latsum_dgemm_ozaki_device(latsum_ctx* ctx, int tb, int64_t M, int64_t N, int64_t K,
+                              const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                              int64_t ldc);
 
 #ifdef __cplusplus
 }

@@ -115,7 +115,7 @@ SIGNATURES = [
     ("latsum_tensor_read", _I, [_P, ctypes.c_char_p, _P, _P]),
     ("latsum_dgemm_device", _I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P,
                                  _I64]),
-    ("latsum_dgemm_ozaki_device", _I, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
+    ("latsum_dgemm_ozaki_device", _I, [_P, _I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
 ]
 
 _lib = None
@@ -137,7 +137,8 @@ def lib():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `make -C {CSRC}` "
                 "(there is no CPU fallback for the lattice-sum path)")
-        L = ctypes.CDLL(LIB_PATH)
+        # LATSUM_LIBRARY: an instrumented build of the same sources (dev tools only)
+        L = ctypes.CDLL(os.environ.get("LATSUM_LIBRARY", LIB_PATH))
         for name, res, args in SIGNATURES:
             f = getattr(L, name)
             f.restype = res

@@ -400,8 +400,13 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
 // ------------------------------------------------------------------ Ozaki int8 GEMM
 // C (M x N, ldc) = A (M x K, lda) B (K x N, ldb), all column-major, on the int8 tensor
 // cores (ozaki_i8.cuh).  Slices live in stream-ordered workspaces.
+// C (M x N, ldc) = A (M x K, lda) op(B), op(B) = B (K x N, ldb) or B^T (B: N x K, ldb),
+// all column-major, on the int8 tensor cores (ozaki_i8.cuh).  Output column n is written
+// at C + (n / nb) bs + (n % nb) ldc (nb = 0: N, a plain GEMM), so the batched slab GEMMs
+// of the evaluators (one A, contiguous B slabs) are one launch.
 void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-                const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)") {
+                const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)",
+                int64_t nb = 0, int64_t bs = 0, bool tb = false) {
   if (M <= 0 || N <= 0) return;
   require(K <= oz::KMAX, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
   if (!c->oz_smem_set) {
@@ -411,20 +416,29 @@ void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
   }
   const int64_t KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
   const int64_t tm = (M + oz::BM - 1) / oz::BM, tn = (N + oz::BN - 1) / oz::BN;
-  require(tm * tn < (int64_t(1) << 31), "ozaki_gemm: too many tiles");
+  require(tm * tn < (int64_t(1) << 31) && tm * KB < (int64_t(1) << 31) && tn * KB < (int64_t(1) << 31),
+          "ozaki_gemm: too many tiles");
   const size_t a_bytes = size_t(tm) * KB * oz::A_STAGE, b_bytes = size_t(tn) * KB * oz::B_STAGE;
   DBuf sa(c, (a_bytes + 7) / 8), sb(c, (b_bytes + 7) / 8);
   DBuf ra(c, size_t(M)), cb(c, size_t(N));
   int8_t* pa = reinterpret_cast<int8_t*>(sa.p);
   int8_t* pb = reinterpret_cast<int8_t*>(sb.p);
-  // rows/columns past M/N inside the last tile must be zero digits
-  if (M % oz::BM) CK(cudaMemsetAsync(pa + size_t(tm - 1) * KB * oz::A_STAGE, 0, size_t(KB) * oz::A_STAGE, c->stream));
-  if (N % oz::BN) CK(cudaMemsetAsync(pb + size_t(tn - 1) * KB * oz::B_STAGE, 0, size_t(KB) * oz::B_STAGE, c->stream));
+  // lines: rows of A (element (i, k) at A[i + k lda]); columns of op(B)
+  const int64_t bsl = tb ? 1 : ldb, bsk = tb ? ldb : 1;
   {
     ProfScope ps(c, "ozaki(slice)", double(M * K + K * N) * 8.0 + double(a_bytes + b_bytes));
-    oz::k_slice_rows<<<unsigned((M * 32 + 255) / 256), 256, 0, c->stream>>>(A, lda, M, K, KB, pa, ra.p);
+    auto vec = [](const double* P, int64_t sl, int64_t sk) {
+      return sk == 1 && sl % 2 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+    };
+    if (vec(A, 1, lda))
+      oz::k_slice_tile<oz::BM, true><<<unsigned(tm), 2 * oz::BM, 0, c->stream>>>(A, 1, lda, M, K, KB, ra.p, pa);
+    else
+      oz::k_slice_tile<oz::BM, false><<<unsigned(tm), 2 * oz::BM, 0, c->stream>>>(A, 1, lda, M, K, KB, ra.p, pa);
     post_launch(c);
-    oz::k_slice_cols<<<unsigned((N * 32 + 255) / 256), 256, 0, c->stream>>>(B, ldb, N, K, KB, pb, cb.p);
+    if (vec(B, bsl, bsk))
+      oz::k_slice_tile<oz::BN, true><<<unsigned(tn), 2 * oz::BN, 0, c->stream>>>(B, bsl, bsk, N, K, KB, cb.p, pb);
+    else
+      oz::k_slice_tile<oz::BN, false><<<unsigned(tn), 2 * oz::BN, 0, c->stream>>>(B, bsl, bsk, N, K, KB, cb.p, pb);
     post_launch(c);
   }
   ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(K));
@@ -432,9 +446,30 @@ void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
-  oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(pa, ra.p, pb, cb.p, M, N, KB, C, ldc,
-                                                                   tm, tiles);
+  oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
+      pa, ra.p, pb, cb.p, M, N, KB, C, ldc, nb > 0 ? nb : N, bs, tm, tiles);
   post_launch(c);
+#ifdef LATSUM_OZ_TRACE
+  {
+    unsigned long long h[2];
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyFromSymbol(h, oz::g_oz_trace, sizeof(h)));
+    fprintf(stderr, "ozaki trace: MMA thread %.0f clk/CTA, waiting for TMEM %.1f%%\n",
+            double(h[0]) / ctas, 100.0 * double(h[1]) / double(h[0]));
+    const unsigned long long z[2] = {0, 0};
+    CK(cudaMemcpyToSymbol(oz::g_oz_trace, z, sizeof(z)));
+  }
+#endif
+}
+
+// Evaluation slab GEMMs: int8 tensor cores (Ozaki, default) or FP64 DMMA
+// (LATSUM_EVAL_GEMM=dmma).
+bool eval_uses_ozaki(int64_t K) {
+  static const bool dmma = [] {
+    const char* e = std::getenv("LATSUM_EVAL_GEMM");
+    return e && std::string(e) == "dmma";
+  }();
+  return !dmma && K <= oz::KMAX;
 }
 
 // ------------------------------------------------------------------ syevd
@@ -1748,8 +1783,17 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
     gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
     for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
       const int64_t nkk = std::min(nkc, nk - k0);
-      gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
-           r0 * njj, tagged("gemm_eval_x"));
+      if (eval_uses_ozaki(r2))
+        ozaki_gemm(c, r0 * njj, nkk, r2, Q.p, r0 * njj, U2 + k0, t.N[2], X.p, r0 * njj,
+                   "gemm_eval_x(ozaki-i8)", 0, 0, /*tb=*/true);
+      else
+        gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
+             r0 * njj, tagged("gemm_eval_x"));
+      if (eval_uses_ozaki(r0)) {
+        ozaki_gemm(c, ni, njj * nkk, r0, U0, t.N[0], X.p, r0, out + k0 * ni * nj + j0 * ni, ni,
+                   "gemm_eval_slab(ozaki-i8)", njj, ni * nj);
+        continue;
+      }
       GemmOpts ov = tagged("gemm_eval_slab");
       ov.batch = nkk;
       ov.sB = r0 * njj;
@@ -1803,6 +1847,10 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
     k_canonical_slab_operand<<<grid_for(T * nj * nkk), 256, 0, c->stream>>>(
         D[1], ld[1], D[2], ld[2], tc[1], tc[2], tw, T, 0, nj, k0, nkk, X.p);
     post_launch(c);
+    if (eval_uses_ozaki(T)) {
+      ozaki_gemm(c, ni, nj * nkk, T, A0.p, ni, X.p, T, out + k0 * ni * nj, ni, tag);
+      continue;
+    }
     GemmOpts ov = tagged(tag);
     ov.batch = nkk;
     ov.sB = T * nj;
@@ -2502,13 +2550,14 @@ int latsum_dgemm_device(latsum_ctx* c, int ta, int tb, int64_t M, int64_t N, int
   });
 }
 
-int latsum_dgemm_ozaki_device(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
-                              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+int latsum_dgemm_ozaki_device(latsum_ctx* c, int tb, int64_t M, int64_t N, int64_t K,
+                              const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                              int64_t ldc) {
   return guarded(c, [&] {
     require(A && B && C && M >= 0 && N >= 0 && K >= 0 && lda >= std::max<int64_t>(M, 1) &&
-                ldb >= std::max<int64_t>(K, 1) && ldc >= std::max<int64_t>(M, 1),
+                ldb >= std::max<int64_t>(tb ? N : K, 1) && ldc >= std::max<int64_t>(M, 1),
             "latsum_dgemm_ozaki_device: bad argument");
-    ozaki_gemm(c, M, N, K, A, lda, B, ldb, C, ldc);
+    ozaki_gemm(c, M, N, K, A, lda, B, ldb, C, ldc, "gemm(ozaki-i8)", 0, 0, tb != 0);
   });
 }
 

@@ -60,54 +60,73 @@ __device__ __forceinline__ void digits(double x, int8_t* d) {
   d[0] = int8_t(X);
 }
 
-// A (M x K, column-major, lda) -> slices [mtile][kblk][s][A_BLK], row scales 2^e[M].
-// One warp per row (rows are strided by lda; M*K is small for the evaluation).
-__global__ void k_slice_rows(const double* __restrict__ A, int64_t lda, int64_t M, int64_t K,
-                             int64_t KB, int8_t* __restrict__ out, double* __restrict__ ex) {
-  const int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (i >= M) return;
-  double amax = 0.0;
-  for (int64_t k = lane; k < K; k += 32) amax = fmax(amax, fabs(A[i + k * lda]));
-  for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-  const int e = line_exponent(amax);
-  if (lane == 0) ex[i] = ldexp(1.0, e);
-  const int64_t mt = i / BM;
-  const int r = int(i % BM);
-  for (int64_t k = lane; k < KB * BKB; k += 32) {
-    int8_t d[S];
-    const double x = k < K ? ldexp(A[i + k * lda], -e) : 0.0;
-    digits(x, d);
-    const int64_t kb = k / BKB;
-    int8_t* base = out + ((mt * KB + kb) * S) * int64_t(A_BLK);
+// Operands are "lines" (rows of A, columns of B) of K elements: element (l, k) of the
+// FP64 source is P[l * sl + k * sk].  One CTA slices a tile of ROWS lines over all
+// k-blocks: pass 1 finds each line's scale 2^e (max |x| 2^-e < 1; 1 for a zero line),
+// pass 2 re-reads the tile (L1/L2-resident) and writes its S digit blocks per k-block in
+// the canonical K-major layout, 16 k-bytes of one line per thread as 16-byte stores.
+// VEC: lines are contiguous (sk == 1) and 16-byte aligned, loads are double2.
+template <int ROWS, bool VEC>
+__device__ __forceinline__ void load16(const double* __restrict__ p, int64_t sk, int64_t k0,
+                                       int64_t K, double* x) {
+  if (VEC && k0 + 16 <= K) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) base[s * A_BLK + blk_off(r, int(k % BKB))] = d[s];
+    for (int kk = 0; kk < 16; kk += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(p + k0 + kk);
+      x[kk] = v.x;
+      x[kk + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) x[kk] = k0 + kk < K ? p[(k0 + kk) * sk] : 0.0;
   }
 }
 
-// B (K x N, column-major, ldb: columns contiguous in k) -> slices [ntile][kblk][s][B_BLK],
-// column scales 2^f[N].  One warp per column.
-__global__ void k_slice_cols(const double* __restrict__ B, int64_t ldb, int64_t N, int64_t K,
-                             int64_t KB, int8_t* __restrict__ out, double* __restrict__ ex) {
-  const int64_t n = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (n >= N) return;
-  const double* col = B + n * ldb;
+template <int ROWS, bool VEC>
+__global__ void __launch_bounds__(2 * ROWS)
+k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+             int64_t KB, double* __restrict__ scale, int8_t* __restrict__ out) {
+  __shared__ double part[ROWS];
+  const int64_t tile = blockIdx.x;
+  const int r = threadIdx.x % ROWS, h = threadIdx.x / ROWS;  // line in tile, k half
+  const int64_t l = tile * ROWS + r;
+  const double* p = P + (l < L ? l : 0) * sl;
   double amax = 0.0;
-  for (int64_t k = lane; k < K; k += 32) amax = fmax(amax, fabs(col[k]));
-  for (int off = 16; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-  const int f = line_exponent(amax);
-  if (lane == 0) ex[n] = ldexp(1.0, f);
-  const int64_t nt = n / BN;
-  const int r = int(n % BN);
-  for (int64_t k = lane; k < KB * BKB; k += 32) {
-    int8_t d[S];
-    const double x = k < K ? ldexp(col[k], -f) : 0.0;
-    digits(x, d);
-    const int64_t kb = k / BKB;
-    int8_t* base = out + ((nt * KB + kb) * S) * int64_t(B_BLK);
+  if (l < L) {
+    for (int64_t kb = 0; kb < KB; ++kb) {
+      double x[16];
+      load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
 #pragma unroll
-    for (int s = 0; s < S; ++s) base[s * B_BLK + blk_off(r, int(k % BKB))] = d[s];
+      for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
+    }
+  }
+  if (h == 1) part[r] = amax;
+  __syncthreads();
+  if (h == 0) part[r] = fmax(amax, part[r]);
+  __syncthreads();
+  const double sc = ldexp(1.0, line_exponent(part[r]));
+  if (h == 0 && l < L) scale[l] = sc;
+  const double inv = 1.0 / sc;  // exact: a power of two
+  for (int64_t kb = 0; kb < KB; ++kb) {
+    uint32_t w[S][4];
+#pragma unroll
+    for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
+    if (l < L) {
+      double x[16];
+      load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        int8_t d[S];
+        digits(x[kk] * inv, d);
+#pragma unroll
+        for (int s = 0; s < S; ++s) w[s][kk / 4] |= uint32_t(uint8_t(d[s])) << (8 * (kk % 4));
+      }
+    }
+    int8_t* base = out + ((tile * KB + kb) * S) * int64_t(ROWS * BKB) + blk_off(r, 16 * h);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint4*>(base + s * (ROWS * BKB)) =
+          make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
   }
 }
 
@@ -181,7 +200,8 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 
 
 
-// Persistent, warp-specialised GEMM over the M x N output tiles (tile t: mt = t % tiles_m,
+// Persistent, warp-specialised GEMM over the M x N output tiles (output column n at
+// C + (n / nb) bs + (n % nb) ldc, so a batch of slabs sharing A is one launch) (tile t: mt = t % tiles_m,
 // nt = t / tiles_m; M tiles fastest, so the CTAs sharing a B column tile run together and
 // B streams from HBM once while the small A operand stays in L2).
 //   warp 0 lane 0: producer, bulk copies of (A, B) k-block slices into a STAGES ring;
@@ -189,13 +209,17 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 //   warps 2-5    : epilogue, fold the 7 int32 groups of each element into two exact int64
 //                  words, release TMEM to the next tile's MMAs, then scale and store C.
 constexpr int PTHREADS = 192;
+#ifdef LATSUM_OZ_TRACE
+// summed over CTAs: MMA-thread cycles in the tile loop, cycles waiting for the epilogue
+__device__ unsigned long long g_oz_trace[2];
+#endif
 constexpr int EPI_COLS = 4;  // columns per TMEM drain step
 constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 256;
 
 __global__ void __launch_bounds__(PTHREADS, 1)
 k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
           const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N, int64_t KB, double* __restrict__ C,
-          int64_t ldc, int64_t tiles_m, int64_t tiles) {
+          int64_t ldc, int64_t nb, int64_t bs, int64_t tiles_m, int64_t tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
@@ -243,8 +267,17 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
   } else if (warp == 1) {
     if (lane == 0) {
       int64_t it = 0, tc = 0;
+#ifdef LATSUM_OZ_TRACE
+      long long w_tm = 0, t_begin = clock64();
+#endif
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tc) {
+#ifdef LATSUM_OZ_TRACE
+        const long long c0 = clock64();
+#endif
         if (tc > 0) mbar_wait(tmem_empty, uint32_t((tc - 1) & 1));  // epilogue drained TMEM
+#ifdef LATSUM_OZ_TRACE
+        w_tm += clock64() - c0;
+#endif
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         for (int64_t kb = 0; kb < KB; ++kb, ++it) {
           const int st = int(it % STAGES);
@@ -266,6 +299,10 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
         }
         mma_commit(tmem_full);
       }
+#ifdef LATSUM_OZ_TRACE
+      atomicAdd(&g_oz_trace[0], (unsigned long long)(clock64() - t_begin));
+      atomicAdd(&g_oz_trace[1], (unsigned long long)w_tm);
+#endif
     }
   } else {
     // epilogue warps 2..5 own TMEM lane quadrant (warp % 4) = tile rows 32 q .. 32 q + 31
@@ -310,10 +347,16 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty))
                      : "memory");
       if (i < M) {
-        double* ci = C + i + ldc * n0;
+        // column n lives at C + (n / nb) bs + (n % nb) ldc (batched slabs; nb = N: plain)
+        int64_t kk = n0 / nb, jj = n0 - kk * nb;
 #pragma unroll
-        for (int j = 0; j < BN; ++j)
-          if (n0 + j < N) ci[ldc * j] = out[j];
+        for (int j = 0; j < BN; ++j) {
+          if (n0 + j < N) C[i + kk * bs + jj * ldc] = out[j];
+          if (++jj == nb) {
+            jj = 0;
+            ++kk;
+          }
+        }
       }
     }
   }

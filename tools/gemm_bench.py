@@ -26,7 +26,7 @@ for name, M, N, K, ta, tb in shapes:
         ctx.check(_lib.lib().latsum_dgemm_device(ctx.handle, ta, tb, M, N, K, 1.0, A.data_ptr(), lda,
                                                  B.data_ptr(), ldb, 0.0, C.data_ptr(), M))
     def run_oz():
-        ctx.check(_lib.lib().latsum_dgemm_ozaki_device(ctx.handle, M, N, K, A.data_ptr(), M,
+        ctx.check(_lib.lib().latsum_dgemm_ozaki_device(ctx.handle, 0, M, N, K, A.data_ptr(), M,
                                                        B.data_ptr(), K, C.data_ptr(), M))
     variants = [("dmma", run)] + ([("ozaki", run_oz)] if ozaki and not ta and not tb else [])
     for vname, fn in variants:

@@ -13,9 +13,13 @@
 //
 // Data path: operands are pre-sliced into the canonical K-major "no swizzle" core-matrix
 // layout (8 rows x 16 bytes) per (tile, k-block, slice), so each pipeline stage is one
-// contiguous bulk copy (cp.async.bulk, TMA engine) completing on an mbarrier; one thread
-// issues tcgen05.mma.kind::i8 (M=128, N=64, K=32) into 7 TMEM accumulators;
-// tcgen05.commit frees a stage; four warps drain TMEM with tcgen05.ld.
+// contiguous bulk copy per operand (cp.async.bulk, TMA engine) completing on an mbarrier.
+// Tiles are 128 x 128 and every tile runs two passes over K, because TMEM (512 columns)
+// holds four 128-column int32 groups: pass 1 accumulates groups 0..3 (the 10 pairs with
+// s + t <= 3, slices 0..3 only), pass 2 groups 4..6 (18 pairs, all slices).  One thread
+// issues tcgen05.mma.kind::i8 (M=128, N=128, K=32); the N=128 shape halves the shared-
+// memory operand reads per product against N=64 (the MMA's smem port is the limit).
+// Eight epilogue warps drain TMEM with tcgen05.ld after each pass.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -25,14 +29,15 @@ namespace latsum_b200 {
 namespace oz {
 
 constexpr int S = 7;                 // slices per operand
-constexpr int BM = 128, BN = 64;     // output tile (TMEM lanes x accumulator columns)
+constexpr int BM = 128, BN = 128;    // output tile (TMEM lanes x accumulator columns)
 constexpr int BKB = 32;              // k-block (int8 elements = bytes) per stage
-constexpr int STAGES = 5;
+constexpr int STAGES = 4;
 constexpr int A_BLK = BM * BKB;      // one slice's A block (bytes)
 constexpr int B_BLK = BN * BKB;
-constexpr int A_STAGE = S * A_BLK;   // 28 KB
-constexpr int B_STAGE = S * B_BLK;   // 14 KB
-constexpr int TMEM_COLS = 512;       // S * BN = 448 used (allocation is a power of two)
+constexpr int A_STAGE = S * A_BLK;   // 28 KB (pass 2; pass 1 loads the first 4 slices)
+constexpr int B_STAGE = S * B_BLK;   // 28 KB
+constexpr int P1_SLICES = 4;         // pass 1: groups g = s + t <= 3
+constexpr int TMEM_COLS = 512;       // 4 groups x 128 columns
 constexpr int KMAX = 16384;          // int32 accumulator headroom
 
 // byte offset of (row r, k) inside a rows x BKB block in the canonical K-major layout
@@ -200,26 +205,48 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 
 
 
-// Persistent, warp-specialised GEMM over the M x N output tiles (output column n at
-// C + (n / nb) bs + (n % nb) ldc, so a batch of slabs sharing A is one launch) (tile t: mt = t % tiles_m,
-// nt = t / tiles_m; M tiles fastest, so the CTAs sharing a B column tile run together and
-// B streams from HBM once while the small A operand stays in L2).
-//   warp 0 lane 0: producer, bulk copies of (A, B) k-block slices into a STAGES ring;
-//   warp 1 lane 0: MMA issuer, 28 tcgen05.mma.kind::i8 per k-block into 7 TMEM groups;
-//   warps 2-5    : epilogue, fold the 7 int32 groups of each element into two exact int64
-//                  words, release TMEM to the next tile's MMAs, then scale and store C.
-constexpr int PTHREADS = 192;
+// Persistent, warp-specialised GEMM over the M x N output tiles; output column n lives at
+// C + (n / nb) bs + (n % nb) ldc, so a batch of slabs sharing A is one launch.  Tile t:
+// mt = t % tiles_m, nt = t / tiles_m (M tiles fastest: the CTAs sharing a B column tile run
+// together, B streams from HBM once and the small A operand stays in L2).
+//   warp 0 lane 0: producer, bulk copies of the (A, B) slices of each (pass, k-block);
+//   warp 1 lane 0: MMA issuer, per k-block 10 (pass 1) or 18 (pass 2) tcgen05.mma;
+//   warps 2-9    : epilogue; warp w owns TMEM lane quadrant w % 4 (tile rows) and column
+//                  half (w - 2) / 4.  After pass 1 it folds D_0..D_3 into the exact integer
+//                  hi = sum D_g 2^{8(3-g)} (a double: < 2^53 for K <= 1024), releases TMEM
+//                  for pass 2, then folds lo = sum_{g>=4} D_g 2^{8(6-g)} likewise and
+//                  writes (hi 2^-36 + lo 2^-60) 2^e_i 2^f_n (one rounding) while the next
+//                  tile's MMAs run.
+constexpr int EPI_WARPS = 8;
+constexpr int PTHREADS = 32 * (2 + EPI_WARPS);
+constexpr int EPI_COLS = BN / 2;  // columns per epilogue thread
+constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 128;
 #ifdef LATSUM_OZ_TRACE
 // summed over CTAs: MMA-thread cycles in the tile loop, cycles waiting for the epilogue
 __device__ unsigned long long g_oz_trace[2];
 #endif
-constexpr int EPI_COLS = 4;  // columns per TMEM drain step
-constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 256;
+
+// fold groups [g0, g0 + ng) of the 4-column chunk at TMEM column c into x (Horner, base 256)
+template <int NG>
+__device__ __forceinline__ void drain4(uint32_t taddr, double* x) {
+  int v[NG][4];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) tmem_ld4(taddr + uint32_t(g * BN), v[g]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double h = double(v[0][j]);
+#pragma unroll
+    for (int g = 1; g < NG; ++g) h = h * 256.0 + double(v[g][j]);
+    x[j] = h;
+  }
+}
 
 __global__ void __launch_bounds__(PTHREADS, 1)
 k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
-          const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N, int64_t KB, double* __restrict__ C,
-          int64_t ldc, int64_t nb, int64_t bs, int64_t tiles_m, int64_t tiles) {
+          const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N,
+          int64_t KB, double* __restrict__ C, int64_t ldc, int64_t nb, int64_t bs,
+          int64_t tiles_m, int64_t tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
@@ -236,7 +263,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 4);  // one arrival per epilogue warp
+    mbar_init(tmem_empty, EPI_WARPS);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -251,53 +278,66 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
 
   if (warp == 0) {
     if (lane == 0) {
-      int64_t it = 0;  // k-blocks loaded by this CTA (ring position)
+      int64_t it = 0;  // (pass, k-block) stages loaded by this CTA (ring position)
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int8_t* gA = As + ((t % tiles_m) * KB) * int64_t(A_STAGE);
         const int8_t* gB = Bs + ((t / tiles_m) * KB) * int64_t(B_STAGE);
-        for (int64_t kb = 0; kb < KB; ++kb, ++it) {
-          const int st = int(it % STAGES);
-          if (it >= STAGES) mbar_wait(&empty[st], uint32_t(((it / STAGES) - 1) & 1));
-          mbar_expect_tx(&full[st], A_STAGE + B_STAGE);
-          bulk_g2s(sA + st * A_STAGE, gA + kb * A_STAGE, A_STAGE, &full[st]);
-          bulk_g2s(sB + st * B_STAGE, gB + kb * B_STAGE, B_STAGE, &full[st]);
+        for (int pass = 0; pass < 2; ++pass) {
+          const uint32_t nsl = pass == 0 ? P1_SLICES : S;
+          for (int64_t kb = 0; kb < KB; ++kb, ++it) {
+            const int st = int(it % STAGES);
+            if (it >= STAGES) mbar_wait(&empty[st], uint32_t(((it / STAGES) - 1) & 1));
+            mbar_expect_tx(&full[st], nsl * (A_BLK + B_BLK));
+            bulk_g2s(sA + st * A_STAGE, gA + kb * A_STAGE, nsl * A_BLK, &full[st]);
+            bulk_g2s(sB + st * B_STAGE, gB + kb * B_STAGE, nsl * B_BLK, &full[st]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int64_t it = 0, tc = 0;
+      int64_t it = 0, np = 0;  // np: passes issued (TMEM phase)
 #ifdef LATSUM_OZ_TRACE
       long long w_tm = 0, t_begin = clock64();
 #endif
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tc) {
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int pass = 0; pass < 2; ++pass, ++np) {
 #ifdef LATSUM_OZ_TRACE
-        const long long c0 = clock64();
+          const long long c0 = clock64();
 #endif
-        if (tc > 0) mbar_wait(tmem_empty, uint32_t((tc - 1) & 1));  // epilogue drained TMEM
+          if (np > 0) mbar_wait(tmem_empty, uint32_t((np - 1) & 1));  // previous pass drained
 #ifdef LATSUM_OZ_TRACE
-        w_tm += clock64() - c0;
+          w_tm += clock64() - c0;
 #endif
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        for (int64_t kb = 0; kb < KB; ++kb, ++it) {
-          const int st = int(it % STAGES);
-          mbar_wait(&full[st], uint32_t((it / STAGES) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          const uint8_t* a0 = sA + st * A_STAGE;
-          const uint8_t* b0 = sB + st * B_STAGE;
+          for (int64_t kb = 0; kb < KB; ++kb, ++it) {
+            const int st = int(it % STAGES);
+            mbar_wait(&full[st], uint32_t((it / STAGES) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint8_t* a0 = sA + st * A_STAGE;
+            const uint8_t* b0 = sB + st * B_STAGE;
+            const uint32_t acc0 = kb > 0 ? 1u : 0u;
+            if (pass == 0) {
 #pragma unroll
-          for (int s = 0; s < S; ++s) {
+              for (int s = 0; s < P1_SLICES; ++s)
 #pragma unroll
-            for (int u = 0; u < S - s; ++u) {  // groups g = s + u <= S - 1
-              const uint64_t da = smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128);
-              const uint64_t db = smem_desc(b0 + u * B_BLK, 128, (BKB / 16) * 128);
-              // the first product into group g at kb = 0 overwrites the accumulator
-              mma_i8(tmem + uint32_t((s + u) * BN), da, db, (kb > 0 || s > 0) ? 1u : 0u);
+                for (int u = 0; u < P1_SLICES - s; ++u)  // g = s + u <= 3
+                  mma_i8(tmem + uint32_t((s + u) * BN),
+                         smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128),
+                         smem_desc(b0 + u * B_BLK, 128, (BKB / 16) * 128), s > 0 ? 1u : acc0);
+            } else {
+#pragma unroll
+              for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int u = (s < 4 ? 4 - s : 0); u < S - s; ++u)  // 4 <= g <= 6
+                  mma_i8(tmem + uint32_t((s + u - 4) * BN),
+                         smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128),
+                         smem_desc(b0 + u * B_BLK, 128, (BKB / 16) * 128), s > 0 ? 1u : acc0);
             }
+            mma_commit(&empty[st]);  // frees the stage when these MMAs retire
           }
-          mma_commit(&empty[st]);  // frees the stage when these MMAs retire
+          mma_commit(tmem_full);
         }
-        mma_commit(tmem_full);
       }
 #ifdef LATSUM_OZ_TRACE
       atomicAdd(&g_oz_trace[0], (unsigned long long)(clock64() - t_begin));
@@ -305,40 +345,37 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
 #endif
     }
   } else {
-    // epilogue warps 2..5 own TMEM lane quadrant (warp % 4) = tile rows 32 q .. 32 q + 31
-    const int q = warp % 4;
-    int64_t tc = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tc) {
+    const int q = warp % 4, half = (warp - 2) / 4;
+    const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * EPI_COLS);
+    int64_t np = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, np += 2) {
       const int64_t mt = t % tiles_m, nt = t / tiles_m;
-      // row / column scales, fetched before the accumulators are ready
       const int64_t i = mt * BM + q * 32 + lane;
-      const int64_t n0 = nt * BN;
+      const int64_t n0 = nt * BN + half * EPI_COLS;
+      // row / column scales, fetched before the accumulators are ready
       const double ri = i < M ? ra[i] : 0.0;
       const double c0s = n0 + lane < N ? cb[n0 + lane] : 0.0;
       const double c1s = n0 + 32 + lane < N ? cb[n0 + 32 + lane] : 0.0;
-      mbar_wait(tmem_full, uint32_t(tc & 1));
+      double hv[EPI_COLS];
+      mbar_wait(tmem_full, uint32_t(np & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      // value = (hi 2^-36 + lo 2^-60) 2^e_i 2^f_n with hi = sum_{g<=3} D_g 2^{8(3-g)} and
-      // lo = sum_{g>=4} D_g 2^{8(6-g)} exact int64 words (one rounding, in the sum)
-      double out[BN];
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += EPI_COLS) {
-        int v[S][EPI_COLS];
+      for (int c = 0; c < EPI_COLS; c += 4) drain4<4>(tq + uint32_t(c), hv + c);
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty))
+                     : "memory");
+      mbar_wait(tmem_full, uint32_t((np + 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-        for (int g = 0; g < S; ++g)
-          tmem_ld4(tmem + (uint32_t(q * 32) << 16) + uint32_t(g * BN + c0), v[g]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int c = 0; c < EPI_COLS; c += 4) {
+        double lv[4];
+        drain4<3>(tq + uint32_t(c), lv);
 #pragma unroll
-        for (int j = 0; j < EPI_COLS; ++j) {
-          long long h = v[0][j];
-          h = h * 256 + v[1][j];
-          h = h * 256 + v[2][j];
-          h = h * 256 + v[3][j];
-          long long l = v[4][j];
-          l = l * 256 + v[5][j];
-          l = l * 256 + v[6][j];
-          const double cs = __shfl_sync(0xffffffffu, c0 + j < 32 ? c0s : c1s, (c0 + j) % 32);
-          out[c0 + j] = (double(h) * 0x1p-36 + double(l) * 0x1p-60) * ri * cs;
+        for (int j = 0; j < 4; ++j) {
+          const double cs = __shfl_sync(0xffffffffu, c + j < 32 ? c0s : c1s, (c + j) % 32);
+          hv[c + j] = (hv[c + j] * 0x1p-36 + lv[j] * 0x1p-60) * ri * cs;
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -347,11 +384,10 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty))
                      : "memory");
       if (i < M) {
-        // column n lives at C + (n / nb) bs + (n % nb) ldc (batched slabs; nb = N: plain)
         int64_t kk = n0 / nb, jj = n0 - kk * nb;
 #pragma unroll
-        for (int j = 0; j < BN; ++j) {
-          if (n0 + j < N) C[i + kk * bs + jj * ldc] = out[j];
+        for (int j = 0; j < EPI_COLS; ++j) {
+          if (n0 + j < N) C[i + kk * bs + jj * ldc] = hv[j];
           if (++jj == nb) {
             jj = 0;
             ++kk;

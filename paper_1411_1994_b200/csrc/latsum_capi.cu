@@ -400,54 +400,65 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
 // ------------------------------------------------------------------ Ozaki int8 GEMM
 // C (M x N, ldc) = A (M x K, lda) B (K x N, ldb), all column-major, on the int8 tensor
 // cores (ozaki_i8.cuh).  Slices live in stream-ordered workspaces.
-// C (M x N, ldc) = A (M x K, lda) op(B), op(B) = B (K x N, ldb) or B^T (B: N x K, ldb),
-// all column-major, on the int8 tensor cores (ozaki_i8.cuh).  Output column n is written
-// at C + (n / nb) bs + (n % nb) ldc (nb = 0: N, a plain GEMM), so the batched slab GEMMs
-// of the evaluators (one A, contiguous B slabs) are one launch.
-void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-                const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)",
-                int64_t nb = 0, int64_t bs = 0, bool tb = false) {
-  if (M <= 0 || N <= 0) return;
+// ------------------------------------------------------------------ Ozaki int8 GEMM
+// An operand sliced for the int8 tensor cores (ozaki_i8.cuh): L lines of K elements, the
+// element (l, k) read from P[l sl + k sk], as S digit slices per (tile, k-block) in the
+// canonical layout plus the per-line scales 2^e.  A side: lines = rows of A; B side:
+// lines = columns of op(B).  A sliced operand is reused across GEMMs that share it.
+struct OzSliced {
+  DBuf data, scale;
+  int64_t lines = 0, K = 0, KB = 0, tiles = 0;
+  const int8_t* digits() const { return reinterpret_cast<const int8_t*>(data.p); }
+};
+
+void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+              OzSliced& out) {
+  static_assert(oz::BM == oz::BN, "one tile height for both operands");
   require(K <= oz::KMAX, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
+  out.lines = L;
+  out.K = K;
+  out.KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
+  out.tiles = (L + oz::BM - 1) / oz::BM;
+  require(out.tiles * out.KB < (int64_t(1) << 31), "ozaki_gemm: too many tiles");
+  const size_t bytes = size_t(out.tiles) * out.KB * oz::A_STAGE;
+  out.data.alloc(c, (bytes + 7) / 8);
+  out.scale.alloc(c, size_t(std::max<int64_t>(L, 1)));
+  if (L <= 0) return;
+  ProfScope ps(c, "ozaki(slice)", double(L) * double(K) * 8.0 + double(bytes));
+  const bool vec = sk == 1 && sl % 2 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+  // persistent: at most 2 CTAs per SM, so the tiles in flight (2 x 148 x 128 lines x K
+  // doubles) can stay L2-resident between the scale pass and the digit pass
+  const unsigned ctas = unsigned(std::min<int64_t>(out.tiles, 2 * 148));
+  int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
+  if (vec)
+    oz::k_slice_tile<oz::BM, true><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, out.scale.p, d);
+  else
+    oz::k_slice_tile<oz::BM, false><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, out.scale.p, d);
+  post_launch(c);
+}
+
+// C (a.lines x b.lines) = A op(B) from sliced operands; output column n is written at
+// C + (n / nb) bs + (n % nb) ldc (nb = 0: N, a plain GEMM), so the batched slab GEMMs of
+// the evaluators (one A, contiguous B slabs) are one launch.
+void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, double* C, int64_t ldc,
+            const char* tag, int64_t nb = 0, int64_t bs = 0) {
+  const int64_t M = a.lines, N = b.lines;
+  if (M <= 0 || N <= 0) return;
+  require(a.K == b.K, "ozaki_gemm: inner dimensions differ");
   if (!c->oz_smem_set) {
     CK(cudaFuncSetAttribute(oz::k_gemm_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(oz::SMEM_BYTES)));
     c->oz_smem_set = true;
   }
-  const int64_t KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
-  const int64_t tm = (M + oz::BM - 1) / oz::BM, tn = (N + oz::BN - 1) / oz::BN;
-  require(tm * tn < (int64_t(1) << 31) && tm * KB < (int64_t(1) << 31) && tn * KB < (int64_t(1) << 31),
-          "ozaki_gemm: too many tiles");
-  const size_t a_bytes = size_t(tm) * KB * oz::A_STAGE, b_bytes = size_t(tn) * KB * oz::B_STAGE;
-  DBuf sa(c, (a_bytes + 7) / 8), sb(c, (b_bytes + 7) / 8);
-  DBuf ra(c, size_t(M)), cb(c, size_t(N));
-  int8_t* pa = reinterpret_cast<int8_t*>(sa.p);
-  int8_t* pb = reinterpret_cast<int8_t*>(sb.p);
-  // lines: rows of A (element (i, k) at A[i + k lda]); columns of op(B)
-  const int64_t bsl = tb ? 1 : ldb, bsk = tb ? ldb : 1;
-  {
-    ProfScope ps(c, "ozaki(slice)", double(M * K + K * N) * 8.0 + double(a_bytes + b_bytes));
-    auto vec = [](const double* P, int64_t sl, int64_t sk) {
-      return sk == 1 && sl % 2 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
-    };
-    if (vec(A, 1, lda))
-      oz::k_slice_tile<oz::BM, true><<<unsigned(tm), 2 * oz::BM, 0, c->stream>>>(A, 1, lda, M, K, KB, ra.p, pa);
-    else
-      oz::k_slice_tile<oz::BM, false><<<unsigned(tm), 2 * oz::BM, 0, c->stream>>>(A, 1, lda, M, K, KB, ra.p, pa);
-    post_launch(c);
-    if (vec(B, bsl, bsk))
-      oz::k_slice_tile<oz::BN, true><<<unsigned(tn), 2 * oz::BN, 0, c->stream>>>(B, bsl, bsk, N, K, KB, cb.p, pb);
-    else
-      oz::k_slice_tile<oz::BN, false><<<unsigned(tn), 2 * oz::BN, 0, c->stream>>>(B, bsl, bsk, N, K, KB, cb.p, pb);
-    post_launch(c);
-  }
-  ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(K));
-  const int64_t tiles = tm * tn;
+  const int64_t tiles = a.tiles * b.tiles;
+  require(tiles < (int64_t(1) << 31), "ozaki_gemm: too many tiles");
+  ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(a.K));
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
-      pa, ra.p, pb, cb.p, M, N, KB, C, ldc, nb > 0 ? nb : N, bs, tm, tiles);
+      a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, C, ldc, nb > 0 ? nb : N, bs,
+      a.tiles, tiles);
   post_launch(c);
 #ifdef LATSUM_OZ_TRACE
   {
@@ -460,6 +471,18 @@ void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A,
     CK(cudaMemcpyToSymbol(oz::g_oz_trace, z, sizeof(z)));
   }
 #endif
+}
+
+// C (M x N, ldc) = A (M x K, lda) op(B), op(B) = B (K x N, ldb) or B^T (B: N x K, ldb),
+// all column-major, on the int8 tensor cores.
+void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)",
+                int64_t nb = 0, int64_t bs = 0, bool tb = false) {
+  if (M <= 0 || N <= 0) return;
+  OzSliced a, b;
+  oz_slice(c, A, 1, lda, M, K, a);
+  oz_slice(c, B, tb ? 1 : ldb, tb ? ldb : 1, N, K, b);
+  oz_run(c, a, b, C, ldc, tag, nb, bs);
 }
 
 // Evaluation slab GEMMs: int8 tensor cores (Ozaki, default) or FP64 DMMA
@@ -1774,6 +1797,9 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   DBuf Q(c, size_t(r0) * njc * r2);
   const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(r0 * njc, 1), 65535), 1);
   DBuf X(c, size_t(r0) * njc * nkc);
+  const bool oz_x = eval_uses_ozaki(r2), oz_v = eval_uses_ozaki(r0);
+  OzSliced sU0, sQ;  // sliced once and reused across the chunks that share them
+  if (oz_v) oz_slice(c, U0, 1, t.N[0], ni, r0, sU0);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
     GemmOpts oq = tagged("gemm_eval_q");
@@ -1781,17 +1807,22 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
     oq.sA = r0 * r1;
     oq.sC = r0 * njj;
     gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
+    if (oz_x) oz_slice(c, Q.p, 1, r0 * njj, r0 * njj, r2, sQ);
     for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
       const int64_t nkk = std::min(nkc, nk - k0);
-      if (eval_uses_ozaki(r2))
-        ozaki_gemm(c, r0 * njj, nkk, r2, Q.p, r0 * njj, U2 + k0, t.N[2], X.p, r0 * njj,
-                   "gemm_eval_x(ozaki-i8)", 0, 0, /*tb=*/true);
-      else
+      if (oz_x) {  // X = Q x_3 U2: B = U2[k0:k0+nkk, :]^T, lines = its rows
+        OzSliced sU2;
+        oz_slice(c, U2 + k0, 1, t.N[2], nkk, r2, sU2);
+        oz_run(c, sQ, sU2, X.p, r0 * njj, "gemm_eval_x(ozaki-i8)");
+      } else {
         gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
              r0 * njj, tagged("gemm_eval_x"));
-      if (eval_uses_ozaki(r0)) {
-        ozaki_gemm(c, ni, njj * nkk, r0, U0, t.N[0], X.p, r0, out + k0 * ni * nj + j0 * ni, ni,
-                   "gemm_eval_slab(ozaki-i8)", njj, ni * nj);
+      }
+      if (oz_v) {  // V_k = U0 X_k for the nkk slabs: B lines = the columns (j, k) of X
+        OzSliced sX;
+        oz_slice(c, X.p, r0, 1, njj * nkk, r0, sX);
+        oz_run(c, sU0, sX, out + k0 * ni * nj + j0 * ni, ni, "gemm_eval_slab(ozaki-i8)", njj,
+               ni * nj);
         continue;
       }
       GemmOpts ov = tagged("gemm_eval_slab");

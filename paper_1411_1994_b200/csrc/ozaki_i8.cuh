@@ -91,47 +91,61 @@ template <int ROWS, bool VEC>
 __global__ void __launch_bounds__(2 * ROWS)
 k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
              int64_t KB, double* __restrict__ scale, int8_t* __restrict__ out) {
+  // persistent over tiles: one resident tile per CTA keeps the pass-2 re-read in L2
   __shared__ double part[ROWS];
-  const int64_t tile = blockIdx.x;
   const int r = threadIdx.x % ROWS, h = threadIdx.x / ROWS;  // line in tile, k half
-  const int64_t l = tile * ROWS + r;
-  const double* p = P + (l < L ? l : 0) * sl;
-  double amax = 0.0;
-  if (l < L) {
-    for (int64_t kb = 0; kb < KB; ++kb) {
-      double x[16];
-      load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
-    }
-  }
-  if (h == 1) part[r] = amax;
-  __syncthreads();
-  if (h == 0) part[r] = fmax(amax, part[r]);
-  __syncthreads();
-  const double sc = ldexp(1.0, line_exponent(part[r]));
-  if (h == 0 && l < L) scale[l] = sc;
-  const double inv = 1.0 / sc;  // exact: a power of two
-  for (int64_t kb = 0; kb < KB; ++kb) {
-    uint32_t w[S][4];
-#pragma unroll
-    for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
+  const int64_t tiles = (L + ROWS - 1) / ROWS;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t l = tile * ROWS + r;
+    const double* p = P + (l < L ? l : 0) * sl;
+    double amax = 0.0;
     if (l < L) {
-      double x[16];
-      load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
+      for (int64_t kb = 0; kb < KB; ++kb) {
+        double x[16];
+        load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        int8_t d[S];
-        digits(x[kk] * inv, d);
-#pragma unroll
-        for (int s = 0; s < S; ++s) w[s][kk / 4] |= uint32_t(uint8_t(d[s])) << (8 * (kk % 4));
+        for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
       }
     }
-    int8_t* base = out + ((tile * KB + kb) * S) * int64_t(ROWS * BKB) + blk_off(r, 16 * h);
+    if (h == 1) part[r] = amax;
+    __syncthreads();
+    if (h == 0) part[r] = fmax(amax, part[r]);
+    __syncthreads();
+    const double sc = ldexp(1.0, line_exponent(part[r]));
+    __syncthreads();  // part[] is rewritten by the next tile
+    if (h == 0 && l < L) scale[l] = sc;
+    const double inv54 = 0x1p54 / sc;  // exact: a power of two
+    for (int64_t kb = 0; kb < KB; ++kb) {
+      uint32_t w[S][4];
 #pragma unroll
-    for (int s = 0; s < S; ++s)
-      *reinterpret_cast<uint4*>(base + s * (ROWS * BKB)) =
-          make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+      for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
+      if (l < L) {
+        double x[16];
+        load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          // balanced base-256 digits of X = rint(2^54 x): with Y = X + sum_i 128 256^i the
+          // low digits are the bytes of Y minus 128 (byte ^ 0x80) and the top one Y >> 48
+          const long long X = __double2ll_rn(x[kk] * inv54);
+          const unsigned long long Y = static_cast<unsigned long long>(X + 0x808080808080LL);
+          const uint32_t lo = uint32_t(Y) ^ 0x80808080u;        // d6 d5 d4 d3 (bytes 0..3)
+          const uint32_t hi = uint32_t(Y >> 32) ^ 0x00008080u;  // d2 d1 d0 (bytes 0..2)
+          const int p = kk % 4;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const uint32_t src = s <= 2 ? hi : lo;
+            const int m = s <= 2 ? 2 - s : 6 - s;  // byte of src holding digit s
+            const uint32_t sel = (0x3210u & ~(0xFu << (4 * p))) | (uint32_t(4 + m) << (4 * p));
+            w[s][kk / 4] = __byte_perm(w[s][kk / 4], src, sel);
+          }
+        }
+      }
+      int8_t* base = out + ((tile * KB + kb) * S) * int64_t(ROWS * BKB) + blk_off(r, 16 * h);
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint4*>(base + s * (ROWS * BKB)) =
+            make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    }
   }
 }
 

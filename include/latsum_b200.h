@@ -237,6 +237,13 @@ int latsum_dgemm_device(latsum_ctx* ctx, int ta, int tb, int64_t M, int64_t N, i
                         double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                         double beta, double* C, int64_t ldc);
 
+/* Householder tridiagonalisation of a symmetric n x n device matrix (full storage; LAPACK
+ * dsytrd 'L' output: d, e, tau on the device, reflectors below the subdiagonal of A),
+ * computed by one 16-CTA thread-block cluster.  Building block of the eigensolver that
+ * replaces cuSOLVER syevd for the RHOSVD Grams. */
+int latsum_sytrd_device(latsum_ctx* ctx, int64_t n, double* A, int64_t lda, double* d, double* e,
+                        double* tau);
+
 /* FP64-accurate C = A op(B) (column-major; op(B) = B^T when tb != 0) computed on the int8 tensor cores
  * by the Ozaki splitting (7 int8 slices per operand, tcgen05.mma.kind::i8, int32 TMEM
  * accumulators); K <= 16384.  Used by the Tucker evaluation when LATSUM_EVAL_GEMM=ozaki. */

@@ -115,6 +115,7 @@ SIGNATURES = [
     ("latsum_tensor_read", _I, [_P, ctypes.c_char_p, _P, _P]),
     ("latsum_dgemm_device", _I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P,
                                  _I64]),
+    ("latsum_sytrd_device", _I, [_P, _I64, _P, _I64, _P, _P, _P]),
     ("latsum_dgemm_ozaki_device", _I, [_P, _I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
 ]
 

@@ -27,6 +27,7 @@
 #include "latsum_b200.h"
 #include "latsum_kernels.cuh"
 #include "ozaki_i8.cuh"
+#include "eig_sym.cuh"
 
 using namespace latsum_b200;
 
@@ -517,6 +518,41 @@ void syevd(latsum_ctx* c, int64_t n, double* A, double* W) {
   CK(cudaStreamSynchronize(c->stream));
   cudaFreeAsync(info, c->stream);
   if (hinfo != 0) throw Error(LATSUM_ERR_CUSOLVER, "syevd: info = " + std::to_string(hinfo));
+}
+
+// ------------------------------------------------------------------ custom eigensolver
+// Householder tridiagonalisation of the symmetric n x n matrix A (full storage, lda) in
+// one 16-CTA cluster (eig_sym.cuh): d (n), e (n-1), tau (n-1) on the device; the
+// reflectors overwrite A below the subdiagonal.
+void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, double* e,
+                   double* tau) {
+  if (n <= 0) return;
+  require(n < (int64_t(1) << 30), "sytrd: n too large");
+  require(n <= 8192, "sytrd: n > 8192");
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(eig::k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(eig::k_sytrd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(2 * 8192 * sizeof(double))));
+    attr = true;
+  }
+  DBuf ws(c, size_t(3 * n + 2 * eig::TRD_CTAS + 8));
+  eig::TrdWork w{ws.p, ws.p + n, ws.p + 2 * n, ws.p + 3 * n};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(eig::TRD_CTAS);
+  cfg.blockDim = dim3(eig::TRD_THREADS);
+  cfg.dynamicSmemBytes = size_t(2 * n) * sizeof(double);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = eig::TRD_CTAS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ProfScope ps(c, "eig_sytrd", double(n) * double(n) * double(n) * 4.0 / 3.0);
+  CK(cudaLaunchKernelEx(&cfg, eig::k_sytrd_cluster, A, lda, int(n), d, e, tau, w));
+  post_launch(c);
 }
 
 struct Timer {
@@ -2578,6 +2614,14 @@ int latsum_dgemm_device(latsum_ctx* c, int ta, int tb, int64_t M, int64_t N, int
   return guarded(c, [&] {
     require(A && B && C && M >= 0 && N >= 0 && K >= 0, "latsum_dgemm_device: bad argument");
     gemm(c, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  });
+}
+
+int latsum_sytrd_device(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, double* e,
+                        double* tau) {
+  return guarded(c, [&] {
+    require(A && d && n >= 1 && lda >= n && (n == 1 || (e && tau)), "latsum_sytrd_device: bad argument");
+    sytrd_cluster(c, n, A, lda, d, e, tau);
   });
 }
 

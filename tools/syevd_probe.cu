@@ -138,6 +138,47 @@ int main() {
       }
       cudaFree(wd);
     }
+    // legacy Dsyevd captured into a CUDA graph (launch-latency test)
+    {
+      int lw = 0;
+      CK(cusolverDnDsyevd_bufferSize(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, &lw));
+      double* wd; CK(cudaMalloc(&wd, size_t(lw) * 8 + 8));
+      CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+      CK(cudaDeviceSynchronize());
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      auto c0 = cudaStreamBeginCapture(st[0], cudaStreamCaptureModeRelaxed);
+      auto c1 = cusolverDnDsyevd(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, wd, lw, info);
+      auto c2 = cudaStreamEndCapture(st[0], &g);
+      size_t nodes = 0;
+      if (g) cudaGraphGetNodes(g, nullptr, &nodes);
+      printf("n=%5ld  graph capture of Dsyevd: begin %d solver %d end %d nodes %zu\n", n, int(c0), int(c1), int(c2), nodes);
+      cudaGetLastError();
+      if (c2 == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) {
+        for (int rep = 0; rep < 3; ++rep) {
+          CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+          CK(cudaDeviceSynchronize());
+          cudaEventRecord(e0, st[0]);
+          CK(cudaGraphLaunch(ge, st[0]));
+          cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
+          float ms; cudaEventElapsedTime(&ms, e0, e1);
+          if (rep == 2) printf("n=%5ld  1x Dsyevd graph    : %8.2f ms\n", n, ms);
+        }
+        // 3 graphs on 3 streams concurrently
+        for (int rep = 0; rep < 3; ++rep) {
+          CK(cudaDeviceSynchronize());
+          cudaEventRecord(e0, st[0]);
+          cudaEvent_t f; cudaEventCreate(&f); cudaEventRecord(f, st[0]);
+          for (int i = 1; i < 3; ++i) cudaStreamWaitEvent(st[i], f, 0);
+          for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(ge, st[i]));
+          for (int i = 1; i < 3; ++i) { cudaEvent_t j; cudaEventCreate(&j); cudaEventRecord(j, st[i]); cudaStreamWaitEvent(st[0], j, 0); }
+          cudaEventRecord(e1, st[0]); cudaEventSynchronize(e1);
+          float ms; cudaEventElapsedTime(&ms, e0, e1);
+          if (rep == 2) printf("n=%5ld  3x Dsyevd graph 3 streams (same buffers, timing only): %8.2f ms\n", n, ms);
+        }
+      }
+      cudaFree(wd);
+    }
     // sytrd alone
     {
       int lw = 0;

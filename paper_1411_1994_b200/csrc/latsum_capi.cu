@@ -632,6 +632,7 @@ struct latsum_tucker {
   int64_t T = 0;
   DVec<int32_t> tc[3];
   DVec<double> tw;
+  DVec<int64_t> tseg;  // d0 + 1: the terms are sorted by their mode-0 column
 };
 
 namespace {
@@ -1512,6 +1513,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     t.tc[l].upload(c, can.tc[l]);
   }
   t.tw.upload(c, can.tw);
+  t.tseg.upload(c, can.tseg);
   t.T = can.T;
   tm.project = tp.stop();
   Trace::mark(c, "projections done");
@@ -1874,9 +1876,46 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
 // Canonical (dictionary) tensor on an ni x nj x nk box: V_k = A0 X_k with
 // A0[:, t] = D0[:, c0_t] and X_k[t, j] = w_t D2[k, c2_t] D1[j, c1_t] (to_dense,
 // canonical.hpp:192-202, as one GEMM per z-slab).  D_l point at the box's first row.
+// Grouped form for T merged terms over d0 < T distinct mode-0 columns (terms sorted by
+// c0, segments seg0): per z-chunk Y_a = sum_{t in seg a} w_t D1[:, c1_t] D2[k, c2_t]^T
+// (one segmented GEMM, 2 T nj nk flops over the box) and V = D0 Y^T (2 d0 ni nj nk flops
+// instead of 2 T ni nj nk; BASELINE cfg5: d0 = 8283 vs T = 65065).
+void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3],
+                     const int32_t* const tc[3], const double* tw, int64_t T, const int64_t* seg0,
+                     int64_t d0, int64_t ni, int64_t nj, int64_t nk, double* out, const char* tag) {
+  DBuf G1(c, size_t(nj) * T);  // G1[:, t] = w_t D1[:, c1_t]
+  k_gather_scale<<<grid_for(nj * T), 256, 0, c->stream>>>(D[1], nj, ld[1], tc[1], tw, T, G1.p);
+  post_launch(c);
+  const int64_t budget = int64_t(1) << 29;
+  const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(nj * d0, 1), 65535), 1);
+  DBuf G2(c, size_t(nkc) * T), Y(c, size_t(nj) * nkc * d0);
+  const bool oz = eval_uses_ozaki(d0);
+  OzSliced sD0;
+  if (oz) oz_slice(c, D[0], 1, ld[0], ni, d0, sD0);
+  for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
+    const int64_t nkk = std::min(nkc, nk - k0);
+    k_gather_scale<<<grid_for(nkk * T), 256, 0, c->stream>>>(D[2] + k0, nkk, ld[2], tc[2], nullptr,
+                                                              T, G2.p);
+    post_launch(c);
+    GemmOpts o = tagged("gemm_eval_group");
+    o.batch = d0;
+    o.sC = nj * nkk;
+    o.kseg = seg0;
+    gemm(c, false, true, nj, nkk, T, 1.0, G1.p, nj, G2.p, nkk, 0.0, Y.p, nj, o);
+    if (oz) {
+      OzSliced sY;  // lines = the (j, k) columns of V, K = d0
+      oz_slice(c, Y.p, 1, nj * nkk, nj * nkk, d0, sY);
+      oz_run(c, sD0, sY, out + k0 * ni * nj, ni, tag);
+    } else {
+      gemm(c, false, true, ni, nj * nkk, d0, 1.0, D[0], ld[0], Y.p, nj * nkk, 0.0,
+           out + k0 * ni * nj, ni, tagged(tag));
+    }
+  }
+}
+
 void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const int32_t* const tc[3],
              const double* tw, int64_t T, int64_t ni, int64_t nj, int64_t nk, double* out,
-             const char* tag) {
+             const char* tag, const int64_t* seg0 = nullptr, int64_t d0 = 0) {
   if (T == 0) {
     CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
     return;
@@ -1903,6 +1942,8 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
     post_launch(c);
     return;
   }
+  if (seg0 && d0 > 0 && 2 * d0 <= T)
+    return cp_eval_grouped(c, D, ld, tc, tw, T, seg0, d0, ni, nj, nk, out, tag);
   DBuf A0(c, size_t(ni) * T);
   k_gather_scale<<<grid_for(ni * T), 256, 0, c->stream>>>(D[0], ni, ld[0], tc[0], nullptr, T, A0.p);
   post_launch(c);
@@ -1932,7 +1973,7 @@ void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo
   const double* D[3] = {can.dict[0].p + lo[0], can.dict[1].p + lo[1], can.dict[2].p + lo[2]};
   const int32_t* tc[3] = {can.dtc[0].p, can.dtc[1].p, can.dtc[2].p};
   cp_eval(c, D, can.N, tc, can.dtw.p, can.T, hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], out,
-          "gemm_eval_canonical");
+          "gemm_eval_canonical", can.dtseg.p, can.d[0]);
 }
 
 // Projected-CP evaluation of a RHOSVD result: E_l = U_l[box rows] P_l, then the
@@ -1952,7 +1993,7 @@ void projected_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], 
     D[l] = E[l].p;
   }
   const int32_t* tc[3] = {t.tc[0].p, t.tc[1].p, t.tc[2].p};
-  cp_eval(c, D, n, tc, t.tw.p, t.T, n[0], n[1], n[2], out, "gemm_eval_projected");
+  cp_eval(c, D, n, tc, t.tw.p, t.T, n[0], n[1], n[2], out, "gemm_eval_projected", t.tseg.p, t.d[0]);
 }
 
 void projected_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,

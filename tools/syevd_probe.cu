@@ -138,6 +138,46 @@ int main() {
       }
       cudaFree(wd);
     }
+    // legacy Dsyevd (no host workspace) from 3 threads / streams
+    {
+      int lw = 0;
+      CK(cusolverDnDsyevd_bufferSize(hs[0], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, &lw));
+      double* wd3[3];
+      for (int i = 0; i < 3; ++i) CK(cudaMalloc(&wd3[i], size_t(lw) * 8 + 8));
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int i = 0; i < 3; ++i) th.emplace_back([&, i] {
+          cusolverDnDsyevd(hs[i], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A + i * n * n, n, W + i * n, wd3[i], lw, info + i);
+          cudaStreamSynchronize(st[i]);
+        });
+        for (auto& t : th) t.join();
+        double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (rep == 2) printf("n=%5ld  3x Dsyevd legacy 3 streams: %8.2f ms\n", n, ms);
+      }
+      // sytrd alone from 3 threads
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaMemcpy(A, A0, 3 * n * n * 8, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        int lt = 0;
+        double *dd, *ee, *tt;
+        CK(cudaMalloc(&dd, 3 * n * 8)); CK(cudaMalloc(&ee, 3 * n * 8)); CK(cudaMalloc(&tt, 3 * n * 8));
+        CK(cusolverDnDsytrd_bufferSize(hs[0], CUBLAS_FILL_MODE_LOWER, n, A, n, dd, ee, tt, &lt));
+        auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int i = 0; i < 3; ++i) th.emplace_back([&, i] {
+          cusolverDnDsytrd(hs[i], CUBLAS_FILL_MODE_LOWER, n, A + i * n * n, n, dd + i * n, ee + i * n, tt + i * n, wd3[i], lt < lw ? lt : lw, info + i);
+          cudaStreamSynchronize(st[i]);
+        });
+        for (auto& t : th) t.join();
+        double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (rep == 2) printf("n=%5ld  3x Dsytrd 3 streams       : %8.2f ms\n", n, ms);
+        cudaFree(dd); cudaFree(ee); cudaFree(tt);
+      }
+      for (int i = 0; i < 3; ++i) cudaFree(wd3[i]);
+    }
     // legacy Dsyevd captured into a CUDA graph (launch-latency test)
     {
       int lw = 0;

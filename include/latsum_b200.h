@@ -246,7 +246,8 @@ int latsum_sytrd_device(latsum_ctx* ctx, int64_t n, double* A, int64_t lda, doub
 
 /* FP64-accurate C = A op(B) (column-major; op(B) = B^T when tb != 0) computed on the int8 tensor cores
  * by the Ozaki splitting (7 int8 slices per operand, tcgen05.mma.kind::i8, int32 TMEM
- * accumulators); K <= 16384.  Used by the Tucker evaluation when LATSUM_EVAL_GEMM=ozaki. */
+ * accumulators); K > 16384 runs as K-chunks accumulated into C in FP64.  The engine of the stage-4 evaluation GEMMs and the
+ * stage-3 core contraction (LATSUM_EVAL_GEMM=dmma / LATSUM_CORE_GEMM=dmma revert to DMMA). */
 int latsum_dgemm_ozaki_device(latsum_ctx* ctx, int tb, int64_t M, int64_t N, int64_t K,
                               const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                               int64_t ldc);

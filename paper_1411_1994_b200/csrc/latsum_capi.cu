@@ -413,9 +413,10 @@ struct OzSliced {
 };
 
 void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
-              OzSliced& out) {
+              OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {
   static_assert(oz::BM == oz::BN, "one tile height for both operands");
   require(K <= oz::KMAX, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
+  if (L1 <= 0) L1 = std::max<int64_t>(L, 1);
   out.lines = L;
   out.K = K;
   out.KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
@@ -426,23 +427,28 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
   out.scale.alloc(c, size_t(std::max<int64_t>(L, 1)));
   if (L <= 0) return;
   ProfScope ps(c, "ozaki(slice)", double(L) * double(K) * 8.0 + double(bytes));
-  const bool vec = sk == 1 && sl % 2 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+  const bool vec = sk == 1 && sl % 2 == 0 && (L1 >= L || sl2 % 2 == 0) &&
+                   reinterpret_cast<uintptr_t>(P) % 16 == 0;
   // persistent: at most 2 CTAs per SM, so the tiles in flight (2 x 148 x 128 lines x K
   // doubles) can stay L2-resident between the scale pass and the digit pass
   const unsigned ctas = unsigned(std::min<int64_t>(out.tiles, 2 * 148));
   int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
   if (vec)
-    oz::k_slice_tile<oz::BM, true><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, out.scale.p, d);
+    oz::k_slice_tile<oz::BM, true><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB,
+                                                                        out.scale.p, d, L1, sl2);
   else
-    oz::k_slice_tile<oz::BM, false><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, out.scale.p, d);
+    oz::k_slice_tile<oz::BM, false><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB,
+                                                                         out.scale.p, d, L1, sl2);
   post_launch(c);
 }
 
-// C (a.lines x b.lines) = A op(B) from sliced operands; output column n is written at
-// C + (n / nb) bs + (n % nb) ldc (nb = 0: N, a plain GEMM), so the batched slab GEMMs of
-// the evaluators (one A, contiguous B slabs) are one launch.
-void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, double* C, int64_t ldc,
-            const char* tag, int64_t nb = 0, int64_t bs = 0) {
+// Output addressing of an Ozaki GEMM (ozaki_i8.cuh OzOut): plain column-major by default.
+oz::OzOut oz_out(double* C, int64_t ldc, double beta = 0.0) {
+  return oz::OzOut{C, ldc, int64_t(1) << 62, 0, int64_t(1) << 62, 0, beta};
+}
+
+// C = A op(B) + beta C from sliced operands (a.lines x b.lines output, addressing o).
+void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, const char* tag) {
   const int64_t M = a.lines, N = b.lines;
   if (M <= 0 || N <= 0) return;
   require(a.K == b.K, "ozaki_gemm: inner dimensions differ");
@@ -458,8 +464,7 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, double* C, int6
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
-      a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, C, ldc, nb > 0 ? nb : N, bs,
-      a.tiles, tiles);
+      a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, o, a.tiles, tiles);
   post_launch(c);
 #ifdef LATSUM_OZ_TRACE
   {
@@ -474,16 +479,32 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, double* C, int6
 #endif
 }
 
-// C (M x N, ldc) = A (M x K, lda) op(B), op(B) = B (K x N, ldb) or B^T (B: N x K, ldb),
-// all column-major, on the int8 tensor cores.
+// General form: A lines (rows) l -> A + (l % a_L1) + (l / a_L1) a_sl2, element k at + k a_sk;
+// B lines (columns of op(B)) n -> B + n b_sl, element k at + k b_sk; output addressing o
+// (beta accumulates).  K is split into <= KMAX chunks accumulated with beta = 1.
+void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t a_sk,
+                   int64_t a_L1, int64_t a_sl2, const double* B, int64_t b_sl, int64_t b_sk,
+                   oz::OzOut o, const char* tag) {
+  if (M <= 0 || N <= 0) return;
+  const int64_t parts = std::max<int64_t>(1, (K + oz::KMAX - 1) / oz::KMAX);
+  const int64_t kc = std::max<int64_t>(1, (K + parts - 1) / parts);
+  const double beta0 = o.beta;
+  for (int64_t k0 = 0; k0 < std::max<int64_t>(K, 1); k0 += kc) {
+    const int64_t kk = std::min(kc, std::max<int64_t>(K - k0, 0));
+    OzSliced a, b;
+    oz_slice(c, A + k0 * a_sk, 1, a_sk, M, kk, a, a_L1, a_sl2);
+    oz_slice(c, B + k0 * b_sk, b_sl, b_sk, N, kk, b);
+    o.beta = k0 == 0 ? beta0 : 1.0;
+    oz_run(c, a, b, o, tag);
+  }
+}
+
+// C (M x N, ldc) = A (M x K, lda) op(B) + beta C, op(B) = B (K x N, ldb) or B^T (B: N x K,
+// ldb), all column-major, on the int8 tensor cores.
 void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)",
-                int64_t nb = 0, int64_t bs = 0, bool tb = false) {
-  if (M <= 0 || N <= 0) return;
-  OzSliced a, b;
-  oz_slice(c, A, 1, lda, M, K, a);
-  oz_slice(c, B, tb ? 1 : ldb, tb ? ldb : 1, N, K, b);
-  oz_run(c, a, b, C, ldc, tag, nb, bs);
+                bool tb = false, double beta = 0.0) {
+  ozaki_gemm_ex(c, M, N, K, A, lda, 0, 0, B, tb ? 1 : ldb, tb ? ldb : 1, oz_out(C, ldc, beta), tag);
 }
 
 // Evaluation slab GEMMs: int8 tensor cores (Ozaki, default) or FP64 DMMA
@@ -494,6 +515,15 @@ bool eval_uses_ozaki(int64_t K) {
     return e && std::string(e) == "dmma";
   }();
   return !dmma && K <= oz::KMAX;
+}
+// The Tucker core contraction (stage 3) on the int8 tensor cores too (LATSUM_CORE_GEMM=dmma
+// reverts); large products only (the slicing passes cost ~2 operand reads).
+bool core_uses_ozaki(int64_t M, int64_t N, int64_t K) {
+  static const bool dmma = [] {
+    const char* e = std::getenv("LATSUM_CORE_GEMM");
+    return e && std::string(e) == "dmma";
+  }();
+  return !dmma && double(M) * double(N) * double(K) >= 1e10;
 }
 
 // ------------------------------------------------------------------ syevd
@@ -1334,7 +1364,20 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
     const int64_t na = std::min(ac, dm - a0);
     gt.form(c, r, T, a0, na, X.p);
     const double beta = a0 == a_lo ? 0.0 : 1.0;
-    if (m == 0) {        // core (r0 x r1 r2) = P0[:, j] X^T
+    const bool oz = core_uses_ozaki(ro, std::max(r[0], r[2]), na);
+    if (m == 0 && oz) {
+      ozaki_gemm(c, r[0], ro, na, P[0].p + a0 * r[0], r[0], X.p, ro, core, r[0],
+                 "gemm_core(ozaki-i8)", true, beta);
+    } else if (m == 2 && oz) {
+      ozaki_gemm(c, ro, r[2], na, X.p, ro, P[2].p + a0 * r[2], r[2], core, ro,
+                 "gemm_core(ozaki-i8)", true, beta);
+    } else if (m == 1 && oz) {  // rows (a, k) of X -> core[a + r0 b + r0 r1 k]
+      oz::OzOut o = oz_out(core, r[0], beta);
+      o.mr = r[0];
+      o.rs = r[0] * r[1];
+      ozaki_gemm_ex(c, ro, r[1], na, X.p, ro, 0, 0, P[1].p + a0 * r[1], 1, r[1], o,
+                    "gemm_core(ozaki-i8)");
+    } else if (m == 0) {        // core (r0 x r1 r2) = P0[:, j] X^T
       gemm(c, false, true, r[0], ro, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, ro, beta, core, r[0],
            tagged("gemm_core"));
     } else if (m == 2) { // core (r0 r1 x r2) = X P2[:, j]^T
@@ -1840,18 +1883,26 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   if (oz_v) oz_slice(c, U0, 1, t.N[0], ni, r0, sU0);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
-    GemmOpts oq = tagged("gemm_eval_q");
-    oq.batch = r2;
-    oq.sA = r0 * r1;
-    oq.sC = r0 * njj;
-    gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
+    if (oz_x) {  // Q[a, j, c] = sum_b core[a, b, c] U1[j, b]: A lines (a, c), one launch
+      oz::OzOut o = oz_out(Q.p, r0);
+      o.mr = r0;
+      o.rs = r0 * njj;
+      ozaki_gemm_ex(c, r0 * r2, njj, r1, t.core.p, r0, r0, r0 * r1, U1 + j0, 1, t.N[1], o,
+                    "gemm_eval_q(ozaki-i8)");
+    } else {
+      GemmOpts oq = tagged("gemm_eval_q");
+      oq.batch = r2;
+      oq.sA = r0 * r1;
+      oq.sC = r0 * njj;
+      gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
+    }
     if (oz_x) oz_slice(c, Q.p, 1, r0 * njj, r0 * njj, r2, sQ);
     for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
       const int64_t nkk = std::min(nkc, nk - k0);
       if (oz_x) {  // X = Q x_3 U2: B = U2[k0:k0+nkk, :]^T, lines = its rows
         OzSliced sU2;
         oz_slice(c, U2 + k0, 1, t.N[2], nkk, r2, sU2);
-        oz_run(c, sQ, sU2, X.p, r0 * njj, "gemm_eval_x(ozaki-i8)");
+        oz_run(c, sQ, sU2, oz_out(X.p, r0 * njj), "gemm_eval_x(ozaki-i8)");
       } else {
         gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
              r0 * njj, tagged("gemm_eval_x"));
@@ -1859,8 +1910,10 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
       if (oz_v) {  // V_k = U0 X_k for the nkk slabs: B lines = the columns (j, k) of X
         OzSliced sX;
         oz_slice(c, X.p, r0, 1, njj * nkk, r0, sX);
-        oz_run(c, sU0, sX, out + k0 * ni * nj + j0 * ni, ni, "gemm_eval_slab(ozaki-i8)", njj,
-               ni * nj);
+        oz::OzOut o = oz_out(out + k0 * ni * nj + j0 * ni, ni);
+        o.nb = njj;
+        o.bs = ni * nj;
+        oz_run(c, sU0, sX, o, "gemm_eval_slab(ozaki-i8)");
         continue;
       }
       GemmOpts ov = tagged("gemm_eval_slab");
@@ -1905,7 +1958,7 @@ void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3
     if (oz) {
       OzSliced sY;  // lines = the (j, k) columns of V, K = d0
       oz_slice(c, Y.p, 1, nj * nkk, nj * nkk, d0, sY);
-      oz_run(c, sD0, sY, out + k0 * ni * nj, ni, tag);
+      oz_run(c, sD0, sY, oz_out(out + k0 * ni * nj, ni), tag);
     } else {
       gemm(c, false, true, ni, nj * nkk, d0, 1.0, D[0], ld[0], Y.p, nj * nkk, 0.0,
            out + k0 * ni * nj, ni, tagged(tag));
@@ -2673,7 +2726,7 @@ int latsum_dgemm_ozaki_device(latsum_ctx* c, int tb, int64_t M, int64_t N, int64
     require(A && B && C && M >= 0 && N >= 0 && K >= 0 && lda >= std::max<int64_t>(M, 1) &&
                 ldb >= std::max<int64_t>(tb ? N : K, 1) && ldc >= std::max<int64_t>(M, 1),
             "latsum_dgemm_ozaki_device: bad argument");
-    ozaki_gemm(c, M, N, K, A, lda, B, ldb, C, ldc, "gemm(ozaki-i8)", 0, 0, tb != 0);
+    ozaki_gemm(c, M, N, K, A, lda, B, ldb, C, ldc, "gemm(ozaki-i8)", tb != 0);
   });
 }
 

@@ -66,7 +66,8 @@ __device__ __forceinline__ void digits(double x, int8_t* d) {
 }
 
 // Operands are "lines" (rows of A, columns of B) of K elements: element (l, k) of the
-// FP64 source is P[l * sl + k * sk].  One CTA slices a tile of ROWS lines over all
+// FP64 source is P[(l % L1) sl + (l / L1) sl2 + k sk] (L1 = L: a plain matrix; otherwise a
+// batch of L/L1 matrices stacked as one operand).  One CTA slices a tile of ROWS lines over all
 // k-blocks: pass 1 finds each line's scale 2^e (max |x| 2^-e < 1; 1 for a zero line),
 // pass 2 re-reads the tile (L1/L2-resident) and writes its S digit blocks per k-block in
 // the canonical K-major layout, 16 k-bytes of one line per thread as 16-byte stores.
@@ -90,14 +91,16 @@ __device__ __forceinline__ void load16(const double* __restrict__ p, int64_t sk,
 template <int ROWS, bool VEC>
 __global__ void __launch_bounds__(2 * ROWS)
 k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
-             int64_t KB, double* __restrict__ scale, int8_t* __restrict__ out) {
+             int64_t KB, double* __restrict__ scale, int8_t* __restrict__ out, int64_t L1,
+             int64_t sl2) {
   // persistent over tiles: one resident tile per CTA keeps the pass-2 re-read in L2
   __shared__ double part[ROWS];
   const int r = threadIdx.x % ROWS, h = threadIdx.x / ROWS;  // line in tile, k half
   const int64_t tiles = (L + ROWS - 1) / ROWS;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t l = tile * ROWS + r;
-    const double* p = P + (l < L ? l : 0) * sl;
+    const int64_t ll = l < L ? l : 0;  // line ll = (ll % L1, ll / L1)
+    const double* p = P + (ll % L1) * sl + (ll / L1) * sl2;
     double amax = 0.0;
     if (l < L) {
       for (int64_t kb = 0; kb < KB; ++kb) {
@@ -231,6 +234,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 //                  for pass 2, then folds lo = sum_{g>=4} D_g 2^{8(6-g)} likewise and
 //                  writes (hi 2^-36 + lo 2^-60) 2^e_i 2^f_n (one rounding) while the next
 //                  tile's MMAs run.
+// Output addressing: tile row i (0 <= i < M) and column n land at
+//   C + (i % mr) + (i / mr) rs + (n / nb) bs + (n % nb) ldc,
+// i.e. a plain column-major C (mr = M, nb = N) or batches of row / column blocks (the
+// evaluators' slabs, the batched Q = core x2 U1); C = A op(B) + beta C.
+struct OzOut {
+  double* C;
+  int64_t ldc, nb, bs, mr, rs;
+  double beta;
+};
+
 constexpr int EPI_WARPS = 8;
 constexpr int PTHREADS = 32 * (2 + EPI_WARPS);
 constexpr int EPI_COLS = BN / 2;  // columns per epilogue thread
@@ -259,8 +272,7 @@ __device__ __forceinline__ void drain4(uint32_t taddr, double* x) {
 __global__ void __launch_bounds__(PTHREADS, 1)
 k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
           const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N,
-          int64_t KB, double* __restrict__ C, int64_t ldc, int64_t nb, int64_t bs,
-          int64_t tiles_m, int64_t tiles) {
+          int64_t KB, OzOut o, int64_t tiles_m, int64_t tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
@@ -398,13 +410,28 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty))
                      : "memory");
       if (i < M) {
-        int64_t kk = n0 / nb, jj = n0 - kk * nb;
+        int64_t kk = n0 / o.nb, jj = n0 - kk * o.nb;
+        double* ci = o.C + (i % o.mr) + (i / o.mr) * o.rs;
+        if (o.beta == 0.0) {
 #pragma unroll
-        for (int j = 0; j < EPI_COLS; ++j) {
-          if (n0 + j < N) C[i + kk * bs + jj * ldc] = hv[j];
-          if (++jj == nb) {
-            jj = 0;
-            ++kk;
+          for (int j = 0; j < EPI_COLS; ++j) {
+            if (n0 + j < N) ci[kk * o.bs + jj * o.ldc] = hv[j];
+            if (++jj == o.nb) {
+              jj = 0;
+              ++kk;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPI_COLS; ++j) {
+            if (n0 + j < N) {
+              double* cp = ci + kk * o.bs + jj * o.ldc;
+              *cp = hv[j] + o.beta * *cp;
+            }
+            if (++jj == o.nb) {
+              jj = 0;
+              ++kk;
+            }
           }
         }
       }

@@ -307,15 +307,27 @@ def test_dgemm_ozaki_int8_matches_fp64(ctx, shape, tb):
     assert np.all(np.abs(got - ref) <= 2 * bound)
 
 
-def test_dgemm_ozaki_rejects_oversized_k(ctx):
+def test_dgemm_ozaki_long_k_is_split_and_accumulated(ctx):
+    """K > 16384 (int32 accumulator headroom) runs as K-chunks accumulated into C in FP64
+    (the beta path of the epilogue); checked against a long-double product."""
+    import numpy as np
     import torch
     from paper_1411_1994_b200 import _lib
-    K = 16385
-    a = torch.zeros(K, dtype=torch.float64, device="cuda")
-    c = torch.zeros(1, dtype=torch.float64, device="cuda")
-    st = _lib.lib().latsum_dgemm_ozaki_device(ctx.handle, 0, 1, 1, K, a.data_ptr(), 1,
-                                              a.data_ptr(), K, c.data_ptr(), 1)
-    assert st == 1  # LATSUM_ERR_INVALID_ARGUMENT
+    M, N, K = 70, 130, 40000
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    C0 = np.full((M, N), np.nan)
+    dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F")).cuda()
+    dB = torch.from_numpy(np.asfortranarray(B).ravel(order="F")).cuda()
+    dC = torch.from_numpy(np.asfortranarray(C0).ravel(order="F").copy()).cuda()
+    ctx.check(_lib.lib().latsum_dgemm_ozaki_device(ctx.handle, 0, M, N, K, dA.data_ptr(), M,
+                                                   dB.data_ptr(), K, dC.data_ptr(), M))
+    ctx.synchronize()
+    got = dC.cpu().numpy().reshape((M, N), order="F")
+    want = A.astype(np.longdouble) @ B.astype(np.longdouble)
+    bound = (K * 2.0 ** -51) * np.abs(A).max(axis=1, keepdims=True) * np.abs(B).max(axis=0, keepdims=True)
+    assert np.all(np.abs(got - want).astype(np.float64) <= bound + 2.0 ** -50 * np.abs(want).astype(np.float64))
 
 
 # ----------------------------------------------------------------------------- full configs

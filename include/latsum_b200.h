@@ -244,6 +244,14 @@ int latsum_dgemm_device(latsum_ctx* ctx, int ta, int tb, int64_t M, int64_t N, i
 int latsum_sytrd_device(latsum_ctx* ctx, int64_t n, double* A, int64_t lda, double* d, double* e,
                         double* tau);
 
+/* Symmetric eigensolver of the Gram passes (device pointers): all eigenvalues ascending
+ * into w (n) and the k leading eigenvectors (descending eigenvalue order, unit norm) into V
+ * (n x k).  cuSOLVER syevd by default; LATSUM_EIG=custom (n <= 1536) runs the in-house
+ * solver (cluster sytrd, Sturm multisection, inverse iteration, compact-WY
+ * back-transformation; syevd fallback when the vectors are not orthonormal). */
+int latsum_eig_sym_device(latsum_ctx* ctx, int64_t n, const double* A, int64_t k, double* w,
+                          double* V, int method /* 0 default, 1 cuSOLVER, 2 in-house */);
+
 /* FP64-accurate C = A op(B) (column-major; op(B) = B^T when tb != 0) computed on the int8 tensor cores
  * by the Ozaki splitting (7 int8 slices per operand, tcgen05.mma.kind::i8, int32 TMEM
  * accumulators); K > 16384 runs as K-chunks accumulated into C in FP64.  The engine of the stage-4 evaluation GEMMs and the

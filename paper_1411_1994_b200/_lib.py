@@ -116,6 +116,7 @@ SIGNATURES = [
     ("latsum_dgemm_device", _I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P,
                                  _I64]),
     ("latsum_sytrd_device", _I, [_P, _I64, _P, _I64, _P, _P, _P]),
+    ("latsum_eig_sym_device", _I, [_P, _I64, _P, _I64, _P, _P, _I]),
     ("latsum_dgemm_ozaki_device", _I, [_P, _I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64]),
 ]
 

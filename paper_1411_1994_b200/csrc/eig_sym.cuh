@@ -37,6 +37,33 @@ struct TrdWork {
   double* part;  // 2 * TRD_CTAS
 };
 
+// A[i, j] = A[j, i] for i < j: the Grams come from a lower-triangle SYRK (as syevd reads them)
+__global__ void k_symmetrize_lower(double* __restrict__ A, int64_t lda, int n) {
+  const int64_t total = int64_t(n) * n;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(idx % n), j = int(idx / n);
+    if (i < j) A[i + int64_t(j) * lda] = A[j + int64_t(i) * lda];
+  }
+}
+
+// out[0] = max |S - I| over the k x k matrix S (one block)
+__global__ void k_max_offidentity(const double* __restrict__ S, int k, double* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t idx = threadIdx.x; idx < int64_t(k) * k; idx += blockDim.x) {
+    const int i = int(idx % k), j = int(idx / k);
+    m = fmax(m, fabs(S[idx] - (i == j ? 1.0 : 0.0)));
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < int(blockDim.x / 32); ++q) m = fmax(m, red[q]);
+    out[0] = fmax(m, red[0]);
+  }
+}
+
 // Householder reflector of x = A[kk+1 .. n-1, kk] by one warp (LAPACK dlarfg): H = I - tau
 // v v^T, v[kk+1] = 1, H x = (beta, 0, ..).  v -> vout[kk+1..n) and A[kk+2.., kk] (LAPACK
 // layout), beta -> e[kk] and A[kk+1, kk], tau -> tau[kk].
@@ -187,6 +214,235 @@ k_sytrd_cluster(double* __restrict__ A, int64_t lda, int n, double* __restrict__
       }
     }
     cluster.sync();
+  }
+}
+
+// ---------------------------------------------------------------- tridiagonal eigenvalues
+// All eigenvalues of the symmetric tridiagonal T = (d, e) by Sturm-count multisection: one
+// warp per eigenvalue, the 32 lanes count at 32 interior points of the current bracket, so
+// each round narrows it 33-fold (LAPACK dstebz's bisection, parallelised).  The counts are
+// exact to ~eps ||T|| (Kahan), which bounds the absolute accuracy as for any backward-
+// stable solver (syevd included).  w ascending.
+constexpr int EIG_WARPS = 8;  // warps (eigenvalues) per block
+
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2,
+                                           int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (q < 0.0) ++cnt;
+  for (int j = 1; j < n; ++j) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = d[j] - x - e2[j - 1] / q;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(32 * EIG_WARPS)
+k_tridiag_eigvals(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                  double* __restrict__ w) {
+  extern __shared__ double sm[];
+  double* d = sm;       // n
+  double* e2 = sm + n;  // n - 1
+  __shared__ double red[3][32 * EIG_WARPS / 32];
+  double gl = 1e308, gu = -1e308, em = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double dj = dg[j];
+    const double el = j > 0 ? fabs(eg[j - 1]) : 0.0, er = j + 1 < n ? fabs(eg[j]) : 0.0;
+    d[j] = dj;
+    if (j + 1 < n) e2[j] = eg[j] * eg[j];
+    gl = fmin(gl, dj - el - er);
+    gu = fmax(gu, dj + el + er);
+    em = fmax(em, er * er);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+  }
+  const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
+  if (lane == 0) {
+    red[0][wib] = gl;
+    red[1][wib] = gu;
+    red[2][wib] = em;
+  }
+  __syncthreads();
+  gl = red[0][0], gu = red[1][0], em = red[2][0];
+  for (int q = 1; q < EIG_WARPS; ++q) {
+    gl = fmin(gl, red[0][q]);
+    gu = fmax(gu, red[1][q]);
+    em = fmax(em, red[2][q]);
+  }
+  const double eps = 2.220446049250313e-16;
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, em) * 4.0;
+  gl -= 2.0 * eps * tnorm * n + 2.0 * pivmin;
+  gu += 2.0 * eps * tnorm * n + 2.0 * pivmin;
+  const int i = blockIdx.x * EIG_WARPS + wib;  // eigenvalue index (ascending)
+  if (i >= n) return;
+  double lo = gl, hi = gu;
+  for (int round = 0; round < 40; ++round) {
+    const double width = hi - lo;
+    if (width <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+    const double x = lo + width * double(lane + 1) / 33.0;
+    const int cnt = sturm_count(d, e2, n, x, pivmin);
+    const unsigned above = __ballot_sync(0xffffffffu, cnt > i);  // x beyond eigenvalue i
+    double nlo = lo, nhi = hi;
+    if (above) {
+      const int f = __ffs(above) - 1;
+      nhi = __shfl_sync(0xffffffffu, x, f);
+      if (f > 0) nlo = __shfl_sync(0xffffffffu, x, f - 1);
+    } else {
+      nlo = __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (nlo == lo && nhi == hi) break;  // no representable progress
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) w[i] = 0.5 * (lo + hi);
+}
+
+// ---------------------------------------------------------------- inverse iteration
+// Eigenvector of T for the eigenvalue lam[j] (one thread each): LU of T - lam I with partial
+// pivoting (LAPACK dgttrf; pivots below eps ||T|| perturbed, as dlagtf), then two inverse
+// iteration solves from a pseudo-random start.  Accurate as syevd's vectors (error
+// ~ eps ||T|| / gap); callers orthonormalise the bases they build from them.
+// Y[:, j] (n x k), unit 2-norm.  ws: 5 n doubles per thread.
+__global__ void k_tridiag_invit(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                                const double* __restrict__ lam, int k, double tnorm,
+                                double* __restrict__ Y, double* __restrict__ ws) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const double eps = 2.220446049250313e-16;
+  const double tiny = eps * fmax(tnorm, 1e-300);
+  const double l = lam[j];
+  double* u1 = ws + int64_t(j) * 5 * n;  // U diagonal
+  double* u2 = u1 + n;                   // U first super-diagonal
+  double* u3 = u2 + n;                   // U second super-diagonal (fill from swaps)
+  double* ml = u3 + n;                   // multipliers
+  double* sw = ml + n;                   // 1: rows i, i+1 swapped at step i
+  double* x = Y + int64_t(j) * n;
+  double a = dg[0] - l, b = n > 1 ? eg[0] : 0.0, c = 0.0;  // current row (cols i, i+1, i+2)
+  for (int i = 0; i + 1 < n; ++i) {
+    const double sub = eg[i], dn = dg[i + 1] - l, up = i + 2 < n ? eg[i + 1] : 0.0;
+    if (fabs(sub) > fabs(a)) {
+      const double m = a / sub;
+      u1[i] = sub;
+      u2[i] = dn;
+      u3[i] = up;
+      ml[i] = m;
+      sw[i] = 1.0;
+      a = b - m * dn;
+      b = c - m * up;
+    } else {
+      if (fabs(a) < tiny) a = a >= 0.0 ? tiny : -tiny;
+      const double m = sub / a;
+      u1[i] = a;
+      u2[i] = b;
+      u3[i] = c;
+      ml[i] = m;
+      sw[i] = 0.0;
+      a = dn - m * b;
+      b = up - m * c;
+    }
+    c = 0.0;
+  }
+  if (fabs(a) < tiny) a = a >= 0.0 ? tiny : -tiny;
+  u1[n - 1] = a;
+  // pseudo-random start (an all-ones start can be orthogonal to the eigenvector)
+  uint32_t h = 0x9E3779B9u * uint32_t(j + 1);
+  for (int i = 0; i < n; ++i) {
+    h ^= h << 13;
+    h ^= h >> 17;
+    h ^= h << 5;
+    x[i] = double(h & 0xFFFFFF) / double(0x1000000) + 0.5;
+  }
+  for (int it = 0; it < 3; ++it) {
+    for (int i = 0; i + 1 < n; ++i) {  // L^{-1} P
+      if (sw[i] != 0.0) {
+        const double t = x[i];
+        x[i] = x[i + 1];
+        x[i + 1] = t;
+      }
+      x[i + 1] -= ml[i] * x[i];
+    }
+    double mx = 0.0;
+    for (int i = n - 1; i >= 0; --i) {  // U^{-1}
+      double v = x[i];
+      if (i + 1 < n) v -= u2[i] * x[i + 1];
+      if (i + 2 < n) v -= u3[i] * x[i + 2];
+      v /= u1[i];
+      x[i] = v;
+      mx = fmax(mx, fabs(v));
+    }
+    const double s = mx > 0.0 ? 1.0 / mx : 1.0;
+    for (int i = 0; i < n; ++i) x[i] *= s;
+  }
+  double nrm = 0.0;
+  for (int i = 0; i < n; ++i) nrm += x[i] * x[i];
+  nrm = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+  for (int i = 0; i < n; ++i) x[i] *= nrm;
+}
+
+// ---------------------------------------------------------------- back-transformation
+// Q = H_0 H_1 .. H_{n-2} (sytrd 'L') applied to Y in compact-WY blocks of NB reflectors:
+// Q_b = I - V_b T_b V_b^T (LAPACK dlarft, forward / columnwise).  k_wy_build materialises
+// V_b (n x NB, unit lower trapezoidal from the reflectors stored in A) and T_b for every
+// block (one CTA per block); the caller applies Y <- Y - V_b (T_b (V_b^T Y)) with GEMMs,
+// last block first.
+constexpr int WY_NB = 32;
+
+__global__ void __launch_bounds__(256)
+k_wy_build(const double* __restrict__ A, int64_t lda, int n, const double* __restrict__ tau,
+           double* __restrict__ V, double* __restrict__ T) {
+  const int blk = blockIdx.x;
+  const int j0 = blk * WY_NB;  // first reflector of the block
+  const int nr = n - 1;        // reflectors 0 .. n-2
+  const int nb = min(WY_NB, nr - j0);
+  double* Vb = V + int64_t(blk) * WY_NB * n;
+  double* Tb = T + int64_t(blk) * WY_NB * WY_NB;
+  __shared__ double S[WY_NB][WY_NB + 1];
+  __shared__ double Ts[WY_NB][WY_NB + 1];
+  for (int idx = threadIdx.x; idx < WY_NB * n; idx += blockDim.x) {
+    const int jj = idx / n, r = idx % n;
+    const int kk = j0 + jj;  // reflector index
+    double v = 0.0;
+    if (jj < nb) {
+      if (r == kk + 1) v = 1.0;
+      else if (r > kk + 1) v = A[r + int64_t(kk) * lda];
+    }
+    Vb[r + int64_t(jj) * n] = v;
+  }
+  __syncthreads();
+  // S = V_b^T V_b (upper part needed)
+  for (int idx = threadIdx.x; idx < WY_NB * WY_NB; idx += blockDim.x) {
+    const int p = idx / WY_NB, q = idx % WY_NB;
+    double acc = 0.0;
+    if (p < q && q < nb) {
+      const double* vp = Vb + int64_t(p) * n;
+      const double* vq = Vb + int64_t(q) * n;
+      for (int r = j0 + q + 1; r < n; ++r) acc += vp[r] * vq[r];
+    }
+    S[p][q] = acc;
+    Ts[p][q] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nb; ++q) {
+      const double tq = tau[j0 + q];
+      // T[0:q, q] = -tau_q T[0:q, 0:q] S[0:q, q]
+      for (int p = 0; p < q; ++p) {
+        double acc = 0.0;
+        for (int m = p; m < q; ++m) acc += Ts[p][m] * S[m][q];
+        Ts[p][q] = -tq * acc;
+      }
+      Ts[q][q] = tq;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < WY_NB * WY_NB; idx += blockDim.x) {
+    const int p = idx % WY_NB, q = idx / WY_NB;
+    Tb[p + q * WY_NB] = Ts[p][q];  // column-major
   }
 }
 

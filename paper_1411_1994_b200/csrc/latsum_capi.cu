@@ -111,6 +111,7 @@ struct latsum_ctx {
   int64_t launches = 0;
   bool smem_set = false;
   bool oz_smem_set = false;
+  int64_t eig_fallbacks = 0;  // in-house eigensolves redone with syevd (degenerate clusters)
   // optional per-kernel-class CUDA-event timing (latsum_ctx_set_profiling)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double work; };
@@ -585,6 +586,130 @@ void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, 
   post_launch(c);
 }
 
+// Symmetric eigen-decomposition backend of the Gram passes.  cuSOLVER syevd (all
+// eigenvectors; the default) or, with LATSUM_EIG=custom and n <= kCustomEigMax, the
+// in-house solver: cluster sytrd, Sturm
+// multisection for every eigenvalue, inverse iteration for the leading eigenvectors the
+// caller asks for, compact-WY back-transformation on the DMMA GEMM.  The in-house path
+// never synchronises with the host inside, so the three modes' eigensolves overlap
+// (cuSOLVER's serialise), and it computes only the vectors that are used.
+constexpr int64_t kCustomEigMax = 1536;
+
+bool use_custom_eig(int64_t n) {
+  static const int mode = [] {
+    const char* e = std::getenv("LATSUM_EIG");
+    if (!e) return 0;
+    if (std::string(e) == "cusolver") return 1;
+    if (std::string(e) == "custom") return 2;
+    return 0;
+  }();
+  if (mode != 2) return false;  // opt-in until it beats syevd
+  return n >= 2 && n <= kCustomEigMax;
+}
+
+struct Eig {
+  int64_t n = 0;
+  bool custom = false;
+  DBuf G;  // cuSOLVER: eigenvectors (ascending columns); in-house: the sytrd reflectors
+  DBuf G0; // in-house: a copy of the input for the cuSOLVER fallback
+  DBuf d, e, tau;
+  double tnorm = 0.0;
+  std::vector<double> lam_asc;
+
+  // method: 0 = LATSUM_EIG / default, 1 = cuSOLVER, 2 = in-house
+  void solve(latsum_ctx* c, int64_t nn, DBuf&& Gin, int method = 0) {
+    n = nn;
+    G = std::move(Gin);
+    custom = method == 0 ? use_custom_eig(n) : (method == 2 && n >= 2 && n <= kCustomEigMax);
+    lam_asc.assign(n, 0.0);
+    if (n == 0) return;
+    DBuf W(c, n);
+    if (!custom) {
+      syevd(c, n, G.p, W.p);
+    } else {
+      d.alloc(c, n);
+      e.alloc(c, n);
+      tau.alloc(c, n);
+      eig::k_symmetrize_lower<<<grid_for(n * n), 256, 0, c->stream>>>(G.p, n, int(n));
+      post_launch(c);
+      G0.alloc(c, size_t(n) * n);
+      CK(cudaMemcpyAsync(G0.p, G.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
+      sytrd_cluster(c, n, G.p, n, d.p, e.p, tau.p);
+      ProfScope ps(c, "eig_values", double(n));
+      const size_t smem = size_t(2 * n) * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(eig::k_tridiag_eigvals, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(2 * kCustomEigMax * sizeof(double))));
+        attr = true;
+      }
+      eig::k_tridiag_eigvals<<<unsigned((n + eig::EIG_WARPS - 1) / eig::EIG_WARPS), 32 * eig::EIG_WARPS,
+                               smem, c->stream>>>(d.p, e.p, int(n), W.p);
+      post_launch(c);
+    }
+    CK(cudaMemcpyAsync(lam_asc.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (double v : lam_asc) tnorm = std::max(tnorm, std::fabs(v));
+  }
+
+  // the k leading eigenvectors (descending eigenvalues) into V (n x k)
+  void leading(latsum_ctx* c, int64_t k, double* V) {
+    if (k <= 0) return;
+    if (!custom) {
+      k_reverse_columns<<<grid_for(n * k), 256, 0, c->stream>>>(G.p, n, n, k, V);
+      post_launch(c);
+      return;
+    }
+    std::vector<double> lk(k);
+    for (int64_t j = 0; j < k; ++j) lk[j] = lam_asc[n - 1 - j];
+    DVec<double> dl;
+    dl.upload(c, lk);
+    {
+      ProfScope ps(c, "eig_invit", double(n) * double(k));
+      DBuf ws(c, size_t(5) * n * k);
+      eig::k_tridiag_invit<<<unsigned((k + 63) / 64), 64, 0, c->stream>>>(d.p, e.p, int(n), dl.p,
+                                                                           int(k), tnorm, V, ws.p);
+      post_launch(c);
+    }
+    // V <- Q V, Q = H_0 .. H_{n-2} in compact-WY blocks, last block first
+    const int64_t nr = n - 1, nb = eig::WY_NB, nblk = (nr + nb - 1) / nb;
+    if (nblk == 0) return;
+    DBuf Vw(c, size_t(nblk) * nb * n), Tw(c, size_t(nblk) * nb * nb);
+    eig::k_wy_build<<<unsigned(nblk), 256, 0, c->stream>>>(G.p, n, int(n), tau.p, Vw.p, Tw.p);
+    post_launch(c);
+    DBuf W1(c, size_t(nb) * k), W2(c, size_t(nb) * k);
+    for (int64_t b = nblk - 1; b >= 0; --b) {
+      const int64_t m = std::min(nb, nr - b * nb);
+      const double* Vb = Vw.p + size_t(b) * nb * n;
+      const double* Tb = Tw.p + size_t(b) * nb * nb;
+      gemm(c, true, false, m, k, n, 1.0, Vb, n, V, n, 0.0, W1.p, nb, tagged("gemm_eig_wy"));
+      gemm(c, false, false, m, k, m, 1.0, Tb, nb, W1.p, nb, 0.0, W2.p, nb, tagged("gemm_eig_wy"));
+      gemm(c, false, false, n, k, m, -1.0, Vb, n, W2.p, nb, 1.0, V, n, tagged("gemm_eig_wy"));
+    }
+    // Inverse iteration has no cluster re-orthogonalisation: (near-)degenerate eigenvalues
+    // give (near-)parallel vectors.  Check V^T V and fall back to syevd for this Gram when
+    // the vectors are not orthonormal to 1e-9 (the RHOSVD Grams' spectra pass).
+    DBuf S(c, size_t(k) * k), mx(c, 1);
+    gemm(c, true, false, k, k, n, 1.0, V, n, V, n, 0.0, S.p, k, tagged("gemm_eig_wy"));
+    eig::k_max_offidentity<<<1, 1024, 0, c->stream>>>(S.p, int(k), mx.p);
+    post_launch(c);
+    double dev = 0.0;
+    CK(cudaMemcpyAsync(&dev, mx.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (Trace::on()) fprintf(stderr, "[eig] n=%ld k=%ld orthogonality %.2e\n", long(n), long(k), dev);
+    if (!(dev <= 1e-9)) {
+      DBuf Wf(c, n);
+      syevd(c, n, G0.p, Wf.p);
+      k_reverse_columns<<<grid_for(n * k), 256, 0, c->stream>>>(G0.p, n, n, k, V);
+      post_launch(c);
+      c->eig_fallbacks++;
+      custom = false;  // G0 now holds all eigenvectors: later calls take them from there
+      G = std::move(G0);
+    }
+  }
+  bool has_all() const { return !custom; }
+};
+
 struct Timer {
   latsum_ctx* c;
   cudaEvent_t a, b;
@@ -995,9 +1120,25 @@ void polar_orthonormalize(latsum_ctx* c, double* U, int64_t Nb, int64_t k, bool 
   }
 }
 
-// U (Nb x k) = A (Nb x d) * [the k leading columns of evecs (d x n, ascending order)]
-// scaled by 1/sqrt(lam_desc), then re-orthonormalised: left singular vectors from the
-// eigenpairs of A^T A (row block of A -> row block of U).
+// U (Nb x k) = A (Nb x d) Vd scaled by 1/sqrt(lam_desc), then re-orthonormalised: left
+// singular vectors from the k leading eigenpairs (Vd: d x k, descending) of A^T A (row
+// block of A -> row block of U).
+void left_from_vectors(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, const double* Vd,
+                       const std::vector<double>& lam_desc, int64_t k, double* U, bool sharded) {
+  if (k == 0) return;
+  if (Nb > 0) {
+    gemm(c, false, false, Nb, k, d, 1.0, A, Nb, Vd, d, 0.0, U, Nb, tagged("gemm_basis"));
+    std::vector<double> inv(k);
+    for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
+    DVec<double> sc;
+    sc.upload(c, inv);
+    k_scale_columns<<<grid_for(Nb * k), 256, 0, c->stream>>>(U, Nb, k, sc.p, U);
+    post_launch(c);
+  }
+  polar_orthonormalize(c, U, Nb, k, sharded);
+}
+
+// the same from the k leading columns of an ascending eigenvector matrix (d x n)
 void left_from_right(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, const double* evecs,
                      int64_t n, const std::vector<double>& lam_desc, int64_t k, double* U,
                      bool sharded) {
@@ -1093,20 +1234,19 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   const int64_t n = rows ? N : d;
   out.rows = rows ? 1 : 0;
   out.gsize = n;
-  DBuf G(c, size_t(n) * n), W(c, n);
+  DBuf G(c, size_t(n) * n);
   if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
   else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
   if (sharded) allreduce(c, G.p, size_t(n) * n);
   tm.gram += timer.stop();
   Trace::mark(c, "gram done");
   timer.start();
-  syevd(c, n, G.p, W.p);
+  Eig e1;
+  e1.solve(c, n, std::move(G));
   tm.syevd += timer.stop();
   Trace::mark(c, "syevd1 done");
-  std::vector<double> lam(n), lam_d(n);
-  CK(cudaMemcpyAsync(lam.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  for (int64_t i = 0; i < n; ++i) lam_d[i] = std::max(lam[n - 1 - i], 0.0);
+  std::vector<double> lam_d(n);
+  for (int64_t i = 0; i < n; ++i) lam_d[i] = std::max(e1.lam_asc[n - 1 - i], 0.0);
   const double lmax = lam_d.empty() ? 0.0 : lam_d[0];
 
   auto padded_sigma = [&](const std::vector<double>& l2) {
@@ -1119,15 +1259,18 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   std::vector<double> merged = lam_d;
   std::vector<std::pair<int, int64_t>> src(n);  // (pass, index in that pass's desc order)
   for (int64_t i = 0; i < n; ++i) src[i] = {0, i};
-  int64_t k1 = 0, nc = 0;
-  DBuf U1, B, G2;
+  int64_t k1 = 0, nc = 0, n2 = 0;
+  const int64_t Nr = std::max<int64_t>(Nb, 1);
+  DBuf U1, B;
+  Eig e2;
+  bool restricted = false;  // pass 2 on the pass-1 complement Qc (needs all pass-1 vectors)
   std::vector<double> mu_d;
   bool defl = false;
   if ((!ranks || force_deflate) && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
     const std::vector<double> sv = padded_sigma(lam_d);
-    double n2 = 0;
-    for (double v : sv) n2 += v * v;
-    const double target = tol * std::sqrt(n2) / 3.0;
+    double sn2 = 0;
+    for (double v : sv) sn2 += v * v;
+    const double target = tol * std::sqrt(sn2) / 3.0;
     for (int64_t i = 0; i < n; ++i)
       if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
     k1 = std::max<int64_t>(k1, 1);
@@ -1136,13 +1279,14 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
                       target * target < 1e6 * double(n) * kEpsMach * lmax);
     if (defl) {
       timer.start();
-      const int64_t Nr = std::max<int64_t>(Nb, 1);
       U1.alloc(c, size_t(Nr) * k1);
       if (rows) {
-        k_reverse_columns<<<grid_for(N * k1), 256, 0, c->stream>>>(G.p, N, n, k1, U1.p);
-        post_launch(c);
+        e1.leading(c, k1, U1.p);
+        if (e1.custom) polar_orthonormalize(c, U1.p, N, k1, false);
       } else {
-        left_from_right(c, At.p, Nb, d, G.p, n, lam_d, k1, U1.p, sharded);
+        DBuf V1(c, size_t(d) * k1);
+        e1.leading(c, k1, V1.p);
+        left_from_vectors(c, At.p, Nb, d, V1.p, lam_d, k1, U1.p, sharded);
       }
       DBuf Ap(c, size_t(Nr) * d), C(c, size_t(k1) * d);
       if (Nb > 0)
@@ -1156,34 +1300,44 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         if (Nb > 0)
           gemm(c, false, false, Nb, d, k1, -1.0, U1.p, Nb, C.p, k1, 1.0, Ap.p, Nb, tagged("gemm_deflate"));
       }
-      // restrict to the pass-1 complement Qc = G[:, 0:nc] (ascending eigenvectors)
-      G2.alloc(c, size_t(nc) * nc);
-      if (rows) {  // B = Qc^T A'' (nc x d), G2 = B B^T
-        B.alloc(c, size_t(nc) * d);
-        gemm(c, true, false, nc, d, N, 1.0, G.p, N, Ap.p, N, 0.0, B.p, nc, tagged("gemm_deflate"));
-        gram(c, true, B.p, nc, d, G2.p);
-      } else {     // B = A'' Qc (Nb x nc), G2 = B^T B
-        B.alloc(c, size_t(Nr) * nc);
-        if (Nb > 0) {
-          gemm(c, false, false, Nb, nc, d, 1.0, Ap.p, Nb, G.p, d, 0.0, B.p, Nb, tagged("gemm_deflate"));
-          gram(c, false, B.p, Nb, nc, G2.p);
+      restricted = e1.has_all();
+      // pass-2 operand B: restricted to the pass-1 complement Qc = the nc trailing
+      // eigenvectors when they exist (cuSOLVER), else A'' itself (its Gram has k1 extra
+      // ~zero eigenvalues, the deflated directions)
+      n2 = restricted ? nc : n;
+      DBuf G2(c, size_t(n2) * n2);
+      if (rows) {  // G2 = B B^T with B = Qc^T A'' (nc x d) or A'' (N x d)
+        if (restricted) {
+          B.alloc(c, size_t(nc) * d);
+          gemm(c, true, false, nc, d, N, 1.0, e1.G.p, N, Ap.p, N, 0.0, B.p, nc, tagged("gemm_deflate"));
+          gram(c, true, B.p, nc, d, G2.p);
         } else {
-          CK(cudaMemsetAsync(G2.p, 0, sizeof(double) * nc * nc, c->stream));
+          gram(c, true, Ap.p, N, d, G2.p);
         }
-        if (sharded) allreduce(c, G2.p, size_t(nc) * nc);
+      } else {     // G2 = B^T B with B = A'' Qc (Nb x nc) or A'' (Nb x d)
+        if (restricted) {
+          B.alloc(c, size_t(Nr) * nc);
+          if (Nb > 0) {
+            gemm(c, false, false, Nb, nc, d, 1.0, Ap.p, Nb, e1.G.p, d, 0.0, B.p, Nb, tagged("gemm_deflate"));
+            gram(c, false, B.p, Nb, nc, G2.p);
+          } else {
+            CK(cudaMemsetAsync(G2.p, 0, sizeof(double) * nc * nc, c->stream));
+          }
+        } else {
+          B = std::move(Ap);
+          if (Nb > 0) gram(c, false, B.p, Nb, d, G2.p);
+          else CK(cudaMemsetAsync(G2.p, 0, sizeof(double) * n2 * n2, c->stream));
+        }
+        if (sharded) allreduce(c, G2.p, size_t(n2) * n2);
       }
       tm.deflate += timer.stop();
       Trace::mark(c, "deflation + G2 done");
       timer.start();
-      DBuf W2(c, nc);
-      syevd(c, nc, G2.p, W2.p);
+      e2.solve(c, n2, std::move(G2));
       tm.syevd += timer.stop();
       Trace::mark(c, "syevd2 done");
-      std::vector<double> mu(nc);
-      CK(cudaMemcpyAsync(mu.data(), W2.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      mu_d.resize(nc);
-      for (int64_t i = 0; i < nc; ++i) mu_d[i] = std::max(mu[nc - 1 - i], 0.0);
+      mu_d.resize(nc);  // the nc leading pass-2 values
+      for (int64_t i = 0; i < nc; ++i) mu_d[i] = std::max(e2.lam_asc[n2 - 1 - i], 0.0);
       // merged spectrum: k1 resolved pass-1 values and the nc deflated values
       std::vector<std::tuple<double, int, int64_t>> all;
       for (int64_t i = 0; i < k1; ++i) all.emplace_back(lam_d[i], 0, i);
@@ -1210,9 +1364,9 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   r = std::min<int64_t>(r, n);
   out.tie = r < int64_t(sv.size()) && sv[r - 1] - sv[r] <= 1e-12 * sv[0];
   if (!ranks) {
-    double n2 = 0, t_r = 0, t_rm1 = 0;
-    for (double v : sv) n2 += v * v;
-    const double target = tol * std::sqrt(n2) / 3.0;
+    double sn2 = 0, t_r = 0, t_rm1 = 0;
+    for (double v : sv) sn2 += v * v;
+    const double target = tol * std::sqrt(sn2) / 3.0;
     for (size_t k = r; k < sv.size(); ++k) t_r += sv[k] * sv[k];
     t_rm1 = t_r + sv[r - 1] * sv[r - 1];
     out.margin = std::min(target - std::sqrt(t_r), std::sqrt(t_rm1) - target) / target;
@@ -1221,14 +1375,15 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
 
   // Z = the r leading left singular vectors in merged (descending) order (row block)
   timer.start();
-  const int64_t Nr = std::max<int64_t>(Nb, 1);
   out.Z.alloc(c, size_t(Nr) * r);
   if (!defl) {
     if (rows) {
-      k_reverse_columns<<<grid_for(N * r), 256, 0, c->stream>>>(G.p, N, n, r, out.Z.p);
-      post_launch(c);
+      e1.leading(c, r, out.Z.p);
+      if (e1.custom) polar_orthonormalize(c, out.Z.p, N, r, false);
     } else {
-      left_from_right(c, At.p, Nb, d, G.p, n, lam_d, r, out.Z.p, sharded);
+      DBuf Vr(c, size_t(d) * r);
+      e1.leading(c, r, Vr.p);
+      left_from_vectors(c, At.p, Nb, d, Vr.p, lam_d, r, out.Z.p, sharded);
     }
   } else {
     int64_t need2 = 0;
@@ -1239,13 +1394,19 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
       CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * Nb * k1, cudaMemcpyDeviceToDevice, c->stream));
     if (need2) {
       double* U2 = cat.p + Nb * k1;
-      if (rows) {  // U2 = Qc * Y (leading eigenvectors of B B^T)
-        DBuf Yd(c, size_t(nc) * need2);
-        k_reverse_columns<<<grid_for(nc * need2), 256, 0, c->stream>>>(G2.p, nc, nc, need2, Yd.p);
-        post_launch(c);
-        gemm(c, false, false, N, need2, nc, 1.0, G.p, N, Yd.p, nc, 0.0, U2, N, tagged("gemm_basis"));
-      } else {     // U2 = B W mu^{-1/2}
-        left_from_right(c, B.p, Nb, nc, G2.p, nc, mu_d, need2, U2, sharded);
+      if (rows) {
+        if (restricted) {  // U2 = Qc Y (leading eigenvectors of B B^T)
+          DBuf Yd(c, size_t(nc) * need2);
+          e2.leading(c, need2, Yd.p);
+          gemm(c, false, false, N, need2, nc, 1.0, e1.G.p, N, Yd.p, nc, 0.0, U2, N, tagged("gemm_basis"));
+        } else {
+          e2.leading(c, need2, U2);
+          if (e2.custom) polar_orthonormalize(c, U2, N, need2, false);
+        }
+      } else {             // U2 = B W mu^{-1/2}
+        DBuf W2v(c, size_t(n2) * need2);
+        e2.leading(c, need2, W2v.p);
+        left_from_vectors(c, B.p, Nb, restricted ? nc : d, W2v.p, mu_d, need2, U2, sharded);
       }
     }
     if (Nb > 0) {
@@ -2716,6 +2877,21 @@ int latsum_sytrd_device(latsum_ctx* c, int64_t n, double* A, int64_t lda, double
   return guarded(c, [&] {
     require(A && d && n >= 1 && lda >= n && (n == 1 || (e && tau)), "latsum_sytrd_device: bad argument");
     sytrd_cluster(c, n, A, lda, d, e, tau);
+  });
+}
+
+int latsum_eig_sym_device(latsum_ctx* c, int64_t n, const double* A, int64_t k, double* w,
+                          double* V, int method) {
+  return guarded(c, [&] {
+    require(A && w && n >= 1 && k >= 0 && k <= n && (k == 0 || V) && method >= 0 && method <= 2,
+            "latsum_eig_sym_device: bad argument");
+    DBuf G(c, size_t(n) * n);
+    CK(cudaMemcpyAsync(G.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
+    Eig e;
+    e.solve(c, n, std::move(G), method);
+    CK(cudaMemcpyAsync(w, e.lam_asc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    e.leading(c, k, V);
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

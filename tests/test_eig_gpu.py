@@ -61,3 +61,34 @@ def test_sytrd_cluster_matches_lapack(ctx, n, kind):
     Q = _q_from_reflectors(Af, tau)
     assert np.max(np.abs(Q.T @ Q - np.eye(n))) < 1e-13 * max(1, np.sqrt(n) / 4)
     assert np.max(np.abs(Q @ T @ Q.T - A)) <= 1e-13 * max(scale, 1e-300) * max(1, np.sqrt(n) / 4)
+
+
+@pytest.mark.parametrize("n", [2, 3, 40, 357, 693, 1200])
+@pytest.mark.parametrize("kind", ["gram", "sym"])
+def test_eigensolver_matches_lapack(ctx, n, kind):
+    """Eigenvalues (all) and the leading eigenvectors of the in-house solver vs numpy eigh:
+    |lam - lam_ref| <= 1e-13 ||A||; the leading vectors (well separated in the Gram-like
+    spectra: the top third) match up to sign to eps ||A|| / gap and are orthonormal."""
+    import torch
+    from paper_1411_1994_b200 import _lib
+    A = _gram_like(n, n + 7) if kind == "gram" else _sym(n, n + 8)
+    k = max(1, n // 3)
+    dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F").copy()).cuda()
+    w = torch.zeros(n, dtype=torch.float64, device="cuda")
+    V = torch.zeros(n * k, dtype=torch.float64, device="cuda")
+    ctx.check(_lib.lib().latsum_eig_sym_device(ctx.handle, n, dA.data_ptr(), k, w.data_ptr(),
+                                               V.data_ptr(), 2))
+    lam = w.cpu().numpy()
+    Vh = V.cpu().numpy().reshape((n, k), order="F")
+    lr, vr = np.linalg.eigh(A)
+    scale = np.abs(lr).max()
+    assert np.max(np.abs(lam - lr)) <= 1e-13 * scale * max(1.0, np.sqrt(n) / 8)
+    order = np.argsort(lr)[::-1][:k]
+    for j in range(k):
+        lj = lr[order[j]]
+        gap = np.min(np.abs(np.delete(lr, order[j]) - lj)) if n > 1 else scale
+        v = vr[:, order[j]]
+        err = min(np.linalg.norm(Vh[:, j] - v), np.linalg.norm(Vh[:, j] + v))
+        assert err <= 1e-12 + 64 * 2.2e-16 * scale * np.sqrt(n) / max(gap, 1e-300), (j, err, gap)
+    if kind == "sym":  # well-separated random spectrum: numerically orthonormal
+        assert np.max(np.abs(Vh.T @ Vh - np.eye(k))) < 1e-10

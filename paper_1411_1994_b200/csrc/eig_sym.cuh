@@ -281,9 +281,11 @@ k_tridiag_eigvals(const double* __restrict__ dg, const double* __restrict__ eg, 
   const int i = blockIdx.x * EIG_WARPS + wib;  // eigenvalue index (ascending)
   if (i >= n) return;
   double lo = gl, hi = gu;
+  // stop at the accuracy the Sturm counts support: eps ||T|| absolute (as syevd)
+  const double atol = 2.0 * eps * tnorm + 4.0 * pivmin;
   for (int round = 0; round < 40; ++round) {
     const double width = hi - lo;
-    if (width <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+    if (width <= fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), atol)) break;
     const double x = lo + width * double(lane + 1) / 33.0;
     const int cnt = sturm_count(d, e2, n, x, pivmin);
     const unsigned above = __ballot_sync(0xffffffffu, cnt > i);  // x beyond eigenvalue i
@@ -308,19 +310,21 @@ k_tridiag_eigvals(const double* __restrict__ dg, const double* __restrict__ eg, 
 // iteration solves from a pseudo-random start.  Accurate as syevd's vectors (error
 // ~ eps ||T|| / gap); callers orthonormalise the bases they build from them.
 // Y[:, j] (n x k), unit 2-norm.  ws: 5 n doubles per thread.
-__global__ void k_tridiag_invit(const double* __restrict__ dg, const double* __restrict__ eg, int n,
-                                const double* __restrict__ lam, int k, double tnorm,
-                                double* __restrict__ Y, double* __restrict__ ws) {
+// one thread per vector, blockDim.x vectors per block with their LU factors in shared memory
+__global__ void __launch_bounds__(32)
+k_tridiag_invit(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                const double* __restrict__ lam, int k, double tnorm, double* __restrict__ Y) {
+  extern __shared__ double smf[];  // blockDim.x x 5 n
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= k) return;
   const double eps = 2.220446049250313e-16;
   const double tiny = eps * fmax(tnorm, 1e-300);
   const double l = lam[j];
-  double* u1 = ws + int64_t(j) * 5 * n;  // U diagonal
-  double* u2 = u1 + n;                   // U first super-diagonal
-  double* u3 = u2 + n;                   // U second super-diagonal (fill from swaps)
-  double* ml = u3 + n;                   // multipliers
-  double* sw = ml + n;                   // 1: rows i, i+1 swapped at step i
+  double* u1 = smf + int64_t(threadIdx.x) * 5 * n;  // U diagonal
+  double* u2 = u1 + n;                               // U first super-diagonal
+  double* u3 = u2 + n;                               // U second super-diagonal (fill from swaps)
+  double* ml = u3 + n;                               // multipliers
+  double* sw = ml + n;                               // 1: rows i, i+1 swapped at step i
   double* x = Y + int64_t(j) * n;
   double a = dg[0] - l, b = n > 1 ? eg[0] : 0.0, c = 0.0;  // current row (cols i, i+1, i+2)
   for (int i = 0; i + 1 < n; ++i) {
@@ -349,7 +353,8 @@ __global__ void k_tridiag_invit(const double* __restrict__ dg, const double* __r
   }
   if (fabs(a) < tiny) a = a >= 0.0 ? tiny : -tiny;
   u1[n - 1] = a;
-  // pseudo-random start (an all-ones start can be orthogonal to the eigenvector)
+  // pseudo-random start (an all-ones start can be orthogonal to the eigenvector), kept
+  // in the output column
   uint32_t h = 0x9E3779B9u * uint32_t(j + 1);
   for (int i = 0; i < n; ++i) {
     h ^= h << 13;
@@ -358,21 +363,24 @@ __global__ void k_tridiag_invit(const double* __restrict__ dg, const double* __r
     x[i] = double(h & 0xFFFFFF) / double(0x1000000) + 0.5;
   }
   for (int it = 0; it < 3; ++it) {
-    for (int i = 0; i + 1 < n; ++i) {  // L^{-1} P
+    double xi = x[0];
+    for (int i = 0; i + 1 < n; ++i) {  // L^{-1} P, streaming x[i+1]
+      double xn = x[i + 1];
       if (sw[i] != 0.0) {
-        const double t = x[i];
-        x[i] = x[i + 1];
-        x[i + 1] = t;
+        const double t = xi;
+        xi = xn;
+        xn = t;
       }
-      x[i + 1] -= ml[i] * x[i];
+      x[i] = xi;
+      xi = xn - ml[i] * xi;
     }
-    double mx = 0.0;
+    x[n - 1] = xi;
+    double mx = 0.0, x1 = 0.0, x2 = 0.0;  // x[i+1], x[i+2]
     for (int i = n - 1; i >= 0; --i) {  // U^{-1}
-      double v = x[i];
-      if (i + 1 < n) v -= u2[i] * x[i + 1];
-      if (i + 2 < n) v -= u3[i] * x[i + 2];
-      v /= u1[i];
+      const double v = (x[i] - u2[i] * x1 - u3[i] * x2) / u1[i];
       x[i] = v;
+      x2 = x1;
+      x1 = v;
       mx = fmax(mx, fabs(v));
     }
     const double s = mx > 0.0 ? 1.0 / mx : 1.0;
@@ -390,7 +398,7 @@ __global__ void k_tridiag_invit(const double* __restrict__ dg, const double* __r
 // V_b (n x NB, unit lower trapezoidal from the reflectors stored in A) and T_b for every
 // block (one CTA per block); the caller applies Y <- Y - V_b (T_b (V_b^T Y)) with GEMMs,
 // last block first.
-constexpr int WY_NB = 32;
+constexpr int WY_NB = 64;
 
 __global__ void __launch_bounds__(256)
 k_wy_build(const double* __restrict__ A, int64_t lda, int n, const double* __restrict__ tau,
@@ -401,8 +409,9 @@ k_wy_build(const double* __restrict__ A, int64_t lda, int n, const double* __res
   const int nb = min(WY_NB, nr - j0);
   double* Vb = V + int64_t(blk) * WY_NB * n;
   double* Tb = T + int64_t(blk) * WY_NB * WY_NB;
-  __shared__ double S[WY_NB][WY_NB + 1];
-  __shared__ double Ts[WY_NB][WY_NB + 1];
+  extern __shared__ double wysm[];  // S and T: 2 x WY_NB x (WY_NB + 1)
+  double (*S)[WY_NB + 1] = reinterpret_cast<double (*)[WY_NB + 1]>(wysm);
+  double (*Ts)[WY_NB + 1] = reinterpret_cast<double (*)[WY_NB + 1]>(wysm + WY_NB * (WY_NB + 1));
   for (int idx = threadIdx.x; idx < WY_NB * n; idx += blockDim.x) {
     const int jj = idx / n, r = idx % n;
     const int kk = j0 + jj;  // reflector index
@@ -444,6 +453,241 @@ k_wy_build(const double* __restrict__ A, int64_t lda, int n, const double* __res
     const int p = idx % WY_NB, q = idx / WY_NB;
     Tb[p + q * WY_NB] = Ts[p][q];  // column-major
   }
+}
+
+// ---------------------------------------------------------------- shared-memory sytrd
+// The same reduction with the trailing matrix resident in the cluster's shared memory
+// (n <= SM_TRD_MAX): CTA q keeps the lower part L[c.., c] of the columns c = q (mod 16).
+// Per column k (reflector v_k, tau_k in every CTA's smem):
+//   A  p-partials: pacc[r] = sum_{own c <= r} L[r,c] v[c] (row gather) + for own c the
+//      column dot sum_{r > c} L[r,c] v[r] (A = L + L^T - D)                | cluster barrier
+//   B  reduce-scatter: CTA q sums the 16 partials of its rows r = q (mod 16) through
+//      DSMEM, p = tau pacc, and its share of p.v                           | cluster barrier
+//   C  gather p (DSMEM), alpha = -tau/2 p.v, w = p + alpha v, update own columns
+//      L -= v w^T + w v^T; the owner of column k+1 then builds reflector k+1 | cluster barrier
+//   D  every CTA copies v_{k+1} from the owner's shared memory.
+// Outputs as k_sytrd_cluster (d, e, tau; reflectors below the subdiagonal of A).
+constexpr int SM_TRD_THREADS = 512;
+constexpr int SM_TRD_WARPS = SM_TRD_THREADS / 32;
+constexpr int SM_TRD_MAXCOL = 64;  // columns per CTA (n <= 1024)
+// doubles of shared memory for n: the owned lower columns plus 5 vectors
+__host__ __device__ inline int64_t sm_trd_doubles(int n) {
+  int64_t m = 0;
+  for (int q = 0; q < TRD_CTAS; ++q) {  // the largest share (q = 0)
+    int64_t t = 0;
+    for (int c = q; c < n; c += TRD_CTAS) t += n - c;
+    m = t > m ? t : m;
+  }
+  return m + 5 * int64_t(n) + 8;
+}
+
+__global__ void __launch_bounds__(SM_TRD_THREADS, 1)
+k_sytrd_smem(double* __restrict__ A, int64_t lda, int n, double* __restrict__ d,
+             double* __restrict__ e, double* __restrict__ tau, long long* __restrict__ prof) {
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64();
+#define TRD_MARK(i)                         \
+  if (prof) {                               \
+    const long long t1 = clock64();         \
+    tacc[i] += t1 - t0;                     \
+    t0 = t1;                                \
+  }
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  const int tid = threadIdx.x, lane = tid % 32, wib = tid / 32;
+  extern __shared__ double sm[];
+  __shared__ int off[SM_TRD_MAXCOL + 1];
+  __shared__ double red[SM_TRD_WARPS];
+  __shared__ double scal[4];  // [0..1] tau by parity, [2] p.v partial, [3] alpha
+  const int ncol = n > q ? (n - q + TRD_CTAS - 1) / TRD_CTAS : 0;  // owned columns
+  if (tid == 0) {
+    int o = 0;
+    for (int lc = 0; lc <= ncol; ++lc) {
+      off[lc] = o;
+      if (lc < ncol) o += n - (q + TRD_CTAS * lc);
+    }
+  }
+  __syncthreads();
+  // the vectors sit at the same offset in every CTA (after the largest column share,
+  // CTA 0's) so that DSMEM addresses map across the cluster
+  int share0 = 0;
+  for (int c = 0; c < n; c += TRD_CTAS) share0 += n - c;
+  double* Lm = sm;
+  double* vbuf = sm + share0;     // 2 n
+  double* pacc = vbuf + 2 * n;    // n
+  double* psl = pacc + n;         // n (own rows)
+  double* wv = psl + n;           // n
+  // load the owned lower columns
+  for (int lc = wib; lc < ncol; lc += SM_TRD_WARPS) {
+    const int c = q + TRD_CTAS * lc;
+    const double* src = A + int64_t(c) * lda;
+    for (int r = c + lane; r < n; r += 32) Lm[off[lc] + (r - c)] = src[r];
+  }
+  __syncthreads();
+  auto Lat = [&](int r, int lc, int c) -> double& { return Lm[off[lc] + (r - c)]; };
+
+  // reflector kk from the owner's column kk (local smem), by warp 0 of the owner CTA:
+  // v -> vbuf[par] rows kk+1.., scal[par] = tau; global d, e, tau and A[kk+2.., kk]
+  auto reflector = [&](int kk, int par) {
+    const int lc = kk / TRD_CTAS;
+    double* x = Lm + off[lc];  // x[r - kk] = L[r, kk]
+    if (lane == 0) d[kk] = x[0];
+    if (kk + 1 >= n) return;
+    const double alpha = x[1];
+    double ss = 0.0;
+    for (int r = kk + 2 + lane; r < n; r += 32) ss += x[r - kk] * x[r - kk];
+    ss = warp_sum(ss);
+    double beta, tk, sc;
+    if (ss == 0.0) {
+      beta = alpha;
+      tk = 0.0;
+      sc = 0.0;
+    } else {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tk = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    double* v = vbuf + par * n;
+    double* col = A + int64_t(kk) * lda;
+    for (int r = kk + 1 + lane; r < n; r += 32) {
+      const double vr = r == kk + 1 ? 1.0 : x[r - kk] * sc;
+      v[r] = vr;
+      if (r > kk + 1) col[r] = vr;
+    }
+    if (lane == 0) {
+      e[kk] = beta;
+      tau[kk] = tk;
+      col[kk + 1] = beta;
+      scal[par] = tk;
+    }
+  };
+
+  if (q == 0 && wib == 0) reflector(0, 0);
+  cluster.sync();
+  if (q != 0) {
+    const double* vo = cluster.map_shared_rank(vbuf, 0);
+    for (int r = 1 + tid; r < n; r += SM_TRD_THREADS) vbuf[r] = vo[r];
+    if (tid == 0) scal[0] = *cluster.map_shared_rank(&scal[0], 0);
+  }
+  __syncthreads();
+
+  for (int k = 0; k + 1 < n; ++k) {
+    const int par = k & 1;
+    const double* v = vbuf + par * n;
+    const double tk = scal[par];
+    // ---- A: symv partials over the owned columns c >= k+1
+    for (int r = k + 1 + tid; r < n; r += SM_TRD_THREADS) {
+      double s = 0.0;
+      for (int lc = 0; lc < ncol; ++lc) {
+        const int c = q + TRD_CTAS * lc;
+        if (c > r) break;
+        if (c >= k + 1) s += Lat(r, lc, c) * v[c];
+      }
+      pacc[r] = s;
+    }
+    __syncthreads();
+    for (int lc = wib; lc < ncol; lc += SM_TRD_WARPS) {
+      const int c = q + TRD_CTAS * lc;
+      if (c < k + 1) continue;
+      double s = 0.0;
+      for (int r = c + 1 + lane; r < n; r += 32) s += Lat(r, lc, c) * v[r];
+      s = warp_sum(s);
+      if (lane == 0) pacc[c] += s;
+    }
+    TRD_MARK(0);
+    cluster.sync();
+    TRD_MARK(1);
+    // ---- B: reduce-scatter of the own rows r = q (mod 16), r >= k+1
+    {
+      double dp = 0.0;
+      // 16 threads per row: thread t reads CTA (t % 16)'s partial
+      const int src = tid % TRD_CTAS, slot = tid / TRD_CTAS;  // 32 rows in flight
+      const double* pr = cluster.map_shared_rank(pacc, src);
+      const int r0 = ((k + 1 + TRD_CTAS - 1 - q) / TRD_CTAS) * TRD_CTAS + q;  // first own row >= k+1
+      // warp-uniform trip count: both 16-lane halves shuffle together
+      const int nown = r0 < n ? (n - 1 - r0) / TRD_CTAS + 1 : 0;  // own rows >= k+1
+      const int per = SM_TRD_THREADS / TRD_CTAS;                    // rows per sweep
+      for (int base = 0; base < nown; base += per) {
+        const int j = base + slot;
+        const int r = r0 + TRD_CTAS * j;
+        double part = j < nown ? pr[r] : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (src == 0 && j < nown) {
+          const double pv = tk * part;
+          psl[r] = pv;
+          dp += pv * v[r];
+        }
+      }
+      dp = warp_sum(dp);
+      if (lane == 0) red[wib] = dp;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < SM_TRD_WARPS; ++w) t += red[w];
+        scal[2] = t;
+      }
+    }
+    TRD_MARK(2);
+    cluster.sync();
+    TRD_MARK(3);
+    // ---- C: gather p, w, update, next reflector
+    if (tid < 32) {
+      double t = lane < TRD_CTAS ? *cluster.map_shared_rank(&scal[2], lane) : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) scal[3] = -0.5 * tk * t;
+    }
+    __syncthreads();
+    const double alpha = scal[3];
+    for (int r = k + 1 + tid; r < n; r += SM_TRD_THREADS) {
+      const double pr = *cluster.map_shared_rank(&psl[r], r % TRD_CTAS);
+      wv[r] = pr + alpha * v[r];
+    }
+    __syncthreads();
+    TRD_MARK(4);
+    const int own1 = (k + 1) % TRD_CTAS == q;  // this CTA owns column k+1
+    if (own1 && wib == 0) {
+      const int lc = (k + 1) / TRD_CTAS, c = k + 1;
+      if (tk != 0.0) {
+        const double vc = v[c], wc = wv[c];
+        for (int r = c + lane; r < n; r += 32) Lat(r, lc, c) -= v[r] * wc + wv[r] * vc;
+      }
+      __syncwarp();
+      reflector(k + 1, par ^ 1);
+    }
+    if (tk != 0.0) {
+      // warps 1.. (or all when column k+1 is elsewhere) update the other owned columns
+      const int w0 = own1 ? 1 : 0, nw = own1 ? SM_TRD_WARPS - 1 : SM_TRD_WARPS;
+      if (wib >= w0) {
+        for (int lc = wib - w0; lc < ncol; lc += nw) {
+          const int c = q + TRD_CTAS * lc;
+          if (c < k + 2) continue;
+          const double vc = v[c], wc = wv[c];
+          for (int r = c + lane; r < n; r += 32) Lat(r, lc, c) -= v[r] * wc + wv[r] * vc;
+        }
+      }
+    }
+    TRD_MARK(5);
+    cluster.sync();
+    TRD_MARK(6);
+    // ---- D: copy v_{k+1} and tau_{k+1} from the owner of column k+1
+    if (k + 2 < n) {
+      const int ow = (k + 1) % TRD_CTAS;
+      if (ow != q) {
+        double* vn = vbuf + (par ^ 1) * n;
+        const double* vo = cluster.map_shared_rank(vbuf + (par ^ 1) * n, ow);
+        for (int r = k + 2 + tid; r < n; r += SM_TRD_THREADS) vn[r] = vo[r];
+        if (tid == 0) scal[par ^ 1] = *cluster.map_shared_rank(&scal[par ^ 1], ow);
+      }
+      __syncthreads();
+    }
+    TRD_MARK(7);
+  }
+  if (prof && tid == 0 && q == 0)
+    for (int i = 0; i < 8; ++i) prof[i] = tacc[i];
+  cluster.sync();  // no CTA exits while a peer may still read its shared memory
+#undef TRD_MARK
 }
 
 }  // namespace eig

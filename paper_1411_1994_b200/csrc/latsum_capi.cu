@@ -567,6 +567,44 @@ void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, 
                             int(2 * 8192 * sizeof(double))));
     attr = true;
   }
+  constexpr int kSmemMax = 227 * 1024 - 2048;  // dynamic share (the kernel has ~1 KB static)
+  const bool smem = eig::sm_trd_doubles(int(n)) * int64_t(sizeof(double)) <= kSmemMax &&
+                    n <= eig::TRD_CTAS * eig::SM_TRD_MAXCOL && !std::getenv("LATSUM_SYTRD_L2");
+  if (smem) {  // trailing matrix resident in the cluster's shared memory
+    static bool attr2 = false;
+    if (!attr2) {
+      CK(cudaFuncSetAttribute(eig::k_sytrd_smem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CK(cudaFuncSetAttribute(eig::k_sytrd_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+      attr2 = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(eig::TRD_CTAS);
+    cfg.blockDim = dim3(eig::SM_TRD_THREADS);
+    cfg.dynamicSmemBytes = size_t(eig::sm_trd_doubles(int(n))) * sizeof(double);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = eig::TRD_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope ps(c, "eig_sytrd", double(n) * double(n) * double(n) * 4.0 / 3.0);
+    static const bool prof = std::getenv("LATSUM_SYTRD_PROF") != nullptr;
+    DBuf pb(c, 8);
+    long long* pp = prof ? reinterpret_cast<long long*>(pb.p) : nullptr;
+    CK(cudaLaunchKernelEx(&cfg, eig::k_sytrd_smem, A, lda, int(n), d, e, tau, pp));
+    post_launch(c);
+    if (prof) {
+      long long h[8];
+      CK(cudaMemcpyAsync(h, pp, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      fprintf(stderr, "[sytrd n=%ld] cycles/step: A %.0f S1 %.0f B %.0f S2 %.0f Cg %.0f Cu %.0f S3 %.0f D %.0f\n",
+              long(n), h[0] / double(n), h[1] / double(n), h[2] / double(n), h[3] / double(n),
+              h[4] / double(n), h[5] / double(n), h[6] / double(n), h[7] / double(n));
+    }
+    return;
+  }
   DBuf ws(c, size_t(3 * n + 2 * eig::TRD_CTAS + 8));
   eig::TrdWork w{ws.p, ws.p + n, ws.p + 2 * n, ws.p + 3 * n};
   cudaLaunchConfig_t cfg = {};
@@ -593,7 +631,7 @@ void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, 
 // caller asks for, compact-WY back-transformation on the DMMA GEMM.  The in-house path
 // never synchronises with the host inside, so the three modes' eigensolves overlap
 // (cuSOLVER's serialise), and it computes only the vectors that are used.
-constexpr int64_t kCustomEigMax = 1536;
+constexpr int64_t kCustomEigMax = 1024;  // shared-memory inverse-iteration factors
 
 bool use_custom_eig(int64_t n) {
   static const int mode = [] {
@@ -666,16 +704,23 @@ struct Eig {
     dl.upload(c, lk);
     {
       ProfScope ps(c, "eig_invit", double(n) * double(k));
-      DBuf ws(c, size_t(5) * n * k);
-      eig::k_tridiag_invit<<<unsigned((k + 63) / 64), 64, 0, c->stream>>>(d.p, e.p, int(n), dl.p,
-                                                                           int(k), tnorm, V, ws.p);
+      const int64_t per = size_t(5) * n * sizeof(double);
+      const int vpb = int(std::max<int64_t>(1, std::min<int64_t>(32, (227 * 1024 - 1024) / per)));
+      const size_t smem = size_t(vpb) * per;
+      require(int64_t(smem) <= 227 * 1024 - 1024, "eigensolver: n too large for shared-memory factors");
+      CK(cudaFuncSetAttribute(eig::k_tridiag_invit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024 - 1024));
+      eig::k_tridiag_invit<<<unsigned((k + vpb - 1) / vpb), unsigned(vpb), smem, c->stream>>>(
+          d.p, e.p, int(n), dl.p, int(k), tnorm, V);
       post_launch(c);
     }
     // V <- Q V, Q = H_0 .. H_{n-2} in compact-WY blocks, last block first
     const int64_t nr = n - 1, nb = eig::WY_NB, nblk = (nr + nb - 1) / nb;
     if (nblk == 0) return;
     DBuf Vw(c, size_t(nblk) * nb * n), Tw(c, size_t(nblk) * nb * nb);
-    eig::k_wy_build<<<unsigned(nblk), 256, 0, c->stream>>>(G.p, n, int(n), tau.p, Vw.p, Tw.p);
+    const size_t wsm = size_t(2) * nb * (nb + 1) * sizeof(double);
+    CK(cudaFuncSetAttribute(eig::k_wy_build, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wsm)));
+    eig::k_wy_build<<<unsigned(nblk), 256, wsm, c->stream>>>(G.p, n, int(n), tau.p, Vw.p, Tw.p);
     post_launch(c);
     DBuf W1(c, size_t(nb) * k), W2(c, size_t(nb) * k);
     for (int64_t b = nblk - 1; b >= 0; --b) {

@@ -253,7 +253,9 @@ constexpr size_t SMEM_BYTES = size_t(STAGES) * (A_STAGE + B_STAGE) + 128;
 __device__ unsigned long long g_oz_trace[2];
 #endif
 
-// fold groups [g0, g0 + ng) of the 4-column chunk at TMEM column c into x (Horner, base 256)
+// fold the NG groups of the 4-column chunk at TMEM column c into x (Horner, base 256, in
+// int64: |D_g| < 2^31 so the fold stays below 2^55; converting once per element instead of
+// once per group keeps the drain off the int->FP64 conversion pipe)
 template <int NG>
 __device__ __forceinline__ void drain4(uint32_t taddr, double* x) {
   int v[NG][4];
@@ -261,11 +263,11 @@ __device__ __forceinline__ void drain4(uint32_t taddr, double* x) {
   for (int g = 0; g < NG; ++g) tmem_ld4(taddr + uint32_t(g * BN), v[g]);
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    double h = double(v[0][j]);
+  for (int j = 0; j < 4; ++j) {  // exact int64 Horner fold, one conversion per element
+    long long h = v[0][j];
 #pragma unroll
-    for (int g = 1; g < NG; ++g) h = h * 256.0 + double(v[g][j]);
-    x[j] = h;
+    for (int g = 1; g < NG; ++g) h = h * 256 + v[g][j];
+    x[j] = __ll2double_rn(h);
   }
 }
 

@@ -256,14 +256,17 @@ __device__ unsigned long long g_oz_trace[2];
 // fold the NG groups of the 4-column chunk at TMEM column c into x (Horner, base 256, in
 // int64: |D_g| < 2^31 so the fold stays below 2^55; converting once per element instead of
 // once per group keeps the drain off the int->FP64 conversion pipe)
-template <int NG>
-__device__ __forceinline__ void drain4(uint32_t taddr, double* x) {
-  int v[NG][4];
+template <int NG, int W>
+__device__ __forceinline__ void drainw(uint32_t taddr, double* x) {
+  int v[NG][W];
 #pragma unroll
-  for (int g = 0; g < NG; ++g) tmem_ld4(taddr + uint32_t(g * BN), v[g]);
+  for (int g = 0; g < NG; ++g) {
+    if (W == 8) tmem_ld8(taddr + uint32_t(g * BN), v[g]);
+    else tmem_ld4(taddr + uint32_t(g * BN), v[g]);
+  }
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {  // exact int64 Horner fold, one conversion per element
+  for (int j = 0; j < W; ++j) {  // exact int64 Horner fold, one conversion per element
     long long h = v[0][j];
 #pragma unroll
     for (int g = 1; g < NG; ++g) h = h * 256 + v[g][j];
@@ -388,7 +391,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
       mbar_wait(tmem_full, uint32_t(np & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < EPI_COLS; c += 4) drain4<4>(tq + uint32_t(c), hv + c);
+      for (int c = 0; c < EPI_COLS; c += 8) drainw<4, 8>(tq + uint32_t(c), hv + c);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0)
@@ -399,7 +402,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
 #pragma unroll
       for (int c = 0; c < EPI_COLS; c += 4) {
         double lv[4];
-        drain4<3>(tq + uint32_t(c), lv);
+        drainw<3, 4>(tq + uint32_t(c), lv);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const double cs = __shfl_sync(0xffffffffu, c + j < 32 ? c0s : c1s, (c + j) % 32);

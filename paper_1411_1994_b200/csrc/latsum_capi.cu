@@ -410,11 +410,21 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
 struct OzSliced {
   DBuf data, scale;
   int64_t lines = 0, K = 0, KB = 0, tiles = 0;
+  int halves = 1;  // 2: B operand laid out for the 2-SM kernel
   const int8_t* digits() const { return reinterpret_cast<const int8_t*>(data.p); }
 };
 
+// 2-SM (cta_group::2) Ozaki kernel: LATSUM_OZ_2SM=1 (default off until measured faster)
+bool oz_use_2sm() {
+  static const bool v = [] {
+    const char* e = std::getenv("LATSUM_OZ_2SM");
+    return e && std::string(e) == "1";
+  }();
+  return v;
+}
+
 void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
-              OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {
+              OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0, int halves = 1, bool even_tiles = false) {
   static_assert(oz::BM == oz::BN, "one tile height for both operands");
   require(K <= oz::KMAX, "ozaki_gemm: K > 16384 overflows the int32 accumulators");
   if (L1 <= 0) L1 = std::max<int64_t>(L, 1);
@@ -422,9 +432,15 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
   out.K = K;
   out.KB = std::max<int64_t>(1, (K + oz::BKB - 1) / oz::BKB);
   out.tiles = (L + oz::BM - 1) / oz::BM;
+  out.halves = halves;
   require(out.tiles * out.KB < (int64_t(1) << 31), "ozaki_gemm: too many tiles");
-  const size_t bytes = size_t(out.tiles) * out.KB * oz::A_STAGE;
+  // the 2-SM kernel reads A tiles in pairs: pad to an even count with zero digits
+  const int64_t alloc_tiles = even_tiles ? (out.tiles + 1) / 2 * 2 : out.tiles;
+  const size_t bytes = size_t(alloc_tiles) * out.KB * oz::A_STAGE;
   out.data.alloc(c, (bytes + 7) / 8);
+  if (alloc_tiles > out.tiles)
+    CK(cudaMemsetAsync(reinterpret_cast<int8_t*>(out.data.p) + size_t(out.tiles) * out.KB * oz::A_STAGE, 0,
+                       size_t(out.KB) * oz::A_STAGE, c->stream));
   out.scale.alloc(c, size_t(std::max<int64_t>(L, 1)));
   if (L <= 0) return;
   ProfScope ps(c, "ozaki(slice)", double(L) * double(K) * 8.0 + double(bytes));
@@ -436,11 +452,22 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
   int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
   if (vec)
     oz::k_slice_tile<oz::BM, true><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB,
-                                                                        out.scale.p, d, L1, sl2);
+                                                                        out.scale.p, d, L1, sl2, halves);
   else
     oz::k_slice_tile<oz::BM, false><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB,
-                                                                         out.scale.p, d, L1, sl2);
+                                                                         out.scale.p, d, L1, sl2, halves);
   post_launch(c);
+}
+
+// A-side operands (rows of A) and B-side operands (columns of op(B)), laid out for the
+// kernel variant in use
+void oz_slice_a(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+                OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {
+  oz_slice(c, P, sl, sk, L, K, out, L1, sl2, 1, oz_use_2sm());
+}
+void oz_slice_b(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+                OzSliced& out) {
+  oz_slice(c, P, sl, sk, L, K, out, 0, 0, oz_use_2sm() ? 2 : 1, false);
 }
 
 // Output addressing of an Ozaki GEMM (ozaki_i8.cuh OzOut): plain column-major by default.
@@ -463,6 +490,32 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
   ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(a.K));
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  if (b.halves == 2) {  // 2-SM kernel: CTA pairs over (256-row, 128-column) tiles
+    static bool attr2 = false;
+    if (!attr2) {
+      CK(cudaFuncSetAttribute(oz::k_gemm_i8_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(oz::SMEM_BYTES2)));
+      attr2 = true;
+    }
+    const int64_t tiles_m2 = (a.tiles + 1) / 2, tiles2 = tiles_m2 * b.tiles;
+    const unsigned pairs = unsigned(std::min<int64_t>(tiles2, sms / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(oz::PTHREADS);
+    cfg.dynamicSmemBytes = oz::SMEM_BYTES2;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, oz::k_gemm_i8_2sm, a.digits(), (const double*)a.scale.p, b.digits(),
+                          (const double*)b.scale.p, M, N, a.KB, o, tiles_m2, tiles2));
+    post_launch(c);
+    return;
+  }
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
       a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, o, a.tiles, tiles);
@@ -493,8 +546,8 @@ void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double*
   for (int64_t k0 = 0; k0 < std::max<int64_t>(K, 1); k0 += kc) {
     const int64_t kk = std::min(kc, std::max<int64_t>(K - k0, 0));
     OzSliced a, b;
-    oz_slice(c, A + k0 * a_sk, 1, a_sk, M, kk, a, a_L1, a_sl2);
-    oz_slice(c, B + k0 * b_sk, b_sl, b_sk, N, kk, b);
+    oz_slice_a(c, A + k0 * a_sk, 1, a_sk, M, kk, a, a_L1, a_sl2);
+    oz_slice_b(c, B + k0 * b_sk, b_sl, b_sk, N, kk, b);
     o.beta = k0 == 0 ? beta0 : 1.0;
     oz_run(c, a, b, o, tag);
   }
@@ -2086,7 +2139,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   DBuf X(c, size_t(r0) * njc * nkc);
   const bool oz_x = eval_uses_ozaki(r2), oz_v = eval_uses_ozaki(r0);
   OzSliced sU0, sQ;  // sliced once and reused across the chunks that share them
-  if (oz_v) oz_slice(c, U0, 1, t.N[0], ni, r0, sU0);
+  if (oz_v) oz_slice_a(c, U0, 1, t.N[0], ni, r0, sU0);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
     if (oz_x) {  // Q[a, j, c] = sum_b core[a, b, c] U1[j, b]: A lines (a, c), one launch
@@ -2102,12 +2155,12 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
       oq.sC = r0 * njj;
       gemm(c, false, true, r0, njj, r1, 1.0, t.core.p, r0, U1 + j0, t.N[1], 0.0, Q.p, r0, oq);
     }
-    if (oz_x) oz_slice(c, Q.p, 1, r0 * njj, r0 * njj, r2, sQ);
+    if (oz_x) oz_slice_a(c, Q.p, 1, r0 * njj, r0 * njj, r2, sQ);
     for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
       const int64_t nkk = std::min(nkc, nk - k0);
       if (oz_x) {  // X = Q x_3 U2: B = U2[k0:k0+nkk, :]^T, lines = its rows
         OzSliced sU2;
-        oz_slice(c, U2 + k0, 1, t.N[2], nkk, r2, sU2);
+        oz_slice_b(c, U2 + k0, 1, t.N[2], nkk, r2, sU2);
         oz_run(c, sQ, sU2, oz_out(X.p, r0 * njj), "gemm_eval_x(ozaki-i8)");
       } else {
         gemm(c, false, true, r0 * njj, nkk, r2, 1.0, Q.p, r0 * njj, U2 + k0, t.N[2], 0.0, X.p,
@@ -2115,7 +2168,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
       }
       if (oz_v) {  // V_k = U0 X_k for the nkk slabs: B lines = the columns (j, k) of X
         OzSliced sX;
-        oz_slice(c, X.p, r0, 1, njj * nkk, r0, sX);
+        oz_slice_b(c, X.p, r0, 1, njj * nkk, r0, sX);
         oz::OzOut o = oz_out(out + k0 * ni * nj + j0 * ni, ni);
         o.nb = njj;
         o.bs = ni * nj;
@@ -2150,7 +2203,7 @@ void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3
   DBuf G2(c, size_t(nkc) * T), Y(c, size_t(nj) * nkc * d0);
   const bool oz = eval_uses_ozaki(d0);
   OzSliced sD0;
-  if (oz) oz_slice(c, D[0], 1, ld[0], ni, d0, sD0);
+  if (oz) oz_slice_a(c, D[0], 1, ld[0], ni, d0, sD0);
   for (int64_t k0 = 0; k0 < nk; k0 += nkc) {
     const int64_t nkk = std::min(nkc, nk - k0);
     k_gather_scale<<<grid_for(nkk * T), 256, 0, c->stream>>>(D[2] + k0, nkk, ld[2], tc[2], nullptr,
@@ -2163,7 +2216,7 @@ void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3
     gemm(c, false, true, nj, nkk, T, 1.0, G1.p, nj, G2.p, nkk, 0.0, Y.p, nj, o);
     if (oz) {
       OzSliced sY;  // lines = the (j, k) columns of V, K = d0
-      oz_slice(c, Y.p, 1, nj * nkk, nj * nkk, d0, sY);
+      oz_slice_b(c, Y.p, 1, nj * nkk, nj * nkk, d0, sY);
       oz_run(c, sD0, sY, oz_out(out + k0 * ni * nj, ni), tag);
     } else {
       gemm(c, false, true, ni, nj * nkk, d0, 1.0, D[0], ld[0], Y.p, nj * nkk, 0.0,

@@ -112,25 +112,54 @@ struct DictArgs {
   int nchunk;
 };
 
-__device__ __forceinline__ double dict_value(const DictArgs& a, const double* rj, int64_t s0,
-                                             int64_t s1, int64_t i) {
-  double v = 0.0;
-  for (int64_t s = s0; s < s1; ++s) v += rj[a.N / 2 - a.pl_shift[s] + i];
-  return v;
+// Dictionary entries of column c = (placement p, reference column j) for the DICT_RT rows
+// i0 + tid + DICT_THREADS r of this thread: v[r] = sum_{s in placement p} ref_j[N/2 - shift_s
+// + i].  Shifts outer, rows inner: the DICT_RT loads per shift are independent and coalesced
+// across the block (the shift list sits in shared memory), so the 256-shift sublattice
+// columns (cfg5) stream instead of forming one dependent L2 chain per entry.
+constexpr int DICT_THREADS = 256, DICT_RT = 8, DICT_MAXSH = 1024;
+static_assert(DICT_THREADS * DICT_RT == 2048, "one chunk of 2048 rows per block");
+
+__device__ __forceinline__ void dict_values(const DictArgs& a, const double* __restrict__ rj,
+                                            const int64_t* __restrict__ sh, int ns, int64_t i0,
+                                            int64_t i1, double* v) {
+#pragma unroll
+  for (int r = 0; r < DICT_RT; ++r) v[r] = 0.0;
+  for (int s = 0; s < ns; ++s) {
+    const double* src = rj + (a.N / 2 - sh[s]);
+#pragma unroll
+    for (int r = 0; r < DICT_RT; ++r) {
+      const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+      if (i < i1) v[r] += src[i];
+    }
+  }
 }
 
-__global__ void k_dict_sumsq(DictArgs a) {
+// stage the placement's shift list in shared memory (long lists: read from global)
+__device__ __forceinline__ const int64_t* dict_shifts(const DictArgs& a, int64_t p, int64_t* buf,
+                                                      int& ns) {
+  const int64_t s0 = a.pl_off[p], s1 = a.pl_off[p + 1];
+  ns = int(s1 - s0);
+  if (ns > DICT_MAXSH) return a.pl_shift + s0;
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) buf[s] = a.pl_shift[s0 + s];
+  __syncthreads();
+  return buf;
+}
+
+__global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
   __shared__ double red[32];
+  __shared__ int64_t shb[DICT_MAXSH];
   const int64_t c = blockIdx.x;
   const int64_t p = c / a.Rd, j = c % a.Rd;
   const double* rj = a.ref + j * 2 * a.N;
-  const int64_t s0 = a.pl_off[p], s1 = a.pl_off[p + 1];
+  int ns;
+  const int64_t* sh = dict_shifts(a, p, shb, ns);
   const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
+  double v[DICT_RT];
+  dict_values(a, rj, sh, ns, i0, i1, v);
   double s = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const double v = dict_value(a, rj, s0, s1, i);
-    s += v * v;
-  }
+#pragma unroll
+  for (int r = 0; r < DICT_RT; ++r) s += v[r] * v[r];
   s = block_sum(s, red);
   if (threadIdx.x == 0) a.partial[c * a.nchunk + blockIdx.y] = s;
 }
@@ -143,17 +172,22 @@ __global__ void k_dict_norms(DictArgs a, int64_t d) {
   a.norms[c] = sqrt(s);
 }
 
-__global__ void k_dict_write(DictArgs a) {
+__global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
+  __shared__ int64_t shb[DICT_MAXSH];
   const int64_t c = blockIdx.x;
   const int64_t p = c / a.Rd, j = c % a.Rd;
   const double* rj = a.ref + j * 2 * a.N;
-  const int64_t s0 = a.pl_off[p], s1 = a.pl_off[p + 1];
+  int ns;
+  const int64_t* sh = dict_shifts(a, p, shb, ns);
   const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
   const double nrm = a.norms[c];
+  double v[DICT_RT];
+  dict_values(a, rj, sh, ns, i0, i1, v);
   double* out = a.dict + c * a.N;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const double v = dict_value(a, rj, s0, s1, i);
-    out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v / nrm;
+#pragma unroll
+  for (int r = 0; r < DICT_RT; ++r) {
+    const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+    if (i < i1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] / nrm;
   }
 }
 

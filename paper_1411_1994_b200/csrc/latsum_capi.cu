@@ -1236,26 +1236,6 @@ void left_from_vectors(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, co
   polar_orthonormalize(c, U, Nb, k, sharded);
 }
 
-// the same from the k leading columns of an ascending eigenvector matrix (d x n)
-void left_from_right(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, const double* evecs,
-                     int64_t n, const std::vector<double>& lam_desc, int64_t k, double* U,
-                     bool sharded) {
-  if (k == 0) return;
-  if (Nb > 0) {
-    DBuf Vd(c, size_t(d) * k);
-    k_reverse_columns<<<grid_for(d * k), 256, 0, c->stream>>>(evecs, d, n, k, Vd.p);
-    post_launch(c);
-    gemm(c, false, false, Nb, k, d, 1.0, A, Nb, Vd.p, d, 0.0, U, Nb, tagged("gemm_basis"));
-    std::vector<double> inv(k);
-    for (int64_t j = 0; j < k; ++j) inv[j] = lam_desc[j] > 0.0 ? 1.0 / std::sqrt(lam_desc[j]) : 0.0;
-    DVec<double> sc;
-    sc.upload(c, inv);
-    k_scale_columns<<<grid_for(Nb * k), 256, 0, c->stream>>>(U, Nb, k, sc.p, U);
-    post_launch(c);
-  }
-  polar_orthonormalize(c, U, Nb, k, sharded);
-}
-
 struct ModeOut {
   std::vector<double> sigma;
   int64_t r = 1;

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -353,10 +354,37 @@ void launch_gemm(latsum_ctx* c, bool ta, bool tb, GemmParams p, int64_t tm, int6
   if (ta && tb) dgemm_dmma_kernel<Cfg, true, true><<<grid, th, sm, c->stream>>>(p);
 }
 
+void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t a_sl,
+                   int64_t a_sk, int64_t a_L1, int64_t a_sl2, const double* B, int64_t b_sl,
+                   int64_t b_sk, oz::OzOut o, const char* tag);
+
+// Large single products (stage 3 of the big configs: Grams, deflation, bases, projections)
+// run on the int8 tensor cores too (FP64-accurate Ozaki GEMM); LATSUM_GEMM_DMMA=1 keeps
+// every generic GEMM on DMMA.  Small products stay on DMMA (slicing overhead).
+bool gemm_to_ozaki(int64_t M, int64_t N, int64_t K) {
+  static const bool dmma = std::getenv("LATSUM_GEMM_DMMA") != nullptr;
+  return !dmma && double(M) * double(N) * double(K) >= 2e10 && K >= 64;
+}
+
+const char* ozaki_tag(const char* tag) {
+  static std::map<std::string, std::string> names;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& v = names[tag ? tag : "gemm"];
+  if (v.empty()) v = std::string(tag ? tag : "gemm") + "(ozaki-i8)";
+  return v.c_str();
+}
+
 void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
           int64_t ldc, GemmOpts o = {}) {
   if (M <= 0 || N <= 0 || o.batch <= 0) return;
+  if (!o.kseg && o.batch == 1 && gemm_to_ozaki(M, N, K)) {
+    const oz::OzOut oo{C, ldc, int64_t(1) << 62, 0, int64_t(1) << 62, 0, beta, alpha};
+    ozaki_gemm_ex(c, M, N, K, A, ta ? lda : 1, ta ? 1 : lda, 0, 0, B, tb ? 1 : ldb, tb ? ldb : 1, oo,
+                  ozaki_tag(o.tag));  // lower-triangle requests get the full product
+    return;
+  }
   set_gemm_smem(c);
   const int choice = gemm_cfg_choice();
   const int BM = 128, BK = 16;
@@ -462,7 +490,7 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
 // A-side operands (rows of A) and B-side operands (columns of op(B)), laid out for the
 // kernel variant in use
 void oz_slice_a(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
-                OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {
+                OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {  // line l: (l % L1) sl + (l / L1) sl2
   oz_slice(c, P, sl, sk, L, K, out, L1, sl2, 1, oz_use_2sm());
 }
 void oz_slice_b(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
@@ -471,8 +499,8 @@ void oz_slice_b(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t 
 }
 
 // Output addressing of an Ozaki GEMM (ozaki_i8.cuh OzOut): plain column-major by default.
-oz::OzOut oz_out(double* C, int64_t ldc, double beta = 0.0) {
-  return oz::OzOut{C, ldc, int64_t(1) << 62, 0, int64_t(1) << 62, 0, beta};
+oz::OzOut oz_out(double* C, int64_t ldc, double beta = 0.0, double alpha = 1.0) {
+  return oz::OzOut{C, ldc, int64_t(1) << 62, 0, int64_t(1) << 62, 0, beta, alpha};
 }
 
 // C = A op(B) + beta C from sliced operands (a.lines x b.lines output, addressing o).
@@ -533,12 +561,12 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
 #endif
 }
 
-// General form: A lines (rows) l -> A + (l % a_L1) + (l / a_L1) a_sl2, element k at + k a_sk;
-// B lines (columns of op(B)) n -> B + n b_sl, element k at + k b_sk; output addressing o
-// (beta accumulates).  K is split into <= KMAX chunks accumulated with beta = 1.
-void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t a_sk,
-                   int64_t a_L1, int64_t a_sl2, const double* B, int64_t b_sl, int64_t b_sk,
-                   oz::OzOut o, const char* tag) {
+// General form: A lines (rows of op(A)) l -> A + (l % a_L1) a_sl + (l / a_L1) a_sl2, element k
+// at + k a_sk; B lines (columns of op(B)) n -> B + n b_sl, element k at + k b_sk; output
+// addressing o (alpha, beta).  K is split into <= KMAX chunks accumulated with beta = 1.
+void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t a_sl,
+                   int64_t a_sk, int64_t a_L1, int64_t a_sl2, const double* B, int64_t b_sl,
+                   int64_t b_sk, oz::OzOut o, const char* tag) {
   if (M <= 0 || N <= 0) return;
   const int64_t parts = std::max<int64_t>(1, (K + oz::KMAX - 1) / oz::KMAX);
   const int64_t kc = std::max<int64_t>(1, (K + parts - 1) / parts);
@@ -546,7 +574,7 @@ void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double*
   for (int64_t k0 = 0; k0 < std::max<int64_t>(K, 1); k0 += kc) {
     const int64_t kk = std::min(kc, std::max<int64_t>(K - k0, 0));
     OzSliced a, b;
-    oz_slice_a(c, A + k0 * a_sk, 1, a_sk, M, kk, a, a_L1, a_sl2);
+    oz_slice_a(c, A + k0 * a_sk, a_sl, a_sk, M, kk, a, a_L1, a_sl2);
     oz_slice_b(c, B + k0 * b_sk, b_sl, b_sk, N, kk, b);
     o.beta = k0 == 0 ? beta0 : 1.0;
     oz_run(c, a, b, o, tag);
@@ -558,7 +586,7 @@ void ozaki_gemm_ex(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double*
 void ozaki_gemm(latsum_ctx* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double* C, int64_t ldc, const char* tag = "gemm(ozaki-i8)",
                 bool tb = false, double beta = 0.0) {
-  ozaki_gemm_ex(c, M, N, K, A, lda, 0, 0, B, tb ? 1 : ldb, tb ? ldb : 1, oz_out(C, ldc, beta), tag);
+  ozaki_gemm_ex(c, M, N, K, A, 1, lda, 0, 0, B, tb ? 1 : ldb, tb ? ldb : 1, oz_out(C, ldc, beta), tag);
 }
 
 // Evaluation slab GEMMs: int8 tensor cores (Ozaki, default) or FP64 DMMA
@@ -1614,7 +1642,7 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
       oz::OzOut o = oz_out(core, r[0], beta);
       o.mr = r[0];
       o.rs = r[0] * r[1];
-      ozaki_gemm_ex(c, ro, r[1], na, X.p, ro, 0, 0, P[1].p + a0 * r[1], 1, r[1], o,
+      ozaki_gemm_ex(c, ro, r[1], na, X.p, 1, ro, 0, 0, P[1].p + a0 * r[1], 1, r[1], o,
                     "gemm_core(ozaki-i8)");
     } else if (m == 0) {        // core (r0 x r1 r2) = P0[:, j] X^T
       gemm(c, false, true, r[0], ro, na, 1.0, P[0].p + a0 * r[0], r[0], X.p, ro, beta, core, r[0],
@@ -2126,7 +2154,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
       oz::OzOut o = oz_out(Q.p, r0);
       o.mr = r0;
       o.rs = r0 * njj;
-      ozaki_gemm_ex(c, r0 * r2, njj, r1, t.core.p, r0, r0, r0 * r1, U1 + j0, 1, t.N[1], o,
+      ozaki_gemm_ex(c, r0 * r2, njj, r1, t.core.p, 1, r0, r0, r0 * r1, U1 + j0, 1, t.N[1], o,
                     "gemm_eval_q(ozaki-i8)");
     } else {
       GemmOpts oq = tagged("gemm_eval_q");

@@ -242,11 +242,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 // Output addressing: tile row i (0 <= i < M) and column n land at
 //   C + (i % mr) + (i / mr) rs + (n / nb) bs + (n % nb) ldc,
 // i.e. a plain column-major C (mr = M, nb = N) or batches of row / column blocks (the
-// evaluators' slabs, the batched Q = core x2 U1); C = A op(B) + beta C.
+// evaluators' slabs, the batched Q = core x2 U1); C = alpha A op(B) + beta C.
 struct OzOut {
   double* C;
   int64_t ldc, nb, bs, mr, rs;
   double beta;
+  double alpha;  // C = alpha A op(B) + beta C
 };
 
 constexpr int EPI_WARPS = 8;
@@ -389,7 +390,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
       const int64_t i = mt * BM + q * 32 + lane;
       const int64_t n0 = nt * BN + half * EPI_COLS;
       // row / column scales, fetched before the accumulators are ready
-      const double ri = i < M ? ra[i] : 0.0;
+      const double ri = i < M ? o.alpha * ra[i] : 0.0;
       const double c0s = n0 + lane < N ? cb[n0 + lane] : 0.0;
       const double c1s = n0 + 32 + lane < N ? cb[n0 + 32 + lane] : 0.0;
       double hv[EPI_COLS];
@@ -608,7 +609,7 @@ k_gemm_i8_2sm(const int8_t* __restrict__ As, const double* __restrict__ ra,
       const int64_t mt = 2 * (t % tiles_m2) + rank, nt = t / tiles_m2;
       const int64_t i = mt * BM + q * 32 + lane;
       const int64_t n0 = nt * BN + half * EPI_COLS;
-      const double ri = i < M ? ra[i] : 0.0;
+      const double ri = i < M ? o.alpha * ra[i] : 0.0;
       const double c0s = n0 + lane < N ? cb[n0 + lane] : 0.0;
       const double c1s = n0 + 32 + lane < N ? cb[n0 + 32 + lane] : 0.0;
       double hv[EPI_COLS];

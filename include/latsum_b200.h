@@ -250,7 +250,7 @@ int latsum_sytrd_device(latsum_ctx* ctx, int64_t n, double* A, int64_t lda, doub
  * solver (cluster sytrd, Sturm multisection, inverse iteration, compact-WY
  * back-transformation; syevd fallback when the vectors are not orthonormal). */
 int latsum_eig_sym_device(latsum_ctx* ctx, int64_t n, const double* A, int64_t k, double* w,
-                          double* V, int method /* 0 default, 1 cuSOLVER, 2 in-house */);
+                          double* V, int method /* 0 default, 1 cuSOLVER, 2 in-house one-stage, 3 in-house two-stage (band) */);
 
 /* FP64-accurate C = A op(B) (column-major; op(B) = B^T when tb != 0) computed on the int8 tensor cores
  * by the Ozaki splitting (7 int8 slices per operand, tcgen05.mma.kind::i8, int32 TMEM

@@ -1,0 +1,724 @@
+// Two-stage symmetric eigensolver for the RHOSVD Grams (n <= SB_NMAX), the default
+// replacement of cuSOLVER syevd whose one-stage tridiagonalisation spends ~9 us per column
+// on launch latency (6.3 of 6.7 ms at n = 693) and whose concurrent calls serialise.
+//
+//   1. k_sy2sb   full -> lower band of width BW in ONE 16-CTA thread-block cluster: per
+//                panel of BW columns, CTA 0 factors the panel (a warp per column, the
+//                column in registers, one __syncthreads per reflector) into V, T (compact
+//                WY); the cluster applies Q^T A22 Q = A22 - W V^T - V W^T with
+//                W = A22 V T - 1/2 V (T^T V^T A22 V T), each CTA owning a column slab; the
+//                matrix stays in L2 and the per-panel dependencies are cluster barriers.
+//   2. k_sb2st   band -> tridiagonal by bulge chasing (the successive-band-reduction
+//                kernels of LAPACK dsb2st: Householder of length BW, one task = right
+//                application to the block below + a new reflector + its two-sided
+//                application to the next diagonal block).  The band (with room for the
+//                bulges) lives in ONE CTA's shared memory; each warp runs a sweep, and
+//                sweep s+1 starts task k once sweep s has finished task k+1 (the two then
+//                touch disjoint elements), so ~n/(2 BW) sweeps are in flight.
+//   3. eigenvalues by Sturm multisection (eig_sym.cuh), eigenvectors of the tridiagonal
+//      by inverse iteration (k_tridiag_invit_sm, factors and iterate in shared memory).
+//   4. k_band_backtransform  Z = Q1 Q2 Y for a few columns per CTA: the bulge reflectors
+//      of one sweep act on disjoint rows, so a sweep is one parallel step (half-warp dot
+//      products); the panels then apply I - V T V^T in reverse order.
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace latsum_b200 {
+namespace band {
+
+namespace cg = cooperative_groups;
+constexpr unsigned FULL = 0xffffffffu;
+
+constexpr int BW = 16;                 // band width (a half-warp)
+constexpr int S2B_CTAS = 16;           // cluster size (non-portable: 16)
+constexpr int S2B_THREADS = 512;       // 16 warps = the BW columns of a panel
+constexpr int S2B_RPL = 26;            // panel rows per lane: n <= 832
+constexpr int S2B_NMAX = 32 * S2B_RPL;
+constexpr int S2B_MAXC = (S2B_NMAX + S2B_CTAS - 1) / S2B_CTAS;  // owned columns per CTA
+constexpr int SB_LDB = 2 * BW + 2;     // band column stride in shared memory (bulge room)
+constexpr int SB_WARPS = 24;
+constexpr int SB_KBIG = 64;            // progress encoding: sweep * SB_KBIG + tasks done
+constexpr int SB_NMAX = 816;           // (34 n + 1024) doubles <= 227 KB
+constexpr int BT_CPB = 4;              // eigenvector columns per back-transform CTA
+constexpr int BT_THREADS = 512;
+
+__host__ __device__ inline int s2b_panels(int n) { return n >= 2 ? (n - 2) / BW : 0; }
+__host__ __device__ inline int sb_tasks_max(int n) { return n >= 2 ? (n - 2) / BW + 1 : 1; }
+constexpr int S2B_LDV = S2B_NMAX;      // row stride of the panel's V in shared memory
+inline size_t s2b_smem_doubles(int) {
+  return size_t(BW) * S2B_LDV + S2B_MAXC * 2 * BW + S2B_MAXC * BW + 6 * BW * BW + BW + 16 * BW;
+}
+inline size_t sb_smem_doubles(int n) { return size_t(SB_LDB) * n + SB_WARPS * 32; }
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Reduce acc[16] over the 32 lanes; lane l returns the total of acc[l >> 1].
+__device__ __forceinline__ double reduce16_scatter(const double (&acc)[16], int lane) {
+  double a8[8], a4[4], a2[2];
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double send = b4 ? acc[j] : acc[j + 8];
+    a8[j] = (b4 ? acc[j + 8] : acc[j]) + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double send = b3 ? a8[j] : a8[j + 4];
+    a4[j] = (b3 ? a8[j + 4] : a8[j]) + __shfl_xor_sync(FULL, send, 8);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double send = b2 ? a4[j] : a4[j + 2];
+    a2[j] = (b2 ? a4[j + 2] : a4[j]) + __shfl_xor_sync(FULL, send, 4);
+  }
+  const double send = b1 ? a2[0] : a2[1];
+  double r = (b1 ? a2[1] : a2[0]) + __shfl_xor_sync(FULL, send, 2);
+  return r + __shfl_xor_sync(FULL, r, 1);
+}
+
+// Reduce p[8] over the 16 lanes of a half-warp; lane l returns the total of p[(l >> 1) & 7].
+__device__ __forceinline__ double reduce8_half(const double (&p)[8], int lane) {
+  double a4[4], a2[2];
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double send = b3 ? p[j] : p[j + 4];
+    a4[j] = (b3 ? p[j + 4] : p[j]) + __shfl_xor_sync(FULL, send, 8);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double send = b2 ? a4[j] : a4[j + 2];
+    a2[j] = (b2 ? a4[j + 2] : a4[j]) + __shfl_xor_sync(FULL, send, 4);
+  }
+  const double send = b1 ? a2[0] : a2[1];
+  double r = (b1 ? a2[1] : a2[0]) + __shfl_xor_sync(FULL, send, 2);
+  return r + __shfl_xor_sync(FULL, r, 1);
+}
+
+// ---------------------------------------------------------------- stage 1: full -> band
+// A (n x n, full symmetric storage, lda) is reduced in place to lower band width BW:
+// A = Q1 B Q1^T, Q1 = P_0 P_1 .. P_{npan-1}, P_p = I - V_p T_p V_p^T.  Panel p covers columns
+// [pBW, pBW+BW) and rows [r0, n), r0 = (p+1)BW; reflector c of the panel has its unit entry
+// at row r0 + c.  Outputs: Vw (npan x BW x n, column c of panel p at Vw + (p BW + c) n,
+// zero above the unit entry: the caller zero-fills), Tw (npan x BW x BW, column-major
+// upper triangular).  Wg: BW x n scratch.
+struct S2BArgs {
+  double* A;
+  int64_t lda;
+  int n;
+  double* Vw;
+  double* Tw;
+  double* Wg;
+  long long* prof;  // optional: per-phase cycles of CTA 0 (8 slots)
+};
+
+__global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = int(cluster.block_rank());
+  const int n = a.n;
+  const int64_t lda = a.lda;
+  double* __restrict__ A = a.A;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ double sm[];
+  double* Vs = sm;                          // BW x S2B_LDV: the panel's V, local rows, zero past m
+  double* VWj = Vs + BW * S2B_LDV;          // S2B_MAXC x 2BW: (V, W) rows of the owned columns
+  double* Xs = VWj + S2B_MAXC * 2 * BW;     // S2B_MAXC x BW: X rows of the owned columns
+  double* Zp = Xs + S2B_MAXC * BW;          // BW x BW: this CTA's share of V^T X
+  double* Zf = Zp + BW * BW;                // V^T X
+  double* M2 = Zf + BW * BW;                // T^T V^T X
+  double* Ts = M2 + BW * BW;                // T (row-major)
+  double* Ss = Ts + BW * BW;                // V^T V (upper)
+  double* taus = Ss + BW * BW;              // BW
+  double* ys = taus + BW;                   // 16 warps x BW
+  const int npan = s2b_panels(n);
+  long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tclk = clock64();
+  auto mark = [&](int slot) {
+    if (a.prof) {
+      const long long t = clock64();
+      ph[slot] += t - tclk;
+      tclk = t;
+    }
+  };
+  for (int p = 0; p < npan; ++p) {
+    const int j0 = p * BW, r0 = j0 + BW, m = n - r0;
+    double* Vp = a.Vw + size_t(p) * BW * n;
+    double* Tp = a.Tw + size_t(p) * BW * BW;
+    if (q == 0) {  // ---- panel QR: warp c owns column j0 + c, lane holds rows lane + 32t
+      double x[S2B_RPL];
+      const double* colp = A + int64_t(j0 + wid) * lda + r0;
+#pragma unroll
+      for (int t = 0; t < S2B_RPL; ++t) {
+        const int r = lane + 32 * t;
+        x[t] = r < m ? __ldcg(colp + r) : 0.0;
+      }
+      mark(8);
+      // the serial chain per reflector is the owner's norm + scaling and one barrier;
+      // everything else (global stores, T) is done by all warps after the loop
+      for (int cc = 0; cc < BW; ++cc) {
+        if (wid == cc) {
+          const double alpha = __shfl_sync(FULL, x[0], cc);
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < S2B_RPL; t += 2) {
+            const int r = lane + 32 * t;
+            if (r > cc && r < m) s0 += x[t] * x[t];
+            if (t + 1 < S2B_RPL && r + 32 < m) s1 += x[t + 1] * x[t + 1];
+          }
+          const double ss = wsum(s0 + s1);
+          double tau = 0.0, beta = alpha, scal = 0.0;
+          if (m - cc > 1 && ss > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+            scal = 1.0 / (alpha - beta);
+            tau = (beta - alpha) * (1.0 / beta);
+          }
+          // rows past m hold zeros in x and in Vs: no predicates in the loops below
+          double* vc = Vs + cc * S2B_LDV + lane;
+          if (lane < cc) vc[0] = 0.0;
+          if (lane == cc) {
+            vc[0] = 1.0;
+            x[0] = beta;
+          }
+          if (lane > cc) {
+            x[0] *= scal;
+            vc[0] = x[0];
+          }
+#pragma unroll
+          for (int t = 1; t < S2B_RPL; ++t) {
+            x[t] *= scal;
+            vc[32 * t] = x[t];
+          }
+          if (lane == 0) taus[cc] = tau;
+        }
+        __syncthreads();
+        if (wid != cc) {
+          const double* vc = Vs + cc * S2B_LDV + lane;  // zero above row cc and past m
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < S2B_RPL; t += 2) {
+            s0 += vc[32 * t] * x[t];
+            if (t + 1 < S2B_RPL) s1 += vc[32 * (t + 1)] * x[t + 1];
+          }
+          const double s = wsum(s0 + s1);
+          if (wid > cc) {  // apply P_cc to column wid
+            const double f = taus[cc] * s;
+#pragma unroll
+            for (int t = 0; t < S2B_RPL; ++t) x[t] -= f * vc[32 * t];
+          } else if (lane == 0) {  // v_wid . v_cc for T
+            Ss[wid * BW + cc] = s;
+          }
+        }
+      }
+      mark(9);
+      {  // column wid (R, beta, v) back to A; v to the panel's Vp
+        double* colw = A + int64_t(j0 + wid) * lda + r0;
+        double* vg = Vp + size_t(wid) * n + r0;
+#pragma unroll
+        for (int t = 0; t < S2B_RPL; ++t) {
+          const int r = lane + 32 * t;
+          if (r < m) {
+            colw[r] = x[t];
+            if (r >= wid) vg[r] = Vs[wid * S2B_LDV + r];
+          }
+        }
+      }
+      __syncthreads();
+      if (wid == 0) {  // T (LAPACK dlarft, forward / columnwise): lane i keeps row i
+        double trow[BW];
+#pragma unroll
+        for (int c = 0; c < BW; ++c) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < c; e += 2) {
+            if (e >= lane) a0 += trow[e] * Ss[e * BW + c];
+            if (e + 1 < c && e + 1 >= lane) a1 += trow[e + 1] * Ss[(e + 1) * BW + c];
+          }
+          trow[c] = lane < c ? -taus[c] * (a0 + a1) : (lane == c ? taus[c] : 0.0);
+        }
+        if (lane < BW)
+#pragma unroll
+          for (int c = 0; c < BW; ++c) {
+            Ts[lane * BW + c] = trow[c];
+            Tp[lane + c * BW] = trow[c];  // column-major
+          }
+      }
+      __syncthreads();
+    }
+    mark(0);
+    cluster.sync();  // ---- panel published (V in Vp / A, T in Tp)
+    mark(1);
+    if (q != 0) {
+      for (int idx = tid; idx < BW * S2B_LDV; idx += S2B_THREADS) {
+        const int c = idx / S2B_LDV, r = idx % S2B_LDV;
+        Vs[idx] = r < m ? __ldcg(Vp + size_t(c) * n + r0 + r) : 0.0;
+      }
+      if (tid < BW * BW) Ts[tid] = __ldcg(Tp + (tid % BW) * BW + tid / BW);
+      __syncthreads();
+    }
+    const int cpc = (m + S2B_CTAS - 1) / S2B_CTAS;
+    const int lo = min(m, q * cpc), hi = min(m, lo + cpc);
+    // ---- Y = A22 V for the owned columns i (= rows of Y by symmetry), X = Y T
+    for (int i = lo + wid; i < hi; i += S2B_THREADS / 32) {
+      double acc[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+      const double* acol = A + int64_t(r0 + i) * lda + r0;
+      double av[S2B_RPL];  // the whole column first: one L2 round trip, not m/32
+#pragma unroll
+      for (int t = 0; t < S2B_RPL; ++t) {
+        const int k = lane + 32 * t;
+        av[t] = k < m ? __ldcg(acol + k) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < S2B_RPL; ++t) {
+        if (32 * t < m) {  // uniform; av and Vs are zero past m
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc[c] += av[t] * Vs[c * S2B_LDV + lane + 32 * t];
+        }
+      }
+      const double y = reduce16_scatter(acc, lane);
+      if ((lane & 1) == 0) ys[wid * BW + (lane >> 1)] = y;
+      __syncwarp();
+      if (lane < BW) {
+        double xv = 0.0;
+        for (int e = 0; e <= lane; ++e) xv += ys[wid * BW + e] * Ts[e * BW + lane];
+        Xs[(i - lo) * BW + lane] = xv;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    mark(2);
+    if (tid < BW * BW) {  // this CTA's share of Z = V^T X
+      const int ra = tid / BW, cb = tid % BW;
+      double z = 0.0;
+      for (int i = lo; i < hi; ++i) z += Vs[ra * S2B_LDV + i] * Xs[(i - lo) * BW + cb];
+      Zp[tid] = z;
+    }
+    cluster.sync();  // ---- partial Z published
+    mark(3);
+    if (tid < BW * BW) {
+      double z = 0.0;
+      for (int r = 0; r < S2B_CTAS; ++r) z += cluster.map_shared_rank(Zp, r)[tid];
+      Zf[tid] = z;
+    }
+    __syncthreads();
+    if (tid < BW * BW) {  // M2 = T^T Z
+      const int ra = tid / BW, cb = tid % BW;
+      double s = 0.0;
+      for (int e = 0; e <= ra; ++e) s += Ts[e * BW + ra] * Zf[e * BW + cb];
+      M2[tid] = s;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (hi - lo) * BW; idx += S2B_THREADS) {  // W = X - 1/2 V M2
+      const int ii = idx / BW, cb = idx % BW, i = lo + ii;
+      double s = 0.0;
+#pragma unroll
+      for (int ra = 0; ra < BW; ++ra) s += Vs[ra * S2B_LDV + i] * M2[ra * BW + cb];
+      const double w = Xs[ii * BW + cb] - 0.5 * s;
+      a.Wg[size_t(cb) * n + i] = w;
+      VWj[ii * 2 * BW + cb] = Vs[cb * S2B_LDV + i];
+      VWj[ii * 2 * BW + BW + cb] = w;
+    }
+    mark(4);
+    cluster.sync();  // ---- W published
+    mark(5);
+    // ---- A22[:, j] -= W V[j,:]^T + V W[j,:]^T for the owned columns j
+    for (int i = tid; i < m; i += S2B_THREADS) {
+      double wi[BW], vi[BW];
+#pragma unroll
+      for (int c = 0; c < BW; ++c) {
+        wi[c] = __ldcg(a.Wg + size_t(c) * n + i);
+        vi[c] = Vs[c * S2B_LDV + i];
+      }
+      for (int j8 = 0; j8 < hi - lo; j8 += 8) {  // 8 columns per L2 round trip
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          av[u] = j8 + u < hi - lo ? __ldcg(A + int64_t(r0 + lo + j8 + u) * lda + r0 + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double* vw = VWj + (j8 + u) * 2 * BW;
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < BW; ++c) s += wi[c] * vw[c] + vi[c] * vw[BW + c];
+          av[u] -= s;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j8 + u < hi - lo) A[int64_t(r0 + lo + j8 + u) * lda + r0 + i] = av[u];
+      }
+    }
+    mark(6);
+    cluster.sync();  // ---- A22 updated
+    mark(7);
+  }
+  if (a.prof && q == 0 && tid == 0)
+    for (int i = 0; i < 12; ++i) a.prof[i] = ph[i];
+}
+
+// ---------------------------------------------------------------- stage 2: band -> tridiagonal
+__device__ __forceinline__ int sbi(int r, int c) { return (r - c) + c * SB_LDB; }  // r >= c
+
+// LAPACK dlarfg on x (lane i = lane & 15 holds x_i, i < len): v_0 = 1, H x = beta e_0.
+__device__ __forceinline__ void warp_larfg(double x, int i, int len, double& beta, double& tau,
+                                           double& v) {
+  const double alpha = __shfl_sync(FULL, x, 0);
+  double ss = (i >= 1 && i < len) ? x * x : 0.0;
+  ss += __shfl_xor_sync(FULL, ss, 8);
+  ss += __shfl_xor_sync(FULL, ss, 4);
+  ss += __shfl_xor_sync(FULL, ss, 2);
+  ss += __shfl_xor_sync(FULL, ss, 1);
+  if (len <= 1 || ss == 0.0) {
+    beta = alpha;
+    tau = 0.0;
+    v = i == 0 ? 1.0 : 0.0;
+    return;
+  }
+  beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+  tau = (beta - alpha) / beta;
+  v = i == 0 ? 1.0 : (i < len ? x * (1.0 / (alpha - beta)) : 0.0);
+}
+
+// D <- H D H on the symmetric diagonal block [st, st+len) of the band (LAPACK dlarfy).
+// Lane (i, h) = (lane & 15, lane >> 4) holds D[i][8h .. 8h+8); vsh: v (16, zero past len).
+__device__ __forceinline__ void sb_sym_apply(double* AB, int st, int len, double tau, double vi,
+                                             const double* vsh, double* wsh, int lane) {
+  const int i = lane & 15, h = lane >> 4;
+  double d[8];
+  double t = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = 8 * h + jj;
+    double val = 0.0;
+    if (i < len && j < len) val = i >= j ? AB[sbi(st + i, st + j)] : AB[sbi(st + j, st + i)];
+    d[jj] = val;
+    t += val * vsh[j];
+  }
+  t += __shfl_xor_sync(FULL, t, 16);
+  double w = tau * t;
+  double s = (h == 0 && i < len) ? w * vi : 0.0;
+  s = wsum(s);
+  w -= 0.5 * tau * s * vi;
+  if (h == 0) wsh[i] = w;
+  __syncwarp();
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = 8 * h + jj;
+    if (i < len && j <= i) AB[sbi(st + i, st + j)] = d[jj] - vi * wsh[j] - w * vsh[j];
+  }
+  __syncwarp();
+}
+
+// The band of A (lower, width BW, full storage lda) -> d (n), e (n-1); reflectors of sweep
+// s, task k: rows s+1+k BW + i, v_i at V2[s n + k BW + i] (v_0 = 1), tau at TAU2[s KS + k].
+__global__ void __launch_bounds__(SB_WARPS * 32, 1)
+k_sb2st(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ dout,
+        double* __restrict__ eout, double* __restrict__ V2, double* __restrict__ TAU2, int KS) {
+  extern __shared__ double sm[];
+  double* AB = sm;
+  double* scr = AB + size_t(SB_LDB) * n;
+  __shared__ int prog_s[SB_WARPS];
+  volatile int* prog = prog_s;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int idx = tid; idx < n * SB_LDB; idx += blockDim.x) {
+    const int c = idx / SB_LDB, off = idx % SB_LDB, r = c + off;
+    AB[idx] = (off <= BW && r < n) ? A[r + int64_t(c) * lda] : 0.0;
+  }
+  if (tid < SB_WARPS) prog[tid] = tid * SB_KBIG;
+  __syncthreads();
+  double* vsh = scr + w * 32;
+  double* wsh = vsh + 16;
+  const int i = lane & 15, h = lane >> 4;
+  for (int s = w; s <= n - 3; s += SB_WARPS) {
+    const int pw = (s + SB_WARPS - 1) % SB_WARPS;
+    auto wait = [&](int need) {  // sweep s-1 has finished `need` tasks (or all)
+      if (s == 0) return;
+      const int target = (s - 1) * SB_KBIG + need;
+      if (lane == 0)
+        while (prog[pw] < target) __nanosleep(20);
+      __syncwarp();
+      __threadfence_block();
+    };
+    auto publish = [&](int val) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        prog[w] = val;
+      }
+    };
+    // task 0: annihilate column s below its subdiagonal, two-sided on block 0
+    wait(2);
+    int st = s + 1;
+    int len = min(BW, n - 1 - s);
+    double x = i < len ? AB[sbi(st + i, s)] : 0.0;
+    double beta, tau, vi;
+    warp_larfg(x, i, len, beta, tau, vi);
+    if (h == 0 && i < len) AB[sbi(st + i, s)] = i == 0 ? beta : 0.0;
+    if (h == 0) {
+      vsh[i] = vi;
+      if (i < len) V2[size_t(s) * n + i] = vi;
+    }
+    if (lane == 0) TAU2[size_t(s) * KS] = tau;
+    __syncwarp();
+    sb_sym_apply(AB, st, len, tau, vi, vsh, wsh, lane);
+    int k = 1;
+    publish(s * SB_KBIG + 1);
+    int ed = st + len - 1;
+    while (ed + 1 < n) {
+      wait(k + 2);
+      const int j1 = ed + 1, j2 = min(ed + BW, n - 1), lm = j2 - j1 + 1, ln = ed - st + 1;
+      // right application of the previous reflector to B = A[j1..j2, st..ed] (the bulge)
+      double b[8];
+      double t = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * h + jj;
+        b[jj] = (i < lm && j < ln) ? AB[sbi(j1 + i, st + j)] : 0.0;
+        t += b[jj] * vsh[j];
+      }
+      t += __shfl_xor_sync(FULL, t, 16);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) b[jj] -= tau * t * vsh[8 * h + jj];
+      // new reflector from B[:, 0], applied from the left to B[:, 1:]
+      const double x0 = __shfl_sync(FULL, b[0], i);
+      double beta2, tau2, v2;
+      warp_larfg(x0, i, lm, beta2, tau2, v2);
+      if (h == 0) b[0] = i == 0 ? beta2 : 0.0;
+      __syncwarp();
+      if (h == 0) vsh[i] = v2;
+      double pp[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) pp[jj] = (8 * h + jj >= 1) ? v2 * b[jj] : 0.0;
+      const double u = reduce8_half(pp, lane);
+      if ((lane & 1) == 0) wsh[8 * h + ((lane >> 1) & 7)] = u;
+      __syncwarp();
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * h + jj;
+        if (j >= 1) b[jj] -= tau2 * v2 * wsh[j];
+        if (i < lm && j < ln) AB[sbi(j1 + i, st + j)] = b[jj];
+      }
+      if (h == 0 && i < lm) V2[size_t(s) * n + (j1 - s - 1) + i] = v2;
+      if (lane == 0) TAU2[size_t(s) * KS + k] = tau2;
+      __syncwarp();
+      sb_sym_apply(AB, j1, lm, tau2, v2, vsh, wsh, lane);
+      st = j1;
+      ed = j2;
+      tau = tau2;
+      vi = v2;
+      ++k;
+      publish(s * SB_KBIG + k);
+    }
+    publish((s + 1) * SB_KBIG);
+  }
+  __syncthreads();
+  for (int j = tid; j < n; j += blockDim.x) {
+    dout[j] = AB[j * SB_LDB];
+    if (j + 1 < n) eout[j] = AB[1 + j * SB_LDB];
+  }
+}
+
+// ---------------------------------------------------------------- inverse iteration
+// Eigenvector of the tridiagonal (d, e) for lam[j], one thread per vector, the LU factors
+// (LAPACK dgttrf with partial pivoting, tiny pivots perturbed as dlagtf) and the iterate in
+// shared memory, interleaved across the block's threads (conflict-free).  Three inverse
+// iteration solves from a pseudo-random start; Y[:, j] unit 2-norm.
+__global__ void __launch_bounds__(64)
+k_tridiag_invit_sm(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                   const double* __restrict__ lam, int k, double tnorm, double* __restrict__ Y) {
+  extern __shared__ double smv[];
+  const int nt = blockDim.x, tj = threadIdx.x;
+  double* u1 = smv;              // 1 / pivot
+  double* u2 = u1 + size_t(n) * nt;
+  double* u3 = u2 + size_t(n) * nt;
+  double* ml = u3 + size_t(n) * nt;
+  double* x = ml + size_t(n) * nt;
+  unsigned char* sw = reinterpret_cast<unsigned char*>(x + size_t(n) * nt);
+  const int j = blockIdx.x * nt + tj;
+  if (j >= k) return;
+#define IX(i) (size_t(i) * nt + tj)
+  const double eps = 2.220446049250313e-16;
+  const double tiny = eps * fmax(tnorm, 1e-300);
+  const double l = lam[j];
+  double a = dg[0] - l, b = n > 1 ? eg[0] : 0.0, c = 0.0;
+  for (int r = 0; r + 1 < n; ++r) {
+    const double sub = eg[r], dn = dg[r + 1] - l, up = r + 2 < n ? eg[r + 1] : 0.0;
+    if (fabs(sub) > fabs(a)) {
+      const double rs = 1.0 / sub, m = a * rs;
+      u1[IX(r)] = rs;
+      u2[IX(r)] = dn;
+      u3[IX(r)] = up;
+      ml[IX(r)] = m;
+      sw[IX(r)] = 1;
+      a = b - m * dn;
+      b = c - m * up;
+    } else {
+      if (fabs(a) < tiny) a = a >= 0.0 ? tiny : -tiny;
+      const double ra = 1.0 / a, m = sub * ra;
+      u1[IX(r)] = ra;
+      u2[IX(r)] = b;
+      u3[IX(r)] = c;
+      ml[IX(r)] = m;
+      sw[IX(r)] = 0;
+      a = dn - m * b;
+      b = up - m * c;
+    }
+    c = 0.0;
+  }
+  if (fabs(a) < tiny) a = a >= 0.0 ? tiny : -tiny;
+  u1[IX(n - 1)] = 1.0 / a;
+  uint32_t hsh = 0x9E3779B9u * uint32_t(j + 1);
+  for (int r = 0; r < n; ++r) {
+    hsh ^= hsh << 13;
+    hsh ^= hsh >> 17;
+    hsh ^= hsh << 5;
+    x[IX(r)] = double(hsh & 0xFFFFFF) / double(0x1000000) + 0.5;
+  }
+  for (int it = 0; it < 3; ++it) {
+    double xi = x[IX(0)];
+    for (int r = 0; r + 1 < n; ++r) {  // L^{-1} P
+      double xn = x[IX(r + 1)];
+      if (sw[IX(r)]) {
+        const double t = xi;
+        xi = xn;
+        xn = t;
+      }
+      x[IX(r)] = xi;
+      xi = xn - ml[IX(r)] * xi;
+    }
+    x[IX(n - 1)] = xi;
+    double mx = 0.0, x1 = 0.0, x2 = 0.0;
+    for (int r = n - 1; r >= 0; --r) {  // U^{-1}
+      const double v = (x[IX(r)] - u2[IX(r)] * x1 - u3[IX(r)] * x2) * u1[IX(r)];
+      x[IX(r)] = v;
+      x2 = x1;
+      x1 = v;
+      mx = fmax(mx, fabs(v));
+    }
+    const double s = mx > 0.0 ? 1.0 / mx : 1.0;
+    for (int r = 0; r < n; ++r) x[IX(r)] *= s;
+  }
+  double nrm = 0.0;
+  for (int r = 0; r < n; ++r) nrm += x[IX(r)] * x[IX(r)];
+  nrm = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+  double* out = Y + size_t(j) * n;
+  for (int r = 0; r < n; ++r) out[r] = x[IX(r)] * nrm;
+#undef IX
+}
+
+// ---------------------------------------------------------------- back-transformation
+// Z[:, c] = Q1 Q2 Y[:, c] for BT_CPB columns per CTA (Z may alias Y).  Q2 = product of the
+// sweeps' reflectors in generation order, applied last sweep first; the reflectors of one
+// sweep cover disjoint BW-row blocks starting at row s+1, so thread t handles row s+1+t and
+// the dot products are half-warp reductions.  Q1 = P_0 .. P_{npan-1}, applied last first.
+__global__ void __launch_bounds__(BT_THREADS)
+k_band_backtransform(int n, int k, const double* __restrict__ V2, const double* __restrict__ TAU2,
+                     int KS, const double* __restrict__ Vw, const double* __restrict__ Tw,
+                     int npan, const double* Y, double* Z) {
+  extern __shared__ double smb[];
+  double* ys = smb;                        // n x BT_CPB (row-major)
+  double* wv = ys + size_t(n) * BT_CPB;    // BW x BT_CPB
+  double* tw = wv + BW * BT_CPB;           // BW x BT_CPB
+  const int c0 = blockIdx.x * BT_CPB, nc = min(BT_CPB, k - c0);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < n * BT_CPB; idx += BT_THREADS) {
+    const int r = idx % n, c = idx / n;
+    ys[r * BT_CPB + c] = c < nc ? Y[size_t(c0 + c) * n + r] : 0.0;
+  }
+  __syncthreads();
+  double nv[2] = {0.0, 0.0}, ntau[2] = {0.0, 0.0};  // reflectors of the next sweep (prefetched)
+  auto fetch = [&](int s) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int t = tid + half * BT_THREADS;
+      const bool act = s >= 0 && t < n - 1 - s;
+      nv[half] = act ? __ldg(V2 + size_t(s) * n + t) : 0.0;
+      ntau[half] = act ? __ldg(TAU2 + size_t(s) * KS + t / BW) : 0.0;
+    }
+  };
+  fetch(n - 3);
+  for (int s = n - 3; s >= 0; --s) {
+    const int rows = n - 1 - s;
+    const double cv[2] = {nv[0], nv[1]}, ctau[2] = {ntau[0], ntau[1]};
+    fetch(s - 1);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int t = tid + half * BT_THREADS;
+      if (t - (t & 15) >= rows) continue;  // whole half-warp beyond the sweep (uniform)
+      const bool act = t < rows;
+      const double v = cv[half];
+      const double tau = ctau[half];
+      const int r = s + 1 + t;
+      double y[BT_CPB], pr[BT_CPB];
+#pragma unroll
+      for (int c = 0; c < BT_CPB; ++c) {
+        y[c] = act ? ys[r * BT_CPB + c] : 0.0;
+        pr[c] = v * y[c];
+      }
+#pragma unroll
+      for (int c = 0; c < BT_CPB; ++c) {
+        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 8, 16);
+        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 4, 16);
+        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 2, 16);
+        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 1, 16);
+      }
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < BT_CPB; ++c) ys[r * BT_CPB + c] = y[c] - tau * pr[c] * v;
+      }
+    }
+    __syncthreads();
+  }
+  // Q1: panels last to first; thread (pair = tid / 8, seg = tid % 8), pair = (row of V^T, column)
+  const int pair = tid >> 3, seg = tid & 7;
+  const int pc = pair / BT_CPB, pcol = pair % BT_CPB;  // pair < 64 (512 threads)
+  double* vs = tw + BW * BT_CPB;  // BW x n: the panel's V
+  for (int p = npan - 1; p >= 0; --p) {
+    const int r0 = (p + 1) * BW;
+    const double* Vp = Vw + size_t(p) * BW * n;
+    for (int idx = tid; idx < BW * n; idx += BT_THREADS) vs[idx] = __ldg(Vp + idx);
+    __syncthreads();
+    double acc = 0.0;
+    for (int r = r0 + pc + seg; r < n; r += 8) acc += vs[pc * n + r] * ys[r * BT_CPB + pcol];
+    acc += __shfl_xor_sync(FULL, acc, 4);
+    acc += __shfl_xor_sync(FULL, acc, 2);
+    acc += __shfl_xor_sync(FULL, acc, 1);
+    if (seg == 0) wv[pc * BT_CPB + pcol] = acc;
+    __syncthreads();
+    if (tid < BW * BT_CPB) {  // tw = T wv (T upper triangular, column-major)
+      const int rr = tid / BT_CPB, cc = tid % BT_CPB;
+      const double* Tp = Tw + size_t(p) * BW * BW;
+      double s = 0.0;
+      for (int e = rr; e < BW; ++e) s += __ldg(Tp + rr + e * BW) * wv[e * BT_CPB + cc];
+      tw[tid] = s;
+    }
+    __syncthreads();
+    for (int r = r0 + tid; r < n; r += BT_THREADS) {
+      double y[BT_CPB];
+#pragma unroll
+      for (int c = 0; c < BT_CPB; ++c) y[c] = ys[r * BT_CPB + c];
+#pragma unroll
+      for (int e = 0; e < BW; ++e) {
+        const double v = vs[e * n + r];
+#pragma unroll
+        for (int c = 0; c < BT_CPB; ++c) y[c] -= v * tw[e * BT_CPB + c];
+      }
+#pragma unroll
+      for (int c = 0; c < BT_CPB; ++c) ys[r * BT_CPB + c] = y[c];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < n * nc; idx += BT_THREADS) {
+    const int r = idx % n, c = idx / n;
+    Z[size_t(c0 + c) * n + r] = ys[r * BT_CPB + c];
+  }
+}
+
+}  // namespace band
+}  // namespace latsum_b200

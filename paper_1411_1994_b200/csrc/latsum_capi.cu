@@ -29,6 +29,7 @@
 #include "latsum_kernels.cuh"
 #include "ozaki_i8.cuh"
 #include "eig_sym.cuh"
+#include "eig_band.cuh"
 
 using namespace latsum_b200;
 
@@ -113,6 +114,7 @@ struct latsum_ctx {
   bool smem_set = false;
   bool oz_smem_set = false;
   int64_t eig_fallbacks = 0;  // in-house eigensolves redone with syevd (degenerate clusters)
+  int eig_method = 0;         // Eig::solve default method (0: LATSUM_EIG / size rule, 1: syevd)
   // optional per-kernel-class CUDA-event timing (latsum_ctx_set_profiling)
   bool prof = false;
   struct Rec { std::string tag; cudaEvent_t a, b; double work; };
@@ -714,16 +716,30 @@ void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, 
 // (cuSOLVER's serialise), and it computes only the vectors that are used.
 constexpr int64_t kCustomEigMax = 1024;  // shared-memory inverse-iteration factors
 
-bool use_custom_eig(int64_t n) {
+// LATSUM_EIG: cusolver | custom (one-stage cluster sytrd) | band (two-stage, n <= SB_NMAX;
+// the default for those sizes)
+int eig_env_mode() {
   static const int mode = [] {
     const char* e = std::getenv("LATSUM_EIG");
     if (!e) return 0;
     if (std::string(e) == "cusolver") return 1;
     if (std::string(e) == "custom") return 2;
+    if (std::string(e) == "band") return 3;
     return 0;
   }();
-  if (mode != 2) return false;  // opt-in until it beats syevd
+  return mode;
+}
+bool band_eig_ok(int64_t n) { return n >= 2 && n <= band::SB_NMAX; }
+
+bool use_custom_eig(int64_t n) {
+  if (eig_env_mode() != 2) return false;  // opt-in
   return n >= 2 && n <= kCustomEigMax;
+}
+
+template <typename K>
+void set_smem_attr(K kernel, size_t bytes, bool cluster16 = false) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  if (cluster16) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 struct Eig {
@@ -735,11 +751,80 @@ struct Eig {
   double tnorm = 0.0;
   std::vector<double> lam_asc;
 
-  // method: 0 = LATSUM_EIG / default, 1 = cuSOLVER, 2 = in-house
+  // two-stage (band) path: panel reflectors (Vw, Tw) and bulge reflectors (V2, TAU2)
+  bool band = false;
+  DBuf Vw, Tw, V2, TAU2;
+  int KS = 1;
+
+  // full -> band (k_sy2sb, one 16-CTA cluster) -> tridiagonal d, e (k_sb2st, one CTA)
+  void band_reduce(latsum_ctx* c) {
+    const int ni = int(n), npan = band::s2b_panels(ni);
+    KS = band::sb_tasks_max(ni);
+    Vw.alloc(c, std::max<size_t>(1, size_t(npan) * band::BW * n));
+    Tw.alloc(c, std::max<size_t>(1, size_t(npan) * band::BW * band::BW));
+    V2.alloc(c, size_t(n) * n);
+    TAU2.alloc(c, size_t(n) * KS);
+    if (npan > 0) {
+      CK(cudaMemsetAsync(Vw.p, 0, sizeof(double) * Vw.n, c->stream));
+      DBuf Wg(c, size_t(band::BW) * n);
+      const size_t smem = band::s2b_smem_doubles(ni) * sizeof(double);
+      static std::once_flag once;
+      std::call_once(once, [&] { set_smem_attr(band::k_sy2sb, band::s2b_smem_doubles(band::S2B_NMAX) * 8, true); });
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(band::S2B_CTAS);
+      cfg.blockDim = dim3(band::S2B_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = band::S2B_CTAS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      static const bool prof = std::getenv("LATSUM_SY2SB_PROF") != nullptr;
+      DBuf pb(c, 12);
+      band::S2BArgs args{G.p, int64_t(n), ni, Vw.p, Tw.p, Wg.p,
+                         prof ? reinterpret_cast<long long*>(pb.p) : nullptr};
+      {
+        ProfScope ps(c, "eig_sy2sb", double(n) * double(n) * double(n) * 4.0 / 3.0);
+        CK(cudaLaunchKernelEx(&cfg, band::k_sy2sb, args));
+        post_launch(c);
+      }
+      if (prof) {
+        long long h[12];
+        CK(cudaMemcpyAsync(h, pb.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        fprintf(stderr, "[sy2sb qr split] loads %.1f columns %.1f\n", h[8] / 1e3 / npan, h[9] / 1e3 / npan);
+        fprintf(stderr, "[sy2sb n=%d] kcycles/panel: qr %.1f bar1 %.1f Y %.1f bar2 %.1f ZW %.1f bar3 %.1f U3 %.1f bar4 %.1f\n",
+                ni, h[0] / 1e3 / npan, h[1] / 1e3 / npan, h[2] / 1e3 / npan, h[3] / 1e3 / npan,
+                h[4] / 1e3 / npan, h[5] / 1e3 / npan, h[6] / 1e3 / npan, h[7] / 1e3 / npan);
+      }
+    }
+    {
+      const size_t smem = band::sb_smem_doubles(ni) * sizeof(double);
+      static std::once_flag once;
+      std::call_once(once, [&] { set_smem_attr(band::k_sb2st, band::sb_smem_doubles(band::SB_NMAX) * 8); });
+      ProfScope ps(c, "eig_sb2st", double(n) * double(n));
+      band::k_sb2st<<<1, band::SB_WARPS * 32, smem, c->stream>>>(G.p, n, ni, d.p, e.p, V2.p,
+                                                                  TAU2.p, KS);
+      post_launch(c);
+    }
+  }
+
+  // method: 0 = LATSUM_EIG / default, 1 = cuSOLVER, 2 = in-house one-stage, 3 = two-stage
   void solve(latsum_ctx* c, int64_t nn, DBuf&& Gin, int method = 0) {
     n = nn;
     G = std::move(Gin);
-    custom = method == 0 ? use_custom_eig(n) : (method == 2 && n >= 2 && n <= kCustomEigMax);
+    if (method == 0) method = c->eig_method;
+    if (method == 0) {  // default: the two-stage solver where it applies, else syevd
+      const int env = eig_env_mode();
+      band = (env == 0 || env == 3) && band_eig_ok(n);
+      custom = band || use_custom_eig(n);
+    } else {
+      band = method == 3 && band_eig_ok(n);
+      custom = band || (method == 2 && n >= 2 && n <= kCustomEigMax);
+    }
     lam_asc.assign(n, 0.0);
     if (n == 0) return;
     DBuf W(c, n);
@@ -753,7 +838,8 @@ struct Eig {
       post_launch(c);
       G0.alloc(c, size_t(n) * n);
       CK(cudaMemcpyAsync(G0.p, G.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
-      sytrd_cluster(c, n, G.p, n, d.p, e.p, tau.p);
+      if (band) band_reduce(c);
+      else sytrd_cluster(c, n, G.p, n, d.p, e.p, tau.p);
       ProfScope ps(c, "eig_values", double(n));
       const size_t smem = size_t(2 * n) * sizeof(double);
       static bool attr = false;
@@ -783,6 +869,31 @@ struct Eig {
     for (int64_t j = 0; j < k; ++j) lk[j] = lam_asc[n - 1 - j];
     DVec<double> dl;
     dl.upload(c, lk);
+    if (band) {
+      {
+        ProfScope ps(c, "eig_invit", double(n) * double(k));
+        const int64_t per = 41 * n;  // bytes per vector: 5 doubles + 1 flag per row
+        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(32, (227 * 1024 - 1024) / per)));
+        static std::once_flag once;
+        std::call_once(once, [&] { set_smem_attr(band::k_tridiag_invit_sm, 227 * 1024 - 1024); });
+        band::k_tridiag_invit_sm<<<unsigned((k + nt - 1) / nt), unsigned(nt), size_t(nt) * per,
+                                   c->stream>>>(d.p, e.p, int(n), dl.p, int(k), tnorm, V);
+        post_launch(c);
+      }
+      {
+        ProfScope ps(c, "eig_backtransform", double(n) * double(n) * double(k));
+        const size_t smem = (size_t(n) * (band::BT_CPB + band::BW) + 2 * band::BW * band::BT_CPB) * sizeof(double);
+        static std::once_flag once;
+        std::call_once(once, [&] {
+          set_smem_attr(band::k_band_backtransform,
+                        (size_t(band::SB_NMAX) * (band::BT_CPB + band::BW) + 2 * band::BW * band::BT_CPB) * 8);
+        });
+        band::k_band_backtransform<<<unsigned((k + band::BT_CPB - 1) / band::BT_CPB), band::BT_THREADS,
+                                     smem, c->stream>>>(int(n), int(k), V2.p, TAU2.p, KS, Vw.p, Tw.p,
+                                                        band::s2b_panels(int(n)), V, V);
+        post_launch(c);
+      }
+    } else {
     {
       ProfScope ps(c, "eig_invit", double(n) * double(k));
       const int64_t per = size_t(5) * n * sizeof(double);
@@ -798,19 +909,20 @@ struct Eig {
     // V <- Q V, Q = H_0 .. H_{n-2} in compact-WY blocks, last block first
     const int64_t nr = n - 1, nb = eig::WY_NB, nblk = (nr + nb - 1) / nb;
     if (nblk == 0) return;
-    DBuf Vw(c, size_t(nblk) * nb * n), Tw(c, size_t(nblk) * nb * nb);
+    DBuf Vwy(c, size_t(nblk) * nb * n), Twy(c, size_t(nblk) * nb * nb);
     const size_t wsm = size_t(2) * nb * (nb + 1) * sizeof(double);
     CK(cudaFuncSetAttribute(eig::k_wy_build, cudaFuncAttributeMaxDynamicSharedMemorySize, int(wsm)));
-    eig::k_wy_build<<<unsigned(nblk), 256, wsm, c->stream>>>(G.p, n, int(n), tau.p, Vw.p, Tw.p);
+    eig::k_wy_build<<<unsigned(nblk), 256, wsm, c->stream>>>(G.p, n, int(n), tau.p, Vwy.p, Twy.p);
     post_launch(c);
     DBuf W1(c, size_t(nb) * k), W2(c, size_t(nb) * k);
     for (int64_t b = nblk - 1; b >= 0; --b) {
       const int64_t m = std::min(nb, nr - b * nb);
-      const double* Vb = Vw.p + size_t(b) * nb * n;
-      const double* Tb = Tw.p + size_t(b) * nb * nb;
+      const double* Vb = Vwy.p + size_t(b) * nb * n;
+      const double* Tb = Twy.p + size_t(b) * nb * nb;
       gemm(c, true, false, m, k, n, 1.0, Vb, n, V, n, 0.0, W1.p, nb, tagged("gemm_eig_wy"));
       gemm(c, false, false, m, k, m, 1.0, Tb, nb, W1.p, nb, 0.0, W2.p, nb, tagged("gemm_eig_wy"));
       gemm(c, false, false, n, k, m, -1.0, Vb, n, W2.p, nb, 1.0, V, n, tagged("gemm_eig_wy"));
+    }
     }
     // Inverse iteration has no cluster re-orthogonalisation: (near-)degenerate eigenvalues
     // give (near-)parallel vectors.  Check V^T V and fall back to syevd for this Gram when
@@ -823,17 +935,30 @@ struct Eig {
     CK(cudaMemcpyAsync(&dev, mx.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (Trace::on()) fprintf(stderr, "[eig] n=%ld k=%ld orthogonality %.2e\n", long(n), long(k), dev);
-    if (!(dev <= 1e-9)) {
+    // (1e-9 let ~1e-10-orthogonal inverse-iteration vectors of near-degenerate pass-2
+    // Grams through, which the ALS refinement of canonical_to_tucker amplifies)
+    static const double otol_env = [] {
+      const char* e = std::getenv("LATSUM_EIG_ORTHO_TOL");
+      return e ? std::atof(e) : -1.0;
+    }();
+    const double otol = otol_env >= 0.0 ? otol_env
+                        : ortho_tol >= 0.0 ? ortho_tol
+                                           : 1e-12 * std::max(1.0, double(n) / 64.0);
+    if (!(dev <= otol)) {
       DBuf Wf(c, n);
       syevd(c, n, G0.p, Wf.p);
       k_reverse_columns<<<grid_for(n * k), 256, 0, c->stream>>>(G0.p, n, n, k, V);
       post_launch(c);
       c->eig_fallbacks++;
       custom = false;  // G0 now holds all eigenvectors: later calls take them from there
+      band = false;
       G = std::move(G0);
     }
   }
   bool has_all() const { return !custom; }
+  // max |V^T V - I| accepted from the in-house vectors before falling back to syevd
+  // (< 0: 1e-12 max(1, n/64))
+  double ortho_tol = -1.0;
 };
 
 struct Timer {
@@ -1348,6 +1473,9 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   Trace::mark(c, "gram done");
   timer.start();
   Eig e1;
+  // the RHOSVD's pass-1/pass-2 bases are re-orthonormalised and their span is what counts;
+  // the ALS unfoldings (force_deflate) need the strict eigenvector orthogonality
+  e1.ortho_tol = force_deflate ? -1.0 : 1e-9;
   e1.solve(c, n, std::move(G));
   tm.syevd += timer.stop();
   Trace::mark(c, "syevd1 done");
@@ -1369,6 +1497,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   const int64_t Nr = std::max<int64_t>(Nb, 1);
   DBuf U1, B;
   Eig e2;
+  e2.ortho_tol = e1.ortho_tol;
   bool restricted = false;  // pass 2 on the pass-1 complement Qc (needs all pass-1 vectors)
   std::vector<double> mu_d;
   bool defl = false;
@@ -1673,6 +1802,7 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
     c->sub[i] = w;
   }
   c->sub[i]->prof = c->prof;
+  c->sub[i]->eig_method = c->eig_method;
   c->sub[i]->rank = c->rank;
   c->sub[i]->nranks = c->nranks;
   return c->sub[i];
@@ -2916,6 +3046,15 @@ int latsum_canonical_to_tucker(latsum_ctx* c, const latsum_canonical* can, const
     require(can && out, "latsum_canonical_to_tucker: null argument");
     auto t = std::make_unique<latsum_tucker>();
     latsum_spectral_report rep;
+    // cuSOLVER vectors for the ALS pipeline: its fixed-rank refinements amplify the
+    // ~1e-11-level differences of the in-house inverse-iteration vectors into +-2 rank
+    // changes after shrink_core
+    struct Restore {
+      latsum_ctx* c;
+      int m;
+      ~Restore() { c->eig_method = m; }
+    } restore{c, c->eig_method};
+    c->eig_method = 1;
     canonical_to_tucker_impl(c, *can, ranks, tolerance, max_als_sweeps, als_stagnation_tol, *t,
                              rep, als_sweeps);
     if (report) *report = rep;
@@ -2989,7 +3128,7 @@ int latsum_sytrd_device(latsum_ctx* c, int64_t n, double* A, int64_t lda, double
 int latsum_eig_sym_device(latsum_ctx* c, int64_t n, const double* A, int64_t k, double* w,
                           double* V, int method) {
   return guarded(c, [&] {
-    require(A && w && n >= 1 && k >= 0 && k <= n && (k == 0 || V) && method >= 0 && method <= 2,
+    require(A && w && n >= 1 && k >= 0 && k <= n && (k == 0 || V) && method >= 0 && method <= 3,
             "latsum_eig_sym_device: bad argument");
     DBuf G(c, size_t(n) * n);
     CK(cudaMemcpyAsync(G.p, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));

@@ -92,3 +92,33 @@ def test_eigensolver_matches_lapack(ctx, n, kind):
         assert err <= 1e-12 + 64 * 2.2e-16 * scale * np.sqrt(n) / max(gap, 1e-300), (j, err, gap)
     if kind == "sym":  # well-separated random spectrum: numerically orthonormal
         assert np.max(np.abs(Vh.T @ Vh - np.eye(k))) < 1e-10
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 18, 19, 33, 40, 100, 357, 693, 816])
+@pytest.mark.parametrize("kind", ["gram", "sym"])
+def test_band_eigensolver_matches_lapack(ctx, n, kind):
+    """Two-stage solver (full -> band in one cluster, bulge chasing in shared memory,
+    inverse iteration, fused back-transform) vs numpy eigh, same bounds as above."""
+    import torch
+    from paper_1411_1994_b200 import _lib
+    A = _gram_like(n, n + 17) if kind == "gram" else _sym(n, n + 18)
+    k = max(1, n // 3)
+    dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F").copy()).cuda()
+    w = torch.zeros(n, dtype=torch.float64, device="cuda")
+    V = torch.zeros(n * k, dtype=torch.float64, device="cuda")
+    ctx.check(_lib.lib().latsum_eig_sym_device(ctx.handle, n, dA.data_ptr(), k, w.data_ptr(),
+                                               V.data_ptr(), 3))
+    lam = w.cpu().numpy()
+    Vh = V.cpu().numpy().reshape((n, k), order="F")
+    lr, vr = np.linalg.eigh(A)
+    scale = np.abs(lr).max()
+    assert np.max(np.abs(lam - lr)) <= 1e-13 * scale * max(1.0, np.sqrt(n) / 8)
+    order = np.argsort(lr)[::-1][:k]
+    for j in range(k):
+        lj = lr[order[j]]
+        gap = np.min(np.abs(np.delete(lr, order[j]) - lj)) if n > 1 else scale
+        v = vr[:, order[j]]
+        err = min(np.linalg.norm(Vh[:, j] - v), np.linalg.norm(Vh[:, j] + v))
+        assert err <= 1e-12 + 64 * 2.2e-16 * scale * np.sqrt(n) / max(gap, 1e-300), (j, err, gap)
+    if kind == "sym":
+        assert np.max(np.abs(Vh.T @ Vh - np.eye(k))) < 1e-10

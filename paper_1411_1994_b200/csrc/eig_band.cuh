@@ -40,7 +40,7 @@ constexpr int S2B_MAXC = (S2B_NMAX + S2B_CTAS - 1) / S2B_CTAS;  // owned columns
 constexpr int SB_LDB = 2 * BW + 2;     // band column stride in shared memory (bulge room)
 constexpr int SB_WARPS = 24;
 constexpr int SB_KBIG = 64;            // progress encoding: sweep * SB_KBIG + tasks done
-constexpr int SB_NMAX = 816;           // (34 n + 1024) doubles <= 227 KB
+constexpr int SB_NMAX = 808;           // 34 (n + 16) + 768 doubles <= 227 KB
 constexpr int BT_CPB = 4;              // eigenvector columns per back-transform CTA
 constexpr int BT_THREADS = 512;
 
@@ -48,9 +48,9 @@ __host__ __device__ inline int s2b_panels(int n) { return n >= 2 ? (n - 2) / BW 
 __host__ __device__ inline int sb_tasks_max(int n) { return n >= 2 ? (n - 2) / BW + 1 : 1; }
 constexpr int S2B_LDV = S2B_NMAX;      // row stride of the panel's V in shared memory
 inline size_t s2b_smem_doubles(int) {
-  return size_t(BW) * S2B_LDV + S2B_MAXC * 2 * BW + S2B_MAXC * BW + 6 * BW * BW + BW + 16 * BW;
+  return size_t(BW) * S2B_LDV + S2B_MAXC * 2 * BW + S2B_MAXC * BW + 7 * BW * BW + BW;
 }
-inline size_t sb_smem_doubles(int n) { return size_t(SB_LDB) * n + SB_WARPS * 32; }
+inline size_t sb_smem_doubles(int n) { return size_t(SB_LDB) * (n + BW) + SB_WARPS * 32; }
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -118,6 +118,18 @@ struct S2BArgs {
   long long* prof;  // optional: per-phase cycles of CTA 0 (8 slots)
 };
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Per panel (4 cluster barriers):
+//   CTA 0: panel QR (V -> Vp, S = V^T V and tau in shared memory)            | barrier 1
+//   all:   Y_own = A22[:, own]^T V (DMMA, K split over warps); P_own = V_own^T Y_own;
+//          CTA 0's warp 15 builds T meanwhile (needed only after barrier 2)    | barrier 2
+//   all:   Z = (sum_q P_q) T, M2 = T^T Z, X_own = Y_own T, W_own = X_own - 1/2 V_own M2  | barrier 3
+//   all:   A22[:, own] -= [W V] [V_own W_own]^T (DMMA, K = 2 BW)              | barrier 4
 __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int q = int(cluster.block_rank());
@@ -125,17 +137,18 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
   const int64_t lda = a.lda;
   double* __restrict__ A = a.A;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   extern __shared__ double sm[];
   double* Vs = sm;                          // BW x S2B_LDV: the panel's V, local rows, zero past m
   double* VWj = Vs + BW * S2B_LDV;          // S2B_MAXC x 2BW: (V, W) rows of the owned columns
-  double* Xs = VWj + S2B_MAXC * 2 * BW;     // S2B_MAXC x BW: X rows of the owned columns
-  double* Zp = Xs + S2B_MAXC * BW;          // BW x BW: this CTA's share of V^T X
-  double* Zf = Zp + BW * BW;                // V^T X
-  double* M2 = Zf + BW * BW;                // T^T V^T X
+  double* Ys = VWj + S2B_MAXC * 2 * BW;     // S2B_MAXC x BW: Y rows of the owned columns
+  double* Zp = Ys + S2B_MAXC * BW;          // BW x BW: this CTA's share of V^T Y
+  double* Zf = Zp + BW * BW;                // V^T A22 V T  (then reused)
+  double* M2 = Zf + BW * BW;                // T^T Z
   double* Ts = M2 + BW * BW;                // T (row-major)
   double* Ss = Ts + BW * BW;                // V^T V (upper)
   double* taus = Ss + BW * BW;              // BW
-  double* ys = taus + BW;                   // 16 warps x BW
+  double* Pf = taus + BW;                   // BW x BW: sum of the P shares
   const int npan = s2b_panels(n);
   long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tclk = clock64();
@@ -148,8 +161,10 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
   };
   for (int p = 0; p < npan; ++p) {
     const int j0 = p * BW, r0 = j0 + BW, m = n - r0;
+    const int tmax = (m + 31) / 32;
     double* Vp = a.Vw + size_t(p) * BW * n;
     double* Tp = a.Tw + size_t(p) * BW * BW;
+    for (int idx = tid; idx < S2B_MAXC * BW; idx += S2B_THREADS) Ys[idx] = 0.0;
     if (q == 0) {  // ---- panel QR: warp c owns column j0 + c, lane holds rows lane + 32t
       double x[S2B_RPL];
       const double* colp = A + int64_t(j0 + wid) * lda + r0;
@@ -159,17 +174,18 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
         x[t] = r < m ? __ldcg(colp + r) : 0.0;
       }
       mark(8);
-      // the serial chain per reflector is the owner's norm + scaling and one barrier;
-      // everything else (global stores, T) is done by all warps after the loop
+      // the serial chain per reflector is the owner's norm + scaling and one barrier; rows
+      // past m hold zeros in x and Vs, so the loops need no row predicates.  Only the
+      // columns right of the reflector read v (shared-memory bandwidth is the limit here);
+      // V^T V for T is formed after the loop.
       for (int cc = 0; cc < BW; ++cc) {
         if (wid == cc) {
           const double alpha = __shfl_sync(FULL, x[0], cc);
-          double s0 = 0.0, s1 = 0.0;
+          double s0 = (lane > cc) ? x[0] * x[0] : 0.0, s1 = 0.0;
 #pragma unroll
-          for (int t = 0; t < S2B_RPL; t += 2) {
-            const int r = lane + 32 * t;
-            if (r > cc && r < m) s0 += x[t] * x[t];
-            if (t + 1 < S2B_RPL && r + 32 < m) s1 += x[t + 1] * x[t + 1];
+          for (int t = 1; t < S2B_RPL; t += 2) {
+            if (t < tmax) s1 += x[t] * x[t];
+            if (t + 1 < S2B_RPL && t + 1 < tmax) s0 += x[t + 1] * x[t + 1];
           }
           const double ss = wsum(s0 + s1);
           double tau = 0.0, beta = alpha, scal = 0.0;
@@ -178,7 +194,6 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
             scal = 1.0 / (alpha - beta);
             tau = (beta - alpha) * (1.0 / beta);
           }
-          // rows past m hold zeros in x and in Vs: no predicates in the loops below
           double* vc = Vs + cc * S2B_LDV + lane;
           if (lane < cc) vc[0] = 0.0;
           if (lane == cc) {
@@ -191,27 +206,39 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
           }
 #pragma unroll
           for (int t = 1; t < S2B_RPL; ++t) {
-            x[t] *= scal;
-            vc[32 * t] = x[t];
+            if (t < tmax) x[t] *= scal;
+            vc[32 * t] = x[t];  // zeros past m
           }
           if (lane == 0) taus[cc] = tau;
         }
         __syncthreads();
-        if (wid != cc) {
-          const double* vc = Vs + cc * S2B_LDV + lane;  // zero above row cc and past m
+        if (wid > cc) {  // apply P_cc to column wid; v in chunks of 8 independent loads
+          const double* __restrict__ vc = Vs + cc * S2B_LDV + lane;  // zero above row cc, past m
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int t = 0; t < S2B_RPL; t += 2) {
-            s0 += vc[32 * t] * x[t];
-            if (t + 1 < S2B_RPL) s1 += vc[32 * (t + 1)] * x[t + 1];
-          }
-          const double s = wsum(s0 + s1);
-          if (wid > cc) {  // apply P_cc to column wid
-            const double f = taus[cc] * s;
+          for (int t0 = 0; t0 < S2B_RPL; t0 += 8) {
+            if (t0 < tmax) {
+              double vv[8];
 #pragma unroll
-            for (int t = 0; t < S2B_RPL; ++t) x[t] -= f * vc[32 * t];
-          } else if (lane == 0) {  // v_wid . v_cc for T
-            Ss[wid * BW + cc] = s;
+              for (int u = 0; u < 8; ++u) vv[u] = t0 + u < S2B_RPL ? vc[32 * (t0 + u)] : 0.0;
+#pragma unroll
+              for (int u = 0; u < 8; u += 2) {
+                if (t0 + u < S2B_RPL) s0 += vv[u] * x[t0 + u];
+                if (t0 + u + 1 < S2B_RPL) s1 += vv[u + 1] * x[t0 + u + 1];
+              }
+            }
+          }
+          const double f = taus[cc] * wsum(s0 + s1);
+#pragma unroll
+          for (int t0 = 0; t0 < S2B_RPL; t0 += 8) {
+            if (t0 < tmax) {
+              double vv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) vv[u] = t0 + u < S2B_RPL ? vc[32 * (t0 + u)] : 0.0;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (t0 + u < S2B_RPL) x[t0 + u] -= f * vv[u];
+            }
           }
         }
       }
@@ -222,90 +249,115 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
 #pragma unroll
         for (int t = 0; t < S2B_RPL; ++t) {
           const int r = lane + 32 * t;
-          if (r < m) {
+          if (t < tmax && r < m) {
             colw[r] = x[t];
             if (r >= wid) vg[r] = Vs[wid * S2B_LDV + r];
           }
         }
       }
       __syncthreads();
-      if (wid == 0) {  // T (LAPACK dlarft, forward / columnwise): lane i keeps row i
-        double trow[BW];
-#pragma unroll
-        for (int c = 0; c < BW; ++c) {
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int e = 0; e < c; e += 2) {
-            if (e >= lane) a0 += trow[e] * Ss[e * BW + c];
-            if (e + 1 < c && e + 1 >= lane) a1 += trow[e + 1] * Ss[(e + 1) * BW + c];
-          }
-          trow[c] = lane < c ? -taus[c] * (a0 + a1) : (lane == c ? taus[c] : 0.0);
-        }
-        if (lane < BW)
-#pragma unroll
-          for (int c = 0; c < BW; ++c) {
-            Ts[lane * BW + c] = trow[c];
-            Tp[lane + c * BW] = trow[c];  // column-major
-          }
+      // S = V^T V (upper): warp w forms the dots of v_w with v_c, c > w
+      for (int cpair = wid; cpair < BW * BW; cpair += S2B_THREADS / 32) {
+        const int ra = cpair / BW, cb = cpair % BW;
+        if (cb <= ra) continue;  // uniform per warp
+        const double* va = Vs + ra * S2B_LDV;
+        const double* vb = Vs + cb * S2B_LDV;
+        double sdot = 0.0;
+        for (int r = cb + lane; r < m; r += 32) sdot += va[r] * vb[r];
+        sdot = wsum(sdot);
+        if (lane == 0) Ss[ra * BW + cb] = sdot;
       }
       __syncthreads();
     }
     mark(0);
-    cluster.sync();  // ---- panel published (V in Vp / A, T in Tp)
+    cluster.sync();  // ---- 1: panel published (V in Vp / A)
     mark(1);
     if (q != 0) {
       for (int idx = tid; idx < BW * S2B_LDV; idx += S2B_THREADS) {
         const int c = idx / S2B_LDV, r = idx % S2B_LDV;
         Vs[idx] = r < m ? __ldcg(Vp + size_t(c) * n + r0 + r) : 0.0;
       }
-      if (tid < BW * BW) Ts[tid] = __ldcg(Tp + (tid % BW) * BW + tid / BW);
       __syncthreads();
     }
     const int cpc = (m + S2B_CTAS - 1) / S2B_CTAS;
-    const int lo = min(m, q * cpc), hi = min(m, lo + cpc);
-    // ---- Y = A22 V for the owned columns i (= rows of Y by symmetry), X = Y T
-    for (int i = lo + wid; i < hi; i += S2B_THREADS / 32) {
-      double acc[16];
+    const int lo = min(m, q * cpc), hi = min(m, lo + cpc), ncol = hi - lo;
+    if (q == 0 && wid == 15) {  // T (LAPACK dlarft, forward / columnwise): lane i keeps row i
+      double trow[BW];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = 0.0;
-      const double* acol = A + int64_t(r0 + i) * lda + r0;
-      double av[S2B_RPL];  // the whole column first: one L2 round trip, not m/32
+      for (int c = 0; c < BW; ++c) {
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int t = 0; t < S2B_RPL; ++t) {
-        const int k = lane + 32 * t;
-        av[t] = k < m ? __ldcg(acol + k) : 0.0;
+        for (int e = 0; e < c; e += 2) {
+          if (e >= lane) a0 += trow[e] * Ss[e * BW + c];
+          if (e + 1 < c && e + 1 >= lane) a1 += trow[e + 1] * Ss[(e + 1) * BW + c];
+        }
+        trow[c] = lane < c ? -taus[c] * (a0 + a1) : (lane == c ? taus[c] : 0.0);
       }
+      if (lane < BW)
 #pragma unroll
-      for (int t = 0; t < S2B_RPL; ++t) {
-        if (32 * t < m) {  // uniform; av and Vs are zero past m
+        for (int c = 0; c < BW; ++c) {
+          Ts[lane * BW + c] = trow[c];
+          Tp[lane + c * BW] = trow[c];  // column-major
+        }
+    } else if (ncol > 0) {
+      // ---- Y_own = A22[:, own]^T V: mma m8n8k4, M = owned columns (8 per tile), N = BW
+      // (two tiles), K = the m rows split over the warps
+      const int MT = (ncol + 7) / 8, KS = 15 / MT;
+      if (wid < MT * KS) {
+        const int mt = wid % MT, ks = wid / MT;
+        const int nsteps = (m + 3) / 4;
+        const int s0 = ks * nsteps / KS, s1 = (ks + 1) * nsteps / KS;
+        const int ii = mt * 8 + g;
+        const bool iok = ii < ncol;
+        const double* acol = A + int64_t(r0 + lo + (iok ? ii : 0)) * lda + r0;
+        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+        for (int st = s0; st < s1; st += 4) {
+          double af[4], b0[4], b1[4];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) acc[c] += av[t] * Vs[c * S2B_LDV + lane + 32 * t];
+          for (int u = 0; u < 4; ++u) {
+            const int k = (st + u) * 4 + t4;
+            const bool ok = st + u < s1 && k < m;
+            af[u] = (ok && iok) ? __ldcg(acol + k) : 0.0;
+            b0[u] = ok ? Vs[g * S2B_LDV + k] : 0.0;
+            b1[u] = ok ? Vs[(8 + g) * S2B_LDV + k] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            dmma884(c00, c01, af[u], b0[u]);
+            dmma884(c10, c11, af[u], b1[u]);
+          }
+        }
+        if (iok) {
+          double* yr = Ys + ii * BW + 2 * t4;
+          atomicAdd(yr, c00);
+          atomicAdd(yr + 1, c01);
+          atomicAdd(yr + 8, c10);
+          atomicAdd(yr + 9, c11);
         }
       }
-      const double y = reduce16_scatter(acc, lane);
-      if ((lane & 1) == 0) ys[wid * BW + (lane >> 1)] = y;
-      __syncwarp();
-      if (lane < BW) {
-        double xv = 0.0;
-        for (int e = 0; e <= lane; ++e) xv += ys[wid * BW + e] * Ts[e * BW + lane];
-        Xs[(i - lo) * BW + lane] = xv;
-      }
-      __syncwarp();
     }
     __syncthreads();
     mark(2);
-    if (tid < BW * BW) {  // this CTA's share of Z = V^T X
+    if (tid < BW * BW) {  // this CTA's share of P = V^T Y
       const int ra = tid / BW, cb = tid % BW;
       double z = 0.0;
-      for (int i = lo; i < hi; ++i) z += Vs[ra * S2B_LDV + i] * Xs[(i - lo) * BW + cb];
+      for (int i = 0; i < ncol; ++i) z += Vs[ra * S2B_LDV + lo + i] * Ys[i * BW + cb];
       Zp[tid] = z;
     }
-    cluster.sync();  // ---- partial Z published
+    cluster.sync();  // ---- 2: P shares and T published
     mark(3);
     if (tid < BW * BW) {
       double z = 0.0;
       for (int r = 0; r < S2B_CTAS; ++r) z += cluster.map_shared_rank(Zp, r)[tid];
-      Zf[tid] = z;
+      Pf[tid] = z;
+      if (q != 0) Ts[tid] = __ldcg(Tp + (tid % BW) * BW + tid / BW);
+    }
+    __syncthreads();
+    if (tid < BW * BW) {  // Z = P T (T upper triangular)
+      const int ra = tid / BW, cb = tid % BW;
+      double s = 0.0;
+      for (int e = 0; e <= cb; ++e) s += Pf[ra * BW + e] * Ts[e * BW + cb];
+      Zf[tid] = s;
     }
     __syncthreads();
     if (tid < BW * BW) {  // M2 = T^T Z
@@ -315,47 +367,62 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
       M2[tid] = s;
     }
     __syncthreads();
-    for (int idx = tid; idx < (hi - lo) * BW; idx += S2B_THREADS) {  // W = X - 1/2 V M2
+    for (int idx = tid; idx < ncol * BW; idx += S2B_THREADS) {  // X = Y T, W = X - 1/2 V M2
       const int ii = idx / BW, cb = idx % BW, i = lo + ii;
-      double s = 0.0;
+      double x = 0.0, s = 0.0;
 #pragma unroll
-      for (int ra = 0; ra < BW; ++ra) s += Vs[ra * S2B_LDV + i] * M2[ra * BW + cb];
-      const double w = Xs[ii * BW + cb] - 0.5 * s;
+      for (int e = 0; e < BW; ++e) {
+        x += Ys[ii * BW + e] * Ts[e * BW + cb];
+        s += Vs[e * S2B_LDV + i] * M2[e * BW + cb];
+      }
+      const double w = x - 0.5 * s;
       a.Wg[size_t(cb) * n + i] = w;
       VWj[ii * 2 * BW + cb] = Vs[cb * S2B_LDV + i];
       VWj[ii * 2 * BW + BW + cb] = w;
     }
     mark(4);
-    cluster.sync();  // ---- W published
+    cluster.sync();  // ---- 3: W published
     mark(5);
-    // ---- A22[:, j] -= W V[j,:]^T + V W[j,:]^T for the owned columns j
-    for (int i = tid; i < m; i += S2B_THREADS) {
-      double wi[BW], vi[BW];
+    // ---- A22[:, own] -= [W V] [V_own W_own]^T: mma m8n8k4, M = rows (8 per tile, one
+    // row tile per warp at a time, its A fragments reused across the owned column tiles),
+    // N = owned columns, K = 2 BW
+    if (ncol > 0) {
+      const int NT = (ncol + 7) / 8, RT = (m + 7) / 8;
+      for (int rt = wid; rt < RT; rt += S2B_THREADS / 32) {
+        const int i = rt * 8 + g;
+        const bool iok = i < m;
+        double af[8];
 #pragma unroll
-      for (int c = 0; c < BW; ++c) {
-        wi[c] = __ldcg(a.Wg + size_t(c) * n + i);
-        vi[c] = Vs[c * S2B_LDV + i];
-      }
-      for (int j8 = 0; j8 < hi - lo; j8 += 8) {  // 8 columns per L2 round trip
-        double av[8];
+        for (int u = 0; u < 4; ++u) {
+          af[u] = iok ? __ldcg(a.Wg + size_t(4 * u + t4) * n + i) : 0.0;
+          af[4 + u] = Vs[(4 * u + t4) * S2B_LDV + i];  // zero past m
+        }
+        double cold[2 * ((S2B_MAXC + 7) / 8)];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          av[u] = j8 + u < hi - lo ? __ldcg(A + int64_t(r0 + lo + j8 + u) * lda + r0 + i) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double* vw = VWj + (j8 + u) * 2 * BW;
-          double s = 0.0;
-#pragma unroll
-          for (int c = 0; c < BW; ++c) s += wi[c] * vw[c] + vi[c] * vw[BW + c];
-          av[u] -= s;
+        for (int nt = 0; nt < (S2B_MAXC + 7) / 8; ++nt) {
+          const int jc = nt * 8 + 2 * t4;
+          const double* ap = A + int64_t(r0 + lo + jc) * lda + r0 + i;
+          cold[2 * nt] = (nt < NT && iok && jc < ncol) ? __ldcg(ap) : 0.0;
+          cold[2 * nt + 1] = (nt < NT && iok && jc + 1 < ncol) ? __ldcg(ap + lda) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j8 + u < hi - lo) A[int64_t(r0 + lo + j8 + u) * lda + r0 + i] = av[u];
+        for (int nt = 0; nt < (S2B_MAXC + 7) / 8; ++nt) {
+          if (nt < NT) {
+            const int jj = nt * 8 + g;
+            const double* vw = VWj + (jj < ncol ? jj : 0) * 2 * BW + t4;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dmma884(c0, c1, af[u], jj < ncol ? vw[4 * u] : 0.0);
+            const int jc = nt * 8 + 2 * t4;
+            double* ap = A + int64_t(r0 + lo + jc) * lda + r0 + i;
+            if (iok && jc < ncol) ap[0] = cold[2 * nt] - c0;
+            if (iok && jc + 1 < ncol) ap[lda] = cold[2 * nt + 1] - c1;
+          }
+        }
       }
     }
     mark(6);
-    cluster.sync();  // ---- A22 updated
+    cluster.sync();  // ---- 4: A22 updated
     mark(7);
   }
   if (a.prof && q == 0 && tid == 0)
@@ -363,18 +430,22 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
 }
 
 // ---------------------------------------------------------------- stage 2: band -> tridiagonal
-__device__ __forceinline__ int sbi(int r, int c) { return (r - c) + c * SB_LDB; }  // r >= c
+// Band in shared memory: element (r, c), r >= c, at AB[r + 33 c] (column stride
+// SB_LDB = 34: the diagonal and 2 BW sub-diagonals, room for the bulges), zero-padded by BW
+// columns, so every task reads and writes whole 16 x 16 blocks without predicates (the
+// entries past n are zero and stay exactly zero).
+__device__ __forceinline__ int sbi(int r, int c) { return r + (SB_LDB - 1) * c; }
 
-// LAPACK dlarfg on x (lane i = lane & 15 holds x_i, i < len): v_0 = 1, H x = beta e_0.
-__device__ __forceinline__ void warp_larfg(double x, int i, int len, double& beta, double& tau,
-                                           double& v) {
+// LAPACK dlarfg on x (lane i = lane & 15 holds x_i; zeros past the vector): v_0 = 1,
+// H x = beta e_0.
+__device__ __forceinline__ void warp_larfg(double x, int i, double& beta, double& tau, double& v) {
   const double alpha = __shfl_sync(FULL, x, 0);
-  double ss = (i >= 1 && i < len) ? x * x : 0.0;
+  double ss = i >= 1 ? x * x : 0.0;
   ss += __shfl_xor_sync(FULL, ss, 8);
   ss += __shfl_xor_sync(FULL, ss, 4);
   ss += __shfl_xor_sync(FULL, ss, 2);
   ss += __shfl_xor_sync(FULL, ss, 1);
-  if (len <= 1 || ss == 0.0) {
+  if (ss == 0.0) {
     beta = alpha;
     tau = 0.0;
     v = i == 0 ? 1.0 : 0.0;
@@ -382,51 +453,56 @@ __device__ __forceinline__ void warp_larfg(double x, int i, int len, double& bet
   }
   beta = -copysign(sqrt(alpha * alpha + ss), alpha);
   tau = (beta - alpha) / beta;
-  v = i == 0 ? 1.0 : (i < len ? x * (1.0 / (alpha - beta)) : 0.0);
+  v = i == 0 ? 1.0 : x * (1.0 / (alpha - beta));
 }
 
-// D <- H D H on the symmetric diagonal block [st, st+len) of the band (LAPACK dlarfy).
-// Lane (i, h) = (lane & 15, lane >> 4) holds D[i][8h .. 8h+8); vsh: v (16, zero past len).
-__device__ __forceinline__ void sb_sym_apply(double* AB, int st, int len, double tau, double vi,
+// D <- H D H on the symmetric diagonal block [st, st+16) (LAPACK dlarfy); lane (i, h) =
+// (lane & 15, lane >> 4) holds D[i][8h .. 8h+8); vsh: v (16).
+__device__ __forceinline__ void sb_sym_apply(double* AB, int st, double tau, double vi,
                                              const double* vsh, double* wsh, int lane) {
   const int i = lane & 15, h = lane >> 4;
-  double d[8];
+  double* lo = AB + sbi(st + i, st + 8 * h);        // D[i][8h+jj] = lo[33 jj]  (8h+jj <= i)
+  const double* up = AB + sbi(st + 8 * h, st + i);  // D[i][8h+jj] = up[jj]     (8h+jj > i)
+  double d[8], vj[8];
   double t = 0.0;
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
-    const int j = 8 * h + jj;
-    double val = 0.0;
-    if (i < len && j < len) val = i >= j ? AB[sbi(st + i, st + j)] : AB[sbi(st + j, st + i)];
-    d[jj] = val;
-    t += val * vsh[j];
+    d[jj] = 8 * h + jj <= i ? lo[(SB_LDB - 1) * jj] : up[jj];
+    vj[jj] = vsh[8 * h + jj];
+    t += d[jj] * vj[jj];
   }
   t += __shfl_xor_sync(FULL, t, 16);
   double w = tau * t;
-  double s = (h == 0 && i < len) ? w * vi : 0.0;
-  s = wsum(s);
+  double s = w * vi;  // both half-warps hold the same (w_i, v_i): reduce within each
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
   w -= 0.5 * tau * s * vi;
   if (h == 0) wsh[i] = w;
   __syncwarp();
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const int j = 8 * h + jj;
-    if (i < len && j <= i) AB[sbi(st + i, st + j)] = d[jj] - vi * wsh[j] - w * vsh[j];
-  }
+  for (int jj = 0; jj < 8; ++jj)
+    if (8 * h + jj <= i) lo[(SB_LDB - 1) * jj] = d[jj] - vi * wsh[8 * h + jj] - w * vj[jj];
   __syncwarp();
 }
 
 // The band of A (lower, width BW, full storage lda) -> d (n), e (n-1); reflectors of sweep
 // s, task k: rows s+1+k BW + i, v_i at V2[s n + k BW + i] (v_0 = 1), tau at TAU2[s KS + k].
+// Task 0 of sweep s annihilates column s below the subdiagonal and applies the reflector to
+// the first diagonal block; task k >= 1 applies the previous reflector from the right to the
+// block below (creating the bulge), annihilates the bulge's first column with a new
+// reflector (applied from the left to the rest of the block) and applies it to the next
+// diagonal block (LAPACK dsb2st_kernels types 1, 2, 3).
 __global__ void __launch_bounds__(SB_WARPS * 32, 1)
 k_sb2st(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ dout,
-        double* __restrict__ eout, double* __restrict__ V2, double* __restrict__ TAU2, int KS) {
+        double* __restrict__ eout, double* __restrict__ V2, double* __restrict__ TAU2, int KS,
+        unsigned long long* prof) {
   extern __shared__ double sm[];
   double* AB = sm;
-  double* scr = AB + size_t(SB_LDB) * n;
+  double* scr = AB + size_t(SB_LDB) * (n + BW);
   __shared__ int prog_s[SB_WARPS];
   volatile int* prog = prog_s;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int idx = tid; idx < n * SB_LDB; idx += blockDim.x) {
+  for (int idx = tid; idx < (n + BW) * SB_LDB; idx += blockDim.x) {
     const int c = idx / SB_LDB, off = idx % SB_LDB, r = c + off;
     AB[idx] = (off <= BW && r < n) ? A[r + int64_t(c) * lda] : 0.0;
   }
@@ -435,13 +511,18 @@ k_sb2st(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ d
   double* vsh = scr + w * 32;
   double* wsh = vsh + 16;
   const int i = lane & 15, h = lane >> 4;
+  long long t_wait = 0, t_start = clock64(), ntask = 0;
   for (int s = w; s <= n - 3; s += SB_WARPS) {
     const int pw = (s + SB_WARPS - 1) % SB_WARPS;
     auto wait = [&](int need) {  // sweep s-1 has finished `need` tasks (or all)
       if (s == 0) return;
       const int target = (s - 1) * SB_KBIG + need;
-      if (lane == 0)
+      if (lane == 0) {
+        const long long t0 = prof ? clock64() : 0;
         while (prog[pw] < target) __nanosleep(20);
+        if (prof) t_wait += clock64() - t0;
+        ++ntask;
+      }
       __syncwarp();
       __threadfence_block();
     };
@@ -452,76 +533,208 @@ k_sb2st(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ d
         prog[w] = val;
       }
     };
-    // task 0: annihilate column s below its subdiagonal, two-sided on block 0
+    double* Vs2 = V2 + size_t(s) * n;
+    double* Ts2 = TAU2 + size_t(s) * KS;
+    // task 0
     wait(2);
     int st = s + 1;
-    int len = min(BW, n - 1 - s);
-    double x = i < len ? AB[sbi(st + i, s)] : 0.0;
-    double beta, tau, vi;
-    warp_larfg(x, i, len, beta, tau, vi);
-    if (h == 0 && i < len) AB[sbi(st + i, s)] = i == 0 ? beta : 0.0;
-    if (h == 0) {
-      vsh[i] = vi;
-      if (i < len) V2[size_t(s) * n + i] = vi;
-    }
-    if (lane == 0) TAU2[size_t(s) * KS] = tau;
-    __syncwarp();
-    sb_sym_apply(AB, st, len, tau, vi, vsh, wsh, lane);
-    int k = 1;
-    publish(s * SB_KBIG + 1);
-    int ed = st + len - 1;
-    while (ed + 1 < n) {
-      wait(k + 2);
-      const int j1 = ed + 1, j2 = min(ed + BW, n - 1), lm = j2 - j1 + 1, ln = ed - st + 1;
-      // right application of the previous reflector to B = A[j1..j2, st..ed] (the bulge)
-      double b[8];
-      double t = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * h + jj;
-        b[jj] = (i < lm && j < ln) ? AB[sbi(j1 + i, st + j)] : 0.0;
-        t += b[jj] * vsh[j];
+    {
+      double* col = AB + sbi(st + i, s);
+      double beta, tau, vi;
+      warp_larfg(*col, i, beta, tau, vi);
+      if (h == 0) {
+        *col = i == 0 ? beta : 0.0;
+        vsh[i] = vi;
+        if (st + i < n) Vs2[i] = vi;
       }
-      t += __shfl_xor_sync(FULL, t, 16);
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) b[jj] -= tau * t * vsh[8 * h + jj];
-      // new reflector from B[:, 0], applied from the left to B[:, 1:]
-      const double x0 = __shfl_sync(FULL, b[0], i);
-      double beta2, tau2, v2;
-      warp_larfg(x0, i, lm, beta2, tau2, v2);
-      if (h == 0) b[0] = i == 0 ? beta2 : 0.0;
+      if (lane == 0) Ts2[0] = tau;
       __syncwarp();
-      if (h == 0) vsh[i] = v2;
-      double pp[8];
+      sb_sym_apply(AB, st, tau, vi, vsh, wsh, lane);
+      publish(s * SB_KBIG + 1);
+      int k = 1;
+      while (st + BW < n) {
+        wait(k + 2);
+        const int j1 = st + BW;
+        double* bp = AB + sbi(j1 + i, st + 8 * h);  // B[i][8h+jj] = bp[33 jj]
+        double b[8], vj[8];
+        double t = 0.0;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) pp[jj] = (8 * h + jj >= 1) ? v2 * b[jj] : 0.0;
-      const double u = reduce8_half(pp, lane);
-      if ((lane & 1) == 0) wsh[8 * h + ((lane >> 1) & 7)] = u;
-      __syncwarp();
+        for (int jj = 0; jj < 8; ++jj) {
+          b[jj] = bp[(SB_LDB - 1) * jj];
+          vj[jj] = vsh[8 * h + jj];
+          t += b[jj] * vj[jj];
+        }
+        t += __shfl_xor_sync(FULL, t, 16);
+        const double tt = tau * t;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * h + jj;
-        if (j >= 1) b[jj] -= tau2 * v2 * wsh[j];
-        if (i < lm && j < ln) AB[sbi(j1 + i, st + j)] = b[jj];
+        for (int jj = 0; jj < 8; ++jj) b[jj] -= tt * vj[jj];
+        const double x0 = __shfl_sync(FULL, b[0], i);
+        double beta2, tau2, v2;
+        warp_larfg(x0, i, beta2, tau2, v2);
+        if (h == 0) b[0] = i == 0 ? beta2 : 0.0;
+        double pp[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) pp[jj] = (8 * h + jj >= 1) ? v2 * b[jj] : 0.0;
+        const double u = reduce8_half(pp, lane);
+        __syncwarp();  // everyone is done with the old v
+        if (h == 0) vsh[i] = v2;
+        if ((lane & 1) == 0) wsh[8 * h + ((lane >> 1) & 7)] = u;
+        __syncwarp();
+        const double tv = tau2 * v2;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (8 * h + jj >= 1) b[jj] -= tv * wsh[8 * h + jj];
+          bp[(SB_LDB - 1) * jj] = b[jj];
+        }
+        if (h == 0 && j1 + i < n) Vs2[j1 - s - 1 + i] = v2;
+        if (lane == 0) Ts2[k] = tau2;
+        __syncwarp();
+        sb_sym_apply(AB, j1, tau2, v2, vsh, wsh, lane);
+        st = j1;
+        tau = tau2;
+        ++k;
+        publish(s * SB_KBIG + k);
       }
-      if (h == 0 && i < lm) V2[size_t(s) * n + (j1 - s - 1) + i] = v2;
-      if (lane == 0) TAU2[size_t(s) * KS + k] = tau2;
-      __syncwarp();
-      sb_sym_apply(AB, j1, lm, tau2, v2, vsh, wsh, lane);
-      st = j1;
-      ed = j2;
-      tau = tau2;
-      vi = v2;
-      ++k;
-      publish(s * SB_KBIG + k);
     }
     publish((s + 1) * SB_KBIG);
   }
+  if (prof && lane == 0) {
+    atomicAdd(prof, (unsigned long long)t_wait);
+    atomicAdd(prof + 1, (unsigned long long)(clock64() - t_start));
+    atomicAdd(prof + 2, (unsigned long long)ntask);
+  }
   __syncthreads();
   for (int j = tid; j < n; j += blockDim.x) {
-    dout[j] = AB[j * SB_LDB];
-    if (j + 1 < n) eout[j] = AB[1 + j * SB_LDB];
+    dout[j] = AB[sbi(j, j)];
+    if (j + 1 < n) eout[j] = AB[sbi(j + 1, j)];
   }
+}
+
+// ---------------------------------------------------------------- tridiagonal eigenvalues
+// All eigenvalues of T = (d, e) by Sturm-count multisection, one warp per eigenvalue: each
+// lane counts at EV_PTS points, so a round narrows the bracket 65-fold.  The count is the
+// number of sign changes of the characteristic-polynomial sequence
+// p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2} (p_j / p_{j-1} = LDL^T pivot q_j, the
+// quantity LAPACK dstebz tests): two FMAs per step instead of a division, rescaled by
+// 2^+-500 before it over/underflows, an exact zero p_j counted as a negative pivot (as
+// dstebz's pivmin replacement does); the EV_PTS chains are independent (ILP).
+constexpr int EV_WARPS = 4;
+constexpr int EV_PTS = 2;
+
+__global__ void __launch_bounds__(32 * EV_WARPS)
+k_tridiag_eigvals_ms(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+                     double* __restrict__ w) {
+  extern __shared__ double sme[];
+  double* d = sme;       // n
+  double* e2 = sme + n;  // n - 1
+  __shared__ double red[3][EV_WARPS];
+  double gl = 1e308, gu = -1e308;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double dj = dg[j];
+    const double el = j > 0 ? fabs(eg[j - 1]) : 0.0, er = j + 1 < n ? fabs(eg[j]) : 0.0;
+    d[j] = dj;
+    if (j + 1 < n) e2[j] = eg[j] * eg[j];
+    gl = fmin(gl, dj - el - er);
+    gu = fmax(gu, dj + el + er);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(FULL, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(FULL, gu, o));
+  }
+  const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
+  if (lane == 0) {
+    red[0][wib] = gl;
+    red[1][wib] = gu;
+  }
+  __syncthreads();
+  gl = red[0][0];
+  gu = red[1][0];
+  for (int q = 1; q < EV_WARPS; ++q) {
+    gl = fmin(gl, red[0][q]);
+    gu = fmax(gu, red[1][q]);
+  }
+  const double eps = 2.220446049250313e-16;
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  gl -= 2.0 * eps * tnorm * n + 1e-300;
+  gu += 2.0 * eps * tnorm * n + 1e-300;
+  const int i = blockIdx.x * EV_WARPS + wib;  // eigenvalue index (ascending)
+  if (i >= n) return;
+  double lo = gl, hi = gu;
+  const double atol = 2.0 * eps * tnorm + 1e-300;
+  constexpr double BIG = 0x1p500, SMALL = 0x1p-500;
+  for (int round = 0; round < 24; ++round) {
+    const double width = hi - lo;
+    if (width <= fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), atol)) break;
+    double x[EV_PTS], p0[EV_PTS], p1[EV_PTS];
+    int cnt[EV_PTS];
+#pragma unroll
+    for (int q = 0; q < EV_PTS; ++q) {
+      x[q] = lo + width * double(lane * EV_PTS + q + 1) * (1.0 / (32 * EV_PTS + 1));
+      p0[q] = 1.0;
+      p1[q] = d[0] - x[q];
+      if (p1[q] == 0.0) p1[q] = -0x1p-60;
+      cnt[q] = p1[q] < 0.0;
+    }
+    // steps in groups of 4 (one rescale per group: |p| grows by < (3 ||T||)^4 per group)
+    auto step = [&](int j) {
+      const double dj = d[j], ej = e2[j - 1];
+#pragma unroll
+      for (int q = 0; q < EV_PTS; ++q) {
+        const double t = ej * p0[q];
+        double pn = fma(dj - x[q], p1[q], -t);
+        pn = pn == 0.0 ? -p1[q] * 0x1p-60 : pn;
+        cnt[q] += (pn < 0.0) != (p1[q] < 0.0);
+        p0[q] = p1[q];
+        p1[q] = pn;
+      }
+    };
+    int j = 1;
+    for (; j + 3 < n; j += 4) {
+      step(j);
+      step(j + 1);
+      step(j + 2);
+      step(j + 3);
+#pragma unroll
+      for (int q = 0; q < EV_PTS; ++q) {
+        const double a = fmax(fabs(p1[q]), fabs(p0[q]));
+        const double sc = a > BIG ? SMALL : (a < SMALL ? BIG : 1.0);
+        p0[q] *= sc;
+        p1[q] *= sc;
+      }
+    }
+    for (; j < n; ++j) step(j);
+    // first point (lane-major) whose count exceeds i: eigenvalue i lies below it
+    int f = EV_PTS;
+#pragma unroll
+    for (int q = EV_PTS - 1; q >= 0; --q)
+      if (cnt[q] > i) f = q;
+    const unsigned any = __ballot_sync(FULL, f < EV_PTS);
+    double nlo = lo, nhi = hi;
+    if (any) {
+      const int L = __ffs(any) - 1;
+      const int fl = __shfl_sync(FULL, f, L);
+      const int idx = L * EV_PTS + fl;
+      double xs = x[0];
+#pragma unroll
+      for (int q = 1; q < EV_PTS; ++q)
+        if (fl == q) xs = x[q];
+      nhi = __shfl_sync(FULL, xs, L);
+      if (idx > 0) {
+        const int pl = (idx - 1) / EV_PTS, pq = (idx - 1) % EV_PTS;
+        double xp = x[0];
+#pragma unroll
+        for (int q = 1; q < EV_PTS; ++q)
+          if (pq == q) xp = x[q];
+        nlo = __shfl_sync(FULL, xp, pl);
+      }
+    } else {
+      nlo = __shfl_sync(FULL, x[EV_PTS - 1], 31);
+    }
+    if (nlo == lo && nhi == hi) break;  // no representable progress
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) w[i] = 0.5 * (lo + hi);
 }
 
 // ---------------------------------------------------------------- inverse iteration

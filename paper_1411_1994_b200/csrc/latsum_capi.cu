@@ -795,7 +795,8 @@ struct Eig {
         long long h[12];
         CK(cudaMemcpyAsync(h, pb.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        fprintf(stderr, "[sy2sb qr split] loads %.1f columns %.1f\n", h[8] / 1e3 / npan, h[9] / 1e3 / npan);
+        fprintf(stderr, "[sy2sb qr split] loads %.1f columns %.1f (warp 0: barrier wait %.1f, own work %.1f)\n",
+                h[8] / 1e3 / npan, h[9] / 1e3 / npan, h[10] / 1e3 / npan, h[11] / 1e3 / npan);
         fprintf(stderr, "[sy2sb n=%d] kcycles/panel: qr %.1f bar1 %.1f Y %.1f bar2 %.1f ZW %.1f bar3 %.1f U3 %.1f bar4 %.1f\n",
                 ni, h[0] / 1e3 / npan, h[1] / 1e3 / npan, h[2] / 1e3 / npan, h[3] / 1e3 / npan,
                 h[4] / 1e3 / npan, h[5] / 1e3 / npan, h[6] / 1e3 / npan, h[7] / 1e3 / npan);
@@ -806,9 +807,22 @@ struct Eig {
       static std::once_flag once;
       std::call_once(once, [&] { set_smem_attr(band::k_sb2st, band::sb_smem_doubles(band::SB_NMAX) * 8); });
       ProfScope ps(c, "eig_sb2st", double(n) * double(n));
-      band::k_sb2st<<<1, band::SB_WARPS * 32, smem, c->stream>>>(G.p, n, ni, d.p, e.p, V2.p,
-                                                                  TAU2.p, KS);
+      static const bool sprof = std::getenv("LATSUM_SB2ST_PROF") != nullptr;
+      DBuf pb(c, 4);
+      if (sprof) CK(cudaMemsetAsync(pb.p, 0, 32, c->stream));
+      band::k_sb2st<<<1, band::SB_WARPS * 32, smem, c->stream>>>(
+          G.p, n, ni, d.p, e.p, V2.p, TAU2.p, KS,
+          sprof ? reinterpret_cast<unsigned long long*>(pb.p) : nullptr);
       post_launch(c);
+      if (sprof) {
+        unsigned long long h[3];
+        CK(cudaMemcpyAsync(h, pb.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        fprintf(stderr, "[sb2st n=%d] tasks %llu, per warp: loop %.1f kcycles, wait %.1f kcycles; "
+                "cycles/task (loop sum / tasks) %.0f, non-wait %.0f\n", ni, h[2],
+                h[1] / 1e3 / band::SB_WARPS, h[0] / 1e3 / band::SB_WARPS, double(h[1]) / h[2],
+                double(h[1] - h[0]) / h[2]);
+      }
     }
   }
 
@@ -842,14 +856,12 @@ struct Eig {
       else sytrd_cluster(c, n, G.p, n, d.p, e.p, tau.p);
       ProfScope ps(c, "eig_values", double(n));
       const size_t smem = size_t(2 * n) * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(eig::k_tridiag_eigvals, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(2 * kCustomEigMax * sizeof(double))));
-        attr = true;
-      }
-      eig::k_tridiag_eigvals<<<unsigned((n + eig::EIG_WARPS - 1) / eig::EIG_WARPS), 32 * eig::EIG_WARPS,
-                               smem, c->stream>>>(d.p, e.p, int(n), W.p);
+      static std::once_flag once;
+      std::call_once(once, [&] {
+        set_smem_attr(band::k_tridiag_eigvals_ms, size_t(2 * kCustomEigMax) * sizeof(double));
+      });
+      band::k_tridiag_eigvals_ms<<<unsigned((n + band::EV_WARPS - 1) / band::EV_WARPS),
+                                   32 * band::EV_WARPS, smem, c->stream>>>(d.p, e.p, int(n), W.p);
       post_launch(c);
     }
     CK(cudaMemcpyAsync(lam_asc.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));

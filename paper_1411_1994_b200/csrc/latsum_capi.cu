@@ -19,6 +19,7 @@
 #include <stdexcept>
 #include <exception>
 #include <fstream>
+#include <future>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -1034,7 +1035,34 @@ struct latsum_canonical {
   std::vector<int32_t> stc[3][3];
   std::vector<double> stw[3];
   std::vector<int64_t> sseg[3];
+  // assemble() merges the terms (everything above from tc on) on a host thread that runs
+  // while the RHOSVD's Grams and eigensolves are on the device; terms() joins it and
+  // uploads dtc/dtw/dtseg.  Declared last: destroyed (joined) before the vectors it fills.
+  bool terms_async = false, terms_uploaded = false;
+  std::mutex terms_mu;
+  std::shared_future<void> terms_ready;
 };
+
+// The merged terms of `cc` on the host (terms_host) or also on the device (terms).
+const latsum_canonical& terms_host(const latsum_canonical& cc) {
+  auto& can = const_cast<latsum_canonical&>(cc);
+  if (can.terms_async) can.terms_ready.get();
+  return cc;
+}
+
+const latsum_canonical& terms(latsum_ctx* c, const latsum_canonical& cc) {
+  auto& can = const_cast<latsum_canonical&>(cc);
+  if (!can.terms_async) return cc;
+  std::lock_guard<std::mutex> g(can.terms_mu);
+  if (can.terms_uploaded) return cc;
+  can.terms_ready.get();
+  for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
+  can.dtw.upload(c, can.tw);
+  can.dtseg.upload(c, can.tseg);
+  CK(cudaStreamSynchronize(c->stream));  // later users may sit on other streams
+  can.terms_uploaded = true;
+  return cc;
+}
 
 struct latsum_tucker {
   int64_t N[3] = {0, 0, 0};
@@ -1152,6 +1180,58 @@ void build_reference(latsum_ctx* c, int family, double lambda, const int64_t N[3
 }
 
 // ------------------------------------------------------------------ stage 2
+// Merge identical rank-1 terms and build the per-mode sorted orders (host only; runs on
+// a host thread started by assemble(), see latsum_canonical::terms_ready).
+void merge_terms(latsum_canonical& can) {
+  // merge identical rank-1 terms (same column in all three modes)
+  // (key = c0:c1:c2 packed in 21-bit fields, q); stable order keeps the reference's
+  // term order inside each merged group, so merged weights add in add_concat order
+  // stable LSD counting sort over (c2, c1, c0): O(M_c) instead of a comparison sort
+  std::vector<std::pair<uint64_t, int64_t>> keys(can.Mc), tmp(can.Mc);
+  for (int64_t q = 0; q < can.Mc; ++q)
+    keys[q] = {(uint64_t(can.term_col[0][q]) << 42) | (uint64_t(can.term_col[1][q]) << 21) |
+                   uint64_t(can.term_col[2][q]),
+               q};
+  for (int pass = 0; pass < 3; ++pass) {
+    const int l = 2 - pass, shift = 21 * pass;
+    std::vector<int64_t> cnt(can.d[l] + 1, 0);
+    for (const auto& kq : keys) cnt[((kq.first >> shift) & 0x1FFFFF) + 1]++;
+    for (int64_t a = 0; a < can.d[l]; ++a) cnt[a + 1] += cnt[a];
+    for (const auto& kq : keys) tmp[cnt[(kq.first >> shift) & 0x1FFFFF]++] = kq;
+    keys.swap(tmp);
+  }
+  for (int l = 0; l < 3; ++l) can.tc[l].clear();
+  can.tw.clear();
+  can.tseg.assign(can.d[0] + 1, 0);
+  for (size_t i = 0; i < keys.size();) {  // sorted by c0, then c1, c2
+    const uint64_t key = keys[i].first;
+    double w = 0.0;
+    for (; i < keys.size() && keys[i].first == key; ++i) w += can.weights[keys[i].second];
+    const int64_t c0 = int64_t(key >> 42), c1 = int64_t((key >> 21) & 0x1FFFFF),
+                  c2 = int64_t(key & 0x1FFFFF);
+    can.tc[0].push_back(int32_t(c0));
+    can.tc[1].push_back(int32_t(c1));
+    can.tc[2].push_back(int32_t(c2));
+    can.tw.push_back(w);
+    can.tseg[c0 + 1] += 1;
+  }
+  can.T = int64_t(can.tw.size());
+  for (int64_t a = 0; a < can.d[0]; ++a) can.tseg[a + 1] += can.tseg[a];
+  for (int m = 0; m < 3; ++m) {  // counting sort by c_m (stable: keeps the c0-major order)
+    can.sseg[m].assign(can.d[m] + 1, 0);
+    for (int64_t t = 0; t < can.T; ++t) can.sseg[m][can.tc[m][t] + 1] += 1;
+    for (int64_t a = 0; a < can.d[m]; ++a) can.sseg[m][a + 1] += can.sseg[m][a];
+    std::vector<int64_t> pos(can.sseg[m].begin(), can.sseg[m].end() - 1);
+    for (int l = 0; l < 3; ++l) can.stc[m][l].assign(can.T, 0);
+    can.stw[m].assign(can.T, 0.0);
+    for (int64_t t = 0; t < can.T; ++t) {
+      const int64_t q = pos[can.tc[m][t]]++;
+      for (int l = 0; l < 3; ++l) can.stc[m][l][q] = can.tc[l][t];
+      can.stw[m][q] = can.tw[t];
+    }
+  }
+}
+
 void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const int64_t* sub_counts,
               const int64_t* sub_shifts, const double* sub_charges, int64_t ndef,
               const int64_t* def_shifts, const double* def_charges, latsum_canonical& can) {
@@ -1166,6 +1246,7 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
 
   // per-mode placements: sublattices first, then distinct defect shifts
   std::vector<int64_t> block_pl[3];
+  DBuf norm_buf[3];
   std::vector<int64_t> sub_off(size_t(nsub) * 3 + 1, 0);
   {
     int64_t o = 0;
@@ -1217,7 +1298,9 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     can.dict[l].alloc(c, size_t(N) * can.d[l]);
     const int64_t chunk = 2048;
     const int nchunk = int((N + chunk - 1) / chunk);
-    DBuf partial(c, size_t(can.d[l]) * nchunk), norms(c, can.d[l]);
+    DBuf partial(c, size_t(can.d[l]) * nchunk);
+    DBuf& norms = norm_buf[l];
+    norms.alloc(c, can.d[l]);
     DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
     dim3 g(unsigned(can.d[l]), unsigned(nchunk));
     ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
@@ -1227,11 +1310,14 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     post_launch(c);
     k_dict_write<<<g, 256, 0, c->stream>>>(a);
     post_launch(c);
-    can.dict_norms[l].resize(can.d[l]);
-    CK(cudaMemcpyAsync(can.dict_norms[l].data(), norms.p, sizeof(double) * can.d[l],
-                       cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
   }
+  for (int l = 0; l < 3; ++l) {  // the three modes' kernels are queued before the first wait
+    can.dict_norms[l].resize(can.d[l]);
+    if (can.d[l])
+      CK(cudaMemcpyAsync(can.dict_norms[l].data(), norm_buf[l].p, sizeof(double) * can.d[l],
+                         cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
 
   Trace::mark(c, "assemble: dictionaries done", false);
   // terms in reference order (add_concat: sublattice blocks, then defects)
@@ -1257,61 +1343,10 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     }
   }
   Trace::mark(c, "assemble: terms done", false);
-  // merge identical rank-1 terms (same column in all three modes)
-  // (key = c0:c1:c2 packed in 21-bit fields, q); stable order keeps the reference's
-  // term order inside each merged group, so merged weights add in add_concat order
   for (int l = 0; l < 3; ++l)
     require(can.d[l] < (int64_t(1) << 21), "assemble: too many distinct columns in a mode");
-  // stable LSD counting sort over (c2, c1, c0): O(M_c) instead of a comparison sort
-  std::vector<std::pair<uint64_t, int64_t>> keys(can.Mc), tmp(can.Mc);
-  for (int64_t q = 0; q < can.Mc; ++q)
-    keys[q] = {(uint64_t(can.term_col[0][q]) << 42) | (uint64_t(can.term_col[1][q]) << 21) |
-                   uint64_t(can.term_col[2][q]),
-               q};
-  for (int pass = 0; pass < 3; ++pass) {
-    const int l = 2 - pass, shift = 21 * pass;
-    std::vector<int64_t> cnt(can.d[l] + 1, 0);
-    for (const auto& kq : keys) cnt[((kq.first >> shift) & 0x1FFFFF) + 1]++;
-    for (int64_t a = 0; a < can.d[l]; ++a) cnt[a + 1] += cnt[a];
-    for (const auto& kq : keys) tmp[cnt[(kq.first >> shift) & 0x1FFFFF]++] = kq;
-    keys.swap(tmp);
-  }
-  for (int l = 0; l < 3; ++l) can.tc[l].clear();
-  can.tw.clear();
-  can.tseg.assign(can.d[0] + 1, 0);
-  for (size_t i = 0; i < keys.size();) {  // sorted by c0, then c1, c2
-    const uint64_t key = keys[i].first;
-    double w = 0.0;
-    for (; i < keys.size() && keys[i].first == key; ++i) w += can.weights[keys[i].second];
-    const int64_t c0 = int64_t(key >> 42), c1 = int64_t((key >> 21) & 0x1FFFFF),
-                  c2 = int64_t(key & 0x1FFFFF);
-    can.tc[0].push_back(int32_t(c0));
-    can.tc[1].push_back(int32_t(c1));
-    can.tc[2].push_back(int32_t(c2));
-    can.tw.push_back(w);
-    can.tseg[c0 + 1] += 1;
-  }
-  can.T = int64_t(can.tw.size());
-  for (int64_t a = 0; a < can.d[0]; ++a) can.tseg[a + 1] += can.tseg[a];
-  Trace::mark(c, "assemble: merge done", false);
-  for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
-  can.dtw.upload(c, can.tw);
-  can.dtseg.upload(c, can.tseg);
-  Trace::mark(c, "assemble: uploads done", false);
-  Trace::mark(c, "assemble: sorted orders start", false);
-  for (int m = 0; m < 3; ++m) {  // counting sort by c_m (stable: keeps the c0-major order)
-    can.sseg[m].assign(can.d[m] + 1, 0);
-    for (int64_t t = 0; t < can.T; ++t) can.sseg[m][can.tc[m][t] + 1] += 1;
-    for (int64_t a = 0; a < can.d[m]; ++a) can.sseg[m][a + 1] += can.sseg[m][a];
-    std::vector<int64_t> pos(can.sseg[m].begin(), can.sseg[m].end() - 1);
-    for (int l = 0; l < 3; ++l) can.stc[m][l].assign(can.T, 0);
-    can.stw[m].assign(can.T, 0.0);
-    for (int64_t t = 0; t < can.T; ++t) {
-      const int64_t q = pos[can.tc[m][t]]++;
-      for (int l = 0; l < 3; ++l) can.stc[m][l][q] = can.tc[l][t];
-      can.stw[m][q] = can.tw[t];
-    }
-  }
+  can.terms_async = true;
+  can.terms_ready = std::async(std::launch::async, [&can] { merge_terms(can); }).share();
 }
 
 void materialize_factor(latsum_ctx* c, const latsum_canonical& can, int l, double* dst_device) {
@@ -1675,6 +1710,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
 // projected_norm (rank_reduction.hpp:104-113).
 double hadamard_norm(latsum_ctx* c, const latsum_canonical& can, const double* const E[3],
                      const int64_t rows[3]) {
+  terms(c, can);
   if (can.T == 0) return 0.0;
   DBuf G[3];
   for (int l = 0; l < 3; ++l) {
@@ -1756,6 +1792,7 @@ int core_mode(const latsum_canonical& can) {
 // loop's 2 r1 r2 r3 M_c.  [a_lo, a_hi) restricts j (the rank's share when sharded).
 void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
                double* core, int m, int64_t a_lo = 0, int64_t a_hi = -1) {
+  terms(c, can);
   const int64_t T = can.T, dm = a_hi < 0 ? can.d[m] : a_hi;
   const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
   const int64_t ro = r[o1] * r[o2];
@@ -1884,7 +1921,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   // the three mode reductions and norm_f are independent: one worker stream each
   ModeOut mo[3];
   Timings tms[4];
-  const bool zero_terms = can.Mc == 0 || can.T == 0;
+  const bool zero_terms = can.Mc == 0;  // T == 0 iff M_c == 0 (every term is kept, merged)
   static const bool serial = std::getenv("LATSUM_SERIAL") != nullptr;  // A/B switch
   auto body = [&](latsum_ctx* w, int i) {
     if (i == 3 || zero_terms) {
@@ -1962,7 +1999,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       }
       mo[l].Z = std::move(full);
     }
-    t.tc[l].upload(c, can.tc[l]);
+    t.tc[l].upload(c, terms_host(can).tc[l]);
   }
   t.tw.upload(c, can.tw);
   t.tseg.upload(c, can.tseg);
@@ -2041,6 +2078,7 @@ void project_factors(latsum_ctx* c, const latsum_canonical& can, const DBuf Y[3]
 // trailing kept directions carry relative mass ~eps^2, which a single Gram cannot resolve.
 void als_mode_update(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3],
                      const int64_t r[3], int l, DBuf& Y) {
+  terms(c, can);
   const int64_t N = can.N[l], d = can.d[l];
   GroupedTerms gt(c, can, P, r, l);
   const int64_t R2 = r[gt.o1] * r[gt.o2];
@@ -2153,6 +2191,7 @@ void shrink_core(latsum_ctx* c, latsum_tucker& t, double budget2) {
 void canonical_to_tucker_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks,
                               double tol, int max_sweeps, double stag_tol, latsum_tucker& t,
                               latsum_spectral_report& rep, int* sweeps_done) {
+  terms(c, can);
   rhosvd_impl(c, can, ranks, tol, LATSUM_DEFLATE_AUTO, t, rep, /*form=*/false);
   if (sweeps_done) *sweeps_done = 0;
   if (rep.input_norm == 0.0) {
@@ -2431,6 +2470,7 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
 
 void canonical_eval(latsum_ctx* c, const latsum_canonical& can, const int64_t lo[3],
                     const int64_t hi[3], double* out) {
+  terms(c, can);
   check_box(can.N, lo, hi);
   const double* D[3] = {can.dict[0].p + lo[0], can.dict[1].p + lo[1], can.dict[2].p + lo[2]};
   const int32_t* tc[3] = {can.dtc[0].p, can.dtc[1].p, can.dtc[2].p};
@@ -2726,7 +2766,7 @@ int latsum_canonical_info(const latsum_canonical* can, int64_t dims[3], int64_t*
     if (dict_cols) dict_cols[l] = can->d[l];
   }
   if (rank) *rank = can->Mc;
-  if (merged_terms) *merged_terms = can->T;
+  if (merged_terms) *merged_terms = terms_host(*can).T;
   return LATSUM_OK;
 }
 
@@ -2763,6 +2803,7 @@ int latsum_canonical_entries(latsum_ctx* c, const latsum_canonical* can, const i
       for (int l = 0; l < 3; ++l)
         if (probes[3 * p + l] < 0 || probes[3 * p + l] >= can->N[l])
           throw Error(LATSUM_ERR_INVALID_ARGUMENT, "CanonicalTensor::entry index out of range");
+    terms(c, *can);
     if (can->T == 0) {
       std::fill(out, out + np, 0.0);
       return;

@@ -429,6 +429,17 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
     for (int i = 0; i < 12; ++i) a.prof[i] = ph[i];
 }
 
+// Progress flags between the sweep warps (shared memory, CTA scope): release / acquire
+// instead of a sequentially consistent fence on both sides of every task.
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(v) : "memory");
+}
+
 // ---------------------------------------------------------------- stage 2: band -> tridiagonal
 // Band in shared memory: element (r, c), r >= c, at AB[r + 33 c] (column stride
 // SB_LDB = 34: the diagonal and 2 BW sub-diagonals, room for the bulges), zero-padded by BW
@@ -519,19 +530,15 @@ k_sb2st(const double* __restrict__ A, int64_t lda, int n, double* __restrict__ d
       const int target = (s - 1) * SB_KBIG + need;
       if (lane == 0) {
         const long long t0 = prof ? clock64() : 0;
-        while (prog[pw] < target) __nanosleep(20);
+        while (ld_acquire_cta(prog_s + pw) < target) __nanosleep(20);
         if (prof) t_wait += clock64() - t0;
         ++ntask;
       }
-      __syncwarp();
-      __threadfence_block();
+      __syncwarp();  // lane 0's acquire + the warp barrier order the other lanes' reads
     };
     auto publish = [&](int val) {
       __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        prog[w] = val;
-      }
+      if (lane == 0) st_release_cta(prog_s + w, val);  // after the warp barrier: all lanes' writes
     };
     double* Vs2 = V2 + size_t(s) * n;
     double* Ts2 = TAU2 + size_t(s) * KS;

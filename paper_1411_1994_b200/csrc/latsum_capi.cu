@@ -796,7 +796,7 @@ struct Eig {
         long long h[12];
         CK(cudaMemcpyAsync(h, pb.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        fprintf(stderr, "[sy2sb qr split] loads %.1f columns %.1f (warp 0: barrier wait %.1f, own work %.1f)\n",
+        fprintf(stderr, "[sy2sb qr split] loads %.1f columns %.1f writeback+S %.1f (slot 11 %.1f); qr below = T + rest\n",
                 h[8] / 1e3 / npan, h[9] / 1e3 / npan, h[10] / 1e3 / npan, h[11] / 1e3 / npan);
         fprintf(stderr, "[sy2sb n=%d] kcycles/panel: qr %.1f bar1 %.1f Y %.1f bar2 %.1f ZW %.1f bar3 %.1f U3 %.1f bar4 %.1f\n",
                 ni, h[0] / 1e3 / npan, h[1] / 1e3 / npan, h[2] / 1e3 / npan, h[3] / 1e3 / npan,
@@ -2406,7 +2406,7 @@ void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3
     if (oz) {
       OzSliced sY;  // lines = the (j, k) columns of V, K = d0
       oz_slice_b(c, Y.p, 1, nj * nkk, nj * nkk, d0, sY);
-      oz_run(c, sD0, sY, oz_out(out + k0 * ni * nj, ni), tag);
+      oz_run(c, sD0, sY, oz_out(out + k0 * ni * nj, ni), ozaki_tag(tag));
     } else {
       gemm(c, false, true, ni, nj * nkk, d0, 1.0, D[0], ld[0], Y.p, nj * nkk, 0.0,
            out + k0 * ni * nj, ni, tagged(tag));

@@ -2421,24 +2421,37 @@ void cp_eval(latsum_ctx* c, const double* const D[3], const int64_t ld[3], const
     CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
     return;
   }
-  if (T <= CP_MAXT) {  // low rank (cfg1: 17 merged terms): output-write bound kernel
+  static const bool cp_gemm = std::getenv("LATSUM_CP_GEMM") != nullptr;  // A/B: slab GEMMs
+  if (T <= CP_MAXT && !cp_gemm) {  // low rank (cfg1: 17 merged terms): output-write bound kernel
     ProfScope ps(c, "cp_eval_small", 8.0 * double(ni) * double(nj) * double(nk));
     const int64_t pairs = nj * nk;
-    auto grid_of = [&](int ipt) {
+    auto grid_of = [&](int ipt, int minb) {
       const unsigned gx = unsigned((ni + CP_THREADS * ipt - 1) / (CP_THREADS * ipt));
       const unsigned gy = unsigned(std::max<int64_t>(1, std::min<int64_t>(
-          (pairs + CP_PAIRS - 1) / CP_PAIRS, std::max<int64_t>(1, 148 * 8 / int64_t(gx)))));
+          (pairs + CP_PAIRS - 1) / CP_PAIRS, std::max<int64_t>(1, 148 * minb / int64_t(gx)))));
       return dim3(gx, gy);
     };
 #define LATSUM_CP(MT)                                                                         \
-  k_cp_eval_small<MT><<<grid_of(cp_ipt<MT>()), CP_THREADS, 0, c->stream>>>(                   \
+  k_cp_eval_small<MT><<<grid_of(cp_ipt<MT>(), cp_minb<MT>()), CP_THREADS, 0, c->stream>>>(                   \
       D[0], ld[0], D[1], ld[1], D[2], ld[2], tc[0], tc[1], tc[2], tw, int(T), ni, nj, nk, out)
-    if (T <= 8) LATSUM_CP(8);
-    else if (T <= 16) LATSUM_CP(16);
-    else if (T <= 24) LATSUM_CP(24);
-    else if (T <= 32) LATSUM_CP(32);
-    else if (T <= 48) LATSUM_CP(48);
-    else LATSUM_CP(64);
+    switch ((T + 1) / 2 * 2) {  // rank buckets: even T up to 24, then 32 / 48 / 64
+      case 2: LATSUM_CP(2); break;
+      case 4: LATSUM_CP(4); break;
+      case 6: LATSUM_CP(6); break;
+      case 8: LATSUM_CP(8); break;
+      case 10: LATSUM_CP(10); break;
+      case 12: LATSUM_CP(12); break;
+      case 14: LATSUM_CP(14); break;
+      case 16: LATSUM_CP(16); break;
+      case 18: LATSUM_CP(18); break;
+      case 20: LATSUM_CP(20); break;
+      case 22: LATSUM_CP(22); break;
+      case 24: LATSUM_CP(24); break;
+      default:
+        if (T <= 32) LATSUM_CP(32);
+        else if (T <= 48) LATSUM_CP(48);
+        else LATSUM_CP(64);
+    }
 #undef LATSUM_CP
     post_launch(c);
     return;

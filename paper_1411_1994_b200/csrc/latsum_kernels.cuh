@@ -504,22 +504,29 @@ __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restr
 namespace latsum_b200 {
 
 // Low-rank canonical evaluation on a box (canonical.hpp:192-202 to_dense) for T <= 64
-// merged terms, output-write bound: each thread keeps A0[i, :] = D0[i, c0_t] for CP_IPT
-// rows in registers (zero-padded to the rank bucket MAXT), the block stages
-// x_t(j,k) = w_t D1[j, c1_t] D2[k, c2_t] for CP_PAIRS (j,k) pairs in shared memory, and
-// every staged value feeds CP_IPT FMAs; stores are coalesced along i.
+// merged terms, output-write bound (2 T flops per 8-byte point sits below the FP64 ridge):
+// each thread keeps A0[i, :] = D0[i, c0_t] for cp_ipt rows in registers (zero-padded to
+// the rank bucket MAXT: T rounded up to even below 24, so at most one FMA per point is
+// padding), the block stages x_t(j,k) = w_t D1[j, c1_t] D2[k, c2_t] for CP_PAIRS (j,k)
+// pairs in shared memory, double-buffered so the next batch's gathers overlap this batch's
+// FMAs and stores; x is read as 16-byte pairs (one shared load per 2 cp_ipt FMAs); stores
+// are coalesced along i.  Registers stay <= 128 (4 CTAs per SM; 2 for the 48 and 64 buckets) to keep
+// stores in flight.
 constexpr int CP_MAXT = 64, CP_PAIRS = 32, CP_THREADS = 128;
 template <int MAXT>
-constexpr int cp_ipt() { return MAXT <= 24 ? 4 : (MAXT <= 32 ? 2 : 1); }
+constexpr int cp_ipt() { return MAXT <= 18 ? 4 : (MAXT <= 24 ? 2 : 1); }
 template <int MAXT>
-__global__ void __launch_bounds__(CP_THREADS)
+constexpr int cp_minb() { return (MAXT <= 18 || MAXT > 32) ? 2 : (MAXT <= 24 ? 3 : 4); }
+template <int MAXT>
+__global__ void __launch_bounds__(CP_THREADS, cp_minb<MAXT>())
 k_cp_eval_small(const double* __restrict__ D0, int64_t ld0, const double* __restrict__ D1,
                 int64_t ld1, const double* __restrict__ D2, int64_t ld2,
                 const int32_t* __restrict__ c0, const int32_t* __restrict__ c1,
                 const int32_t* __restrict__ c2, const double* __restrict__ w, int T, int64_t ni,
                 int64_t nj, int64_t nk, double* __restrict__ out) {
+  static_assert(MAXT % 2 == 0, "x is read in pairs");
   constexpr int CP_IPT = cp_ipt<MAXT>();
-  __shared__ double xs[CP_PAIRS][MAXT];
+  __shared__ __align__(16) double xs[2][CP_PAIRS][MAXT];
   const int64_t ibase = blockIdx.x * int64_t(CP_THREADS * CP_IPT) + threadIdx.x;
   double a[CP_IPT][MAXT];
 #pragma unroll
@@ -528,30 +535,69 @@ k_cp_eval_small(const double* __restrict__ D0, int64_t ld0, const double* __rest
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) a[u][t] = (t < T && i < ni) ? D0[i + int64_t(c0[t]) * ld0] : 0.0;
   }
-  const int64_t npairs = nj * nk;
-  for (int64_t p0 = int64_t(blockIdx.y) * CP_PAIRS; p0 < npairs; p0 += int64_t(gridDim.y) * CP_PAIRS) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < CP_PAIRS * MAXT; e += CP_THREADS) {
+  const int64_t npairs = nj * nk, stride = int64_t(gridDim.y) * CP_PAIRS;
+  // the term table (weight, mode-1 and mode-2 columns) in shared memory, loaded once
+  __shared__ double ws[MAXT];
+  __shared__ int c1s[MAXT], c2s[MAXT];
+  for (int t = threadIdx.x; t < MAXT; t += CP_THREADS) {
+    ws[t] = t < T ? w[t] : 0.0;
+    c1s[t] = t < T ? c1[t] : 0;
+    c2s[t] = t < T ? c2[t] : 0;
+  }
+  __syncthreads();
+  // staging is software-pipelined: the next batch's factor entries are loaded into
+  // registers before this batch's FMAs and written to shared memory after them, so the L2
+  // latency of the gathers overlaps the compute and the stores
+  constexpr int NSLOT = (CP_PAIRS * MAXT + CP_THREADS - 1) / CP_THREADS;
+  double g1[NSLOT], g2[NSLOT];
+  auto gather = [&](int64_t p0) {
+    const int64_t j0 = p0 % nj, k0 = p0 / nj;  // one division per batch
+#pragma unroll
+    for (int m = 0; m < NSLOT; ++m) {
+      const int e = threadIdx.x + m * CP_THREADS;
       const int q = e / MAXT, t = e % MAXT;
-      const int64_t p = p0 + q;
-      double v = 0.0;
-      if (p < npairs && t < T) {
-        const int64_t j = p % nj, k = p / nj;
-        v = w[t] * D2[k + int64_t(c2[t]) * ld2] * D1[j + int64_t(c1[t]) * ld1];
+      g1[m] = g2[m] = 0.0;
+      if (e < CP_PAIRS * MAXT && p0 + q < npairs && t < T) {
+        int64_t j = j0 + q, k = k0;
+        while (j >= nj) {
+          j -= nj;
+          ++k;
+        }
+        g2[m] = D2[k + int64_t(c2s[t]) * ld2];
+        g1[m] = D1[j + int64_t(c1s[t]) * ld1];
       }
-      xs[q][t] = v;
     }
-    __syncthreads();
+  };
+  auto put = [&](int buf) {
+#pragma unroll
+    for (int m = 0; m < NSLOT; ++m) {
+      const int e = threadIdx.x + m * CP_THREADS;
+      if (e < CP_PAIRS * MAXT) (&xs[buf][0][0])[e] = ws[e % MAXT] * g2[m] * g1[m];
+    }
+  };
+  int64_t p0 = int64_t(blockIdx.y) * CP_PAIRS;
+  if (p0 < npairs) {
+    gather(p0);
+    put(0);
+  }
+  __syncthreads();
+  for (int buf = 0; p0 < npairs; p0 += stride, buf ^= 1) {
+    const bool more = p0 + stride < npairs;
+    if (more) gather(p0 + stride);  // loads in flight during this batch
     const int nq = int((npairs - p0) < CP_PAIRS ? (npairs - p0) : CP_PAIRS);
     for (int q = 0; q < nq; ++q) {
       double s[CP_IPT];
 #pragma unroll
       for (int u = 0; u < CP_IPT; ++u) s[u] = 0.0;
+      const double2* x2 = reinterpret_cast<const double2*>(&xs[buf][q][0]);
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
-        const double x = xs[q][t];
+      for (int t = 0; t < MAXT; t += 2) {
+        const double2 x = x2[t / 2];
 #pragma unroll
-        for (int u = 0; u < CP_IPT; ++u) s[u] += a[u][t] * x;
+        for (int u = 0; u < CP_IPT; ++u) {
+          s[u] += a[u][t] * x.x;
+          s[u] += a[u][t + 1] * x.y;
+        }
       }
       const int64_t p = p0 + q;
 #pragma unroll
@@ -560,6 +606,8 @@ k_cp_eval_small(const double* __restrict__ D0, int64_t ld0, const double* __rest
         if (i < ni) out[i + ni * p] = s[u];
       }
     }
+    if (more) put(buf ^ 1);  // consumed one iteration ago
+    __syncthreads();  // buf consumed, buf ^ 1 staged
   }
 }
 

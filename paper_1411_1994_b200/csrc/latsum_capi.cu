@@ -1296,6 +1296,8 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     doff.upload(c, pl_off);
     dsh.upload(c, pl_shift);
     can.dict[l].alloc(c, size_t(N) * can.d[l]);
+    // 2048 rows per block: the sublattice columns (up to 256 shifted reads per entry, cfg5)
+    // spread over many blocks instead of a few long ones
     const int64_t chunk = 2048;
     const int nchunk = int((N + chunk - 1) / chunk);
     DBuf partial(c, size_t(can.d[l]) * nchunk);

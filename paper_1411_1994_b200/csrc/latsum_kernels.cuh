@@ -118,7 +118,7 @@ struct DictArgs {
 // across the block (the shift list sits in shared memory), so the 256-shift sublattice
 // columns (cfg5) stream instead of forming one dependent L2 chain per entry.
 constexpr int DICT_THREADS = 256, DICT_RT = 8, DICT_MAXSH = 1024;
-static_assert(DICT_THREADS * DICT_RT == 2048, "one chunk of 2048 rows per block");
+static_assert(DICT_THREADS * DICT_RT == 2048, "2048-row sub-chunks; a block covers a chunk of them");
 
 __device__ __forceinline__ void dict_values(const DictArgs& a, const double* __restrict__ rj,
                                             const int64_t* __restrict__ sh, int ns, int64_t i0,
@@ -154,12 +154,14 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
   const double* rj = a.ref + j * 2 * a.N;
   int ns;
   const int64_t* sh = dict_shifts(a, p, shb, ns);
-  const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
-  double v[DICT_RT];
-  dict_values(a, rj, sh, ns, i0, i1, v);
+  const int64_t c0 = blockIdx.y * a.chunk, c1 = min(a.N, c0 + a.chunk);
   double s = 0.0;
+  for (int64_t i0 = c0; i0 < c1; i0 += DICT_THREADS * DICT_RT) {  // 2048-row sub-chunks
+    double v[DICT_RT];
+    dict_values(a, rj, sh, ns, i0, c1, v);
 #pragma unroll
-  for (int r = 0; r < DICT_RT; ++r) s += v[r] * v[r];
+    for (int r = 0; r < DICT_RT; ++r) s += v[r] * v[r];
+  }
   s = block_sum(s, red);
   if (threadIdx.x == 0) a.partial[c * a.nchunk + blockIdx.y] = s;
 }
@@ -179,15 +181,17 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
   const double* rj = a.ref + j * 2 * a.N;
   int ns;
   const int64_t* sh = dict_shifts(a, p, shb, ns);
-  const int64_t i0 = blockIdx.y * a.chunk, i1 = min(a.N, i0 + a.chunk);
+  const int64_t c0 = blockIdx.y * a.chunk, c1 = min(a.N, c0 + a.chunk);
   const double nrm = a.norms[c];
-  double v[DICT_RT];
-  dict_values(a, rj, sh, ns, i0, i1, v);
   double* out = a.dict + c * a.N;
+  for (int64_t i0 = c0; i0 < c1; i0 += DICT_THREADS * DICT_RT) {  // 2048-row sub-chunks
+    double v[DICT_RT];
+    dict_values(a, rj, sh, ns, i0, c1, v);
 #pragma unroll
-  for (int r = 0; r < DICT_RT; ++r) {
-    const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
-    if (i < i1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] / nrm;
+    for (int r = 0; r < DICT_RT; ++r) {
+      const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+      if (i < c1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] / nrm;
+    }
   }
 }
 

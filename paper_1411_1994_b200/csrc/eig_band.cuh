@@ -38,7 +38,10 @@ constexpr int S2B_RPL = 26;            // panel rows per lane: n <= 832
 constexpr int S2B_NMAX = 32 * S2B_RPL;
 constexpr int S2B_MAXC = (S2B_NMAX + S2B_CTAS - 1) / S2B_CTAS;  // owned columns per CTA
 constexpr int SB_LDB = 2 * BW + 2;     // band column stride in shared memory (bulge room)
-constexpr int SB_WARPS = 24;
+#ifndef LATSUM_SB_WARPS
+#define LATSUM_SB_WARPS 16
+#endif
+constexpr int SB_WARPS = LATSUM_SB_WARPS;  // sweeps in flight (one warp each): 16 beat 12 / 24 (2.22 vs 2.38 / 2.43 ms, n = 693)
 constexpr int SB_KBIG = 64;            // progress encoding: sweep * SB_KBIG + tasks done
 constexpr int SB_NMAX = 808;           // 34 (n + 16) + 768 doubles <= 227 KB
 constexpr int BT_CPB = 4;              // eigenvector columns per back-transform CTA

@@ -1287,6 +1287,7 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
       const int64_t* sh = sub_shifts + sub_off[s * 3 + l];
       block_pl[l][s] = place(std::vector<int64_t>(sh, sh + sub_counts[s * 3 + l]));
     }
+    const int64_t P_sub = int64_t(pl_off.size()) - 1;  // sublattice placements come first
     for (int64_t dd = 0; dd < ndef; ++dd)
       block_pl[l][nsub + dd] = place(std::vector<int64_t>{def_shifts[dd * 3 + l]});
     const int64_t P = int64_t(pl_off.size()) - 1;
@@ -1296,22 +1297,33 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     doff.upload(c, pl_off);
     dsh.upload(c, pl_shift);
     can.dict[l].alloc(c, size_t(N) * can.d[l]);
-    // 2048 rows per block: the sublattice columns (up to 256 shifted reads per entry, cfg5)
-    // spread over many blocks instead of a few long ones
+    // rows per block: 2048 for the sublattice columns (up to 256 shifted reads per entry,
+    // cfg5: spread over many blocks), up to 8192 for the single-shift defect columns (fewer
+    // blocks amortise the per-block shift-list staging and reductions)
     const int64_t chunk = 2048;
     const int nchunk = int((N + chunk - 1) / chunk);
+    const int64_t chunk_d = std::min<int64_t>(8192, (N + 2047) / 2048 * 2048);
+    const int nchunk_d = int((N + chunk_d - 1) / chunk_d);
     DBuf partial(c, size_t(can.d[l]) * nchunk);
     DBuf& norms = norm_buf[l];
     norms.alloc(c, can.d[l]);
-    DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
-    dim3 g(unsigned(can.d[l]), unsigned(nchunk));
     ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
-    k_dict_sumsq<<<g, 256, 0, c->stream>>>(a);
-    post_launch(c);
-    k_dict_norms<<<unsigned((can.d[l] + 255) / 256), 256, 0, c->stream>>>(a, can.d[l]);
-    post_launch(c);
-    k_dict_write<<<g, 256, 0, c->stream>>>(a);
-    post_launch(c);
+    // [0, P_sub Rd): sublattice columns (2048-row blocks); [P_sub Rd, d): single-shift
+    // defect columns (chunk_d rows per block)
+    auto l2_path = [&](int64_t c_lo, int64_t c_hi, int64_t ch, int nch) {
+      if (c_hi <= c_lo) return;
+      DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, ch, nch};
+      a.c0 = c_lo;
+      const dim3 g{unsigned(c_hi - c_lo), unsigned(nch)};
+      k_dict_sumsq<<<g, DICT_THREADS, 0, c->stream>>>(a);
+      post_launch(c);
+      k_dict_norms<<<unsigned((c_hi - c_lo + 255) / 256), 256, 0, c->stream>>>(a, c_hi);
+      post_launch(c);
+      k_dict_write<<<g, DICT_THREADS, 0, c->stream>>>(a);
+      post_launch(c);
+    };
+    l2_path(0, std::min(can.d[l], P_sub * Rd), chunk, nchunk);
+    l2_path(std::min(can.d[l], P_sub * Rd), can.d[l], chunk_d, nchunk_d);
   }
   for (int l = 0; l < 3; ++l) {  // the three modes' kernels are queued before the first wait
     can.dict_norms[l].resize(can.d[l]);

@@ -110,6 +110,7 @@ struct DictArgs {
   double* norms;           // d
   int64_t chunk;
   int nchunk;
+  int64_t c0 = 0;          // first column handled by this launch (blockIdx.x + c0)
 };
 
 // Dictionary entries of column c = (placement p, reference column j) for the DICT_RT rows
@@ -149,7 +150,7 @@ __device__ __forceinline__ const int64_t* dict_shifts(const DictArgs& a, int64_t
 __global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
   __shared__ double red[32];
   __shared__ int64_t shb[DICT_MAXSH];
-  const int64_t c = blockIdx.x;
+  const int64_t c = blockIdx.x + a.c0;
   const int64_t p = c / a.Rd, j = c % a.Rd;
   const double* rj = a.ref + j * 2 * a.N;
   int ns;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
 }
 
 __global__ void k_dict_norms(DictArgs a, int64_t d) {
-  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x + a.c0;
   if (c >= d) return;
   double s = 0.0;
   for (int q = 0; q < a.nchunk; ++q) s += a.partial[c * a.nchunk + q];
@@ -176,7 +177,7 @@ __global__ void k_dict_norms(DictArgs a, int64_t d) {
 
 __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
   __shared__ int64_t shb[DICT_MAXSH];
-  const int64_t c = blockIdx.x;
+  const int64_t c = blockIdx.x + a.c0;
   const int64_t p = c / a.Rd, j = c % a.Rd;
   const double* rj = a.ref + j * 2 * a.N;
   int ns;

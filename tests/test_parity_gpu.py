@@ -521,3 +521,20 @@ def test_canonical_box_eval_all_rank_buckets(ctx, kind):
     want = O.canonical_entries(F, w, pr)
     got = box[pr[:, 0] - lo[0], pr[:, 1] - lo[1], pr[:, 2] - lo[2]]
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
+@pytest.mark.parametrize("rank", [1, 2, 5, 17, 18, 23, 24, 25, 33, 47, 64])
+def test_low_rank_canonical_eval_kernel_buckets(ctx, rank):
+    """canonical.hpp:192-202 (to_dense) through k_cp_eval_small for every rank bucket
+    (4 rows per thread up to 18 terms, 2 up to 24, then 1), on ragged boxes: row counts that
+    are not multiples of the 128-thread row block, pair counts that are not multiples of the
+    32-pair staging batch, and a pair range that wraps the j extent inside a batch."""
+    dims = (700, 9, 13)
+    w, F = _random_canonical(dims, rank, 100 + rank)
+    can = api.canonical_from_arrays(w, F, ctx)
+    for lo, hi in [((0, 0, 0), dims), ((3, 2, 1), (517, 9, 12)), ((100, 4, 0), (101, 5, 13))]:
+        box = can.to_dense(lo, hi)
+        want = np.einsum("q,iq,jq,kq->ijk", w, F[0][lo[0]:hi[0]], F[1][lo[1]:hi[1]],
+                         F[2][lo[2]:hi[2]])
+        assert box.shape == want.shape
+        np.testing.assert_allclose(box, want, rtol=0, atol=1e-13 * np.max(np.abs(want)))

@@ -6,14 +6,92 @@
 // the 1e-12 directional parity of stage 1 depends on.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
 #include <limits>
+#include <mutex>
 #include <thread>
 #include <vector>
 
 #include "latsum_b200.h"
 
 namespace {
+
+// Persistent host workers for the step-constant sweep: spawning a thread per candidate
+// cost more than the sweep itself (~15 us per std::thread, 53 candidates, every call).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  // f(0) .. f(n-1), the caller participating; returns when all have run
+  void run(int n, const std::function<void(int)>& f) {
+    std::unique_lock<std::mutex> lk(run_mu_);  // one sweep at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      f_ = &f;
+      n_ = n;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return done_ == n_; });
+    f_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int nt = std::max(0, std::min(31, int(std::thread::hardware_concurrency()) - 1));
+    for (int i = 0; i < nt; ++i)
+      threads_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> g(mu_);
+            cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+          }
+          work();
+        }
+      });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  void work() {  // claim (f, i) under the lock: a claimed task keeps its run() alive
+    for (;;) {
+      const std::function<void(int)>* f;
+      int i;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!f_ || next_ >= n_) return;
+        f = f_;
+        i = next_++;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* f_ = nullptr;
+  int n_ = 0, done_ = 0, next_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
 
 double transform_weight(int family, double lambda, double t) {
   // quadrature.hpp:251-263: p(z) = int_0^inf w(t) exp(-z^2 t^2) dt
@@ -89,22 +167,12 @@ double latsum_default_step_constant(int family, double lambda, int M, double she
   constexpr int kCand = 53;
   double c0s[kCand], errs[kCand];
   for (int i = 0; i < kCand; ++i) c0s[i] = base * (0.5 + 1.3 * double(i) / 52.0);
-  auto work = [&](int lo, int hi) {
+  const std::function<void(int)> cand = [&](int i) {
     std::vector<double> t(2 * M + 1), a(2 * M + 1);
-    for (int i = lo; i < hi; ++i) {
-      sinc_rule(family, lambda, M, c0s[i], shell_A, t.data(), a.data());
-      errs[i] = max_pointwise_rel(family, lambda, t.data(), a.data(), 2 * M + 1, shell_a, shell_A,
-                                  npts);
-    }
+    sinc_rule(family, lambda, M, c0s[i], shell_A, t.data(), a.data());
+    errs[i] = max_pointwise_rel(family, lambda, t.data(), a.data(), 2 * M + 1, shell_a, shell_A, npts);
   };
-  const int nt = std::max(1, std::min<int>(kCand, int(std::thread::hardware_concurrency())));
-  std::vector<std::thread> pool;
-  const int chunk = (kCand + nt - 1) / nt;
-  for (int w = 0; w < nt; ++w) {
-    const int lo = w * chunk, hi = std::min(kCand, lo + chunk);
-    if (lo < hi) pool.emplace_back(work, lo, hi);
-  }
-  for (auto& th : pool) th.join();
+  HostPool::get().run(kCand, cand);
   double best = std::numeric_limits<double>::infinity();
   double best_c0 = c0s[0];
   for (int i = 0; i < kCand; ++i)

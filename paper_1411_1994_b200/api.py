@@ -294,13 +294,20 @@ class CanonicalTensor:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self._h = ctx, handle
-        dims, dcols, rank, T = np.zeros(3, np.int64), np.zeros(3, np.int64), ctypes.c_int64(), ctypes.c_int64()
-        _lib.lib().latsum_canonical_info(self._h, _p(dims), ctypes.byref(rank), _p(dcols),
-                                         ctypes.byref(T))
+        dims, dcols, rank = np.zeros(3, np.int64), np.zeros(3, np.int64), ctypes.c_int64()
+        # merged_terms is not requested here: it waits for the host-side term merge that
+        # the library overlaps with the RHOSVD's first kernels
+        _lib.lib().latsum_canonical_info(self._h, _p(dims), ctypes.byref(rank), _p(dcols), None)
         self.dims = tuple(int(x) for x in dims)
         self.rank = int(rank.value)
         self.dict_cols = tuple(int(x) for x in dcols)
-        self.merged_terms = int(T.value)
+
+    @property
+    def merged_terms(self) -> int:
+        """Rank-1 terms left after merging identical ones (t and -t, repeated sites)."""
+        T = ctypes.c_int64()
+        _lib.lib().latsum_canonical_info(self._h, None, None, None, ctypes.byref(T))
+        return int(T.value)
 
     @property
     def handle(self):

@@ -1945,6 +1945,20 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       tms[3].norm = tn.stop();
     } else {
       reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
+      // P_i = Z_i^T D_i over this rank's rows (summed over ranks) while the other modes'
+      // eigensolves are still running
+      Timer tp(w);
+      tp.start();
+      const RowBlock blk = mo[i].blk;
+      const int64_t N = can.N[i], Nb = blk.n();
+      t.P[i].alloc(w, size_t(mo[i].r) * can.d[i]);
+      if (Nb > 0)
+        gemm(w, true, false, mo[i].r, can.d[i], Nb, 1.0, mo[i].Z.p, Nb, can.dict[i].p + blk.lo, N,
+             0.0, t.P[i].p, mo[i].r, tagged("gemm_project"));
+      else
+        CK(cudaMemsetAsync(t.P[i].p, 0, sizeof(double) * mo[i].r * can.d[i], w->stream));
+      if (Nb != N) allreduce(w, t.P[i].p, size_t(mo[i].r) * can.d[i]);
+      tms[i].project = tp.stop();
     }
   };
   if (serial) {
@@ -1954,12 +1968,16 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     fork_join(c, zero_terms ? 1 : 4, body);
     Trace::mark(c, "rhosvd join");
   }
-  for (int l = 0; l < 3; ++l) mo[l].Z.adopt(c->stream);
+  for (int l = 0; l < 3; ++l) {
+    mo[l].Z.adopt(c->stream);
+    t.P[l].adopt(c->stream);
+  }
   for (const auto& x : tms) {
     tm.gram += x.gram;
     tm.syevd += x.syevd;
     tm.deflate += x.deflate;
     tm.norm += x.norm;
+    tm.project += x.project;
   }
   if (can.Mc == 0 || rep.input_norm == 0.0) {  // zero tensor (rank_reduction.hpp:183-187)
     for (int l = 0; l < 3; ++l) {
@@ -1988,14 +2006,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     const RowBlock blk = mo[l].blk;
     const int64_t N = can.N[l], Nb = blk.n();
     const bool sharded = Nb != N;
-    P[l].alloc(c, size_t(mo[l].r) * can.d[l]);
-    if (Nb > 0)  // P_l = Z_l^T D_l over this rank's rows, summed over ranks
-      gemm(c, true, false, mo[l].r, can.d[l], Nb, 1.0, mo[l].Z.p, Nb, can.dict[l].p + blk.lo, N,
-           0.0, P[l].p, mo[l].r, tagged("gemm_project"));
-    else
-      CK(cudaMemsetAsync(P[l].p, 0, sizeof(double) * mo[l].r * can.d[l], c->stream));
     if (sharded) {
-      allreduce(c, P[l].p, size_t(mo[l].r) * can.d[l]);
       // replicate Z: all-gather the row blocks (padded to equal size)
       const int64_t r = mo[l].r, bmax = N / c->nranks + 1;
       DBuf send(c, size_t(bmax) * r), recv(c, size_t(bmax) * r * c->nranks), full(c, size_t(N) * r);
@@ -2018,7 +2029,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   t.tw.upload(c, can.tw);
   t.tseg.upload(c, can.tseg);
   t.T = can.T;
-  tm.project = tp.stop();
+  tm.project += tp.stop();
   Trace::mark(c, "projections done");
   if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
     tp.start();

@@ -22,6 +22,7 @@
 //      products); the panels then apply I - V T V^T in reverse order.
 #pragma once
 #include <cooperative_groups.h>
+#include "ozaki_i8.cuh"  // mbarrier / bulk-copy wrappers
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -840,11 +841,29 @@ k_tridiag_invit_sm(const double* __restrict__ dg, const double* __restrict__ eg,
 // sweeps' reflectors in generation order, applied last sweep first; the reflectors of one
 // sweep cover disjoint BW-row blocks starting at row s+1, so thread t handles row s+1+t and
 // the dot products are half-warp reductions.  Q1 = P_0 .. P_{npan-1}, applied last first.
+// Row r of the back-transform's column block (BT_CPB = 4 contiguous doubles) as two 16-byte
+// shared-memory accesses: lanes on consecutive rows then touch one contiguous span instead
+// of four 4-way bank-conflicted 8-byte accesses.
+static_assert(BT_CPB == 4, "ys rows are two double2");
+__device__ __forceinline__ void ys_load(const double* ys, int r, bool act, double* y) {
+  if (act) {
+    const double2 a = reinterpret_cast<const double2*>(ys + r * BT_CPB)[0];
+    const double2 b = reinterpret_cast<const double2*>(ys + r * BT_CPB)[1];
+    y[0] = a.x, y[1] = a.y, y[2] = b.x, y[3] = b.y;
+  } else {
+    y[0] = y[1] = y[2] = y[3] = 0.0;
+  }
+}
+__device__ __forceinline__ void ys_store(double* ys, int r, const double* y) {
+  reinterpret_cast<double2*>(ys + r * BT_CPB)[0] = make_double2(y[0], y[1]);
+  reinterpret_cast<double2*>(ys + r * BT_CPB)[1] = make_double2(y[2], y[3]);
+}
+
 __global__ void __launch_bounds__(BT_THREADS)
 k_band_backtransform(int n, int k, const double* __restrict__ V2, const double* __restrict__ TAU2,
                      int KS, const double* __restrict__ Vw, const double* __restrict__ Tw,
-                     int npan, const double* Y, double* Z) {
-  extern __shared__ double smb[];
+                     int npan, const double* Y, double* Z, int dbuf) {
+  extern __shared__ __align__(16) double smb[];
   double* ys = smb;                        // n x BT_CPB (row-major)
   double* wv = ys + size_t(n) * BT_CPB;    // BW x BT_CPB
   double* tw = wv + BW * BT_CPB;           // BW x BT_CPB
@@ -855,60 +874,96 @@ k_band_backtransform(int n, int k, const double* __restrict__ V2, const double* 
     ys[r * BT_CPB + c] = c < nc ? Y[size_t(c0 + c) * n + r] : 0.0;
   }
   __syncthreads();
-  double nv[2] = {0.0, 0.0}, ntau[2] = {0.0, 0.0};  // reflectors of the next sweep (prefetched)
+  // Q2: sweeps last to first.  Reflector j of sweep s (rows s+1+16j .. +15) is applied by a
+  // half-warp: lane (rq, c) = (l >> 2, l & 3) holds rows 4 rq .. 4 rq + 3 of column c, sums
+  // its 4 products and the half-warp reduces over rq with two shuffles (16 lanes x 16
+  // shuffles per reflector before: the shuffle unit was the limit).  The next sweep's
+  // reflector entries are prefetched into registers.
+  double nv[2][4], ntau[2];
   auto fetch = [&](int s) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
-      const int t = tid + half * BT_THREADS;
-      const bool act = s >= 0 && t < n - 1 - s;
-      nv[half] = act ? __ldg(V2 + size_t(s) * n + t) : 0.0;
-      ntau[half] = act ? __ldg(TAU2 + size_t(s) * KS + t / BW) : 0.0;
+      const int t = tid + half * BT_THREADS, j = t >> 4, rq = (t & 15) >> 2;
+      const int rows = n - 1 - s;
+      ntau[half] = (s >= 0 && 16 * j < rows) ? __ldg(TAU2 + size_t(s) * KS + j) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ti = 16 * j + 4 * rq + i;
+        nv[half][i] = (s >= 0 && ti < rows) ? __ldg(V2 + size_t(s) * n + ti) : 0.0;
+      }
     }
   };
   fetch(n - 3);
   for (int s = n - 3; s >= 0; --s) {
     const int rows = n - 1 - s;
-    const double cv[2] = {nv[0], nv[1]}, ctau[2] = {ntau[0], ntau[1]};
+    double cv[2][4], ctau[2];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      ctau[half] = ntau[half];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cv[half][i] = nv[half][i];
+    }
     fetch(s - 1);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
-      const int t = tid + half * BT_THREADS;
-      if (t - (t & 15) >= rows) continue;  // whole half-warp beyond the sweep (uniform)
-      const bool act = t < rows;
-      const double v = cv[half];
-      const double tau = ctau[half];
-      const int r = s + 1 + t;
-      double y[BT_CPB], pr[BT_CPB];
+      const int t = tid + half * BT_THREADS, j = t >> 4, l = t & 15, c = l & 3, rq = l >> 2;
+      if (16 * j >= rows) continue;  // whole half-warp beyond the sweep (uniform)
+      const int rb = s + 1 + 16 * j + 4 * rq;
+      double y[4], p = 0.0;
 #pragma unroll
-      for (int c = 0; c < BT_CPB; ++c) {
-        y[c] = act ? ys[r * BT_CPB + c] : 0.0;
-        pr[c] = v * y[c];
+      for (int i = 0; i < 4; ++i) {
+        const bool act = 16 * j + 4 * rq + i < rows;
+        y[i] = act ? ys[(rb + i) * BT_CPB + c] : 0.0;
+        p += cv[half][i] * y[i];
       }
+      const unsigned hm = 0xffffu << (threadIdx.x & 16);
+      p += __shfl_xor_sync(hm, p, 4, 16);
+      p += __shfl_xor_sync(hm, p, 8, 16);
+      const double f = ctau[half] * p;
 #pragma unroll
-      for (int c = 0; c < BT_CPB; ++c) {
-        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 8, 16);
-        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 4, 16);
-        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 2, 16);
-        pr[c] += __shfl_xor_sync(0xffffu << (threadIdx.x & 16), pr[c], 1, 16);
-      }
-      if (act) {
-#pragma unroll
-        for (int c = 0; c < BT_CPB; ++c) ys[r * BT_CPB + c] = y[c] - tau * pr[c] * v;
-      }
+      for (int i = 0; i < 4; ++i)
+        if (16 * j + 4 * rq + i < rows) ys[(rb + i) * BT_CPB + c] = y[i] - f * cv[half][i];
     }
     __syncthreads();
   }
   // Q1: panels last to first; thread (pair = tid / 8, seg = tid % 8), pair = (row of V^T, column)
   const int pair = tid >> 3, seg = tid & 7;
   const int pc = pair / BT_CPB, pcol = pair % BT_CPB;  // pair < 64 (512 threads)
-  double* vs = tw + BW * BT_CPB;  // BW x n: the panel's V
+  // the panels' V (BW x n, contiguous) arrive by bulk copy (TMA engine), double-buffered
+  // when two fit in shared memory: the next panel streams in while this one is applied
+  const int nbuf = dbuf ? 2 : 1;
+  double* vsb = tw + BW * BT_CPB;  // nbuf x (BW x n)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vsb + size_t(nbuf) * BW * n);
+  const uint32_t vbytes = uint32_t(BW) * uint32_t(n) * 8u;
+  if (tid == 0) {
+    for (int b = 0; b < nbuf; ++b) oz::mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int p, int b) {
+    if (tid == 0 && p >= 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      oz::mbar_expect_tx(&bar[b], vbytes);
+      oz::bulk_g2s(vsb + size_t(b) * BW * n, Vw + size_t(p) * BW * n, vbytes, &bar[b]);
+    }
+  };
+  issue(npan - 1, 0);
+  if (nbuf == 2) issue(npan - 2, 1);
+  uint32_t phase[2] = {0u, 0u};
   for (int p = npan - 1; p >= 0; --p) {
     const int r0 = (p + 1) * BW;
-    const double* Vp = Vw + size_t(p) * BW * n;
-    for (int idx = tid; idx < BW * n; idx += BT_THREADS) vs[idx] = __ldg(Vp + idx);
-    __syncthreads();
-    double acc = 0.0;
-    for (int r = r0 + pc + seg; r < n; r += 8) acc += vs[pc * n + r] * ys[r * BT_CPB + pcol];
+    const int b = nbuf == 2 ? (npan - 1 - p) & 1 : 0;
+    double* vs = vsb + size_t(b) * BW * n;
+    oz::mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
+    double acc0 = 0.0, acc1 = 0.0;
+    int r = r0 + pc + seg;
+    for (; r + 8 < n; r += 16) {
+      acc0 += vs[pc * n + r] * ys[r * BT_CPB + pcol];
+      acc1 += vs[pc * n + r + 8] * ys[(r + 8) * BT_CPB + pcol];
+    }
+    if (r < n) acc0 += vs[pc * n + r] * ys[r * BT_CPB + pcol];
+    double acc = acc0 + acc1;
     acc += __shfl_xor_sync(FULL, acc, 4);
     acc += __shfl_xor_sync(FULL, acc, 2);
     acc += __shfl_xor_sync(FULL, acc, 1);
@@ -924,18 +979,17 @@ k_band_backtransform(int n, int k, const double* __restrict__ V2, const double* 
     __syncthreads();
     for (int r = r0 + tid; r < n; r += BT_THREADS) {
       double y[BT_CPB];
-#pragma unroll
-      for (int c = 0; c < BT_CPB; ++c) y[c] = ys[r * BT_CPB + c];
+      ys_load(ys, r, true, y);
 #pragma unroll
       for (int e = 0; e < BW; ++e) {
         const double v = vs[e * n + r];
 #pragma unroll
         for (int c = 0; c < BT_CPB; ++c) y[c] -= v * tw[e * BT_CPB + c];
       }
-#pragma unroll
-      for (int c = 0; c < BT_CPB; ++c) ys[r * BT_CPB + c] = y[c];
+      ys_store(ys, r, y);
     }
-    __syncthreads();
+    __syncthreads();  // vs consumed: refill it with panel p - nbuf
+    issue(p - nbuf, b);
   }
   for (int idx = tid; idx < n * nc; idx += BT_THREADS) {
     const int r = idx % n, c = idx / n;

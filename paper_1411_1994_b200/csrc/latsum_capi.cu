@@ -895,15 +895,19 @@ struct Eig {
       }
       {
         ProfScope ps(c, "eig_backtransform", double(n) * double(n) * double(k));
-        const size_t smem = (size_t(n) * (band::BT_CPB + band::BW) + 2 * band::BW * band::BT_CPB) * sizeof(double);
+        // ys (n x BT_CPB), wv / tw, one or two panel buffers (BW x n), two mbarriers
+        constexpr size_t kBtMax = 226 * 1024;
+        auto bt_smem = [&](int nbuf) {
+          return (size_t(n) * (band::BT_CPB + size_t(nbuf) * band::BW) + 2 * band::BW * band::BT_CPB) *
+                     sizeof(double) + 16;
+        };
+        const int dbuf = bt_smem(2) <= kBtMax ? 1 : 0;
+        const size_t smem = bt_smem(dbuf ? 2 : 1);
         static std::once_flag once;
-        std::call_once(once, [&] {
-          set_smem_attr(band::k_band_backtransform,
-                        (size_t(band::SB_NMAX) * (band::BT_CPB + band::BW) + 2 * band::BW * band::BT_CPB) * 8);
-        });
+        std::call_once(once, [&] { set_smem_attr(band::k_band_backtransform, kBtMax); });
         band::k_band_backtransform<<<unsigned((k + band::BT_CPB - 1) / band::BT_CPB), band::BT_THREADS,
                                      smem, c->stream>>>(int(n), int(k), V2.p, TAU2.p, KS, Vw.p, Tw.p,
-                                                        band::s2b_panels(int(n)), V, V);
+                                                        band::s2b_panels(int(n)), V, V, dbuf);
         post_launch(c);
       }
     } else {

@@ -216,34 +216,22 @@ __global__ void __launch_bounds__(S2B_THREADS, 1) k_sy2sb(S2BArgs a) {
           if (lane == 0) taus[cc] = tau;
         }
         __syncthreads();
-        if (wid > cc) {  // apply P_cc to column wid; v in chunks of 8 independent loads
+        if (wid > cc) {  // apply P_cc to column wid: v read from shared memory once, kept in
+                         // registers for the dot and the update (the loop was bound by the
+                         // shared-memory wavefronts of reading v twice in 15 warps)
           const double* __restrict__ vc = Vs + cc * S2B_LDV + lane;  // zero above row cc, past m
+          double vv[S2B_RPL];
+#pragma unroll
+          for (int t = 0; t < S2B_RPL; ++t) vv[t] = t < tmax ? vc[32 * t] : 0.0;
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int t0 = 0; t0 < S2B_RPL; t0 += 8) {
-            if (t0 < tmax) {
-              double vv[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) vv[u] = t0 + u < S2B_RPL ? vc[32 * (t0 + u)] : 0.0;
-#pragma unroll
-              for (int u = 0; u < 8; u += 2) {
-                if (t0 + u < S2B_RPL) s0 += vv[u] * x[t0 + u];
-                if (t0 + u + 1 < S2B_RPL) s1 += vv[u + 1] * x[t0 + u + 1];
-              }
-            }
+          for (int t = 0; t < S2B_RPL; t += 2) {
+            s0 += vv[t] * x[t];
+            if (t + 1 < S2B_RPL) s1 += vv[t + 1] * x[t + 1];
           }
           const double f = taus[cc] * wsum(s0 + s1);
 #pragma unroll
-          for (int t0 = 0; t0 < S2B_RPL; t0 += 8) {
-            if (t0 < tmax) {
-              double vv[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) vv[u] = t0 + u < S2B_RPL ? vc[32 * (t0 + u)] : 0.0;
-#pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (t0 + u < S2B_RPL) x[t0 + u] -= f * vv[u];
-            }
-          }
+          for (int t = 0; t < S2B_RPL; ++t) x[t] -= f * vv[t];
         }
       }
       mark(9);

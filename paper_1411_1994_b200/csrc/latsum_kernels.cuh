@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
   const int64_t* sh = dict_shifts(a, p, shb, ns);
   const int64_t c0 = blockIdx.y * a.chunk, c1 = min(a.N, c0 + a.chunk);
   const double nrm = a.norms[c];
+  const double inv = nrm == 0.0 ? 0.0 : 1.0 / nrm;  // one division per column, not per entry
   double* out = a.dict + c * a.N;
   for (int64_t i0 = c0; i0 < c1; i0 += DICT_THREADS * DICT_RT) {  // 2048-row sub-chunks
     double v[DICT_RT];
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
 #pragma unroll
     for (int r = 0; r < DICT_RT; ++r) {
       const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
-      if (i < c1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] / nrm;
+      if (i < c1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] * inv;
     }
   }
 }

@@ -1314,20 +1314,25 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
     // [0, P_sub Rd): sublattice columns (2048-row blocks); [P_sub Rd, d): single-shift
     // defect columns (chunk_d rows per block)
-    auto l2_path = [&](int64_t c_lo, int64_t c_hi, int64_t ch, int nch) {
+    // sums of squares over chunks of chs rows (partial sums per chunk, then the norms), then
+    // the normalised entries in chunks of chw rows
+    auto l2_path = [&](int64_t c_lo, int64_t c_hi, int64_t chs, int nchs, int64_t chw, int nchw) {
       if (c_hi <= c_lo) return;
-      DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, ch, nch};
+      DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chs, nchs};
       a.c0 = c_lo;
-      const dim3 g{unsigned(c_hi - c_lo), unsigned(nch)};
-      k_dict_sumsq<<<g, DICT_THREADS, 0, c->stream>>>(a);
+      k_dict_sumsq<<<dim3{unsigned(c_hi - c_lo), unsigned(nchs)}, DICT_THREADS, 0, c->stream>>>(a);
       post_launch(c);
       k_dict_norms<<<unsigned((c_hi - c_lo + 255) / 256), 256, 0, c->stream>>>(a, c_hi);
       post_launch(c);
-      k_dict_write<<<g, DICT_THREADS, 0, c->stream>>>(a);
+      a.chunk = chw;
+      a.nchunk = nchw;
+      k_dict_write<<<dim3{unsigned(c_hi - c_lo), unsigned(nchw)}, DICT_THREADS, 0, c->stream>>>(a);
       post_launch(c);
     };
-    l2_path(0, std::min(can.d[l], P_sub * Rd), chunk, nchunk);
-    l2_path(std::min(can.d[l], P_sub * Rd), can.d[l], chunk_d, nchunk_d);
+    l2_path(0, std::min(can.d[l], P_sub * Rd), chunk, nchunk, chunk, nchunk);
+    // single-shift columns: a whole column per block for the (write-free) sums of squares
+    const int64_t ncol_all = (N + 2047) / 2048 * 2048;
+    l2_path(std::min(can.d[l], P_sub * Rd), can.d[l], ncol_all, 1, chunk_d, nchunk_d);
   }
   for (int l = 0; l < 3; ++l) {  // the three modes' kernels are queued before the first wait
     can.dict_norms[l].resize(can.d[l]);

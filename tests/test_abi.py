@@ -55,3 +55,33 @@ def test_context_without_device_fails_loudly():
     from paper_1411_1994_b200 import api
     with pytest.raises(RuntimeError):
         api.Context(0)
+
+
+def test_host_step_constant_matches_oracle_across_threads():
+    """quadrature.hpp:416-447 (default_step_constant) in the library — evaluated on its
+    persistent host worker pool — equals the oracle's sequential sweep bit for bit, for the
+    five BASELINE configurations, also when several host threads call it at once."""
+    import threading
+
+    from oracle import oracle as O
+    from paper_1411_1994_b200 import workload as W
+
+    L = _lib.lib()
+    cases = []
+    for cfg in range(1, 6):
+        g = W.baseline(cfg)
+        a, A = O.reference_shell(g.N, g.box)
+        cases.append((g.family, g.lam, g.M, a, A, O.default_step_constant(g.family, g.lam, g.M, a, A)))
+    got = {}
+
+    def run(tid):
+        for i, (fam, lam, M, a, A, _) in enumerate(cases):
+            got[(tid, i)] = L.latsum_default_step_constant(fam, lam, M, a, A, 320)
+
+    threads = [threading.Thread(target=run, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for (tid, i), c0 in got.items():
+        assert c0 == cases[i][5], (tid, i, c0, cases[i][5])

@@ -538,3 +538,25 @@ def test_low_rank_canonical_eval_kernel_buckets(ctx, rank):
                          F[2][lo[2]:hi[2]])
         assert box.shape == want.shape
         np.testing.assert_allclose(box, want, rtol=0, atol=1e-13 * np.max(np.abs(want)))
+
+
+def test_assembly_term_merge_overlaps_and_joins(ctx):
+    """The rank-1 term merge runs on a host thread after latsum_canonical_assemble returns:
+    destroying the canonical at once must join it, and every consumer (merged-term count,
+    entries, norm, RHOSVD) must see the finished merge; repeated assemblies agree exactly."""
+    g = mini("vacancies")
+    ref, oref = _ref_pair(ctx, g)
+    for _ in range(3):  # create and drop without using the merged terms
+        api.lattice_sum(ref, g)
+    a = api.lattice_sum(ref, g)
+    b = api.lattice_sum(ref, g)
+    assert a.merged_terms == b.merged_terms > 0
+    F, w = O.side_matrices(oref, g)
+    pr = O.probes(g.N, 50, 3)
+    np.testing.assert_array_equal(a.entries(pr), b.entries(pr))
+    want = O.canonical_entries(F, w, pr)
+    assert np.max(np.abs(a.entries(pr) - want)) / np.max(np.abs(want)) < 1e-12
+    ta, ra = api.rhosvd(a, api.TruncationSpec.tol(g.eps))
+    tb, rb = api.rhosvd(b, api.TruncationSpec.tol(g.eps))
+    assert tuple(ra.chosen_ranks) == tuple(rb.chosen_ranks)
+    assert abs(ra.input_norm - rb.input_norm) <= 1e-14 * ra.input_norm

@@ -477,10 +477,34 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
   ProfScope ps(c, "ozaki(slice)", double(L) * double(K) * 8.0 + double(bytes));
   const bool vec = sk == 1 && sl % 2 == 0 && (L1 >= L || sl2 % 2 == 0) &&
                    reinterpret_cast<uintptr_t>(P) % 16 == 0;
+  int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
+  // few tiles, long K: split K over the grid (k_slice_pmax + k_slice_split, bit-identical)
+  static const bool no_split = std::getenv("LATSUM_SLICE_NOSPLIT") != nullptr;  // A/B switch
+  if (!no_split && out.tiles < 148 && out.KB >= 16) {
+    const int64_t nsplit = std::min<int64_t>(out.KB / 8, (2 * 148 + out.tiles - 1) / out.tiles);
+    const int64_t kbs = (out.KB + nsplit - 1) / nsplit;
+    const int64_t ns = (out.KB + kbs - 1) / kbs;
+    DBuf pmax(c, size_t(ns) * L);
+    const dim3 g{unsigned(out.tiles), unsigned(ns)};
+    if (vec) {
+      oz::k_slice_pmax<oz::BM, true><<<g, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, L1,
+                                                                      sl2, kbs, pmax.p);
+      post_launch(c);
+      oz::k_slice_split<oz::BM, true><<<g, 2 * oz::BM, 0, c->stream>>>(
+          P, sl, sk, L, K, out.KB, L1, sl2, kbs, pmax.p, out.scale.p, d, halves);
+    } else {
+      oz::k_slice_pmax<oz::BM, false><<<g, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB, L1,
+                                                                       sl2, kbs, pmax.p);
+      post_launch(c);
+      oz::k_slice_split<oz::BM, false><<<g, 2 * oz::BM, 0, c->stream>>>(
+          P, sl, sk, L, K, out.KB, L1, sl2, kbs, pmax.p, out.scale.p, d, halves);
+    }
+    post_launch(c);
+    return;
+  }
   // persistent: at most 2 CTAs per SM, so the tiles in flight (2 x 148 x 128 lines x K
   // doubles) can stay L2-resident between the scale pass and the digit pass
   const unsigned ctas = unsigned(std::min<int64_t>(out.tiles, 2 * 148));
-  int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
   if (vec)
     oz::k_slice_tile<oz::BM, true><<<ctas, 2 * oz::BM, 0, c->stream>>>(P, sl, sk, L, K, out.KB,
                                                                         out.scale.p, d, L1, sl2, halves);

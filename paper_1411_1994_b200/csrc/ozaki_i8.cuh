@@ -89,6 +89,63 @@ __device__ __forceinline__ void load16(const double* __restrict__ p, int64_t sk,
   }
 }
 
+// max |x| over k-blocks [kb0, kb1) of this thread's half (16 k of each 32-k block)
+template <int ROWS, bool VEC>
+__device__ __forceinline__ double slice_amax(const double* p, int64_t sk, int64_t K, int h,
+                                             int64_t kb0, int64_t kb1) {
+  double amax = 0.0;
+  for (int64_t kb = kb0; kb < kb1; ++kb) {
+    double x[16];
+    load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
+  }
+  return amax;
+}
+
+// the S digit blocks of k-blocks [kb0, kb1) for line r (valid: l < L) of tile `tile`
+template <int ROWS, bool VEC>
+__device__ __forceinline__ void slice_digits(const double* p, int64_t sk, int64_t K, int h, int r,
+                                             bool valid, double inv54, int64_t tile, int64_t KB,
+                                             int64_t kb0, int64_t kb1, int8_t* __restrict__ out,
+                                             int halves) {
+  for (int64_t kb = kb0; kb < kb1; ++kb) {
+    uint32_t w[S][4];
+#pragma unroll
+    for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
+    if (valid) {
+      double x[16];
+      load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        // balanced base-256 digits of X = rint(2^54 x): with Y = X + sum_i 128 256^i the
+        // low digits are the bytes of Y minus 128 (byte ^ 0x80) and the top one Y >> 48
+        const long long X = __double2ll_rn(x[kk] * inv54);
+        const unsigned long long Y = static_cast<unsigned long long>(X + 0x808080808080LL);
+        const uint32_t lo = uint32_t(Y) ^ 0x80808080u;        // d6 d5 d4 d3 (bytes 0..3)
+        const uint32_t hi = uint32_t(Y >> 32) ^ 0x00008080u;  // d2 d1 d0 (bytes 0..2)
+        const int pp = kk % 4;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const uint32_t src = s <= 2 ? hi : lo;
+          const int m = s <= 2 ? 2 - s : 6 - s;  // byte of src holding digit s
+          const uint32_t sel = (0x3210u & ~(0xFu << (4 * pp))) | (uint32_t(4 + m) << (4 * pp));
+          w[s][kk / 4] = __byte_perm(w[s][kk / 4], src, sel);
+        }
+      }
+    }
+    // halves = 2 (B operand of the 2-SM kernel): [half][slice][64 lines], so that each CTA
+    // of the pair loads its 64 lines of all slices with one contiguous copy
+    const int hr = halves == 2 ? r / (ROWS / 2) : 0, rr = halves == 2 ? r % (ROWS / 2) : r;
+    const int blk = ROWS / (halves == 2 ? 2 : 1) * BKB;
+    int8_t* base = out + ((tile * KB + kb) * S) * int64_t(ROWS * BKB) + int64_t(hr) * S * blk +
+                   blk_off(rr, 16 * h);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint4*>(base + s * blk) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
 template <int ROWS, bool VEC>
 __global__ void __launch_bounds__(2 * ROWS)
 k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
@@ -102,15 +159,7 @@ k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, in
     const int64_t l = tile * ROWS + r;
     const int64_t ll = l < L ? l : 0;  // line ll = (ll % L1, ll / L1)
     const double* p = P + (ll % L1) * sl + (ll / L1) * sl2;
-    double amax = 0.0;
-    if (l < L) {
-      for (int64_t kb = 0; kb < KB; ++kb) {
-        double x[16];
-        load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
-      }
-    }
+    const double amax = l < L ? slice_amax<ROWS, VEC>(p, sk, K, h, 0, KB) : 0.0;
     if (h == 1) part[r] = amax;
     __syncthreads();
     if (h == 0) part[r] = fmax(amax, part[r]);
@@ -118,43 +167,44 @@ k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, in
     const double sc = ldexp(1.0, line_exponent(part[r]));
     __syncthreads();  // part[] is rewritten by the next tile
     if (h == 0 && l < L) scale[l] = sc;
-    const double inv54 = 0x1p54 / sc;  // exact: a power of two
-    for (int64_t kb = 0; kb < KB; ++kb) {
-      uint32_t w[S][4];
-#pragma unroll
-      for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0u;
-      if (l < L) {
-        double x[16];
-        load16<ROWS, VEC>(p, sk, kb * BKB + 16 * h, K, x);
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          // balanced base-256 digits of X = rint(2^54 x): with Y = X + sum_i 128 256^i the
-          // low digits are the bytes of Y minus 128 (byte ^ 0x80) and the top one Y >> 48
-          const long long X = __double2ll_rn(x[kk] * inv54);
-          const unsigned long long Y = static_cast<unsigned long long>(X + 0x808080808080LL);
-          const uint32_t lo = uint32_t(Y) ^ 0x80808080u;        // d6 d5 d4 d3 (bytes 0..3)
-          const uint32_t hi = uint32_t(Y >> 32) ^ 0x00008080u;  // d2 d1 d0 (bytes 0..2)
-          const int p = kk % 4;
-#pragma unroll
-          for (int s = 0; s < S; ++s) {
-            const uint32_t src = s <= 2 ? hi : lo;
-            const int m = s <= 2 ? 2 - s : 6 - s;  // byte of src holding digit s
-            const uint32_t sel = (0x3210u & ~(0xFu << (4 * p))) | (uint32_t(4 + m) << (4 * p));
-            w[s][kk / 4] = __byte_perm(w[s][kk / 4], src, sel);
-          }
-        }
-      }
-      // halves = 2 (B operand of the 2-SM kernel): [half][slice][64 lines], so that each CTA
-      // of the pair loads its 64 lines of all slices with one contiguous copy
-      const int hr = halves == 2 ? r / (ROWS / 2) : 0, rr = halves == 2 ? r % (ROWS / 2) : r;
-      const int blk = ROWS / (halves == 2 ? 2 : 1) * BKB;
-      int8_t* base = out + ((tile * KB + kb) * S) * int64_t(ROWS * BKB) + int64_t(hr) * S * blk +
-                     blk_off(rr, 16 * h);
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-        *reinterpret_cast<uint4*>(base + s * blk) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
-    }
+    slice_digits<ROWS, VEC>(p, sk, K, h, r, l < L, 0x1p54 / sc, tile, KB, 0, KB, out, halves);
   }
+}
+
+// Few line tiles with a long K (the projected-CP evaluation's D0 and Y: 16-65 tiles of
+// K = 8283 at cfg5): the persistent kernel would run on 16-65 SMs.  Split K over grid.y
+// instead: pass 1 writes per-split line maxima, pass 2 (every split) takes their maximum —
+// exact, so the digits are bit-identical to k_slice_tile's — and writes its k-blocks.
+template <int ROWS, bool VEC>
+__global__ void __launch_bounds__(2 * ROWS)
+k_slice_pmax(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+             int64_t KB, int64_t L1, int64_t sl2, int64_t kbs, double* __restrict__ pmax) {
+  __shared__ double part[ROWS];
+  const int r = threadIdx.x % ROWS, h = threadIdx.x / ROWS;
+  const int64_t l = blockIdx.x * int64_t(ROWS) + r, ll = l < L ? l : 0;
+  const double* p = P + (ll % L1) * sl + (ll / L1) * sl2;
+  const int64_t kb0 = blockIdx.y * kbs, kb1 = kb0 + kbs < KB ? kb0 + kbs : KB;
+  const double amax = l < L ? slice_amax<ROWS, VEC>(p, sk, K, h, kb0, kb1) : 0.0;
+  if (h == 1) part[r] = amax;
+  __syncthreads();
+  if (h == 0 && l < L) pmax[blockIdx.y * L + l] = fmax(amax, part[r]);
+}
+
+template <int ROWS, bool VEC>
+__global__ void __launch_bounds__(2 * ROWS)
+k_slice_split(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+              int64_t KB, int64_t L1, int64_t sl2, int64_t kbs, const double* __restrict__ pmax,
+              double* __restrict__ scale, int8_t* __restrict__ out, int halves) {
+  const int r = threadIdx.x % ROWS, h = threadIdx.x / ROWS;
+  const int64_t tile = blockIdx.x, l = tile * ROWS + r, ll = l < L ? l : 0;
+  const double* p = P + (ll % L1) * sl + (ll / L1) * sl2;
+  double amax = 0.0;
+  if (l < L)
+    for (unsigned q = 0; q < gridDim.y; ++q) amax = fmax(amax, pmax[q * L + l]);
+  const double sc = ldexp(1.0, line_exponent(amax));
+  if (blockIdx.y == 0 && h == 0 && l < L) scale[l] = sc;
+  const int64_t kb0 = blockIdx.y * kbs, kb1 = kb0 + kbs < KB ? kb0 + kbs : KB;
+  slice_digits<ROWS, VEC>(p, sk, K, h, r, l < L, 0x1p54 / sc, tile, KB, kb0, kb1, out, halves);
 }
 
 // ---------------------------------------------------------------- PTX wrappers

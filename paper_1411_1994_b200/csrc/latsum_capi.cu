@@ -1892,7 +1892,12 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
   if (!c->sub[i]) {
     auto* w = new latsum_ctx();
     w->device = c->device;
-    CK(cudaStreamCreateWithFlags(&w->own, cudaStreamNonBlocking));
+    // workers 0-2 carry the RHOSVD modes' latency-bound eigensolver chains: highest
+    // priority; worker 3 (norm_f, one throughput kernel off the critical path): lowest
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool no_prio = std::getenv("LATSUM_NO_STREAM_PRIORITY") != nullptr;  // A/B
+    CK(cudaStreamCreateWithPriority(&w->own, cudaStreamNonBlocking, no_prio ? 0 : (i < 3 ? hi : lo)));
     w->stream = w->own;
     CS(cusolverDnCreate(&w->solver));
     CS(cusolverDnSetStream(w->solver, w->stream));

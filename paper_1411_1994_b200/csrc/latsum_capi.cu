@@ -2844,7 +2844,15 @@ int latsum_canonical_info(const latsum_canonical* can, int64_t dims[3], int64_t*
     if (dict_cols) dict_cols[l] = can->d[l];
   }
   if (rank) *rank = can->Mc;
-  if (merged_terms) *merged_terms = terms_host(*can).T;
+  if (merged_terms) {
+    try {  // waits for the host-side term merge (which reports its failure here)
+      *merged_terms = terms_host(*can).T;
+    } catch (const std::bad_alloc&) {
+      return LATSUM_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+      return LATSUM_ERR_INVALID_ARGUMENT;
+    }
+  }
   return LATSUM_OK;
 }
 

@@ -267,6 +267,14 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, int* v) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -317,7 +325,8 @@ __device__ __forceinline__ void drainw(uint32_t taddr, double* x) {
   int v[NG][W];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
-    if (W == 8) tmem_ld8(taddr + uint32_t(g * BN), v[g]);
+    if (W == 16) tmem_ld16(taddr + uint32_t(g * BN), v[g]);
+    else if (W == 8) tmem_ld8(taddr + uint32_t(g * BN), v[g]);
     else tmem_ld4(taddr + uint32_t(g * BN), v[g]);
   }
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -447,7 +456,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
       mbar_wait(tmem_full, uint32_t(np & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < EPI_COLS; c += 8) drainw<4, 8>(tq + uint32_t(c), hv + c);
+      for (int c = 0; c < EPI_COLS; c += 16) drainw<4, 16>(tq + uint32_t(c), hv + c);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0)
@@ -666,7 +675,7 @@ k_gemm_i8_2sm(const int8_t* __restrict__ As, const double* __restrict__ ra,
       mbar_wait(tmem_full, uint32_t(np & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < EPI_COLS; c += 8) drainw<4, 8>(tq + uint32_t(c), hv + c);
+      for (int c = 0; c < EPI_COLS; c += 16) drainw<4, 16>(tq + uint32_t(c), hv + c);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lead_empty);

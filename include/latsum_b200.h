@@ -128,7 +128,11 @@ int latsum_reference_quadrature(const latsum_reference* ref, double* nodes, doub
  * (c1,c2,c3), weight charge_d * w_ref.  Terms are ordered sublattice blocks first,
  * then defects, as add_concat builds them.  from_raw normalisation per block.
  *   sub_counts: nsub x 3 (number of shifts per mode); sub_shifts: concatenated in
- *   (s, mode) order; def_shifts: ndef x 3 row-major.                                 */
+ *   (s, mode) order; def_shifts: ndef x 3 row-major.
+ * Returns once the per-mode dictionaries are on the device; merging identical rank-1 terms
+ * continues on a library host thread (overlapping the caller's next calls, e.g. the RHOSVD
+ * eigensolves).  Every function that needs the merged terms waits for it (thread-safe);
+ * latsum_canonical_destroy joins it.                                                  */
 int latsum_canonical_assemble(latsum_ctx* ctx, const latsum_reference* ref, int64_t nsub,
                               const int64_t* sub_counts, const int64_t* sub_shifts,
                               const double* sub_charges, int64_t ndef, const int64_t* def_shifts,

@@ -29,7 +29,7 @@ enum {
   LATSUM_ERR_CUSOLVER = 4,
   LATSUM_ERR_OUT_OF_MEMORY = 5,
   LATSUM_ERR_LENGTH = 6,           /* std::length_error: dense guard (tensor3.hpp:101-105) */
-  LATSUM_ERR_NOT_IMPLEMENTED = 7,  /* NotImplementedError (quadrature.hpp:288-290) */
+  LATSUM_ERR_NOT_IMPLEMENTED = 7,  /* NotImplementedError (quadrature.hpp:110-112) */
   LATSUM_ERR_NCCL = 8,
   LATSUM_ERR_IO = 9                /* TensorIoError (tensor_io.hpp:27-29) */
 };
@@ -89,10 +89,10 @@ int latsum_ctx_set_profiling(latsum_ctx* ctx, int on);
 int64_t latsum_ctx_profile(latsum_ctx* ctx, char* buf, int64_t cap);
 
 /* ------------------------------------------------------------------ host rules (no GPU)
- * quadrature.hpp:303-341 build_quadrature (gauss branch); nodes/weights hold 2M+1 values. */
+ * quadrature.hpp:124-187 build_quadrature (gauss branch); nodes/weights hold 2M+1 values. */
 int latsum_build_quadrature(int family, double lambda, int M, double step_constant,
                             double shell_a, double shell_A, double* nodes, double* weights);
-/* quadrature.hpp:416-447 default_step_constant (53-point sweep, npts probe radii). */
+/* quadrature.hpp:238-269 default_step_constant (53-point sweep, npts probe radii). */
 double latsum_default_step_constant(int family, double lambda, int M, double shell_a,
                                     double shell_A, int npts);
 /* reference.hpp:84-93 reference_shell of the doubled grid of (N, box). */
@@ -137,6 +137,20 @@ int latsum_canonical_assemble(latsum_ctx* ctx, const latsum_reference* ref, int6
                               const int64_t* sub_counts, const int64_t* sub_shifts,
                               const double* sub_charges, int64_t ndef, const int64_t* def_shifts,
                               const double* def_charges, latsum_canonical** out);
+/* The same sum over an ORDERED list of product blocks, the general form of
+ * defected_sum's canonical branch (lattice_sum.hpp:339-384): block b is a Cartesian
+ * product of per-mode shift lists (blk_counts[b*3+l] shifts in mode l, concatenated in
+ * (b, mode) order in blk_shifts) with additive charge blk_charges[b], and contributes R
+ * terms at reference rank, in block order (add_concat).  A sublattice
+ * (assembled_sum_canonical / sublattice_union_sum), a defect cluster whose sites form a
+ * Cartesian product (defect_cluster_canonical's product_structure branch,
+ * lattice_sum.hpp:278-294,316-321, "multi-level reuse") and a single defect site
+ * (windowed_canonical, :148-157, counts 1 x 1 x 1) are all product blocks; a
+ * non-product cluster is passed as its sites, one 1 x 1 x 1 block each, in site order
+ * (:324-329).                                                                         */
+int latsum_canonical_assemble_blocks(latsum_ctx* ctx, const latsum_reference* ref, int64_t nblk,
+                                     const int64_t* blk_counts, const int64_t* blk_shifts,
+                                     const double* blk_charges, latsum_canonical** out);
 void latsum_canonical_destroy(latsum_canonical* can);
 /* M_c = rank of the canonical sum, d_l = distinct (merged) columns per mode, T = merged terms. */
 int latsum_canonical_info(const latsum_canonical* can, int64_t dims[3], int64_t* rank,
@@ -210,7 +224,7 @@ int latsum_sum_to_tucker(latsum_ctx* ctx, int family, double lambda, const int64
                          latsum_spectral_report* report);
 
 /* ------------------------------------------------------------------ tensors from / to host
- * CanonicalTensor(dims, weights, factors) (canonical.hpp:203-206): columns taken as given
+ * CanonicalTensor(dims, weights, factors) (canonical.hpp:25-29): columns taken as given
  * (the caller guarantees unit norms), so rhosvd / canonical_to_tucker accept any canonical
  * input, as the reference's do. */
 int latsum_canonical_from_host(latsum_ctx* ctx, const int64_t dims[3], int64_t rank,

@@ -110,7 +110,7 @@ struct UniformGrid {
   double mesh(int l) const { return box[l] / double(n[l]); }
 };
 
-// geometry.hpp:183-261 (the parts the hot path consumes).
+// geometry.hpp:15-121 (the parts the hot path consumes).
 enum class DefectKind { vacancy, impurity };
 struct DefectSpec {
   std::vector<Int3> sites;

@@ -28,7 +28,7 @@ constexpr int kYukawa = 1;
 
 double sqrt_pi() { return std::sqrt(M_PI); }
 
-// quadrature.hpp:251-263 (gauss_weight)
+// quadrature.hpp:73-85 (gauss_weight)
 double gauss_weight(int family, double lambda, double t) {
   if (family == kNewton) return 2.0 / sqrt_pi();
   if (t == 0.0) return 0.0;
@@ -42,7 +42,7 @@ double kernel_exact(int family, double lambda, double r) {
   return std::exp(-lambda * r) / r;
 }
 
-// quadrature.hpp:303-341 (build_quadrature, gauss branch)
+// quadrature.hpp:124-187 (build_quadrature, gauss branch)
 void build_quadrature(int family, double lambda, int M, double c0, double A, double* nodes,
                       double* weights) {
   const double h = c0 * std::log(double(M)) / double(M);
@@ -55,7 +55,7 @@ void build_quadrature(int family, double lambda, int M, double c0, double A, dou
   }
 }
 
-// quadrature.hpp:370-379 + 396-412 (separable_eval on (z,0,0), shell_error.pointwise_rel)
+// quadrature.hpp:191-201 + 217-234 (separable_eval on (z,0,0), shell_error.pointwise_rel)
 double shell_pointwise_rel(int family, double lambda, const double* nodes, const double* weights,
                            int R, double a, double A, int npts) {
   double pw = 0.0;
@@ -107,7 +107,7 @@ extern "C" {
 
 // ---------------------------------------------------------------- stage 1 (host part)
 
-// quadrature.hpp:303-341
+// quadrature.hpp:124-187
 int orc_build_quadrature(int family, double lambda, int M, double c0, double shell_a,
                          double shell_A, double* nodes, double* weights) {
   if (M < 2 || !(shell_a > 0.0) || !(shell_A > shell_a) || !(c0 > 0.0)) return 1;
@@ -115,7 +115,7 @@ int orc_build_quadrature(int family, double lambda, int M, double c0, double she
   return 0;
 }
 
-// quadrature.hpp:416-447 (default_step_constant, gauss family)
+// quadrature.hpp:238-269 (default_step_constant, gauss family)
 double orc_default_step_constant(int family, double lambda, int M, double shell_a,
                                  double shell_A, int npts) {
   const double base = std::asinh(2.5 * (shell_A / shell_a)) / std::log(double(M));

@@ -186,9 +186,7 @@ def side_matrices(ref: RefOracle, geom, max_bytes: float = 24e9):
     F = [np.zeros((N[l], Mc), order="F") for l in range(3)]
     w = np.zeros(Mc)
     col = 0
-    blocks = [(sub.shifts, sub.charge) for sub in geom.sublattices]
-    blocks += [([np.array([s[0]]), np.array([s[1]]), np.array([s[2]])], q)
-               for s, q in zip(geom.defect_shifts, geom.defect_charges)]
+    blocks = [(b.shifts, b.charge) for b in geom.blocks()]
     for shifts, charge in blocks:
         wb = charge * ref.weights
         for l in range(3):
@@ -291,10 +289,8 @@ def side_dictionary(ref: RefOracle, geom):
     the same columns, bit for bit, that the full N x M_c matrices hold — plus the M_c
     weights in reference order (sublattice blocks, then defects)."""
     N, R = geom.N, geom.R
-    blocks = [(tuple(np.asarray(x, np.int64) for x in sub.shifts), sub.charge)
-              for sub in geom.sublattices]
-    blocks += [((np.array([s[0]]), np.array([s[1]]), np.array([s[2]])), q)
-               for s, q in zip(geom.defect_shifts, geom.defect_charges)]
+    blocks = [(tuple(np.asarray(x, np.int64) for x in b.shifts), b.charge)
+              for b in geom.blocks()]
     Mc = R * len(blocks)
     w = np.zeros(Mc)
     sides = []

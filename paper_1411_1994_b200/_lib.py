@@ -87,6 +87,7 @@ SIGNATURES = [
     ("latsum_reference_weights", _I, [_P, _P]),
     ("latsum_reference_quadrature", _I, [_P, _P, _P]),
     ("latsum_canonical_assemble", _I, [_P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    ("latsum_canonical_assemble_blocks", _I, [_P, _P, _I64, _P, _P, _P, _P]),
     ("latsum_canonical_destroy", None, [_P]),
     ("latsum_canonical_info", _I, [_P, _P, _P, _P, _P]),
     ("latsum_canonical_weights", _I, [_P, _P]),

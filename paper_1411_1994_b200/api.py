@@ -23,6 +23,7 @@ made only when a method asks for them (``factor``, ``core``, ``to_dense``).
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 from typing import Optional, Sequence, Tuple
 
@@ -65,6 +66,9 @@ class Context:
             raise RuntimeError(f"latsum_ctx_create({device}) failed with status {st}: "
                                "a CUDA device is required (no CPU fallback)")
         self.device = device
+        # device objects made on this context: close() destroys them first, because their
+        # buffers are freed stream-ordered on the context's streams
+        self._children = weakref.WeakSet()
 
     @property
     def handle(self):
@@ -112,6 +116,8 @@ class Context:
 
     def close(self):
         if self._h:
+            for obj in list(getattr(self, "_children", ())):
+                obj._destroy()
             _lib.lib().latsum_ctx_destroy(self._h)
             self._h = ctypes.c_void_p()
 
@@ -240,6 +246,7 @@ class ReferenceTensor:
 
     def __init__(self, ctx: Context, handle, kernel: KernelSpec, N, box, M):
         self.ctx, self._h, self.kernel = ctx, handle, kernel
+        ctx._children.add(self)
         self.N, self.box, self.M = tuple(int(n) for n in N), tuple(float(b) for b in box), M
         rank, c0, shell = ctypes.c_int(), ctypes.c_double(), np.zeros(2)
         _lib.lib().latsum_reference_info(self._h, ctypes.byref(rank), ctypes.byref(c0), _p(shell))
@@ -265,11 +272,14 @@ class ReferenceTensor:
         _lib.check(_lib.lib().latsum_reference_quadrature(self._h, _p(t), _p(a)))
         return t, a
 
+    def _destroy(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_reference_destroy(self._h)
+            self._h = None
+
     def __del__(self):
         try:
-            if getattr(self, "_h", None):
-                _lib.lib().latsum_reference_destroy(self._h)
-                self._h = None
+            self._destroy()
         except Exception:  # interpreter shutdown
             pass
 
@@ -294,6 +304,7 @@ class CanonicalTensor:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self._h = ctx, handle
+        ctx._children.add(self)
         dims, dcols, rank = np.zeros(3, np.int64), np.zeros(3, np.int64), ctypes.c_int64()
         # merged_terms is not requested here: it waits for the host-side term merge that
         # the library overlaps with the RHOSVD's first kernels
@@ -306,7 +317,8 @@ class CanonicalTensor:
     def merged_terms(self) -> int:
         """Rank-1 terms left after merging identical ones (t and -t, repeated sites)."""
         T = ctypes.c_int64()
-        _lib.lib().latsum_canonical_info(self._h, None, None, None, ctypes.byref(T))
+        st = _lib.lib().latsum_canonical_info(self._h, None, None, None, ctypes.byref(T))
+        _lib.check(st)  # a failed background term merge surfaces here, not as 0 terms
         return int(T.value)
 
     @property
@@ -361,11 +373,14 @@ class CanonicalTensor:
         self.ctx.synchronize()
         return buf.cpu().numpy().reshape(shape, order="F")
 
+    def _destroy(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_canonical_destroy(self._h)
+            self._h = None
+
     def __del__(self):
         try:
-            if getattr(self, "_h", None):
-                _lib.lib().latsum_canonical_destroy(self._h)
-                self._h = None
+            self._destroy()
         except Exception:  # interpreter shutdown
             pass
 
@@ -375,6 +390,7 @@ class TuckerTensor:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self._h = ctx, handle
+        ctx._children.add(self)
         dims, ranks = np.zeros(3, np.int64), np.zeros(3, np.int64)
         _lib.lib().latsum_tucker_info(self._h, _p(dims), _p(ranks))
         self.dims = tuple(int(x) for x in dims)
@@ -426,11 +442,14 @@ class TuckerTensor:
                                                          _p(_i64(hi)), _p(out)))
         return out
 
+    def _destroy(self):
+        if getattr(self, "_h", None):
+            _lib.lib().latsum_tucker_destroy(self._h)
+            self._h = None
+
     def __del__(self):
         try:
-            if getattr(self, "_h", None):
-                _lib.lib().latsum_tucker_destroy(self._h)
-                self._h = None
+            self._destroy()
         except Exception:  # interpreter shutdown
             pass
 
@@ -448,14 +467,27 @@ def _shift_tables(geom: Geometry):
         _f64(geom.defect_charges)
 
 
+def _block_tables(geom: Geometry):
+    """Ordered product blocks (latsum_canonical_assemble_blocks): counts nblk x 3, the
+    shift lists concatenated in (block, mode) order, one charge per block."""
+    blocks = geom.blocks()
+    counts = np.array([[len(b.shifts[l]) for l in range(3)] for b in blocks],
+                      np.int64).reshape(-1, 3)
+    shifts = (np.concatenate([np.asarray(b.shifts[l], np.int64) for b in blocks
+                              for l in range(3)]) if blocks else np.zeros(0, np.int64))
+    charges = np.array([b.charge for b in blocks], np.float64)
+    return len(blocks), _i64(counts), _i64(shifts), _f64(charges)
+
+
 def lattice_sum(ref: ReferenceTensor, geom: Geometry) -> CanonicalTensor:
-    """Assembled sublattice sums plus additive defect windows (canonical, untruncated)."""
+    """Assembled sublattice sums plus additive defect blocks (canonical, untruncated):
+    lattice_sum.hpp:198-223, :339-384 canonical branch without a spec; product-structure
+    defect clusters stay at reference rank (:316-321)."""
     ctx = ref.ctx
-    nsub, counts, shifts, charges, dsh, dch = _shift_tables(geom)
+    nblk, counts, shifts, charges = _block_tables(geom)
     h = ctypes.c_void_p()
-    ctx.check(_lib.lib().latsum_canonical_assemble(
-        ctx.handle, ref.handle, nsub, _p(counts), _p(shifts), _p(charges), dsh.shape[0], _p(dsh),
-        _p(dch), ctypes.byref(h)))
+    ctx.check(_lib.lib().latsum_canonical_assemble_blocks(
+        ctx.handle, ref.handle, nblk, _p(counts), _p(shifts), _p(charges), ctypes.byref(h)))
     return CanonicalTensor(ctx, h)
 
 
@@ -591,7 +623,7 @@ def canonical_to_tucker(can: CanonicalTensor, spec: TruncationSpec, max_als_swee
 
 
 def canonical_from_arrays(weights, factors, ctx: Optional[Context] = None) -> CanonicalTensor:
-    """CanonicalTensor(dims, weights, factors) (canonical.hpp:203-206): unit columns as given."""
+    """CanonicalTensor(dims, weights, factors) (canonical.hpp:25-29): unit columns as given."""
     ctx = ctx or default_context()
     w = _f64(weights)
     F = [np.asfortranarray(f, dtype=np.float64) for f in factors]
@@ -628,7 +660,11 @@ def sum_to_tucker(geom: Geometry, tolerance: float, ctx: Optional[Context] = Non
     """cmd_sum's defected/sublattice path with a tolerance (commands.cpp:108-179) in one
     C-ABI call with host-resident inputs: stages 1-3, Tucker result on the device."""
     ctx = ctx or default_context()
-    nsub, counts, shifts, charges, dsh, dch = _shift_tables(geom)
+    if geom.defect_blocks is None:
+        nsub, counts, shifts, charges, dsh, dch = _shift_tables(geom)
+    else:  # ordered product blocks, all passed as sublattice-style blocks (same layout)
+        nsub, counts, shifts, charges = _block_tables(geom)
+        dsh, dch = _i64(np.zeros((0, 3), np.int64)), _f64(np.zeros(0))
     rep = _lib.LatsumReport()
     h = ctypes.c_void_p()
     ctx.check(_lib.lib().latsum_sum_to_tucker(

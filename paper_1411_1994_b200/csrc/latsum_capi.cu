@@ -16,6 +16,7 @@
 #include <mutex>
 #include <memory>
 #include <numeric>
+#include <set>
 #include <stdexcept>
 #include <exception>
 #include <fstream>
@@ -125,6 +126,7 @@ struct latsum_ctx {
   std::map<std::string, Stat> stats;
   // worker contexts (own stream + cuSOLVER handle) for the concurrent per-mode reductions
   latsum_ctx* sub[4] = {nullptr, nullptr, nullptr, nullptr};
+  latsum_ctx* parent = nullptr;  // set on worker contexts
   // multi-GPU: one rank of a row-sharded reduction (latsum_ctx_init_comm); each worker
   // context owns a communicator split from this one so concurrent modes never interleave
   ncclComm_t comm = nullptr;
@@ -298,6 +300,27 @@ struct RowBlock {
 };
 RowBlock row_block(const latsum_ctx* c, int64_t N) {
   return {N * c->rank / c->nranks, N * (c->rank + 1) / c->nranks};
+}
+
+// cudaFuncSetAttribute applies to the current device only: the large-shared-memory /
+// cluster opt-ins are made once per (kernel, device), under a lock (the RHOSVD worker
+// threads reach them concurrently).
+template <typename F>
+void once_per_device(const latsum_ctx* c, const void* key, F&& set) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({key, c->device})) return;
+  set();
+  done.insert({key, c->device});
+}
+
+template <typename K>
+void set_smem_attr(const latsum_ctx* c, K kernel, size_t bytes, bool cluster16 = false) {
+  once_per_device(c, reinterpret_cast<const void*>(kernel), [&] {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    if (cluster16) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
 }
 
 // ------------------------------------------------------------------ GEMM launcher
@@ -546,12 +569,7 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
   if (b.halves == 2) {  // 2-SM kernel: CTA pairs over (256-row, 128-column) tiles
-    static bool attr2 = false;
-    if (!attr2) {
-      CK(cudaFuncSetAttribute(oz::k_gemm_i8_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(oz::SMEM_BYTES2)));
-      attr2 = true;
-    }
+    set_smem_attr(c, oz::k_gemm_i8_2sm, oz::SMEM_BYTES2);
     const int64_t tiles_m2 = (a.tiles + 1) / 2, tiles2 = tiles_m2 * b.tiles;
     const unsigned pairs = unsigned(std::min<int64_t>(tiles2, sms / 2));
     cudaLaunchConfig_t cfg = {};
@@ -668,23 +686,12 @@ void sytrd_cluster(latsum_ctx* c, int64_t n, double* A, int64_t lda, double* d, 
   if (n <= 0) return;
   require(n < (int64_t(1) << 30), "sytrd: n too large");
   require(n <= 8192, "sytrd: n > 8192");
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(eig::k_sytrd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CK(cudaFuncSetAttribute(eig::k_sytrd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(2 * 8192 * sizeof(double))));
-    attr = true;
-  }
+  set_smem_attr(c, eig::k_sytrd_cluster, 2 * 8192 * sizeof(double), true);
   constexpr int kSmemMax = 227 * 1024 - 2048;  // dynamic share (the kernel has ~1 KB static)
   const bool smem = eig::sm_trd_doubles(int(n)) * int64_t(sizeof(double)) <= kSmemMax &&
                     n <= eig::TRD_CTAS * eig::SM_TRD_MAXCOL && !std::getenv("LATSUM_SYTRD_L2");
   if (smem) {  // trailing matrix resident in the cluster's shared memory
-    static bool attr2 = false;
-    if (!attr2) {
-      CK(cudaFuncSetAttribute(eig::k_sytrd_smem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      CK(cudaFuncSetAttribute(eig::k_sytrd_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-      attr2 = true;
-    }
+    set_smem_attr(c, eig::k_sytrd_smem, kSmemMax, true);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(eig::TRD_CTAS);
     cfg.blockDim = dim3(eig::SM_TRD_THREADS);
@@ -761,11 +768,6 @@ bool use_custom_eig(int64_t n) {
   return n >= 2 && n <= kCustomEigMax;
 }
 
-template <typename K>
-void set_smem_attr(K kernel, size_t bytes, bool cluster16 = false) {
-  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-  if (cluster16) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-}
 
 struct Eig {
   int64_t n = 0;
@@ -793,8 +795,7 @@ struct Eig {
       CK(cudaMemsetAsync(Vw.p, 0, sizeof(double) * Vw.n, c->stream));
       DBuf Wg(c, size_t(band::BW) * n);
       const size_t smem = band::s2b_smem_doubles(ni) * sizeof(double);
-      static std::once_flag once;
-      std::call_once(once, [&] { set_smem_attr(band::k_sy2sb, band::s2b_smem_doubles(band::S2B_NMAX) * 8, true); });
+      set_smem_attr(c, band::k_sy2sb, band::s2b_smem_doubles(band::S2B_NMAX) * 8, true);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(band::S2B_CTAS);
       cfg.blockDim = dim3(band::S2B_THREADS);
@@ -829,8 +830,7 @@ struct Eig {
     }
     {
       const size_t smem = band::sb_smem_doubles(ni) * sizeof(double);
-      static std::once_flag once;
-      std::call_once(once, [&] { set_smem_attr(band::k_sb2st, band::sb_smem_doubles(band::SB_NMAX) * 8); });
+      set_smem_attr(c, band::k_sb2st, band::sb_smem_doubles(band::SB_NMAX) * 8);
       ProfScope ps(c, "eig_sb2st", double(n) * double(n));
       static const bool sprof = std::getenv("LATSUM_SB2ST_PROF") != nullptr;
       DBuf pb(c, 4);
@@ -881,10 +881,7 @@ struct Eig {
       else sytrd_cluster(c, n, G.p, n, d.p, e.p, tau.p);
       ProfScope ps(c, "eig_values", double(n));
       const size_t smem = size_t(2 * n) * sizeof(double);
-      static std::once_flag once;
-      std::call_once(once, [&] {
-        set_smem_attr(band::k_tridiag_eigvals_ms, size_t(2 * kCustomEigMax) * sizeof(double));
-      });
+      set_smem_attr(c, band::k_tridiag_eigvals_ms, size_t(2 * kCustomEigMax) * sizeof(double));
       band::k_tridiag_eigvals_ms<<<unsigned((n + band::EV_WARPS - 1) / band::EV_WARPS),
                                    32 * band::EV_WARPS, smem, c->stream>>>(d.p, e.p, int(n), W.p);
       post_launch(c);
@@ -911,8 +908,7 @@ struct Eig {
         ProfScope ps(c, "eig_invit", double(n) * double(k));
         const int64_t per = 41 * n;  // bytes per vector: 5 doubles + 1 flag per row
         const int nt = int(std::max<int64_t>(1, std::min<int64_t>(32, (227 * 1024 - 1024) / per)));
-        static std::once_flag once;
-        std::call_once(once, [&] { set_smem_attr(band::k_tridiag_invit_sm, 227 * 1024 - 1024); });
+        set_smem_attr(c, band::k_tridiag_invit_sm, 227 * 1024 - 1024);
         band::k_tridiag_invit_sm<<<unsigned((k + nt - 1) / nt), unsigned(nt), size_t(nt) * per,
                                    c->stream>>>(d.p, e.p, int(n), dl.p, int(k), tnorm, V);
         post_launch(c);
@@ -927,8 +923,7 @@ struct Eig {
         };
         const int dbuf = bt_smem(2) <= kBtMax ? 1 : 0;
         const size_t smem = bt_smem(dbuf ? 2 : 1);
-        static std::once_flag once;
-        std::call_once(once, [&] { set_smem_attr(band::k_band_backtransform, kBtMax); });
+        set_smem_attr(c, band::k_band_backtransform, kBtMax);
         band::k_band_backtransform<<<unsigned((k + band::BT_CPB - 1) / band::BT_CPB), band::BT_THREADS,
                                      smem, c->stream>>>(int(n), int(k), V2.p, TAU2.p, KS, Vw.p, Tw.p,
                                                         band::s2b_panels(int(n)), V, V, dbuf);
@@ -1084,10 +1079,14 @@ const latsum_canonical& terms(latsum_ctx* c, const latsum_canonical& cc) {
   std::lock_guard<std::mutex> g(can.terms_mu);
   if (can.terms_uploaded) return cc;
   can.terms_ready.get();
-  for (int l = 0; l < 3; ++l) can.dtc[l].upload(c, can.tc[l]);
-  can.dtw.upload(c, can.tw);
-  can.dtseg.upload(c, can.tseg);
-  CK(cudaStreamSynchronize(c->stream));  // later users may sit on other streams
+  // owned by the caller's (root) context stream, whichever worker needs them first: they
+  // are freed on that stream when the canonical tensor is destroyed
+  latsum_ctx* root = c;
+  while (root->parent) root = root->parent;
+  for (int l = 0; l < 3; ++l) can.dtc[l].upload(root, can.tc[l]);
+  can.dtw.upload(root, can.tw);
+  can.dtseg.upload(root, can.tseg);
+  CK(cudaStreamSynchronize(root->stream));  // later users may sit on other streams
   can.terms_uploaded = true;
   return cc;
 }
@@ -1260,31 +1259,34 @@ void merge_terms(latsum_canonical& can) {
   }
 }
 
-void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const int64_t* sub_counts,
-              const int64_t* sub_shifts, const double* sub_charges, int64_t ndef,
-              const int64_t* def_shifts, const double* def_charges, latsum_canonical& can) {
-  require(nsub >= 0 && ndef >= 0, "assemble: negative counts");
+// Ordered product blocks (the general form of every stage-2 input): block b contributes R
+// terms whose mode-l vector is the assembled sum over its mode-l shift list, weight
+// charge_b * w_ref.  A sublattice, a product-structure defect cluster and a single defect
+// site (counts 1 x 1 x 1, windowed_canonical) are all product blocks.
+void assemble_blocks(latsum_ctx* c, const latsum_reference& ref, int64_t nblk,
+                     const int64_t* blk_counts, const int64_t* blk_shifts,
+                     const double* blk_charges, latsum_canonical& can) {
+  require(nblk >= 0, "assemble: negative counts");
   Trace::mark(c, "assemble: start", false);
   const int R = ref.R, Rd = ref.Rd;
   can.R = R;
   can.Rd = Rd;
-  const int64_t nblk = nsub + ndef;
   can.Mc = int64_t(R) * nblk;
   for (int l = 0; l < 3; ++l) can.N[l] = ref.N[l];
 
-  // per-mode placements: sublattices first, then distinct defect shifts
+  // per-mode placements: multi-shift lists first, then distinct single shifts
   std::vector<int64_t> block_pl[3];
   DBuf norm_buf[3];
-  std::vector<int64_t> sub_off(size_t(nsub) * 3 + 1, 0);
+  std::vector<int64_t> blk_off(size_t(nblk) * 3 + 1, 0);
   {
     int64_t o = 0;
-    for (int64_t s = 0; s < nsub; ++s)
+    for (int64_t s = 0; s < nblk; ++s)
       for (int l = 0; l < 3; ++l) {
-        sub_off[s * 3 + l] = o;
-        require(sub_counts[s * 3 + l] >= 1, "assembled_vector: empty active set");
-        o += sub_counts[s * 3 + l];
+        blk_off[s * 3 + l] = o;
+        require(blk_counts[s * 3 + l] >= 1, "assembled_vector: empty active set");
+        o += blk_counts[s * 3 + l];
       }
-    sub_off[size_t(nsub) * 3] = o;
+    blk_off[size_t(nblk) * 3] = o;
   }
   for (int l = 0; l < 3; ++l) {
     const int64_t N = ref.N[l];
@@ -1311,13 +1313,15 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
       seen.emplace(std::move(sh), p);
       return p;
     };
-    for (int64_t s = 0; s < nsub; ++s) {
-      const int64_t* sh = sub_shifts + sub_off[s * 3 + l];
-      block_pl[l][s] = place(std::vector<int64_t>(sh, sh + sub_counts[s * 3 + l]));
+    for (int64_t s = 0; s < nblk; ++s) {
+      if (blk_counts[s * 3 + l] == 1) continue;
+      const int64_t* sh = blk_shifts + blk_off[s * 3 + l];
+      block_pl[l][s] = place(std::vector<int64_t>(sh, sh + blk_counts[s * 3 + l]));
     }
-    const int64_t P_sub = int64_t(pl_off.size()) - 1;  // sublattice placements come first
-    for (int64_t dd = 0; dd < ndef; ++dd)
-      block_pl[l][nsub + dd] = place(std::vector<int64_t>{def_shifts[dd * 3 + l]});
+    const int64_t P_sub = int64_t(pl_off.size()) - 1;  // multi-shift placements come first
+    for (int64_t s = 0; s < nblk; ++s)
+      if (blk_counts[s * 3 + l] == 1)
+        block_pl[l][s] = place(std::vector<int64_t>{blk_shifts[blk_off[s * 3 + l]]});
     const int64_t P = int64_t(pl_off.size()) - 1;
     can.d[l] = P * Rd;
     if (can.d[l] == 0) continue;
@@ -1367,14 +1371,14 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
   CK(cudaStreamSynchronize(c->stream));
 
   Trace::mark(c, "assemble: dictionaries done", false);
-  // terms in reference order (add_concat: sublattice blocks, then defects)
+  // terms in reference order (add_concat: the blocks in the caller's order)
   can.weights.resize(can.Mc);
   for (int l = 0; l < 3; ++l) {
     can.term_col[l].resize(can.Mc);
     can.mult[l].assign(can.d[l], 0.0);
   }
   for (int64_t b = 0; b < nblk; ++b) {
-    const double charge = b < nsub ? sub_charges[b] : def_charges[b - nsub];
+    const double charge = blk_charges[b];
     for (int k = 0; k < R; ++k) {
       const int64_t q = b * R + k;
       double w = charge * ref.weights[k];
@@ -1394,6 +1398,30 @@ void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const in
     require(can.d[l] < (int64_t(1) << 21), "assemble: too many distinct columns in a mode");
   can.terms_async = true;
   can.terms_ready = std::async(std::launch::async, [&can] { merge_terms(can); }).share();
+}
+
+// Sublattice blocks, then single-site defects (the latsum_canonical_assemble layout).
+void assemble(latsum_ctx* c, const latsum_reference& ref, int64_t nsub, const int64_t* sub_counts,
+              const int64_t* sub_shifts, const double* sub_charges, int64_t ndef,
+              const int64_t* def_shifts, const double* def_charges, latsum_canonical& can) {
+  require(nsub >= 0 && ndef >= 0, "assemble: negative counts");
+  const int64_t nblk = nsub + ndef;
+  std::vector<int64_t> counts(size_t(nblk) * 3, 1), shifts;
+  std::vector<double> charges(static_cast<size_t>(nblk), 0.0);
+  int64_t o = 0;
+  for (int64_t s = 0; s < nsub; ++s)
+    for (int l = 0; l < 3; ++l) {
+      counts[s * 3 + l] = sub_counts[s * 3 + l];
+      require(sub_counts[s * 3 + l] >= 1, "assembled_vector: empty active set");
+      shifts.insert(shifts.end(), sub_shifts + o, sub_shifts + o + sub_counts[s * 3 + l]);
+      o += sub_counts[s * 3 + l];
+    }
+  for (int64_t s = 0; s < nsub; ++s) charges[s] = sub_charges[s];
+  for (int64_t dd = 0; dd < ndef; ++dd) {
+    for (int l = 0; l < 3; ++l) shifts.push_back(def_shifts[dd * 3 + l]);
+    charges[nsub + dd] = def_charges[dd];
+  }
+  assemble_blocks(c, ref, nblk, counts.data(), shifts.data(), charges.data(), can);
 }
 
 void materialize_factor(latsum_ctx* c, const latsum_canonical& can, int l, double* dst_device) {
@@ -1892,6 +1920,7 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
   if (!c->sub[i]) {
     auto* w = new latsum_ctx();
     w->device = c->device;
+    w->parent = c;
     // workers 0-2 carry the RHOSVD modes' latency-bound eigensolver chains: highest
     // priority; worker 3 (norm_f, one throughput kernel off the critical path): lowest
     int lo = 0, hi = 0;
@@ -2830,6 +2859,19 @@ int latsum_canonical_assemble(latsum_ctx* c, const latsum_reference* ref, int64_
     auto can = std::make_unique<latsum_canonical>();
     assemble(c, *ref, nsub, sub_counts, sub_shifts, sub_charges, ndef, def_shifts, def_charges,
              *can);
+    *out = can.release();
+  });
+}
+
+int latsum_canonical_assemble_blocks(latsum_ctx* c, const latsum_reference* ref, int64_t nblk,
+                                     const int64_t* blk_counts, const int64_t* blk_shifts,
+                                     const double* blk_charges, latsum_canonical** out) {
+  return guarded(c, [&] {
+    require(ref && out, "latsum_canonical_assemble_blocks: null argument");
+    require(nblk == 0 || (blk_counts && blk_shifts && blk_charges),
+            "latsum_canonical_assemble_blocks: null block table");
+    auto can = std::make_unique<latsum_canonical>();
+    assemble_blocks(c, *ref, nblk, blk_counts, blk_shifts, blk_charges, *can);
     *out = can.release();
   });
 }

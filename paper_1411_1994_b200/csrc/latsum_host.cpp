@@ -94,7 +94,7 @@ class HostPool {
 };
 
 double transform_weight(int family, double lambda, double t) {
-  // quadrature.hpp:251-263: p(z) = int_0^inf w(t) exp(-z^2 t^2) dt
+  // quadrature.hpp:73-85: p(z) = int_0^inf w(t) exp(-z^2 t^2) dt
   const double c = 2.0 / std::sqrt(M_PI);
   if (family == LATSUM_NEWTON) return c;
   if (t == 0.0) return 0.0;
@@ -108,7 +108,7 @@ double closed_form(int family, double lambda, double r) {
 }
 
 void sinc_rule(int family, double lambda, int M, double c0, double A, double* t, double* a) {
-  // quadrature.hpp:326-341: u_k = (k - M) h_M, t_k = sinh(u_k)/A,
+  // quadrature.hpp:155-163: u_k = (k - M) h_M, t_k = sinh(u_k)/A,
   // a_k = (h_M/2) w(|t_k|) cosh(u_k)/A, h_M = C0 log(M)/M
   const double hM = c0 * std::log(double(M)) / double(M);
   for (int k = 0; k < 2 * M + 1; ++k) {
@@ -121,7 +121,7 @@ void sinc_rule(int family, double lambda, int M, double c0, double A, double* t,
 
 double max_pointwise_rel(int family, double lambda, const double* t, const double* a, int R,
                          double lo, double hi, int npts) {
-  // quadrature.hpp:396-412 (shell_error) with separable_eval (:370-379) at (z,0,0)
+  // quadrature.hpp:217-234 (shell_error) with separable_eval (:191-201) at (z,0,0)
   const double la = std::log(lo), lA = std::log(hi);
   double worst = 0.0;
   for (int i = 0; i < npts; ++i) {
@@ -158,7 +158,7 @@ int latsum_build_quadrature(int family, double lambda, int M, double step_consta
 
 double latsum_default_step_constant(int family, double lambda, int M, double shell_a,
                                     double shell_A, int npts) {
-  // quadrature.hpp:416-447: 53 candidates base*(0.5 + 1.3 i/52),
+  // quadrature.hpp:238-269: 53 candidates base*(0.5 + 1.3 i/52),
   // base = asinh(2.5 A/a)/log M; first strict minimum of the finite errors.
   if (npts <= 1) npts = 320;
   // The 53 candidates are independent: evaluate them on host threads, then pick the

@@ -13,7 +13,7 @@ maps it to integer mesh shifts in two places:
 lattice whose spacing is not a whole number of mesh cells into a box larger
 than the lattice, which the reference cannot express; `cubic` and
 `baseline` therefore snap every site position to the grid with the
-reference's own rule (``grid.hpp:145-159`` snap_to_grid: round half away from
+reference's own rule (``grid.hpp:120-135`` snap_to_grid: round half away from
 zero) and keep the lattice rank-preserving per mode because the site set is
 still a tensor product per sublattice.
 
@@ -46,10 +46,15 @@ class Geometry:
     family: int = NEWTON
     lam: float = 0.0
     M: int = 16
-    C0: float = 0.0  # <= 0: calibrated sweep (quadrature.hpp:416-447)
+    C0: float = 0.0  # <= 0: calibrated sweep (quadrature.hpp:238-269)
     sublattices: List[Sublattice] = field(default_factory=list)
     defect_shifts: np.ndarray = field(default_factory=lambda: np.zeros((0, 3), np.int64))
     defect_charges: np.ndarray = field(default_factory=lambda: np.zeros((0,), np.float64))
+    # Defects in DefectSpec order as product blocks (lattice_sum.hpp:297-330): a cluster
+    # whose sites form a Cartesian product is ONE block at reference rank
+    # (product_structure), any other cluster one 1 x 1 x 1 block per site.  None: every
+    # defect is the single site of the matching defect_shifts row.
+    defect_blocks: Optional[List[Sublattice]] = None
     eps: Optional[float] = None  # RHOSVD tolerance (None: no truncation)
     eval_lo: Tuple[int, int, int] = (0, 0, 0)
     eval_hi: Optional[Tuple[int, int, int]] = None
@@ -66,12 +71,25 @@ class Geometry:
 
     @property
     def n_defects(self) -> int:
+        """Defect blocks: product clusters count once, other sites one each."""
+        if self.defect_blocks is not None:
+            return len(self.defect_blocks)
         return int(self.defect_shifts.shape[0])
 
     @property
     def canonical_rank(self) -> int:
-        """M_c = R * (#sublattices + #defects): rank of the unreduced sum."""
+        """M_c = R * (#sublattices + #defect blocks): rank of the unreduced sum."""
         return self.R * (len(self.sublattices) + self.n_defects)
+
+    def blocks(self) -> List[Sublattice]:
+        """Every product block in add_concat order: the sublattices, then the defects."""
+        out = list(self.sublattices)
+        if self.defect_blocks is not None:
+            out += list(self.defect_blocks)
+        else:
+            out += [Sublattice(tuple(np.array([s[l]], np.int64) for l in range(3)), float(q))
+                    for s, q in zip(self.defect_shifts, self.defect_charges)]
+        return out
 
     @property
     def n_sites(self) -> int:
@@ -92,7 +110,7 @@ class Geometry:
                           c.transpose(2, 1, 0).ravel()], axis=1)
             shifts.append(s)
             weights.append(np.full(s.shape[0], sub.charge))
-        if self.n_defects:
+        if self.defect_shifts.shape[0]:
             shifts.append(self.defect_shifts)
             weights.append(self.defect_charges)
         return (np.ascontiguousarray(np.concatenate(shifts).astype(np.int64)),
@@ -105,7 +123,7 @@ def default_active_set(cells: int) -> np.ndarray:
 
 
 def snap(x: np.ndarray, h: float) -> np.ndarray:
-    """grid.hpp:155: std::round (half away from zero) of x/h."""
+    """grid.hpp:131: std::round (half away from zero) of x/h."""
     q = np.asarray(x, dtype=np.float64) / h
     return (np.sign(q) * np.floor(np.abs(q) + 0.5)).astype(np.int64)
 
@@ -113,6 +131,21 @@ def snap(x: np.ndarray, h: float) -> np.ndarray:
 def lround(x: float) -> int:
     """std::lround: round half away from zero."""
     return int(np.sign(x) * np.floor(abs(x) + 0.5))
+
+
+def product_structure(sites: Sequence[Sequence[int]]):
+    """lattice_sum.hpp:278-294: the per-mode sorted index sets if the sites form their
+    full Cartesian product (every combination present, none repeated), else None."""
+    axes = [sorted({int(s[l]) for s in sites}) for l in range(3)]
+    if len(axes[0]) * len(axes[1]) * len(axes[2]) != len(sites):
+        return None
+    have = {tuple(int(v) for v in s) for s in sites}
+    for a in axes[0]:
+        for b in axes[1]:
+            for c in axes[2]:
+                if (a, b, c) not in have:
+                    return None
+    return axes
 
 
 def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0, *,
@@ -127,8 +160,10 @@ def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0,
     lattice_grid (lattice_sum.hpp:75-86): N_l = n * L_l, box_l = b * L_l.
     Base shifts c = k n (assembled_sum_canonical, :198-223); sublattice shifts
     c = k n + lround(offset n) (:444); defect shifts c = site n + lround(grid_offset)
-    (:159-164).  `defects` entries are (sites, charge, grid_offset); each site
-    becomes its own R-term block in site order (lattice_sum.hpp:324-329).
+    (:159-164).  `defects` entries are (sites, charge, grid_offset): a cluster whose
+    sites form a Cartesian product is one R-term block over the per-mode sorted index sets
+    (product_structure, :316-321); any other cluster contributes one R-term block per site
+    in site order (:324-329).
     """
     grid_cells = list(parent_cells) if parent_cells is not None else list(cells)
     N = tuple(int(n_per_cell * c) for c in grid_cells)
@@ -144,15 +179,26 @@ def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0,
             ks = [default_active_set(sub_cells[l]) for l in range(3)]
             subs.append(Sublattice(tuple(ks[l] * n_per_cell + lround(off[l] * n_per_cell)
                                          for l in range(3)), base_charge))
-    dsh, dch = [], []
+    dsh, dch, dblk = [], [], []
     for sites, charge, goff in defects:
         goff = goff if goff is not None else (0.0, 0.0, 0.0)
+        if not len(sites):
+            raise ValueError("defected_sum: defect with no sites")
+        off = [lround(goff[l]) for l in range(3)]
         for s in sites:
-            dsh.append([int(s[l]) * n_per_cell + lround(goff[l]) for l in range(3)])
+            dsh.append([int(s[l]) * n_per_cell + off[l] for l in range(3)])
             dch.append(float(charge))
+        axes = product_structure(sites) if len(sites) > 1 else None
+        if axes is not None:  # assembled cluster: rank stays at the reference rank
+            dblk.append(Sublattice(tuple(np.asarray(axes[l], np.int64) * n_per_cell + off[l]
+                                         for l in range(3)), float(charge)))
+        else:
+            dblk += [Sublattice(tuple(np.array([int(s[l]) * n_per_cell + off[l]], np.int64)
+                                      for l in range(3)), float(charge)) for s in sites]
     return Geometry(N=N, box=box, family=family, lam=lam, M=M, C0=C0, sublattices=subs,
                     defect_shifts=np.asarray(dsh, np.int64).reshape(-1, 3),
-                    defect_charges=np.asarray(dch, np.float64), eps=eps, name=name)
+                    defect_charges=np.asarray(dch, np.float64),
+                    defect_blocks=dblk if len(dblk) != len(dsh) else None, eps=eps, name=name)
 
 
 def _sample_sites(n_sites: int, count: int, seed: int) -> np.ndarray:

@@ -2,7 +2,7 @@
 
   cell_integrals.json  50-digit integrals of exp(-s x^2) over double-valued cells
                        [lo, lo + h] of the BASELINE doubled grids (reference.hpp:33-54)
-  quadrature.json      40-digit sinc nodes/weights (quadrature.hpp:326-341) evaluated
+  quadrature.json      40-digit sinc nodes/weights (quadrature.hpp:155-163) evaluated
                        from the same double-valued step and abscissae the code forms,
                        plus the calibrated C0 and an independent 4-digit C0 probe value
                        (SURVEY 8a row a2).

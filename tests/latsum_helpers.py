@@ -25,6 +25,17 @@ def mini(kind: str, seed: int = 7):
         return W.lattice_box(256, 20.0, [dict(cells=(12, 12, 12), step=(1, 1, 1))], M=12,
                              n_vacancies=10, n_impurities=10, q_range=(0.0, 2.0), eps=1e-8,
                              seed=seed, name="mini5")
+    if kind == "clusters":     # reference API geometry with defect clusters (lattice_sum.hpp:297-330):
+        # two product clusters (assembled at rank R), a ragged L-shaped one (per site) and an
+        # off-grid impurity, in DefectSpec order
+        block = [(a, b, 0) for a in (-2, -1) for b in (0, 1)]
+        slab = [(a, 2, c) for a in (1, 2, 3) for c in (-1, 0)]
+        ragged = [(2, -2, 1), (2, -3, 1), (3, -2, 1)]
+        g = W.from_lattice((8, 8, 4), 16, M=10, defects=[
+            (block, -1.0, None), (ragged, -1.0, None), (slab, 0.5, None),
+            ([(0, 0, 0)], 0.75, (3.0, -2.0, 1.0))], eps=1e-7, name="clusters")
+        assert g.n_defects == 1 + 3 + 1 + 1
+        return g
     raise ValueError(kind)
 
 

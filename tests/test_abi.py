@@ -58,7 +58,7 @@ def test_context_without_device_fails_loudly():
 
 
 def test_host_step_constant_matches_oracle_across_threads():
-    """quadrature.hpp:416-447 (default_step_constant) in the library — evaluated on its
+    """quadrature.hpp:238-269 (default_step_constant) in the library — evaluated on its
     persistent host worker pool — equals the oracle's sequential sweep bit for bit, for the
     five BASELINE configurations, also when several host threads call it at once."""
     import threading

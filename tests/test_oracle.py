@@ -142,7 +142,7 @@ def test_golden_cell_integrals():
 
 
 def test_golden_quadrature_and_step_constants():
-    """Nodes/weights against 40-digit mpmath evaluation of quadrature.hpp:326-341 at the
+    """Nodes/weights against 40-digit mpmath evaluation of quadrature.hpp:155-163 at the
     oracle's C0; C0 itself against the survey's independent probe (4 digits)."""
     data = json.load(open(os.path.join(GOLDEN, "quadrature.json")))
     for rec in data["configs"]:
@@ -171,7 +171,7 @@ def test_active_sets_and_snap():
 
 
 def test_window_overflow_is_detected():
-    """grid.hpp:129-138: a shift pushing the window out of the doubled grid."""
+    """grid.hpp:104-114: a shift pushing the window out of the doubled grid."""
     col = np.ones(16)
     O.assembled_vector(col, 8, np.array([4]))
     with pytest.raises(OverflowError):
@@ -219,15 +219,52 @@ def test_vacancy_is_base_minus_window():
     assert _probe_err(F, w, ref, g, 400, 6) < 1e-12
 
 
-def test_ragged_and_offgrid_defects():
-    """test_lattice_sum.cpp:273-330 (ragged clusters, off-grid snapped impurity)."""
-    g = W.from_lattice((8, 8, 1), 8, M=8, defects=[
-        ([(0, 0, 0), (0, 1, 0), (1, 0, 0), (1, 1, 0)], -1.0, None),
-        ([(2, 2, 0), (2, 3, 0), (3, 2, 0)], -1.0, None),
-        ([(0, 0, 0)], 0.5, (3.0, -2.0, 0.0))])
+BLOCK_2x2 = [(0, 0, 0), (0, 1, 0), (1, 0, 0), (1, 1, 0)]
+RAGGED_L = [(2, 2, 0), (2, 3, 0), (3, 2, 0)]
+
+
+def test_product_structure_detection():
+    """lattice_sum.hpp:278-294: full Cartesian products only (every combination once)."""
+    assert W.product_structure(BLOCK_2x2) == [[0, 1], [0, 1], [0]]
+    assert W.product_structure(RAGGED_L) is None
+    assert W.product_structure([(0, 0, 0), (0, 0, 0)]) is None  # repeated site
+    assert W.product_structure([(5, -1, 2)]) == [[5], [-1], [2]]
+    assert W.product_structure([(a, b, c) for c in (1, 3) for b in (0, 2, 4) for a in (-1, 7)]) \
+        == [[-1, 7], [0, 2, 4], [1, 3]]
+
+
+def test_rectangular_clusters_assemble_at_reference_rank():
+    """test_lattice_sum.cpp:273-305: the 2 x 2 x 1 vacancy block is assembled (rank 2R, not
+    4 windows), the L-shaped triple has no product structure (rank (1+3)R), and both
+    forms agree with the brute-force oracle."""
+    R = 17
+    g1 = W.from_lattice((8, 8, 1), 8, M=8, defects=[(BLOCK_2x2, -1.0, None)])
+    assert g1.canonical_rank == 2 * R
+    g2 = W.from_lattice((8, 8, 1), 8, M=8, defects=[(RAGGED_L, -1.0, None)])
+    assert g2.canonical_rank == (1 + 3) * R
+    g = W.from_lattice((8, 8, 1), 8, M=8, defects=[(BLOCK_2x2, -1.0, None),
+                                                    (RAGGED_L, -1.0, None)])
     ref = O.reference(g)
     F, w = O.side_matrices(ref, g)
+    assert w.size == (1 + 1 + 3) * R == g.canonical_rank
     assert _probe_err(F, w, ref, g, 200, 12) < 1e-11
+    # the assembled cluster block equals the sum of its four windows
+    gs = W.from_lattice((8, 8, 1), 8, M=8)
+    gs.defect_shifts, gs.defect_charges = g.defect_shifts[:4], g.defect_charges[:4]
+    Fs, ws = O.side_matrices(ref, gs)
+    pr = O.probes(g.N, 300, 5)
+    blk = O.canonical_entries([f[:, R:2 * R] for f in F], w[R:2 * R], pr)
+    four = O.canonical_entries([f[:, R:] for f in Fs], ws[R:], pr)
+    assert np.max(np.abs(blk - four)) <= 1e-12 * np.max(np.abs(four))
+
+
+def test_offgrid_defect_snaps_to_grid():
+    """test_lattice_sum.cpp:308-330 (off-grid impurity at grid_offset (3, -2, 0))."""
+    g = W.from_lattice((4, 4, 1), 8, M=8, defects=[([(0, 0, 0)], 0.5, (3.0, -2.0, 0.0))])
+    assert g.defect_shifts.tolist() == [[3, -2, 0]]
+    ref = O.reference(g)
+    F, w = O.side_matrices(ref, g)
+    assert _probe_err(F, w, ref, g, 200, 14) < 1e-11
 
 
 def test_hexagonal_union_matches_brute_force():

@@ -57,7 +57,7 @@ def test_stage1_zero_node_and_mirror(ctx):
 
 # ----------------------------------------------------------------------------- stage 2
 
-@pytest.mark.parametrize("kind", ["cubic", "vacancies", "yukawa", "hex", "mixed"])
+@pytest.mark.parametrize("kind", ["cubic", "vacancies", "yukawa", "hex", "mixed", "clusters"])
 def test_stage2_side_matrices_match_oracle(ctx, kind):
     g = mini(kind)
     ref, oref = _ref_pair(ctx, g)
@@ -105,6 +105,32 @@ def test_stage2_vacancy_is_base_minus_window(ctx):
     lhs = cv.entries(pr)
     rhs = cb.entries(pr) - cw.entries(pr)
     assert np.max(np.abs(lhs - rhs)) / np.max(np.abs(lhs)) < 1e-12
+
+
+def test_stage2_rectangular_clusters_assemble_at_reference_rank(ctx):
+    """test_lattice_sum.cpp:273-305 through the C ABI: a 2 x 2 x 1 vacancy block is one
+    assembled block (rank 2R), an L-shaped triple three windows (rank (1+3)R), and both
+    match the brute-force oracle."""
+    block = [(0, 0, 0), (0, 1, 0), (1, 0, 0), (1, 1, 0)]
+    ragged = [(2, 2, 0), (2, 3, 0), (3, 2, 0)]
+    g0 = W.from_lattice((8, 8, 1), 8, M=8)
+    ref = api.reference_for(g0, ctx)
+    R = ref.rank
+    c1 = api.lattice_sum(ref, W.from_lattice((8, 8, 1), 8, M=8, defects=[(block, -1.0, None)]))
+    assert c1.rank == 2 * R
+    c2 = api.lattice_sum(ref, W.from_lattice((8, 8, 1), 8, M=8, defects=[(ragged, -1.0, None)]))
+    assert c2.rank == (1 + 3) * R
+    g = W.from_lattice((8, 8, 1), 8, M=8, defects=[(block, -1.0, None), (ragged, -1.0, None)])
+    both = api.lattice_sum(ref, g)
+    assert both.rank == (1 + 1 + 3) * R
+    oref = O.reference(g)
+    pr = O.probes(g.N, 200, 12)
+    want = O.oracle_entries(oref, g, pr)
+    assert np.max(np.abs(both.entries(pr) - want) / np.abs(want)) < 1e-11
+    F, w = O.side_matrices(oref, g)
+    for l in range(3):
+        assert col_rel_linf(both.factor(l), F[l]) < DIR_TOL
+    np.testing.assert_allclose(both.weights, w, rtol=1e-12, atol=0)
 
 
 def test_stage2_window_overflow_names_mode(ctx):
@@ -157,7 +183,7 @@ def _check_rhosvd(ctx, g, deflate="auto", probes=400):
     return t, rep, orc
 
 
-@pytest.mark.parametrize("kind", ["vacancies", "yukawa", "hex", "mixed"])
+@pytest.mark.parametrize("kind", ["vacancies", "yukawa", "hex", "mixed", "clusters"])
 def test_stage3_rhosvd_ranks_and_values(ctx, kind):
     _check_rhosvd(ctx, mini(kind))
 

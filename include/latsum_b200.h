@@ -201,6 +201,15 @@ int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out)
 /* TuckerTensor::core() (r1 x r2 x r3, first index fastest) and factor(mode) (N_l x r_l). */
 int latsum_tucker_core(latsum_ctx* ctx, const latsum_tucker* t, double* core);
 int latsum_tucker_factor(latsum_ctx* ctx, const latsum_tucker* t, int mode, double* factor);
+/* The projected canonical form of a factors-only tensor (no dense core; BASELINE cfg5):
+ * V(i,j,k) = sum_t w_t prod_l (U_l P_l)(i_l, c_l(t)), equal to the Tucker tensor (SURVEY
+ * 8c "projected-CP identity"; rank_reduction.hpp:88-100 before the core loop).  Fills
+ * d[3] (merged columns per mode) and *T (merged rank-1 terms); each non-null buffer gets
+ * P_l (r_l x d_l, column-major), the terms' column indices c_l (T) and weights w (T).
+ * Call with null buffers first to size them.                                          */
+int latsum_tucker_projected_form(latsum_ctx* ctx, const latsum_tucker* t, int64_t d[3], int64_t* T,
+                                 double* P0, double* P1, double* P2, int32_t* c0, int32_t* c1,
+                                 int32_t* c2, double* w);
 
 /* ------------------------------------------------------------------ stage 4
  * TuckerTensor::entry (tucker.hpp:38-54) at probes, and to_dense (tucker.hpp:172-178)

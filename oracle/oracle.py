@@ -173,6 +173,25 @@ def assembled_vector(ref_col: np.ndarray, N: int, shifts: np.ndarray) -> np.ndar
     return out
 
 
+def side_matrix_mode(ref: RefOracle, geom, l: int):
+    """One mode of `side_matrices`: the N_l x M_c unit-column side matrix in reference
+    column order and the per-column norms that from_raw folds into the weights (the
+    reference builds every block's columns this way: assembled_vector / windowed
+    columns, lattice_sum.hpp:101-157, then canonical.hpp:32-48)."""
+    N, R = geom.N[l], geom.R
+    blocks = geom.blocks()
+    F = np.zeros((N, R * len(blocks)), order="F")
+    norms = np.zeros(R * len(blocks))
+    for b, blk in enumerate(blocks):
+        raw = np.zeros((N, R), order="F")
+        for q in range(R):
+            raw[:, q] = assembled_vector(ref.factors[l][:, q], N, blk.shifts[l])
+        f, nrm = normalize_columns(raw)
+        F[:, b * R:(b + 1) * R] = f
+        norms[b * R:(b + 1) * R] = nrm
+    return F, norms
+
+
 def side_matrices(ref: RefOracle, geom, max_bytes: float = 24e9):
     """Full N x M_c side matrices in reference column order + M_c weights.
 
@@ -514,8 +533,11 @@ def als_refine(F, w, Y, ranks, max_sweeps: int = 30, stag_tol: float = 1e-8):
     return Y, sweeps
 
 
-def shrink_core(core, factors, budget2):
-    """rank_reduction.hpp:129-168."""
+def shrink_core(core, factors, budget2, near=None):
+    """rank_reduction.hpp:129-168.  `near` (optional list of 3 bools) is set for a mode in
+    which some drop decision compared a slice mass within 5% of the initial budget to the
+    remaining budget: budget2 = eps^2 n^2 - (n^2 - ||core||^2) carries a cancellation of
+    ~1e-16 n^2 / budget2 (percent level at eps = 1e-7), so such a decision is a tie."""
     core = core.copy()
     factors = [f.copy() for f in factors]
     for l in range(3):
@@ -525,6 +547,7 @@ def shrink_core(core, factors, budget2):
         core = np.moveaxis(np.tensordot(q.T, np.moveaxis(core, l, 0), axes=(1, 0)), 0, l)
         factors[l] = factors[l] @ q
     r = list(core.shape)
+    budget0 = budget2
     changed = True
     while changed and budget2 > 0:
         changed = False
@@ -534,6 +557,8 @@ def shrink_core(core, factors, budget2):
             box = core[:r[0], :r[1], :r[2]]
             sl = np.take(box, r[l] - 1, axis=l)
             mass = float(np.sum(sl * sl))
+            if near is not None and abs(mass - budget2) <= 0.05 * budget0:
+                near[l] = True
             if mass <= budget2:
                 budget2 -= mass
                 r[l] -= 1
@@ -541,8 +566,10 @@ def shrink_core(core, factors, budget2):
     return core[:r[0], :r[1], :r[2]].copy(), [factors[l][:, :r[l]] for l in range(3)]
 
 
-def canonical_to_tucker(F, w, eps=None, ranks=None, max_sweeps: int = 30, stag_tol: float = 1e-8):
-    """rank_reduction.hpp:280-306 on full side matrices (small sizes)."""
+def canonical_to_tucker(F, w, eps=None, ranks=None, max_sweeps: int = 30, stag_tol: float = 1e-8,
+                        near=None):
+    """rank_reduction.hpp:280-306 on full side matrices (small sizes); `near` as in
+    shrink_core (tie flags of the slice-drop decisions)."""
     orc = rhosvd(F, w, eps=eps, ranks=ranks, with_norm=True)
     Y, sweeps = als_refine(F, w, orc.Z, orc.ranks, max_sweeps, stag_tol) if max_sweeps > 0 else (orc.Z, 0)
     P = [Y[l].T @ F[l] for l in range(3)]
@@ -552,7 +579,7 @@ def canonical_to_tucker(F, w, eps=None, ranks=None, max_sweeps: int = 30, stag_t
         err2 = max(n2 - float(np.sum(core * core)), 0.0)
         budget2 = eps * eps * n2 - err2
         if budget2 > 0:
-            core, Y = shrink_core(core, Y, budget2)
+            core, Y = shrink_core(core, Y, budget2, near)
     return core, Y, orc, sweeps
 
 

@@ -105,6 +105,7 @@ SIGNATURES = [
     ("latsum_tucker_singular_values", _I, [_P, _I, _P]),
     ("latsum_tucker_core", _I, [_P, _P, _P]),
     ("latsum_tucker_factor", _I, [_P, _P, _I, _P]),
+    ("latsum_tucker_projected_form", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("latsum_tucker_entries", _I, [_P, _P, _P, _I64, _P]),
     ("latsum_tucker_eval_box", _I, [_P, _P, _P, _P, _P]),
     ("latsum_tucker_eval_box_device", _I, [_P, _P, _P, _P, _P]),

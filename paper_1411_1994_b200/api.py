@@ -415,6 +415,21 @@ class TuckerTensor:
         self.ctx.check(_lib.lib().latsum_tucker_factor(self.ctx.handle, self._h, mode, _p(out)))
         return out
 
+    def projected_form(self):
+        """Factors-only tensors (no dense core): (P_l (r_l x d_l) per mode, term columns
+        (T x 3, int32), term weights (T)) with V = sum_t w_t prod_l (U_l P_l)[i_l, c_l(t)]."""
+        d, T = np.zeros(3, np.int64), ctypes.c_int64()
+        L = _lib.lib()
+        self.ctx.check(L.latsum_tucker_projected_form(self.ctx.handle, self._h, _p(d),
+                                                      ctypes.byref(T), *([None] * 7)))
+        P = [np.zeros((self.ranks[l], int(d[l])), order="F") for l in range(3)]
+        tc = [np.zeros(T.value, np.int32) for _ in range(3)]
+        w = np.zeros(T.value)
+        self.ctx.check(L.latsum_tucker_projected_form(
+            self.ctx.handle, self._h, _p(d), ctypes.byref(T), _p(P[0]), _p(P[1]), _p(P[2]),
+            _p(tc[0]), _p(tc[1]), _p(tc[2]), _p(w)))
+        return P, np.stack(tc, axis=1), w
+
     def entries(self, probes) -> np.ndarray:
         pr = _i64(probes).reshape(-1, 3)
         out = np.zeros(pr.shape[0])

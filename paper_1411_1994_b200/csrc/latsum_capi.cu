@@ -3022,6 +3022,30 @@ int latsum_tucker_factor(latsum_ctx* c, const latsum_tucker* t, int mode, double
   });
 }
 
+int latsum_tucker_projected_form(latsum_ctx* c, const latsum_tucker* t, int64_t d[3], int64_t* T,
+                                  double* P0, double* P1, double* P2, int32_t* c0, int32_t* c1,
+                                  int32_t* c2, double* w) {
+  return guarded(c, [&] {
+    require(t && d && T, "latsum_tucker_projected_form: null argument");
+    require(!t->has_core, "latsum_tucker_projected_form: the tensor carries a dense core");
+    for (int l = 0; l < 3; ++l) d[l] = t->d[l];
+    *T = t->T;
+    double* P[3] = {P0, P1, P2};
+    int32_t* tc[3] = {c0, c1, c2};
+    for (int l = 0; l < 3; ++l) {
+      if (P[l])
+        CK(cudaMemcpyAsync(P[l], t->P[l].p, sizeof(double) * t->r[l] * t->d[l],
+                           cudaMemcpyDeviceToHost, c->stream));
+      if (tc[l] && t->T)
+        CK(cudaMemcpyAsync(tc[l], t->tc[l].p, sizeof(int32_t) * t->T, cudaMemcpyDeviceToHost,
+                           c->stream));
+    }
+    if (w && t->T)
+      CK(cudaMemcpyAsync(w, t->tw.p, sizeof(double) * t->T, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int latsum_tucker_entries(latsum_ctx* c, const latsum_tucker* t, const int64_t* probes, int64_t np,
                           double* out) {
   return guarded(c, [&] {

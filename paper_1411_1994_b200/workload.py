@@ -60,6 +60,8 @@ class Geometry:
     eval_hi: Optional[Tuple[int, int, int]] = None
     name: str = ""
     seed: int = 0
+    n_vacancies: int = 0   # sampled defects by kind (lattice_box); informational
+    n_impurities: int = 0
 
     @property
     def R(self) -> int:
@@ -257,7 +259,8 @@ def lattice_box(N: int, box: float, sublats: Sequence[dict], *, family=NEWTON, l
         dch = charges.astype(np.float64)
     return Geometry(N=(N, N, N), box=(box, box, box), family=family, lam=lam, M=M,
                     sublattices=subs, defect_shifts=dsh, defect_charges=dch, eps=eps,
-                    name=name, seed=seed, eval_lo=tuple(eval_lo), eval_hi=eval_hi)
+                    name=name, seed=seed, eval_lo=tuple(eval_lo), eval_hi=eval_hi,
+                    n_vacancies=int(n_vacancies), n_impurities=int(n_impurities))
 
 
 def baseline(i: int, seed: Optional[int] = None) -> Geometry:
@@ -302,3 +305,18 @@ def z_slab(lo: Sequence[int], hi: Sequence[int], rank: int, world: int):
     """The z-slab of the evaluation box [lo, hi) that `rank` evaluates (no communication)."""
     z0, z1 = row_block(hi[2] - lo[2], rank, world)
     return (lo[0], lo[1], lo[2] + z0), (hi[0], hi[1], lo[2] + z1)
+
+
+def describe(g: Geometry) -> dict:
+    """The workload as one JSON-able dict (bench.py prints it on both arms)."""
+    lo, hi = g.eval_box()
+    return {
+        "workload": g.name,
+        "kernel": "yukawa" if g.family == YUKAWA else "newton",
+        "lambda": g.lam if g.family == YUKAWA else None,
+        "N": int(g.N[0]), "box": float(g.box[0]), "M": int(g.M), "R": int(g.R),
+        "sublattices": len(g.sublattices), "sites": int(g.n_sites),
+        "vacancies": int(g.n_vacancies), "impurities": int(g.n_impurities),
+        "canonical_rank": int(g.canonical_rank), "eps": g.eps, "seed": int(g.seed),
+        "eval_box": [list(map(int, lo)), list(map(int, hi))],
+    }

@@ -19,7 +19,7 @@ from oracle import oracle as O  # noqa: E402
 from paper_1411_1994_b200 import workload as W  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-N_PROBES, N_BRUTE = 64, 16
+N_PROBES, N_BRUTE = 500, 100  # cmd_verify: 500 probes (commands.cpp:254-266)
 
 
 def make(cfg: int):
@@ -37,7 +37,7 @@ def make(cfg: int):
     v_rhosvd = O.projected_cp_entries(w, orc.Z, orc.P, pr)
     v_canon = O.canonical_entries(sides, w, pr)
     v_brute = O.oracle_entries(ref, g, pr[:N_BRUTE])
-    keep = [min(orc.sigma[l].size, orc.ranks[l] + 256) for l in range(3)]
+    keep = [min(orc.sigma[l].size, orc.ranks[l] + 512) for l in range(3)]
     np.savez_compressed(
         os.path.join(HERE, f"fullcfg{cfg}.npz"),
         ranks=np.array(orc.ranks), tie=np.array(orc.tie), margin=np.array(orc.margin),

@@ -395,6 +395,97 @@ def test_full_config_against_oracle_fixture(ctx, cfg):
     assert np.max(np.abs(exact[:nb] - fx["v_brute"])) / np.max(np.abs(fx["v_brute"])) < 1e-12
     np.testing.assert_allclose(rep.weight_norm, float(fx["weight_norm"]), rtol=1e-12)
     np.testing.assert_allclose(rep.input_norm, float(fx["input_norm"]), rtol=1e-9)
+    # singular values around the cut-off, per value (the rank rule reads this tail)
+    for l in range(3):
+        s_orc = fx[f"sigma{l}"]
+        s_gpu = rep.singular_values[l][:s_orc.size]
+        r = ranks[l]
+        idx = np.arange(max(0, r - 64), min(s_orc.size, r + 64))
+        idx = idx[s_orc[idx] >= 1e-2 * s_orc[r - 1]]  # values that weigh in the tail sum
+        # 1e-6 relative per value, floor 1e-7 sigma_r (a 1e-7 share of the tail sum)
+        err = np.abs(s_gpu[idx] - s_orc[idx]) - (1e-6 * s_orc[idx] + 1e-7 * s_orc[r - 1])
+        assert np.max(err) <= 0, (l, int(idx[np.argmax(err)]),
+                                  float(np.max(np.abs(s_gpu[idx] - s_orc[idx]) / s_orc[idx])))
+        # the tail the rank rule compares with eps ||sigma|| / 3 (rank_reduction.hpp:73-84)
+        tail_g = np.sqrt(np.sum(rep.singular_values[l][r:] ** 2))
+        tail_o = np.sqrt(np.sum(s_orc[r:] ** 2))
+        assert abs(tail_g - tail_o) <= 1e-4 * tail_o, (l, tail_g, tail_o)
+    # the benchmarked evaluation of the box, whole z-slices at the chunk boundaries
+    _check_box_slices(ctx, t, g)
+
+
+def _balanced_chunk(n, cap, align):
+    """latsum_capi.cu balanced_chunk (the evaluation's z / y chunking)."""
+    cap = max(1, cap)
+    if n <= cap:
+        return max(n, 1)
+    parts = -(-n // cap)
+    c = -(-n // parts)
+    if align > 1 and c > align:
+        c = min(cap, -(-c // align) * align)
+    return max(1, min(c, cap))
+
+
+def _box_slices(t, g, d0=None):
+    """First and last z-slices of the evaluation box plus the two slices on each side of
+    the first two z-chunk boundaries of the library's chunking (tucker_eval /
+    cp_eval_grouped)."""
+    lo, hi = g.eval_box()
+    ni, nj, nk = (hi[l] - lo[l] for l in range(3))
+    budget = 1 << 29
+    if t.has_core:
+        r0, r2 = t.ranks[0], t.ranks[2]
+        njc = _balanced_chunk(nj, budget // max(r0 * r2, 1), 128)
+        nkc = _balanced_chunk(nk, min(budget // max(r0 * njc, 1), 65535), 1)
+    else:
+        nkc = _balanced_chunk(nk, min(budget // max(nj * d0, 1), 65535), 1)
+    ks = {0, nk - 1}
+    for b in list(range(nkc, nk, nkc))[:2]:
+        ks |= {b - 1, b}
+    return sorted(ks), nkc
+
+
+def _check_box_slices(ctx, t, g):
+    """eval_box_device on the config's full evaluation box (the launch shape bench.py
+    times: multi-chunk Ozaki slab chain, or cp_eval_grouped for factors-only tensors)
+    against an FP64 evaluation on the host of the same tensor's core and factors
+    (tucker.hpp:38-54 as a TTM chain) or projected form (V = sum_t w_t prod_l
+    (U_l P_l)[i_l, c_l(t)]), whole z-slices, 1e-12 relative to the slices' max |V|."""
+    import scipy.sparse as sp
+    import torch
+    lo, hi = g.eval_box()
+    ni, nj, nk = (hi[l] - lo[l] for l in range(3))
+    U = [t.factor(l)[lo[l]:hi[l]] for l in range(3)]
+    if t.has_core:
+        ks, nkc = _box_slices(t, g)
+    else:
+        P, tc, w = t.projected_form()
+        D = [np.ascontiguousarray(U[l] @ P[l]) for l in range(3)]
+        ks, nkc = _box_slices(t, g, D[0].shape[1])
+    assert nkc < nk, "the box must span several z-chunks"
+    torch.cuda.synchronize()
+    out = torch.empty(ni * nj * nk, dtype=torch.float64, device="cuda")
+    t.eval_box_device(lo, hi, out.data_ptr())
+    ctx.synchronize()
+    got = {k: out[k * ni * nj:(k + 1) * ni * nj].view(nj, ni).T.cpu().numpy() for k in ks}
+    del out
+    torch.cuda.empty_cache()
+    if t.has_core:
+        core = t.core
+        r = t.ranks
+        Q = core.reshape(r[0] * r[1], r[2], order="F") @ U[2][ks].T  # (r0 r1) x |ks|
+        del core
+        want = {k: U[0] @ Q[:, i].reshape(r[0], r[1], order="F") @ U[1].T for i, k in enumerate(ks)}
+    else:
+        want = {}
+        for k in ks:
+            M = sp.csr_matrix((w * D[2][k, tc[:, 2]], (tc[:, 0], tc[:, 1])),
+                              shape=(D[0].shape[1], D[1].shape[1]))
+            want[k] = np.asarray((M.T @ D[0].T).T) @ D[1].T
+    scale = max(np.max(np.abs(v)) for v in want.values())
+    for k in ks:
+        err = np.max(np.abs(got[k] - want[k])) / scale
+        assert err < 1e-12, (k, err)
 
 
 @pytest.mark.parametrize("fixed_mode", [0, 1, 2])
@@ -407,7 +498,11 @@ def test_stage3_core_contracted_over_smallest_mode(ctx, fixed_mode):
             s = [a, b]
             s.insert(fixed_mode, 0)
             sites.append(tuple(s))
+    # one site short of the 4 x 4 x 1 product: a ragged cluster, one window per site
+    # (a full product would be assembled at reference rank, lattice_sum.hpp:316-321)
+    sites = sites[:-1]
     g = W.from_lattice((4, 4, 4), 16, M=6, defects=[(sites, -1.0, None)], eps=1e-7)
+    assert g.n_defects == 15
     ref, oref = _ref_pair(ctx, g)
     can = api.lattice_sum(ref, g)
     assert int(np.argmin(can.dict_cols)) == fixed_mode
@@ -460,10 +555,16 @@ def test_canonical_to_tucker_matches_oracle(ctx, kind):
     ref, oref = _ref_pair(ctx, g)
     can = api.lattice_sum(ref, g)
     F, w = O.side_matrices(oref, g)
-    core, Y, orc, sweeps = O.canonical_to_tucker(F, w, eps=g.eps, max_sweeps=3)
+    near = [False, False, False]
+    core, Y, orc, sweeps = O.canonical_to_tucker(F, w, eps=g.eps, max_sweeps=3, near=near)
     t, rep, gsweeps = api.canonical_to_tucker(can, api.TruncationSpec.tol(g.eps), max_als_sweeps=3)
     for l in range(3):
-        assert abs(rep.chosen_ranks[l] - core.shape[l]) <= 1, (rep.chosen_ranks, core.shape)
+        # identical ranks; +-1 only where the oracle's slice-drop decision was a tie
+        # (the greedy drop loop interleaves the modes, so a tie in one mode moves the budget
+        # every later decision sees: any flagged tie admits +-1)
+        if rep.chosen_ranks[l] != core.shape[l]:
+            assert any(near) and abs(rep.chosen_ranks[l] - core.shape[l]) <= 1, \
+                (l, rep.chosen_ranks, core.shape, near)
         assert rep.chosen_ranks[l] <= orc.ranks[l]
     pr = O.probes(g.N, 300, 41)
     exact = O.canonical_entries(F, w, pr)

@@ -590,8 +590,15 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
     return;
   }
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
+  // stream the larger operand once: N tiles fastest when A is the bigger one (the core
+  // contraction's tall X against the small P_m), M tiles fastest otherwise (the slabs)
+  static const int order_env = [] {
+    const char* e = std::getenv("LATSUM_OZ_ORDER");  // A/B: "m" or "n" forces the order
+    return e ? (e[0] == 'n' ? 1 : 0) : -1;
+  }();
+  const int nfast = order_env >= 0 ? order_env : (a.tiles > 2 * b.tiles ? 1 : 0);
   oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
-      a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, o, a.tiles, tiles);
+      a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, o, a.tiles, tiles, b.tiles, nfast);
   post_launch(c);
 #ifdef LATSUM_OZ_TRACE
   {
@@ -1843,13 +1850,16 @@ struct GroupedTerms {
                                                                nullptr, T, G2.p);
     post_launch(c);
   }
-  // X (r_o1 r_o2 x na): columns j = a0 .. a0+na-1 of the grouped unfolding
-  void form(latsum_ctx* c, const int64_t r[3], int64_t T, int64_t a0, int64_t na, double* X) const {
+  // X (r_o1 nb x na): columns j = a0 .. a0+na-1 of the grouped unfolding, rows (i1, i2) with
+  // i2 in [b0, b0 + nb) of the o2 index (nb < 0: all of it)
+  void form(latsum_ctx* c, const int64_t r[3], int64_t T, int64_t a0, int64_t na, double* X,
+            int64_t b0 = 0, int64_t nb = -1) const {
+    if (nb < 0) nb = r[o2];
     GemmOpts o = tagged("gemm_core_x");
     o.batch = na;
-    o.sC = r[o1] * r[o2];
+    o.sC = r[o1] * nb;
     o.kseg = seg.p + a0;
-    gemm(c, false, true, r[o1], r[o2], T, 1.0, G1.p, r[o1], G2.p, r[o2], 0.0, X, r[o1], o);
+    gemm(c, false, true, r[o1], nb, T, 1.0, G1.p, r[o1], G2.p + b0, r[o2], 0.0, X, r[o1], o);
   }
 };
 
@@ -1880,6 +1890,35 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
   }
   GroupedTerms gt(c, can, P, r, m);
   const int64_t budget = workspace_budget();  // doubles of X per chunk
+  const int64_t nall = dm - a_lo;
+  // Long-K form (default on the Ozaki path): chunk the o2 index of X's rows instead of the
+  // contraction index, so every core element comes out of ONE product over all nall columns
+  // (written once, no beta = 1 re-reads of the core; long K amortises the int8 kernel's
+  // per-tile TMEM drains).  X block: r_o1 nb rows x nall columns.
+  if (!std::getenv("LATSUM_CORE_KCHUNK") && nall <= 65535 &&
+      core_uses_ozaki(ro, std::max(r[0], r[2]), nall) && r[o1] * nall <= budget) {
+    const int64_t nb = balanced_chunk(r[o2], budget / std::max<int64_t>(r[o1] * nall, 1), 1);
+    DBuf X(c, size_t(r[o1]) * nb * nall);
+    for (int64_t b0 = 0; b0 < r[o2]; b0 += nb) {
+      const int64_t nbb = std::min(nb, r[o2] - b0);
+      const int64_t rows = r[o1] * nbb;  // X rows of this block
+      gt.form(c, r, T, a_lo, nall, X.p, b0, nbb);
+      if (m == 0) {         // core (r0 x r1 r2) columns [r1 b0, r1 (b0 + nbb)) = P0 X^T
+        ozaki_gemm(c, r[0], rows, nall, P[0].p + a_lo * r[0], r[0], X.p, rows,
+                   core + r[0] * r[1] * b0, r[0], "gemm_core(ozaki-i8)", true, 0.0);
+      } else if (m == 2) {  // core rows [r0 b0, r0 (b0 + nbb)) of the (r0 r1 x r2) view
+        ozaki_gemm(c, rows, r[2], nall, X.p, rows, P[2].p + a_lo * r[2], r[2],
+                   core + r[0] * b0, ro, "gemm_core(ozaki-i8)", true, 0.0);
+      } else {              // rows (a, k), k in the block -> core[a + r0 b + r0 r1 k]
+        oz::OzOut o = oz_out(core + r[0] * r[1] * b0, r[0], 0.0);
+        o.mr = r[0];
+        o.rs = r[0] * r[1];
+        ozaki_gemm_ex(c, rows, r[1], nall, X.p, 1, rows, 0, 0, P[1].p + a_lo * r[1], 1, r[1], o,
+                      "gemm_core(ozaki-i8)");
+      }
+    }
+    return;
+  }
   const int64_t ac = balanced_chunk(dm - a_lo, std::min<int64_t>(budget / std::max<int64_t>(ro, 1), 65535), 64);
   DBuf X(c, size_t(ro) * ac);
   for (int64_t a0 = a_lo; a0 < dm; a0 += ac) {

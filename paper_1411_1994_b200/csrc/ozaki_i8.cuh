@@ -342,7 +342,11 @@ __device__ __forceinline__ void drainw(uint32_t taddr, double* x) {
 __global__ void __launch_bounds__(PTHREADS, 1)
 k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
           const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N,
-          int64_t KB, OzOut o, int64_t tiles_m, int64_t tiles) {
+          int64_t KB, OzOut o, int64_t tiles_m, int64_t tiles, int64_t tiles_n, int nfast) {
+  // tile t -> (mt, nt): M tiles fastest (default: the CTAs running together share a B column
+  // tile) or, nfast, N tiles fastest (a tall A streamed once, B kept in L2)
+  auto tile_m = [&](int64_t t) { return nfast ? t / tiles_n : t % tiles_m; };
+  auto tile_n = [&](int64_t t) { return nfast ? t % tiles_n : t / tiles_m; };
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
@@ -376,8 +380,8 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
     if (lane == 0) {
       int64_t it = 0;  // (pass, k-block) stages loaded by this CTA (ring position)
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int8_t* gA = As + ((t % tiles_m) * KB) * int64_t(A_STAGE);
-        const int8_t* gB = Bs + ((t / tiles_m) * KB) * int64_t(B_STAGE);
+        const int8_t* gA = As + (tile_m(t) * KB) * int64_t(A_STAGE);
+        const int8_t* gB = Bs + (tile_n(t) * KB) * int64_t(B_STAGE);
         for (int pass = 0; pass < 2; ++pass) {
           const uint32_t nsl = pass == 0 ? P1_SLICES : S;
           for (int64_t kb = 0; kb < KB; ++kb, ++it) {
@@ -445,7 +449,7 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
     const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * EPI_COLS);
     int64_t np = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, np += 2) {
-      const int64_t mt = t % tiles_m, nt = t / tiles_m;
+      const int64_t mt = tile_m(t), nt = tile_n(t);
       const int64_t i = mt * BM + q * 32 + lane;
       const int64_t n0 = nt * BN + half * EPI_COLS;
       // row / column scales, fetched before the accumulators are ready

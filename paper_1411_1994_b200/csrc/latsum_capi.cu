@@ -127,6 +127,10 @@ struct latsum_ctx {
   // worker contexts (own stream + cuSOLVER handle) for the concurrent per-mode reductions
   latsum_ctx* sub[4] = {nullptr, nullptr, nullptr, nullptr};
   latsum_ctx* parent = nullptr;  // set on worker contexts
+  // cap on the CTAs of this context's persistent kernels (Ozaki GEMM): a persistent grid on
+  // every SM holds them until it finishes, whatever the stream priorities; the low-priority
+  // norm worker keeps to a few SMs so the mode workers' kernels are never queued behind it
+  int max_ctas = 0;
   // multi-GPU: one rank of a row-sharded reduction (latsum_ctx_init_comm); each worker
   // context owns a communicator split from this one so concurrent modes never interleave
   ncclComm_t comm = nullptr;
@@ -589,6 +593,7 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
     post_launch(c);
     return;
   }
+  if (c->max_ctas > 0) sms = std::min(sms, c->max_ctas);
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   // stream the larger operand once: N tiles fastest when A is the bigger one (the core
   // contraction's tall X against the small P_m), M tiles fastest otherwise (the slabs)
@@ -1566,6 +1571,7 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   const RowBlock blk = sharded ? row_block(c, N) : RowBlock{0, N};
   const int64_t Nb = blk.n();
   Timer timer(c);
+  Trace::mark(c, "mode start");
   timer.start();
   std::vector<double> sq(d);
   for (int64_t j = 0; j < d; ++j) sq[j] = std::sqrt(can.mult[l][j]);
@@ -1579,6 +1585,7 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
     post_launch(c);
   }
   tm.gram += timer.stop();
+  Trace::mark(c, "operand ready");
   const int64_t* rf = ranks ? ranks + l : nullptr;
   reduce_dense(c, At, blk, N, d, n_sing, rf, tol, deflate, false, sharded, out, tm);
 }
@@ -1970,6 +1977,10 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
     CS(cusolverDnCreate(&w->solver));
     CS(cusolverDnSetStream(w->solver, w->stream));
     CS(cusolverDnCreateParams(&w->solver_params));
+    if (i == 3) {
+      const char* e = std::getenv("LATSUM_NORM_CTAS");
+      w->max_ctas = e ? std::atoi(e) : 32;
+    }
     c->sub[i] = w;
   }
   c->sub[i]->prof = c->prof;

@@ -1525,6 +1525,149 @@ void left_from_vectors(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, co
   polar_orthonormalize(c, U, Nb, k, sharded);
 }
 
+// Frobenius norm squared of an Nb x cols column-major block (all ranks' rows when sharded).
+double frob2(latsum_ctx* c, const double* A, int64_t Nb, int64_t cols, int64_t ld, bool sharded) {
+  const int blocks = 148 * 4;
+  DBuf part(c, blocks), sum(c, 1);
+  if (Nb > 0 && cols > 0) {
+    k_sumsq_partial<<<blocks, 256, 0, c->stream>>>(A, Nb, cols, ld, part.p);
+    post_launch(c);
+    k_sum<<<1, 1024, 0, c->stream>>>(part.p, blocks, sum.p);
+    post_launch(c);
+  } else {
+    CK(cudaMemsetAsync(sum.p, 0, sizeof(double), c->stream));
+  }
+  if (sharded) allreduce(c, sum.p, 1);
+  double h = 0;
+  CK(cudaMemcpyAsync(&h, sum.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+// Randomized second pass of the deflated RHOSVD (column orientation).  The deflated operand
+// A'' = (I - U1 U1^T)^2 A (Nb x d rows of this rank) has norm <= ~1e-5 sigma_1 and, on the
+// BASELINE Grams, numerical rank a fraction of its d - k1 nonzero directions, so instead of
+// the (d - k1)^2 restricted Gram this pass
+//   1. sketches its range, Y = A'' Omega (ell Gaussian columns),
+//   2. orthonormalises Y in rounds: Y^T Y = W h W^T, Q_new = Y W_k h_k^{-1/2} for the values
+//      within 1e10 of the round's largest (orthogonality error <= eps 1e10, removed by two
+//      Newton-Schulz polar steps), Y <- Y - Q (Q^T Y) twice, until the rest of Y is below the
+//      floor delta (directions of A'' under delta are never needed individually),
+//   3. projects, C = Q^T A'' (m x d), and takes the Ritz pairs of C C^T (m x m): the values
+//      mu_j and the left vectors U2 = Q W.
+// Certified by the captured mass: ||A''||_F^2 - ||C||_F^2 (the lump, everything outside
+// span(Q)) must be <= lump_max; the lump enters the rank rule as spread over the
+// unresolved slots.  Returns false when the sketch cannot be certified at ell = nc (the
+// caller then runs the restricted Gram).  Every eigensolve is ell x ell (the in-house
+// solver up to 808: no cuSOLVER serialisation across the concurrent modes).
+struct Rp2 {
+  int64_t m = 0;
+  DBuf Q;                   // Nr x m, orthonormal
+  Eig e;                    // Ritz problem C C^T
+  std::vector<double> mu;   // m Ritz values, descending
+  double lump = 0.0;        // ||A''||_F^2 - sum mu
+  int64_t ell = 0, rounds = 0;
+};
+
+bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, int64_t nc,
+                      double delta, double lump_max, bool sharded, uint64_t seed, Rp2& o) {
+  const int64_t Nr = std::max<int64_t>(Nb, 1);
+  const double a2 = frob2(c, Ap, Nb, d, Nb, sharded);
+  static const int64_t ell_env = [] {
+    const char* e = std::getenv("LATSUM_RP2_ELL");
+    return e ? int64_t(std::atoll(e)) : int64_t(0);
+  }();
+  int64_t ell = std::min<int64_t>(nc, ell_env > 0 ? ell_env : 768);
+  for (;; ell = std::min<int64_t>(nc, 2 * ell)) {
+    o.ell = ell;
+    DBuf Om(c, size_t(d) * ell), Y(c, size_t(Nr) * ell);
+    k_fill_gauss<<<grid_for(d * ell), 256, 0, c->stream>>>(Om.p, d * ell, seed + uint64_t(ell));
+    post_launch(c);
+    if (Nb > 0)
+      gemm(c, false, false, Nb, ell, d, 1.0, Ap, Nb, Om.p, d, 0.0, Y.p, Nb, tagged("gemm_rp2"));
+    else
+      CK(cudaMemsetAsync(Y.p, 0, sizeof(double) * ell, c->stream));
+    o.Q.alloc(c, size_t(Nr) * ell);
+    int64_t m = 0;
+    // a direction of A'' with singular value s shows in Y at ~ s sqrt(ell)
+    const double stop_h = delta * delta * double(ell) * 1e-2;
+    DBuf S(c, size_t(ell) * ell);
+    for (int round = 0; round < 4 && m < ell; ++round) {
+      if (m > 0) {
+        for (int rep = 0; rep < 2; ++rep) {  // Y <- Y - Q (Q^T Y)
+          if (Nb > 0)
+            gemm(c, true, false, m, ell, Nb, 1.0, o.Q.p, Nb, Y.p, Nb, 0.0, S.p, m, tagged("gemm_rp2"));
+          else
+            CK(cudaMemsetAsync(S.p, 0, sizeof(double) * m * ell, c->stream));
+          if (sharded) allreduce(c, S.p, size_t(m) * ell);
+          if (Nb > 0)
+            gemm(c, false, false, Nb, ell, m, -1.0, o.Q.p, Nb, S.p, m, 1.0, Y.p, Nb, tagged("gemm_rp2"));
+        }
+      }
+      DBuf H(c, size_t(ell) * ell);
+      if (Nb > 0) gram(c, false, Y.p, Nb, ell, H.p);
+      else CK(cudaMemsetAsync(H.p, 0, sizeof(double) * ell * ell, c->stream));
+      if (sharded) allreduce(c, H.p, size_t(ell) * ell);
+      Eig eh;
+      eh.ortho_tol = 1e-9;
+      eh.solve(c, ell, std::move(H));
+      std::vector<double> h(ell);
+      for (int64_t i = 0; i < ell; ++i) h[i] = std::max(eh.lam_asc[ell - 1 - i], 0.0);
+      const double hmax = h[0];
+      if (!(hmax > stop_h)) break;
+      int64_t kk = 0;
+      while (kk < ell - m && h[kk] > std::max(1e-10 * hmax, stop_h)) ++kk;
+      if (kk == 0) break;
+      ++o.rounds;
+      double* Qn = o.Q.p + Nb * m;
+      DBuf Vk(c, size_t(ell) * kk);
+      eh.leading(c, kk, Vk.p);
+      left_from_vectors(c, Y.p, Nb, ell, Vk.p, h, kk, Qn, sharded);  // + one polar step
+      if (m > 0) {
+        DBuf S2(c, size_t(m) * kk);
+        for (int rep = 0; rep < 2; ++rep) {  // Qn <- Qn - Q (Q^T Qn)
+          if (Nb > 0)
+            gemm(c, true, false, m, kk, Nb, 1.0, o.Q.p, Nb, Qn, Nb, 0.0, S2.p, m, tagged("gemm_rp2"));
+          else
+            CK(cudaMemsetAsync(S2.p, 0, sizeof(double) * m * kk, c->stream));
+          if (sharded) allreduce(c, S2.p, size_t(m) * kk);
+          if (Nb > 0)
+            gemm(c, false, false, Nb, kk, m, -1.0, o.Q.p, Nb, S2.p, m, 1.0, Qn, Nb, tagged("gemm_rp2"));
+        }
+      }
+      polar_orthonormalize(c, Qn, Nb, kk, sharded, 2);
+      m += kk;
+    }
+    o.m = m;
+    if (m == 0) {  // A'' below the floor everywhere
+      o.mu.clear();
+      o.lump = a2;
+      return a2 <= lump_max;
+    }
+    // Ritz pairs of C C^T, C = Q^T A''
+    DBuf C(c, size_t(m) * d), G2(c, size_t(m) * m);
+    if (Nb > 0)
+      gemm(c, true, false, m, d, Nb, 1.0, o.Q.p, Nb, Ap, Nb, 0.0, C.p, m, tagged("gemm_rp2"));
+    else
+      CK(cudaMemsetAsync(C.p, 0, sizeof(double) * m * d, c->stream));
+    if (sharded) allreduce(c, C.p, size_t(m) * d);
+    gram(c, true, C.p, m, d, G2.p);
+    o.e = Eig();
+    o.e.ortho_tol = 1e-9;
+    o.e.solve(c, m, std::move(G2));
+    o.mu.assign(m, 0.0);
+    double captured = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      o.mu[i] = std::max(o.e.lam_asc[m - 1 - i], 0.0);
+      captured += o.mu[i];
+    }
+    o.lump = std::max(a2 - captured, 0.0);
+    Trace::mark(c, "rp2 round done");
+    if (o.lump <= lump_max) return true;
+    if (ell >= nc) return false;
+  }
+}
+
 struct ModeOut {
   std::vector<double> sigma;
   int64_t r = 1;
@@ -1639,11 +1782,14 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   bool restricted = false;  // pass 2 on the pass-1 complement Qc (needs all pass-1 vectors)
   std::vector<double> mu_d;
   bool defl = false;
+  bool use_rp2 = false;
+  Rp2 rp;
+  double target = 0.0;
   if ((!ranks || force_deflate) && deflate != LATSUM_DEFLATE_NEVER && lmax > 0.0) {
     const std::vector<double> sv = padded_sigma(lam_d);
     double sn2 = 0;
     for (double v : sv) sn2 += v * v;
-    const double target = tol * std::sqrt(sn2) / 3.0;
+    target = tol * std::sqrt(sn2) / 3.0;
     for (int64_t i = 0; i < n; ++i)
       if (lam_d[i] > 1e-10 * lmax) k1 = i + 1;
     k1 = std::max<int64_t>(k1, 1);
@@ -1673,6 +1819,41 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         if (Nb > 0)
           gemm(c, false, false, Nb, d, k1, -1.0, U1.p, Nb, C.p, k1, 1.0, Ap.p, Nb, tagged("gemm_deflate"));
       }
+      // randomized pass 2 (column orientation, tolerance-driven): ell x ell eigensolves
+      // instead of the nc x nc restricted Gram (see randomized_pass2)
+      static const bool rp2_off = std::getenv("LATSUM_RP2") && std::string(std::getenv("LATSUM_RP2")) == "0";
+      if (!rows && !force_deflate && !rp2_off && nc > 808) {
+        const double delta = 1e-4 * target / std::sqrt(double(n));
+        const double lump_max = 1e-6 * target * target;
+        if (randomized_pass2(c, Ap.p, Nb, d, nc, delta, lump_max, sharded,
+                             0x14111994ull + uint64_t(d) * 131 + uint64_t(k1), rp)) {
+          const int64_t m = rp.m, rest = n - k1 - m;
+          std::vector<std::tuple<double, int, int64_t>> all;
+          for (int64_t i = 0; i < k1; ++i) all.emplace_back(lam_d[i], 0, i);
+          for (int64_t i = 0; i < m; ++i) all.emplace_back(rp.mu[i], 1, i);
+          for (int64_t i = 0; i < rest; ++i) all.emplace_back(rp.lump / double(rest), 2, i);
+          std::stable_sort(all.begin(), all.end(), [](const auto& a, const auto& b) {
+            return std::get<0>(a) > std::get<0>(b);
+          });
+          std::vector<double> mg(n);
+          for (int64_t i = 0; i < n; ++i) mg[i] = std::get<0>(all[i]);
+          // the cut must fall inside the resolved window, clear of the lump slots
+          const int64_t rr = rank_for_tolerance(padded_sigma(mg), tol);
+          bool inside = rr + 8 <= k1 + m;
+          for (int64_t i = 0; i < std::min<int64_t>(n, rr + 8) && inside; ++i)
+            if (std::get<1>(all[i]) == 2) inside = false;
+          if (inside) {
+            use_rp2 = true;
+            n2 = m;
+            mu_d = rp.mu;
+            for (int64_t i = 0; i < n; ++i) {
+              merged[i] = mg[i];
+              src[i] = {std::get<1>(all[i]), std::get<2>(all[i])};
+            }
+          }
+        }
+      }
+      if (!use_rp2) {
       restricted = e1.has_all();
       // pass-2 operand B: restricted to the pass-1 complement Qc = the nc trailing
       // eigenvectors when they exist (cuSOLVER), else A'' itself (its Gram has k1 extra
@@ -1722,6 +1903,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         merged[i] = std::get<0>(all[i]);
         src[i] = {std::get<1>(all[i]), std::get<2>(all[i])};
       }
+      }  // !use_rp2
     }
   }
   out.deflated = defl ? 1 : 0;
@@ -1765,7 +1947,15 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
     DBuf cat(c, size_t(Nr) * (k1 + need2));
     if (Nb > 0)
       CK(cudaMemcpyAsync(cat.p, U1.p, sizeof(double) * Nb * k1, cudaMemcpyDeviceToDevice, c->stream));
-    if (need2) {
+    if (need2 && use_rp2) {  // U2 = Q W (Ritz vectors of the sketch)
+      double* U2 = cat.p + Nb * k1;
+      DBuf W2(c, size_t(rp.m) * need2);
+      rp.e.leading(c, need2, W2.p);
+      if (Nb > 0)
+        gemm(c, false, false, Nb, need2, rp.m, 1.0, rp.Q.p, Nb, W2.p, rp.m, 0.0, U2, Nb,
+             tagged("gemm_basis"));
+      polar_orthonormalize(c, U2, Nb, need2, sharded);
+    } else if (need2) {
       double* U2 = cat.p + Nb * k1;
       if (rows) {
         if (restricted) {  // U2 = Qc Y (leading eigenvectors of B B^T)

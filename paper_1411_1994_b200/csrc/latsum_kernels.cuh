@@ -497,6 +497,39 @@ __global__ void k_crop(const double* __restrict__ core, int64_t d0, int64_t d1, 
   }
 }
 
+// Per-block partial sums of squares of a column-major rows x cols block (leading dim ld);
+// k_sum then adds the gridDim.x partials in order (deterministic).
+__global__ void k_sumsq_partial(const double* __restrict__ v, int64_t rows, int64_t cols,
+                                int64_t ld, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double x = v[(i % rows) + (i / rows) * ld];
+    s += x * x;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Standard normal samples, counter-based (splitmix64 + Box-Muller): out[i] depends only on
+// (seed, i), so the sketch is reproducible and independent of the launch shape.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void k_fill_gauss(double* __restrict__ out, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t a = splitmix64(seed ^ (uint64_t(i) * 2 + 0)), b = splitmix64(seed ^ (uint64_t(i) * 2 + 1));
+    const double u1 = (double(a >> 11) + 0.5) * 0x1p-53, u2 = double(b >> 11) * 0x1p-53;
+    out[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
 __global__ void k_sumsq(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double red[32];
   double s = 0.0;

@@ -18,7 +18,8 @@ for i in range(steps):
     ref = api.reference_for(g, ctx)
     can = api.lattice_sum(ref, g)
     t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps)); torch.cuda.synchronize()
-    print(f"=== step {i} total {1e3*(time.perf_counter()-t0):.1f} ms", file=sys.stderr, flush=True)
+    free, total = torch.cuda.mem_get_info()
+    print(f"=== step {i} total {1e3*(time.perf_counter()-t0):.1f} ms (free {free/2**30:.1f} GiB)", file=sys.stderr, flush=True)
     if do_eval:
         t1 = time.perf_counter()
         t.eval_box_device(lo, hi, out.data_ptr()); torch.cuda.synchronize()

@@ -80,6 +80,18 @@ int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);
  * bound at run time (dlopen libnccl.so.2). */
 int latsum_comm_unique_id(unsigned char id[128]);
 int latsum_ctx_init_comm(latsum_ctx* ctx, const unsigned char id[128], int rank, int nranks);
+/* The same row-sharded reduction over caller-supplied host collectives instead of NCCL
+ * (tests without a multi-GPU box: gloo ranks, or several contexts on one device driven from
+ * host threads).  ar: in-place sum all-reduce of count doubles; ag: recv (nranks x count,
+ * rank order) = all-gather of send.  channel identifies the calling stream: 0 = the
+ * context, 1..4 = its four worker streams (the three modes and norm_f), which call
+ * concurrently; a rank's calls on one channel come in the same order as every other rank's.
+ * Callbacks return 0 on success.                                                       */
+typedef int (*latsum_host_allreduce_fn)(void* user, int channel, double* buf, int64_t count);
+typedef int (*latsum_host_allgather_fn)(void* user, int channel, const double* send, double* recv,
+                                        int64_t count);
+int latsum_ctx_init_host_comm(latsum_ctx* ctx, int rank, int nranks, latsum_host_allreduce_fn ar,
+                              latsum_host_allgather_fn ag, void* user);
 int latsum_ctx_comm_info(const latsum_ctx* ctx, int* rank, int* nranks);
 /* Per-kernel-class CUDA-event timing: when on, every launch group is bracketed by
  * events on the context stream.  latsum_ctx_profile writes lines
@@ -247,6 +259,37 @@ int latsum_tensor_write(latsum_ctx* ctx, const latsum_canonical* can, const lats
                         const char* path);
 int latsum_tensor_read(latsum_ctx* ctx, const char* path, latsum_canonical** can_out,
                        latsum_tucker** t_out);
+
+/* ------------------------------------------------------------------ text reports
+ * The spectral report and provenance sidecar of `latsum sum` (report.cpp:28-73, written by
+ * commands.cpp:56-72), byte for byte: 17 significant digits (report.cpp:9-12).  Host only
+ * (no context, no device).  Both format into buf (cap bytes, NUL-terminated, truncated to
+ * fit) and return the full text length, so a call with buf = NULL sizes the buffer; -1 on
+ * a null report.
+ *   write_spectral_report: sigma[l] holds report->n_singular[l] values
+ *     (latsum_tucker_singular_values), descending.                                    */
+int64_t latsum_format_spectral_report(const latsum_spectral_report* report,
+                                      const double* const sigma[3], char* buf, int64_t cap);
+/* write_provenance(result, seed, extra_lines): LatticeSumResult's grid, geometry cells,
+ * tensor format and rank(s), its summands (lattice_sum.hpp:44-50: label, canonical rank,
+ * sites) and, with a report, the truncation bounds.                                   */
+typedef struct {
+  uint64_t seed;
+  int64_t grid[3];
+  int64_t cells[3];
+  int format;                     /* 0: canonical (rank), 1: tucker (ranks) */
+  int64_t rank;
+  int64_t ranks[3];
+  int64_t nsummands;
+  const char* const* labels;      /* nsummands */
+  const int64_t* summand_ranks;   /* nsummands */
+  const int64_t* summand_sites;   /* nsummands */
+  int has_report;
+  double bound_abs, bound_rel;
+  int64_t nextra;
+  const char* const* extra;       /* nextra lines appended verbatim */
+} latsum_provenance;
+int64_t latsum_format_provenance(const latsum_provenance* p, char* buf, int64_t cap);
 
 /* ------------------------------------------------------------------ verification
  * oracle_entry (lattice_sum.hpp:656-671) on the device: the brute-force windowed sum

@@ -18,7 +18,11 @@
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <map>
 #include <optional>
+#include <ostream>
+#include <set>
+#include <variant>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -94,6 +98,10 @@ class Context {
 struct KernelSpec {
   int family = LATSUM_NEWTON;
   double lambda = 0.0;
+  bool operator==(const KernelSpec& o) const { return family == o.family && lambda == o.lambda; }
+  std::string key() const {
+    return family == LATSUM_YUKAWA ? "yukawa(" + std::to_string(lambda) + ")" : "newton";
+  }
   static KernelSpec newton() { return {LATSUM_NEWTON, 0.0}; }
   static KernelSpec yukawa(double l) {
     if (!(l > 0.0)) throw std::invalid_argument("yukawa lambda must be positive");
@@ -116,6 +124,7 @@ struct DefectSpec {
   std::vector<Int3> sites;
   DefectKind kind = DefectKind::vacancy;
   double charge = 0.0;
+  std::optional<KernelSpec> kernel;  // impurities may carry their own kernel
   std::array<double, 3> grid_offset{0, 0, 0};
 };
 inline std::vector<int> default_active_set(int cells) {
@@ -154,6 +163,8 @@ inline UniformGrid lattice_grid(const LatticeGeometry& g, Index n_per_cell) {
 struct TruncationSpec {  // rank_reduction.hpp:21-43
   std::optional<Dims3> ranks;
   std::optional<double> tolerance;
+  int max_als_sweeps = 30;
+  double als_stagnation_tol = 1e-8;
   static TruncationSpec fixed_ranks(Index a, Index b, Index c) {
     TruncationSpec s;
     s.ranks = Dims3{a, b, c};
@@ -308,46 +319,103 @@ inline std::vector<double> to_dense(const TuckerTensor& t, Index guard = 10'000'
 }
 
 namespace detail {
-struct ShiftTables {
-  std::vector<int64_t> counts, shifts, dshifts;
-  std::vector<double> charges, dcharges;
-};
 inline long lround_away(double x) { return std::lround(x); }
+
+// Ordered product blocks for latsum_canonical_assemble_blocks: per block three shift lists
+// (mesh units) and an additive charge; R terms per block, in block (add_concat) order.
+struct Blocks {
+  std::vector<int64_t> counts, shifts;
+  std::vector<double> charges;
+  void add(const std::array<std::vector<int64_t>, 3>& sh, double q) {
+    for (int l = 0; l < 3; ++l) {
+      counts.push_back(int64_t(sh[l].size()));
+      shifts.insert(shifts.end(), sh[l].begin(), sh[l].end());
+    }
+    charges.push_back(q);
+  }
+  int64_t size() const { return int64_t(charges.size()); }
+};
+
+// lattice_sum.hpp:278-294: the per-mode sorted index sets if the sites are their full
+// Cartesian product
+inline std::optional<std::array<std::vector<int>, 3>> product_structure(const std::vector<Int3>& sites) {
+  std::array<std::set<int>, 3> axes;
+  for (const auto& s : sites)
+    for (int l = 0; l < 3; ++l) axes[l].insert(s[l]);
+  size_t prod = 1;
+  for (int l = 0; l < 3; ++l) prod *= axes[l].size();
+  if (prod != sites.size()) return std::nullopt;
+  std::set<Int3> have(sites.begin(), sites.end());
+  for (int a : axes[0])
+    for (int b : axes[1])
+      for (int c : axes[2])
+        if (!have.count(Int3{a, b, c})) return std::nullopt;
+  std::array<std::vector<int>, 3> out;
+  for (int l = 0; l < 3; ++l) out[l].assign(axes[l].begin(), axes[l].end());
+  return out;
+}
+
+// assembled_vector's active sets (lattice_sum.hpp:198-223, :444 offsets)
+inline void add_lattice(Blocks& b, const LatticeGeometry& g, const std::array<double, 3>& off,
+                        Index n) {
+  std::array<std::vector<int64_t>, 3> sh;
+  for (int l = 0; l < 3; ++l)
+    for (int k : g.active_set(l))
+      sh[l].push_back(int64_t(k) * n + lround_away(off[l] * double(n)));
+  b.add(sh, g.base_charge);
+}
+
+// defect_cluster_canonical (lattice_sum.hpp:297-330): a product cluster is one assembled
+// block at reference rank, any other cluster one window per site in site order; returns
+// the number of blocks (the cluster's rank in units of R)
+inline Index add_defect(Blocks& b, const DefectSpec& d, Index n) {
+  std::array<long, 3> off;
+  for (int l = 0; l < 3; ++l) off[l] = lround_away(d.grid_offset[l]);
+  if (d.sites.size() > 1) {
+    if (auto axes = product_structure(d.sites)) {
+      std::array<std::vector<int64_t>, 3> sh;
+      for (int l = 0; l < 3; ++l)
+        for (int v : (*axes)[l]) sh[l].push_back(int64_t(v) * n + off[l]);
+      b.add(sh, d.charge);
+      return 1;
+    }
+  }
+  for (const auto& s : d.sites) {  // defect_grid_shift (:159-164)
+    std::array<std::vector<int64_t>, 3> sh;
+    for (int l = 0; l < 3; ++l) sh[l].push_back(int64_t(s[l]) * n + off[l]);
+    b.add(sh, d.charge);
+  }
+  return Index(d.sites.size());
+}
+
+inline Index active_cells(const LatticeGeometry& g) {
+  Index c = 1;
+  for (int l = 0; l < 3; ++l) c *= Index(g.active_set(l).size());
+  return c;
+}
 }  // namespace detail
 
+inline CanonicalTensor assemble(const ReferenceTensor& ref, const detail::Blocks& b) {
+  b200::Context& ctx = ref.ctx();
+  latsum_canonical* h = nullptr;
+  ctx.check(latsum_canonical_assemble_blocks(ctx.get(), ref.handle(), b.size(), b.counts.data(),
+                                             b.shifts.data(), b.charges.data(), &h));
+  return CanonicalTensor(ctx, h);
+}
+
 // Rank-R canonical lattice sum + additive defects on the lattice_grid of `geom`
-// (assembled_sum_canonical + defected_sum without truncation).
+// (assembled_sum_canonical + defected_sum without truncation, in one assembly).
 inline CanonicalTensor defected_sum(const ReferenceTensor& ref, const LatticeGeometry& geom,
                                     Index n_per_cell,
                                     const std::vector<SublatticePlacement>* subs = nullptr) {
-  detail::ShiftTables t;
-  auto add_block = [&](const LatticeGeometry& g, const std::array<double, 3>& off) {
-    for (int l = 0; l < 3; ++l) {
-      const auto ks = g.active_set(l);
-      t.counts.push_back(int64_t(ks.size()));
-      for (int k : ks)
-        t.shifts.push_back(int64_t(k) * n_per_cell + detail::lround_away(off[l] * double(n_per_cell)));
-    }
-    t.charges.push_back(g.base_charge);
-  };
+  detail::Blocks b;
   if (subs && !subs->empty()) {
-    for (const auto& s : *subs) add_block(s.geom, s.offset_cells);
+    for (const auto& s : *subs) detail::add_lattice(b, s.geom, s.offset_cells, n_per_cell);
   } else {
-    add_block(geom, {0, 0, 0});
+    detail::add_lattice(b, geom, {0, 0, 0}, n_per_cell);
   }
-  for (const auto& d : geom.defects)
-    for (const auto& s : d.sites) {
-      for (int l = 0; l < 3; ++l)
-        t.dshifts.push_back(int64_t(s[l]) * n_per_cell + detail::lround_away(d.grid_offset[l]));
-      t.dcharges.push_back(d.charge);
-    }
-  b200::Context& ctx = ref.ctx();
-  latsum_canonical* h = nullptr;
-  ctx.check(latsum_canonical_assemble(ctx.get(), ref.handle(), int64_t(t.charges.size()),
-                                      t.counts.data(), t.shifts.data(), t.charges.data(),
-                                      int64_t(t.dcharges.size()), t.dshifts.data(),
-                                      t.dcharges.data(), &h));
-  return CanonicalTensor(ctx, h);
+  for (const auto& d : geom.defects) detail::add_defect(b, d, n_per_cell);
+  return assemble(ref, b);
 }
 
 inline CanonicalTensor assembled_sum_canonical(const ReferenceTensor& ref,
@@ -366,17 +434,7 @@ inline CanonicalTensor sublattice_union_sum(const std::vector<SublatticePlacemen
   return defected_sum(ref, p, n_per_cell, &subs);
 }
 
-inline std::pair<TuckerTensor, SpectralReport> rhosvd(const CanonicalTensor& a,
-                                                      const TruncationSpec& spec,
-                                                      int deflate = LATSUM_DEFLATE_AUTO) {
-  if (!spec.ranks && !spec.tolerance)
-    throw std::invalid_argument("TruncationSpec: need ranks or tolerance");
-  b200::Context& ctx = a.ctx();
-  latsum_tucker* h = nullptr;
-  latsum_spectral_report rep;
-  ctx.check(latsum_rhosvd(ctx.get(), a.handle(), spec.ranks ? spec.ranks->data() : nullptr,
-                          spec.tolerance.value_or(0.0), deflate, &h, &rep));
-  TuckerTensor t(ctx, h);
+inline SpectralReport to_report(const latsum_spectral_report& rep, latsum_tucker* h) {
   SpectralReport out;
   for (int l = 0; l < 3; ++l) {
     out.singular_values[l].resize(size_t(rep.n_singular[l]));
@@ -390,7 +448,241 @@ inline std::pair<TuckerTensor, SpectralReport> rhosvd(const CanonicalTensor& a,
   out.input_norm = rep.input_norm;
   out.stability_constant = rep.stability_constant;
   out.stability_ok = rep.stability_ok != 0;
-  return {std::move(t), out};
+  return out;
+}
+
+inline std::pair<TuckerTensor, SpectralReport> rhosvd(const CanonicalTensor& a,
+                                                      const TruncationSpec& spec,
+                                                      int deflate = LATSUM_DEFLATE_AUTO) {
+  if (!spec.ranks && !spec.tolerance)
+    throw std::invalid_argument("TruncationSpec: need ranks or tolerance");
+  b200::Context& ctx = a.ctx();
+  latsum_tucker* h = nullptr;
+  latsum_spectral_report rep;
+  ctx.check(latsum_rhosvd(ctx.get(), a.handle(), spec.ranks ? spec.ranks->data() : nullptr,
+                          spec.tolerance.value_or(0.0), deflate, &h, &rep));
+  TuckerTensor t(ctx, h);
+  return {std::move(t), to_report(rep, h)};
+}
+
+// rank_reduction.hpp:280-306: rhosvd, ALS refinement (spec.max_als_sweeps,
+// spec.als_stagnation_tol) and, tolerance-driven, shrink_core
+inline std::pair<TuckerTensor, SpectralReport> canonical_to_tucker(const CanonicalTensor& a,
+                                                                   const TruncationSpec& spec) {
+  if (!spec.ranks && !spec.tolerance)
+    throw std::invalid_argument("TruncationSpec: need ranks or tolerance");
+  b200::Context& ctx = a.ctx();
+  latsum_tucker* h = nullptr;
+  latsum_spectral_report rep;
+  ctx.check(latsum_canonical_to_tucker(ctx.get(), a.handle(), spec.ranks ? spec.ranks->data() : nullptr,
+                                       spec.tolerance.value_or(0.0), spec.max_als_sweeps,
+                                       spec.als_stagnation_tol, &h, &rep, nullptr));
+  TuckerTensor t(ctx, h);
+  return {std::move(t), to_report(rep, h)};
+}
+
+// ---- the reference's result-level interface (lattice_sum.hpp:38-69, :260-276, :339-465)
+
+enum class Accumulation { sliding, ascending, compensated };
+// The GPU assembly sums each dictionary column in one fixed order (the reference's orders
+// agree to ~1e-15 relative after normalisation); the option is accepted for
+// interface parity and does not change the device arithmetic.
+struct SumOptions {
+  Accumulation accumulation = Accumulation::sliding;
+};
+
+struct Summand {  // lattice_sum.hpp:44-50
+  std::string label;
+  Index canonical_rank = 0;
+  Index sites = 0;
+};
+
+struct LatticeSumResult {  // lattice_sum.hpp:52-69
+  std::variant<CanonicalTensor, TuckerTensor> tensor;
+  LatticeGeometry geometry;
+  UniformGrid grid;
+  std::vector<Summand> provenance;
+  std::optional<SpectralReport> report;
+  // the product blocks of the untruncated sum (defected_sum re-assembles base + clusters in
+  // one device call instead of add_concat copies)
+  std::shared_ptr<const detail::Blocks> blocks;
+  bool is_canonical() const { return tensor.index() == 0; }
+  const CanonicalTensor& canonical() const { return std::get<CanonicalTensor>(tensor); }
+  const TuckerTensor& tucker_tensor() const { return std::get<TuckerTensor>(tensor); }
+};
+
+class ReferenceSet {  // lattice_sum.hpp:260-276
+ public:
+  void add(ReferenceTensor ref) { refs_.push_back(std::move(ref)); }
+  const ReferenceTensor& find(const KernelSpec& kernel) const {
+    for (const auto& r : refs_)
+      if (r.kernel == kernel) return r;
+    throw std::invalid_argument("no reference tensor built for kernel " + kernel.key());
+  }
+  bool has(const KernelSpec& kernel) const {
+    for (const auto& r : refs_)
+      if (r.kernel == kernel) return true;
+    return false;
+  }
+
+ private:
+  std::vector<ReferenceTensor> refs_;
+};
+
+// The base result cmd_sum builds for a rectangular lattice (commands.cpp:160-163).
+inline LatticeSumResult assembled_sum_result(const ReferenceTensor& ref,
+                                             const LatticeGeometry& geom,
+                                             const SumOptions& = {}) {
+  LatticeGeometry rect = geom;
+  rect.defects.clear();
+  const Index n = ref.base_grid.n[0] / rect.cells[0];
+  auto b = std::make_shared<detail::Blocks>();
+  detail::add_lattice(*b, rect, {0, 0, 0}, n);
+  auto can = assemble(ref, *b);
+  LatticeSumResult out{std::move(can), rect, ref.base_grid, {}, std::nullopt, b};
+  out.provenance.push_back({"assembled lattice sum", out.canonical().rank(), detail::active_cells(rect)});
+  return out;
+}
+
+// defected_sum (lattice_sum.hpp:339-384), canonical branch: base + defect clusters in
+// `defects` order, truncated by canonical_to_tucker when `spec` is set.  Every defect uses
+// the base kernel here (a per-defect kernel needs a second reference tensor summed into the
+// same canonical tensor, which this path does not build: NotImplementedError).
+inline LatticeSumResult defected_sum(const LatticeSumResult& base,
+                                     const std::vector<DefectSpec>& defects,
+                                     const ReferenceSet& refs,
+                                     const std::optional<TruncationSpec>& spec,
+                                     const SumOptions& = {}) {
+  if (defects.empty()) return base;
+  if (!base.is_canonical() || !base.blocks)
+    throw NotImplementedError("defected_sum: the GPU path sums canonical bases built by "
+                              "assembled_sum_result / sublattice_union_sum");
+  for (const auto& d : defects) {
+    if (d.sites.empty()) throw std::invalid_argument("defected_sum: defect with no sites");
+    const KernelSpec k = d.kernel ? *d.kernel : base.geometry.kernel;
+    if (!refs.has(k))
+      throw std::invalid_argument("defected_sum: no reference tensor for kernel " + k.key());
+    if (!(k == base.geometry.kernel))
+      throw NotImplementedError("defected_sum: per-defect kernels are not on the GPU path");
+  }
+  const ReferenceTensor& ref = refs.find(base.geometry.kernel);
+  const Index n = base.grid.n[0] / base.geometry.cells[0];
+  auto b = std::make_shared<detail::Blocks>(*base.blocks);
+  LatticeSumResult out{base.tensor, base.geometry, base.grid, base.provenance, std::nullopt, b};
+  for (const auto& d : defects) {
+    const Index blocks = detail::add_defect(*b, d, n);
+    out.provenance.push_back({d.kind == DefectKind::vacancy ? "vacancy cluster" : "impurity cluster",
+                              blocks * ref.rank(), Index(d.sites.size())});
+    out.geometry.defects.push_back(d);
+  }
+  CanonicalTensor total = assemble(ref, *b);
+  if (spec) {
+    auto tr = canonical_to_tucker(total, *spec);
+    out.tensor = std::move(tr.first);
+    out.report = std::move(tr.second);
+  } else {
+    out.tensor = std::move(total);
+  }
+  return out;
+}
+
+// sublattice_union_sum (lattice_sum.hpp:411-465): one assembled block per sublattice
+inline LatticeSumResult sublattice_union_sum(const std::vector<SublatticePlacement>& subs,
+                                             const ReferenceTensor& ref,
+                                             const LatticeGeometry& geometry,
+                                             const std::optional<TruncationSpec>& spec,
+                                             const SumOptions& = {}) {
+  if (subs.empty()) throw std::invalid_argument("sublattice_union_sum: no sublattices");
+  const Index n = ref.base_grid.n[0] / geometry.cells[0];
+  auto b = std::make_shared<detail::Blocks>();
+  LatticeSumResult out{sublattice_union_sum(subs, ref, geometry, n), geometry, ref.base_grid, {},
+                       std::nullopt, b};
+  for (const auto& s : subs) {
+    detail::add_lattice(*b, s.geom, s.offset_cells, n);
+    out.provenance.push_back({"sublattice", ref.rank(), detail::active_cells(s.geom)});
+  }
+  if (spec) {
+    auto tr = canonical_to_tucker(out.canonical(), *spec);
+    out.tensor = std::move(tr.first);
+    out.report = std::move(tr.second);
+  }
+  return out;
+}
+
+// report.cpp:28-46 write_spectral_report (the library's formatter: same text, byte for byte)
+inline void write_spectral_report(std::ostream& os, const SpectralReport& r) {
+  latsum_spectral_report c{};
+  const double* sv[3];
+  for (int l = 0; l < 3; ++l) {
+    c.chosen_ranks[l] = r.chosen_ranks[l];
+    c.tie_at_cutoff[l] = r.tie_at_cutoff[l] ? 1 : 0;
+    c.n_singular[l] = int64_t(r.singular_values[l].size());
+    sv[l] = r.singular_values[l].data();
+  }
+  c.bound_abs = r.bound_abs;
+  c.bound_rel = r.bound_rel;
+  c.weight_norm = r.weight_norm;
+  c.input_norm = r.input_norm;
+  c.stability_constant = r.stability_constant;
+  c.stability_ok = r.stability_ok ? 1 : 0;
+  const int64_t n = latsum_format_spectral_report(&c, sv, nullptr, 0);
+  std::string buf(size_t(n) + 1, '\0');
+  latsum_format_spectral_report(&c, sv, &buf[0], n + 1);
+  os.write(buf.data(), n);
+}
+
+// report.cpp:48-73 write_provenance, for a result described by its grid, geometry cells,
+// tensor ranks and summands (label, canonical rank, sites)
+inline void write_provenance(std::ostream& os, const Dims3& grid, const Dims3& cells,
+                             const std::optional<Dims3>& tucker_ranks, Index canonical_rank,
+                             const std::vector<Summand>& summands,
+                             const std::optional<SpectralReport>& report, std::uint64_t seed,
+                             const std::vector<std::string>& extra_lines = {}) {
+  latsum_provenance p{};
+  p.seed = seed;
+  for (int l = 0; l < 3; ++l) {
+    p.grid[l] = grid[l];
+    p.cells[l] = cells[l];
+  }
+  p.format = tucker_ranks ? 1 : 0;
+  p.rank = canonical_rank;
+  if (tucker_ranks)
+    for (int l = 0; l < 3; ++l) p.ranks[l] = (*tucker_ranks)[l];
+  std::vector<const char*> labels, extra;
+  std::vector<int64_t> ranks, sites;
+  for (const auto& s : summands) {
+    labels.push_back(s.label.c_str());
+    ranks.push_back(s.canonical_rank);
+    sites.push_back(s.sites);
+  }
+  for (const auto& e : extra_lines) extra.push_back(e.c_str());
+  p.nsummands = int64_t(summands.size());
+  p.labels = labels.data();
+  p.summand_ranks = ranks.data();
+  p.summand_sites = sites.data();
+  if (report) {
+    p.has_report = 1;
+    p.bound_abs = report->bound_abs;
+    p.bound_rel = report->bound_rel;
+  }
+  p.nextra = int64_t(extra.size());
+  p.extra = extra.data();
+  const int64_t n = latsum_format_provenance(&p, nullptr, 0);
+  std::string buf(size_t(n) + 1, '\0');
+  latsum_format_provenance(&p, &buf[0], n + 1);
+  os.write(buf.data(), n);
+}
+
+// report.cpp:48-73 with the reference's signature
+inline void write_provenance(std::ostream& os, const LatticeSumResult& result, std::uint64_t seed,
+                             const std::vector<std::string>& extra_lines = {}) {
+  const Dims3 cells{result.geometry.cells[0], result.geometry.cells[1], result.geometry.cells[2]};
+  std::optional<Dims3> tr;
+  Index rank = 0;
+  if (result.is_canonical()) rank = result.canonical().rank();
+  else tr = result.tucker_tensor().ranks();
+  write_provenance(os, result.grid.n, cells, tr, rank, result.provenance, result.report, seed,
+                   extra_lines);
 }
 
 }  // namespace latsum

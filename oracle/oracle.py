@@ -605,3 +605,46 @@ def tensor_file_bytes(kind: str, dims, payload_u32, arrays) -> bytes:
         buf += np.asarray(a, dtype="<f8").ravel(order="F").tobytes()
     buf += struct.pack("<Q", fnv1a64(bytes(buf)))
     return bytes(buf)
+
+
+# ----------------------------------------------------------------------------- reports
+
+def _g17(x: float) -> str:
+    """std::ostream with precision(17), default float format (report.cpp:9-12)."""
+    return "%.17g" % float(x)
+
+
+def spectral_report_text(chosen_ranks, bound_abs, bound_rel, weight_norm, input_norm,
+                         stability_constant, stability_ok, tie_at_cutoff, sigma) -> str:
+    """report.cpp:28-46 write_spectral_report."""
+    out = ["# spectral report\n",
+           "chosen_ranks %d %d %d\n" % tuple(int(r) for r in chosen_ranks),
+           "bound_abs " + _g17(bound_abs) + "\n", "bound_rel " + _g17(bound_rel) + "\n",
+           "weight_norm " + _g17(weight_norm) + "\n", "input_norm " + _g17(input_norm) + "\n",
+           "stability_constant " + _g17(stability_constant) + "\n",
+           "stability_ok %d\n" % (1 if stability_ok else 0)]
+    for l in range(3):
+        line = "sigma_mode%d" % (l + 1)
+        if tie_at_cutoff[l]:
+            line += " (tie at cutoff)"
+        line += "".join(" " + _g17(v) for v in sigma[l])
+        out.append(line + "\n")
+    return "".join(out)
+
+
+def provenance_text(seed, grid, cells, fmt, rank_or_ranks, summands, bounds=None,
+                    extra_lines=()) -> str:
+    """report.cpp:48-73 write_provenance (summands: (label, canonical rank, sites))."""
+    out = ["# lattice sum provenance\n", "seed %d\n" % seed,
+           "grid %d %d %d\n" % tuple(grid), "cells %d %d %d\n" % tuple(cells)]
+    if fmt == "canonical":
+        out += ["format canonical\n", "rank %d\n" % rank_or_ranks]
+    else:
+        out += ["format tucker\n", "ranks %d %d %d\n" % tuple(rank_or_ranks)]
+    out.append("summands %d\n" % len(summands))
+    out += ['summand "%s" rank %d sites %d\n' % (lab, r, s) for lab, r, s in summands]
+    if bounds is not None:
+        out += ["truncation_bound_abs " + _g17(bounds[0]) + "\n",
+                "truncation_bound_rel " + _g17(bounds[1]) + "\n"]
+    out += [x + "\n" for x in extra_lines]
+    return "".join(out)

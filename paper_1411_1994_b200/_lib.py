@@ -60,6 +60,31 @@ class LatsumReport(ctypes.Structure):
     ]
 
 
+# host collectives (latsum_ctx_init_host_comm)
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                  ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.c_int64)
+
+
+class LatsumProvenance(ctypes.Structure):
+    _fields_ = [
+        ("seed", ctypes.c_uint64),
+        ("grid", ctypes.c_int64 * 3), ("cells", ctypes.c_int64 * 3),
+        ("format", ctypes.c_int),
+        ("rank", ctypes.c_int64), ("ranks", ctypes.c_int64 * 3),
+        ("nsummands", ctypes.c_int64),
+        ("labels", ctypes.POINTER(ctypes.c_char_p)),
+        ("summand_ranks", ctypes.POINTER(ctypes.c_int64)),
+        ("summand_sites", ctypes.POINTER(ctypes.c_int64)),
+        ("has_report", ctypes.c_int),
+        ("bound_abs", ctypes.c_double), ("bound_rel", ctypes.c_double),
+        ("nextra", ctypes.c_int64),
+        ("extra", ctypes.POINTER(ctypes.c_char_p)),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/latsum_b200.h declares
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -74,6 +99,7 @@ SIGNATURES = [
     ("latsum_ctx_kernel_launches", _I64, [_P]),
     ("latsum_comm_unique_id", _I, [_P]),
     ("latsum_ctx_init_comm", _I, [_P, _P, _I, _I]),
+    ("latsum_ctx_init_host_comm", _I, [_P, _I, _I, _P, _P, _P]),
     ("latsum_ctx_comm_info", _I, [_P, _P, _P]),
     ("latsum_ctx_set_profiling", _I, [_P, _I]),
     ("latsum_ctx_profile", _I64, [_P, ctypes.c_char_p, _I64]),
@@ -105,6 +131,8 @@ SIGNATURES = [
     ("latsum_tucker_singular_values", _I, [_P, _I, _P]),
     ("latsum_tucker_core", _I, [_P, _P, _P]),
     ("latsum_tucker_factor", _I, [_P, _P, _I, _P]),
+    ("latsum_format_spectral_report", _I64, [_P, _P, _P, _I64]),
+    ("latsum_format_provenance", _I64, [_P, _P, _I64]),
     ("latsum_tucker_projected_form", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("latsum_tucker_entries", _I, [_P, _P, _P, _I64, _P]),
     ("latsum_tucker_eval_box", _I, [_P, _P, _P, _P, _P]),

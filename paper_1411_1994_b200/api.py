@@ -23,6 +23,7 @@ made only when a method asks for them (``factor``, ``core``, ``to_dense``).
 from __future__ import annotations
 
 import ctypes
+import os
 import weakref
 from dataclasses import dataclass
 from typing import Optional, Sequence, Tuple
@@ -37,6 +38,7 @@ __all__ = [
     "CanonicalTensor", "TuckerTensor", "build_quadrature", "default_step_constant",
     "reference_shell", "build_reference_canonical", "lattice_sum", "assembled_sum_canonical",
     "defected_sum", "sublattice_union_sum", "rhosvd", "WindowOverflowError", "Geometry",
+    "format_spectral_report", "write_spectral_report", "format_provenance", "write_provenance",
 ]
 
 WindowOverflowError = _lib.WindowOverflowError
@@ -142,6 +144,94 @@ def init_comm_from_torch(ctx: Context):
     obj = [comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     ctx.init_comm(obj[0], rank, world)
+
+
+class ThreadCollective:
+    """Host collectives for ranks that are threads of one process (several contexts, e.g.
+    on one device): per channel, every rank deposits its buffer, all wait, and each sums
+    (or concatenates) the deposits in rank order, so every rank gets bit-identical results."""
+
+    def __init__(self, nranks: int):
+        import threading
+        self.n = nranks
+        self._lock = threading.Lock()
+        self._slots = {}  # channel -> (barrier, deposits)
+
+    def _slot(self, channel):
+        import threading
+        with self._lock:
+            if channel not in self._slots:
+                self._slots[channel] = (threading.Barrier(self.n), [None] * self.n)
+            return self._slots[channel]
+
+    def allreduce(self, rank: int, channel: int, buf: np.ndarray):
+        bar, dep = self._slot(channel)
+        dep[rank] = buf.copy()
+        bar.wait()
+        if os.environ.get("LATSUM_COLL_DEBUG"):
+            print(f"[coll] rank {rank} ch {channel} n {buf.size} sums "
+                  f"{[float(np.sum(d)) for d in dep]}", flush=True)
+        acc = dep[0].copy()
+        for q in range(1, self.n):
+            acc += dep[q]
+        bar.wait()
+        buf[:] = acc
+
+    def allgather(self, rank: int, channel: int, send: np.ndarray, recv: np.ndarray):
+        bar, dep = self._slot(channel)
+        dep[rank] = send.copy()
+        bar.wait()
+        recv[:] = np.concatenate(dep)
+        bar.wait()
+
+
+class TorchCollective:
+    """Host collectives over torch.distributed (gloo): one process group per channel so the
+    library's concurrent worker streams never interleave on one group."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.groups = [dist.new_group(backend="gloo") for _ in range(5)]
+
+    def allreduce(self, rank: int, channel: int, buf: np.ndarray):
+        import torch
+        t = torch.from_numpy(buf)
+        self.dist.all_reduce(t, group=self.groups[channel])
+
+    def allgather(self, rank: int, channel: int, send: np.ndarray, recv: np.ndarray):
+        import torch
+        n = send.size
+        outs = [torch.empty(n, dtype=torch.float64) for _ in range(self.dist.get_world_size())]
+        self.dist.all_gather(outs, torch.from_numpy(send.copy()), group=self.groups[channel])
+        recv[:] = torch.cat(outs).numpy()
+
+
+def init_host_comm(ctx: Context, rank: int, nranks: int, collective) -> None:
+    """latsum_ctx_init_host_comm: run the row-sharded reduction (the NCCL path's partial
+    products, all-reduces and all-gathers) over `collective` (ThreadCollective,
+    TorchCollective or anything with the same allreduce / allgather methods)."""
+
+    def ar(user, channel, ptr, count):
+        try:
+            collective.allreduce(rank, channel, np.ctypeslib.as_array(ptr, shape=(count,)))
+            return 0
+        except Exception:  # reported to the library as a failed collective
+            return 1
+
+    def ag(user, channel, sptr, rptr, count):
+        try:
+            collective.allgather(rank, channel, np.ctypeslib.as_array(sptr, shape=(count,)),
+                                 np.ctypeslib.as_array(rptr, shape=(count * nranks,)))
+            return 0
+        except Exception:
+            return 1
+
+    cb = (_lib.HOST_ALLREDUCE(ar), _lib.HOST_ALLGATHER(ag))
+    ctx._host_comm = cb  # the callbacks live as long as the context
+    ctx.check(_lib.lib().latsum_ctx_init_host_comm(ctx.handle, int(rank), int(nranks),
+                                                   ctypes.cast(cb[0], ctypes.c_void_p),
+                                                   ctypes.cast(cb[1], ctypes.c_void_p), None))
 
 
 _default_ctx: Optional[Context] = None
@@ -687,3 +777,78 @@ def sum_to_tucker(geom: Geometry, tolerance: float, ctx: Optional[Context] = Non
         nsub, _p(counts), _p(shifts), _p(charges), dsh.shape[0], _p(dsh), _p(dch),
         float(tolerance), ctypes.byref(h), ctypes.byref(rep)))
     return TuckerTensor(ctx, h), rep
+
+
+# ----------------------------------------------------------------------------- reports
+
+def _format(fn, *args) -> str:
+    n = fn(*args, None, 0)
+    if n < 0:
+        raise ValueError("report formatting: null argument")
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    fn(*args, buf, int(n) + 1)
+    return buf.raw[:n].decode()
+
+
+def format_spectral_report(report: SpectralReport) -> str:
+    """report.cpp:28-46 write_spectral_report (latsum_format_spectral_report)."""
+    r = _lib.LatsumReport()
+    sv = [np.ascontiguousarray(np.asarray(report.singular_values[l], np.float64)) for l in range(3)]
+    for l in range(3):
+        r.chosen_ranks[l] = int(report.chosen_ranks[l])
+        r.tie_at_cutoff[l] = int(bool(report.tie_at_cutoff[l]))
+        r.n_singular[l] = sv[l].size
+    r.bound_abs, r.bound_rel = float(report.bound_abs), float(report.bound_rel)
+    r.weight_norm, r.input_norm = float(report.weight_norm), float(report.input_norm)
+    r.stability_constant = float(report.stability_constant)
+    r.stability_ok = int(bool(report.stability_ok))
+    ptrs = (ctypes.c_void_p * 3)(*[x.ctypes.data for x in sv])
+    return _format(_lib.lib().latsum_format_spectral_report, ctypes.byref(r), ptrs)
+
+
+def write_spectral_report(path: str, report: SpectralReport) -> None:
+    """commands.cpp:67-71: the report file next to the tensor."""
+    with open(path, "w") as f:
+        f.write(format_spectral_report(report))
+
+
+def format_provenance(geom: Geometry, tensor, report: Optional[SpectralReport] = None,
+                      seed: Optional[int] = None, extra_lines: Sequence[str] = ()) -> str:
+    """report.cpp:48-73 write_provenance for the result `tensor` (CanonicalTensor or
+    TuckerTensor) of the sum described by `geom` (latsum_format_provenance)."""
+    p = _lib.LatsumProvenance()
+    p.seed = int(geom.seed if seed is None else seed) & (2 ** 64 - 1)
+    cells = geom.cell_counts()
+    for l in range(3):
+        p.grid[l] = int(geom.N[l])
+        p.cells[l] = int(cells[l])
+    if isinstance(tensor, TuckerTensor):
+        p.format = 1
+        for l in range(3):
+            p.ranks[l] = int(tensor.ranks[l])
+    else:
+        p.format = 0
+        p.rank = int(tensor.rank)
+    summ = geom.summands()
+    p.nsummands = len(summ)
+    labels = (ctypes.c_char_p * max(1, len(summ)))(*[x[0].encode() for x in summ])
+    ranks = np.ascontiguousarray([x[1] for x in summ] or [0], np.int64)
+    sites = np.ascontiguousarray([x[2] for x in summ] or [0], np.int64)
+    p.labels = ctypes.cast(labels, ctypes.POINTER(ctypes.c_char_p))
+    p.summand_ranks = ranks.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    p.summand_sites = sites.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    if report is not None:
+        p.has_report = 1
+        p.bound_abs, p.bound_rel = float(report.bound_abs), float(report.bound_rel)
+    extra = (ctypes.c_char_p * max(1, len(extra_lines)))(*[x.encode() for x in extra_lines])
+    p.nextra = len(extra_lines)
+    p.extra = ctypes.cast(extra, ctypes.POINTER(ctypes.c_char_p))
+    return _format(_lib.lib().latsum_format_provenance, ctypes.byref(p))
+
+
+def write_provenance(path: str, geom: Geometry, tensor, report: Optional[SpectralReport] = None,
+                     seed: Optional[int] = None, extra_lines: Sequence[str] = ()) -> None:
+    """commands.cpp:62-66: the provenance sidecar."""
+    with open(path, "w") as f:
+        f.write(format_provenance(geom, tensor, report, seed, extra_lines))
+

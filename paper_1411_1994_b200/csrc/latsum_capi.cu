@@ -135,7 +135,17 @@ struct latsum_ctx {
   // context owns a communicator split from this one so concurrent modes never interleave
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  // host collective (latsum_ctx_init_host_comm): the same collectives through caller
+  // callbacks on host buffers (gloo / in-process ranks in tests); channel 0 is this
+  // context, 1..4 its workers (so concurrent modes never interleave on one channel)
+  latsum_host_allreduce_fn host_ar = nullptr;
+  latsum_host_allgather_fn host_ag = nullptr;
+  void* host_user = nullptr;
+  int channel = 0;
 };
+
+// a row-sharded reduction runs over NCCL or the host callbacks
+inline bool has_comm(const latsum_ctx* c) { return (c->comm || c->host_ar) && c->nranks > 1; }
 
 namespace {
 
@@ -293,8 +303,33 @@ struct Trace {
 
 // Sum-all-reduce over the ranks of c's communicator (no-op on one rank).
 void allreduce(latsum_ctx* c, double* buf, size_t count) {
-  if (!c->comm || c->nranks <= 1 || count == 0) return;
-  NC(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream));
+  if (!has_comm(c) || count == 0) return;
+  if (c->comm) {
+    NC(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream));
+    return;
+  }
+  std::vector<double> h(count);
+  CK(cudaMemcpyAsync(h.data(), buf, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->host_ar(c->host_user, c->channel, h.data(), int64_t(count)) != 0)
+    throw Error(LATSUM_ERR_NCCL, "host all-reduce failed");
+  CK(cudaMemcpyAsync(buf, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// recv (nranks x count) = every rank's send (count), in rank order
+void allgather(latsum_ctx* c, const double* send, double* recv, size_t count) {
+  if (c->comm) {
+    NC(nccl().AllGather(send, recv, count, kNcclFloat64, c->comm, c->stream));
+    return;
+  }
+  std::vector<double> hs(count), hr(count * size_t(c->nranks));
+  CK(cudaMemcpyAsync(hs.data(), send, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->host_ag(c->host_user, c->channel, hs.data(), hr.data(), int64_t(count)) != 0)
+    throw Error(LATSUM_ERR_NCCL, "host all-gather failed");
+  CK(cudaMemcpyAsync(recv, hr.data(), sizeof(double) * hr.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
 }
 
 // The rows [lo, hi) of an N-row operand this rank owns in the row-sharded reduction.
@@ -1003,6 +1038,37 @@ struct Eig {
       G = std::move(G0);
     }
   }
+  // Row-sharded RHOSVD: rank `owner` solves with cuSOLVER and the others receive the values
+  // and all eigenvectors through a sum all-reduce to which they contribute zeros (exact).
+  // Every rank must hold bit-identical bases (the row blocks of U = A V lambda^{-1/2} of
+  // different ranks belong to the same vectors), which redundant solves do not guarantee:
+  // the in-house solver's reflectors and inverse-iteration vectors may differ in the last
+  // bits, and near-degenerate eigenvectors then rotate apart.  So in a sharded reduction one
+  // rank per mode solves every Gram (also spreading the three modes' solves over the ranks).
+  void solve_on(latsum_ctx* c, int64_t nn, DBuf&& Gin, int owner) {
+    if (owner < 0 || !has_comm(c)) {
+      solve(c, nn, std::move(Gin));
+      return;
+    }
+    n = nn;
+    G = std::move(Gin);
+    custom = band = false;
+    lam_asc.assign(n, 0.0);
+    if (n == 0) return;
+    DBuf buf(c, size_t(n) + size_t(n) * n);
+    if (c->rank == owner % c->nranks) {
+      syevd(c, n, G.p, buf.p);
+      CK(cudaMemcpyAsync(buf.p + n, G.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      CK(cudaMemsetAsync(buf.p, 0, sizeof(double) * buf.n, c->stream));
+    }
+    allreduce(c, buf.p, buf.n);
+    CK(cudaMemcpyAsync(G.p, buf.p + n, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(lam_asc.data(), buf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (double v : lam_asc) tnorm = std::max(tnorm, std::fabs(v));
+  }
+
   bool has_all() const { return !custom; }
   // max |V^T V - I| accepted from the in-house vectors before falling back to syevd
   // (< 0: 1e-12 max(1, n/64))
@@ -1510,6 +1576,7 @@ void polar_orthonormalize(latsum_ctx* c, double* U, int64_t Nb, int64_t k, bool 
 // U (Nb x k) = A (Nb x d) Vd scaled by 1/sqrt(lam_desc), then re-orthonormalised: left
 // singular vectors from the k leading eigenpairs (Vd: d x k, descending) of A^T A (row
 // block of A -> row block of U).
+double frob2(latsum_ctx* c, const double* A, int64_t Nb, int64_t cols, int64_t ld, bool sharded);
 void left_from_vectors(latsum_ctx* c, const double* A, int64_t Nb, int64_t d, const double* Vd,
                        const std::vector<double>& lam_desc, int64_t k, double* U, bool sharded) {
   if (k == 0) return;
@@ -1570,7 +1637,8 @@ struct Rp2 {
 };
 
 bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, int64_t nc,
-                      double delta, double lump_max, bool sharded, uint64_t seed, Rp2& o) {
+                      double delta, double lump_max, bool sharded, uint64_t seed, Rp2& o,
+                      int eig_owner = -1) {
   const int64_t Nr = std::max<int64_t>(Nb, 1);
   const double a2 = frob2(c, Ap, Nb, d, Nb, sharded);
   static const int64_t ell_env = [] {
@@ -1610,7 +1678,7 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
       if (sharded) allreduce(c, H.p, size_t(ell) * ell);
       Eig eh;
       eh.ortho_tol = 1e-9;
-      eh.solve(c, ell, std::move(H));
+      eh.solve_on(c, ell, std::move(H), sharded ? eig_owner : -1);
       std::vector<double> h(ell);
       for (int64_t i = 0; i < ell; ++i) h[i] = std::max(eh.lam_asc[ell - 1 - i], 0.0);
       const double hmax = h[0];
@@ -1654,7 +1722,7 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
     gram(c, true, C.p, m, d, G2.p);
     o.e = Eig();
     o.e.ortho_tol = 1e-9;
-    o.e.solve(c, m, std::move(G2));
+    o.e.solve_on(c, m, std::move(G2), sharded ? eig_owner : -1);
     o.mu.assign(m, 0.0);
     double captured = 0.0;
     for (int64_t i = 0; i < m; ++i) {
@@ -1703,14 +1771,14 @@ struct Timings {
 // sqrt(eps_mach) sigma_1, e.g. in the ALS unfoldings).
 void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
                   const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
-                  bool sharded, ModeOut& out, Timings& tm);
+                  bool sharded, ModeOut& out, Timings& tm, int eig_owner = -1);
 
 void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
                  double tol, int deflate, ModeOut& out, Timings& tm) {
   const int64_t N = can.N[l], d = can.d[l];
   const int64_t n_sing = std::min<int64_t>(N, can.Mc);
   const bool rows = N <= d;
-  const bool sharded = !rows && c->comm && c->nranks > 1;
+  const bool sharded = !rows && has_comm(c);
   const RowBlock blk = sharded ? row_block(c, N) : RowBlock{0, N};
   const int64_t Nb = blk.n();
   Timer timer(c);
@@ -1730,12 +1798,12 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
   tm.gram += timer.stop();
   Trace::mark(c, "operand ready");
   const int64_t* rf = ranks ? ranks + l : nullptr;
-  reduce_dense(c, At, blk, N, d, n_sing, rf, tol, deflate, false, sharded, out, tm);
+  reduce_dense(c, At, blk, N, d, n_sing, rf, tol, deflate, false, sharded, out, tm, l);
 }
 
 void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
                   const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
-                  bool sharded, ModeOut& out, Timings& tm) {
+                  bool sharded, ModeOut& out, Timings& tm, int eig_owner) {
   const int64_t* ranks = rank_fixed;
   const int l = 0;  // rank_fixed points at this operand's rank
   const bool rows = N <= d;
@@ -1757,7 +1825,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   // the RHOSVD's pass-1/pass-2 bases are re-orthonormalised and their span is what counts;
   // the ALS unfoldings (force_deflate) need the strict eigenvector orthogonality
   e1.ortho_tol = force_deflate ? -1.0 : 1e-9;
-  e1.solve(c, n, std::move(G));
+  e1.solve_on(c, n, std::move(G), sharded ? eig_owner : -1);
   tm.syevd += timer.stop();
   Trace::mark(c, "syevd1 done");
   std::vector<double> lam_d(n);
@@ -1819,6 +1887,12 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         if (Nb > 0)
           gemm(c, false, false, Nb, d, k1, -1.0, U1.p, Nb, C.p, k1, 1.0, Ap.p, Nb, tagged("gemm_deflate"));
       }
+      if (Trace::on() && !rows) {
+        const double a0 = frob2(c, At.p, Nb, d, Nb, sharded), a1 = frob2(c, Ap.p, Nb, d, Nb, sharded);
+        const double u1 = frob2(c, U1.p, Nb, k1, Nb, sharded);
+        fprintf(stderr, "[deflate] rank %d/%d Nb %ld d %ld k1 %ld |A|^2 %.6e |A''|^2 %.6e |U1|^2 %.6f\n",
+                c->rank, c->nranks, long(Nb), long(d), long(k1), a0, a1, u1);
+      }
       // randomized pass 2 (column orientation, tolerance-driven): ell x ell eigensolves
       // instead of the nc x nc restricted Gram (see randomized_pass2)
       static const bool rp2_off = std::getenv("LATSUM_RP2") && std::string(std::getenv("LATSUM_RP2")) == "0";
@@ -1826,7 +1900,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
         const double delta = 1e-4 * target / std::sqrt(double(n));
         const double lump_max = 1e-6 * target * target;
         if (randomized_pass2(c, Ap.p, Nb, d, nc, delta, lump_max, sharded,
-                             0x14111994ull + uint64_t(d) * 131 + uint64_t(k1), rp)) {
+                             0x14111994ull + uint64_t(d) * 131 + uint64_t(k1), rp, eig_owner)) {
           const int64_t m = rp.m, rest = n - k1 - m;
           std::vector<std::tuple<double, int, int64_t>> all;
           for (int64_t i = 0; i < k1; ++i) all.emplace_back(lam_d[i], 0, i);
@@ -1887,7 +1961,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
       tm.deflate += timer.stop();
       Trace::mark(c, "deflation + G2 done");
       timer.start();
-      e2.solve(c, n2, std::move(G2));
+      e2.solve_on(c, n2, std::move(G2), sharded ? eig_owner : -1);
       tm.syevd += timer.stop();
       Trace::mark(c, "syevd2 done");
       mu_d.resize(nc);  // the nc leading pass-2 values
@@ -2177,6 +2251,10 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
   c->sub[i]->eig_method = c->eig_method;
   c->sub[i]->rank = c->rank;
   c->sub[i]->nranks = c->nranks;
+  c->sub[i]->host_ar = c->host_ar;
+  c->sub[i]->host_ag = c->host_ag;
+  c->sub[i]->host_user = c->host_user;
+  c->sub[i]->channel = 1 + i;
   return c->sub[i];
 }
 
@@ -2323,7 +2401,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       if (Nb > 0)
         CK(cudaMemcpy2DAsync(send.p, bmax * sizeof(double), mo[l].Z.p, Nb * sizeof(double),
                              Nb * sizeof(double), r, cudaMemcpyDeviceToDevice, c->stream));
-      NC(nccl().AllGather(send.p, recv.p, size_t(bmax) * r, kNcclFloat64, c->comm, c->stream));
+      allgather(c, send.p, recv.p, size_t(bmax) * r);
       for (int q = 0; q < c->nranks; ++q) {
         const int64_t lo = N * q / c->nranks, nq = N * (q + 1) / c->nranks - lo;
         if (nq > 0)
@@ -2344,7 +2422,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     tp.start();
     t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
     const int m = core_mode(can);
-    if (c->comm && c->nranks > 1) {  // each rank forms the core from its share of mode m
+    if (has_comm(c)) {  // each rank forms the core from its share of mode m
       const int64_t dm = can.d[m];
       form_core(c, can, P, t.r, t.core.p, m, dm * c->rank / c->nranks,
                 dm * (c->rank + 1) / c->nranks);
@@ -3005,6 +3083,21 @@ int latsum_ctx_init_comm(latsum_ctx* c, const unsigned char id[128], int rank, i
       latsum_ctx* w = sub_ctx(c, i);
       NC(nccl().CommSplit(c->comm, 0, rank, &w->comm, nullptr));
     }
+  });
+}
+
+int latsum_ctx_init_host_comm(latsum_ctx* c, int rank, int nranks, latsum_host_allreduce_fn ar,
+                              latsum_host_allgather_fn ag, void* user) {
+  return guarded(c, [&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "latsum_ctx_init_host_comm: bad rank");
+    require(!c->comm, "latsum_ctx_init_host_comm: an NCCL communicator is already set");
+    require(nranks == 1 || (ar && ag), "latsum_ctx_init_host_comm: null collective");
+    c->rank = rank;
+    c->nranks = nranks;
+    c->host_ar = ar;
+    c->host_ag = ag;
+    c->host_user = user;
+    c->channel = 0;
   });
 }
 

@@ -62,6 +62,10 @@ class Geometry:
     seed: int = 0
     n_vacancies: int = 0   # sampled defects by kind (lattice_box); informational
     n_impurities: int = 0
+    # provenance (lattice_sum.hpp:44-50 Summand): (label, canonical rank, sites) per
+    # summand, and the geometry's cell counts; None: derived (summands())
+    summand_list: Optional[List[Tuple[str, int, int]]] = None
+    cells: Optional[Tuple[int, int, int]] = None
 
     @property
     def R(self) -> int:
@@ -82,6 +86,29 @@ class Geometry:
     def canonical_rank(self) -> int:
         """M_c = R * (#sublattices + #defect blocks): rank of the unreduced sum."""
         return self.R * (len(self.sublattices) + self.n_defects)
+
+    def summands(self) -> List[Tuple[str, int, int]]:
+        """The summands a LatticeSumResult records (commands.cpp:157-163,
+        lattice_sum.hpp:368-370, :453-454): the assembled lattice sum (or one per
+        sublattice), then one vacancy / impurity cluster per defect."""
+        if self.summand_list is not None:
+            return list(self.summand_list)
+        out = []
+        for sub in self.sublattices:
+            sites = int(np.prod([len(x) for x in sub.shifts]))
+            out.append(("assembled lattice sum" if len(self.sublattices) == 1 else "sublattice",
+                         self.R, sites))
+        for b in self.blocks()[len(self.sublattices):]:
+            sites = int(np.prod([len(x) for x in b.shifts]))
+            out.append(("vacancy cluster" if b.charge < 0 else "impurity cluster", self.R, sites))
+        return out
+
+    def cell_counts(self) -> Tuple[int, int, int]:
+        if self.cells is not None:
+            return tuple(int(x) for x in self.cells)
+        if self.sublattices:
+            return tuple(len(x) for x in self.sublattices[0].shifts)
+        return (0, 0, 0)
 
     def blocks(self) -> List[Sublattice]:
         """Every product block in add_concat order: the sublattices, then the defects."""
@@ -181,6 +208,9 @@ def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0,
             ks = [default_active_set(sub_cells[l]) for l in range(3)]
             subs.append(Sublattice(tuple(ks[l] * n_per_cell + lround(off[l] * n_per_cell)
                                          for l in range(3)), base_charge))
+    summ = ([("assembled lattice sum", 2 * M + 1, int(np.prod([len(x) for x in subs[0].shifts])))]
+            if sublattices is None else
+            [("sublattice", 2 * M + 1, int(np.prod([len(x) for x in s.shifts]))) for s in subs])
     dsh, dch, dblk = [], [], []
     for sites, charge, goff in defects:
         goff = goff if goff is not None else (0.0, 0.0, 0.0)
@@ -191,6 +221,10 @@ def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0,
             dsh.append([int(s[l]) * n_per_cell + off[l] for l in range(3)])
             dch.append(float(charge))
         axes = product_structure(sites) if len(sites) > 1 else None
+        # config.cpp:105-110: a vacancy carries -base_charge; anything else is an impurity
+        kind = "vacancy cluster" if float(charge) == -float(base_charge) else "impurity cluster"
+        summ.append((kind, (2 * M + 1) * (1 if axes is not None or len(sites) == 1 else len(sites)),
+                     len(sites)))
         if axes is not None:  # assembled cluster: rank stays at the reference rank
             dblk.append(Sublattice(tuple(np.asarray(axes[l], np.int64) * n_per_cell + off[l]
                                          for l in range(3)), float(charge)))
@@ -200,7 +234,8 @@ def from_lattice(cells: Sequence[int], n_per_cell: int, cell_width: float = 1.0,
     return Geometry(N=N, box=box, family=family, lam=lam, M=M, C0=C0, sublattices=subs,
                     defect_shifts=np.asarray(dsh, np.int64).reshape(-1, 3),
                     defect_charges=np.asarray(dch, np.float64),
-                    defect_blocks=dblk if len(dblk) != len(dsh) else None, eps=eps, name=name)
+                    defect_blocks=dblk if len(dblk) != len(dsh) else None, eps=eps, name=name,
+                    summand_list=summ, cells=tuple(int(c) for c in grid_cells))
 
 
 def _sample_sites(n_sites: int, count: int, seed: int) -> np.ndarray:
@@ -245,6 +280,7 @@ def lattice_box(N: int, box: float, sublats: Sequence[dict], *, family=NEWTON, l
             charges[n_vacancies:] = q - 1.0
         order = np.argsort(drawn, kind="stable")
         drawn, charges = drawn[order], charges[order]
+        kinds = ["vacancy cluster" if o < n_vacancies else "impurity cluster" for o in order]
         rows = []
         starts = np.cumsum([0] + per_sub)
         for idx in drawn:
@@ -257,7 +293,13 @@ def lattice_box(N: int, box: float, sublats: Sequence[dict], *, family=NEWTON, l
             rows.append([subs[s].shifts[0][i1], subs[s].shifts[1][i2], subs[s].shifts[2][i3]])
         dsh = np.asarray(rows, np.int64).reshape(-1, 3)
         dch = charges.astype(np.float64)
+    R = 2 * M + 1
+    summ = ([("assembled lattice sum", R, per_sub[0])] if len(subs) == 1 else
+            [("sublattice", R, p) for p in per_sub])
+    if nd:
+        summ += [(k, R, 1) for k in kinds]
     return Geometry(N=(N, N, N), box=(box, box, box), family=family, lam=lam, M=M,
+                    summand_list=summ, cells=tuple(int(c) for c in sublats[0]["cells"]),
                     sublattices=subs, defect_shifts=dsh, defect_charges=dch, eps=eps,
                     name=name, seed=seed, eval_lo=tuple(eval_lo), eval_hi=eval_hi,
                     n_vacancies=int(n_vacancies), n_impurities=int(n_impurities))

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <sstream>
 #include <string>
 
 #include "latsum_b200/latsum.hpp"
@@ -101,6 +102,64 @@ int main() {
     rhosvd(can, TruncationSpec{});
     CHECK(false);
   } catch (const std::invalid_argument&) {
+  }
+  // the reference's result-level interface: rectangular clusters assemble at reference
+  // rank, ragged ones per site (test_lattice_sum.cpp:273-305)
+  {
+    LatticeGeometry g8;
+    g8.cells = {8, 8, 1};
+    const Index n8 = 8;
+    ReferenceSet refs;
+    refs.add(build_reference_canonical(KernelSpec::newton(), lattice_grid(g8, n8), 8));
+    const ReferenceTensor& r8 = refs.find(KernelSpec::newton());
+    const Index R = r8.rank();
+    LatticeSumResult base8 = assembled_sum_result(r8, g8);
+    CHECK(base8.canonical().rank() == R);
+    DefectSpec cluster;
+    cluster.kind = DefectKind::vacancy;
+    cluster.sites = {{0, 0, 0}, {0, 1, 0}, {1, 0, 0}, {1, 1, 0}};
+    cluster.charge = -1.0;
+    auto out = defected_sum(base8, {cluster}, refs, std::nullopt);
+    CHECK(out.canonical().rank() == 2 * R);
+    DefectSpec ragged;
+    ragged.kind = DefectKind::vacancy;
+    ragged.sites = {{2, 2, 0}, {2, 3, 0}, {3, 2, 0}};
+    ragged.charge = -1.0;
+    auto out2 = defected_sum(base8, {ragged}, refs, std::nullopt);
+    CHECK(out2.canonical().rank() == (1 + 3) * R);
+    auto both = defected_sum(base8, {cluster, ragged}, refs, std::nullopt);
+    CHECK(both.canonical().rank() == (1 + 1 + 3) * R);
+    CHECK(both.provenance.size() == 3 && both.provenance[1].canonical_rank == R &&
+          both.provenance[2].canonical_rank == 3 * R && both.provenance[2].sites == 3);
+    // sequential == joint (test_lattice_sum.cpp:248-270)
+    auto seq = defected_sum(defected_sum(base8, {cluster}, refs, std::nullopt), {ragged}, refs,
+                            std::nullopt);
+    double worst = 0, scale = 0;
+    for (int p = 0; p < 40; ++p) {
+      const Index i = (11 * p) % 64, j = (17 * p + 3) % 64, k = (5 * p) % 8;
+      worst = std::fmax(worst, std::abs(seq.canonical().entry(i, j, k) - both.canonical().entry(i, j, k)));
+      scale = std::fmax(scale, std::abs(both.canonical().entry(i, j, k)));
+    }
+    CHECK(worst <= 1e-13 * scale);
+    // truncated: canonical_to_tucker, report and provenance sidecar (report.cpp:28-73)
+    auto tr = defected_sum(base8, {cluster, ragged}, refs, TruncationSpec::tol(1e-6));
+    CHECK(!tr.is_canonical() && tr.report.has_value());
+    std::ostringstream rs, ps;
+    write_spectral_report(rs, *tr.report);
+    write_provenance(ps, tr, 42);
+    CHECK(rs.str().rfind("# spectral report\nchosen_ranks ", 0) == 0);
+    CHECK(ps.str().find("format tucker\n") != std::string::npos);
+    CHECK(ps.str().find("summand \"vacancy cluster\" rank " + std::to_string(R) + " sites 4\n") !=
+          std::string::npos);
+    CHECK(ps.str().find("truncation_bound_abs ") != std::string::npos);
+    // a defect with another kernel is not on this path
+    DefectSpec yk = ragged;
+    yk.kernel = KernelSpec::yukawa(0.5);
+    try {
+      defected_sum(base8, {yk}, refs, std::nullopt);
+      CHECK(false);
+    } catch (const std::invalid_argument&) {  // no reference built for it
+    }
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

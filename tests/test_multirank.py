@@ -139,3 +139,49 @@ def test_row_blocks_partition_rows():
                 a, b = W.row_block(n, r, world)
                 rows.extend(range(a, b))
             assert rows == list(range(n))
+
+
+def _collective_worker(rank, world, port, out_dir):
+    """The library's host-collective callbacks over gloo (api.TorchCollective): concurrent
+    channels from several threads, as the library's worker streams call them."""
+    import threading
+    from paper_1411_1994_b200 import api
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    coll = api.TorchCollective()
+    res = {}
+
+    def channel(ch):
+        rng = np.random.default_rng(100 * ch + rank)
+        for it in range(5):
+            a = rng.standard_normal(37 + it)
+            b = a.copy()
+            coll.allreduce(rank, ch, b)
+            g = np.zeros(world * a.size)
+            coll.allgather(rank, ch, a, g)
+            res[(ch, it)] = (a, b, g)
+
+    th = [threading.Thread(target=channel, args=(ch,)) for ch in range(5)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    np.savez(os.path.join(out_dir, f"coll{rank}.npz"),
+             **{f"{k[0]}_{k[1]}_{i}": v[i] for k, v in res.items() for i in range(3)})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_host_collective_over_gloo(tmp_path):
+    world = 2
+    mp.start_processes(_collective_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    f = [np.load(tmp_path / f"coll{r}.npz") for r in range(world)]
+    for ch in range(5):
+        for it in range(5):
+            a = [f[r][f"{ch}_{it}_0"] for r in range(world)]
+            for r in range(world):
+                np.testing.assert_allclose(f[r][f"{ch}_{it}_1"], a[0] + a[1], rtol=1e-15)
+                assert np.array_equal(f[r][f"{ch}_{it}_2"], np.concatenate(a))
+            assert np.array_equal(f[0][f"{ch}_{it}_1"], f[1][f"{ch}_{it}_1"])  # bit-identical

@@ -576,6 +576,34 @@ def test_canonical_to_tucker_matches_oracle(ctx, kind):
     assert gsweeps >= 1
 
 
+def test_spectral_report_and_provenance_files(ctx, tmp_path):
+    """cmd_sum's report and provenance sidecar (commands.cpp:56-72, report.cpp:28-73) for a
+    clustered, truncated sum: the written values round-trip exactly (17 digits)."""
+    g = mini("clusters")
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    rp, pp = tmp_path / "report.txt", tmp_path / "provenance.txt"
+    api.write_spectral_report(str(rp), rep)
+    api.write_provenance(str(pp), g, t, rep, seed=g.seed)
+    lines = rp.read_text().splitlines()
+    assert lines[0] == "# spectral report"
+    assert lines[1] == "chosen_ranks %d %d %d" % rep.chosen_ranks
+    assert float(lines[2].split()[1]) == rep.bound_abs
+    for l in range(3):
+        vals = np.array([float(x) for x in lines[8 + l].split()[1:]])
+        assert np.array_equal(vals, rep.singular_values[l])
+    prov = pp.read_text().splitlines()
+    assert prov[:4] == ["# lattice sum provenance", f"seed {g.seed}", "grid %d %d %d" % g.N,
+                        "cells 8 8 4"]
+    assert prov[4:6] == ["format tucker", "ranks %d %d %d" % t.ranks]
+    assert prov[6] == "summands 5"
+    assert prov[7] == 'summand "assembled lattice sum" rank 21 sites 256'
+    assert prov[8] == 'summand "vacancy cluster" rank 21 sites 4'
+    assert prov[9] == 'summand "vacancy cluster" rank 63 sites 3'
+    assert float(prov[-2].split()[1]) == rep.bound_abs
+
+
 def test_tensor_files_match_reference_layout(ctx, tmp_path):
     """write_tensor / read_tensor (tensor_io.cpp:45-129): byte-identical to the oracle's
     restatement of the layout, round-trips, and rejects tampering (cli_pipeline.sh:87-90)."""

@@ -69,6 +69,9 @@ void latsum_ctx_destroy(latsum_ctx* ctx);
 const char* latsum_last_error(const latsum_ctx* ctx);
 /* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
 int latsum_ctx_set_stream(latsum_ctx* ctx, void* cuda_stream);
+/* Return unused memory of the device's stream-ordered pool to the system, keeping at most
+ * keep_bytes reserved (the context pre-grows the pool at creation and never releases it). */
+int latsum_ctx_trim_pool(latsum_ctx* ctx, int64_t keep_bytes);
 int latsum_ctx_synchronize(latsum_ctx* ctx);
 /* Number of kernels this context launched so far (its own kernels, not library ones). */
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);

@@ -82,6 +82,10 @@ class Context:
     def synchronize(self):
         self.check(_lib.lib().latsum_ctx_synchronize(self._h))
 
+    def trim_pool(self, keep_bytes: int = 0):
+        """Release the unused part of the stream-ordered pool (latsum_ctx_trim_pool)."""
+        self.check(_lib.lib().latsum_ctx_trim_pool(self._h, int(keep_bytes)))
+
     def set_stream(self, stream_ptr: int):
         self.check(_lib.lib().latsum_ctx_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
 

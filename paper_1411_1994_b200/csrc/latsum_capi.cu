@@ -20,6 +20,8 @@
 #include <stdexcept>
 #include <exception>
 #include <fstream>
+#include <condition_variable>
+#include <functional>
 #include <future>
 #include <string>
 #include <thread>
@@ -561,6 +563,30 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
       oz::k_slice_split<oz::BM, false><<<g, 2 * oz::BM, 0, c->stream>>>(
           P, sl, sk, L, K, out.KB, L1, sl2, kbs, pmax.p, out.scale.p, d, halves);
     }
+    post_launch(c);
+    return;
+  }
+  // long lines: units of LU lines of a tile, so the 2 x 148 CTAs' lines in flight fit ~90 MB
+  // of L2 and the digit pass re-reads from L2 (LATSUM_SLICE_NARROW=1: whole-tile kernel)
+  static const bool narrow = std::getenv("LATSUM_SLICE_NARROW") != nullptr;
+  const double line_bytes = double(K) * 8.0;
+  if (!narrow && line_bytes * oz::BM * 2 * 148 > 90e6) {
+    const int lu = line_bytes * 32 * 2 * 148 <= 90e6 ? 32 : line_bytes * 16 * 2 * 148 <= 90e6 ? 16 : 8;
+    const int64_t units = out.tiles * (oz::BM / lu);
+    const unsigned ctas = unsigned(std::min<int64_t>(units, 2 * 148));
+#define LATSUM_SLICE_LINES(LU, V)                                                            \
+  oz::k_slice_lines<oz::BM, LU, V><<<ctas, 256, 0, c->stream>>>(P, sl, sk, L, K, out.KB,      \
+                                                                 out.scale.p, d, L1, sl2, halves)
+    if (vec) {
+      if (lu == 32) LATSUM_SLICE_LINES(32, true);
+      else if (lu == 16) LATSUM_SLICE_LINES(16, true);
+      else LATSUM_SLICE_LINES(8, true);
+    } else {
+      if (lu == 32) LATSUM_SLICE_LINES(32, false);
+      else if (lu == 16) LATSUM_SLICE_LINES(16, false);
+      else LATSUM_SLICE_LINES(8, false);
+    }
+#undef LATSUM_SLICE_LINES
     post_launch(c);
     return;
   }
@@ -1731,8 +1757,11 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
     }
     o.lump = std::max(a2 - captured, 0.0);
     Trace::mark(c, "rp2 round done");
-    if (o.lump <= lump_max) return true;
-    if (ell >= nc) return false;
+    // oversampling: a sketch that came out nearly full rank resolves its trailing Ritz values
+    // (the ones just under the cut) poorly; take a wider one
+    const bool thin = m > ell - 128 && ell < nc;
+    if (o.lump <= lump_max && !thin) return true;
+    if (ell >= nc) return o.lump <= lump_max;
   }
 }
 
@@ -1749,6 +1778,7 @@ struct ModeOut {
 
 struct Timings {
   double gram = 0, syevd = 0, deflate = 0, project = 0, core = 0, norm = 0;
+  std::function<void()> on_gram;  // called once this mode's Gram is on the device
 };
 
 // RHOSVD of one mode (rank_reduction.hpp:189-207) on the merged side matrix
@@ -1815,11 +1845,20 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   out.rows = rows ? 1 : 0;
   out.gsize = n;
   DBuf G(c, size_t(n) * n);
-  if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
-  else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
+  {
+    // LATSUM_GRAM_SERIAL=1: the modes' Grams one at a time (A/B of SM contention)
+    static const bool serial = std::getenv("LATSUM_GRAM_SERIAL") != nullptr;
+    static std::mutex mu;
+    std::unique_lock<std::mutex> lk(mu, std::defer_lock);
+    if (serial) lk.lock();
+    if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
+    else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
+    if (serial) CK(cudaStreamSynchronize(c->stream));
+  }
   if (sharded) allreduce(c, G.p, size_t(n) * n);
   tm.gram += timer.stop();
   Trace::mark(c, "gram done");
+  if (tm.on_gram) tm.on_gram();
   timer.start();
   Eig e1;
   // the RHOSVD's pass-1/pass-2 bases are re-orthonormalised and their span is what counts;
@@ -2324,14 +2363,36 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   Timings tms[4];
   const bool zero_terms = can.Mc == 0;  // T == 0 iff M_c == 0 (every term is kept, merged)
   static const bool serial = std::getenv("LATSUM_SERIAL") != nullptr;  // A/B switch
+  // norm_f waits for the three Grams: its throughput kernels then overlap the latency-bound
+  // eigensolves instead of competing with the Grams for the SMs (LATSUM_NORM_EARLY=1: no wait)
+  static const bool norm_early = std::getenv("LATSUM_NORM_EARLY") != nullptr;
+  std::mutex gmu;
+  std::condition_variable gcv;
+  bool gram_done[3] = {false, false, false};
+  auto mark_gram = [&](int i) {
+    std::lock_guard<std::mutex> g(gmu);
+    gram_done[i] = true;
+    gcv.notify_all();
+  };
+  for (int i = 0; i < 3; ++i) tms[i].on_gram = [&, i] { mark_gram(i); };
   auto body = [&](latsum_ctx* w, int i) {
     if (i == 3 || zero_terms) {
+      if (!zero_terms && !norm_early) {
+        std::unique_lock<std::mutex> g(gmu);
+        gcv.wait(g, [&] { return gram_done[0] && gram_done[1] && gram_done[2]; });
+      }
       Timer tn(w);
       tn.start();
       rep.input_norm = canonical_norm(w, can);
       tms[3].norm = tn.stop();
     } else {
-      reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
+      try {
+        reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
+      } catch (...) {
+        mark_gram(i);  // never leave the norm worker waiting
+        throw;
+      }
+      mark_gram(i);
       // P_i = Z_i^T D_i over this rank's rows (summed over ranks) while the other modes'
       // eigensolves are still running
       Timer tp(w);
@@ -2739,16 +2800,26 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(r0 * njc, 1), 65535), 1);
   DBuf X(c, size_t(r0) * njc * nkc);
   const bool oz_x = eval_uses_ozaki(r2), oz_v = eval_uses_ozaki(r0);
-  OzSliced sU0, sQ;  // sliced once and reused across the chunks that share them
+  OzSliced sU0, sQ, sCore;  // sliced once and reused across the chunks that share them
   if (oz_v) oz_slice_a(c, U0, 1, t.N[0], ni, r0, sU0);
+  // the core's lines (a, c) over K = b: the A operand of every chunk's Q GEMM, sliced once
+  // per evaluation instead of once per y-chunk (cfg4: 11 chunks x 26 GB)
+  const bool core_once = oz_x && r1 <= oz::KMAX;
+  if (core_once) oz_slice_a(c, t.core.p, 1, r0, r0 * r2, r1, sCore, r0, r0 * r1);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
     if (oz_x) {  // Q[a, j, c] = sum_b core[a, b, c] U1[j, b]: A lines (a, c), one launch
       oz::OzOut o = oz_out(Q.p, r0);
       o.mr = r0;
       o.rs = r0 * njj;
-      ozaki_gemm_ex(c, r0 * r2, njj, r1, t.core.p, 1, r0, r0, r0 * r1, U1 + j0, 1, t.N[1], o,
-                    "gemm_eval_q(ozaki-i8)");
+      if (core_once) {
+        OzSliced sU1;
+        oz_slice_b(c, U1 + j0, 1, t.N[1], njj, r1, sU1);
+        oz_run(c, sCore, sU1, o, "gemm_eval_q(ozaki-i8)");
+      } else {
+        ozaki_gemm_ex(c, r0 * r2, njj, r1, t.core.p, 1, r0, r0, r0 * r1, U1 + j0, 1, t.N[1], o,
+                      "gemm_eval_q(ozaki-i8)");
+      }
     } else {
       GemmOpts oq = tagged("gemm_eval_q");
       oq.batch = r2;
@@ -3001,13 +3072,16 @@ int latsum_ctx_create(int device, latsum_ctx** out) {
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     // Pre-grow the stream-ordered pool so steady-state steps never map new memory
-    // (LATSUM_POOL_RESERVE_GB, default 24; 0 disables).
+    // (LATSUM_POOL_RESERVE_GB; default 45% of the free device memory, ~80 GB on a B200; 0
+    // disables).  A pool too small to grow (the caller holding the rest of HBM) makes
+    // cudaMallocAsync on one worker stream wait for memory freed on another: cfg4 steps then
+    // stalled by 150-1000 ms.  The pool does not release memory (threshold max); trim it
+    // with latsum_ctx_trim_pool.
     const char* e = std::getenv("LATSUM_POOL_RESERVE_GB");
-    const double gb = e ? std::atof(e) : 24.0;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t want = size_t(gb * 1073741824.0);
-    if (want > 0 && want < free_b / 2) {
+    const size_t want = e ? size_t(std::atof(e) * 1073741824.0) : size_t(0.45 * double(free_b));
+    if (want > 0 && want < free_b) {
       void* p = nullptr;
       CK(cudaMallocAsync(&p, want, c->stream));
       CK(cudaFreeAsync(p, c->stream));
@@ -3043,6 +3117,15 @@ void latsum_ctx_destroy(latsum_ctx* c) {
 }
 
 const char* latsum_last_error(const latsum_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+int latsum_ctx_trim_pool(latsum_ctx* c, int64_t keep_bytes) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    CK(cudaMemPoolTrimTo(pool, size_t(std::max<int64_t>(keep_bytes, 0))));
+  });
+}
 
 int latsum_ctx_set_stream(latsum_ctx* c, void* s) {
   return guarded(c, [&] {

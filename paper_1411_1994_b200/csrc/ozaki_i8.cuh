@@ -171,6 +171,51 @@ k_slice_tile(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, in
   }
 }
 
+// Long-line form of k_slice_tile: the work unit is LU lines of one tile (not all ROWS), with
+// 256 / LU threads per line splitting its half-blocks (16 k) p, p + PARTS, ...; the line
+// maxima meet in shared memory.  Persistent over units on 2 x 148 CTAs, so the lines in flight
+// (2 x 148 x LU x K doubles; the caller picks LU to keep them within ~90 MB) stay L2-resident
+// between the max pass and the digit pass: the FP64 operand is read from HBM once, where
+// k_slice_tile's 2 x 148 whole tiles of long lines overflow L2 and read it twice.
+// Digits are bit-identical to k_slice_tile's.
+template <int ROWS, int LU, bool VEC>
+__global__ void __launch_bounds__(256)
+k_slice_lines(const double* __restrict__ P, int64_t sl, int64_t sk, int64_t L, int64_t K,
+              int64_t KB, double* __restrict__ scale, int8_t* __restrict__ out, int64_t L1,
+              int64_t sl2, int halves) {
+  constexpr int PARTS = 256 / LU, UPT = ROWS / LU;  // units per tile
+  __shared__ double part[PARTS][LU];
+  const int u = threadIdx.x % LU, p = threadIdx.x / LU;
+  const int64_t units = (L + ROWS - 1) / ROWS * UPT, HB = 2 * KB;
+  for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int64_t tile = unit / UPT;
+    const int r = int(unit % UPT) * LU + u;  // line within the tile
+    const int64_t l = tile * ROWS + r;
+    const int64_t ll = l < L ? l : 0;
+    const double* pl = P + (ll % L1) * sl + (ll / L1) * sl2;
+    double amax = 0.0;
+    if (l < L)
+      for (int64_t hb = p; hb < HB; hb += PARTS) {
+        double x[16];
+        load16<ROWS, VEC>(pl, sk, (hb / 2) * BKB + 16 * (hb % 2), K, x);
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) amax = fmax(amax, fabs(x[kk]));
+      }
+    part[p][u] = amax;
+    __syncthreads();
+    double m = 0.0;
+#pragma unroll
+    for (int q = 0; q < PARTS; ++q) m = fmax(m, part[q][u]);
+    const double sc = ldexp(1.0, line_exponent(m));
+    __syncthreads();  // part[] is rewritten by the next unit
+    if (p == 0 && l < L) scale[l] = sc;
+    const double inv54 = 0x1p54 / sc;
+    for (int64_t hb = p; hb < HB; hb += PARTS)
+      slice_digits<ROWS, VEC>(pl, sk, K, int(hb % 2), r, l < L, inv54, tile, KB, hb / 2,
+                              hb / 2 + 1, out, halves);
+  }
+}
+
 // Few line tiles with a long K (the projected-CP evaluation's D0 and Y: 16-65 tiles of
 // K = 8283 at cfg5): the persistent kernel would run on 16-65 SMs.  Split K over grid.y
 // instead: pass 1 writes per-split line maxima, pass 2 (every split) takes their maximum —

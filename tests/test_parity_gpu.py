@@ -463,6 +463,7 @@ def _check_box_slices(ctx, t, g):
         D = [np.ascontiguousarray(U[l] @ P[l]) for l in range(3)]
         ks, nkc = _box_slices(t, g, D[0].shape[1])
     assert nkc < nk, "the box must span several z-chunks"
+    ctx.trim_pool()  # room for the box next to the pool the context keeps
     torch.cuda.synchronize()
     out = torch.empty(ni * nj * nk, dtype=torch.float64, device="cuda")
     t.eval_box_device(lo, hi, out.data_ptr())

@@ -65,7 +65,9 @@ def test_row_sharded_rhosvd_matches_single_rank(ctx, nranks):
         assert tuple(repq.chosen_ranks) == tuple(rep1.chosen_ranks) == tuple(orc.ranks)
         for l in range(3):
             s1, sq = rep1.singular_values[l], repq.singular_values[l]
-            assert np.max(np.abs(s1 - sq)) <= 1e-12 * s1[0]
+            # the sharded run's eigensolves are cuSOLVER's (owner-solved), the single run's
+            # the in-house solver's: the spectra agree to rounding of the smallest values
+            assert np.max(np.abs(s1 - sq)) <= 1e-11 * s1[0]
         got = tq.entries(pr)
         scale = np.max(np.abs(want))
         assert np.max(np.abs(got - want)) / scale < 1e-11, q  # same tensor, other summation order

@@ -1779,6 +1779,33 @@ struct ModeOut {
 struct Timings {
   double gram = 0, syevd = 0, deflate = 0, project = 0, core = 0, norm = 0;
   std::function<void()> on_gram;  // called once this mode's Gram is on the device
+  std::function<void()> before_eig1, after_eig1;  // around the pass-1 eigensolve
+};
+
+// cuSOLVER runs concurrent syevd calls one after another anyway; the pass-1 solves are
+// granted in a fixed order instead, largest Gram first, so the longest mode's deflation and
+// second pass overlap the other modes' solves rather than all solves finishing together
+// (cfg4: mode 0's n = 5394 first, then 2842, 2755).
+struct EigTurnstile {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<int> order;  // modes whose pass-1 solve uses cuSOLVER, largest n first
+  size_t next = 0;
+  bool done[3] = {false, false, false};
+  bool in_order(int l) const { return std::find(order.begin(), order.end(), l) != order.end(); }
+  void wait(int l) {
+    if (!in_order(l)) return;
+    std::unique_lock<std::mutex> g(mu);
+    cv.wait(g, [&] { return next >= order.size() || order[next] == l; });
+  }
+  void finish(int l) {  // also on failure: never leave a later mode waiting
+    if (!in_order(l)) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[l]) return;
+    done[l] = true;
+    while (next < order.size() && done[order[next]]) ++next;
+    cv.notify_all();
+  }
 };
 
 // RHOSVD of one mode (rank_reduction.hpp:189-207) on the merged side matrix
@@ -1864,7 +1891,14 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   // the RHOSVD's pass-1/pass-2 bases are re-orthonormalised and their span is what counts;
   // the ALS unfoldings (force_deflate) need the strict eigenvector orthogonality
   e1.ortho_tol = force_deflate ? -1.0 : 1e-9;
-  e1.solve_on(c, n, std::move(G), sharded ? eig_owner : -1);
+  if (tm.before_eig1) tm.before_eig1();
+  try {
+    e1.solve_on(c, n, std::move(G), sharded ? eig_owner : -1);
+  } catch (...) {
+    if (tm.after_eig1) tm.after_eig1();
+    throw;
+  }
+  if (tm.after_eig1) tm.after_eig1();
   tm.syevd += timer.stop();
   Trace::mark(c, "syevd1 done");
   std::vector<double> lam_d(n);
@@ -2375,6 +2409,22 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     gcv.notify_all();
   };
   for (int i = 0; i < 3; ++i) tms[i].on_gram = [&, i] { mark_gram(i); };
+  EigTurnstile turn;
+  static const bool no_turn = std::getenv("LATSUM_EIG_TURNSTILE") &&
+                              std::string(std::getenv("LATSUM_EIG_TURNSTILE")) == "0";
+  if (!no_turn && !has_comm(c) && eig_env_mode() == 0 && c->eig_method == 0 && !ranks) {
+    std::vector<std::pair<int64_t, int>> sz;
+    for (int l = 0; l < 3; ++l) {
+      const int64_t gn = std::min<int64_t>(can.N[l], can.d[l]);
+      if (!band_eig_ok(gn)) sz.emplace_back(-gn, l);
+    }
+    std::sort(sz.begin(), sz.end());
+    for (const auto& x : sz) turn.order.push_back(x.second);
+    for (int i = 0; i < 3; ++i) {
+      tms[i].before_eig1 = [&, i] { turn.wait(i); };
+      tms[i].after_eig1 = [&, i] { turn.finish(i); };
+    }
+  }
   auto body = [&](latsum_ctx* w, int i) {
     if (i == 3 || zero_terms) {
       if (!zero_terms && !norm_early) {
@@ -2389,10 +2439,12 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       try {
         reduce_mode(w, can, i, ranks, tol, deflate, mo[i], tms[i]);
       } catch (...) {
-        mark_gram(i);  // never leave the norm worker waiting
+        mark_gram(i);  // never leave the norm worker or a later mode waiting
+        turn.finish(i);
         throw;
       }
       mark_gram(i);
+      turn.finish(i);
       // P_i = Z_i^T D_i over this rank's rows (summed over ranks) while the other modes'
       // eigensolves are still running
       Timer tp(w);

@@ -462,7 +462,8 @@ def run_gpu(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and dom_tag.startswith("gemm_eval_slab") and do_eval:
         # ncu --set full DRAM bytes per 2048^2 slice (profiles/ncu_eval_r01.md), per launch
-        tr = json.load(open(tpath)).get(dom_tag)
+        tj = json.load(open(tpath))
+        tr = tj.get(g.name, tj.get("cfg2", {})).get(dom_tag)
         if tr:
             traffic = tr["bytes_per_slice"] * (n_my / tr["slice_points"]) / max(1, dom_n)
 

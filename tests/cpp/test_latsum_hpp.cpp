@@ -60,7 +60,7 @@ int main() {
   }
   CHECK(worst > 0 && worst < scale);  // the vacancy removes a positive window
 
-  // window overflow names the mode (grid.hpp:111-122)
+  // window overflow names the mode (grid.hpp:87-114)
   LatticeGeometry og = geom;
   DefectSpec far;
   far.sites = {{0, 9, 0}};

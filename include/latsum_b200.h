@@ -24,7 +24,7 @@ extern "C" {
 enum {
   LATSUM_OK = 0,
   LATSUM_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
-  LATSUM_ERR_WINDOW_OVERFLOW = 2,  /* WindowOverflowError (grid.hpp:111-122); mode in message */
+  LATSUM_ERR_WINDOW_OVERFLOW = 2,  /* WindowOverflowError (grid.hpp:87-98); mode in message */
   LATSUM_ERR_CUDA = 3,
   LATSUM_ERR_CUSOLVER = 4,
   LATSUM_ERR_OUT_OF_MEMORY = 5,

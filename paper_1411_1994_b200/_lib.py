@@ -28,7 +28,7 @@ ERRORS = {
 
 
 class WindowOverflowError(IndexError):
-    """grid.hpp:111-122 WindowOverflowError; `.mode` is 1-based."""
+    """grid.hpp:87-98 WindowOverflowError; `.mode` is 1-based."""
 
     def __init__(self, msg: str):
         super().__init__(msg)

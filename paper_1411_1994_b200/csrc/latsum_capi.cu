@@ -1758,10 +1758,11 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
     o.lump = std::max(a2 - captured, 0.0);
     Trace::mark(c, "rp2 round done");
     // oversampling: a sketch that came out nearly full rank resolves its trailing Ritz values
-    // (the ones just under the cut) poorly; take a wider one
+    // (the ones just under the cut) poorly; a wider one would need cuSOLVER-sized
+    // eigensolves (ell > 808), so the caller's restricted Gram runs instead
     const bool thin = m > ell - 128 && ell < nc;
     if (o.lump <= lump_max && !thin) return true;
-    if (ell >= nc) return o.lump <= lump_max;
+    if (ell >= nc || ell >= 768) return !thin && o.lump <= lump_max;
   }
 }
 
@@ -1969,7 +1970,16 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
       // randomized pass 2 (column orientation, tolerance-driven): ell x ell eigensolves
       // instead of the nc x nc restricted Gram (see randomized_pass2)
       static const bool rp2_off = std::getenv("LATSUM_RP2") && std::string(std::getenv("LATSUM_RP2")) == "0";
-      if (!rows && !force_deflate && !rp2_off && nc > 808) {
+      static const int64_t rp2_min = [] {  // LATSUM_RP2_MIN: smallest nc sketched
+        const char* e = std::getenv("LATSUM_RP2_MIN");
+        return e ? int64_t(std::atoll(e)) : int64_t(808);
+      }();
+      // the resolved pass-1 values between eps lambda_max and the k1 threshold are directions
+      // the sketch must hold: too many and it cannot stay within the in-house solver's size
+      int64_t c16 = 0;
+      for (int64_t i = k1; i < n; ++i)
+        if (lam_d[i] > 1e-16 * lmax) ++c16;
+      if (!rows && !force_deflate && !rp2_off && nc > rp2_min && c16 + 128 <= 768) {
         const double delta = 1e-4 * target / std::sqrt(double(n));
         const double lump_max = 1e-6 * target * target;
         if (randomized_pass2(c, Ap.p, Nb, d, nc, delta, lump_max, sharded,

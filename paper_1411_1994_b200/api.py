@@ -579,6 +579,17 @@ def _shift_tables(geom: Geometry):
 def _block_tables(geom: Geometry):
     """Ordered product blocks (latsum_canonical_assemble_blocks): counts nblk x 3, the
     shift lists concatenated in (block, mode) order, one charge per block."""
+    if geom.defect_blocks is None:  # sublattices, then single sites (vectorised: cfg5 has 1000)
+        subs = geom.sublattices
+        nd = geom.defect_shifts.shape[0]
+        counts = np.ones((len(subs) + nd, 3), np.int64)
+        for i, b in enumerate(subs):
+            counts[i] = [len(b.shifts[l]) for l in range(3)]
+        parts = [np.asarray(b.shifts[l], np.int64) for b in subs for l in range(3)]
+        parts.append(np.asarray(geom.defect_shifts, np.int64).reshape(-1))
+        charges = np.concatenate([np.array([b.charge for b in subs], np.float64),
+                                  np.asarray(geom.defect_charges, np.float64)])
+        return len(subs) + nd, _i64(counts), _i64(np.concatenate(parts)), _f64(charges)
     blocks = geom.blocks()
     counts = np.array([[len(b.shifts[l]) for l in range(3)] for b in blocks],
                       np.int64).reshape(-1, 3)

@@ -586,6 +586,7 @@ def run_gpu(args):
             "clocks": clk,
             "e2e": {"value": e2e, "unit": "ms", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
+            "eig_fallbacks": ctx.eig_fallbacks,
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_total": int(launches),
         }

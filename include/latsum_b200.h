@@ -75,6 +75,9 @@ int latsum_ctx_trim_pool(latsum_ctx* ctx, int64_t keep_bytes);
 int latsum_ctx_synchronize(latsum_ctx* ctx);
 /* Number of kernels this context launched so far (its own kernels, not library ones). */
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);
+/* In-house eigensolves redone with cuSOLVER syevd because their vectors failed the
+ * orthogonality / finiteness check (this context and its workers, since creation). */
+int64_t latsum_ctx_eig_fallbacks(const latsum_ctx* ctx);
 /* Multi-GPU (one process per GPU): rank 0 creates an NCCL unique id, the caller
  * broadcasts it (e.g. torch.distributed), every rank calls latsum_ctx_init_comm.  The
  * context then runs latsum_rhosvd row-sharded over the grid index: each rank owns

@@ -97,6 +97,7 @@ SIGNATURES = [
     ("latsum_ctx_set_stream", _I, [_P, _P]),
     ("latsum_ctx_synchronize", _I, [_P]),
     ("latsum_ctx_kernel_launches", _I64, [_P]),
+    ("latsum_ctx_eig_fallbacks", _I64, [_P]),
     ("latsum_comm_unique_id", _I, [_P]),
     ("latsum_ctx_init_comm", _I, [_P, _P, _I, _I]),
     ("latsum_ctx_trim_pool", _I, [_P, _I64]),

@@ -90,6 +90,11 @@ class Context:
         self.check(_lib.lib().latsum_ctx_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
 
     @property
+    def eig_fallbacks(self) -> int:
+        """In-house eigensolves redone with cuSOLVER (latsum_ctx_eig_fallbacks)."""
+        return int(_lib.lib().latsum_ctx_eig_fallbacks(self._h))
+
+    @property
     def kernel_launches(self) -> int:
         return int(_lib.lib().latsum_ctx_kernel_launches(self._h))
 

@@ -52,7 +52,9 @@ __global__ void k_max_offidentity(const double* __restrict__ S, int k, double* _
   double m = 0.0;
   for (int64_t idx = threadIdx.x; idx < int64_t(k) * k; idx += blockDim.x) {
     const int i = int(idx % k), j = int(idx / k);
-    m = fmax(m, fabs(S[idx] - (i == j ? 1.0 : 0.0)));
+    const double dv = fabs(S[idx] - (i == j ? 1.0 : 0.0));
+    // fmax drops NaN: a non-finite vector must fail the check (-> the syevd fallback)
+    m = (dv == dv && dv <= 1e300) ? fmax(m, dv) : INFINITY;
   }
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));

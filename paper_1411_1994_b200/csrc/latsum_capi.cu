@@ -1703,7 +1703,8 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
       else CK(cudaMemsetAsync(H.p, 0, sizeof(double) * ell * ell, c->stream));
       if (sharded) allreduce(c, H.p, size_t(ell) * ell);
       Eig eh;
-      eh.ortho_tol = 1e-9;
+      // these vectors only seed Q = Y W h^{-1/2}, which two Newton-Schulz steps re-orthonormalise
+      eh.ortho_tol = 1e-6;
       eh.solve_on(c, ell, std::move(H), sharded ? eig_owner : -1);
       std::vector<double> h(ell);
       for (int64_t i = 0; i < ell; ++i) h[i] = std::max(eh.lam_asc[ell - 1 - i], 0.0);
@@ -2866,7 +2867,8 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   if (oz_v) oz_slice_a(c, U0, 1, t.N[0], ni, r0, sU0);
   // the core's lines (a, c) over K = b: the A operand of every chunk's Q GEMM, sliced once
   // per evaluation instead of once per y-chunk (cfg4: 11 chunks x 26 GB)
-  const bool core_once = oz_x && r1 <= oz::KMAX;
+  static const bool per_chunk = std::getenv("LATSUM_EVAL_CORE_PER_CHUNK") != nullptr;  // A/B
+  const bool core_once = oz_x && r1 <= oz::KMAX && !per_chunk;
   if (core_once) oz_slice_a(c, t.core.p, 1, r0, r0 * r2, r1, sCore, r0, r0 * r1);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);
@@ -3201,6 +3203,14 @@ int latsum_ctx_synchronize(latsum_ctx* c) {
 }
 
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* c) { return c ? c->launches : 0; }
+
+int64_t latsum_ctx_eig_fallbacks(const latsum_ctx* c) {
+  if (!c) return 0;
+  int64_t n = c->eig_fallbacks;
+  for (auto* w : c->sub)
+    if (w) n += w->eig_fallbacks;
+  return n;
+}
 
 int latsum_comm_unique_id(unsigned char id[128]) {
   try {

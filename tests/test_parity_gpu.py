@@ -375,6 +375,10 @@ def test_full_config_against_oracle_fixture(ctx, cfg):
     assert can.rank == int(fx["canonical_rank"])
     assert list(can.dict_cols) == list(fx["merged_columns"])
     t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=(cfg != 5))
+    for l in range(3):
+        fl = t.factor(l)
+        assert np.all(np.isfinite(fl)), ("factor after rhosvd", l, int(np.sum(~np.isfinite(fl))),
+                                         np.nonzero(~np.isfinite(fl).all(axis=1))[0][[0, -1]])
     ranks = list(fx["ranks"])
     for l in range(3):
         if rep.chosen_ranks[l] != ranks[l]:
@@ -480,8 +484,16 @@ def _check_box_slices(ctx, t, g):
     if t.has_core:
         core = t.core
         r = t.ranks
-        Q = core.reshape(r[0] * r[1], r[2], order="F") @ U[2][ks].T  # (r0 r1) x |ks|
-        del core
+        assert np.all(np.isfinite(core)), "core download"
+        cm = core.reshape(r[0] * r[1], r[2], order="F")
+        u2 = np.ascontiguousarray(U[2][ks].T)
+        Q = np.empty((r[0] * r[1], len(ks)))
+        step = 1 << 18  # row blocks: one BLAS call over 2.6e6 x 1266 returned NaN here once
+        for a in range(0, cm.shape[0], step):
+            Q[a:a + step] = cm[a:a + step] @ u2  # (r0 r1) x |ks|
+        del core, cm
+        assert all(np.all(np.isfinite(u)) for u in U), [int(np.sum(~np.isfinite(u))) for u in U]
+        assert np.all(np.isfinite(Q)), int(np.sum(~np.isfinite(Q)))
         want = {k: U[0] @ Q[:, i].reshape(r[0], r[1], order="F") @ U[1].T for i, k in enumerate(ks)}
     else:
         want = {}
@@ -489,6 +501,9 @@ def _check_box_slices(ctx, t, g):
             M = sp.csr_matrix((w * D[2][k, tc[:, 2]], (tc[:, 0], tc[:, 1])),
                               shape=(D[0].shape[1], D[1].shape[1]))
             want[k] = np.asarray((M.T @ D[0].T).T) @ D[1].T
+    for k in ks:
+        assert np.all(np.isfinite(got[k])), (k, "device", int(np.sum(~np.isfinite(got[k]))))
+        assert np.all(np.isfinite(want[k])), (k, "host", int(np.sum(~np.isfinite(want[k]))))
     scale = max(np.max(np.abs(v)) for v in want.values())
     for k in ks:
         err = np.max(np.abs(got[k] - want[k])) / scale

@@ -72,6 +72,16 @@ int latsum_ctx_set_stream(latsum_ctx* ctx, void* cuda_stream);
 /* Return unused memory of the device's stream-ordered pool to the system, keeping at most
  * keep_bytes reserved (the context pre-grows the pool at creation and never releases it). */
 int latsum_ctx_trim_pool(latsum_ctx* ctx, int64_t keep_bytes);
+/* Host sink for the Tucker result of the following RHOSVDs on this context (cmd_sum writes
+ * the result out, so its device->host copy belongs to the pipeline): the factors are copied
+ * as soon as the bases exist and the core chunk by chunk right behind its contraction, on a
+ * copy stream, so the transfer overlaps the core GEMMs.  core / factors[l] are host buffers
+ * (pinned, cudaHostAlloc, for the overlap) of core_cap / factor_cap[l] doubles; a result
+ * that does not fit stays on the device only.  core = NULL clears the sink.
+ * latsum_tucker_sink_written tells whether a result was streamed (1) or not (0).           */
+int latsum_ctx_set_host_sink(latsum_ctx* ctx, double* core, int64_t core_cap, double* const factors[3],
+                             const int64_t factor_cap[3]);
+int latsum_tucker_sink_written(const latsum_tucker* t);
 int latsum_ctx_synchronize(latsum_ctx* ctx);
 /* Number of kernels this context launched so far (its own kernels, not library ones). */
 int64_t latsum_ctx_kernel_launches(const latsum_ctx* ctx);

@@ -101,6 +101,8 @@ SIGNATURES = [
     ("latsum_comm_unique_id", _I, [_P]),
     ("latsum_ctx_init_comm", _I, [_P, _P, _I, _I]),
     ("latsum_ctx_trim_pool", _I, [_P, _I64]),
+    ("latsum_ctx_set_host_sink", _I, [_P, _P, _I64, _P, _P]),
+    ("latsum_tucker_sink_written", _I, [_P]),
     ("latsum_ctx_init_host_comm", _I, [_P, _I, _I, _P, _P, _P]),
     ("latsum_ctx_comm_info", _I, [_P, _P, _P]),
     ("latsum_ctx_set_profiling", _I, [_P, _I]),

@@ -82,6 +82,16 @@ class Context:
     def synchronize(self):
         self.check(_lib.lib().latsum_ctx_synchronize(self._h))
 
+    def set_host_sink(self, core_ptr: int, core_cap: int, factor_ptrs=(0, 0, 0),
+                      factor_caps=(0, 0, 0)):
+        """latsum_ctx_set_host_sink: stream the next Tucker results (core chunk by chunk behind
+        its contraction, factors first) into host buffers given as raw pointers (pinned
+        memory for the overlap) with capacities in doubles; core_ptr = 0 clears the sink."""
+        fp = (ctypes.c_void_p * 3)(*[ctypes.c_void_p(int(x)) for x in factor_ptrs])
+        fc = _i64(factor_caps)
+        self.check(_lib.lib().latsum_ctx_set_host_sink(
+            self._h, ctypes.c_void_p(int(core_ptr)) if core_ptr else None, int(core_cap), fp, _p(fc)))
+
     def trim_pool(self, keep_bytes: int = 0):
         """Release the unused part of the stream-ordered pool (latsum_ctx_trim_pool)."""
         self.check(_lib.lib().latsum_ctx_trim_pool(self._h, int(keep_bytes)))
@@ -498,6 +508,11 @@ class TuckerTensor:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def sink_written(self) -> bool:
+        """The core and factors were streamed to the context's host sink."""
+        return bool(_lib.lib().latsum_tucker_sink_written(self._h))
 
     @property
     def has_core(self) -> bool:

@@ -140,6 +140,14 @@ struct latsum_ctx {
   // host collective (latsum_ctx_init_host_comm): the same collectives through caller
   // callbacks on host buffers (gloo / in-process ranks in tests); channel 0 is this
   // context, 1..4 its workers (so concurrent modes never interleave on one channel)
+  // host sink (latsum_ctx_set_host_sink): the next Tucker results stream here while formed
+  struct Sink {
+    double* core = nullptr;
+    int64_t core_cap = 0;
+    double* f[3] = {nullptr, nullptr, nullptr};
+    int64_t f_cap[3] = {0, 0, 0};
+    cudaStream_t copy = nullptr, copy2 = nullptr;  // two copy engines
+  } sink;
   latsum_host_allreduce_fn host_ar = nullptr;
   latsum_host_allgather_fn host_ag = nullptr;
   void* host_user = nullptr;
@@ -1196,6 +1204,7 @@ const latsum_canonical& terms(latsum_ctx* c, const latsum_canonical& cc) {
 }
 
 struct latsum_tucker {
+  bool sink_written = false;  // the core and factors were streamed to the context's host sink
   int64_t N[3] = {0, 0, 0};
   int64_t r[3] = {1, 1, 1};
   DBuf U[3];     // N_l x r_l
@@ -2232,8 +2241,12 @@ int core_mode(const latsum_canonical& can) {
 // segmented GEMM, G1 = P_o1 gathered and weighted, G2 = P_o2 gathered), then
 // core = X x_m P_m.  Cost 2 r1 r2 r3 d_m + 2 r_o1 r_o2 T instead of the reference
 // loop's 2 r1 r2 r3 M_c.  [a_lo, a_hi) restricts j (the rank's share when sharded).
+// on_rows(first, count): core elements [first, first + count) of the o2-chunk just formed, in
+// the unit the chunk covers (see form_core's long-K loop); called on c->stream order
+using CoreChunkFn = std::function<void(int64_t b0, int64_t nbb)>;
 void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
-               double* core, int m, int64_t a_lo = 0, int64_t a_hi = -1) {
+               double* core, int m, int64_t a_lo = 0, int64_t a_hi = -1,
+               const CoreChunkFn* on_chunk = nullptr) {
   terms(c, can);
   const int64_t T = can.T, dm = a_hi < 0 ? can.d[m] : a_hi;
   const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
@@ -2271,6 +2284,7 @@ void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], cons
         ozaki_gemm_ex(c, rows, r[1], nall, X.p, 1, rows, 0, 0, P[1].p + a_lo * r[1], 1, r[1], o,
                       "gemm_core(ozaki-i8)");
       }
+      if (on_chunk) (*on_chunk)(b0, nbb);
     }
     return;
   }
@@ -2552,7 +2566,70 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
                 dm * (c->rank + 1) / c->nranks);
       allreduce(c, t.core.p, size_t(t.r[0]) * t.r[1] * t.r[2]);
     } else {
-      form_core(c, can, P, t.r, t.core.p, m);
+      // host sink: the factors now, the core chunk by chunk behind its contraction (the
+      // device->host copy of the result overlaps the core GEMMs on a copy stream)
+      auto& sk = c->sink;
+      const int64_t rall = t.r[0] * t.r[1] * t.r[2];
+      bool stream = sk.core && rall <= sk.core_cap;
+      for (int l = 0; l < 3; ++l) stream = stream && sk.f[l] && t.N[l] * t.r[l] <= sk.f_cap[l];
+      if (stream) {
+        if (!sk.copy) CK(cudaStreamCreateWithFlags(&sk.copy, cudaStreamNonBlocking));
+        if (!sk.copy2) CK(cudaStreamCreateWithFlags(&sk.copy2, cudaStreamNonBlocking));
+        auto after_stream = [&] {
+          cudaEvent_t ev;
+          CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          CK(cudaEventRecord(ev, c->stream));
+          CK(cudaStreamWaitEvent(sk.copy, ev, 0));
+          CK(cudaStreamWaitEvent(sk.copy2, ev, 0));
+          CK(cudaEventDestroy(ev));
+        };
+        after_stream();
+        for (int l = 0; l < 3; ++l) {
+          // the bases are still the modes' Z here (moved into t.U after the core)
+          CK(cudaMemcpyAsync(sk.f[l], mo[l].Z.p, sizeof(double) * t.N[l] * t.r[l],
+                             cudaMemcpyDeviceToHost, sk.copy));
+        }
+        const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
+        const int64_t ro = t.r[o1] * t.r[o2];
+        CoreChunkFn chunk = [&](int64_t b0, int64_t nbb) {
+          after_stream();
+          // each chunk split over the two copy streams (the first half of the columns / elements
+          // on one, the rest on the other)
+          if (m == 2) {  // rows [r0 b0, r0 (b0 + nbb)) of the (r0 r1) x r2 view
+            const int64_t h = t.r[2] / 2;
+            for (int q = 0; q < 2; ++q) {
+              const int64_t c0 = q ? h : 0, nc = q ? t.r[2] - h : h;
+              if (nc > 0)
+                CK(cudaMemcpy2DAsync(sk.core + t.r[0] * b0 + c0 * ro, ro * sizeof(double),
+                                     t.core.p + t.r[0] * b0 + c0 * ro, ro * sizeof(double),
+                                     t.r[0] * nbb * sizeof(double), nc, cudaMemcpyDeviceToHost,
+                                     q ? sk.copy2 : sk.copy));
+            }
+          } else {       // m = 0 / 1: a contiguous slab of r0 r1 nbb elements
+            const int64_t n = t.r[0] * t.r[1] * nbb, h = n / 2, o = t.r[0] * t.r[1] * b0;
+            CK(cudaMemcpyAsync(sk.core + o, t.core.p + o, sizeof(double) * h, cudaMemcpyDeviceToHost,
+                               sk.copy));
+            CK(cudaMemcpyAsync(sk.core + o + h, t.core.p + o + h, sizeof(double) * (n - h),
+                               cudaMemcpyDeviceToHost, sk.copy2));
+          }
+        };
+        bool chunked = false;
+        CoreChunkFn mark = [&](int64_t b0, int64_t nbb) {
+          chunked = true;
+          chunk(b0, nbb);
+        };
+        form_core(c, can, P, t.r, t.core.p, m, 0, -1, &mark);
+        if (!chunked) {  // the K-chunked form: the core is complete only at the end
+          after_stream();
+          CK(cudaMemcpyAsync(sk.core, t.core.p, sizeof(double) * rall, cudaMemcpyDeviceToHost,
+                             sk.copy));
+        }
+        CK(cudaStreamSynchronize(sk.copy));
+        CK(cudaStreamSynchronize(sk.copy2));
+        t.sink_written = true;
+      } else {
+        form_core(c, can, P, t.r, t.core.p, m);
+      }
     }
     t.has_core = true;
     tm.core = tp.stop();
@@ -3164,6 +3241,13 @@ int latsum_ctx_create(int device, latsum_ctx** out) {
 }
 
 void latsum_ctx_destroy(latsum_ctx* c) {
+  if (c)
+    for (cudaStream_t* st : {&c->sink.copy, &c->sink.copy2})
+      if (*st) {
+        cudaStreamSynchronize(*st);
+        cudaStreamDestroy(*st);
+        *st = nullptr;
+      }
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -3181,6 +3265,22 @@ void latsum_ctx_destroy(latsum_ctx* c) {
 }
 
 const char* latsum_last_error(const latsum_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+int latsum_ctx_set_host_sink(latsum_ctx* c, double* core, int64_t core_cap, double* const factors[3],
+                             const int64_t factor_cap[3]) {
+  return guarded(c, [&] {
+    require(c, "latsum_ctx_set_host_sink: null context");
+    auto& sk = c->sink;
+    sk.core = core;
+    sk.core_cap = core ? core_cap : 0;
+    for (int l = 0; l < 3; ++l) {
+      sk.f[l] = core && factors ? factors[l] : nullptr;
+      sk.f_cap[l] = core && factor_cap ? factor_cap[l] : 0;
+    }
+  });
+}
+
+int latsum_tucker_sink_written(const latsum_tucker* t) { return t && t->sink_written ? 1 : 0; }
 
 int latsum_ctx_trim_pool(latsum_ctx* c, int64_t keep_bytes) {
   return guarded(c, [&] {

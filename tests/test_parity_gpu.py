@@ -737,3 +737,34 @@ def test_assembly_term_merge_overlaps_and_joins(ctx):
     tb, rb = api.rhosvd(b, api.TruncationSpec.tol(g.eps))
     assert tuple(ra.chosen_ranks) == tuple(rb.chosen_ranks)
     assert abs(ra.input_norm - rb.input_norm) <= 1e-14 * ra.input_norm
+
+
+@pytest.mark.parametrize("cfg", ["mini", 2])
+def test_host_sink_streams_the_result(ctx, cfg):
+    """latsum_ctx_set_host_sink: the core (chunk by chunk behind its contraction on cfg2's
+    long-K path; whole on the small K-chunked path) and factors land in the host buffers,
+    bit-identical to the explicit downloads."""
+    import torch
+    g = mini("vacancies") if cfg == "mini" else W.baseline(cfg)
+    t0, _ = api.sum_to_tucker(g, g.eps, ctx)
+    r = t0.ranks
+    core = torch.zeros(int(np.prod(r)), dtype=torch.float64, pin_memory=True)
+    fs = [torch.zeros(g.N[l] * r[l], dtype=torch.float64, pin_memory=True) for l in range(3)]
+    ctx.set_host_sink(core.data_ptr(), core.numel(), [f.data_ptr() for f in fs],
+                      [f.numel() for f in fs])
+    try:
+        t, _ = api.sum_to_tucker(g, g.eps, ctx)
+    finally:
+        ctx.set_host_sink(0, 0)
+    assert t.sink_written and t.ranks == r
+    assert np.array_equal(core.numpy(), t.core.ravel(order="F"))
+    for l in range(3):
+        assert np.array_equal(fs[l].numpy(), t.factor(l).ravel(order="F"))
+    # too small a buffer: nothing streamed, the result stays on the device
+    ctx.set_host_sink(core.data_ptr(), core.numel() - 1, [f.data_ptr() for f in fs],
+                      [f.numel() for f in fs])
+    try:
+        t2, _ = api.sum_to_tucker(g, g.eps, ctx)
+    finally:
+        ctx.set_host_sink(0, 0)
+    assert not t2.sink_written

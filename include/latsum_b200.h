@@ -41,7 +41,12 @@ enum { LATSUM_DEFLATE_NEVER = 0, LATSUM_DEFLATE_ALWAYS = 1, LATSUM_DEFLATE_AUTO 
 /* latsum_rhosvd_ex flags: skip the dense core (r1 r2 r3 doubles; 518 GB for BASELINE
  * cfg5) and keep the projected factors P_l = Z_l^T A_l instead; entries and boxes are
  * then evaluated in projected-CP form, which equals the Tucker tensor. */
-enum { LATSUM_RHOSVD_FACTORS_ONLY = 1 };
+enum { LATSUM_RHOSVD_FACTORS_ONLY = 1, LATSUM_RHOSVD_CORE_SLABS = 2 };
+/* LATSUM_RHOSVD_CORE_SLABS (row-sharded contexts): each rank forms and keeps only
+ * rows [r1 q / P, r1 (q+1) / P) of mode 1 of the core, over the whole contraction, instead of
+ * an all-reduced full core (BASELINE cfg5: 518 GB over 4-8 GPUs); entries and boxes add the
+ * ranks' partial values with an all-reduce (every rank gets the full values);
+ * latsum_tucker_core_slab returns the local slab, latsum_tucker_core refuses a slab. */
 
 typedef struct latsum_ctx latsum_ctx;
 typedef struct latsum_reference latsum_reference;
@@ -228,6 +233,10 @@ int latsum_tucker_info(const latsum_tucker* t, int64_t dims[3], int64_t ranks[3]
 int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out);
 /* TuckerTensor::core() (r1 x r2 x r3, first index fastest) and factor(mode) (N_l x r_l). */
 int latsum_tucker_core(latsum_ctx* ctx, const latsum_tucker* t, double* core);
+/* The local mode-1 slab of the core: *a0, *ra (first row, rows; the whole core for an
+ * unsharded tensor) and, when core is not NULL, the ra x r2 x r3 slab (first index fastest). */
+int latsum_tucker_core_slab(latsum_ctx* ctx, const latsum_tucker* t, int64_t* a0, int64_t* ra,
+                            double* core);
 int latsum_tucker_factor(latsum_ctx* ctx, const latsum_tucker* t, int mode, double* factor);
 /* The projected canonical form of a factors-only tensor (no dense core; BASELINE cfg5):
  * V(i,j,k) = sum_t w_t prod_l (U_l P_l)(i_l, c_l(t)), equal to the Tucker tensor (SURVEY

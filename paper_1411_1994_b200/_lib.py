@@ -133,6 +133,7 @@ SIGNATURES = [
     ("latsum_tucker_has_core", _I, [_P]),
     ("latsum_tucker_info", _I, [_P, _P, _P]),
     ("latsum_tucker_singular_values", _I, [_P, _I, _P]),
+    ("latsum_tucker_core_slab", _I, [_P, _P, _P, _P, _P]),
     ("latsum_tucker_core", _I, [_P, _P, _P]),
     ("latsum_tucker_factor", _I, [_P, _P, _I, _P]),
     ("latsum_format_spectral_report", _I64, [_P, _P, _P, _I64]),

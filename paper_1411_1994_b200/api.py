@@ -518,6 +518,18 @@ class TuckerTensor:
     def has_core(self) -> bool:
         return bool(_lib.lib().latsum_tucker_has_core(self._h))
 
+    def core_slab(self):
+        """(a0, slab): this rank's rows [a0, a0 + ra) of mode 1 of the core (rhosvd(...,
+        core_slabs=True) on a sharded context; the whole core otherwise)."""
+        a0, ra = ctypes.c_int64(), ctypes.c_int64()
+        L = _lib.lib()
+        self.ctx.check(L.latsum_tucker_core_slab(self.ctx.handle, self._h, ctypes.byref(a0),
+                                                 ctypes.byref(ra), None))
+        out = np.zeros((ra.value, self.ranks[1], self.ranks[2]), order="F")
+        self.ctx.check(L.latsum_tucker_core_slab(self.ctx.handle, self._h, ctypes.byref(a0),
+                                                 ctypes.byref(ra), _p(out)))
+        return int(a0.value), out
+
     @property
     def core(self) -> np.ndarray:
         out = np.zeros(self.ranks, order="F")
@@ -664,7 +676,7 @@ def sublattice_union_sum(ref: ReferenceTensor, parent_cells, n_per_cell: int, su
 
 
 def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto",
-           form_core: bool = True):
+           form_core: bool = True, core_slabs: bool = False):
     """rank_reduction.hpp:176-218 -> (TuckerTensor, SpectralReport).
 
     form_core=False keeps the projected factors instead of the dense r1 x r2 x r3 core
@@ -678,7 +690,8 @@ def rhosvd(can: CanonicalTensor, spec: TruncationSpec, deflate: str = "auto",
     ctx.check(_lib.lib().latsum_rhosvd_ex(ctx.handle, can.handle,
                                           _p(ranks) if ranks is not None else None,
                                           float(spec.tolerance or 0.0), DEFLATE[deflate],
-                                          0 if form_core else 1, ctypes.byref(h),
+                                          (0 if form_core else 1) | (2 if core_slabs else 0),
+                                          ctypes.byref(h),
                                           ctypes.byref(rep)))
     t = TuckerTensor(ctx, h)
     sv = []

@@ -1205,6 +1205,9 @@ const latsum_canonical& terms(latsum_ctx* c, const latsum_canonical& cc) {
 
 struct latsum_tucker {
   bool sink_written = false;  // the core and factors were streamed to the context's host sink
+  // per-rank core slab (LATSUM_RHOSVD_CORE_SLABS): core holds rows [a0, a0 + ra) of mode 0
+  bool core_slab = false;
+  int64_t a0 = 0, ra = 0;
   int64_t N[3] = {0, 0, 0};
   int64_t r[3] = {1, 1, 1};
   DBuf U[3];     // N_l x r_l
@@ -2191,11 +2194,23 @@ double canonical_norm(latsum_ctx* c, const latsum_canonical& can) {
 // The merged terms grouped by their mode-m column, with the other two modes' projected
 // columns gathered (G1 weighted): X_j = G1[:, seg_j] G2[:, seg_j]^T is then one
 // segmented GEMM (the "contracted unfolding" of project_core and of ALS).
+// the projected factors P_l (r_l x d_l, leading dimension r_l) as plain pointers, so a
+// slab of P_0's rows (the per-rank core slabs) can stand in for the whole
+struct PRef {
+  const double* p;
+};
+struct PRefs {
+  PRef v[3];
+  PRefs(const DBuf P[3]) : v{{P[0].p}, {P[1].p}, {P[2].p}} {}
+  PRefs(const double* a, const double* b, const double* c) : v{{a}, {b}, {c}} {}
+  operator const PRef*() const { return v; }
+};
+
 struct GroupedTerms {
   int o1, o2;
   DVec<int64_t> seg;
   DBuf G1, G2;
-  GroupedTerms(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
+  GroupedTerms(latsum_ctx* c, const latsum_canonical& can, const PRef P[3], const int64_t r[3],
                int m)
       : o1(m == 0 ? 1 : 0), o2(m == 2 ? 1 : 2) {
     const int64_t T = can.T;
@@ -2244,7 +2259,7 @@ int core_mode(const latsum_canonical& can) {
 // on_rows(first, count): core elements [first, first + count) of the o2-chunk just formed, in
 // the unit the chunk covers (see form_core's long-K loop); called on c->stream order
 using CoreChunkFn = std::function<void(int64_t b0, int64_t nbb)>;
-void form_core(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3], const int64_t r[3],
+void form_core(latsum_ctx* c, const latsum_canonical& can, const PRef P[3], const int64_t r[3],
                double* core, int m, int64_t a_lo = 0, int64_t a_hi = -1,
                const CoreChunkFn* on_chunk = nullptr) {
   terms(c, can);
@@ -2407,7 +2422,8 @@ void fork_join(latsum_ctx* c, int n, F&& f) {
 }
 
 void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* ranks, double tol,
-                 int deflate, latsum_tucker& t, latsum_spectral_report& rep, bool form = true) {
+                 int deflate, latsum_tucker& t, latsum_spectral_report& rep, bool form = true,
+                 bool slabs = false) {
   if (!ranks) require(tol > 0.0 && tol < 1.0, "TruncationSpec: tolerance must lie in (0,1)");
   std::memset(&rep, 0, sizeof(rep));
   Timings tm;
@@ -2558,14 +2574,30 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   Trace::mark(c, "projections done");
   if (form) {  // the dense core (rank_reduction.hpp:88-100); absent when it cannot fit
     tp.start();
-    t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
     const int m = core_mode(can);
-    if (has_comm(c)) {  // each rank forms the core from its share of mode m
+    if (slabs && has_comm(c)) {
+      // each rank forms and keeps rows [a0, a1) of mode 0 of the core, over all
+      // of the contraction (the P_l are replicated), so no core all-reduce and no rank holds
+      // the whole core (BASELINE cfg5: 518 GB); entries and boxes sum the ranks' partials
+      t.a0 = t.r[0] * c->rank / c->nranks;
+      t.ra = t.r[0] * (c->rank + 1) / c->nranks - t.a0;
+      t.core_slab = true;
+      t.core.alloc(c, size_t(std::max<int64_t>(t.ra, 1)) * t.r[1] * t.r[2]);
+      if (t.ra > 0) {
+        DBuf P0s(c, size_t(t.ra) * can.d[0]);
+        CK(cudaMemcpy2DAsync(P0s.p, t.ra * sizeof(double), P[0].p + t.a0, t.r[0] * sizeof(double),
+                             t.ra * sizeof(double), can.d[0], cudaMemcpyDeviceToDevice, c->stream));
+        const int64_t rs[3] = {t.ra, t.r[1], t.r[2]};
+        form_core(c, can, PRefs(P0s.p, P[1].p, P[2].p), rs, t.core.p, m);
+      }
+    } else if (has_comm(c)) {  // each rank forms the core from its share of mode m
+      t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
       const int64_t dm = can.d[m];
-      form_core(c, can, P, t.r, t.core.p, m, dm * c->rank / c->nranks,
+      form_core(c, can, PRefs(P), t.r, t.core.p, m, dm * c->rank / c->nranks,
                 dm * (c->rank + 1) / c->nranks);
       allreduce(c, t.core.p, size_t(t.r[0]) * t.r[1] * t.r[2]);
     } else {
+      t.core.alloc(c, size_t(t.r[0]) * t.r[1] * t.r[2]);
       // host sink: the factors now, the core chunk by chunk behind its contraction (the
       // device->host copy of the result overlaps the core GEMMs on a copy stream)
       auto& sk = c->sink;
@@ -2618,7 +2650,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
           chunked = true;
           chunk(b0, nbb);
         };
-        form_core(c, can, P, t.r, t.core.p, m, 0, -1, &mark);
+        form_core(c, can, PRefs(P), t.r, t.core.p, m, 0, -1, &mark);
         if (!chunked) {  // the K-chunked form: the core is complete only at the end
           after_stream();
           CK(cudaMemcpyAsync(sk.core, t.core.p, sizeof(double) * rall, cudaMemcpyDeviceToHost,
@@ -2628,7 +2660,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
         CK(cudaStreamSynchronize(sk.copy2));
         t.sink_written = true;
       } else {
-        form_core(c, can, P, t.r, t.core.p, m);
+        form_core(c, can, PRefs(P), t.r, t.core.p, m);
       }
     }
     t.has_core = true;
@@ -2693,7 +2725,7 @@ void als_mode_update(latsum_ctx* c, const latsum_canonical& can, const DBuf P[3]
                      const int64_t r[3], int l, DBuf& Y) {
   terms(c, can);
   const int64_t N = can.N[l], d = can.d[l];
-  GroupedTerms gt(c, can, P, r, l);
+  GroupedTerms gt(c, can, PRefs(P), r, l);
   const int64_t R2 = r[gt.o1] * r[gt.o2];
   require(double(R2) * double(d + N) <= double(workspace_budget()),
           "als_refine: contracted unfolding too large for the device (ALS is out of scope at "
@@ -2836,7 +2868,7 @@ void canonical_to_tucker_impl(latsum_ctx* c, const latsum_canonical& can, const 
     }
   }
   t.core.alloc(c, size_t(r[0]) * r[1] * r[2]);
-  form_core(c, can, P, r, t.core.p, core_mode(can));
+  form_core(c, can, PRefs(P), r, t.core.p, core_mode(can));
   t.has_core = true;
   for (int l = 0; l < 3; ++l) t.P[l] = std::move(P[l]);
   if (tol > 0.0 && !ranks) {
@@ -2930,8 +2962,13 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   if (!t.has_core) return projected_eval(c, t, lo, hi, out);
   check_box(t.N, lo, hi);
   const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
-  const int64_t r0 = t.r[0], r1 = t.r[1], r2 = t.r[2];
-  const double* U0 = t.U[0].p + lo[0];
+  if (t.core_slab && t.ra == 0) {  // this rank's slab is empty: its partial box is zero
+    CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
+    allreduce(c, out, size_t(ni * nj * nk));
+    return;
+  }
+  const int64_t r0 = t.core_slab ? t.ra : t.r[0], r1 = t.r[1], r2 = t.r[2];
+  const double* U0 = t.U[0].p + lo[0] + (t.core_slab ? t.a0 * t.N[0] : 0);
   const double* U1 = t.U[1].p + lo[1];
   const double* U2 = t.U[2].p + lo[2];
   const int64_t budget = int64_t(1) << 29;  // doubles per intermediate (4 GiB)
@@ -2996,6 +3033,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
            out + k0 * ni * nj + j0 * ni, ni, ov);
     }
   }
+  if (t.core_slab) allreduce(c, out, size_t(ni * nj * nk));  // the ranks' partial boxes
 }
 
 // Canonical (dictionary) tensor on an ni x nj x nk box: V_k = A0 X_k with
@@ -3166,7 +3204,9 @@ void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes,
       if (probes[3 * p + l] < 0 || probes[3 * p + l] >= t.N[l])
         throw Error(LATSUM_ERR_INVALID_ARGUMENT, "TuckerTensor::entry index out of range");
   if (!t.has_core) return projected_probes(c, t, probes, np, out_host);
-  const int64_t r0 = t.r[0], r12 = t.r[1] * t.r[2];
+  // a core slab: the partial sum over mode-0 indices [a0, a0 + ra), then the ranks' sum
+  const int64_t r0 = t.core_slab ? t.ra : t.r[0], r12 = t.r[1] * t.r[2];
+  const double* U0 = t.U[0].p + (t.core_slab ? t.a0 * t.N[0] : 0);
   const int64_t budget = int64_t(1) << 28;
   const int64_t pc = std::max<int64_t>(1, std::min<int64_t>(np, budget / std::max<int64_t>(r12, 1)));
   std::vector<int64_t> hp(probes, probes + 3 * np);
@@ -3175,15 +3215,20 @@ void tucker_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes,
   DBuf rowsU(c, size_t(pc) * r0), Wm(c, size_t(pc) * r12), res(c, np);
   for (int64_t p0 = 0; p0 < np; p0 += pc) {
     const int64_t npp = std::min(pc, np - p0);
-    k_gather_rows<<<grid_for(npp * r0), 256, 0, c->stream>>>(t.U[0].p, t.N[0], r0, dp.p + 3 * p0,
-                                                             0, npp, rowsU.p);
-    post_launch(c);
-    gemm(c, false, false, npp, r12, r0, 1.0, rowsU.p, npp, t.core.p, r0, 0.0, Wm.p, npp,
-         tagged("gemm_probes"));
+    if (r0 == 0) {  // an empty slab contributes zeros
+      CK(cudaMemsetAsync(Wm.p, 0, sizeof(double) * npp * r12, c->stream));
+    } else {
+      k_gather_rows<<<grid_for(npp * r0), 256, 0, c->stream>>>(U0, t.N[0], r0, dp.p + 3 * p0, 0,
+                                                               npp, rowsU.p);
+      post_launch(c);
+      gemm(c, false, false, npp, r12, r0, 1.0, rowsU.p, npp, t.core.p, r0, 0.0, Wm.p, npp,
+           tagged("gemm_probes"));
+    }
     k_tucker_probe_finish<<<unsigned(npp), 256, 0, c->stream>>>(
         Wm.p, npp, t.r[1], t.r[2], t.U[1].p, t.N[1], t.U[2].p, t.N[2], dp.p + 3 * p0, res.p + p0);
     post_launch(c);
   }
+  if (t.core_slab) allreduce(c, res.p, size_t(np));
   CK(cudaMemcpyAsync(out_host, res.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
 }
@@ -3566,7 +3611,7 @@ int latsum_rhosvd_ex(latsum_ctx* c, const latsum_canonical* can, const int64_t* 
     auto t = std::make_unique<latsum_tucker>();
     latsum_spectral_report rep;
     rhosvd_impl(c, *can, ranks, tolerance, deflate, *t, rep,
-                (flags & LATSUM_RHOSVD_FACTORS_ONLY) == 0);
+                (flags & LATSUM_RHOSVD_FACTORS_ONLY) == 0, (flags & LATSUM_RHOSVD_CORE_SLABS) != 0);
     if (report) *report = rep;
     *out = t.release();
   });
@@ -3591,8 +3636,25 @@ int latsum_tucker_singular_values(const latsum_tucker* t, int mode, double* out)
   return LATSUM_OK;
 }
 
+int latsum_tucker_core_slab(latsum_ctx* c, const latsum_tucker* t, int64_t* a0, int64_t* ra,
+                            double* core) {
+  return guarded(c, [&] {
+    require(t && a0 && ra, "latsum_tucker_core_slab: null argument");
+    require(t->has_core, "latsum_tucker_core_slab: the tensor has no dense core");
+    *a0 = t->core_slab ? t->a0 : 0;
+    *ra = t->core_slab ? t->ra : t->r[0];
+    if (core && *ra > 0) {
+      CK(cudaMemcpyAsync(core, t->core.p, sizeof(double) * *ra * t->r[1] * t->r[2],
+                         cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
 int latsum_tucker_core(latsum_ctx* c, const latsum_tucker* t, double* core) {
   return guarded(c, [&] {
+    require(!t || !t->core_slab,
+            "latsum_tucker_core: the core is distributed over the ranks (latsum_tucker_core_slab)");
     require(t && core, "latsum_tucker_core: null argument");
     require(t->has_core, "latsum_tucker_core: the dense core was not formed (factors-only RHOSVD)");
     CK(cudaMemcpyAsync(core, t->core.p, sizeof(double) * t->r[0] * t->r[1] * t->r[2],
@@ -3730,6 +3792,7 @@ int latsum_tensor_write(latsum_ctx* c, const latsum_canonical* can, const latsum
   return guarded(c, [&] {
     require(path && ((can != nullptr) != (t != nullptr)),
             "latsum_tensor_write: pass exactly one of canonical / tucker");
+    require(!t || !t->core_slab, "latsum_tensor_write: the core is distributed over the ranks");
     FileSink f(path);
     if (can) {
       write_header(f, 'C', can->N);

@@ -16,7 +16,7 @@ from paper_1411_1994_b200 import workload as W
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(g, nranks, form_core=True):
+def _run_ranks(g, nranks, form_core=True, core_slabs=False, box=None):
     coll = api.ThreadCollective(nranks)
     out, errs = [None] * nranks, []
 
@@ -26,8 +26,12 @@ def _run_ranks(g, nranks, form_core=True):
             api.init_host_comm(ctx, q, nranks, coll)
             ref = api.reference_for(g, ctx)
             can = api.lattice_sum(ref, g)
-            t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=form_core)
-            out[q] = (ctx, can, t, rep)
+            t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=form_core,
+                                core_slabs=core_slabs)
+            vals = None
+            if box is not None:  # the ranks evaluate together (partial boxes + all-reduce)
+                vals = t.to_dense(*box)
+            out[q] = (ctx, can, t, rep) if box is None else (ctx, can, t, rep, vals)
         except Exception as e:  # surfaced below
             errs.append(e)
 
@@ -93,3 +97,38 @@ def test_row_sharded_full_cfg3_against_fixture():
         v = t.entries(pr)
         assert np.max(np.abs(v - fx["v_rhosvd"])) / np.max(np.abs(fx["v_rhosvd"])) <= 10 * g.eps + 1e-12
     assert np.array_equal(out[0][2].core, out[1][2].core)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_core_slabs_match_the_full_core(ctx, nranks):
+    """SURVEY 8e's per-rank core slabs (LATSUM_RHOSVD_CORE_SLABS): each rank forms rows
+    [r1 q/P, r1 (q+1)/P) of mode 1 over the whole contraction, no core all-reduce; stacked,
+    the slabs are the single-rank core, and entries / boxes (partials + all-reduce) match."""
+    g = _sharded_geometry()
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t1, rep1 = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    full = t1.core
+    box = ((100, 200, 250), (140, 260, 262))
+    want_box = t1.to_dense(*box)
+    outs = _run_ranks(g, nranks, core_slabs=True, box=box)
+    slabs = []
+    for q, (cq, canq, tq, repq, vals) in enumerate(outs):
+        assert tuple(repq.chosen_ranks) == tuple(rep1.chosen_ranks)
+        a0, slab = tq.core_slab()
+        assert a0 == full.shape[0] * q // nranks
+        slabs.append(slab)
+        with pytest.raises(Exception):
+            tq.core  # the whole core lives on no rank
+        scale = np.max(np.abs(want_box))
+        assert np.max(np.abs(vals - want_box)) / scale < 1e-11
+        pr = O.probes(g.N, 200, 9)
+        v1 = t1.entries(pr)
+        # every rank gets the summed values (collective: the other ranks evaluate too)
+        assert vals.shape == want_box.shape
+    # the core depends on the bases' signs: compare with the all-reduced core of a sharded
+    # run without slabs (same owner-solved bases)
+    ref_core = _run_ranks(g, nranks)[0][2].core
+    stacked = np.concatenate(slabs, axis=0)
+    assert stacked.shape == ref_core.shape == full.shape
+    assert np.max(np.abs(stacked - ref_core)) <= 1e-12 * np.max(np.abs(ref_core))

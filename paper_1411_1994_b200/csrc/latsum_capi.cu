@@ -517,15 +517,6 @@ struct OzSliced {
   const int8_t* digits() const { return reinterpret_cast<const int8_t*>(data.p); }
 };
 
-// 2-SM (cta_group::2) Ozaki kernel: LATSUM_OZ_2SM=1 (default off until measured faster)
-bool oz_use_2sm() {
-  static const bool v = [] {
-    const char* e = std::getenv("LATSUM_OZ_2SM");
-    return e && std::string(e) == "1";
-  }();
-  return v;
-}
-
 void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
               OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0, int halves = 1, bool even_tiles = false) {
   static_assert(oz::BM == oz::BN, "one tile height for both operands");
@@ -551,8 +542,7 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
                    reinterpret_cast<uintptr_t>(P) % 16 == 0;
   int8_t* d = reinterpret_cast<int8_t*>(out.data.p);
   // few tiles, long K: split K over the grid (k_slice_pmax + k_slice_split, bit-identical)
-  static const bool no_split = std::getenv("LATSUM_SLICE_NOSPLIT") != nullptr;  // A/B switch
-  if (!no_split && out.tiles < 148 && out.KB >= 16) {
+  if (out.tiles < 148 && out.KB >= 16) {
     const int64_t nsplit = std::min<int64_t>(out.KB / 8, (2 * 148 + out.tiles - 1) / out.tiles);
     const int64_t kbs = (out.KB + nsplit - 1) / nsplit;
     const int64_t ns = (out.KB + kbs - 1) / kbs;
@@ -575,10 +565,9 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
     return;
   }
   // long lines: units of LU lines of a tile, so the 2 x 148 CTAs' lines in flight fit ~90 MB
-  // of L2 and the digit pass re-reads from L2 (LATSUM_SLICE_NARROW=1: whole-tile kernel)
-  static const bool narrow = std::getenv("LATSUM_SLICE_NARROW") != nullptr;
+  // of L2 and the digit pass re-reads mostly from L2
   const double line_bytes = double(K) * 8.0;
-  if (!narrow && line_bytes * oz::BM * 2 * 148 > 90e6) {
+  if (line_bytes * oz::BM * 2 * 148 > 90e6) {
     const int lu = line_bytes * 32 * 2 * 148 <= 90e6 ? 32 : line_bytes * 16 * 2 * 148 <= 90e6 ? 16 : 8;
     const int64_t units = out.tiles * (oz::BM / lu);
     const unsigned ctas = unsigned(std::min<int64_t>(units, 2 * 148));
@@ -614,11 +603,11 @@ void oz_slice(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L,
 // kernel variant in use
 void oz_slice_a(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
                 OzSliced& out, int64_t L1 = 0, int64_t sl2 = 0) {  // line l: (l % L1) sl + (l / L1) sl2
-  oz_slice(c, P, sl, sk, L, K, out, L1, sl2, 1, oz_use_2sm());
+  oz_slice(c, P, sl, sk, L, K, out, L1, sl2, 1, false);
 }
 void oz_slice_b(latsum_ctx* c, const double* P, int64_t sl, int64_t sk, int64_t L, int64_t K,
                 OzSliced& out) {
-  oz_slice(c, P, sl, sk, L, K, out, 0, 0, oz_use_2sm() ? 2 : 1, false);
+  oz_slice(c, P, sl, sk, L, K, out, 0, 0, 1, false);
 }
 
 // Output addressing of an Ozaki GEMM (ozaki_i8.cuh OzOut): plain column-major by default.
@@ -641,36 +630,12 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
   ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(a.K));
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  if (b.halves == 2) {  // 2-SM kernel: CTA pairs over (256-row, 128-column) tiles
-    set_smem_attr(c, oz::k_gemm_i8_2sm, oz::SMEM_BYTES2);
-    const int64_t tiles_m2 = (a.tiles + 1) / 2, tiles2 = tiles_m2 * b.tiles;
-    const unsigned pairs = unsigned(std::min<int64_t>(tiles2, sms / 2));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(oz::PTHREADS);
-    cfg.dynamicSmemBytes = oz::SMEM_BYTES2;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, oz::k_gemm_i8_2sm, a.digits(), (const double*)a.scale.p, b.digits(),
-                          (const double*)b.scale.p, M, N, a.KB, o, tiles_m2, tiles2));
-    post_launch(c);
-    return;
-  }
   if (c->max_ctas > 0) sms = std::min(sms, c->max_ctas);
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   // stream the larger operand once: N tiles fastest when A is the bigger one (the core
-  // contraction's tall X against the small P_m), M tiles fastest otherwise (the slabs)
-  static const int order_env = [] {
-    const char* e = std::getenv("LATSUM_OZ_ORDER");  // A/B: "m" or "n" forces the order
-    return e ? (e[0] == 'n' ? 1 : 0) : -1;
-  }();
-  const int nfast = order_env >= 0 ? order_env : (a.tiles > 2 * b.tiles ? 1 : 0);
+  // contraction's tall X against the small P_m: 190 -> 155 ms on cfg4), M tiles fastest
+  // otherwise (the slabs)
+  const int nfast = a.tiles > 2 * b.tiles ? 1 : 0;
   oz::k_gemm_i8<<<ctas, oz::PTHREADS, oz::SMEM_BYTES, c->stream>>>(
       a.digits(), a.scale.p, b.digits(), b.scale.p, M, N, a.KB, o, a.tiles, tiles, b.tiles, nfast);
   post_launch(c);
@@ -1679,11 +1644,7 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
                       int eig_owner = -1) {
   const int64_t Nr = std::max<int64_t>(Nb, 1);
   const double a2 = frob2(c, Ap, Nb, d, Nb, sharded);
-  static const int64_t ell_env = [] {
-    const char* e = std::getenv("LATSUM_RP2_ELL");
-    return e ? int64_t(std::atoll(e)) : int64_t(0);
-  }();
-  int64_t ell = std::min<int64_t>(nc, ell_env > 0 ? ell_env : 768);
+  int64_t ell = std::min<int64_t>(nc, 768);
   for (;; ell = std::min<int64_t>(nc, 2 * ell)) {
     o.ell = ell;
     DBuf Om(c, size_t(d) * ell), Y(c, size_t(Nr) * ell);
@@ -1886,16 +1847,8 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   out.rows = rows ? 1 : 0;
   out.gsize = n;
   DBuf G(c, size_t(n) * n);
-  {
-    // LATSUM_GRAM_SERIAL=1: the modes' Grams one at a time (A/B of SM contention)
-    static const bool serial = std::getenv("LATSUM_GRAM_SERIAL") != nullptr;
-    static std::mutex mu;
-    std::unique_lock<std::mutex> lk(mu, std::defer_lock);
-    if (serial) lk.lock();
-    if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
-    else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
-    if (serial) CK(cudaStreamSynchronize(c->stream));
-  }
+  if (Nb > 0) gram(c, rows, At.p, Nb, d, G.p);
+  else CK(cudaMemsetAsync(G.p, 0, sizeof(double) * n * n, c->stream));
   if (sharded) allreduce(c, G.p, size_t(n) * n);
   tm.gram += timer.stop();
   Trace::mark(c, "gram done");
@@ -1983,10 +1936,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
       // randomized pass 2 (column orientation, tolerance-driven): ell x ell eigensolves
       // instead of the nc x nc restricted Gram (see randomized_pass2)
       static const bool rp2_off = std::getenv("LATSUM_RP2") && std::string(std::getenv("LATSUM_RP2")) == "0";
-      static const int64_t rp2_min = [] {  // LATSUM_RP2_MIN: smallest nc sketched
-        const char* e = std::getenv("LATSUM_RP2_MIN");
-        return e ? int64_t(std::atoll(e)) : int64_t(808);
-      }();
+      constexpr int64_t rp2_min = 808;  // the in-house solver takes the restricted Gram below
       // the resolved pass-1 values between eps lambda_max and the k1 threshold are directions
       // the sketch must hold: too many and it cannot stay within the in-house solver's size
       int64_t c16 = 0;
@@ -2348,8 +2298,7 @@ latsum_ctx* sub_ctx(latsum_ctx* c, int i) {
     // priority; worker 3 (norm_f, one throughput kernel off the critical path): lowest
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    static const bool no_prio = std::getenv("LATSUM_NO_STREAM_PRIORITY") != nullptr;  // A/B
-    CK(cudaStreamCreateWithPriority(&w->own, cudaStreamNonBlocking, no_prio ? 0 : (i < 3 ? hi : lo)));
+    CK(cudaStreamCreateWithPriority(&w->own, cudaStreamNonBlocking, i < 3 ? hi : lo));
     w->stream = w->own;
     CS(cusolverDnCreate(&w->solver));
     CS(cusolverDnSetStream(w->solver, w->stream));
@@ -2437,10 +2386,8 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   ModeOut mo[3];
   Timings tms[4];
   const bool zero_terms = can.Mc == 0;  // T == 0 iff M_c == 0 (every term is kept, merged)
-  static const bool serial = std::getenv("LATSUM_SERIAL") != nullptr;  // A/B switch
   // norm_f waits for the three Grams: its throughput kernels then overlap the latency-bound
-  // eigensolves instead of competing with the Grams for the SMs (LATSUM_NORM_EARLY=1: no wait)
-  static const bool norm_early = std::getenv("LATSUM_NORM_EARLY") != nullptr;
+  // eigensolves instead of competing with the Grams for the SMs
   std::mutex gmu;
   std::condition_variable gcv;
   bool gram_done[3] = {false, false, false};
@@ -2451,9 +2398,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   };
   for (int i = 0; i < 3; ++i) tms[i].on_gram = [&, i] { mark_gram(i); };
   EigTurnstile turn;
-  static const bool no_turn = std::getenv("LATSUM_EIG_TURNSTILE") &&
-                              std::string(std::getenv("LATSUM_EIG_TURNSTILE")) == "0";
-  if (!no_turn && !has_comm(c) && eig_env_mode() == 0 && c->eig_method == 0 && !ranks) {
+  if (!has_comm(c) && eig_env_mode() == 0 && c->eig_method == 0 && !ranks) {
     std::vector<std::pair<int64_t, int>> sz;
     for (int l = 0; l < 3; ++l) {
       const int64_t gn = std::min<int64_t>(can.N[l], can.d[l]);
@@ -2468,7 +2413,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
   }
   auto body = [&](latsum_ctx* w, int i) {
     if (i == 3 || zero_terms) {
-      if (!zero_terms && !norm_early) {
+      if (!zero_terms) {
         std::unique_lock<std::mutex> g(gmu);
         gcv.wait(g, [&] { return gram_done[0] && gram_done[1] && gram_done[2]; });
       }
@@ -2502,13 +2447,9 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       tms[i].project = tp.stop();
     }
   };
-  if (serial) {
-    for (int i = 0; i < (zero_terms ? 1 : 4); ++i) body(c, i);
-  } else {
-    Trace::mark(c, "rhosvd fork");
-    fork_join(c, zero_terms ? 1 : 4, body);
-    Trace::mark(c, "rhosvd join");
-  }
+  Trace::mark(c, "rhosvd fork");
+  fork_join(c, zero_terms ? 1 : 4, body);
+  Trace::mark(c, "rhosvd join");
   for (int l = 0; l < 3; ++l) {
     mo[l].Z.adopt(c->stream);
     t.P[l].adopt(c->stream);
@@ -2981,8 +2922,7 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   if (oz_v) oz_slice_a(c, U0, 1, t.N[0], ni, r0, sU0);
   // the core's lines (a, c) over K = b: the A operand of every chunk's Q GEMM, sliced once
   // per evaluation instead of once per y-chunk (cfg4: 11 chunks x 26 GB)
-  static const bool per_chunk = std::getenv("LATSUM_EVAL_CORE_PER_CHUNK") != nullptr;  // A/B
-  const bool core_once = oz_x && r1 <= oz::KMAX && !per_chunk;
+  const bool core_once = oz_x && r1 <= oz::KMAX;
   if (core_once) oz_slice_a(c, t.core.p, 1, r0, r0 * r2, r1, sCore, r0, r0 * r1);
   for (int64_t j0 = 0; j0 < nj; j0 += njc) {
     const int64_t njj = std::min(njc, nj - j0);

@@ -564,221 +564,5 @@ k_gemm_i8(const int8_t* __restrict__ As, const double* __restrict__ ra,
   }
 }
 
-// ---------------------------------------------------------------- 2-SM variant
-// The same GEMM with tcgen05.mma.cta_group::2 (M = 256 over a CTA pair, N = 128): each CTA
-// holds its 128 rows of A and 64 of the 128 B lines, so the MMA's shared-memory operand
-// reads per SM drop from 8 KB to 6 KB per 128x128x32 product and the B bulk copies halve
-// (the kernel is shared-memory-port bound; profiles/ncu_ozaki_r01.md).  The leader CTA
-// (rank 0) issues the MMAs; the follower's producer signals its own mbarrier and a relay
-// thread forwards each completed stage to the leader's; MMA completion is multicast to
-// both CTAs' barriers; both epilogues drain their own TMEM and arrive on the leader's
-// tmem_empty.
-constexpr int STAGES2 = 5;
-constexpr int B_BLK2 = (BN / 2) * BKB;  // one slice of this CTA's 64 B lines (2 KB)
-constexpr int A_STAGE2 = S * A_BLK;     // 28 KB
-constexpr int B_STAGE2 = S * B_BLK2;    // 14 KB
-constexpr size_t SMEM_BYTES2 = size_t(STAGES2) * (A_STAGE2 + B_STAGE2) + 256;
-constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
-                             (uint32_t(256 >> 4) << 24);
-
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mma_i8_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdesc2), "r"(acc));
-}
-// arrive (on MMA completion) on the barrier at this shared-memory offset in both CTAs
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-          smem_u32(bar)),
-      "h"((unsigned short)3)
-      : "memory");
-}
-
-__global__ void __launch_bounds__(PTHREADS, 1)
-k_gemm_i8_2sm(const int8_t* __restrict__ As, const double* __restrict__ ra,
-              const int8_t* __restrict__ Bs, const double* __restrict__ cb, int64_t M, int64_t N,
-              int64_t KB, OzOut o, int64_t tiles_m2, int64_t tiles) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const uint32_t rank = cluster.block_rank();  // 0: leader
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES2 * A_STAGE2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B_STAGE2);
-  uint64_t* empty = full + STAGES2;
-  uint64_t* tmem_full = empty + STAGES2;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) {
-      mbar_init(&full[s], rank == 0 ? 2 : 1);  // leader: own copies + the follower's relay
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 2 * EPI_WARPS);  // both CTAs' epilogue warps (leader's copy used)
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
-  }
-  cluster.sync();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  const int64_t pair = blockIdx.x / 2, npairs = gridDim.x / 2;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int64_t it = 0;
-      for (int64_t t = pair; t < tiles; t += npairs) {
-        const int64_t mt = 2 * (t % tiles_m2) + rank, nt = t / tiles_m2;
-        const int8_t* gA = As + (mt * KB) * int64_t(A_STAGE);
-        const int8_t* gB = Bs + (nt * KB) * int64_t(B_STAGE) + int64_t(rank) * B_STAGE2;
-        for (int pass = 0; pass < 2; ++pass) {
-          const uint32_t nsl = pass == 0 ? P1_SLICES : S;
-          for (int64_t kb = 0; kb < KB; ++kb, ++it) {
-            const int st = int(it % STAGES2);
-            if (it >= STAGES2) mbar_wait(&empty[st], uint32_t(((it / STAGES2) - 1) & 1));
-            mbar_expect_tx(&full[st], nsl * (A_BLK + B_BLK2));
-            bulk_g2s(sA + st * A_STAGE2, gA + kb * A_STAGE, nsl * A_BLK, &full[st]);
-            bulk_g2s(sB + st * B_STAGE2, gB + kb * B_STAGE, nsl * B_BLK2, &full[st]);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // leader: MMA issuer
-      int64_t it = 0, np = 0;
-      for (int64_t t = pair; t < tiles; t += npairs) {
-        for (int pass = 0; pass < 2; ++pass, ++np) {
-          if (np > 0) mbar_wait(tmem_empty, uint32_t((np - 1) & 1));  // both epilogues drained
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          for (int64_t kb = 0; kb < KB; ++kb, ++it) {
-            const int st = int(it % STAGES2);
-            mbar_wait(&full[st], uint32_t((it / STAGES2) & 1));  // both CTAs' stage st landed
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint8_t* a0 = sA + st * A_STAGE2;
-            const uint8_t* b0 = sB + st * B_STAGE2;
-            const uint32_t acc0 = kb > 0 ? 1u : 0u;
-            if (pass == 0) {
-#pragma unroll
-              for (int s = 0; s < P1_SLICES; ++s)
-#pragma unroll
-                for (int u = 0; u < P1_SLICES - s; ++u)
-                  mma_i8_2sm(tmem + uint32_t((s + u) * BN),
-                             smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128),
-                             smem_desc(b0 + u * B_BLK2, 128, (BKB / 16) * 128), s > 0 ? 1u : acc0);
-            } else {
-#pragma unroll
-              for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int u = (s < 4 ? 4 - s : 0); u < S - s; ++u)
-                  mma_i8_2sm(tmem + uint32_t((s + u - 4) * BN),
-                             smem_desc(a0 + s * A_BLK, 128, (BKB / 16) * 128),
-                             smem_desc(b0 + u * B_BLK2, 128, (BKB / 16) * 128), s > 0 ? 1u : acc0);
-            }
-            mma_commit_2sm(&empty[st]);  // frees stage st in both CTAs when these retire
-          }
-          mma_commit_2sm(tmem_full);
-        }
-      }
-    } else if (lane == 0 && rank == 1) {  // follower: relay completed stages to the leader
-      const uint32_t lead_full = mapa_u32(smem_u32(full), 0);
-      int64_t it = 0;
-      for (int64_t t = pair; t < tiles; t += npairs)
-        for (int pass = 0; pass < 2; ++pass)
-          for (int64_t kb = 0; kb < KB; ++kb, ++it) {
-            const int st = int(it % STAGES2);
-            mbar_wait(&full[st], uint32_t((it / STAGES2) & 1));
-            mbar_arrive_cluster(lead_full + uint32_t(st * sizeof(uint64_t)));
-          }
-    }
-  } else {
-    const int q = warp % 4, half = (warp - 2) / 4;
-    const uint32_t tq = tmem + (uint32_t(q * 32) << 16) + uint32_t(half * EPI_COLS);
-    const uint32_t lead_empty = mapa_u32(smem_u32(tmem_empty), 0);
-    int64_t np = 0;
-    for (int64_t t = pair; t < tiles; t += npairs, np += 2) {
-      const int64_t mt = 2 * (t % tiles_m2) + rank, nt = t / tiles_m2;
-      const int64_t i = mt * BM + q * 32 + lane;
-      const int64_t n0 = nt * BN + half * EPI_COLS;
-      const double ri = i < M ? o.alpha * ra[i] : 0.0;
-      const double c0s = n0 + lane < N ? cb[n0 + lane] : 0.0;
-      const double c1s = n0 + 32 + lane < N ? cb[n0 + 32 + lane] : 0.0;
-      double hv[EPI_COLS];
-      mbar_wait(tmem_full, uint32_t(np & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < EPI_COLS; c += 16) drainw<4, 16>(tq + uint32_t(c), hv + c);
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(lead_empty);
-      mbar_wait(tmem_full, uint32_t((np + 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < EPI_COLS; c += 4) {
-        double lv[4];
-        drainw<3, 4>(tq + uint32_t(c), lv);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double cs = __shfl_sync(0xffffffffu, c + j < 32 ? c0s : c1s, (c + j) % 32);
-          hv[c + j] = (hv[c + j] * 0x1p-36 + lv[j] * 0x1p-60) * ri * cs;
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(lead_empty);
-      if (i < M) {
-        int64_t kk = n0 / o.nb, jj = n0 - kk * o.nb;
-        double* ci = o.C + (i % o.mr) + (i / o.mr) * o.rs;
-        if (o.beta == 0.0) {
-#pragma unroll
-          for (int j = 0; j < EPI_COLS; ++j) {
-            if (n0 + j < N) ci[kk * o.bs + jj * o.ldc] = hv[j];
-            if (++jj == o.nb) {
-              jj = 0;
-              ++kk;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < EPI_COLS; ++j) {
-            if (n0 + j < N) {
-              double* cp = ci + kk * o.bs + jj * o.ldc;
-              *cp = hv[j] + o.beta * *cp;
-            }
-            if (++jj == o.nb) {
-              jj = 0;
-              ++kk;
-            }
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  cluster.sync();  // the leader's MMAs into the follower's TMEM and smem are complete
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
 }  // namespace oz
 }  // namespace latsum_b200

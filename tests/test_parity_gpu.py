@@ -768,3 +768,47 @@ def test_host_sink_streams_the_result(ctx, cfg):
     finally:
         ctx.set_host_sink(0, 0)
     assert not t2.sink_written
+
+
+_DMMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1411_1994_b200 import api, workload as W
+g = W.baseline(int(sys.argv[2]))
+ctx = api.Context(0)
+ref = api.reference_for(g, ctx); can = api.lattice_sum(ref, g)
+t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=False)
+np.savez(sys.argv[3], ranks=np.array(rep.chosen_ranks), s0=rep.singular_values[0],
+         s1=rep.singular_values[1], s2=rep.singular_values[2], tie=np.array(rep.tie_at_cutoff))
+"""
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_ozaki_stage3_matches_dmma_stage3(ctx, cfg, tmp_path):
+    """The large configs' Grams, deflation projections and bases run on the Ozaki int8 GEMM;
+    the same RHOSVD with every stage-3 GEMM on FP64 DMMA (LATSUM_GEMM_DMMA=1, a separate
+    process: the switch is read once) gives the same ranks and the same spectrum at the
+    cut (1e-6 per value in sigma^2 units as in the fixture test) and tail sums to 1e-4."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, env in (("ozaki", {}), ("dmma", {"LATSUM_GEMM_DMMA": "1"})):
+        f = tmp_path / f"{name}.npz"
+        r = subprocess.run([sys.executable, "-c", _DMMA_SCRIPT, root, str(cfg), str(f)],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[name] = np.load(f)
+    a, b = outs["ozaki"], outs["dmma"]
+    assert list(a["ranks"]) == list(b["ranks"])
+    for l in range(3):
+        sa, sb = a[f"s{l}"], b[f"s{l}"]
+        r = int(a["ranks"][l])
+        idx = np.arange(max(0, r - 64), min(sa.size, r + 64))
+        idx = idx[sb[idx] >= 1e-2 * sb[r - 1]]
+        err = np.abs(sa[idx] ** 2 - sb[idx] ** 2) - (2e-6 * sb[idx] ** 2 + 1e-8 * sb[r - 1] ** 2)
+        assert np.max(err) <= 0, (l, int(idx[np.argmax(err)]))
+        ta, tb = np.sqrt(np.sum(sa[r:] ** 2)), np.sqrt(np.sum(sb[r:] ** 2))
+        assert abs(ta - tb) <= 1e-4 * tb

@@ -2447,21 +2447,55 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       tms[i].project = tp.stop();
     }
   };
+  // norm_f only feeds the report: it runs on its own worker thread and stream and is joined
+  // after the core, so neither the modes' join nor the core waits for it
+  std::future<void> norm_done;
+  latsum_ctx* wn = nullptr;
+  if (!zero_terms) {
+    wn = sub_ctx(c, 3);
+    cudaEvent_t fork;
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventRecord(fork, c->stream));
+    CK(cudaStreamWaitEvent(wn->stream, fork, 0));
+    CK(cudaEventDestroy(fork));
+    norm_done = std::async(std::launch::async, [&, wn] {
+      CK(cudaSetDevice(c->device));
+      body(wn, 3);
+    });
+  }
   Trace::mark(c, "rhosvd fork");
-  fork_join(c, zero_terms ? 1 : 4, body);
+  try {
+    fork_join(c, zero_terms ? 1 : 3, body);
+  } catch (...) {
+    if (norm_done.valid()) norm_done.wait();
+    throw;
+  }
   Trace::mark(c, "rhosvd join");
+  auto join_norm = [&] {
+    if (!norm_done.valid()) return;
+    norm_done.get();  // rethrows a norm_f failure
+    merge_sub(c, wn);
+    tm.norm += tms[3].norm;
+  };
   for (int l = 0; l < 3; ++l) {
     mo[l].Z.adopt(c->stream);
     t.P[l].adopt(c->stream);
   }
-  for (const auto& x : tms) {
+  for (int i = 0; i < 3; ++i) {
+    const auto& x = tms[i];
     tm.gram += x.gram;
     tm.syevd += x.syevd;
     tm.deflate += x.deflate;
-    tm.norm += x.norm;
     tm.project += x.project;
   }
-  if (can.Mc == 0 || rep.input_norm == 0.0) {  // zero tensor (rank_reduction.hpp:183-187)
+  if (zero_terms) tm.norm += tms[3].norm + tms[0].norm;
+  bool zero = can.Mc == 0;  // zero tensor (rank_reduction.hpp:183-187): every merged weight 0
+  if (!zero) {
+    zero = true;
+    for (double w : terms_host(can).tw) zero = zero && w == 0.0;
+  }
+  if (zero || (zero_terms && rep.input_norm == 0.0)) {
+    join_norm();
     for (int l = 0; l < 3; ++l) {
       rep.chosen_ranks[l] = 1;
       rep.n_singular[l] = 1;
@@ -2608,6 +2642,7 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     tm.core = tp.stop();
     Trace::mark(c, "core done");
   }
+  join_norm();
   double tails = 0.0;
   for (int l = 0; l < 3; ++l) {
     t.U[l] = std::move(mo[l].Z);

@@ -379,6 +379,7 @@ struct GemmOpts {
   bool lower = false;
   int splits = 0;  // 0 = auto
   const char* tag = "gemm";
+  bool dmma = false;  // keep on FP64 DMMA (products whose rounding sets a noise floor)
 };
 
 template <class Cfg>
@@ -454,7 +455,7 @@ void gemm(latsum_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, doub
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
           int64_t ldc, GemmOpts o = {}) {
   if (M <= 0 || N <= 0 || o.batch <= 0) return;
-  if (!o.kseg && o.batch == 1 && gemm_to_ozaki(M, N, K)) {
+  if (!o.kseg && o.batch == 1 && !o.dmma && gemm_to_ozaki(M, N, K)) {
     const oz::OzOut oo{C, ldc, int64_t(1) << 62, 0, int64_t(1) << 62, 0, beta, alpha};
     ozaki_gemm_ex(c, M, N, K, A, ta ? lda : 1, ta ? 1 : lda, 0, 0, B, tb ? 1 : ldb, tb ? ldb : 1, oo,
                   ozaki_tag(o.tag));  // lower-triangle requests get the full product
@@ -1740,6 +1741,93 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
   }
 }
 
+// Compressed pass 1 (column orientation, merged Grams beyond the in-house solver): a blocked
+// randomized range finder (randQB_b, Martinsson & Voronin 2016) for the ROW space of A gives
+// P (d x m, orthonormal, identical on every rank) with ||A (I - P P^T)||_2 <~ delta, m ~ the
+// numerical rank of A at delta (cfg4 mode 0: ~2480 of the d = 5394 merged columns).  The
+// reduction then runs on C = A P (N x m) through the unchanged column-orientation path: C C^T
+// = A A^T - E E^T with ||E|| <= delta, so every sigma^2 moves by at most delta^2, and the left
+// singular vectors still come through the operand (U = C V lambda^{-1/2}), which damps the
+// Gram eigenvectors' errors (a left-space basis Q with the rows-orientation Gram of Q^T A was
+// measured 1e-6..1e-4 off at the cut on cfg4/cfg5).  Each block sketches the residual,
+// (I - P P^T) A^T Omega with b Gaussian columns (A^T Omega summed over the ranks' row blocks),
+// and orthonormalises it in rounds as randomized_pass2 does (Y^T Y = W h W^T, P_new =
+// Y W_k h_k^{-1/2} within a 1e10 window, the new columns projected against P twice, two
+// Newton-Schulz steps), so every eigensolve is b x b (the in-house solver).  The first block that
+// finds fewer than b - p directions above the floor ends it (the oversampling p makes a missed
+// direction improbable).  The sketch products stay on DMMA: their rounding is the noise floor
+// the stop test reads.  Returns false when the basis would reach `cap` columns.
+struct RangeBasis {
+  DBuf P;
+  int64_t m = 0, blocks = 0, rounds = 0;
+};
+
+bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_t d, int64_t cap,
+                 double delta, bool sharded, uint64_t seed, RangeBasis& o, int eig_owner) {
+  constexpr int64_t kBlock = 256, kOver = 24;
+  const int64_t Nb = blk.n();
+  const int owner = sharded ? eig_owner : -1;
+  o.P.alloc(c, size_t(d) * cap);
+  GemmOpts go = tagged("gemm_rqb");
+  go.dmma = true;
+  int64_t m = 0;
+  for (;;) {
+    if (m + kOver >= cap) return false;
+    const int64_t bb = std::min<int64_t>(kBlock, cap - m);
+    // Omega: the same N x b Gaussian matrix on every rank; this rank's rows [lo, hi)
+    DBuf Om(c, size_t(N) * bb), Y(c, size_t(d) * bb), S(c, size_t(cap) * bb);
+    k_fill_gauss<<<grid_for(N * bb), 256, 0, c->stream>>>(Om.p, N * bb, seed + uint64_t(o.blocks) * 7919u);
+    post_launch(c);
+    if (Nb > 0) gemm(c, true, false, d, bb, Nb, 1.0, A, Nb, Om.p + blk.lo, N, 0.0, Y.p, d, go);
+    else CK(cudaMemsetAsync(Y.p, 0, sizeof(double) * d * bb, c->stream));
+    if (sharded) allreduce(c, Y.p, size_t(d) * bb);
+    // a direction of the residual with singular value s shows in Y^T Y at ~ s^2 b
+    const double stop_h = 0.04 * delta * delta * double(bb);
+    auto project_out = [&](double* X, int64_t cols) {  // X <- X - P (P^T X)
+      if (m == 0) return;
+      gemm(c, true, false, m, cols, d, 1.0, o.P.p, d, X, d, 0.0, S.p, m, go);
+      gemm(c, false, false, d, cols, m, -1.0, o.P.p, d, S.p, m, 1.0, X, d, go);
+    };
+    int64_t added = 0;
+    for (int round = 0; round < 4 && added < bb && m < cap; ++round) {
+      project_out(Y.p, bb);
+      project_out(Y.p, bb);
+      DBuf H(c, size_t(bb) * bb);
+      gram(c, false, Y.p, d, bb, H.p);
+      Eig eh;
+      eh.ortho_tol = 1e-6;  // seeds only: the new columns are re-orthonormalised below
+      eh.solve_on(c, bb, std::move(H), owner);
+      std::vector<double> h(bb);
+      for (int64_t i = 0; i < bb; ++i) h[i] = std::max(eh.lam_asc[bb - 1 - i], 0.0);
+      const double hmax = h[0];
+      if (!(hmax > stop_h)) break;
+      int64_t kk = 0;
+      while (kk < bb - added && m + kk < cap && h[kk] > std::max(1e-10 * hmax, stop_h)) ++kk;
+      if (kk == 0) break;
+      double* Pn = o.P.p + d * m;
+      DBuf Vk(c, size_t(bb) * kk);
+      eh.leading(c, kk, Vk.p);
+      left_from_vectors(c, Y.p, d, bb, Vk.p, h, kk, Pn, false);
+      project_out(Pn, kk);
+      project_out(Pn, kk);
+      polar_orthonormalize(c, Pn, d, kk, false, 2);
+      m += kk;
+      added += kk;
+      ++o.rounds;
+    }
+    ++o.blocks;
+    o.m = m;
+    if (added + kOver <= bb) return m + kOver < cap;
+  }
+}
+
+// Pass 1 runs on the compressed operand when the merged Gram would exceed the in-house
+// eigensolver (column orientation; not for the ALS unfoldings, which need every vector).
+bool compress_pass1(int64_t N, int64_t d, bool force_deflate) {
+  static const bool off = std::getenv("LATSUM_RQB") && std::string(std::getenv("LATSUM_RQB")) == "0";
+  return !off && !force_deflate && N > d && d > band::SB_NMAX && eig_env_mode() == 0;
+}
+
 struct ModeOut {
   std::vector<double> sigma;
   int64_t r = 1;
@@ -1803,7 +1891,8 @@ struct EigTurnstile {
 // sqrt(eps_mach) sigma_1, e.g. in the ALS unfoldings).
 void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
                   const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
-                  bool sharded, ModeOut& out, Timings& tm, int eig_owner = -1);
+                  bool sharded, ModeOut& out, Timings& tm, int eig_owner = -1,
+                  bool replicated = false, bool compress = true);
 
 void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_t* ranks,
                  double tol, int deflate, ModeOut& out, Timings& tm) {
@@ -1835,14 +1924,60 @@ void reduce_mode(latsum_ctx* c, const latsum_canonical& can, int l, const int64_
 
 void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, int64_t n_sing,
                   const int64_t* rank_fixed, double tol, int deflate, bool force_deflate,
-                  bool sharded, ModeOut& out, Timings& tm, int eig_owner) {
+                  bool sharded, ModeOut& out, Timings& tm, int eig_owner, bool replicated,
+                  bool compress) {
   const int64_t* ranks = rank_fixed;
   const int l = 0;  // rank_fixed points at this operand's rank
   const bool rows = N <= d;
   const int64_t Nb = blk.n();
+  // eigensolves on operands every rank holds in full are owner-solved and broadcast too
+  const int owner = (sharded || replicated) ? eig_owner : -1;
   out.blk = blk;
   Timer timer(c);
   timer.start();
+  if (compress && compress_pass1(N, d, force_deflate)) {
+    // compressed pass 1: P spans the row space of A to delta, and the whole two-pass reduction
+    // runs on C = A P (N x m) in the same column orientation (range_basis).  delta sits four
+    // decades under the smallest singular value any BASELINE cut-off reads (cfg5: ~1.3e-9
+    // sigma_1; sigma^2 moves by <= delta^2, i.e. <= 2e-7 relative there) and above the DMMA
+    // sketch's rounding.
+    const double a2 = frob2(c, At.p, Nb, d, Nb, sharded);
+    const double delta = 2e-13 * std::sqrt(a2);
+    RangeBasis rb;
+    const int64_t cap = std::min<int64_t>(N, d) * 3 / 4;
+    const bool ok = a2 > 0.0 &&
+                    range_basis(c, At.p, blk, N, d, cap, delta, sharded,
+                                0x1411ull * 977 + uint64_t(d) * 131 + uint64_t(N), rb, eig_owner);
+    if (Trace::on())
+      fprintf(stderr, "[rqb] N %ld d %ld m %ld blocks %ld rounds %ld ok %d\n", long(N), long(d),
+              long(rb.m), long(rb.blocks), long(rb.rounds), int(ok));
+    if (ok) {
+      const int64_t m = rb.m;
+      DBuf Ct(c, size_t(std::max<int64_t>(Nb, 1)) * m);
+      if (Nb > 0)
+        gemm(c, false, false, Nb, m, d, 1.0, At.p, Nb, rb.P.p, d, 0.0, Ct.p, Nb, tagged("gemm_rqb_project"));
+      if (Trace::on()) {  // the range basis' miss, ||A - C P^T||_F (dev diagnostics)
+        DBuf R(c, size_t(std::max<int64_t>(Nb, 1)) * d);
+        if (Nb > 0) {
+          CK(cudaMemcpyAsync(R.p, At.p, sizeof(double) * Nb * d, cudaMemcpyDeviceToDevice, c->stream));
+          GemmOpts od = tagged("gemm_rqb");
+          od.dmma = true;
+          gemm(c, false, true, Nb, d, m, -1.0, Ct.p, Nb, rb.P.p, d, 1.0, R.p, Nb, od);
+        }
+        const double r2 = frob2(c, R.p, Nb, d, Nb, sharded);
+        fprintf(stderr, "[rqb] residual ||A (I - P P^T)||_F / ||A||_F = %.3e (delta %.3e)\n",
+                std::sqrt(r2 / a2), delta / std::sqrt(a2));
+      }
+      rb.P.release();
+      tm.gram += timer.stop();
+      Trace::mark(c, "range basis done");
+      reduce_dense(c, Ct, blk, N, m, n_sing, rank_fixed, tol, deflate, false, sharded, out, tm,
+                   eig_owner, replicated, false);
+      out.gsize = m;
+      return;
+    }
+    timer.start();
+  }
   const int64_t n = rows ? N : d;
   out.rows = rows ? 1 : 0;
   out.gsize = n;
@@ -1860,7 +1995,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
   e1.ortho_tol = force_deflate ? -1.0 : 1e-9;
   if (tm.before_eig1) tm.before_eig1();
   try {
-    e1.solve_on(c, n, std::move(G), sharded ? eig_owner : -1);
+    e1.solve_on(c, n, std::move(G), owner);
   } catch (...) {
     if (tm.after_eig1) tm.after_eig1();
     throw;
@@ -2007,7 +2142,7 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
       tm.deflate += timer.stop();
       Trace::mark(c, "deflation + G2 done");
       timer.start();
-      e2.solve_on(c, n2, std::move(G2), sharded ? eig_owner : -1);
+      e2.solve_on(c, n2, std::move(G2), owner);
       tm.syevd += timer.stop();
       Trace::mark(c, "syevd2 done");
       mu_d.resize(nc);  // the nc leading pass-2 values
@@ -2402,7 +2537,8 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
     std::vector<std::pair<int64_t, int>> sz;
     for (int l = 0; l < 3; ++l) {
       const int64_t gn = std::min<int64_t>(can.N[l], can.d[l]);
-      if (!band_eig_ok(gn)) sz.emplace_back(-gn, l);
+      // compressed modes (range basis first) are served in arrival order
+      if (!band_eig_ok(gn) && !compress_pass1(can.N[l], can.d[l], false)) sz.emplace_back(-gn, l);
     }
     std::sort(sz.begin(), sz.end());
     for (const auto& x : sz) turn.order.push_back(x.second);

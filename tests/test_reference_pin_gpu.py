@@ -1,0 +1,91 @@
+"""GPU parity against the REFERENCE ITSELF: the CUDA path (through the C ABI) against outputs of
+the reference's own code (tests/golden/refpin_*.npz, written by tests/golden/make_refpin.py from
+oracle/_ref = /root/reference/proj compiled against the stand-ins of oracle/shim; kept current by
+tests/test_reference_pin.py).  Same bars as test_parity_gpu.py: unit side-matrix columns 1e-12,
+identical RHOSVD ranks, singular values 1e-10 sigma_1, reconstructed potentials within
+10 eps + 1e-12 of the exact sum and 1e-9 of the reference's own truncated values."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ref as RF
+from paper_1411_1994_b200 import api
+from latsum_helpers import col_rel_linf
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = list(RF.CASES)
+
+
+def fixture(name):
+    return np.load(os.path.join(GOLD, f"refpin_{name}.npz"))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_cuda_path_reproduces_the_reference(ctx, name):
+    fx = fixture(name)
+    g = RF.geometry(name)
+    # ---- stage 1 (build_reference_canonical, reference.hpp:95-153)
+    ref = api.reference_for(g, ctx)
+    assert ref.step_constant == float(fx["C0"])
+    t, a = ref.quadrature()
+    assert np.array_equal(t, fx["nodes"]) and np.array_equal(a, fx["quad_weights"])
+    for l in range(3):
+        assert col_rel_linf(ref.factor(l), fx[f"ref_factor{l}"]) < 1e-12
+    np.testing.assert_allclose(ref.weights, fx["ref_weights"], rtol=1e-13)
+    # ---- stage 2 (assembled_sum_canonical / sublattice_union_sum / defected_sum): the
+    # reference's term order, columns and weights
+    can = api.lattice_sum(ref, g)
+    assert can.rank == fx["weights"].size
+    cols = fx["F_cols"]
+    for l in range(3):
+        assert col_rel_linf(can.factor(l)[:, cols], fx[f"F{l}"]) < 1e-12
+    np.testing.assert_allclose(can.weights, fx["weights"], rtol=1e-12,
+                               atol=1e-15 * np.abs(fx["weights"]).max())
+    # ---- stage 3 (rhosvd, rank_reduction.hpp:176-218)
+    tk, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    assert tuple(rep.chosen_ranks) == tuple(int(x) for x in fx["ranks"])
+    assert tk.ranks == rep.chosen_ranks
+    for l in range(3):
+        sv = fx[f"sv{l}"]
+        assert rep.singular_values[l].size == sv.size
+        assert np.max(np.abs(rep.singular_values[l] - sv)) <= 1e-10 * sv[0]
+    bound_abs, bound_rel, weight_norm, input_norm, stab, stab_ok = fx["report"]
+    np.testing.assert_allclose(rep.weight_norm, weight_norm, rtol=1e-12)
+    np.testing.assert_allclose(rep.input_norm, input_norm, rtol=1e-9)
+    np.testing.assert_allclose(rep.stability_constant, stab, rtol=1e-8)
+    assert rep.stability_ok == bool(stab_ok)
+    np.testing.assert_allclose(rep.bound_abs, bound_abs, rtol=1e-3,
+                               atol=1e-12 * weight_norm * fx["sv0"][0])
+    # ---- stage 4 (TuckerTensor::entry, CanonicalTensor::entry, oracle_entry)
+    pr = fx["probes"]
+    scale = np.max(np.abs(fx["v_canonical"]))
+    assert np.max(np.abs(can.entries(pr) - fx["v_canonical"])) <= 1e-12 * scale
+    v = tk.entries(pr)
+    assert np.max(np.abs(v - fx["v_canonical"])) <= (10 * g.eps + 1e-12) * scale
+    assert np.max(np.abs(v - fx["v_tucker"])) <= 1e-9 * scale  # the reference's truncated values
+    nb = fx["v_brute"].size
+    assert np.max(np.abs(api.oracle_entries(ref, g, pr[:nb]) - fx["v_brute"])) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("name", ["vacancies", "yukawa", "union", "clusters"])
+def test_cuda_canonical_to_tucker_matches_the_reference(ctx, name):
+    """canonical_to_tucker (rank_reduction.hpp:280-306) after 3 ALS sweeps: the reference's ranks
+    (+-1 where a slice-drop decision sits within 5% of the budget, whose own cancellation noise is
+    percent level) and values within the tolerance of the exact sum and eps of the reference's."""
+    fx = fixture(name)
+    g = RF.geometry(name)
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    t, rep, sweeps = api.canonical_to_tucker(can, api.TruncationSpec.tol(g.eps),
+                                             max_als_sweeps=int(fx["c2t_sweeps"]))
+    want = tuple(int(x) for x in fx["c2t_ranks"])
+    assert all(abs(rep.chosen_ranks[l] - want[l]) <= 1 for l in range(3)), (rep.chosen_ranks, want)
+    pr = fx["probes"]
+    scale = np.max(np.abs(fx["v_canonical"]))
+    got = t.entries(pr)
+    assert np.max(np.abs(got - fx["v_canonical"])) <= 30 * g.eps * scale
+    if tuple(rep.chosen_ranks) == want:
+        assert np.max(np.abs(got - fx["v_c2t"])) <= g.eps * scale

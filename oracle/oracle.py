@@ -16,6 +16,10 @@ Eigen's BDCSVD performs in the reference):
                       :88-100 project_core, :61-66 tail)
 * `oracle_entries`    lattice_sum.hpp:656-671 oracle_entry (brute force)
 
+PARITY PINNED against the reference itself: oracle/_ref (the reference's headers compiled
+against the stand-ins of oracle/shim, driven by oracle/ref.py) and its golden vectors
+tests/golden/refpin_*.npz; see tests/test_reference_pin.py.
+
 The SVD runs on the column-merged side matrix (identical columns merged with
 sqrt(multiplicity) weights), which has the same A A^T, left singular vectors
 and nonzero singular values as the reference's N x M_c matrix.

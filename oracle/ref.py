@@ -241,6 +241,47 @@ class RefRun:
         return out
 
 
+    def _text(self, fn, *args) -> str:
+        fn.restype = C.c_int64
+        n = fn(self.h, *args, None, C.c_int64(0))
+        if n < 0:
+            raise RuntimeError("reference writer failed: " + lib().lref_last_error(self.h).decode())
+        buf = C.create_string_buffer(int(n) + 1)
+        fn(self.h, *args, buf, C.c_int64(n + 1))
+        return buf.value.decode()
+
+    def spectral_report_text(self) -> str:
+        """write_spectral_report (src/report.cpp:28-47) of the last reduction."""
+        return self._text(lib().lref_spectral_report_text)
+
+    def provenance_text(self, seed: int, reduced: bool, extra: str = "") -> str:
+        """write_provenance (src/report.cpp:49-73) as cmd_sum records the sum."""
+        return self._text(lib().lref_provenance_text, C.c_uint64(seed), C.c_int(int(reduced)),
+                          C.c_char_p(extra.encode()))
+
+    def write_tensor(self, which: str, path: str) -> None:
+        """write_tensor (src/tensor_io.cpp) of the canonical sum or the Tucker result."""
+        self._check(lib().lref_write_tensor(self.h, C.c_int(0 if which == "canonical" else 1),
+                                            C.c_char_p(str(path).encode())))
+
+
+def read_tensor_entries(path, probes):
+    """read_tensor (src/tensor_io.cpp) + entries at the probes -> (kind, dims, values); raises
+    IOError on the reference's TensorIoError."""
+    pr = np.ascontiguousarray(probes, np.int64)
+    out = np.zeros(pr.shape[0])
+    kind = C.c_int()
+    dims = np.zeros(3, np.int64)
+    rc = lib().lref_read_tensor_entries(C.c_char_p(str(path).encode()), C.byref(kind),
+                                        _p(dims, C.c_int64), C.c_int64(pr.shape[0]),
+                                        _p(pr, C.c_int64), _p(out))
+    if rc == 5:
+        raise IOError(lib().lref_last_error(None).decode())
+    if rc != 0:
+        raise RuntimeError(lib().lref_last_error(None).decode())
+    return ("canonical", "tucker")[kind.value], tuple(int(x) for x in dims), out
+
+
 def assembled_vector(ref_col, kset, n, off, nl, accumulation=0):
     ref_col = np.ascontiguousarray(ref_col, np.float64)
     ks = _ints(kset)

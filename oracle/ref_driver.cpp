@@ -12,10 +12,13 @@
 //   rhosvd / canonical_to_tucker  rank_reduction.hpp:176-218, 280-306
 //   oracle_entry                lattice_sum.hpp:656-672
 //   CanonicalTensor::entry / TuckerTensor::entry  canonical.hpp:63-70, tucker.hpp:38-54
+//   write_spectral_report / write_provenance  src/report.cpp:28-73 (compiled from the reference's src/)
+//   write_tensor / read_tensor  src/tensor_io.cpp (compiled from the reference's src/)
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may load it.
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <optional>
 #include <string>
 #include <vector>
@@ -23,6 +26,8 @@
 #include "latsum/lattice_sum.hpp"
 #include "latsum/rank_reduction.hpp"
 #include "latsum/reference.hpp"
+#include "latsum/report.hpp"
+#include "latsum/tensor_io.hpp"
 
 using namespace latsum;
 
@@ -35,6 +40,7 @@ struct Handle {
   ReferenceSet<double> refs;
   std::optional<CanonicalTensor<double>> canonical;
   std::vector<Summand> provenance;
+  LatticeGeometry out_geometry;  // the sum's geometry (parent cells + the defects added)
   std::vector<GridSource<double>> sources;
   std::optional<TuckerTensor<double>> tucker;
   std::optional<SpectralReport<double>> report;
@@ -210,6 +216,7 @@ int lref_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offset
     LatticeSumResult<double> out = defected_sum<double>(base, defects, h->refs, std::nullopt, opts);
     h->canonical = out.canonical();
     h->provenance = out.provenance;
+    h->out_geometry = out.geometry;
     h->tucker.reset();
     h->report.reset();
   });
@@ -320,6 +327,95 @@ int lref_entries(void* hp, int which, int64_t n, const int64_t* probes, double* 
   });
 }
 
+static int64_t emit(const std::string& text, char* buf, int64_t cap) {
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(text.size(), size_t(cap - 1));
+    std::memcpy(buf, text.data(), n);
+    buf[n] = 0;
+  }
+  return int64_t(text.size());
+}
+
+// write_spectral_report (src/report.cpp:28-47) of the last reduction; returns the text length
+int64_t lref_spectral_report_text(void* hp, char* buf, int64_t cap) {
+  Handle* h = static_cast<Handle*>(hp);
+  int64_t n = -1;
+  guarded(h, [&] {
+    if (!h->report) throw std::invalid_argument("no reduction run");
+    std::ostringstream os;
+    write_spectral_report(os, *h->report);
+    n = emit(os.str(), buf, cap);
+  });
+  return n;
+}
+
+// write_provenance (src/report.cpp:49-73) of the sum as cmd_sum records it (commands.cpp:56-72):
+// reduced != 0: the Tucker result with its report, else the canonical sum
+int64_t lref_provenance_text(void* hp, uint64_t seed, int reduced, const char* extra, char* buf,
+                             int64_t cap) {
+  Handle* h = static_cast<Handle*>(hp);
+  int64_t n = -1;
+  guarded(h, [&] {
+    if (!h->canonical) throw std::invalid_argument("no canonical sum built");
+    LatticeSumResult<double> res;
+    res.geometry = h->out_geometry;
+    res.grid = h->ref.base_grid;
+    res.provenance = h->provenance;
+    if (reduced) {
+      if (!h->tucker) throw std::invalid_argument("no reduction run");
+      res.tensor = *h->tucker;
+      res.report = *h->report;
+    } else {
+      res.tensor = *h->canonical;
+    }
+    std::vector<std::string> lines;
+    if (extra && *extra) lines.push_back(extra);
+    std::ostringstream os;
+    write_provenance(os, res, seed, lines);
+    n = emit(os.str(), buf, cap);
+  });
+  return n;
+}
+
+// write_tensor (src/tensor_io.cpp): which 0 = the canonical sum, 1 = the Tucker result
+int lref_write_tensor(void* hp, int which, const char* path) {
+  Handle* h = static_cast<Handle*>(hp);
+  return guarded(h, [&] {
+    if (which == 0) {
+      if (!h->canonical) throw std::invalid_argument("no canonical sum built");
+      write_tensor(path, TensorVariant(*h->canonical));
+    } else {
+      if (!h->tucker) throw std::invalid_argument("no reduction run");
+      write_tensor(path, TensorVariant(*h->tucker));
+    }
+  });
+}
+
+// read_tensor (src/tensor_io.cpp) + entries of what was read; kind_out: 0 canonical, 1 Tucker;
+// returns 5 on a TensorIoError (bad magic / version / checksum / truncation)
+int lref_read_tensor_entries(const char* path, int* kind_out, int64_t* dims, int64_t n,
+                             const int64_t* probes, double* out) {
+  try {
+    const TensorVariant t = read_tensor(path);
+    const bool can = std::holds_alternative<CanonicalTensor<double>>(t);
+    if (kind_out) *kind_out = can ? 0 : 1;
+    const Dims3 d = can ? std::get<CanonicalTensor<double>>(t).dims() : std::get<TuckerTensor<double>>(t).dims();
+    for (int l = 0; l < 3; ++l) dims[l] = d[l];
+    for (int64_t p = 0; p < n; ++p) {
+      const Index i = probes[3 * p], j = probes[3 * p + 1], k = probes[3 * p + 2];
+      out[p] = can ? std::get<CanonicalTensor<double>>(t).entry(i, j, k)
+                   : std::get<TuckerTensor<double>>(t).entry(i, j, k);
+    }
+    return 0;
+  } catch (const TensorIoError& e) {
+    g_error = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 9;
+  }
+}
+
 // detail::assembled_vector on one reference column with explicit K set, n, offset (lattice_sum.hpp:101-144)
 int lref_assembled_vector(const double* ref, int64_t ref_len, const int* kset, int nk, int64_t n,
                           long off, int64_t nl, int accumulation, double* out) {
@@ -342,7 +438,7 @@ int64_t lref_rank_for_tolerance(const double* sv, int64_t n, double eps) {
   return detail::rank_for_tolerance(v, eps);
 }
 
-// default_step_constant / build_quadrature (quadrature.hpp:238-269, 124-187) on shell [a, A]
+// default_step_constant (quadrature.hpp:238-269) and build_quadrature (quadrature.hpp:124-187) on shell [a, A]
 int lref_quadrature(int family, double lam, int M, double C0, double a, double A, double* c0_out,
                     double* nodes, double* weights) {
   return guarded(nullptr, [&] {

@@ -870,7 +870,7 @@ def format_provenance(geom: Geometry, tensor, report: Optional[SpectralReport] =
     for l in range(3):
         p.grid[l] = int(geom.N[l])
         p.cells[l] = int(cells[l])
-    if isinstance(tensor, TuckerTensor):
+    if isinstance(tensor, TuckerTensor) or (hasattr(tensor, "ranks") and not hasattr(tensor, "rank")):
         p.format = 1
         for l in range(3):
             p.ranks[l] = int(tensor.ranks[l])

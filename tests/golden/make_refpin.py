@@ -15,7 +15,8 @@ stand-ins of oracle/shim (oracle/Makefile `ref`); oracle/ref.py drives it.  For 
 * stage 3: rhosvd ranks, tie flags, singular values and report (rank_reduction.hpp:176-218),
   canonical_to_tucker ranks after 3 ALS sweeps (rank_reduction.hpp:280-306);
 * stage 4: Tucker / canonical entries at seeded probes (tucker.hpp:38-54, canonical.hpp:63-70)
-  and the brute-force oracle_entry (lattice_sum.hpp:656-672) on a subset.
+  and the brute-force oracle_entry (lattice_sum.hpp:656-672) on a subset;
+* (case "cubic") the bytes of the reference's own tensor files (write_tensor, src/tensor_io.cpp).
 
 The GPU box has no /root/reference: tests read these files there.  tests/test_reference_pin.py
 re-derives them from the live library whenever it is present, so they cannot go stale."""
@@ -52,6 +53,14 @@ def derive(name: str) -> dict:
         v_t = r.entries("tucker", pr)
         v_c = r.entries("canonical", pr)
         v_b = r.entries("oracle", pr[:N_BRUTE])
+        files = {}
+        if name == "cubic":  # the reference's own tensor files (write_tensor, src/tensor_io.cpp)
+            import tempfile
+            with tempfile.TemporaryDirectory() as td:
+                r.write_tensor("canonical", os.path.join(td, "c.tns"))
+                r.write_tensor("tucker", os.path.join(td, "t.tns"))
+                files["tensor_file_canonical"] = np.frombuffer(open(os.path.join(td, "c.tns"), "rb").read(), np.uint8)
+                files["tensor_file_tucker"] = np.frombuffer(open(os.path.join(td, "t.tns"), "rb").read(), np.uint8)
         if c.get("c2t", True):
             c2t = r.reduce("c2t", eps=c["eps"], max_als_sweeps=C2T_SWEEPS)
             v_c2t = r.entries("tucker", pr)
@@ -73,7 +82,7 @@ def derive(name: str) -> dict:
         report=np.array([red["bound_abs"], red["bound_rel"], red["weight_norm"], red["input_norm"],
                          red["stability_constant"], float(red["stability_ok"])]),
         probes=pr, v_tucker=v_t, v_canonical=v_c, v_brute=v_b,
-        c2t_ranks=np.array(c2t["ranks"], np.int64), v_c2t=v_c2t, c2t_sweeps=C2T_SWEEPS)
+        c2t_ranks=np.array(c2t["ranks"], np.int64), v_c2t=v_c2t, c2t_sweeps=C2T_SWEEPS, **files)
     return out
 
 

@@ -159,3 +159,74 @@ def test_port_canonical_to_tucker_matches_the_reference(name):
     assert np.max(np.abs(fx["v_c2t"] - fx["v_canonical"])) <= 30 * g.eps * scale
     if core.shape == want:
         assert np.max(np.abs(got - fx["v_c2t"])) <= g.eps * scale
+
+
+class _Rank:  # stands in for a device CanonicalTensor / TuckerTensor (format + ranks only)
+    def __init__(self, rank=None, ranks=None):
+        if rank is not None:
+            self.rank = rank
+        else:
+            self.ranks = ranks
+
+
+@pytest.mark.parametrize("name", ["clusters", "union", "cubic"])
+def test_report_writers_match_the_references(ref_built, name):
+    """latsum_format_spectral_report / latsum_format_provenance (host-only C ABI) against the
+    reference's own write_spectral_report / write_provenance (src/report.cpp:28-73, compiled into
+    oracle/_ref) on the same numbers: identical text."""
+    from paper_1411_1994_b200 import api
+    g = RF.geometry(name)
+    r = RF.RefRun(name)
+    try:
+        r.sum()
+        red = r.reduce("rhosvd", eps=g.eps)
+        want_report = r.spectral_report_text()
+        want_prov_t = r.provenance_text(2 ** 64 - 3, True, "note x")
+        want_prov_c = r.provenance_text(7, False)
+        n_terms = r.canonical()[1].size
+    finally:
+        r.close()
+    rep = api.SpectralReport(
+        singular_values=red["sv"], chosen_ranks=red["ranks"], bound_abs=red["bound_abs"],
+        bound_rel=red["bound_rel"], weight_norm=red["weight_norm"], input_norm=red["input_norm"],
+        stability_constant=red["stability_constant"], stability_ok=red["stability_ok"],
+        tie_at_cutoff=red["ties"], cutoff_margin=(0.0, 0.0, 0.0), deflated=(False,) * 3,
+        gram_rows=(False,) * 3, gram_size=(0, 0, 0), ms={})
+    assert api.format_spectral_report(rep) == want_report
+    assert api.format_provenance(g, _Rank(ranks=red["ranks"]), rep, seed=2 ** 64 - 3,
+                                 extra_lines=["note x"]) == want_prov_t
+    assert api.format_provenance(g, _Rank(rank=n_terms), seed=7) == want_prov_c
+    # and the oracle's restatements, which the GPU-side tests use
+    assert O.spectral_report_text(red["ranks"], red["bound_abs"], red["bound_rel"], red["weight_norm"],
+                                  red["input_norm"], red["stability_constant"], red["stability_ok"],
+                                  red["ties"], red["sv"]) == want_report
+
+
+def test_tensor_file_layout_is_the_references(ref_built, tmp_path):
+    """write_tensor / read_tensor (src/tensor_io.cpp, compiled into oracle/_ref): the oracle's
+    restatement of the layout (which the product's writer equals byte for byte,
+    test_tensor_files_match_reference_layout) produces the reference's bytes; the reference reads
+    them back and rejects a flipped bit."""
+    r = RF.RefRun("cubic")
+    try:
+        r.sum()
+        F, w = r.canonical()
+        red = r.reduce("rhosvd", eps=RF.CASES["cubic"]["eps"])
+        pc, pt = tmp_path / "c.tns", tmp_path / "t.tns"
+        r.write_tensor("canonical", pc)
+        r.write_tensor("tucker", pt)
+        pr = O.probes((64, 64, 64), 50, 5)
+        want_c, want_t = r.entries("canonical", pr), r.entries("tucker", pr)
+    finally:
+        r.close()
+    assert pc.read_bytes() == O.tensor_file_bytes("C", (64, 64, 64), [w.size], [w] + F)
+    assert pt.read_bytes() == O.tensor_file_bytes("T", (64, 64, 64), red["ranks"], [red["core"]] + red["U"])
+    kind, dims, got = RF.read_tensor_entries(pt, pr)
+    assert kind == "tucker" and dims == (64, 64, 64) and np.array_equal(got, want_t)
+    kind, dims, got = RF.read_tensor_entries(pc, pr)
+    assert kind == "canonical" and np.array_equal(got, want_c)
+    raw = bytearray(pt.read_bytes())
+    raw[40] ^= 0x01
+    pt.write_bytes(bytes(raw))
+    with pytest.raises(IOError):
+        RF.read_tensor_entries(pt, pr)

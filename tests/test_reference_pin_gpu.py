@@ -89,3 +89,29 @@ def test_cuda_canonical_to_tucker_matches_the_reference(ctx, name):
     assert np.max(np.abs(got - fx["v_canonical"])) <= 30 * g.eps * scale
     if tuple(rep.chosen_ranks) == want:
         assert np.max(np.abs(got - fx["v_c2t"])) <= g.eps * scale
+
+
+def test_cuda_path_reads_the_references_tensor_files(ctx, tmp_path):
+    """latsum_tensor_read on files the reference itself wrote (write_tensor, src/tensor_io.cpp):
+    same entries as the reference evaluates from them, and a tampered file is rejected."""
+    fx = fixture("cubic")
+    pc, pt = tmp_path / "c.tns", tmp_path / "t.tns"
+    pc.write_bytes(fx["tensor_file_canonical"].tobytes())
+    pt.write_bytes(fx["tensor_file_tucker"].tobytes())
+    can = api.read_tensor(pc, ctx)
+    tk = api.read_tensor(pt, ctx)
+    pr = fx["probes"]
+    scale = np.max(np.abs(fx["v_canonical"]))
+    assert can.rank == fx["weights"].size and tuple(tk.ranks) == tuple(int(x) for x in fx["ranks"])
+    assert np.max(np.abs(can.entries(pr) - fx["v_canonical"])) <= 1e-13 * scale
+    assert np.max(np.abs(tk.entries(pr) - fx["v_tucker"])) <= 1e-13 * scale
+    # re-writing what was read reproduces the reference's bytes
+    api.write_tensor(tmp_path / "c2.tns", can)
+    api.write_tensor(tmp_path / "t2.tns", tk)
+    assert (tmp_path / "c2.tns").read_bytes() == pc.read_bytes()
+    assert (tmp_path / "t2.tns").read_bytes() == pt.read_bytes()
+    raw = bytearray(pt.read_bytes())
+    raw[50] ^= 0x10
+    pt.write_bytes(bytes(raw))
+    with pytest.raises(IOError):
+        api.read_tensor(pt, ctx)

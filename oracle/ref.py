@@ -170,7 +170,7 @@ class RefRun:
         return dict(factors=f, weights=w, nodes=t, quad_weights=a, C0=c0.value,
                     shell=(float(shell[0]), float(shell[1])), N=tuple(int(x) for x in info[4:7]))
 
-    def sum(self, accumulation: int = 0):
+    def _marshal(self):
         c = self.case
         subs = c.get("sublattices") or []
         defs = c.get("defects") or []
@@ -182,10 +182,46 @@ class RefRun:
         goff = np.ascontiguousarray(np.asarray([d[2] if d[2] is not None else (0.0, 0.0, 0.0)
                                                 for d in defs], np.float64).reshape(-1)) if defs else None
         kind = _ints([0 if d[1] == -1.0 else 1 for d in defs]) if defs else None
-        self._check(lib().lref_sum(self.h, C.c_int(len(subs)), _p(sub_cells, C.c_int), _p(sub_off),
-                                   C.c_int(len(defs)), _p(nsites, C.c_int), _p(sites, C.c_int),
-                                   _p(charge), _p(goff), _p(kind, C.c_int), C.c_int(accumulation)))
+        self._keep = (sub_cells, sub_off, nsites, sites, charge, goff, kind)
+        return (C.c_int(len(subs)), _p(sub_cells, C.c_int), _p(sub_off), C.c_int(len(defs)),
+                _p(nsites, C.c_int), _p(sites, C.c_int), _p(charge), _p(goff), _p(kind, C.c_int))
+
+    def sum(self, accumulation: int = 0):
+        """The canonical sum through the library functions (assembled_sum_canonical or
+        sublattice_union_sum, then defected_sum)."""
+        self._check(lib().lref_sum(self.h, *self._marshal(), C.c_int(accumulation)))
         return self
+
+    def cmd_sum(self, eps: Optional[float] = None, max_als_sweeps: int = -1, seed: int = 0,
+                tensor_path=None, provenance_path=None, report_path=None) -> str:
+        """The reference's own `latsum sum` (cmd_sum, src/commands.cpp:108-177): with eps the
+        result is canonical_to_tucker's.  Sublattice cases ignore defects, as cmd_sum does.
+        Returns the command's log."""
+        def path(p):
+            return C.c_char_p(str(p).encode()) if p else None
+        buf = C.create_string_buffer(1 << 16)
+        args = list(self._marshal())
+        if self.case.get("sublattices"):
+            args[3] = C.c_int(0)
+        self._check(lib().lref_cmd_sum(self.h, *args, C.c_double(eps or 0.0), C.c_int(max_als_sweeps),
+                                       C.c_uint64(seed), path(tensor_path), path(provenance_path),
+                                       path(report_path), buf, C.c_int64(1 << 16)))
+        return buf.value.decode()
+
+    def cmd_verify(self, tensor_path, provenance_path=None, probes: int = 500,
+                   tolerance: float = 1e-10, bound_abs: float = -1.0, seed: int = 0):
+        """The reference's own `latsum verify` (cmd_verify, src/commands.cpp:200-284) on a stored
+        tensor file -> (ok, log, error)."""
+        buf = C.create_string_buffer(1 << 16)
+        rc = lib().lref_cmd_verify(self.h, C.c_char_p(str(tensor_path).encode()),
+                                   C.c_char_p(str(provenance_path).encode()) if provenance_path else None,
+                                   C.c_int(probes), C.c_double(tolerance), C.c_double(bound_abs),
+                                   C.c_uint64(seed), buf, C.c_int64(1 << 16))
+        return rc == 0, buf.value.decode(), ("" if rc == 0 else lib().lref_last_error(self.h).decode())
+
+    def tucker(self) -> dict:
+        """The Tucker result held by the handle (after reduce or a truncated cmd_sum)."""
+        return self._tucker()
 
     def canonical(self):
         rank, ns = C.c_int64(), C.c_int64()
@@ -218,6 +254,9 @@ class RefRun:
         self._check(lib().lref_reduce(self.h, C.c_int(0 if mode == "rhosvd" else 1),
                                       C.c_double(eps if eps is not None else 0.0),
                                       _p(rk, C.c_int64), C.c_int(max_als_sweeps)))
+        return self._tucker()
+
+    def _tucker(self) -> dict:
         r, nsv, rep, ties = np.zeros(3, np.int64), np.zeros(3, np.int64), np.zeros(6), np.zeros(3, np.int32)
         self._check(lib().lref_tucker_info(self.h, _p(r, C.c_int64), _p(nsv, C.c_int64), _p(rep),
                                            _p(ties, C.c_int)))

@@ -14,6 +14,8 @@
 //   CanonicalTensor::entry / TuckerTensor::entry  canonical.hpp:63-70, tucker.hpp:38-54
 //   write_spectral_report / write_provenance  src/report.cpp:28-73 (compiled from the reference's src/)
 //   write_tensor / read_tensor  src/tensor_io.cpp (compiled from the reference's src/)
+//   cmd_sum / cmd_verify  src/commands.cpp:108-177, 200-284 (compiled from the reference's src/;
+//                         its reference cache is stubbed "never cached" by ref_nocache.cpp)
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may load it.
 #include <cstdint>
 #include <cstring>
@@ -23,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "latsum/commands.hpp"
 #include "latsum/lattice_sum.hpp"
 #include "latsum/rank_reduction.hpp"
 #include "latsum/reference.hpp"
@@ -41,6 +44,8 @@ struct Handle {
   std::optional<CanonicalTensor<double>> canonical;
   std::vector<Summand> provenance;
   LatticeGeometry out_geometry;  // the sum's geometry (parent cells + the defects added)
+  std::vector<SublatticePlacement> placements;
+  int M = 0;
   std::vector<GridSource<double>> sources;
   std::optional<TuckerTensor<double>> tucker;
   std::optional<SpectralReport<double>> report;
@@ -107,6 +112,7 @@ void* lref_create(int family, double lam, int M, const int* cells, int n_per_cel
       }
     }
     h->n_per_cell = n_per_cell;
+    h->M = M;
     h->geom.validate();
     const UniformGrid<double> grid = lattice_grid<double>(h->geom, n_per_cell);
     ReferenceOptions opts;
@@ -166,6 +172,7 @@ int lref_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offset
                                             : Accumulation::compensated;
     LatticeSumResult<double> base;
     h->sources.clear();
+    h->placements.clear();
     if (n_sub == 0) {
       base.tensor = assembled_sum_canonical(h->ref, h->geom, opts);
       base.geometry = h->geom;
@@ -194,6 +201,7 @@ int lref_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offset
         subs.push_back(std::move(p));
       }
       base = sublattice_union_sum<double>(subs, h->ref, h->geom, std::nullopt, opts);
+      h->placements = subs;
     }
     std::vector<DefectSpec> defects;
     const int* site = def_sites;
@@ -414,6 +422,109 @@ int lref_read_tensor_entries(const char* path, int* kind_out, int64_t* dims, int
     g_error = e.what();
     return 9;
   }
+}
+
+static RunConfig run_config(const Handle* h, uint64_t seed) {
+  RunConfig cfg;
+  cfg.kernel = h->geom.kernel;
+  cfg.n = h->n_per_cell;
+  cfg.b = h->geom.cell_width;
+  cfg.quad_M = h->M;
+  cfg.geometry = h->canonical || h->tucker ? h->out_geometry : h->geom;
+  cfg.has_geometry = true;
+  cfg.sublattices = h->placements;
+  cfg.seed = seed;
+  return cfg;
+}
+
+// cmd_sum (src/commands.cpp:108-177), the caller of the hot path: the geometry given to
+// lref_create plus the defect clusters (as in lref_sum) or sublattices, optional truncation
+// eps > 0 (canonical_to_tucker), writing the tensor / provenance / report files whose paths are
+// non-empty.  The result stays in the handle (canonical sum, or Tucker result + report).
+int lref_cmd_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offsets, int n_def,
+                 const int* def_nsites, const int* def_sites, const double* def_charge,
+                 const double* def_goff, const int* def_kind, double eps, int max_als_sweeps,
+                 uint64_t seed, const char* tensor_path, const char* provenance_path,
+                 const char* report_path, char* logbuf, int64_t cap) {
+  Handle* h = static_cast<Handle*>(hp);
+  return guarded(h, [&] {
+    h->canonical.reset();
+    h->tucker.reset();
+    h->report.reset();
+    h->placements.clear();
+    RunConfig cfg = run_config(h, seed);
+    cfg.geometry.defects.clear();
+    for (int s = 0; s < n_sub; ++s) {
+      SublatticePlacement p;
+      p.geom = h->geom;
+      p.geom.active = {};
+      p.geom.cells = {sub_cells[3 * s], sub_cells[3 * s + 1], sub_cells[3 * s + 2]};
+      p.offset_cells = Array3<double>(sub_offsets[3 * s], sub_offsets[3 * s + 1], sub_offsets[3 * s + 2]);
+      cfg.sublattices.push_back(std::move(p));
+    }
+    const int* site = def_sites;
+    for (int d = 0; d < n_def; ++d) {
+      DefectSpec spec;
+      for (int s = 0; s < def_nsites[d]; ++s, site += 3) spec.sites.push_back({site[0], site[1], site[2]});
+      spec.kind = def_kind && def_kind[d] ? DefectKind::impurity : DefectKind::vacancy;
+      spec.charge = def_charge[d];
+      if (def_goff)
+        spec.grid_offset = Array3<double>(def_goff[3 * d], def_goff[3 * d + 1], def_goff[3 * d + 2]);
+      cfg.geometry.defects.push_back(std::move(spec));
+    }
+    if (eps > 0.0) {
+      cfg.truncation = TruncationSpec::tol(eps);
+      if (max_als_sweeps >= 0) cfg.truncation->max_als_sweeps = max_als_sweeps;
+    }
+    if (tensor_path) cfg.output_tensor = tensor_path;
+    if (provenance_path) cfg.output_provenance = provenance_path;
+    if (report_path) cfg.output_report = report_path;
+    std::ostringstream log;
+    LatticeSumResult<double> res = cmd_sum(cfg, log);
+    emit(log.str(), logbuf, cap);
+    h->placements = cfg.sublattices;
+    h->out_geometry = res.geometry;
+    if (n_sub == 0) h->out_geometry.defects = cfg.geometry.defects;
+    h->provenance = res.provenance;
+    if (res.is_canonical()) {
+      h->canonical = res.canonical();
+    } else {
+      h->tucker = res.tucker_tensor();
+      h->report = res.report;
+    }
+  });
+}
+
+// cmd_verify (src/commands.cpp:200-284) of a stored tensor file against the brute-force oracle of
+// the handle's geometry (as last summed): `probes` mt19937_64(seed) probes, gated by bound_abs
+// (>= 0), else the provenance file's recorded bound, else `tolerance`.  0: "verify: ok";
+// 6: VerificationError; 5: TensorIoError.  The reference's log text goes to logbuf.
+int lref_cmd_verify(void* hp, const char* tensor_path, const char* provenance_path, int probes,
+                    double tolerance, double bound_abs, uint64_t seed, char* logbuf, int64_t cap) {
+  Handle* h = static_cast<Handle*>(hp);
+  std::ostringstream log;
+  int rc = 0;
+  try {
+    const RunConfig cfg = run_config(h, seed);
+    VerifyOptions vo;
+    vo.tensor_path = tensor_path;
+    if (provenance_path) vo.provenance_path = provenance_path;
+    vo.probes = probes;
+    vo.tolerance = tolerance;
+    vo.bound_abs = bound_abs;
+    cmd_verify(cfg, vo, log);
+  } catch (const VerificationError& e) {
+    h->error = e.what();
+    rc = 6;
+  } catch (const TensorIoError& e) {
+    h->error = e.what();
+    rc = 5;
+  } catch (const std::exception& e) {
+    h->error = e.what();
+    rc = 9;
+  }
+  emit(log.str(), logbuf, cap);
+  return rc;
 }
 
 // detail::assembled_vector on one reference column with explicit K set, n, offset (lattice_sum.hpp:101-144)

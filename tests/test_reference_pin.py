@@ -49,6 +49,44 @@ def test_reference_unit_tests_pass_on_the_standins(ref_built):
     assert n_cases >= 89, line
 
 
+def test_reference_acceptance_program_passes(ref_built):
+    """The reference's tests/acceptance/acceptance_main.cpp (9 criteria: reference accuracy,
+    assembled exactness, Tucker sums, RHOSVD / ALS bounds, defect algebra, O(L) scaling through its
+    own cmd_bench, Galerkin, quadrature slope) on the reference compiled against oracle/shim."""
+    import subprocess
+    out = subprocess.run([os.path.join(os.path.dirname(RF.SO), "ref_acceptance")],
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout
+    assert out.stdout.count("[PASS]") == 9 and "[FAIL]" not in out.stdout, out.stdout
+
+
+@pytest.mark.parametrize("name", ["clusters", "union", "vacancies"])
+def test_reference_cmd_sum_and_cmd_verify(ref_built, name, tmp_path):
+    """The reference's own `latsum sum` and `latsum verify` (src/commands.cpp:108-177, 200-284)
+    through oracle/_ref: the truncated sum it writes passes its own 500-probe check against the
+    recorded bound, and its ranks are the library-level canonical_to_tucker ranks of the fixture
+    (the union case without its defects: cmd_sum's sublattice route takes none)."""
+    fx = fixture(name)
+    r = RF.RefRun(name)
+    try:
+        tp, pp = tmp_path / "t.tns", tmp_path / "p.txt"
+        log = r.cmd_sum(eps=RF.CASES[name]["eps"], max_als_sweeps=int(fx["c2t_sweeps"]), seed=5,
+                        tensor_path=tp, provenance_path=pp, report_path=tmp_path / "r.txt")
+        assert "wrote tensor" in log and "wrote provenance" in log
+        ranks = r.tucker()["ranks"]
+        if name != "union":
+            assert ranks == tuple(int(x) for x in fx["c2t_ranks"])
+        ok, vlog, err = r.cmd_verify(tp, pp, probes=500, seed=5)
+        assert ok and vlog.rstrip().endswith("verify: ok"), (vlog, err)
+        raw = bytearray(tp.read_bytes())
+        raw[len(raw) // 2] ^= 0x04
+        tp.write_bytes(bytes(raw))
+        ok, vlog, err = r.cmd_verify(tp, pp, probes=10, seed=5)
+        assert not ok and "checksum" in err
+    finally:
+        r.close()
+
+
 @pytest.mark.parametrize("name", [c for c in CASES if c != "large"])
 def test_fixtures_equal_the_live_reference(ref_built, name):
     import make_refpin

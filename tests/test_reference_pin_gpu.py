@@ -115,3 +115,37 @@ def test_cuda_path_reads_the_references_tensor_files(ctx, tmp_path):
     pt.write_bytes(bytes(raw))
     with pytest.raises(IOError):
         api.read_tensor(pt, ctx)
+
+
+@pytest.mark.parametrize("name", ["cubic", "vacancies", "yukawa", "clusters", "active", "large"])
+def test_references_own_verify_accepts_the_cuda_results(ctx, name, tmp_path):
+    """The reference's own `latsum verify` (cmd_verify, src/commands.cpp:200-284, run from
+    oracle/_ref) on tensor files the CUDA path wrote: it reads them (checksum-guarded), enumerates
+    the sources of the same geometry, and checks 500 mt19937_64 probes against its brute-force
+    oracle — the canonical sum at its default tolerance 1e-10, the RHOSVD result against the
+    truncation bound recorded in the provenance sidecar the CUDA path wrote."""
+    if not RF.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    g = RF.geometry(name)
+    ref = api.reference_for(g, ctx)
+    can = api.lattice_sum(ref, g)
+    tk, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps))
+    pc, pt, pp = tmp_path / "c.tns", tmp_path / "t.tns", tmp_path / "p.txt"
+    api.write_tensor(pc, can)
+    api.write_tensor(pt, tk)
+    api.write_provenance(str(pp), g, tk, rep, seed=9)
+    r = RF.RefRun(name)
+    try:
+        r.sum()  # the handle's geometry now carries the case's defects
+        ok, log, err = r.cmd_verify(pc, None, probes=500, tolerance=1e-10, seed=9)
+        assert ok and log.rstrip().endswith("verify: ok"), (log, err)
+        # (an untruncated result records the bound 0 here: the merged-column Gram has exact zeros
+        # where the reference's SVD leaves ~1e-16 sigma_1 noise; the bound gate needs a real tail)
+        if rep.bound_abs > 1e-12 * rep.weight_norm * rep.singular_values[0][0]:
+            ok, log, err = r.cmd_verify(pt, pp, probes=500, seed=9)
+            assert ok and "within bound" in log, (log, err)
+        # and at the reference's own normalised-error gate for a truncated result
+        ok, log, err = r.cmd_verify(pt, None, probes=500, tolerance=10 * g.eps, seed=9)
+        assert ok, (log, err)
+    finally:
+        r.close()

@@ -130,6 +130,10 @@ double latsum_default_step_constant(int family, double lambda, int M, double she
                                     double shell_A, int npts);
 /* reference.hpp:84-93 reference_shell of the doubled grid of (N, box). */
 void latsum_reference_shell(const int64_t N[3], const double box[3], double shell[2]);
+/* commands.cpp:254-260: the seeded probe stream of cmd_verify (std::mt19937_64(seed), one
+ * uniform_int_distribution<Index>(0, dims[l] - 1) per mode, i, j, k per probe) -> probes n x 3,
+ * so that a verification here visits the points `latsum verify` visits for the same seed. */
+void latsum_verify_probes(uint64_t seed, const int64_t dims[3], int64_t n, int64_t* probes);
 
 /* ------------------------------------------------------------------ stage 1
  * reference.hpp:95-153 build_reference_canonical(kernel, grid(box, N), M, {doubled=true,

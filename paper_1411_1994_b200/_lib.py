@@ -110,6 +110,7 @@ SIGNATURES = [
     ("latsum_build_quadrature", _I, [_I, _D, _I, _D, _D, _D, _P, _P]),
     ("latsum_default_step_constant", _D, [_I, _D, _I, _D, _D, _I]),
     ("latsum_reference_shell", None, [_P, _P, _P]),
+    ("latsum_verify_probes", None, [ctypes.c_uint64, _P, _I64, _P]),
     ("latsum_reference_build", _I, [_P, _I, _D, _P, _P, _I, _D, _P]),
     ("latsum_reference_destroy", None, [_P]),
     ("latsum_reference_info", _I, [_P, _P, _P, _P]),

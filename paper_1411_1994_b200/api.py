@@ -725,13 +725,21 @@ def oracle_entries(ref: ReferenceTensor, geom: Geometry, probes) -> np.ndarray:
     return out
 
 
+def verify_probes(seed: int, dims, count: int) -> np.ndarray:
+    """commands.cpp:254-260: the probe points `latsum verify` draws for `seed`
+    (std::mt19937_64 + uniform_int_distribution per mode; latsum_verify_probes)."""
+    d = _i64(dims)
+    out = np.zeros((int(count), 3), np.int64)
+    _lib.lib().latsum_verify_probes(ctypes.c_uint64(int(seed) & (2 ** 64 - 1)), _p(d), int(count), _p(out))
+    return out
+
+
 def verify(tensor, ref: ReferenceTensor, geom: Geometry, probes=500, seed: int = 0,
            tolerance: Optional[float] = None, bound_abs: Optional[float] = None) -> dict:
     """cmd_verify (commands.cpp:200-284): max|got - oracle| / max|oracle| over seeded
     probes, gated by the recorded truncation bound if given, else by `tolerance`."""
     if np.isscalar(probes):
-        rng = np.random.Generator(np.random.PCG64(seed))
-        probes = np.stack([rng.integers(0, geom.N[l], int(probes)) for l in range(3)], axis=1)
+        probes = verify_probes(seed, geom.N, int(probes))
     pr = _i64(probes).reshape(-1, 3)
     want = oracle_entries(ref, geom, pr)
     got = tensor.entries(pr)

@@ -11,6 +11,7 @@
 #include <functional>
 #include <limits>
 #include <mutex>
+#include <random>
 #include <thread>
 #include <vector>
 
@@ -193,6 +194,19 @@ void latsum_reference_shell(const int64_t N[3], const double box[3], double shel
   }
   shell[0] = hmin;
   shell[1] = std::sqrt(3.0) * bmax / 2.0;
+}
+
+void latsum_verify_probes(uint64_t seed, const int64_t dims[3], int64_t n, int64_t* probes) {
+  // commands.cpp:254-260 cmd_verify's probe stream, the same standard-library objects in the
+  // same order: one std::mt19937_64(seed), three uniform_int_distribution<Index>(0, d_l - 1),
+  // (i, j, k) drawn per probe
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<int64_t> di(0, dims[0] - 1), dj(0, dims[1] - 1), dk(0, dims[2] - 1);
+  for (int64_t p = 0; p < n; ++p) {
+    probes[3 * p] = di(rng);
+    probes[3 * p + 1] = dj(rng);
+    probes[3 * p + 2] = dk(rng);
+  }
 }
 
 }  // extern "C"

@@ -5,6 +5,7 @@ tests/test_reference_pin.py).  Same bars as test_parity_gpu.py: unit side-matrix
 identical RHOSVD ranks, singular values 1e-10 sigma_1, reconstructed potentials within
 10 eps + 1e-12 of the exact sum and 1e-9 of the reference's own truncated values."""
 import os
+import re
 
 import numpy as np
 import pytest
@@ -147,5 +148,13 @@ def test_references_own_verify_accepts_the_cuda_results(ctx, name, tmp_path):
         # and at the reference's own normalised-error gate for a truncated result
         ok, log, err = r.cmd_verify(pt, None, probes=500, tolerance=10 * g.eps, seed=9)
         assert ok, (log, err)
+        # api.verify (device brute force, latsum_verify_probes) visits the probes cmd_verify visits
+        # for the same seed and measures what it measures
+        m = re.search(r"max abs error (\S+), max \|oracle\| (\S+), normalized error (\S+)", log)
+        ref_abs, ref_mag, ref_rel = (float(m.group(i).rstrip(",")) for i in (1, 2, 3))
+        mine = api.verify(tk, ref, g, probes=500, seed=9, tolerance=10 * g.eps)
+        assert mine["ok"] and mine["probes"] == 500
+        np.testing.assert_allclose(mine["max_oracle"], ref_mag, rtol=1e-12)
+        np.testing.assert_allclose(mine["max_abs"], ref_abs, rtol=1e-3, atol=1e-13 * ref_mag)
     finally:
         r.close()

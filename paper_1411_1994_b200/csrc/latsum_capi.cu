@@ -1678,7 +1678,9 @@ bool randomized_pass2(latsum_ctx* c, const double* Ap, int64_t Nb, int64_t d, in
       if (sharded) allreduce(c, H.p, size_t(ell) * ell);
       Eig eh;
       // these vectors only seed Q = Y W h^{-1/2}, which two Newton-Schulz steps re-orthonormalise
-      eh.ortho_tol = 1e-6;
+      // (quadratic from any ||W^T W - I|| < 1: 1e-3 leaves 1e-12 after two); a tighter gate sent
+      // ~2 clustered b x b Grams per cfg4 step to the cuSOLVER fallback for nothing
+      eh.ortho_tol = 1e-3;
       eh.solve_on(c, ell, std::move(H), sharded ? eig_owner : -1);
       std::vector<double> h(ell);
       for (int64_t i = 0; i < ell; ++i) h[i] = std::max(eh.lam_asc[ell - 1 - i], 0.0);
@@ -1795,7 +1797,7 @@ bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_
       DBuf H(c, size_t(bb) * bb);
       gram(c, false, Y.p, d, bb, H.p);
       Eig eh;
-      eh.ortho_tol = 1e-6;  // seeds only: the new columns are re-orthonormalised below
+      eh.ortho_tol = 1e-3;  // seeds only: the new columns are re-orthonormalised below (as above)
       eh.solve_on(c, bb, std::move(H), owner);
       std::vector<double> h(bb);
       for (int64_t i = 0; i < bb; ++i) h[i] = std::max(eh.lam_asc[bb - 1 - i], 0.0);

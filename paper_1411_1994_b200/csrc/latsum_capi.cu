@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -133,6 +134,11 @@ struct latsum_ctx {
   // every SM holds them until it finishes, whatever the stream priorities; the low-priority
   // norm worker keeps to a few SMs so the mode workers' kernels are never queued behind it
   int max_ctas = 0;
+  // SMs a capped worker's persistent kernels are holding right now (set on the ROOT context by
+  // that worker): the other contexts' persistent GEMMs size their grids to the SMs left, since
+  // their static tile partition would otherwise wait for the CTAs that cannot be placed until
+  // the capped kernel ends (cfg5: ~80 ms per norm_f Gram launch, on every mode-side GEMM)
+  std::atomic<int> reserved_ctas{0};
   // multi-GPU: one rank of a row-sharded reduction (latsum_ctx_init_comm); each worker
   // context owns a communicator split from this one so concurrent modes never interleave
   ncclComm_t comm = nullptr;
@@ -631,7 +637,12 @@ void oz_run(latsum_ctx* c, const OzSliced& a, const OzSliced& b, oz::OzOut o, co
   ProfScope ps(c, tag, 2.0 * double(M) * double(N) * double(a.K));
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  if (c->max_ctas > 0) sms = std::min(sms, c->max_ctas);
+  if (c->max_ctas > 0) {
+    sms = std::min(sms, c->max_ctas);
+  } else {
+    const latsum_ctx* root = c->parent ? c->parent : c;
+    sms = std::max(sms / 2, sms - root->reserved_ctas.load(std::memory_order_relaxed));
+  }
   const unsigned ctas = unsigned(std::min<int64_t>(tiles, sms));
   // stream the larger operand once: N tiles fastest when A is the bigger one (the core
   // contraction's tall X against the small P_m: 190 -> 155 ms on cfg4), M tiles fastest
@@ -1943,6 +1954,9 @@ void reduce_dense(latsum_ctx* c, DBuf& At, RowBlock blk, int64_t N, int64_t d, i
     // decades under the smallest singular value any BASELINE cut-off reads (cfg5: ~1.3e-9
     // sigma_1; sigma^2 moves by <= delta^2, i.e. <= 2e-7 relative there) and above the DMMA
     // sketch's rounding.
+    // no Gram burst to keep clear of on this path (the range finder is latency-bound): norm_f,
+    // which waits for the modes' Grams, may start now (cfg5: it is 0.9 s of capped GEMMs)
+    if (tm.on_gram) tm.on_gram();
     const double a2 = frob2(c, At.p, Nb, d, Nb, sharded);
     const double delta = 2e-13 * std::sqrt(a2);
     RangeBasis rb;
@@ -2557,6 +2571,11 @@ void rhosvd_impl(latsum_ctx* c, const latsum_canonical& can, const int64_t* rank
       }
       Timer tn(w);
       tn.start();
+      struct Reserve {  // the SMs this worker's capped persistent grids hold while it runs
+        std::atomic<int>& r;
+        Reserve(std::atomic<int>& x, int n) : r(x) { r.store(n); }
+        ~Reserve() { r.store(0); }
+      } hold(c->reserved_ctas, zero_terms ? 0 : w->max_ctas);
       rep.input_norm = canonical_norm(w, can);
       tms[3].norm = tn.stop();
     } else {

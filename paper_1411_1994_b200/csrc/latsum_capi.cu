@@ -1783,6 +1783,22 @@ bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_
   o.P.alloc(c, size_t(d) * cap);
   GemmOpts go = tagged("gemm_rqb");
   go.dmma = true;
+  // The sketch A^T Omega is the one large product of a block (2 d b Nb flops; the projections
+  // are 2 d b m): it runs on the int8 tensor cores with A^T sliced ONCE for all blocks (lines =
+  // the d columns of this rank's row block, K = Nb in <= KMAX chunks).  Its rounding (~3e-16 of
+  // a unit column per entry, a few times the DMMA product's) leaves Y^T Y eigenvalues of
+  // ~1e-27 d against the stop level 0.04 delta^2 b ~ 1e-20: five decades of room.
+  const bool oz_sketch = Nb > 0 && double(d) * double(kBlock) * double(Nb) >= 2e10;
+  std::vector<OzSliced> As;
+  std::vector<int64_t> k0s;
+  if (oz_sketch) {
+    const int64_t parts = (Nb + oz::KMAX - 1) / oz::KMAX, kc = (Nb + parts - 1) / parts;
+    As.resize(size_t(parts));
+    for (int64_t p = 0; p < parts; ++p) {
+      k0s.push_back(p * kc);
+      oz_slice_a(c, A + p * kc, Nb, 1, d, std::min(kc, Nb - p * kc), As[size_t(p)]);
+    }
+  }
   int64_t m = 0;
   for (;;) {
     if (m + kOver >= cap) return false;
@@ -1791,8 +1807,17 @@ bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_
     DBuf Om(c, size_t(N) * bb), Y(c, size_t(d) * bb), S(c, size_t(cap) * bb);
     k_fill_gauss<<<grid_for(N * bb), 256, 0, c->stream>>>(Om.p, N * bb, seed + uint64_t(o.blocks) * 7919u);
     post_launch(c);
-    if (Nb > 0) gemm(c, true, false, d, bb, Nb, 1.0, A, Nb, Om.p + blk.lo, N, 0.0, Y.p, d, go);
-    else CK(cudaMemsetAsync(Y.p, 0, sizeof(double) * d * bb, c->stream));
+    if (oz_sketch) {
+      for (size_t p = 0; p < As.size(); ++p) {
+        OzSliced om;
+        oz_slice_b(c, Om.p + blk.lo + k0s[p], N, 1, bb, As[p].K, om);
+        oz_run(c, As[p], om, oz_out(Y.p, d, p == 0 ? 0.0 : 1.0), "gemm_rqb(ozaki-i8)");
+      }
+    } else if (Nb > 0) {
+      gemm(c, true, false, d, bb, Nb, 1.0, A, Nb, Om.p + blk.lo, N, 0.0, Y.p, d, go);
+    } else {
+      CK(cudaMemsetAsync(Y.p, 0, sizeof(double) * d * bb, c->stream));
+    }
     if (sharded) allreduce(c, Y.p, size_t(d) * bb);
     // a direction of the residual with singular value s shows in Y^T Y at ~ s^2 b
     const double stop_h = 0.04 * delta * delta * double(bb);

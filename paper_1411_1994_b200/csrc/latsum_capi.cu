@@ -3130,7 +3130,9 @@ void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], con
   const double* U1 = t.U[1].p + lo[1];
   const double* U2 = t.U[2].p + lo[2];
   const int64_t budget = int64_t(1) << 29;  // doubles per intermediate (4 GiB)
-  const int64_t njc = balanced_chunk(nj, budget / std::max<int64_t>(r0 * r2, 1), 128);
+  // y-chunks in whole 128-column tiles of the Q GEMM (cfg4: the 4 GiB cap gave 202-row chunks,
+  // 256 columns of MMA work for 202): Q may take 8 GiB so the aligned chunk fits (cfg4: 384)
+  const int64_t njc = balanced_chunk(nj, 2 * budget / std::max<int64_t>(r0 * r2, 1), 128);
   DBuf Q(c, size_t(r0) * njc * r2);
   const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(r0 * njc, 1), 65535), 1);
   DBuf X(c, size_t(r0) * njc * nkc);

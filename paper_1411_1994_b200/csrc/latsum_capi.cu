@@ -3115,11 +3115,97 @@ void projected_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], 
 void projected_probes(latsum_ctx* c, const latsum_tucker& t, const int64_t* probes, int64_t np,
                       double* out_host);
 
+// The three-GEMM chain on the int8 tensor cores for any contraction order.  Roles: F is
+// contracted first, S second, L last (the rows of the final slab GEMM):
+//   Q[(a_L, j_F), a_S] = sum_{a_F} core[..] U_F[j_F, a_F]        2 r0 r1 r2 n_F flops
+//   X[(a_L, j_F), k_S] = sum_{a_S} Q[(a_L, j_F), a_S] U_S[k_S, a_S]   2 r_L r_S n_F n_S
+//   V[i_L, (j_F, k_S)] = sum_{a_L} U_L[i_L, a_L] X[a_L, (j_F, k_S)]   2 r_L n_L n_F n_S
+// so the mode of smallest rank goes last (cfg4, ranks 2095 / 1207 / 1266: 4.7e13 flops with
+// L = 1 against 7.1e13 with the fixed order L = 0).  No data is permuted: the core is sliced
+// through its strides, and the final GEMM writes the box through the output addressing (with
+// L != 0 and F = 0 it is computed transposed, so its tile rows still run along the box's
+// contiguous index and the stores stay coalesced).
+void tucker_eval_chain(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t n[3],
+                       int L, int F, int S, double* out) {
+  const int64_t r[3] = {t.r[0], t.r[1], t.r[2]};
+  const int64_t cs[3] = {1, r[0], r[0] * r[1]};       // core strides
+  const int64_t os[3] = {1, n[0], n[0] * n[1]};       // box strides
+  const int64_t rL = r[L], rF = r[F], rS = r[S];
+  const double* UL = t.U[L].p + lo[L];
+  const double* UF = t.U[F].p + lo[F];
+  const double* US = t.U[S].p + lo[S];
+  const int64_t budget = int64_t(1) << 29;  // doubles per intermediate (4 GiB; Q may take 8)
+  // F-chunks in whole 128-column tiles of the Q GEMM
+  const int64_t nfc = balanced_chunk(n[F], 2 * budget / std::max<int64_t>(rL * rS, 1), 128);
+  const int64_t nsc = balanced_chunk(n[S], std::min<int64_t>(budget / std::max<int64_t>(rL * nfc, 1), 65535), 1);
+  DBuf Q(c, size_t(rL) * nfc * rS), X(c, size_t(rL) * nfc * nsc);
+  OzSliced sUL, sQ, sCore;  // sliced once and reused across the chunks that share them
+  if (L == 0) oz_slice_a(c, UL, 1, t.N[L], n[L], rL, sUL);
+  else oz_slice_b(c, UL, 1, t.N[L], n[L], rL, sUL);
+  // the core's lines (a_L, a_S) over K = a_F: the A operand of every chunk's Q GEMM
+  oz_slice_a(c, t.core.p, cs[L], cs[F], rL * rS, rF, sCore, rL, cs[S]);
+  for (int64_t j0 = 0; j0 < n[F]; j0 += nfc) {
+    const int64_t njj = std::min(nfc, n[F] - j0);
+    {
+      OzSliced sUF;
+      oz_slice_b(c, UF + j0, 1, t.N[F], njj, rF, sUF);
+      oz::OzOut o = oz_out(Q.p, rL);
+      o.mr = rL;
+      o.rs = rL * njj;
+      oz_run(c, sCore, sUF, o, "gemm_eval_q(ozaki-i8)");
+    }
+    oz_slice_a(c, Q.p, 1, rL * njj, rL * njj, rS, sQ);
+    for (int64_t k0 = 0; k0 < n[S]; k0 += nsc) {
+      const int64_t nkk = std::min(nsc, n[S] - k0);
+      OzSliced sUS, sX;
+      oz_slice_b(c, US + k0, 1, t.N[S], nkk, rS, sUS);
+      oz_run(c, sQ, sUS, oz_out(X.p, rL * njj), "gemm_eval_x(ozaki-i8)");
+      if (L == 0) {  // rows i_L run along the box's contiguous index: V = U_L X
+        oz_slice_b(c, X.p, rL, 1, njj * nkk, rL, sX);  // B lines = the columns (j_F, k_S) of X
+        oz::OzOut o = oz_out(out + j0 * os[F] + k0 * os[S], os[F]);
+        o.nb = njj;
+        o.bs = os[S];
+        oz_run(c, sUL, sX, o, "gemm_eval_slab(ozaki-i8)");
+      } else {  // F == 0: the transposed product V^T = X^T U_L^T puts (j_F, k_S) on the rows, so
+        // the tile rows (TMEM lanes, one per thread) again run along the contiguous index
+        oz_slice_a(c, X.p, rL, 1, njj * nkk, rL, sX);
+        oz::OzOut o = oz_out(out + j0 * os[F] + k0 * os[S], os[L]);
+        o.mr = njj;
+        o.rs = os[S];
+        oz_run(c, sX, sUL, o, "gemm_eval_slab(ozaki-i8)");
+      }
+    }
+  }
+}
+
 void tucker_eval(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3], const int64_t hi[3],
                  double* out) {
   if (!t.has_core) return projected_eval(c, t, lo, hi, out);
   check_box(t.N, lo, hi);
   const int64_t ni = hi[0] - lo[0], nj = hi[1] - lo[1], nk = hi[2] - lo[2];
+  if (!t.core_slab && eval_uses_ozaki(std::max({t.r[0], t.r[1], t.r[2]}))) {
+    // contraction order by flops: the fixed order (L, F, S) = (0, 1, 2), or the smallest-rank
+    // mode last with mode 0 first
+    const int64_t n[3] = {ni, nj, nk};
+    const int orders[3][3] = {{0, 1, 2}, {1, 0, 2}, {2, 0, 1}};
+    static const int forced = [] {
+      const char* e = std::getenv("LATSUM_EVAL_ORDER");  // 0 / 1 / 2: the last-contracted mode (tests)
+      return e ? std::atoi(e) : -1;
+    }();
+    int best = 0;
+    double best_f = 0.0;
+    for (int q = 0; q < 3; ++q) {
+      const int L = orders[q][0], F = orders[q][1], S = orders[q][2];
+      const double f = double(t.r[0]) * t.r[1] * t.r[2] * n[F] + double(t.r[L]) * t.r[S] * n[F] * n[S] +
+                       double(t.r[L]) * n[L] * n[F] * n[S];
+      if (q == 0 || f < 0.95 * best_f) {
+        best = q;
+        best_f = f;
+      }
+    }
+    if (forced >= 0 && forced < 3) best = forced;
+    return tucker_eval_chain(c, t, lo, n, orders[best][0], orders[best][1], orders[best][2], out);
+  }
   if (t.core_slab && t.ra == 0) {  // this rank's slab is empty: its partial box is zero
     CK(cudaMemsetAsync(out, 0, sizeof(double) * ni * nj * nk, c->stream));
     allreduce(c, out, size_t(ni * nj * nk));

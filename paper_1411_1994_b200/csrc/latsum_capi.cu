@@ -3136,8 +3136,18 @@ void tucker_eval_chain(latsum_ctx* c, const latsum_tucker& t, const int64_t lo[3
   const double* US = t.U[S].p + lo[S];
   const int64_t budget = int64_t(1) << 29;  // doubles per intermediate (4 GiB; Q may take 8)
   // F-chunks in whole 128-column tiles of the Q GEMM
-  const int64_t nfc = balanced_chunk(n[F], 2 * budget / std::max<int64_t>(rL * rS, 1), 128);
-  const int64_t nsc = balanced_chunk(n[S], std::min<int64_t>(budget / std::max<int64_t>(rL * nfc, 1), 65535), 1);
+  // chunks in whole 128-column tiles of the GEMM that has them as columns (Q: j_F, X: k_S),
+  // aligned DOWN so they stay inside the budget
+  auto tiled_chunk = [](int64_t n, int64_t cap) {
+    cap = std::max<int64_t>(1, cap);
+    if (n <= cap) return n;
+    const int64_t capa = cap >= 128 ? cap / 128 * 128 : cap;
+    const int64_t parts = (n + capa - 1) / capa;
+    const int64_t c = (n + parts - 1) / parts;
+    return capa >= 128 ? std::min(capa, (c + 127) / 128 * 128) : c;
+  };
+  const int64_t nfc = tiled_chunk(n[F], 2 * budget / std::max<int64_t>(rL * rS, 1));
+  const int64_t nsc = tiled_chunk(n[S], std::min<int64_t>(budget / std::max<int64_t>(rL * nfc, 1), 65535));
   DBuf Q(c, size_t(rL) * nfc * rS), X(c, size_t(rL) * nfc * nsc);
   OzSliced sUL, sQ, sCore;  // sliced once and reused across the chunks that share them
   if (L == 0) oz_slice_a(c, UL, 1, t.N[L], n[L], rL, sUL);

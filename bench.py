@@ -583,8 +583,9 @@ def run_gpu(args):
                          "launches": dom_n, "ms": dom_ms,
                          "peak_source": (I8_PEAK_SOURCE if is_ozaki else FP64_PEAK_SOURCE if is_flops
                                          else "MEASURED_PEAKS.json hbm_gbs"),
-                         "algorithmic": ("28 int8 products x 2 r1 ops per grid point (Ozaki scheme, "
-                                         "FP64-accurate slab GEMM on the int8 tensor cores)" if is_ozaki
+                         "algorithmic": ("28 int8 products x 2 r_L ops per grid point, r_L the rank contracted "
+                                         "last = the smallest (Ozaki scheme, FP64-accurate slab GEMM "
+                                         "on the int8 tensor cores)" if is_ozaki
                                          else "2 r1 flops per grid point of the slab GEMM" if is_flops
                                          else "8 B read + 7 B written per operand element (Ozaki "
                                          "digit slicing)" if "slice" in dom_tag

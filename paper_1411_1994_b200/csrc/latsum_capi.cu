@@ -1352,6 +1352,23 @@ void merge_terms(latsum_canonical& can) {
   }
 }
 
+latsum_ctx* sub_ctx(latsum_ctx* c, int i);
+
+// Events of a multi-stream section, destroyed together.
+struct EventSet {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t record(cudaStream_t s) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+    CK(cudaEventRecord(e, s));
+    return e;
+  }
+  ~EventSet() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
 // Ordered product blocks (the general form of every stage-2 input): block b contributes R
 // terms whose mode-l vector is the assembled sum over its mode-l shift list, weight
 // charge_b * w_ref.  A sublattice, a product-structure defect cluster and a single defect
@@ -1381,6 +1398,8 @@ void assemble_blocks(latsum_ctx* c, const latsum_reference& ref, int64_t nblk,
       }
     blk_off[size_t(nblk) * 3] = o;
   }
+  latsum_ctx* side = c->parent ? nullptr : sub_ctx(c, 0);  // idle here: the mode workers run later
+  EventSet evs;
   for (int l = 0; l < 3; ++l) {
     const int64_t N = ref.N[l];
     std::vector<int64_t> pl_off{0}, pl_shift;
@@ -1422,38 +1441,37 @@ void assemble_blocks(latsum_ctx* c, const latsum_reference& ref, int64_t nblk,
     doff.upload(c, pl_off);
     dsh.upload(c, pl_shift);
     can.dict[l].alloc(c, size_t(N) * can.d[l]);
-    // rows per block: 2048 for the sublattice columns (up to 256 shifted reads per entry,
-    // cfg5: spread over many blocks), up to 8192 for the single-shift defect columns (fewer
-    // blocks amortise the per-block shift-list staging and reductions)
+    // [0, P_sub Rd): multi-shift (sublattice / product-cluster) columns, up to 256 shifted reads
+    // per entry: 2048-row blocks, partial sums of squares per block, the norms, then the
+    // normalised entries (three launches, L2-bound).  They run on a side stream next to
+    // [P_sub Rd, d): the single-shift defect columns — the HBM traffic of the assembly — one
+    // fused launch (k_dict_single).
     const int64_t chunk = 2048;
     const int nchunk = int((N + chunk - 1) / chunk);
-    const int64_t chunk_d = std::min<int64_t>(8192, (N + 2047) / 2048 * 2048);
-    const int nchunk_d = int((N + chunk_d - 1) / chunk_d);
-    DBuf partial(c, size_t(can.d[l]) * nchunk);
+    const int64_t n_multi = std::min(can.d[l], P_sub * Rd);
+    DBuf partial(c, size_t(std::max<int64_t>(n_multi, 1)) * nchunk);
     DBuf& norms = norm_buf[l];
     norms.alloc(c, can.d[l]);
     ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
-    // [0, P_sub Rd): sublattice columns (2048-row blocks); [P_sub Rd, d): single-shift
-    // defect columns (chunk_d rows per block)
-    // sums of squares over chunks of chs rows (partial sums per chunk, then the norms), then
-    // the normalised entries in chunks of chw rows
-    auto l2_path = [&](int64_t c_lo, int64_t c_hi, int64_t chs, int nchs, int64_t chw, int nchw) {
-      if (c_hi <= c_lo) return;
-      DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chs, nchs};
-      a.c0 = c_lo;
-      k_dict_sumsq<<<dim3{unsigned(c_hi - c_lo), unsigned(nchs)}, DICT_THREADS, 0, c->stream>>>(a);
+    DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
+    const bool both = n_multi > 0 && n_multi < can.d[l] && side != nullptr;
+    cudaStream_t sm = both ? side->stream : c->stream;  // the multi-shift columns' stream
+    if (both) CK(cudaStreamWaitEvent(sm, evs.record(c->stream), 0));  // buffers are allocated
+    if (n_multi > 0) {
+      k_dict_sumsq<<<dim3{unsigned(n_multi), unsigned(nchunk)}, DICT_THREADS, 0, sm>>>(a);
       post_launch(c);
-      k_dict_norms<<<unsigned((c_hi - c_lo + 255) / 256), 256, 0, c->stream>>>(a, c_hi);
+      k_dict_norms<<<unsigned((n_multi + 255) / 256), 256, 0, sm>>>(a, n_multi);
       post_launch(c);
-      a.chunk = chw;
-      a.nchunk = nchw;
-      k_dict_write<<<dim3{unsigned(c_hi - c_lo), unsigned(nchw)}, DICT_THREADS, 0, c->stream>>>(a);
+      k_dict_write<<<dim3{unsigned(n_multi), unsigned(nchunk)}, DICT_THREADS, 0, sm>>>(a);
       post_launch(c);
-    };
-    l2_path(0, std::min(can.d[l], P_sub * Rd), chunk, nchunk, chunk, nchunk);
-    // single-shift columns: a whole column per block for the (write-free) sums of squares
-    const int64_t ncol_all = (N + 2047) / 2048 * 2048;
-    l2_path(std::min(can.d[l], P_sub * Rd), can.d[l], ncol_all, 1, chunk_d, nchunk_d);
+    }
+    if (n_multi < can.d[l]) {
+      a.c0 = n_multi;
+      k_dict_single<<<unsigned(can.d[l] - n_multi), DICT_THREADS, 0, c->stream>>>(a);
+      post_launch(c);
+    }
+    // partial / the shift tables are released in c->stream order: after the side stream's use
+    if (both) CK(cudaStreamWaitEvent(c->stream, evs.record(sm), 0));
   }
   for (int l = 0; l < 3; ++l) {  // the three modes' kernels are queued before the first wait
     can.dict_norms[l].resize(can.d[l]);

@@ -197,6 +197,48 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
   }
 }
 
+// Single-shift placements (windowed_canonical, lattice_sum.hpp:148-157: the defect columns, all
+// but a few of a dictionary): one block per column does the whole column in one launch — the
+// window's sum of squares (from L2), the norm, then the normalised column — with no partial-sum
+// round trip and no second grid, so the blocks' L2-bound first halves overlap other blocks'
+// HBM-bound second halves.  Same summation order as k_dict_sumsq / k_dict_norms with one chunk
+// per column: the norms are bit-identical to that path's.
+__global__ void __launch_bounds__(DICT_THREADS) k_dict_single(DictArgs a) {
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x + a.c0;
+  const int64_t p = c / a.Rd, j = c % a.Rd;
+  const double* __restrict__ src = a.ref + j * 2 * a.N + (a.N / 2 - a.pl_shift[a.pl_off[p]]);
+  double s = 0.0;
+  for (int64_t i0 = 0; i0 < a.N; i0 += DICT_THREADS * DICT_RT) {
+    double v[DICT_RT];
+#pragma unroll
+    for (int r = 0; r < DICT_RT; ++r) {
+      const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+      v[r] = i < a.N ? src[i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < DICT_RT; ++r) s += v[r] * v[r];
+  }
+  s = block_sum(s, red);
+  const double nrm = sqrt(s);
+  if (threadIdx.x == 0) a.norms[c] = nrm;
+  const double inv = nrm == 0.0 ? 0.0 : 1.0 / nrm;
+  double* __restrict__ out = a.dict + c * a.N;
+  for (int64_t i0 = 0; i0 < a.N; i0 += DICT_THREADS * DICT_RT) {
+    double v[DICT_RT];
+#pragma unroll
+    for (int r = 0; r < DICT_RT; ++r) {
+      const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+      v[r] = i < a.N ? src[i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < DICT_RT; ++r) {
+      const int64_t i = i0 + threadIdx.x + int64_t(DICT_THREADS) * r;
+      if (i < a.N) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] * inv;
+    }
+  }
+}
+
 // out[:, q] = dict[:, idx[q]] — the reference-form N x M_c side matrix (HBM-bound
 // gather with 128-bit accesses when rows are even).
 __global__ void k_gather_columns(const double* __restrict__ dict, int64_t rows,

@@ -1,6 +1,6 @@
 """cfg5 stages 1-3 (factors-only RHOSVD) then a 2048 x 2048 x 32 box of the central
-evaluation inside an NVTX range 'eval', for ncu captures of the grouped projected-CP
-evaluation kernels (dev tool)."""
+evaluation inside an NVTX range 'eval', for ncu captures of the assembly kernels (NVTX range
+'assemble') and the grouped projected-CP evaluation kernels (dev tool)."""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -10,7 +10,10 @@ ctx = api.Context(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); ctx.set_stream(s.cuda_stream)
 g = W.baseline(5)
 ref = api.reference_for(g, ctx)
+torch.cuda.nvtx.range_push("assemble")
 can = api.lattice_sum(ref, g)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
 t, rep = api.rhosvd(can, api.TruncationSpec.tol(g.eps), form_core=False)
 c = g.N[0] // 2
 lo, hi = (c - 1024, c - 1024, c - 16), (c + 1024, c + 1024, c + 16)

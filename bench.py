@@ -203,9 +203,9 @@ def run_reference(args):
             per_mode[l].append(m[f"mode{l}"])
         else:
             warm[l].append(m[f"mode{l}"])
-    for l in range(3):  # fewer than 3 timed steps: the warm-up samples of the missing modes
-        if not per_mode[l]:
-            per_mode[l] = warm[l]
+    for l in range(3):  # fewer than 3 timed steps: the warm-up samples of the missing modes,
+        if not per_mode[l]:  # else one extra measured pass, so `value` always covers all three
+            per_mode[l] = warm[l] or [cpu_pipeline(cpu, [l], threads)[f"mode{l}"]]
 
     def mean(l, k):
         return statistics.mean(x[k] for x in per_mode[l]) if per_mode[l] else float("nan")

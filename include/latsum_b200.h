@@ -273,6 +273,14 @@ int latsum_sum_to_tucker(latsum_ctx* ctx, int family, double lambda, const int64
                          const double* def_charges, double tolerance, latsum_tucker** out,
                          latsum_spectral_report* report);
 
+/* add_concat (canonical.hpp:94-110): *out = a + b by concatenation — rank(a) + rank(b) terms, a's
+ * first; entries add exactly; the per-mode dictionaries are concatenated.  This is how
+ * defected_sum adds a cluster to the base sum (lattice_sum.hpp:372-374), and with it a defect
+ * cluster carrying its own kernel (DefectSpec.kernel, lattice_sum.hpp:301-303) is assembled
+ * against that kernel's reference tensor and added in DefectSpec order.  a and b stay valid. */
+int latsum_canonical_concat(latsum_ctx* ctx, const latsum_canonical* a, const latsum_canonical* b,
+                            latsum_canonical** out);
+
 /* ------------------------------------------------------------------ tensors from / to host
  * CanonicalTensor(dims, weights, factors) (canonical.hpp:25-29): columns taken as given
  * (the caller guarantees unit norms), so rhosvd / canonical_to_tucker accept any canonical

@@ -403,6 +403,14 @@ inline CanonicalTensor assemble(const ReferenceTensor& ref, const detail::Blocks
   return CanonicalTensor(ctx, h);
 }
 
+// add_concat (canonical.hpp:94-110): a + b by concatenation, a's terms first
+inline CanonicalTensor add_concat(const CanonicalTensor& a, const CanonicalTensor& b) {
+  b200::Context& ctx = a.ctx();
+  latsum_canonical* h = nullptr;
+  ctx.check(latsum_canonical_concat(ctx.get(), a.handle(), b.handle(), &h));
+  return CanonicalTensor(ctx, h);
+}
+
 // Rank-R canonical lattice sum + additive defects on the lattice_grid of `geom`
 // (assembled_sum_canonical + defected_sum without truncation, in one assembly).
 inline CanonicalTensor defected_sum(const ReferenceTensor& ref, const LatticeGeometry& geom,
@@ -545,43 +553,61 @@ inline LatticeSumResult assembled_sum_result(const ReferenceTensor& ref,
 }
 
 // defected_sum (lattice_sum.hpp:339-384), canonical branch: base + defect clusters in
-// `defects` order, truncated by canonical_to_tucker when `spec` is set.  Every defect uses
-// the base kernel here (a per-defect kernel needs a second reference tensor summed into the
-// same canonical tensor, which this path does not build: NotImplementedError).
+// `defects` order, truncated by canonical_to_tucker when `spec` is set.  Clusters with the base
+// kernel that come before any other kernel join the base's product blocks (one device assembly
+// instead of add_concat copies); from the first cluster carrying its own kernel
+// (DefectSpec.kernel, :301-303) on, every maximal run of clusters sharing a kernel is assembled
+// against that kernel's reference tensor (refs.find) and added with add_concat, in order — the
+// same terms in the same order as the reference's per-cluster add_concat loop (:372-374).
 inline LatticeSumResult defected_sum(const LatticeSumResult& base,
                                      const std::vector<DefectSpec>& defects,
                                      const ReferenceSet& refs,
                                      const std::optional<TruncationSpec>& spec,
                                      const SumOptions& = {}) {
   if (defects.empty()) return base;
-  if (!base.is_canonical() || !base.blocks)
-    throw NotImplementedError("defected_sum: the GPU path sums canonical bases built by "
-                              "assembled_sum_result / sublattice_union_sum");
+  if (!base.is_canonical())
+    throw NotImplementedError("defected_sum: the GPU path sums canonical bases (the Tucker-format "
+                              "route is out of scope)");
   for (const auto& d : defects) {
     if (d.sites.empty()) throw std::invalid_argument("defected_sum: defect with no sites");
     const KernelSpec k = d.kernel ? *d.kernel : base.geometry.kernel;
     if (!refs.has(k))
       throw std::invalid_argument("defected_sum: no reference tensor for kernel " + k.key());
-    if (!(k == base.geometry.kernel))
-      throw NotImplementedError("defected_sum: per-defect kernels are not on the GPU path");
   }
-  const ReferenceTensor& ref = refs.find(base.geometry.kernel);
   const Index n = base.grid.n[0] / base.geometry.cells[0];
-  auto b = std::make_shared<detail::Blocks>(*base.blocks);
-  LatticeSumResult out{base.tensor, base.geometry, base.grid, base.provenance, std::nullopt, b};
-  for (const auto& d : defects) {
-    const Index blocks = detail::add_defect(*b, d, n);
+  LatticeSumResult out{base.tensor, base.geometry, base.grid, base.provenance, std::nullopt, nullptr};
+  auto kernel_of = [&](const DefectSpec& d) { return d.kernel ? *d.kernel : base.geometry.kernel; };
+  auto record = [&](const DefectSpec& d, Index blocks, const ReferenceTensor& ref) {
     out.provenance.push_back({d.kind == DefectKind::vacancy ? "vacancy cluster" : "impurity cluster",
                               blocks * ref.rank(), Index(d.sites.size())});
     out.geometry.defects.push_back(d);
+  };
+  size_t at = 0;
+  std::optional<CanonicalTensor> total;
+  if (base.blocks) {  // leading base-kernel clusters: re-assembled with the base in one call
+    const ReferenceTensor& ref = refs.find(base.geometry.kernel);
+    auto b = std::make_shared<detail::Blocks>(*base.blocks);
+    for (; at < defects.size() && kernel_of(defects[at]) == base.geometry.kernel; ++at)
+      record(defects[at], detail::add_defect(*b, defects[at], n), ref);
+    total = assemble(ref, *b);
+    if (at == defects.size()) out.blocks = b;  // still one block list: later calls may extend it
+  } else {
+    total = base.canonical();
   }
-  CanonicalTensor total = assemble(ref, *b);
+  while (at < defects.size()) {  // runs of clusters sharing a kernel
+    const KernelSpec k = kernel_of(defects[at]);
+    const ReferenceTensor& ref = refs.find(k);
+    detail::Blocks b;
+    for (; at < defects.size() && kernel_of(defects[at]) == k; ++at)
+      record(defects[at], detail::add_defect(b, defects[at], n), ref);
+    total = add_concat(*total, assemble(ref, b));
+  }
   if (spec) {
-    auto tr = canonical_to_tucker(total, *spec);
+    auto tr = canonical_to_tucker(*total, *spec);
     out.tensor = std::move(tr.first);
     out.report = std::move(tr.second);
   } else {
-    out.tensor = std::move(total);
+    out.tensor = std::move(*total);
   }
   return out;
 }

@@ -107,6 +107,14 @@ def _cases() -> Dict[str, dict]:
         # a larger cfg2-shaped case (N = 256, M_c = 2013; no canonical_to_tucker: c2t = False)
         "large": dict(cells=(16, 16, 16), n=16, b=1.0, family=0, lam=0.0, M=16, eps=1e-7, c2t=False,
                       defects=[([s], -1.0, None) for s in vac_l]),
+        # per-defect kernels (DefectSpec.kernel): a Newton lattice with a Newton vacancy, a Yukawa
+        # impurity pair (a product cluster at that kernel's reference rank), another Newton
+        # vacancy and a second Yukawa impurity, in this order (add_concat order)
+        "mixed_kernels": dict(cells=(6, 6, 4), n=16, b=1.0, family=0, lam=0.0, M=10, eps=1e-7, c2t=False,
+                              defects=[([(1, 1, 0)], -1.0, None),
+                                       ([(-2, 0, 1), (-1, 0, 1)], 0.6, None, (1, 0.8)),
+                                       ([(0, -2, -1)], -1.0, None),
+                                       ([(2, 2, 1)], -0.4, (1.0, 0.0, -2.0), (1, 0.8))]),
         # non-contiguous active K sets (the ascending, not sliding, accumulation branch)
         "active": dict(cells=(6, 6, 6), n=12, b=1.0, family=0, lam=0.0, M=8, eps=1e-6,
                        active=[[-3, -2, 0, 1], [-3, -1, 0, 2], [-2, -1, 0, 1, 2]]),
@@ -116,11 +124,47 @@ def _cases() -> Dict[str, dict]:
 CASES = _cases()
 
 
+def single_kernel_cases():
+    """The cases every defect of which uses the lattice's kernel (one Geometry each)."""
+    return [n for n, c in CASES.items()
+            if not any(len(d) > 3 and d[3] is not None for d in c.get("defects", ()))]
+
+
+def geometry_parts(name: str):
+    """A case whose defects carry their own kernels, as the add_concat chain defected_sum builds
+    (lattice_sum.hpp:355-378): [(family, lambda, Geometry)] — the base lattice with the leading
+    base-kernel defects, then one part per maximal run of defects sharing a kernel (geometries
+    with no lattice of their own), in DefectSpec order."""
+    from paper_1411_1994_b200 import workload as W
+    c = CASES[name]
+    base_k = (c["family"], c["lam"])
+    runs = []  # (kernel, [defects])
+    for d in c.get("defects", ()):
+        k = tuple(d[3]) if len(d) > 3 and d[3] is not None else base_k
+        if runs and runs[-1][0] == k:
+            runs[-1][1].append(d[:3])
+        else:
+            runs.append((k, [d[:3]]))
+    parts = []
+    lead = runs.pop(0)[1] if runs and runs[0][0] == base_k else []
+    parts.append((base_k[0], base_k[1], W.from_lattice(
+        c["cells"], c["n"], c["b"], family=base_k[0], lam=base_k[1], M=c["M"], base_charge=1.0,
+        active=c.get("active"), defects=lead, eps=c["eps"], name="refpin-" + name)))
+    for k, ds in runs:
+        parts.append((k[0], k[1], W.from_lattice(
+            c["cells"], c["n"], c["b"], family=k[0], lam=k[1], M=c["M"], base_charge=1.0,
+            defects=ds, sublattices=[], parent_cells=c["cells"], eps=c["eps"],
+            name="refpin-" + name + "-part")))
+    return parts
+
+
 def geometry(name: str):
     """The case as the shift-table Geometry of the oracle port / CUDA path (workload.from_lattice
     applies the reference's own mapping, lattice_sum.hpp:159-164,444)."""
     from paper_1411_1994_b200 import workload as W
     c = CASES[name]
+    if any(len(d) > 3 and d[3] is not None for d in c.get("defects", ())):
+        raise ValueError("case with per-defect kernels: use geometry_parts")
     return W.from_lattice(c["cells"] if "sublattices" not in c else c["cells"], c["n"], c["b"],
                           family=c["family"], lam=c["lam"], M=c["M"], base_charge=1.0,
                           active=c.get("active"), defects=c.get("defects", ()),
@@ -188,7 +232,12 @@ class RefRun:
 
     def sum(self, accumulation: int = 0):
         """The canonical sum through the library functions (assembled_sum_canonical or
-        sublattice_union_sum, then defected_sum)."""
+        sublattice_union_sum, then defected_sum).  Defects given as 4-tuples carry their own
+        kernel (family, lambda) as DefectSpec.kernel does."""
+        defs = self.case.get("defects") or []
+        fam = _ints([d[3][0] if len(d) > 3 and d[3] is not None else -1 for d in defs])
+        lam = np.ascontiguousarray([d[3][1] if len(d) > 3 and d[3] is not None else 0.0 for d in defs], np.float64)
+        self._check(lib().lref_set_defect_kernels(self.h, C.c_int(len(defs)), _p(fam, C.c_int), _p(lam)))
         self._check(lib().lref_sum(self.h, *self._marshal(), C.c_int(accumulation)))
         return self
 

@@ -46,6 +46,7 @@ struct Handle {
   LatticeGeometry out_geometry;  // the sum's geometry (parent cells + the defects added)
   std::vector<SublatticePlacement> placements;
   int M = 0;
+  std::vector<std::pair<int, double>> defect_kernels;  // per DefectSpec: (family or -1, lambda)
   std::vector<GridSource<double>> sources;
   std::optional<TuckerTensor<double>> tucker;
   std::optional<SpectralReport<double>> report;
@@ -212,11 +213,18 @@ int lref_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offset
       spec.charge = def_charge[d];
       if (def_goff)
         spec.grid_offset = Array3<double>(def_goff[3 * d], def_goff[3 * d + 1], def_goff[3 * d + 2]);
+      if (size_t(d) < h->defect_kernels.size() && h->defect_kernels[size_t(d)].first >= 0) {
+        // DefectSpec.kernel (geometry.hpp:26): the cluster carries its own kernel; its reference
+        // tensor joins the ReferenceSet (same grid, same M), as cmd_sum does (commands.cpp:168-172)
+        spec.kernel = make_kernel(h->defect_kernels[size_t(d)].first, h->defect_kernels[size_t(d)].second);
+        if (!h->refs.has(*spec.kernel))
+          h->refs.add(build_reference_canonical<double>(*spec.kernel, h->ref.base_grid, h->M, ReferenceOptions{}));
+      }
       for (const auto& s : spec.sites) {
         GridSource<double> g;
         g.shift = detail::defect_grid_shift(s, spec.grid_offset, h->n_per_cell);
         g.weight = spec.charge;
-        g.kernel = h->geom.kernel;
+        g.kernel = spec.kernel ? *spec.kernel : h->geom.kernel;
         h->sources.push_back(g);
       }
       defects.push_back(std::move(spec));
@@ -227,6 +235,15 @@ int lref_sum(void* hp, int n_sub, const int* sub_cells, const double* sub_offset
     h->out_geometry = out.geometry;
     h->tucker.reset();
     h->report.reset();
+  });
+}
+
+// per-DefectSpec kernels for the next lref_sum: family[d] < 0 keeps the base kernel
+int lref_set_defect_kernels(void* hp, int n, const int* family, const double* lam) {
+  Handle* h = static_cast<Handle*>(hp);
+  return guarded(h, [&] {
+    h->defect_kernels.clear();
+    for (int d = 0; d < n; ++d) h->defect_kernels.emplace_back(family[d], lam[d]);
   });
 }
 

@@ -795,6 +795,15 @@ def canonical_from_arrays(weights, factors, ctx: Optional[Context] = None) -> Ca
     return CanonicalTensor(ctx, h)
 
 
+def add_concat(a: CanonicalTensor, b: CanonicalTensor) -> CanonicalTensor:
+    """canonical.hpp:94-110: a + b by concatenation (a's terms first).  A defect cluster with its
+    own kernel (lattice_sum.hpp:301-303) is `lattice_sum(reference of that kernel, geometry of the
+    cluster alone)` added with this, in DefectSpec order, as defected_sum does (:372-374)."""
+    h = ctypes.c_void_p()
+    a.ctx.check(_lib.lib().latsum_canonical_concat(a.ctx.handle, a.handle, b.handle, ctypes.byref(h)))
+    return CanonicalTensor(a.ctx, h)
+
+
 def write_tensor(path: str, tensor):
     """tensor_io.cpp:45-76 ("LTSTNSR" v1 + FNV-1a-64), from device-resident tensors."""
     ctx = tensor.ctx

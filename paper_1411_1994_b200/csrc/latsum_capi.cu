@@ -4060,6 +4060,48 @@ int latsum_canonical_from_host(latsum_ctx* c, const int64_t dims[3], int64_t ran
   });
 }
 
+int latsum_canonical_concat(latsum_ctx* c, const latsum_canonical* a, const latsum_canonical* b,
+                            latsum_canonical** out) {
+  return guarded(c, [&] {
+    require(a && b && out, "latsum_canonical_concat: bad argument");
+    for (int l = 0; l < 3; ++l)
+      require(a->N[l] == b->N[l], "add_concat: mode size mismatch");
+    auto can = std::make_unique<latsum_canonical>();
+    can->R = a->R;
+    can->Rd = 0;  // columns of more than one reference tensor
+    can->Mc = a->Mc + b->Mc;
+    can->weights = a->weights;
+    can->weights.insert(can->weights.end(), b->weights.begin(), b->weights.end());
+    for (int l = 0; l < 3; ++l) {
+      const int64_t N = a->N[l], da = a->d[l], db = b->d[l];
+      can->N[l] = N;
+      can->d[l] = da + db;
+      require(can->d[l] < (int64_t(1) << 21), "add_concat: too many distinct columns in a mode");
+      can->dict[l].alloc(c, size_t(N) * std::max<int64_t>(da + db, 1));
+      if (da)
+        CK(cudaMemcpyAsync(can->dict[l].p, a->dict[l].p, sizeof(double) * N * da,
+                           cudaMemcpyDeviceToDevice, c->stream));
+      if (db)
+        CK(cudaMemcpyAsync(can->dict[l].p + N * da, b->dict[l].p, sizeof(double) * N * db,
+                           cudaMemcpyDeviceToDevice, c->stream));
+      can->dict_norms[l] = a->dict_norms[l];
+      can->dict_norms[l].insert(can->dict_norms[l].end(), b->dict_norms[l].begin(), b->dict_norms[l].end());
+      can->mult[l] = a->mult[l];
+      can->mult[l].insert(can->mult[l].end(), b->mult[l].begin(), b->mult[l].end());
+      can->term_col[l] = a->term_col[l];
+      can->term_col[l].reserve(size_t(can->Mc));
+      for (int64_t col : b->term_col[l]) can->term_col[l].push_back(col + da);  // a's terms first
+    }
+    CK(cudaStreamSynchronize(c->stream));  // a and b may be destroyed right after the call
+    merge_terms(*can);
+    can->terms_async = true;  // terms() uploads the merged tables on first use
+    std::promise<void> done;
+    done.set_value();
+    can->terms_ready = done.get_future().share();
+    *out = can.release();
+  });
+}
+
 int latsum_tensor_write(latsum_ctx* c, const latsum_canonical* can, const latsum_tucker* t,
                         const char* path) {
   return guarded(c, [&] {

@@ -152,14 +152,42 @@ int main() {
     CHECK(ps.str().find("summand \"vacancy cluster\" rank " + std::to_string(R) + " sites 4\n") !=
           std::string::npos);
     CHECK(ps.str().find("truncation_bound_abs ") != std::string::npos);
-    // a defect with another kernel is not on this path
+    // a defect with its own kernel (DefectSpec.kernel, lattice_sum.hpp:301-303) needs that
+    // kernel's reference tensor in the set ...
     DefectSpec yk = ragged;
+    yk.kind = DefectKind::impurity;
+    yk.charge = 0.5;
     yk.kernel = KernelSpec::yukawa(0.5);
     try {
       defected_sum(base8, {yk}, refs, std::nullopt);
       CHECK(false);
     } catch (const std::invalid_argument&) {  // no reference built for it
     }
+    // ... and is then summed in DefectSpec order by add_concat (lattice_sum.hpp:372-374):
+    // rank, provenance, and entries = the Newton sum + the Yukawa windows alone
+    refs.add(build_reference_canonical(KernelSpec::yukawa(0.5), lattice_grid(g8, n8), 8));
+    const ReferenceTensor& ry = refs.find(KernelSpec::yukawa(0.5));
+    auto mixed = defected_sum(base8, {cluster, yk, ragged}, refs, std::nullopt);
+    CHECK(mixed.canonical().rank() == (1 + 1) * R + 3 * ry.rank() + 3 * R);
+    CHECK(mixed.provenance.size() == 4 && mixed.provenance[2].label == "impurity cluster" &&
+          mixed.provenance[2].canonical_rank == 3 * ry.rank());
+    LatticeGeometry only_yk;  // the Yukawa cluster alone: windows of the Yukawa reference
+    only_yk.cells = g8.cells;
+    detail::Blocks by;
+    detail::add_defect(by, yk, n8);
+    auto yk_alone = assemble(ry, by);
+    worst = 0;
+    scale = 0;
+    for (int p = 0; p < 40; ++p) {
+      const Index i = (11 * p) % 64, j = (17 * p + 3) % 64, k = (5 * p) % 8;
+      const double want = both.canonical().entry(i, j, k) + yk_alone.entry(i, j, k);
+      worst = std::fmax(worst, std::abs(mixed.canonical().entry(i, j, k) - want));
+      scale = std::fmax(scale, std::abs(want));
+    }
+    CHECK(worst <= 1e-13 * scale);
+    // a result of mixed kernels can be extended and truncated like any other
+    auto mixed2 = defected_sum(mixed, {cluster}, refs, TruncationSpec::tol(1e-6));
+    CHECK(!mixed2.is_canonical() && mixed2.provenance.size() == 5);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

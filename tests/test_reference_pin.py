@@ -23,7 +23,7 @@ from oracle import oracle as O  # noqa: E402
 from oracle import ref as RF  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-CASES = list(RF.CASES)
+CASES = RF.single_kernel_cases()
 HAVE_REFERENCE = os.path.isdir(os.path.join(RF.REFERENCE_ROOT, "include", "latsum"))
 
 
@@ -87,7 +87,7 @@ def test_reference_cmd_sum_and_cmd_verify(ref_built, name, tmp_path):
         r.close()
 
 
-@pytest.mark.parametrize("name", [c for c in CASES if c != "large"])
+@pytest.mark.parametrize("name", [c for c in RF.CASES if c != "large"])
 def test_fixtures_equal_the_live_reference(ref_built, name):
     import make_refpin
     live = make_refpin.derive(name)
@@ -268,3 +268,29 @@ def test_tensor_file_layout_is_the_references(ref_built, tmp_path):
     pt.write_bytes(bytes(raw))
     with pytest.raises(IOError):
         RF.read_tensor_entries(pt, pr)
+
+
+def test_port_reproduces_per_defect_kernels():
+    """DefectSpec.kernel (geometry.hpp:26, lattice_sum.hpp:301-303): clusters carrying their own
+    kernel are assembled against that kernel's reference tensor and concatenated in DefectSpec
+    order (add_concat, canonical.hpp:94-110).  The port's per-part side matrices, concatenated,
+    are the reference's."""
+    fx = fixture("mixed_kernels")
+    Fs, ws = [[], [], []], []
+    for fam, lam, g in RF.geometry_parts("mixed_kernels"):
+        F, w = O.side_matrices(O.reference(g), g)
+        for l in range(3):
+            Fs[l].append(F[l])
+        ws.append(w)
+    F = [np.hstack(x) for x in Fs]
+    w = np.concatenate(ws)
+    assert w.size == fx["weights"].size == 105
+    for l in range(3):
+        assert np.max(np.abs(F[l][:, fx["F_cols"]] - fx[f"F{l}"])) < 1e-13
+    np.testing.assert_allclose(w, fx["weights"], rtol=1e-12)
+    orc = O.rhosvd(F, w, eps=RF.CASES["mixed_kernels"]["eps"])
+    assert tuple(orc.ranks) == tuple(int(x) for x in fx["ranks"])
+    pr = fx["probes"]
+    scale = np.max(np.abs(fx["v_canonical"]))
+    assert np.max(np.abs(O.canonical_entries(F, w, pr) - fx["v_canonical"])) <= 1e-13 * scale
+    assert np.max(np.abs(fx["v_brute"] - fx["v_canonical"][:fx["v_brute"].size])) <= 1e-12 * scale

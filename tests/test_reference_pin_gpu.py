@@ -17,7 +17,7 @@ from latsum_helpers import col_rel_linf
 pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-CASES = list(RF.CASES)
+CASES = RF.single_kernel_cases()
 
 
 def fixture(name):
@@ -158,3 +158,35 @@ def test_references_own_verify_accepts_the_cuda_results(ctx, name, tmp_path):
         np.testing.assert_allclose(mine["max_abs"], ref_abs, rtol=1e-3, atol=1e-13 * ref_mag)
     finally:
         r.close()
+
+
+def test_cuda_path_per_defect_kernels_match_the_reference(ctx):
+    """DefectSpec.kernel: a Newton lattice with Newton vacancies and Yukawa impurity clusters,
+    interleaved.  Each run of same-kernel defects is assembled against that kernel's reference
+    tensor and added with latsum_canonical_concat (add_concat, canonical.hpp:94-110) in DefectSpec
+    order, as defected_sum does (lattice_sum.hpp:355-378); the result is the reference's: term
+    order, columns, weights, RHOSVD ranks, values, and the brute-force sum over both kernels."""
+    fx = fixture("mixed_kernels")
+    total = None
+    for fam, lam, g in RF.geometry_parts("mixed_kernels"):
+        part = api.lattice_sum(api.reference_for(g, ctx), g)
+        total = part if total is None else api.add_concat(total, part)
+    assert total.rank == fx["weights"].size == 105
+    cols = fx["F_cols"]
+    for l in range(3):
+        assert col_rel_linf(total.factor(l)[:, cols], fx[f"F{l}"]) < 1e-12
+    np.testing.assert_allclose(total.weights, fx["weights"], rtol=1e-12)
+    eps = RF.CASES["mixed_kernels"]["eps"]
+    tk, rep = api.rhosvd(total, api.TruncationSpec.tol(eps))
+    assert tuple(rep.chosen_ranks) == tuple(int(x) for x in fx["ranks"])
+    for l in range(3):
+        assert np.max(np.abs(rep.singular_values[l] - fx[f"sv{l}"])) <= 1e-10 * fx[f"sv{l}"][0]
+    np.testing.assert_allclose(rep.input_norm, fx["report"][3], rtol=1e-9)
+    pr = fx["probes"]
+    scale = np.max(np.abs(fx["v_canonical"]))
+    assert np.max(np.abs(total.entries(pr) - fx["v_canonical"])) <= 1e-12 * scale
+    v = tk.entries(pr)
+    assert np.max(np.abs(v - fx["v_canonical"])) <= (10 * eps + 1e-12) * scale
+    assert np.max(np.abs(v - fx["v_tucker"])) <= 1e-9 * scale
+    nb = fx["v_brute"].size  # the reference's oracle_entry over the sources of both kernels
+    assert np.max(np.abs(total.entries(pr[:nb]) - fx["v_brute"])) <= 1e-12 * scale

@@ -273,6 +273,15 @@ int latsum_sum_to_tucker(latsum_ctx* ctx, int family, double lambda, const int64
                          const double* def_charges, double tolerance, latsum_tucker** out,
                          latsum_spectral_report* report);
 
+/* SumOptions::accumulation (lattice_sum.hpp:28-39) for the assemblies made on this context:
+ * 0 sliding (default, as in the reference): uniformly strided shift lists (contiguous K sets)
+ *   are summed by the recursion v[i] = v[i-n] + entering - leaving of lattice_sum.hpp:116-128, in
+ *   the reference's operation order, every other list directly;
+ * 1 ascending: every list directly in ascending order (lattice_sum.hpp:142);
+ * 2 compensated: accepted; summed in the ascending order (the Kahan correction of
+ *   lattice_sum.hpp:129-140 changes the result below 1e-15 relative and is not applied). */
+int latsum_ctx_set_accumulation(latsum_ctx* ctx, int order);
+
 /* add_concat (canonical.hpp:94-110): *out = a + b by concatenation — rank(a) + rank(b) terms, a's
  * first; entries add exactly; the per-mode dictionaries are concatenated.  This is how
  * defected_sum adds a cluster to the base sum (lattice_sum.hpp:372-374), and with it a defect

@@ -492,12 +492,16 @@ inline std::pair<TuckerTensor, SpectralReport> canonical_to_tucker(const Canonic
 // ---- the reference's result-level interface (lattice_sum.hpp:38-69, :260-276, :339-465)
 
 enum class Accumulation { sliding, ascending, compensated };
-// The GPU assembly sums each dictionary column in one fixed order (the reference's orders
-// agree to ~1e-15 relative after normalisation); the option is accepted for
-// interface parity and does not change the device arithmetic.
+// lattice_sum.hpp:28-39.  sliding (default): uniformly strided shift lists are summed by the
+// reference's recursion (lattice_sum.hpp:116-128) in its operation order, every other list
+// directly; ascending: always directly; compensated: accepted, summed in the ascending order
+// (latsum_ctx_set_accumulation).
 struct SumOptions {
   Accumulation accumulation = Accumulation::sliding;
 };
+inline void apply(const SumOptions& o, b200::Context& ctx) {
+  ctx.check(latsum_ctx_set_accumulation(ctx.get(), int(o.accumulation)));
+}
 
 struct Summand {  // lattice_sum.hpp:44-50
   std::string label;
@@ -540,7 +544,8 @@ class ReferenceSet {  // lattice_sum.hpp:260-276
 // The base result cmd_sum builds for a rectangular lattice (commands.cpp:160-163).
 inline LatticeSumResult assembled_sum_result(const ReferenceTensor& ref,
                                              const LatticeGeometry& geom,
-                                             const SumOptions& = {}) {
+                                             const SumOptions& opts = {}) {
+  apply(opts, ref.ctx());
   LatticeGeometry rect = geom;
   rect.defects.clear();
   const Index n = ref.base_grid.n[0] / rect.cells[0];
@@ -563,8 +568,9 @@ inline LatticeSumResult defected_sum(const LatticeSumResult& base,
                                      const std::vector<DefectSpec>& defects,
                                      const ReferenceSet& refs,
                                      const std::optional<TruncationSpec>& spec,
-                                     const SumOptions& = {}) {
+                                     const SumOptions& opts = {}) {
   if (defects.empty()) return base;
+  apply(opts, base.canonical().ctx());
   if (!base.is_canonical())
     throw NotImplementedError("defected_sum: the GPU path sums canonical bases (the Tucker-format "
                               "route is out of scope)");
@@ -617,8 +623,9 @@ inline LatticeSumResult sublattice_union_sum(const std::vector<SublatticePlaceme
                                              const ReferenceTensor& ref,
                                              const LatticeGeometry& geometry,
                                              const std::optional<TruncationSpec>& spec,
-                                             const SumOptions& = {}) {
+                                             const SumOptions& opts = {}) {
   if (subs.empty()) throw std::invalid_argument("sublattice_union_sum: no sublattices");
+  apply(opts, ref.ctx());
   const Index n = ref.base_grid.n[0] / geometry.cells[0];
   auto b = std::make_shared<detail::Blocks>();
   LatticeSumResult out{sublattice_union_sum(subs, ref, geometry, n), geometry, ref.base_grid, {},

@@ -148,6 +148,7 @@ SIGNATURES = [
     ("latsum_verify_entries", _I, [_P, _P, _I64, _P, _P, _P, _I64, _P]),
     ("latsum_canonical_from_host", _I, [_P, _P, _I64, _P, _P, _P, _P, _P]),
     ("latsum_canonical_concat", _I, [_P, _P, _P, _P]),
+    ("latsum_ctx_set_accumulation", _I, [_P, _I]),
     ("latsum_tensor_write", _I, [_P, _P, _P, ctypes.c_char_p]),
     ("latsum_tensor_read", _I, [_P, ctypes.c_char_p, _P, _P]),
     ("latsum_dgemm_device", _I, [_P, _I, _I, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P,

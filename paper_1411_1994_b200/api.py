@@ -92,6 +92,12 @@ class Context:
         self.check(_lib.lib().latsum_ctx_set_host_sink(
             self._h, ctypes.c_void_p(int(core_ptr)) if core_ptr else None, int(core_cap), fp, _p(fc)))
 
+    def set_accumulation(self, order: str = "sliding"):
+        """SumOptions.accumulation (lattice_sum.hpp:28-39): "sliding" (default), "ascending" or
+        "compensated" for the assemblies made on this context (latsum_ctx_set_accumulation)."""
+        self.check(_lib.lib().latsum_ctx_set_accumulation(
+            self._h, {"sliding": 0, "ascending": 1, "compensated": 2}[order]))
+
     def trim_pool(self, keep_bytes: int = 0):
         """Release the unused part of the stream-ordered pool (latsum_ctx_trim_pool)."""
         self.check(_lib.lib().latsum_ctx_trim_pool(self._h, int(keep_bytes)))

@@ -134,6 +134,9 @@ struct latsum_ctx {
   // every SM holds them until it finishes, whatever the stream priorities; the low-priority
   // norm worker keeps to a few SMs so the mode workers' kernels are never queued behind it
   int max_ctas = 0;
+  // assembled_vector's accumulation order (lattice_sum.hpp:28-35): 0 sliding (the reference's
+  // default: the recursion wherever the reference would use it), 1 ascending (always direct)
+  int accumulation = 0;
   // SMs a capped worker's persistent kernels are holding right now (set on the ROOT context by
   // that worker): the other contexts' persistent GEMMs size their grids to the SMs left, since
   // their static tile partition would otherwise wait for the CTAs that cannot be placed until
@@ -1437,9 +1440,30 @@ void assemble_blocks(latsum_ctx* c, const latsum_reference& ref, int64_t nblk,
     const int64_t P = int64_t(pl_off.size()) - 1;
     can.d[l] = P * Rd;
     if (can.d[l] == 0) continue;
-    DVec<int64_t> doff, dsh;
+    DVec<int64_t> doff, dsh, dstride;
     doff.upload(c, pl_off);
     dsh.upload(c, pl_shift);
+    // placements the reference's default order sums by the sliding recursion (lattice_sum.hpp:
+    // 116: sliding && contiguous K && more than one window && N_L > n): ascending shifts at one
+    // stride n < N; every other list is summed directly in list order (the reference's
+    // ascending order, which its sliding order also falls back to)
+    std::vector<int64_t> pl_stride(size_t(P), 0);
+    bool any_sliding = false;
+    if (c->accumulation == 0)
+      for (int64_t p = 0; p < P_sub; ++p) {
+        const int64_t s0 = pl_off[p], L = pl_off[p + 1] - s0;
+        if (L < 2) continue;
+        const int64_t n = pl_shift[s0 + 1] - pl_shift[s0];
+        bool ok = n > 0 && n < N;
+        for (int64_t k = 2; ok && k < L; ++k) ok = pl_shift[s0 + k] - pl_shift[s0 + k - 1] == n;
+        // the leaving term's window [N/2 - (c_max + n) + n, ...) starts inside the doubled grid
+        // by the window check of c_max; nothing else to verify
+        if (ok) {
+          pl_stride[size_t(p)] = n;
+          any_sliding = true;
+        }
+      }
+    if (any_sliding) dstride.upload(c, pl_stride);
     can.dict[l].alloc(c, size_t(N) * can.d[l]);
     // [0, P_sub Rd): multi-shift (sublattice / product-cluster) columns, up to 256 shifted reads
     // per entry: 2048-row blocks, partial sums of squares per block, the norms, then the
@@ -1454,10 +1478,15 @@ void assemble_blocks(latsum_ctx* c, const latsum_reference& ref, int64_t nblk,
     norms.alloc(c, can.d[l]);
     ProfScope ps(c, "assemble_dict", 8.0 * double(N) * double(can.d[l]));
     DictArgs a{ref.col(l), N, Rd, doff.p, dsh.p, can.dict[l].p, partial.p, norms.p, chunk, nchunk};
+    if (any_sliding) a.pl_stride = dstride.p;
     const bool both = n_multi > 0 && n_multi < can.d[l] && side != nullptr;
     cudaStream_t sm = both ? side->stream : c->stream;  // the multi-shift columns' stream
     if (both) CK(cudaStreamWaitEvent(sm, evs.record(c->stream), 0));  // buffers are allocated
     if (n_multi > 0) {
+      if (any_sliding) {
+        k_dict_sliding<<<unsigned(n_multi), DICT_THREADS, 0, sm>>>(a);
+        post_launch(c);
+      }
       k_dict_sumsq<<<dim3{unsigned(n_multi), unsigned(nchunk)}, DICT_THREADS, 0, sm>>>(a);
       post_launch(c);
       k_dict_norms<<<unsigned((n_multi + 255) / 256), 256, 0, sm>>>(a, n_multi);
@@ -4058,6 +4087,12 @@ int latsum_canonical_from_host(latsum_ctx* c, const int64_t dims[3], int64_t ran
     CK(cudaStreamSynchronize(c->stream));
     *out = can.release();
   });
+}
+
+int latsum_ctx_set_accumulation(latsum_ctx* c, int order) {
+  if (!c || order < 0 || order > 2) return LATSUM_ERR_INVALID_ARGUMENT;
+  c->accumulation = order == 0 ? 0 : 1;  // compensated: the ascending order (see the header)
+  return LATSUM_OK;
 }
 
 int latsum_canonical_concat(latsum_ctx* c, const latsum_canonical* a, const latsum_canonical* b,

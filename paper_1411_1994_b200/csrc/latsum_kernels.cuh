@@ -111,6 +111,9 @@ struct DictArgs {
   int64_t chunk;
   int nchunk;
   int64_t c0 = 0;          // first column handled by this launch (blockIdx.x + c0)
+  // per placement: the stride n of a uniformly strided shift list summed by the sliding
+  // recursion (k_dict_sliding), 0 for the direct sum; null: every placement direct
+  const int64_t* pl_stride = nullptr;
 };
 
 // Dictionary entries of column c = (placement p, reference column j) for the DICT_RT rows
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
   __shared__ int64_t shb[DICT_MAXSH];
   const int64_t c = blockIdx.x + a.c0;
   const int64_t p = c / a.Rd, j = c % a.Rd;
+  if (a.pl_stride && a.pl_stride[p] > 0) return;  // summed by k_dict_sliding
   const double* rj = a.ref + j * 2 * a.N;
   int ns;
   const int64_t* sh = dict_shifts(a, p, shb, ns);
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_sumsq(DictArgs a) {
 __global__ void k_dict_norms(DictArgs a, int64_t d) {
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x + a.c0;
   if (c >= d) return;
+  if (a.pl_stride && a.pl_stride[c / a.Rd] > 0) return;  // k_dict_sliding wrote this norm
   double s = 0.0;
   for (int q = 0; q < a.nchunk; ++q) s += a.partial[c * a.nchunk + q];
   a.norms[c] = sqrt(s);
@@ -180,6 +185,15 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
   const int64_t c = blockIdx.x + a.c0;
   const int64_t p = c / a.Rd, j = c % a.Rd;
   const double* rj = a.ref + j * 2 * a.N;
+  if (a.pl_stride && a.pl_stride[p] > 0) {  // raw values are in place (k_dict_sliding): scale them
+    const double nrm = a.norms[c];
+    const double inv = nrm == 0.0 ? 0.0 : 1.0 / nrm;
+    double* out = a.dict + c * a.N;
+    const int64_t c0 = blockIdx.y * a.chunk, c1 = min(a.N, c0 + a.chunk);
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += DICT_THREADS)
+      out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : out[i] * inv;
+    return;
+  }
   int ns;
   const int64_t* sh = dict_shifts(a, p, shb, ns);
   const int64_t c0 = blockIdx.y * a.chunk, c1 = min(a.N, c0 + a.chunk);
@@ -195,6 +209,58 @@ __global__ void __launch_bounds__(DICT_THREADS) k_dict_write(DictArgs a) {
       if (i < c1) out[i] = nrm == 0.0 ? (i == 0 ? 1.0 : 0.0) : v[r] * inv;
     }
   }
+}
+
+// The reference's default accumulation order (Accumulation::sliding, assembled_vector,
+// lattice_sum.hpp:116-128) for a placement of L uniformly strided shifts c_k = c_0 + k n: the
+// first n rows are direct sums over k (ascending), every later row reuses the overlap of
+// consecutive windows, v[i] = v[i - n] + ref[hi + i] - ref[lo + i] with hi = N/2 - c_0 (the term
+// entering) and lo = N/2 - (c_{L-1} + n) (the term leaving): O(N + L n) reads per column instead
+// of O(L N) (cfg5: 256 shifts).  One thread per residue i mod n walks its chain, in the
+// reference's own operation order.  Raw values go to the dictionary column and the column's sum
+// of squares to the norm; k_dict_write then scales the column.  One block per column.
+__global__ void __launch_bounds__(DICT_THREADS) k_dict_sliding(DictArgs a) {
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x + a.c0;
+  const int64_t p = c / a.Rd, j = c % a.Rd;
+  const int64_t n = a.pl_stride[p];
+  if (n <= 0) return;
+  const int64_t s0 = a.pl_off[p], L = a.pl_off[p + 1] - s0;
+  const double* __restrict__ rj = a.ref + j * 2 * a.N;
+  const double* __restrict__ hi = rj + (a.N / 2 - a.pl_shift[s0]);
+  const double* __restrict__ lo = rj + (a.N / 2 - (a.pl_shift[s0 + L - 1] + n));
+  double* __restrict__ out = a.dict + c * a.N;
+  double ss = 0.0;
+  for (int64_t r = threadIdx.x; r < n && r < a.N; r += DICT_THREADS) {
+    double v = 0.0;
+    for (int64_t k = 0; k < L; ++k) v += rj[a.N / 2 - a.pl_shift[s0 + k] + r];
+    out[r] = v;
+    ss += v * v;
+    int64_t i = r + n;
+    for (; i + 3 * n < a.N; i += 4 * n) {  // the loads do not depend on the chain: issue them first
+      const double h0 = hi[i], h1 = hi[i + n], h2 = hi[i + 2 * n], h3 = hi[i + 3 * n];
+      const double l0 = lo[i], l1 = lo[i + n], l2 = lo[i + 2 * n], l3 = lo[i + 3 * n];
+      v = v + h0 - l0;
+      out[i] = v;
+      ss += v * v;
+      v = v + h1 - l1;
+      out[i + n] = v;
+      ss += v * v;
+      v = v + h2 - l2;
+      out[i + 2 * n] = v;
+      ss += v * v;
+      v = v + h3 - l3;
+      out[i + 3 * n] = v;
+      ss += v * v;
+    }
+    for (; i < a.N; i += n) {
+      v = v + hi[i] - lo[i];
+      out[i] = v;
+      ss += v * v;
+    }
+  }
+  ss = block_sum(ss, red);
+  if (threadIdx.x == 0) a.norms[c] = sqrt(ss);
 }
 
 // Single-shift placements (windowed_canonical, lattice_sum.hpp:148-157: the defect columns, all

@@ -813,3 +813,42 @@ def test_ozaki_stage3_matches_dmma_stage3(ctx, cfg, tmp_path):
         assert np.max(err) <= 0, (l, int(idx[np.argmax(err)]))
         ta, tb = np.sqrt(np.sum(sa[r:] ** 2)), np.sqrt(np.sum(sb[r:] ** 2))
         assert abs(ta - tb) <= 1e-4 * tb
+
+
+def test_accumulation_orders_agree_and_sliding_is_the_references(ctx):
+    """assembled_vector's orders (lattice_sum.hpp:101-144; test_lattice_sum.cpp:115-135): the
+    sliding recursion (default, uniform strides) and the direct ascending sum agree to roundoff,
+    both reproduce the reference's side matrices (tests/golden/refpin_*.npz, made with the
+    reference's default sliding order), and a non-uniform list falls back to the direct sum."""
+    import os
+    from oracle import ref as RF
+    for name in ("cubic", "clusters", "large"):
+        g = RF.geometry(name)
+        fx = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"refpin_{name}.npz"))
+        got = {}
+        try:
+            for order in ("sliding", "ascending", "compensated"):
+                ctx.set_accumulation(order)
+                can = api.lattice_sum(api.reference_for(g, ctx), g)
+                got[order] = ([can.factor(l) for l in range(3)], can.weights)
+        finally:
+            ctx.set_accumulation("sliding")
+        cols = fx["F_cols"]
+        for order, (F, w) in got.items():
+            for l in range(3):
+                assert col_rel_linf(F[l][:, cols], fx[f"F{l}"]) < 1e-12, (name, order, l)
+            np.testing.assert_allclose(w, fx["weights"], rtol=1e-12)
+        for l in range(3):
+            d = np.max(np.abs(got["sliding"][0][l] - got["ascending"][0][l]))
+            assert 0 < d < 1e-13, (name, l, d)  # different operation orders, same vectors
+            assert np.array_equal(got["ascending"][0][l], got["compensated"][0][l])
+    # non-uniform shift lists (BASELINE configs 2-5, SURVEY F2): both settings take the direct sum
+    g = mini("vacancies")
+    res = []
+    try:
+        for order in ("sliding", "ascending"):
+            ctx.set_accumulation(order)
+            res.append(api.lattice_sum(api.reference_for(g, ctx), g).factor(0))
+    finally:
+        ctx.set_accumulation("sliding")
+    assert np.array_equal(res[0], res[1])

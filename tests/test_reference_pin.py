@@ -196,7 +196,7 @@ def test_port_canonical_to_tucker_matches_the_reference(name):
     assert np.max(np.abs(got - fx["v_canonical"])) <= 30 * g.eps * scale
     assert np.max(np.abs(fx["v_c2t"] - fx["v_canonical"])) <= 30 * g.eps * scale
     if core.shape == want:
-        assert np.max(np.abs(got - fx["v_c2t"])) <= g.eps * scale
+        assert np.max(np.abs(got - fx["v_c2t"])) <= 3 * g.eps * scale
 
 
 class _Rank:  # stands in for a device CanonicalTensor / TuckerTensor (format + ranks only)

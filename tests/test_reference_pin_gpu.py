@@ -75,7 +75,8 @@ def test_cuda_path_reproduces_the_reference(ctx, name):
 def test_cuda_canonical_to_tucker_matches_the_reference(ctx, name):
     """canonical_to_tucker (rank_reduction.hpp:280-306) after 3 ALS sweeps: the reference's ranks
     (+-1 where a slice-drop decision sits within 5% of the budget, whose own cancellation noise is
-    percent level) and values within the tolerance of the exact sum and eps of the reference's."""
+    percent level) and values within the tolerance of the exact sum and 3 eps of the reference's
+    (two truncations at eps ||A|| each)."""
     fx = fixture(name)
     g = RF.geometry(name)
     ref = api.reference_for(g, ctx)
@@ -89,7 +90,7 @@ def test_cuda_canonical_to_tucker_matches_the_reference(ctx, name):
     got = t.entries(pr)
     assert np.max(np.abs(got - fx["v_canonical"])) <= 30 * g.eps * scale
     if tuple(rep.chosen_ranks) == want:
-        assert np.max(np.abs(got - fx["v_c2t"])) <= g.eps * scale
+        assert np.max(np.abs(got - fx["v_c2t"])) <= 3 * g.eps * scale
 
 
 def test_cuda_path_reads_the_references_tensor_files(ctx, tmp_path):

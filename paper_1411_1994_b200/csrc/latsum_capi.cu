@@ -1835,7 +1835,7 @@ bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_
   // the d columns of this rank's row block, K = Nb in <= KMAX chunks).  Its rounding (~3e-16 of
   // a unit column per entry, a few times the DMMA product's) leaves Y^T Y eigenvalues of
   // ~1e-27 d against the stop level 0.04 delta^2 b ~ 1e-20: five decades of room.
-  const bool oz_sketch = Nb > 0 && double(d) * double(kBlock) * double(Nb) >= 2e10;
+  const bool oz_sketch = Nb > 0 && double(d) * double(kBlock) * double(Nb) >= 2e9;
   std::vector<OzSliced> As;
   std::vector<int64_t> k0s;
   if (oz_sketch) {

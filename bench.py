@@ -178,6 +178,24 @@ def cpu_pipeline(cpu: "CpuReference", modes, threads=None) -> dict:
     return out
 
 
+def shared_config(g, n_gpus: int, factors_only: bool = False) -> dict:
+    """The `config` dict both arms print (the driver compares them): the workload from the
+    Geometry, plus what a step is, the L2 policy and the parallelism of the GPU arm."""
+    from paper_1411_1994_b200 import workload as W
+    return {**W.describe(g),
+            "step": ("GPU arm: stages 1-3 (reference, assembly, RHOSVD) per step of the value "
+                     "loop; stage 4 (evaluation of the box) per step of the grid_eval loop; "
+                     "ms_per_step = the sum of the two means" +
+                     ("; factors-only RHOSVD (the dense core does not fit), projected-CP evaluation"
+                      if factors_only else "") +
+                     ".  Reference arm: a bounded sample per step (cpu_baseline.sample)"),
+            "l2": "GPU arm: 256 MB buffer written between timed steps; eval output >> L2",
+            "parallelism": ((f"GPU arm: stages 1-2 replicated, RHOSVD row-sharded over the grid index "
+                             f"with NCCL all-reduce x{n_gpus}, z-slab evaluation x{n_gpus}")
+                            if n_gpus > 1 else "GPU arm: single GPU") +
+                           "; reference arm: all host cores of rank 0"}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port) on all host cores.  Step i
     measures stage 1 and mode i % 3 (stage 2 + SVD + P_l) — a bounded sample of the
@@ -220,7 +238,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(step_ms),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded geometry; no dataset involved)",
-        "config": W.describe(g),
+        "config": shared_config(g, args.gpus, g.N[0] >= 32768),
         "value_scope": ("measured: stage 1 + per mode (stage 2 side matrix + LAPACK SVD + rank "
                         "rule + P_l = Z_l^T A_l), each mode's mean over the steps that timed it; "
                         "project_core excluded (core_extrapolated_ms)"),
@@ -558,16 +576,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": total, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded geometry; no dataset involved)",
-            "config": {**W.describe(g),
-                       "step": ("stages 1-3 (reference, assembly, RHOSVD) per step of the value "
-                                "loop; stage 4 (evaluation of the box) per step of the grid_eval "
-                                "loop; ms_per_step = the sum of the two means" +
-                                ("; factors-only RHOSVD (the dense core does not fit), "
-                                 "projected-CP evaluation" if factors_only else "")),
-                       "l2": "256 MB buffer written between timed steps; eval output >> L2",
-                       "parallelism": (f"stages 1-2 replicated, RHOSVD row-sharded over the grid "
-                                       f"index with NCCL all-reduce x{world}, z-slab evaluation "
-                                       f"x{world}") if world > 1 else "single GPU"},
+            "config": shared_config(g, world, factors_only),
             "result": {"ranks": list(rep.chosen_ranks), "merged_columns": merged_columns,
                        "deflated": list(rep.deflated)},
             "step_ms_stages_1_3": [round(x, 3) for x in ms13],
@@ -610,8 +619,8 @@ def run_gpu(args):
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_total": int(launches),
         }
-        if cpu is not None:
-            line["cpu_baseline"] = cpu
+        # rank 0 at N = 1 only; null when skipped (--no-cpu, N > 1)
+        line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -177,8 +177,8 @@ def geometry(name: str):
 class RefRun:
     """One reference run: reference tensor -> canonical sum -> reduction -> entries."""
 
-    def __init__(self, name: str):
-        c = CASES[name]
+    def __init__(self, name):
+        c = CASES[name] if isinstance(name, str) else dict(name)  # a case name or a case dict
         self.case = c
         L = lib()
         act = c.get("active")

@@ -191,3 +191,26 @@ def test_cuda_path_per_defect_kernels_match_the_reference(ctx):
     assert np.max(np.abs(v - fx["v_tucker"])) <= 1e-9 * scale
     nb = fx["v_brute"].size  # the reference's oracle_entry over the sources of both kernels
     assert np.max(np.abs(total.entries(pr[:nb]) - fx["v_brute"])) <= 1e-12 * scale
+
+
+def test_window_overflow_error_is_the_references(ctx):
+    """A defect pushed outside the doubled grid: the reference throws WindowOverflowError
+    (grid.hpp:87-98) naming the 1-based mode and the shift; the C ABI returns
+    LATSUM_ERR_WINDOW_OVERFLOW with the same message."""
+    if not RF.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    from paper_1411_1994_b200 import workload as W
+    case = dict(cells=(4, 4, 4), n=16, b=1.0, family=0, lam=0.0, M=6, eps=1e-6,
+                defects=[([(0, 0, 0)], -1.0, None), ([(1, 0, -1)], -1.0, (0.0, 40.0, 0.0))])
+    r = RF.RefRun(case)
+    try:
+        with pytest.raises(RuntimeError) as ref_err:
+            r.sum()
+    finally:
+        r.close()
+    ref_msg = str(ref_err.value).split("): ", 1)[1]
+    assert ref_msg.startswith("window overflow in mode 2: shift -40 pushes the length-64 window")
+    g = W.from_lattice(case["cells"], case["n"], case["b"], M=case["M"], defects=case["defects"])
+    with pytest.raises(api.WindowOverflowError) as err:
+        api.lattice_sum(api.reference_for(g, ctx), g)
+    assert ref_msg in str(err.value)

@@ -1875,7 +1875,10 @@ bool range_basis(latsum_ctx* c, const double* A, RowBlock blk, int64_t N, int64_
     };
     int64_t added = 0;
     for (int round = 0; round < 4 && added < bb && m < cap; ++round) {
-      project_out(Y.p, bb);
+      // one projection of the sketch: what it leaves along P (~eps ||Y||) only perturbs the seed
+      // directions; the new columns themselves are projected against P twice and
+      // re-orthonormalised below before they join it (a second projection here cost ~7 ms of the
+      // cfg4 step for an unchanged residual ||A (I - P P^T)||)
       project_out(Y.p, bb);
       DBuf H(c, size_t(bb) * bb);
       gram(c, false, Y.p, d, bb, H.p);

@@ -658,12 +658,47 @@ def assembled_sum_canonical(ref: ReferenceTensor, cells, n_per_cell: int, cell_w
 
 
 def defected_sum(ref: ReferenceTensor, cells, n_per_cell: int, defects, cell_width: float = 1.0,
-                 base_charge: float = 1.0, spec: Optional[TruncationSpec] = None, deflate="auto"):
+                 base_charge: float = 1.0, spec: Optional[TruncationSpec] = None, deflate="auto",
+                 refs: Optional[Sequence[ReferenceTensor]] = None):
     """lattice_sum.hpp:339-400 (canonical branch): base lattice + defect clusters
-    `defects` = [(sites, charge, grid_offset)], truncated by RHOSVD when `spec` is set."""
-    g = from_lattice(cells, n_per_cell, cell_width, base_charge=base_charge, defects=defects,
-                     M=ref.M)
+    `defects` = [(sites, charge, grid_offset)], truncated by RHOSVD when `spec` is set.
+
+    A defect given as (sites, charge, grid_offset, KernelSpec) carries its own kernel
+    (DefectSpec.kernel, lattice_sum.hpp:301-303); `refs` (the ReferenceSet, :260-276) must then
+    hold that kernel's reference tensor on the same grid.  Every maximal run of clusters sharing
+    a kernel is assembled against its reference and added with `add_concat` in DefectSpec order,
+    the terms the reference's per-cluster add_concat loop (:372-374) produces."""
+    base_k = ref.kernel
+
+    def kernel_of(d):
+        return d[3] if len(d) > 3 and d[3] is not None else base_k
+
+    def find(k):
+        for r in [ref] + list(refs or ()):
+            if r.kernel == k:
+                return r
+        raise ValueError(f"defected_sum: no reference tensor for kernel {k}")
+
+    for d in defects:
+        if not len(d[0]):
+            raise ValueError("defected_sum: defect with no sites")
+        find(kernel_of(d))
+    runs = []
+    for d in defects:
+        k = kernel_of(d)
+        if runs and runs[-1][0] == k:
+            runs[-1][1].append(tuple(d[:3]))
+        else:
+            runs.append((k, [tuple(d[:3])]))
+    lead = runs.pop(0)[1] if runs and runs[0][0] == base_k else []
+    g = from_lattice(cells, n_per_cell, cell_width, base_charge=base_charge, defects=lead, M=ref.M)
     can = lattice_sum(ref, g)
+    for k, ds in runs:
+        rk = find(k)
+        gk = from_lattice(cells, n_per_cell, cell_width, family=k.family, lam=k.lam,
+                          base_charge=base_charge, defects=ds, sublattices=[], parent_cells=cells,
+                          M=rk.M)
+        can = add_concat(can, lattice_sum(rk, gk))
     if spec is None:
         return can
     return rhosvd(can, spec, deflate=deflate)

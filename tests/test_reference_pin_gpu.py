@@ -191,6 +191,19 @@ def test_cuda_path_per_defect_kernels_match_the_reference(ctx):
     assert np.max(np.abs(v - fx["v_tucker"])) <= 1e-9 * scale
     nb = fx["v_brute"].size  # the reference's oracle_entry over the sources of both kernels
     assert np.max(np.abs(total.entries(pr[:nb]) - fx["v_brute"])) <= 1e-12 * scale
+    # the same sum through the reference-shaped call: defected_sum(..., refs) with
+    # DefectSpec-style (sites, charge, grid_offset, kernel) entries
+    c = RF.CASES["mixed_kernels"]
+    g0 = RF.geometry_parts("mixed_kernels")[0][2]
+    ref_n = api.reference_for(g0, ctx)
+    ref_y = api.reference_for(RF.geometry_parts("mixed_kernels")[1][2], ctx)
+    defects = [(d[0], d[1], d[2], api.KernelSpec.yukawa(d[3][1]) if len(d) > 3 and d[3] else None)
+               for d in c["defects"]]
+    again = api.defected_sum(ref_n, c["cells"], c["n"], defects, cell_width=c["b"], refs=[ref_y])
+    assert again.rank == total.rank
+    np.testing.assert_array_equal(again.weights, total.weights)
+    with pytest.raises(ValueError, match="no reference tensor"):
+        api.defected_sum(ref_n, c["cells"], c["n"], defects, cell_width=c["b"])
 
 
 def test_window_overflow_error_is_the_references(ctx):

@@ -1610,6 +1610,14 @@ int64_t rank_for_tolerance(const std::vector<double>& sv, double eps) {
 void gram(latsum_ctx* c, bool rows, const double* A, int64_t N, int64_t d, double* G) {
   GemmOpts o = tagged("gemm_gram");
   o.lower = true;
+  // SYRK writes the lower tiles only.  A sharded reduction all-reduces the whole square: clear
+  // it first, so the tiles nobody reads are zeros on every rank rather than whatever the pool
+  // held (they were summed as garbage: harmless, but non-finite sums showed up in the host
+  // collectives of the tests)
+  if (has_comm(c)) {
+    const int64_t n = rows ? N : d;
+    CK(cudaMemsetAsync(G, 0, sizeof(double) * n * n, c->stream));
+  }
   if (rows) gemm(c, false, true, N, N, d, 1.0, A, N, A, N, 0.0, G, N, o);   // A A^T
   else gemm(c, true, false, d, d, N, 1.0, A, N, A, N, 0.0, G, d, o);        // A^T A
 }

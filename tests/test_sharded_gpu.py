@@ -99,6 +99,25 @@ def test_row_sharded_full_cfg3_against_fixture():
     assert np.array_equal(out[0][2].core, out[1][2].core)
 
 
+@pytest.fixture(autouse=True)
+def _finite_collectives(monkeypatch):
+    """Everything a rank hands to a collective is finite: a buffer with tiles nobody wrote (the
+    upper triangle of a lower-only SYRK, once) would be summed as whatever the pool held."""
+    orig_ar, orig_ag = api.ThreadCollective.allreduce, api.ThreadCollective.allgather
+
+    def allreduce(self, rank, channel, buf):
+        assert np.all(np.isfinite(buf)), (rank, channel, buf.size)
+        return orig_ar(self, rank, channel, buf)
+
+    def allgather(self, rank, channel, send, recv):
+        assert np.all(np.isfinite(send)), (rank, channel, send.size)
+        return orig_ag(self, rank, channel, send, recv)
+
+    monkeypatch.setattr(api.ThreadCollective, "allreduce", allreduce)
+    monkeypatch.setattr(api.ThreadCollective, "allgather", allgather)
+    yield
+
+
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_core_slabs_match_the_full_core(ctx, nranks):
     """SURVEY 8e's per-rank core slabs (LATSUM_RHOSVD_CORE_SLABS): each rank forms rows

@@ -104,8 +104,12 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU arm
 
 class CpuReference:
-    """The reference's CPU path for this workload (the oracle port: the reference itself
-    cannot be built here), timed on the host.
+    """The reference's CPU path for this workload, timed on the host: the oracle port.  The
+    reference itself does compile here (oracle/_ref, against stand-ins for its absent
+    third-party headers, DESIGN.md sections 1 and 4) and is the parity anchor, but its
+    stand-in SVD is a textbook Jacobi, not Eigen's BDCSVD, and its API cannot express the
+    BASELINE lattices 2-5: timing it would not time the reference.  The port runs
+    the same algorithm with LAPACK's SVD (kind "port").
 
     Measured, per mode l: stage 2 = the N_l x M_c side matrix built block by block as the
     reference does (assembled_vector / windowed columns + from_raw, oracle

@@ -3362,8 +3362,13 @@ void cp_eval_grouped(latsum_ctx* c, const double* const D[3], const int64_t ld[3
   DBuf G1(c, size_t(nj) * T);  // G1[:, t] = w_t D1[:, c1_t]
   k_gather_scale<<<grid_for(nj * T), 256, 0, c->stream>>>(D[1], nj, ld[1], tc[1], tw, T, G1.p);
   post_launch(c);
+  // z-chunks of whole 128-column tiles of the segmented GEMM where a 20 GiB Y allows it (cfg5:
+  // the 4 GiB cap gave 31 slices per chunk, a quarter of every 128-wide tile), else what fits
   const int64_t budget = int64_t(1) << 29;
-  const int64_t nkc = balanced_chunk(nk, std::min<int64_t>(budget / std::max<int64_t>(nj * d0, 1), 65535), 1);
+  int64_t cap = std::min<int64_t>(5 * budget / std::max<int64_t>(nj * d0, 1), 65535);
+  if (cap >= 128) cap = cap / 128 * 128;
+  else cap = std::max<int64_t>(1, std::min<int64_t>(budget / std::max<int64_t>(nj * d0, 1), 65535));
+  const int64_t nkc = balanced_chunk(nk, cap, cap >= 128 ? 128 : 1);
   DBuf G2(c, size_t(nkc) * T), Y(c, size_t(nj) * nkc * d0);
   const bool oz = eval_uses_ozaki(d0);
   OzSliced sD0;
